@@ -395,14 +395,15 @@ def ser_db(reference, est) -> float:
 
 
 def hicu_reconstruct(x0, mask, kext, stages, rank, circular=(), dc_mode="hard", dc_lambda=0.0,
-                     seed=0, support=None, nullspace="rsvd", inject_v=None, trace=None):
+                     seed=0, support=None, nullspace="rsvd", inject_v=None, trace=None, v_log=None):
     """Algorithm 1 driver restated from solver.py:258-398.
 
     ``stages`` is a list of ``(region, p, gradient_steps, iterations)``.
     ``nullspace="rsvd"`` follows the reference (subspace.py:67); "nystrom"
     follows the B200 route (Gram + Nystrom) in fp64.  ``inject_v(si, it)``
-    may return a V to use instead (lockstep parity).  ``trace`` (a list) gets
-    one dict per step with eta/objective values.  Returns (xhat, steps)."""
+    may return a V to use instead (lockstep parity); ``v_log`` (a dict) receives
+    the V used at each (stage, iteration).  ``trace`` (a list) gets one dict
+    per step with eta/objective values.  Returns (xhat, trace)."""
     x0 = np.ascontiguousarray(x0, dtype=np.complex128)
     mask = np.asarray(mask)
     if x0.shape != mask.shape:
@@ -428,6 +429,8 @@ def hicu_reconstruct(x0, mask, kext, stages, rank, circular=(), dc_mode="hard", 
                 ell = math.ceil(1.5 * rank)
                 omega = complex_normal(rng_generator(seed, (1, si, it)), (n, ell), 1.0)
                 v = nystrom_right_vectors(gram(x, gm), omega, rank)
+            if v_log is not None:
+                v_log[(si, it)] = v
             q = householder_nullspace(v)
             y = x
             for j in range(gsteps):

@@ -1,0 +1,115 @@
+// C-ABI glue: error reporting, geometry validation, device queries and the
+// Gram dispatch.  See include/hicu_b200.h for the contract.
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+
+size_t hicu_gram_simt_workspace(const DevGeom& g);
+int hicu_gram_simt(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st);
+
+namespace {
+thread_local char g_last_error[512] = "";
+}
+
+int hicu_set_error(int code, const char* msg) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s", msg ? msg : "");
+  return code;
+}
+
+int hicu_check_cuda(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HICU_OK;
+  snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
+  return HICU_ERR_CUDA;
+}
+
+int hicu_sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
+
+int hicu_make_devgeom(const hicu_geom* g, DevGeom* out) {
+  if (!g) return hicu_set_error(HICU_ERR_PARAMETER, "null geometry");
+  if (g->ndim < 1 || g->ndim > HICU_MAX_NDIM) return hicu_set_error(HICU_ERR_SHAPE, "ndim out of range");
+  if (g->n < 1) return hicu_set_error(HICU_ERR_SHAPE, "kernel support is empty");
+  if (!g->pos || !g->koff) return hicu_set_error(HICU_ERR_PARAMETER, "null support tables");
+  DevGeom d;
+  memset(&d, 0, sizeof(d));
+  d.ndim = g->ndim;
+  d.n = g->n;
+  d.pos = g->pos;
+  d.koff = g->koff;
+  int64_t st = 1;
+  for (int a = g->ndim - 1; a >= 0; --a) {
+    if (g->dims[a] < 1 || g->rext[a] < 1 || g->roff[a] < 0) return hicu_set_error(HICU_ERR_SHAPE, "invalid region");
+    d.dims[a] = g->dims[a];
+    d.stride[a] = st;
+    st *= g->dims[a];
+  }
+  d.N = st;
+  int64_t rs = 1;
+  for (int a = g->ndim - 1; a >= 0; --a) {
+    d.roff[a] = g->roff[a];
+    d.rext[a] = g->rext[a];
+    d.rstride[a] = rs;
+    rs *= g->rext[a];
+  }
+  d.s = rs;
+  d.ncirc = 0;
+  for (int a = 0; a < g->ndim; ++a) {
+    if (g->circular & (1u << a)) {
+      if (g->roff[a] != 0 || g->rext[a] != g->dims[a])
+        return hicu_set_error(HICU_ERR_SHAPE, "circular axis must span the full extent with offset 0");
+      d.circ_axes[d.ncirc++] = a;
+    }
+  }
+  *out = d;
+  return HICU_OK;
+}
+
+extern "C" int hicu_abi_version(void) { return 1; }
+
+extern "C" const char* hicu_last_error(void) { return g_last_error; }
+
+extern "C" const char* hicu_status_string(int status) {
+  switch (status) {
+    case HICU_OK: return "ok";
+    case HICU_ERR_SHAPE: return "ShapeError";
+    case HICU_ERR_PARAMETER: return "ParameterError";
+    case HICU_ERR_DEGENERATE_INPUT: return "DegenerateInputError";
+    case HICU_ERR_DEGENERATE_DIRECTION: return "DegenerateDirectionError";
+    case HICU_ERR_SIZE: return "SizeError";
+    case HICU_ERR_CONFIG: return "ConfigError";
+    case HICU_ERR_ARRAY_FORMAT: return "ArrayFormatError";
+    case HICU_ERR_CUDA: return "CudaError";
+    case HICU_ERR_WORKSPACE: return "WorkspaceError";
+    default: return "unknown";
+  }
+}
+
+extern "C" int hicu_device_sm_count(int* out) {
+  if (!out) return hicu_set_error(HICU_ERR_PARAMETER, "null out");
+  *out = hicu_sm_count();
+  return HICU_OK;
+}
+
+extern "C" size_t hicu_gram_workspace(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return 0;
+  return hicu_gram_simt_workspace(g);
+}
+
+extern "C" int hicu_gram(const hicu_geom* hg, const void* x, void* G, void* ws, size_t ws_bytes, void* stream) {
+  if (!x || !G || !ws) return hicu_set_error(HICU_ERR_PARAMETER, "gram: null pointer");
+  DevGeom g;
+  int s = hicu_make_devgeom(hg, &g);
+  if (s) return s;
+  return hicu_gram_simt(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
+}

@@ -1,0 +1,146 @@
+// Shared device helpers for the HICU B200 kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hicu_b200.h"
+
+#define HICU_HD __host__ __device__ __forceinline__
+
+// ---------------------------------------------------------------------------
+// complex arithmetic on float2 / double2
+// ---------------------------------------------------------------------------
+HICU_HD float2 cf(float r, float i) { return make_float2(r, i); }
+HICU_HD double2 cd(double r, double i) { return make_double2(r, i); }
+HICU_HD float2 operator+(float2 a, float2 b) { return cf(a.x + b.x, a.y + b.y); }
+HICU_HD float2 operator-(float2 a, float2 b) { return cf(a.x - b.x, a.y - b.y); }
+HICU_HD double2 operator+(double2 a, double2 b) { return cd(a.x + b.x, a.y + b.y); }
+HICU_HD double2 operator-(double2 a, double2 b) { return cd(a.x - b.x, a.y - b.y); }
+HICU_HD double2 operator*(double s, double2 a) { return cd(s * a.x, s * a.y); }
+HICU_HD float2 operator*(float s, float2 a) { return cf(s * a.x, s * a.y); }
+HICU_HD double2 cmul(double2 a, double2 b) { return cd(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+HICU_HD double2 cmulc(double2 a, double2 b) {  // conj(a) * b
+  return cd(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+HICU_HD double2 conjd(double2 a) { return cd(a.x, -a.y); }
+HICU_HD double abs2d(double2 a) { return a.x * a.x + a.y * a.y; }
+HICU_HD float abs2f(float2 a) { return a.x * a.x + a.y * a.y; }
+// acc += a * b
+HICU_HD void cfma(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(-a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+HICU_HD void cfmac(float2& acc, float2 a, float2 b) {
+  acc.x = fmaf(a.x, b.x, acc.x);
+  acc.x = fmaf(a.y, b.y, acc.x);
+  acc.y = fmaf(a.x, b.y, acc.y);
+  acc.y = fmaf(-a.y, b.x, acc.y);
+}
+HICU_HD void zfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+HICU_HD void zfmac(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+
+// ---------------------------------------------------------------------------
+// geometry as seen by kernels (built on the host from hicu_geom)
+// ---------------------------------------------------------------------------
+struct DevGeom {
+  int ndim;
+  int n;
+  int ncirc;               // number of circular axes
+  int circ_axes[HICU_MAX_NDIM];
+  int64_t dims[HICU_MAX_NDIM];
+  int64_t stride[HICU_MAX_NDIM];   // k-space element strides (C order)
+  int64_t roff[HICU_MAX_NDIM];
+  int64_t rext[HICU_MAX_NDIM];
+  int64_t rstride[HICU_MAX_NDIM];  // row-major strides of the region block
+  int64_t s;                        // region size
+  int64_t N;                        // k-space size
+  const int32_t* pos;
+  const int64_t* koff;
+};
+
+// Non-circular part of the flat address of row i, plus the region coordinates
+// on circular axes (needed for the wrap).
+__device__ __forceinline__ int64_t row_base(const DevGeom& g, int64_t i, int* cc) {
+  int64_t base = 0;
+  int ci = 0;
+#pragma unroll
+  for (int d = 0; d < HICU_MAX_NDIM; ++d) {
+    if (d >= g.ndim) break;
+    int64_t r = (i / g.rstride[d]) % g.rext[d];
+    if (ci < g.ncirc && g.circ_axes[ci] == d) {
+      cc[ci++] = (int)r;
+    } else {
+      base += (g.roff[d] + r) * g.stride[d];
+    }
+  }
+  return base;
+}
+
+// wrap contribution for circular axes: sum_d ((r_d + pos_d) mod N_d) * stride_d
+__device__ __forceinline__ int64_t circ_part(const DevGeom& g, const int* cc, const int32_t* pos_k) {
+  int64_t a = 0;
+  for (int c = 0; c < g.ncirc; ++c) {
+    int d = g.circ_axes[c];
+    int64_t v = cc[c] + pos_k[d];
+    if (v >= g.dims[d]) v -= g.dims[d];
+    a += v * g.stride[d];
+  }
+  return a;
+}
+
+// ---------------------------------------------------------------------------
+// deterministic block reduction of NV doubles; result valid in thread 0
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_reduce_store(double (&v)[NV], double* out) {
+  __shared__ double red[32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) red[warp][k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double t = 0.0;
+      for (int w = 0; w < nw; ++w) t += red[w][k];
+      out[k] = t;
+    }
+  }
+}
+
+// fixed-order warp sum of a strided partial array: parts[j*stride + off]
+__device__ __forceinline__ double warp_sum_parts(const double* parts, int np, int stride, int off) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+  for (int j = lane; j < np; j += 32) t += parts[(size_t)j * stride + off];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+int hicu_set_error(int code, const char* msg);
+int hicu_check_cuda(cudaError_t e, const char* where);
+int hicu_make_devgeom(const hicu_geom* g, DevGeom* out);
+int hicu_sm_count();

@@ -1,0 +1,639 @@
+// Small dense complex128 algebra for the nullspace step.
+//
+// Reference: rsvd_right_vectors (subspace.py:67-155) is replaced by the
+// Nystrom form of the same sketch (SURVEY §0 parity fact 1):
+//   Y = G Omega, C = Omega^H Y, C_nu = R^H R (Cholesky, shifted only if C is
+//   numerically indefinite), W = (Y + nu Omega) R^{-1}, M = W^H W = F L F^H
+//   (cyclic parallel Jacobi), V = (W F)[:, top r] L^{-1/2}.
+// W W^H = Y C^{-1} Y^H equals the reference's W_ref W_ref^H, so V spans the
+// reference's subspace for the same Omega.
+// householder_nullspace (subspace.py:158-212) and jl_compress (:215-229) are
+// restated as a reflector build plus a column-parallel reflector apply.
+//
+// All kernels are fp64; single-CTA kernels keep their matrix in shared
+// memory when it fits and fall back to a global workspace otherwise.
+#include "common.cuh"
+
+#include <math.h>
+
+namespace {
+
+constexpr int kSmemCap = 200 * 1024;
+
+// ---------------------------------------------------------------------------
+// C = op(A) op(B), row-major, op in {N, C}
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 load_op(const double2* A, int lda, bool conjT, int i, int l) {
+  // element (i, l) of op(A)
+  return conjT ? conjd(A[(size_t)l * lda + i]) : A[(size_t)i * lda + l];
+}
+
+__global__ void zgemm_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restrict__ A, int lda,
+                             const double2* __restrict__ B, int ldb, double2* __restrict__ C, int ldc) {
+  __shared__ double2 As[16][17];
+  __shared__ double2 Bs[16][17];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double2 acc = cd(0.0, 0.0);
+  for (int l0 = 0; l0 < k; l0 += 16) {
+    As[ty][tx] = (row < m && l0 + tx < k) ? load_op(A, lda, ca, row, l0 + tx) : cd(0.0, 0.0);
+    const int brow = l0 + ty;
+    Bs[ty][tx] = (brow < k && col < n) ? load_op(B, ldb, cb, brow, col) : cd(0.0, 0.0);
+    __syncthreads();
+#pragma unroll
+    for (int l = 0; l < 16; ++l) zfma(acc, As[ty][l], Bs[l][tx]);
+    __syncthreads();
+  }
+  if (row < m && col < n) C[(size_t)row * ldc + col] = acc;
+}
+
+int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int lda, const double2* B, int ldb,
+                 double2* C, int ldc, cudaStream_t st) {
+  dim3 grid((n + 15) / 16, (m + 15) / 16);
+  zgemm_kernel<<<grid, 256, 0, st>>>(opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
+  return hicu_check_cuda(cudaGetLastError(), "zgemm_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Cholesky C_nu = C + nu*O = R^H R (upper R, in place in C)
+// nu starts at 0; on a non-positive pivot it escalates (stabilised Nystrom).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, const double2* __restrict__ G,
+            int n, double2* __restrict__ gws, bool use_smem, double* __restrict__ nu_out, int* __restrict__ status) {
+  extern __shared__ double2 sA[];
+  double2* A = use_smem ? sA : gws;
+  __shared__ double s_scale;
+  __shared__ int s_fail;
+  __shared__ double s_nu;
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < n; ++i) tr += G[(size_t)i * n + i].x;
+    s_scale = tr > 0.0 ? tr / n : 1.0;
+    s_nu = 0.0;
+  }
+  __syncthreads();
+  for (int attempt = 0; attempt < 12; ++attempt) {
+    const double nu = s_nu;
+    for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) {
+      const double2 o = Og[e];
+      A[e] = Cg[e] + nu * o;
+    }
+    if (threadIdx.x == 0) s_fail = 0;
+    __syncthreads();
+    for (int kk = 0; kk < ell; ++kk) {
+      const double d = A[(size_t)kk * ell + kk].x;
+      if (!(d > 0.0) || !isfinite(d)) {
+        if (threadIdx.x == 0) s_fail = 1;
+        __syncthreads();
+        break;
+      }
+      const double rs = sqrt(d), inv = 1.0 / rs;
+      __syncthreads();
+      for (int j = kk + threadIdx.x; j < ell; j += blockDim.x) {
+        if (j == kk) A[(size_t)kk * ell + kk] = cd(rs, 0.0);
+        else A[(size_t)kk * ell + j] = inv * A[(size_t)kk * ell + j];
+      }
+      __syncthreads();
+      const int rem = ell - kk - 1;
+      for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+        const int i = kk + 1 + e / rem, j = kk + 1 + e % rem;
+        if (j < i) continue;
+        // A[i][j] -= conj(R[kk][i]) * R[kk][j]
+        const double2 a = A[(size_t)kk * ell + i], b = A[(size_t)kk * ell + j];
+        double2 v = A[(size_t)i * ell + j];
+        v = v - cmulc(a, b);
+        A[(size_t)i * ell + j] = v;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (!s_fail) break;
+    if (threadIdx.x == 0) s_nu = (s_nu == 0.0) ? 1e-14 * s_scale : s_nu * 100.0;
+    __syncthreads();
+    if (attempt == 11 && threadIdx.x == 0) *status = HICU_ERR_DEGENERATE_INPUT;
+  }
+  // write back R (upper triangle, zero below)
+  for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) {
+    const int i = e / ell, j = e % ell;
+    Cg[e] = (j >= i) ? A[e] : cd(0.0, 0.0);
+  }
+  if (threadIdx.x == 0) *nu_out = s_nu;
+}
+
+// W = (Y + nu*Omega) R^{-1}; one warp per row, R staged in smem when it fits.
+__global__ void trsm_rows_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
+                                 const double* __restrict__ nu_p, const double2* __restrict__ R, bool r_smem,
+                                 double2* __restrict__ W) {
+  extern __shared__ double2 sm[];
+  const int warps = blockDim.x >> 5;
+  double2* sR = sm;
+  double2* rowbuf = sm + (r_smem ? (size_t)ell * ell : 0);
+  if (r_smem) {
+    for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) sR[e] = R[e];
+    __syncthreads();
+  }
+  const double2* RR = r_smem ? sR : R;
+  const double nu = *nu_p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* w = rowbuf + (size_t)warp * ell;
+  for (int row = blockIdx.x * warps + warp; row < n; row += gridDim.x * warps) {
+    for (int j = 0; j < ell; ++j) {
+      double2 part = cd(0.0, 0.0);
+      for (int k = lane; k < j; k += 32) zfma(part, w[k], RR[(size_t)k * ell + j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        part.x += __shfl_xor_sync(0xffffffffu, part.x, o);
+        part.y += __shfl_xor_sync(0xffffffffu, part.y, o);
+      }
+      if (lane == 0) {
+        const double2 yv = Y[(size_t)row * ell + j] + nu * Om[(size_t)row * ell + j];
+        const double2 num = yv - part;
+        const double rjj = RR[(size_t)j * ell + j].x;
+        w[j] = cd(num.x / rjj, num.y / rjj);
+      }
+      __syncwarp();
+    }
+    for (int j = lane; j < ell; j += 32) W[(size_t)row * ell + j] = w[j];
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cyclic parallel two-sided Jacobi for a Hermitian PSD matrix (round-robin
+// ordering).  Logs every rotation (p, q, c, s*e^{i phi}) so the same unitary
+// can be applied to W afterwards; emits eigenvalues and their descending order.
+// ---------------------------------------------------------------------------
+struct RotEntry {
+  int p, q;
+  double c;
+  double2 se;
+};
+
+__device__ __forceinline__ void rr_pair(int m, int round, int i, int& p, int& q) {
+  if (i == 0) {
+    p = m - 1;
+    q = round;
+  } else {
+    p = (round + i) % (m - 1);
+    q = (round - i + (m - 1)) % (m - 1);
+  }
+  if (p > q) { int t = p; p = q; q = t; }
+}
+
+__global__ void __launch_bounds__(1024)
+jacobi_kernel(int ell, const double2* __restrict__ Mg, double2* __restrict__ gws, bool use_smem, int max_sweeps,
+              double tol, RotEntry* __restrict__ log, int* __restrict__ nrounds_out, double* __restrict__ evals,
+              int* __restrict__ order, int* __restrict__ status) {
+  extern __shared__ double2 sA[];
+  double2* A = use_smem ? sA : gws;
+  const int m = ell + (ell & 1);
+  const int half = m / 2;
+  __shared__ RotEntry rot[128];
+  __shared__ int s_any;
+  __shared__ double s_floor;
+  for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) A[e] = Mg[e];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tr = 0.0;
+    for (int i = 0; i < ell; ++i) tr += fabs(A[(size_t)i * ell + i].x);
+    s_floor = 1e-300 + 1e-17 * tr;
+  }
+  __syncthreads();
+  int rounds = 0;
+  int sweep = 0;
+  for (; sweep < max_sweeps; ++sweep) {
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    for (int rd = 0; rd < m - 1; ++rd) {
+      if (threadIdx.x < half) {
+        int p, q;
+        rr_pair(m, rd, threadIdx.x, p, q);
+        RotEntry r{p, q, 1.0, cd(0.0, 0.0)};
+        if (q < ell) {
+          const double a = A[(size_t)p * ell + p].x, d = A[(size_t)q * ell + q].x;
+          const double2 b = A[(size_t)p * ell + q];
+          const double bb = sqrt(abs2d(b));
+          if (bb > s_floor && bb > tol * sqrt(fabs(a * d))) {
+            const double th = (d - a) / (2.0 * bb);
+            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(1.0 + th * th));
+            const double c = 1.0 / sqrt(1.0 + t * t);
+            const double s = t * c;
+            r.c = c;
+            r.se = cd(s * b.x / bb, s * b.y / bb);
+            s_any = 1;
+          }
+        }
+        rot[threadIdx.x] = r;
+        log[(size_t)rounds * half + threadIdx.x] = r;
+      }
+      __syncthreads();
+      // rows: (A_p, A_q) <- (c A_p - se A_q, conj(se) A_p + c A_q)
+      for (int e = threadIdx.x; e < half * ell; e += blockDim.x) {
+        const RotEntry r = rot[e / ell];
+        if (r.q >= ell || (r.se.x == 0.0 && r.se.y == 0.0)) continue;
+        const int j = e % ell;
+        const double2 ap = A[(size_t)r.p * ell + j], aq = A[(size_t)r.q * ell + j];
+        A[(size_t)r.p * ell + j] = r.c * ap - cmul(r.se, aq);
+        A[(size_t)r.q * ell + j] = cmulc(r.se, ap) + r.c * aq;
+      }
+      __syncthreads();
+      // cols: (A_:p, A_:q) <- (c A_:p - conj(se) A_:q, se A_:p + c A_:q)
+      for (int e = threadIdx.x; e < half * ell; e += blockDim.x) {
+        const RotEntry r = rot[e / ell];
+        if (r.q >= ell || (r.se.x == 0.0 && r.se.y == 0.0)) continue;
+        const int j = e % ell;
+        const double2 ap = A[(size_t)j * ell + r.p], aq = A[(size_t)j * ell + r.q];
+        A[(size_t)j * ell + r.p] = r.c * ap - cmulc(r.se, aq);
+        A[(size_t)j * ell + r.q] = cmul(r.se, ap) + r.c * aq;
+      }
+      __syncthreads();
+      ++rounds;
+    }
+    if (!s_any) break;
+  }
+  if (threadIdx.x == 0) *nrounds_out = rounds;
+  for (int i = threadIdx.x; i < ell; i += blockDim.x) evals[i] = A[(size_t)i * ell + i].x;
+  __syncthreads();
+  // descending order by rank counting (ties broken by index: stable)
+  for (int i = threadIdx.x; i < ell; i += blockDim.x) {
+    const double v = evals[i];
+    int rank = 0;
+    for (int j = 0; j < ell; ++j) {
+      const double w = evals[j];
+      rank += (w > v) || (w == v && j < i);
+    }
+    order[rank] = i;
+  }
+}
+
+// Apply the logged rotations to the rows of W (n x ell), one warp per row,
+// then V[row, t] = W'[row, order[t]] / sqrt(evals[order[t]]) for t < r.
+__global__ void rot_apply_kernel(int n, int ell, int r, const double2* __restrict__ W, const RotEntry* __restrict__ log,
+                                 const int* __restrict__ nrounds_p, const double* __restrict__ evals,
+                                 const int* __restrict__ order, double2* __restrict__ V, int* __restrict__ status,
+                                 bool scale) {
+  extern __shared__ double2 sw[];
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = ell + (ell & 1), half = m / 2;
+  const int nrounds = *nrounds_p;
+  double2* w = sw + (size_t)warp * ell;
+  for (int row = blockIdx.x * warps + warp; row < n; row += gridDim.x * warps) {
+    for (int j = lane; j < ell; j += 32) w[j] = W[(size_t)row * ell + j];
+    __syncwarp();
+    for (int rd = 0; rd < nrounds; ++rd) {
+      const RotEntry* lr = log + (size_t)rd * half;
+      for (int i = lane; i < half; i += 32) {
+        const RotEntry e = lr[i];
+        if (e.q >= ell || (e.se.x == 0.0 && e.se.y == 0.0)) continue;
+        const double2 xp = w[e.p], xq = w[e.q];
+        w[e.p] = e.c * xp - cmulc(e.se, xq);
+        w[e.q] = cmul(e.se, xp) + e.c * xq;
+      }
+      __syncwarp();
+    }
+    for (int t = lane; t < r; t += 32) {
+      const int src = order[t];
+      const double lam = evals[src];
+      double2 v = cd(0.0, 0.0);
+      if (!scale) {
+        v = w[src];
+      } else if (lam > 0.0) {
+        const double inv = 1.0 / sqrt(lam);
+        v = inv * w[src];
+      } else if (status) {
+        *status = HICU_ERR_DEGENERATE_INPUT;
+      }
+      V[(size_t)row * r + t] = v;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Householder triangularisation of V (subspace.py:158-201).  refl is r x n
+// (row j = w_j, zero before entry j), tau r, flags r.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024)
+householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ gws,
+                   bool use_smem, double2* __restrict__ refl, double2* __restrict__ tau, int* __restrict__ flags,
+                   int* __restrict__ status) {
+  extern __shared__ double2 sV[];
+  double2* v = use_smem ? sV : gws;  // n x r row-major
+  __shared__ double red[32];
+  __shared__ double2 s_u0inv, s_tau;
+  __shared__ int s_active;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[e] = Vg[e];
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) refl[e] = cd(0.0, 0.0);
+  __syncthreads();
+  for (int col = 0; col < r; ++col) {
+    double t = 0.0;
+    for (int k = col + 1 + threadIdx.x; k < n; k += blockDim.x) t += abs2d(v[(size_t)k * r + col]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[warp] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tail = 0.0;
+      for (int w = 0; w < nw; ++w) tail += red[w];
+      const double2 x0 = v[(size_t)col * r + col];
+      const double beta = sqrt(tail + x0.x * x0.x + x0.y * x0.y);
+      int active = 1;
+      if (beta < tol) {
+        *status = HICU_ERR_DEGENERATE_INPUT;
+        active = 0;
+      } else if (tail == 0.0 && x0.y == 0.0 && x0.x >= 0.0) {
+        active = 0;
+      }
+      double2 u0 = cd(0.0, 0.0), tv = cd(0.0, 0.0);
+      if (active) {
+        if (x0.x > 0.0) {
+          // (-tail + 2i beta x0.im) / (conj(x0) + beta)
+          const double2 nume = cd(-tail, 2.0 * beta * x0.y);
+          const double2 deno = cd(x0.x + beta, -x0.y);
+          const double dd = abs2d(deno);
+          u0 = cd((nume.x * deno.x + nume.y * deno.y) / dd, (nume.y * deno.x - nume.x * deno.y) / dd);
+        } else {
+          u0 = cd(x0.x - beta, x0.y);
+        }
+        tv = cd((beta - x0.x) / beta, x0.y / beta);  // (beta - conj(x0)) / beta
+      }
+      const double uu = abs2d(u0);
+      s_u0inv = active ? cd(u0.x / uu, -u0.y / uu) : cd(0.0, 0.0);
+      s_tau = tv;
+      s_active = active;
+      flags[col] = active;
+      tau[col] = tv;
+    }
+    __syncthreads();
+    if (s_active) {
+      const double2 ui = s_u0inv;
+      // w = xvec / u0, w[0] = 1
+      for (int k = col + threadIdx.x; k < n; k += blockDim.x) {
+        const double2 wv = (k == col) ? cd(1.0, 0.0) : cmul(v[(size_t)k * r + col], ui);
+        refl[(size_t)col * n + k] = wv;
+      }
+      __syncthreads();
+      // rest -= (tau w)(w^H rest), one warp per remaining column
+      const double2 tv = s_tau;
+      const double2* wrow = refl + (size_t)col * n;
+      for (int j = col + 1 + warp; j < r; j += nw) {
+        double2 dot = cd(0.0, 0.0);
+        for (int k = col + lane; k < n; k += 32) zfmac(dot, wrow[k], v[(size_t)k * r + j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+          dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+        }
+        const double2 f = cmul(tv, dot);
+        for (int k = col + lane; k < n; k += 32) v[(size_t)k * r + j] = v[(size_t)k * r + j] - cmul(wrow[k], f);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// B <- H_0^H ... applied for col = r-1 .. 0: block -= conj(tau) w (w^H block).
+// One warp per column of B; the column lives in shared memory.
+__global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
+                                        const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
+                                        double2* __restrict__ B, float2* __restrict__ out32, int p) {
+  extern __shared__ double2 sb[];
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* b = sb + (size_t)warp * n;
+  for (int j = blockIdx.x * warps + warp; j < cols; j += gridDim.x * warps) {
+    for (int k = lane; k < n; k += 32) b[k] = Bin[(size_t)k * cols + j];
+    __syncwarp();
+    for (int col = r - 1; col >= 0; --col) {
+      if (!flags[col]) continue;
+      const double2* w = refl + (size_t)col * n;
+      double2 dot = cd(0.0, 0.0);
+      for (int k = col + lane; k < n; k += 32) zfmac(dot, w[k], b[k]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+        dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+      }
+      const double2 f = cmulc(tau[col], dot);  // conj(tau) * dot
+      for (int k = col + lane; k < n; k += 32) b[k] = b[k] - cmul(w[k], f);
+      __syncwarp();
+    }
+    for (int k = lane; k < n; k += 32) {
+      const double2 v = b[k];
+      B[(size_t)k * cols + j] = v;
+      if (out32) {
+        const int step = j / p, t = j % p;
+        out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+struct NysWs {
+  double2 *Y, *O, *C, *W, *M, *scratch;
+  double* evals;
+  double* nu;
+  int* order;
+  int* nrounds;
+  RotEntry* log;
+  size_t bytes;
+};
+
+constexpr int kMaxSweeps = 30;
+
+NysWs nystrom_layout(int n, int ell, char* base) {
+  NysWs w;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += (bytes + 255) & ~(size_t)255;
+    return p;
+  };
+  const int m = ell + (ell & 1);
+  w.Y = (double2*)take((size_t)n * ell * sizeof(double2));
+  w.O = (double2*)take((size_t)ell * ell * sizeof(double2));
+  w.C = (double2*)take((size_t)ell * ell * sizeof(double2));
+  w.W = (double2*)take((size_t)n * ell * sizeof(double2));
+  w.M = (double2*)take((size_t)ell * ell * sizeof(double2));
+  w.scratch = (double2*)take((size_t)ell * ell * sizeof(double2));
+  w.evals = (double*)take((size_t)ell * sizeof(double));
+  w.nu = (double*)take(sizeof(double));
+  w.order = (int*)take((size_t)ell * sizeof(int));
+  w.nrounds = (int*)take(sizeof(int));
+  w.log = (RotEntry*)take((size_t)kMaxSweeps * (m - 1) * (m / 2) * sizeof(RotEntry));
+  w.bytes = off;
+  return w;
+}
+
+}  // namespace
+
+extern "C" int hicu_zgemm(char opa, char opb, int m, int n, int k, const void* A, int lda, const void* B, int ldb,
+                          void* C, int ldc, void* stream) {
+  if (!A || !B || !C || m < 1 || n < 1 || k < 1) return hicu_set_error(HICU_ERR_PARAMETER, "zgemm: bad arguments");
+  if ((opa != 'N' && opa != 'C') || (opb != 'N' && opb != 'C'))
+    return hicu_set_error(HICU_ERR_PARAMETER, "zgemm: op must be N or C");
+  return zgemm_launch(opa, opb, m, n, k, (const double2*)A, lda, (const double2*)B, ldb, (double2*)C, ldc,
+                      (cudaStream_t)stream);
+}
+
+extern "C" size_t hicu_nystrom_workspace(int n, int ell) { return nystrom_layout(n, ell, nullptr).bytes; }
+
+extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* omega, void* V, void* ws,
+                            size_t ws_bytes, int* status_dev, void* stream) {
+  if (!(1 <= r && r < n)) return hicu_set_error(HICU_ERR_PARAMETER, "nystrom: rank must satisfy 1 <= r < n");
+  if (ell < r || ell > 256) return hicu_set_error(HICU_ERR_PARAMETER, "nystrom: sketch width out of range");
+  if (!G || !omega || !V || !ws || !status_dev) return hicu_set_error(HICU_ERR_PARAMETER, "nystrom: null pointer");
+  NysWs w = nystrom_layout(n, ell, (char*)ws);
+  if (ws_bytes < w.bytes) return hicu_set_error(HICU_ERR_WORKSPACE, "nystrom: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  auto Gp = (const double2*)G;
+  auto Om = (const double2*)omega;
+  int s;
+  if ((s = zgemm_launch('N', 'N', n, ell, n, Gp, n, Om, ell, w.Y, ell, st))) return s;
+  if ((s = zgemm_launch('C', 'N', ell, ell, n, Om, ell, w.Y, ell, w.C, ell, st))) return s;
+  if ((s = zgemm_launch('C', 'N', ell, ell, n, Om, ell, Om, ell, w.O, ell, st))) return s;
+  {
+    const size_t bytes = (size_t)ell * ell * sizeof(double2);
+    const bool sm = bytes <= kSmemCap;
+    if (sm) cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    chol_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.C, w.O, Gp, n, w.scratch, sm, w.nu, status_dev);
+    if ((s = hicu_check_cuda(cudaGetLastError(), "chol_kernel"))) return s;
+  }
+  {
+    const size_t rbytes = (size_t)ell * ell * sizeof(double2);
+    const int warps = 8;
+    const size_t rowb = (size_t)warps * ell * sizeof(double2);
+    const bool sm = rbytes + rowb <= kSmemCap;
+    const size_t smem = (sm ? rbytes : 0) + rowb;
+    cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int blocks = (n + warps - 1) / warps;
+    trsm_rows_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, w.Y, Om, w.nu, w.C, sm, w.W);
+    if ((s = hicu_check_cuda(cudaGetLastError(), "trsm_rows_kernel"))) return s;
+  }
+  if ((s = zgemm_launch('C', 'N', ell, ell, n, w.W, ell, w.W, ell, w.M, ell, st))) return s;
+  {
+    const size_t bytes = (size_t)ell * ell * sizeof(double2);
+    const bool sm = bytes <= kSmemCap;
+    if (sm) cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    jacobi_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.M, w.scratch, sm, kMaxSweeps, 1e-15, w.log, w.nrounds,
+                                                   w.evals, w.order, status_dev);
+    if ((s = hicu_check_cuda(cudaGetLastError(), "jacobi_kernel"))) return s;
+  }
+  {
+    const int warps = 8;
+    const size_t smem = (size_t)warps * ell * sizeof(double2);
+    cudaFuncSetAttribute(rot_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int blocks = (n + warps - 1) / warps;
+    rot_apply_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, r, w.W, w.log, w.nrounds, w.evals, w.order,
+                                                       (double2*)V, status_dev, true);
+    if ((s = hicu_check_cuda(cudaGetLastError(), "rot_apply_kernel"))) return s;
+  }
+  return HICU_OK;
+}
+
+extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* refl, void* tau, int* flags,
+                                int* status_dev, void* stream) {
+  if (r < 0 || r > n || !refl || !tau || !flags || !status_dev)
+    return hicu_set_error(HICU_ERR_DEGENERATE_INPUT, "householder: bad arguments");
+  if (r == 0) return HICU_OK;
+  if (!V) return hicu_set_error(HICU_ERR_PARAMETER, "householder: null V");
+  const size_t bytes = (size_t)n * r * sizeof(double2);
+  const bool sm = bytes <= kSmemCap;
+  void* gws = nullptr;
+  if (!sm) {
+    // large V: work in place in the caller's refl buffer is not possible (different layout);
+    // require the caller to size refl at 2*n*r and use its upper half as scratch.
+    gws = (double2*)refl + (size_t)n * r;
+  }
+  if (sm) cudaFuncSetAttribute(householder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  householder_kernel<<<1, 1024, sm ? bytes : 0, (cudaStream_t)stream>>>(
+      n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
+  return hicu_check_cuda(cudaGetLastError(), "householder_kernel");
+}
+
+extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
+                                     const void* Bin, void* B, void* out32, int p, void* stream) {
+  if (n < 1 || r < 0 || cols < 1 || !B || !Bin) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad arguments");
+  if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad p");
+  int warps = 8;
+  while (warps > 1 && (size_t)warps * n * sizeof(double2) > kSmemCap) warps >>= 1;
+  const size_t smem = (size_t)warps * n * sizeof(double2);
+  if (smem > kSmemCap) return hicu_set_error(HICU_ERR_SIZE, "apply_reflectors: n too large");
+  cudaFuncSetAttribute(apply_reflectors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int blocks = (cols + warps - 1) / warps;
+  apply_reflectors_kernel<<<blocks, warps * 32, smem, (cudaStream_t)stream>>>(
+      n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B, (float2*)out32,
+      p ? p : 1);
+  return hicu_check_cuda(cudaGetLastError(), "apply_reflectors_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// SVD coil compression basis (no reference function):
+// eigenvectors of the nc x nc coil covariance by the same Jacobi kernel,
+// columns sorted by decreasing eigenvalue, phase fixed so the
+// largest-magnitude entry (first on ties) is real positive.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void eye_kernel(int n, double2* __restrict__ I) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x)
+    I[e] = cd((e / n) == (e % n) ? 1.0 : 0.0, 0.0);
+}
+
+__global__ void coil_phase_kernel(int nc, int nv, const double2* __restrict__ E, const double* __restrict__ evals,
+                                  const int* __restrict__ order, double2* __restrict__ basis,
+                                  double* __restrict__ evals_out) {
+  const int j = threadIdx.x;
+  if (j >= nc) return;
+  int best = 0;
+  double bm = -1.0;
+  for (int i = 0; i < nc; ++i) {
+    const double a = abs2d(E[(size_t)i * nc + j]);
+    if (a > bm) { bm = a; best = i; }
+  }
+  const double2 e = E[(size_t)best * nc + j];
+  const double mag = sqrt(abs2d(e));
+  const double2 ph = mag > 0.0 ? cd(e.x / mag, e.y / mag) : cd(1.0, 0.0);
+  if (j < nv) {
+    for (int i = 0; i < nc; ++i) basis[(size_t)i * nv + j] = cmulc(ph, E[(size_t)i * nc + j]);  // E / ph
+  }
+  if (evals_out) evals_out[j] = evals[order[j]];
+}
+
+}  // namespace
+
+extern "C" size_t hicu_coil_basis_workspace(int nc) {
+  return nystrom_layout(nc, nc, nullptr).bytes + 2 * (size_t)nc * nc * sizeof(double2) + 512;
+}
+
+extern "C" int hicu_coil_basis(int nc, int nv, const void* cov, void* basis, double* evals, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (nc < 1 || nc > 32 || nv < 1 || nv > nc || !cov || !basis || !ws)
+    return hicu_set_error(HICU_ERR_PARAMETER, "coil_basis: bad arguments");
+  if (ws_bytes < hicu_coil_basis_workspace(nc)) return hicu_set_error(HICU_ERR_WORKSPACE, "coil_basis: workspace");
+  NysWs w = nystrom_layout(nc, nc, (char*)ws);
+  char* extra = (char*)ws + ((w.bytes + 255) & ~(size_t)255);
+  double2* I = (double2*)extra;
+  double2* E = I + (size_t)nc * nc;
+  int* status = (int*)(E + (size_t)nc * nc);
+  cudaStream_t st = (cudaStream_t)stream;
+  int s;
+  eye_kernel<<<1, 256, 0, st>>>(nc, I);
+  if ((s = hicu_check_cuda(cudaGetLastError(), "eye_kernel"))) return s;
+  const size_t bytes = (size_t)nc * nc * sizeof(double2);
+  cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  jacobi_kernel<<<1, 1024, bytes, st>>>(nc, (const double2*)cov, w.scratch, true, kMaxSweeps, 1e-15, w.log,
+                                        w.nrounds, w.evals, w.order, status);
+  if ((s = hicu_check_cuda(cudaGetLastError(), "jacobi_kernel"))) return s;
+  // E = I J with columns in descending-eigenvalue order (no scaling)
+  rot_apply_kernel<<<1, 32 * 8, (size_t)8 * nc * sizeof(double2), st>>>(nc, nc, nc, I, w.log, w.nrounds, w.evals,
+                                                                       w.order, E, nullptr, false);
+  if ((s = hicu_check_cuda(cudaGetLastError(), "rot_apply_kernel"))) return s;
+  // E columns are already in descending order; identity order for the phase step
+  coil_phase_kernel<<<1, 32, 0, st>>>(nc, nv, E, w.evals, w.order, (double2*)basis, evals);
+  return hicu_check_cuda(cudaGetLastError(), "coil_phase_kernel");
+}

@@ -1,0 +1,480 @@
+// Gradient-step kernels: forward convolution (u = H(y) Q~) with the fused
+// objective reduction, the ELS convolution (w = H(g) Q~ never stored) with
+// fused <w,u> / |w|^2 reductions, the gather-form k-space adjoint (col2im)
+// with the data-consistency epilogue, and the device-side step update.
+//
+// Reference: hankel.py:255-322 (hankel_apply), :394-440
+// (kspace_adjoint_scatter), :473-558 (objective_and_gradient,
+// exact_line_search), solver.py:333-376 (the inlined inner loop).
+//
+// SIMT fp32 arithmetic with fp64 reductions; one thread per output row
+// (conv) or per k-space sample (scatter).  Grid sizes are fixed functions of
+// the geometry so partial counts, and hence results, are deterministic.
+#include "common.cuh"
+
+namespace {
+
+constexpr int kConvThreads = 256;
+constexpr int kScatterThreads = 256;
+
+int conv_blocks(int64_t s) {
+  int64_t b = (s + kConvThreads - 1) / kConvThreads;
+  int64_t cap = (int64_t)hicu_sm_count() * 8;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+int scatter_blocks(int64_t N) {
+  int64_t b = (N + kScatterThreads - 1) / kScatterThreads;
+  int64_t cap = (int64_t)hicu_sm_count() * 8;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// MODE 0: u = H(y) qt, store u, part = sum |u|^2
+// MODE 1: w = H(y) qt, part = (sum Re(conj(w) u), sum |w|^2)
+template <int PMAX, bool CIRC, int MODE>
+__global__ void __launch_bounds__(kConvThreads)
+conv_kernel(DevGeom g, const float2* __restrict__ y, const float2* __restrict__ qt, int p,
+            float2* __restrict__ u, double* __restrict__ parts) {
+  extern __shared__ unsigned char smem_raw[];
+  float2* sq = reinterpret_cast<float2*>(smem_raw);                       // n * PMAX
+  int64_t* skoff = reinterpret_cast<int64_t*>(sq + (size_t)g.n * PMAX);   // n
+  int32_t* spos = reinterpret_cast<int32_t*>(skoff + g.n);                 // n * ndim (CIRC only)
+  for (int t = threadIdx.x; t < g.n * PMAX; t += blockDim.x) {
+    int k = t / PMAX, j = t % PMAX;
+    sq[t] = (j < p) ? qt[(size_t)k * p + j] : cf(0.f, 0.f);
+  }
+  for (int t = threadIdx.x; t < g.n; t += blockDim.x) skoff[t] = g.koff[t];
+  if (CIRC)
+    for (int t = threadIdx.x; t < g.n * g.ndim; t += blockDim.x) spos[t] = g.pos[t];
+  __syncthreads();
+
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.s;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int cc[HICU_MAX_NDIM];
+    const int64_t base = row_base(g, i, cc);
+    float2 acc[PMAX];
+#pragma unroll
+    for (int j = 0; j < PMAX; ++j) acc[j] = cf(0.f, 0.f);
+    for (int k = 0; k < g.n; ++k) {
+      int64_t addr = base + skoff[k];
+      if (CIRC) addr += circ_part(g, cc, spos + (size_t)k * g.ndim);
+      const float2 v = __ldg(y + addr);
+      const float2* qk = sq + (size_t)k * PMAX;
+#pragma unroll
+      for (int j = 0; j < PMAX; ++j) cfma(acc[j], v, qk[j]);
+    }
+    if (MODE == 0) {
+      float2* ui = u + (size_t)i * p;
+#pragma unroll
+      for (int j = 0; j < PMAX; ++j) {
+        if (j < p) {
+          ui[j] = acc[j];
+          a0 += (double)acc[j].x * acc[j].x + (double)acc[j].y * acc[j].y;
+        }
+      }
+    } else {
+      const float2* ui = u + (size_t)i * p;
+#pragma unroll
+      for (int j = 0; j < PMAX; ++j) {
+        if (j < p) {
+          const float2 uv = ui[j];
+          a0 += (double)acc[j].x * uv.x + (double)acc[j].y * uv.y;
+          a1 += (double)acc[j].x * acc[j].x + (double)acc[j].y * acc[j].y;
+        }
+      }
+    }
+  }
+  if (MODE == 0) {
+    double v[1] = {a0};
+    block_reduce_store<1>(v, parts + blockIdx.x);
+  } else {
+    double v[2] = {a0, a1};
+    block_reduce_store<2>(v, parts + 2 * (size_t)blockIdx.x);
+  }
+}
+
+// Gather-form adjoint: g[m] = sum_{kappa,k: m - kappa in region} conj(qt[kappa,k]) u[m-kappa, k]
+// followed by data consistency; parts = (|g|^2, |res|^2, Re<Mg,res>, |Mg|^2).
+template <int PMAX, bool CIRC>
+__global__ void __launch_bounds__(kScatterThreads)
+scatter_kernel(DevGeom g, const float2* __restrict__ qt, int p, const float2* __restrict__ u,
+               const uint8_t* __restrict__ mask, const float2* __restrict__ y,
+               const float2* __restrict__ x0, int dc_mode, float lam, float2* __restrict__ gout,
+               double* __restrict__ parts) {
+  extern __shared__ unsigned char smem_raw[];
+  float2* sq = reinterpret_cast<float2*>(smem_raw);                        // n * PMAX (conj)
+  int32_t* spos = reinterpret_cast<int32_t*>(sq + (size_t)g.n * PMAX);      // n * ndim
+  int64_t* srow = reinterpret_cast<int64_t*>(spos + (((size_t)g.n * g.ndim + 1) & ~(size_t)1));  // n
+  for (int t = threadIdx.x; t < g.n * PMAX; t += blockDim.x) {
+    int k = t / PMAX, j = t % PMAX;
+    float2 q = (j < p) ? qt[(size_t)k * p + j] : cf(0.f, 0.f);
+    sq[t] = cf(q.x, -q.y);
+  }
+  for (int t = threadIdx.x; t < g.n * g.ndim; t += blockDim.x) spos[t] = g.pos[t];
+  __syncthreads();
+  // row-index offset of each tap over the non-circular axes
+  for (int t = threadIdx.x; t < g.n; t += blockDim.x) {
+    int64_t o = 0;
+    for (int d = 0, ci = 0; d < g.ndim; ++d) {
+      if (ci < g.ncirc && g.circ_axes[ci] == d) { ++ci; continue; }
+      o += (int64_t)spos[(size_t)t * g.ndim + d] * g.rstride[d];
+    }
+    srow[t] = o;
+  }
+  __syncthreads();
+
+  double a_g = 0.0, a_res = 0.0, a_num = 0.0, a_den = 0.0;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < g.N;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    int64_t mc[HICU_MAX_NDIM];
+    int64_t rem = m;
+    for (int d = g.ndim - 1; d >= 0; --d) {
+      mc[d] = rem % g.dims[d];
+      rem /= g.dims[d];
+    }
+    // row index of (m - kappa) excluding the tap offset, over non-circular axes
+    int64_t rbase = 0;
+    for (int d = 0, ci = 0; d < g.ndim; ++d) {
+      if (ci < g.ncirc && g.circ_axes[ci] == d) { ++ci; continue; }
+      rbase += (mc[d] - g.roff[d]) * g.rstride[d];
+    }
+    float2 acc = cf(0.f, 0.f);
+    for (int k = 0; k < g.n; ++k) {
+      const int32_t* pk = spos + (size_t)k * g.ndim;
+      bool ok = true;
+      int64_t ci_row = 0;
+      for (int d = 0, ci = 0; d < g.ndim; ++d) {
+        if (ci < g.ncirc && g.circ_axes[ci] == d) {
+          int64_t r = mc[d] - pk[d];
+          if (r < 0) r += g.dims[d];
+          ci_row += r * g.rstride[d];
+          ++ci;
+        } else {
+          int64_t r = mc[d] - g.roff[d] - pk[d];
+          ok = ok && (r >= 0) && (r < g.rext[d]);
+        }
+      }
+      if (!ok) continue;
+      const int64_t row = rbase - srow[k] + ci_row;
+      const float2* ur = u + (size_t)row * p;
+      const float2* qk = sq + (size_t)k * PMAX;
+#pragma unroll
+      for (int j = 0; j < PMAX; ++j)
+        if (j < p) cfma(acc, qk[j], ur[j]);
+    }
+    const bool on = (dc_mode != 2) && mask[m] == 1;
+    if (dc_mode == 0) {
+      if (on) acc = cf(0.f, 0.f);
+    } else if (dc_mode == 1) {
+      float2 res = on ? (y[m] - x0[m]) : cf(0.f, 0.f);
+      a_res += (double)res.x * res.x + (double)res.y * res.y;
+      acc = acc + lam * res;
+      if (on) {
+        a_num += (double)acc.x * res.x + (double)acc.y * res.y;
+        a_den += (double)acc.x * acc.x + (double)acc.y * acc.y;
+      }
+    }
+    a_g += (double)acc.x * acc.x + (double)acc.y * acc.y;
+    gout[m] = acc;
+  }
+  double v[4] = {a_g, a_res, a_num, a_den};
+  block_reduce_store<4>(v, parts + 4 * (size_t)blockIdx.x);
+}
+
+__global__ void update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir,
+                              const double* __restrict__ obj_parts, int n_obj,
+                              const double* __restrict__ dc_parts, int n_dc,
+                              const double* __restrict__ els_parts, int n_els, int dc_mode, double lam,
+                              double* __restrict__ rec) {
+  __shared__ double s_eta;
+  __shared__ int s_skip;
+  if (threadIdx.x < 32) {
+    const double obj_c = warp_sum_parts(obj_parts, n_obj, 1, 0);
+    const double gn2 = warp_sum_parts(dc_parts, n_dc, 4, 0);
+    const double res2 = warp_sum_parts(dc_parts, n_dc, 4, 1);
+    const double snum = warp_sum_parts(dc_parts, n_dc, 4, 2);
+    const double sden = warp_sum_parts(dc_parts, n_dc, 4, 3);
+    const double num_c = warp_sum_parts(els_parts, n_els, 2, 0);
+    const double den_c = warp_sum_parts(els_parts, n_els, 2, 1);
+    if (threadIdx.x == 0) {
+      double obj = obj_c, num = num_c, den = den_c;
+      if (dc_mode == 1) {
+        obj += lam * res2;
+        num += lam * snum;
+        den += lam * sden;
+      }
+      // solver.py:347: the ELS convolution only runs when any(g); H(0) == 0
+      // exactly, so num = den = 0 falls out when g vanishes.
+      const bool degenerate = !(den > 0.0);
+      const double eta = degenerate ? 0.0 : num / den;
+      s_eta = eta;
+      s_skip = degenerate ? 1 : 0;
+      if (blockIdx.x == 0) {
+        rec[HICU_REC_OBJ] = obj;
+        rec[HICU_REC_NUM] = num;
+        rec[HICU_REC_DEN] = den;
+        rec[HICU_REC_ETA] = eta;
+        rec[HICU_REC_OBJ_AFTER] = degenerate ? obj : obj - num * num / den;
+        rec[HICU_REC_GNORM2] = gn2;
+        rec[HICU_REC_DEGENERATE] = degenerate ? 1.0 : 0.0;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        rec[7] = (double)t;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_skip) return;
+  const float eta = (float)s_eta;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const float2 gv = gdir[m];
+    float2 yv = y[m];
+    yv.x = fmaf(-eta, gv.x, yv.x);
+    yv.y = fmaf(-eta, gv.y, yv.y);
+    y[m] = yv;
+  }
+}
+
+__global__ void ser_kernel(int64_t N, const float2* __restrict__ ref, const float2* __restrict__ y,
+                           double* __restrict__ parts) {
+  double e = 0.0, r = 0.0;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N;
+       m += (int64_t)gridDim.x * blockDim.x) {
+    const float2 a = ref[m], b = y[m];
+    const double dx = (double)a.x - b.x, dy = (double)a.y - b.y;
+    e += dx * dx + dy * dy;
+    r += (double)a.x * a.x + (double)a.y * a.y;
+  }
+  double v[2] = {e, r};
+  block_reduce_store<2>(v, parts + 2 * (size_t)blockIdx.x);
+}
+
+template <int PMAX>
+int launch_conv(const DevGeom& g, const float2* y, const float2* qt, int p, float2* u, double* parts,
+                int mode, cudaStream_t st) {
+  const int blocks = conv_blocks(g.s);
+  const bool circ = g.ncirc > 0;
+  size_t smem = (size_t)g.n * PMAX * sizeof(float2) + (size_t)g.n * sizeof(int64_t) +
+                (circ ? (size_t)g.n * g.ndim * sizeof(int32_t) : 0);
+  if (smem > 200 * 1024) return hicu_set_error(HICU_ERR_SIZE, "conv: n*p too large for shared memory");
+#define HICU_LAUNCH_CONV(C, M)                                                                    \
+  do {                                                                                            \
+    auto kfn = conv_kernel<PMAX, C, M>;                                                           \
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    kfn<<<blocks, kConvThreads, smem, st>>>(g, y, qt, p, u, parts);                               \
+  } while (0)
+  if (circ) {
+    if (mode == 0) HICU_LAUNCH_CONV(true, 0); else HICU_LAUNCH_CONV(true, 1);
+  } else {
+    if (mode == 0) HICU_LAUNCH_CONV(false, 0); else HICU_LAUNCH_CONV(false, 1);
+  }
+#undef HICU_LAUNCH_CONV
+  return hicu_check_cuda(cudaGetLastError(), "conv_kernel");
+}
+
+int conv_dispatch(const hicu_geom* hg, const void* y, const void* qt, int p, const void* u_in, void* u_out,
+                  double* parts, int mode, void* stream) {
+  if (!hg || !y || !qt || !parts || p < 1) return hicu_set_error(HICU_ERR_PARAMETER, "conv: bad arguments");
+  if (p > 16) return hicu_set_error(HICU_ERR_PARAMETER, "conv: p > 16 not supported");
+  DevGeom g;
+  int st = hicu_make_devgeom(hg, &g);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  float2* u = mode == 0 ? (float2*)u_out : (float2*)u_in;
+  if (!u) return hicu_set_error(HICU_ERR_PARAMETER, "conv: null u");
+  if (p <= 4) return launch_conv<4>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+  if (p <= 8) return launch_conv<8>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+  return launch_conv<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+}
+
+template <int PMAX>
+int launch_scatter(const DevGeom& g, const float2* qt, int p, const float2* u, const uint8_t* mask,
+                   const float2* y, const float2* x0, int dc_mode, float lam, float2* gout, double* parts,
+                   cudaStream_t st) {
+  const int blocks = scatter_blocks(g.N);
+  size_t smem = (size_t)g.n * PMAX * sizeof(float2) +
+                (((size_t)g.n * g.ndim + 1) & ~(size_t)1) * sizeof(int32_t) + (size_t)g.n * sizeof(int64_t);
+  if (smem > 200 * 1024) return hicu_set_error(HICU_ERR_SIZE, "scatter: n*p too large for shared memory");
+  if (g.ncirc > 0) {
+    auto kfn = scatter_kernel<PMAX, true>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+  } else {
+    auto kfn = scatter_kernel<PMAX, false>;
+    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+  }
+  return hicu_check_cuda(cudaGetLastError(), "scatter_kernel");
+}
+
+}  // namespace
+
+extern "C" int hicu_conv_nparts(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return -1;
+  return conv_blocks(g.s);
+}
+
+extern "C" int hicu_scatter_nparts(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return -1;
+  return scatter_blocks(g.N);
+}
+
+extern "C" int hicu_conv_fwd(const hicu_geom* g, const void* y, const void* qt, int p, void* u,
+                             double* obj_parts, void* stream) {
+  return conv_dispatch(g, y, qt, p, nullptr, u, obj_parts, 0, stream);
+}
+
+extern "C" int hicu_conv_els(const hicu_geom* g, const void* gdir, const void* qt, int p, const void* u,
+                             double* numden_parts, void* stream) {
+  return conv_dispatch(g, gdir, qt, p, u, nullptr, numden_parts, 1, stream);
+}
+
+extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const void* u, const uint8_t* mask,
+                               const void* y, const void* x0, int dc_mode, double lam, void* gout,
+                               double* dc_parts, void* stream) {
+  if (!hg || !qt || !u || (!mask && dc_mode != 2) || !gout || !dc_parts || p < 1)
+    return hicu_set_error(HICU_ERR_PARAMETER, "scatter: bad arguments");
+  if (p > 16) return hicu_set_error(HICU_ERR_PARAMETER, "scatter: p > 16 not supported");
+  if (dc_mode < 0 || dc_mode > 2) return hicu_set_error(HICU_ERR_SHAPE, "scatter: unknown dc mode");
+  if (dc_mode == 1 && (!y || !x0)) return hicu_set_error(HICU_ERR_SHAPE, "soft data consistency requires x0");
+  DevGeom g;
+  int st = hicu_make_devgeom(hg, &g);
+  if (st) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto q = (const float2*)qt;
+  auto uu = (const float2*)u;
+  if (p <= 4)
+    return launch_scatter<4>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
+                             (float2*)gout, dc_parts, s);
+  if (p <= 8)
+    return launch_scatter<8>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
+                             (float2*)gout, dc_parts, s);
+  return launch_scatter<16>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
+                            (float2*)gout, dc_parts, s);
+}
+
+extern "C" int hicu_step_update(int64_t N, void* y, const void* gdir, const double* obj_parts, int n_obj,
+                                const double* dc_parts, int n_dc, const double* els_parts, int n_els,
+                                int dc_mode, double lam, double* rec, void* stream) {
+  if (!y || !gdir || !obj_parts || !dc_parts || !els_parts || !rec || N < 1)
+    return hicu_set_error(HICU_ERR_PARAMETER, "update: bad arguments");
+  int64_t b = (N + 255) / 256;
+  int64_t cap = (int64_t)hicu_sm_count() * 4;
+  if (b > cap) b = cap;
+  update_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(N, (float2*)y, (const float2*)gdir, obj_parts, n_obj,
+                                                           dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec);
+  return hicu_check_cuda(cudaGetLastError(), "update_kernel");
+}
+
+__global__ void timestamp_kernel(double* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = (double)t;
+}
+
+int ser_blocks(int64_t N) {
+  int64_t b = (N + 255) / 256;
+  int64_t cap = (int64_t)hicu_sm_count() * 2;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+extern "C" int hicu_timestamp(double* out, void* stream) {
+  if (!out) return hicu_set_error(HICU_ERR_PARAMETER, "timestamp: null");
+  timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(out);
+  return hicu_check_cuda(cudaGetLastError(), "timestamp_kernel");
+}
+
+extern "C" int hicu_ser_nparts(int64_t N) { return ser_blocks(N); }
+
+extern "C" int hicu_ser_parts(int64_t N, const void* ref, const void* y, double* parts, int* nparts_out,
+                              void* stream) {
+  if (!ref || !y || !parts || N < 1) return hicu_set_error(HICU_ERR_PARAMETER, "ser: bad arguments");
+  const int b = ser_blocks(N);
+  if (nparts_out) *nparts_out = b;
+  ser_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(N, (const float2*)ref, (const float2*)y, parts);
+  return hicu_check_cuda(cudaGetLastError(), "ser_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Kernel-slot adjoint out[kappa, j] = sum_i conj(X[i+kappa]) u[i, j]
+// (hankel_adjoint_apply, hankel.py:325-391).  Not on the solver's hot path
+// (the Gram replaces it); provided for the operator-level API.
+// ---------------------------------------------------------------------------
+namespace {
+template <bool CIRC>
+__global__ void conv_adj_kernel(DevGeom g, const float2* __restrict__ x, const float2* __restrict__ u, int k,
+                                double2* __restrict__ out) {
+  const int kap = blockIdx.x;
+  const int j = blockIdx.y;
+  const int32_t* pk = g.pos + (size_t)kap * g.ndim;
+  double ax = 0.0, ay = 0.0;
+  for (int64_t i = threadIdx.x; i < g.s; i += blockDim.x) {
+    int cc[HICU_MAX_NDIM];
+    int64_t addr = row_base(g, i, cc) + g.koff[kap];
+    if (CIRC) addr += circ_part(g, cc, pk);
+    const float2 xv = x[addr], uv = u[(size_t)i * k + j];
+    ax += (double)xv.x * uv.x + (double)xv.y * uv.y;
+    ay += (double)xv.x * uv.y - (double)xv.y * uv.x;
+  }
+  double v[2] = {ax, ay};
+  __shared__ double res[2];
+  block_reduce_store<2>(v, res);
+  __syncthreads();
+  if (threadIdx.x == 0) out[(size_t)kap * k + j] = cd(res[0], res[1]);
+}
+}  // namespace
+
+extern "C" int hicu_conv_adj(const hicu_geom* hg, const void* x, const void* u, int k, void* out, void* stream) {
+  if (!hg || !x || !u || !out || k < 1) return hicu_set_error(HICU_ERR_PARAMETER, "conv_adj: bad arguments");
+  DevGeom g;
+  int st = hicu_make_devgeom(hg, &g);
+  if (st) return st;
+  dim3 grid(g.n, k);
+  if (g.ncirc > 0)
+    conv_adj_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(g, (const float2*)x, (const float2*)u, k,
+                                                                  (double2*)out);
+  else
+    conv_adj_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(g, (const float2*)x, (const float2*)u, k,
+                                                                   (double2*)out);
+  return hicu_check_cuda(cudaGetLastError(), "conv_adj_kernel");
+}
+
+// Soft-DC line-search terms for the operator-level API (hankel.py:546-550):
+// parts[3b] = Re<Mg, res>, [3b+1] = |Mg|^2, [3b+2] = |res|^2, res = M(y - x0).
+namespace {
+__global__ void soft_terms_kernel(int64_t N, const float2* __restrict__ g, const float2* __restrict__ y,
+                                  const float2* __restrict__ x0, const uint8_t* __restrict__ mask,
+                                  double* __restrict__ parts) {
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N; m += (int64_t)gridDim.x * blockDim.x) {
+    if (mask[m] != 1) continue;
+    const float2 gv = g[m];
+    const float2 res = y[m] - x0[m];
+    a += (double)gv.x * res.x + (double)gv.y * res.y;
+    b += (double)gv.x * gv.x + (double)gv.y * gv.y;
+    c += (double)res.x * res.x + (double)res.y * res.y;
+  }
+  double v[3] = {a, b, c};
+  block_reduce_store<3>(v, parts + 3 * (size_t)blockIdx.x);
+}
+}  // namespace
+
+extern "C" int hicu_soft_terms(int64_t N, const void* g, const void* y, const void* x0, const uint8_t* mask,
+                               double* parts, int* nparts_out, void* stream) {
+  if (!g || !y || !x0 || !mask || !parts || N < 1) return hicu_set_error(HICU_ERR_PARAMETER, "soft_terms: bad args");
+  const int b = ser_blocks(N);
+  if (nparts_out) *nparts_out = b;
+  soft_terms_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(N, (const float2*)g, (const float2*)y, (const float2*)x0,
+                                                         mask, parts);
+  return hicu_check_cuda(cudaGetLastError(), "soft_terms_kernel");
+}

@@ -1,0 +1,539 @@
+"""Staged HICU reconstruction on the B200 — drop-in for ``hicu.hicu_reconstruct``.
+
+Mirrors the reference module ``hicu.solver`` (solver.py): ``StageSpec``,
+``SolverSchedule``, ``stage_region``, the record types and
+``hicu_reconstruct`` keep their names, arguments, validation and error
+classes.  The algorithm is the reference's Algorithm 1 (solver.py:258-398):
+per outer iteration a nullspace estimate of the stage region's lifted matrix,
+its Householder complement, then ``gradient_steps`` steps each with a fresh
+JL compression, a gradient, an exact line search and an update.
+
+B200 execution: all random draws are made on the host up front with the
+reference's streams (``RngStream(seed).child(1, stage, it)`` for the sketch,
+``child(2, stage, it, step)`` for JL), uploaded once, and each stage runs as
+ONE call into the native driver ``hicu_run_stage`` (engine.cu), which
+launches Gram -> Nystrom -> Householder -> Q~ and the fused gradient-step
+kernels on one CUDA stream with no host synchronisation.  Per-step scalars
+live in a device record array that is read once per stage.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ConfigError, DegenerateInputError
+from .hankel import Counters, KernelMask, MemoryMeter, Region, device_geometry, full_region, to_dev
+from .subspace import RngStream, complex_normal
+
+__all__ = [
+    "StageSpec",
+    "SolverSchedule",
+    "stage_region",
+    "StepRecord",
+    "IterationRecord",
+    "ReconReport",
+    "hicu_reconstruct",
+    "ReconEngine",
+]
+
+_RSVD_STREAM = 1
+_JL_STREAM = 2
+
+
+@dataclass
+class StageSpec:
+    """One stage (solver.py:51-72): region, compression p, gradient steps per
+    nullspace update, iterations."""
+
+    region: object
+    p: int
+    gradient_steps: int
+    iterations: int
+
+    def validate(self) -> None:
+        if self.p < 1:
+            raise ConfigError("p must be >= 1")
+        if self.gradient_steps < 1:
+            raise ConfigError("gradient_steps must be >= 1")
+        if self.iterations < 1:
+            raise ConfigError("iterations must be >= 1")
+        if self.p > 16:
+            raise ConfigError("p must be <= 16 on the B200 path")
+
+
+@dataclass
+class SolverSchedule:
+    """Rank, stages, wrap axes, data consistency, seed (solver.py:75-101)."""
+
+    rank: int
+    stages: list
+    circular_axes: tuple = ()
+    dc_mode: str = "hard"
+    dc_lambda: float = 0.0
+    seed: int = 0
+
+    def validate(self, kernel: KernelMask, dims) -> list:
+        if self.rank < 1:
+            raise ConfigError("rank must be >= 1")
+        if self.rank >= kernel.n:
+            raise ConfigError(f"rank {self.rank} must be below the kernel support size {kernel.n}")
+        if not self.stages:
+            raise ConfigError("schedule needs at least one stage")
+        if self.dc_mode not in ("hard", "soft"):
+            raise ConfigError(f"unknown dc_mode {self.dc_mode!r}")
+        if self.dc_mode == "soft" and self.dc_lambda <= 0:
+            raise ConfigError("soft data consistency needs dc_lambda > 0")
+        regions = []
+        for stage in self.stages:
+            stage.validate()
+            regions.append(stage_region(dims, kernel, stage.region, self.circular_axes))
+        return regions
+
+
+def _window_extent(entry, n_d: int, k_d: int, axis: int) -> int:
+    """solver.py:104-124 (fractions use Python's round(): banker's rounding)."""
+    if entry == "full":
+        return n_d
+    if isinstance(entry, bool):
+        raise ConfigError(f"invalid region entry {entry!r} on axis {axis}")
+    if isinstance(entry, (int, np.integer)):
+        w = int(entry)
+    elif isinstance(entry, (float, Fraction)):
+        f = float(entry)
+        if not (0.0 < f <= 1.0):
+            raise ConfigError(f"region fraction on axis {axis} must be in (0, 1], got {f}")
+        w = int(round(f * n_d))
+    else:
+        raise ConfigError(f"invalid region entry {entry!r} on axis {axis}")
+    if w < k_d:
+        raise ConfigError(f"stage window {w} on axis {axis} is smaller than the kernel extent {k_d}")
+    if w > n_d:
+        raise ConfigError(f"stage window {w} on axis {axis} exceeds the array extent {n_d}")
+    return w
+
+
+def stage_region(dims, kernel: KernelMask, fraction, circular_axes=()) -> Region:
+    """Centered convolution-output region for one stage (solver.py:127-158).
+
+    The center-out schedule is a restriction of the same operators (kernel
+    parameters roff/rext), not a separate code path."""
+    dims = tuple(int(d) for d in dims)
+    nd = len(dims)
+    circ = frozenset(int(a) % nd for a in circular_axes)
+    if isinstance(fraction, str) and fraction == "full":
+        entries = ["full"] * nd
+    else:
+        entries = list(fraction)
+        if len(entries) > nd:
+            raise ConfigError(f"region spec has {len(entries)} entries for {nd} axes")
+        entries += ["full"] * (nd - len(entries))
+    offsets, extents = [], []
+    for d, (n_d, k_d) in enumerate(zip(dims, kernel.extents)):
+        if k_d > n_d:
+            raise ConfigError(f"kernel extent {k_d} exceeds array extent {n_d} on axis {d}")
+        if d in circ:
+            offsets.append(0)
+            extents.append(n_d)
+            continue
+        entry = "full" if d == nd - 1 else entries[d]
+        w = _window_extent(entry, n_d, k_d, d)
+        offsets.append((n_d - w) // 2)
+        extents.append(w - k_d + 1)
+    region = Region(tuple(offsets), tuple(extents), circ)
+    region.validate(kernel, dims)
+    return region
+
+
+@dataclass
+class StepRecord:
+    stage: int
+    iteration: int
+    step: int
+    eta: float
+    objective_before: float
+    objective_after: float
+    seconds: float
+    ser_db: float | None = None
+
+
+@dataclass
+class IterationRecord:
+    stage: int
+    iteration: int
+    objective: float | None
+    seconds: float
+    ser_db: float | None = None
+    tail_energy: float | None = None
+
+
+@dataclass
+class ReconReport:
+    """Per-run trace (solver.py:161-231) plus B200 extras (``device``,
+    ``coil_basis``)."""
+
+    steps: list = field(default_factory=list)
+    iterations: list = field(default_factory=list)
+    events: list = field(default_factory=list)
+    counters: dict = field(default_factory=dict)
+    peak_aux_complex: int = 0
+    total_seconds: float = 0.0
+    device: dict = field(default_factory=dict)
+    coil_basis: np.ndarray | None = None
+
+    def to_dict(self) -> dict:
+        def _num(v):
+            if v is None:
+                return None
+            if isinstance(v, float) and not np.isfinite(v):
+                return "+inf" if v > 0 else "-inf"
+            return v
+
+        return {
+            "steps": [
+                {"stage": s.stage, "iteration": s.iteration, "step": s.step, "eta": s.eta,
+                 "objective_before": s.objective_before, "objective_after": s.objective_after,
+                 "seconds": s.seconds, "ser_db": _num(s.ser_db)}
+                for s in self.steps
+            ],
+            "iterations": [
+                {"stage": i.stage, "iteration": i.iteration, "objective": i.objective, "seconds": i.seconds,
+                 "ser_db": _num(i.ser_db), "tail_energy": i.tail_energy}
+                for i in self.iterations
+            ],
+            "events": list(self.events),
+            "counters": dict(self.counters),
+            "peak_aux_complex": self.peak_aux_complex,
+            "total_seconds": self.total_seconds,
+            "device": dict(self.device),
+        }
+
+
+class _Stopwatch:
+    """Wall clock paused while instrumentation runs (solver.py:234-248)."""
+
+    def __init__(self):
+        self.total = 0.0
+        self._t0 = time.perf_counter()
+
+    def pause(self) -> float:
+        self.total += time.perf_counter() - self._t0
+        self._t0 = None
+        return self.total
+
+    def resume(self) -> None:
+        self._t0 = time.perf_counter()
+
+
+def _ser_from_parts(parts: np.ndarray) -> float:
+    e = math.fsum(parts[0::2].tolist())
+    r = math.fsum(parts[1::2].tolist())
+    if e == 0.0:
+        return float("inf")
+    return 20.0 * math.log10(math.sqrt(r) / math.sqrt(e))
+
+
+def draw_stage(schedule: SolverSchedule, si: int, stage: StageSpec, n: int):
+    """Host draws for one stage with the reference streams: omega
+    (iters, n, l) and pbig (iters, n, G*p) with P_j in rows r.. of column
+    block j (solver.py:325-333, subspace.py:112-116, 228)."""
+    r = schedule.rank
+    ell = math.ceil(1.5 * r)
+    root = RngStream(schedule.seed)
+    G, p = stage.gradient_steps, stage.p
+    omega = np.empty((stage.iterations, n, ell), np.complex128)
+    pbig = np.zeros((stage.iterations, n, G * p), np.complex128)
+    for it in range(stage.iterations):
+        omega[it] = complex_normal(root.child(_RSVD_STREAM, si, it).generator(), (n, ell), 1.0)
+        for j in range(G):
+            pbig[it, r:, j * p:(j + 1) * p] = complex_normal(
+                root.child(_JL_STREAM, si, it, j).generator(), (n - r, p), 1.0 / p)
+    return omega, pbig
+
+
+class ReconEngine:
+    """Device-resident state for one reconstruction: the iterate, mask, data
+    and every scratch buffer, plus one ``hicu_stage_args`` per stage.
+
+    ``run_stage`` issues one native call per stage (or per iteration when
+    per-iteration host work is requested).  The same engine can be re-run
+    (``reset``) for benchmarking without reallocating."""
+
+    def __init__(self, x_c64, mask_u8, kernel: KernelMask, schedule: SolverSchedule, regions, reference_c64=None):
+        torch = nat.require_cuda()
+        self.torch = torch
+        self.kernel = kernel
+        self.schedule = schedule
+        self.regions = regions
+        self.dims = tuple(x_c64.shape)
+        self.N = int(np.prod(self.dims))
+        n, r = kernel.n, schedule.rank
+        self.n, self.r = n, r
+        self.ell = math.ceil(1.5 * r)
+        self.soft = schedule.dc_mode == "soft"
+        dev = "cuda"
+        self.x_init = to_dev(x_c64).reshape(-1)
+        self.y = self.x_init.clone()
+        self.mask = to_dev(mask_u8, np.uint8).reshape(-1)
+        self.x0 = self.x_init.clone() if self.soft else None
+        self.ref = to_dev(reference_c64).reshape(-1) if reference_c64 is not None else None
+        self.geoms = [device_geometry(kernel, reg, self.dims) for reg in regions]
+        L = nat.lib()
+        pmax = max(st.p for st in schedule.stages)
+        gmax = max(st.gradient_steps for st in schedule.stages)
+        smax = max(reg.s for reg in regions)
+        ncp = max(g.conv_nparts for g in self.geoms)
+        nsp = max(g.scatter_nparts for g in self.geoms)
+        gram_ws = max(int(L.hicu_gram_workspace(g.ref())) for g in self.geoms)
+        self.nys_bytes = int(L.hicu_nystrom_workspace(n, self.ell))
+        self.gram_bytes = gram_ws
+        c128, c64, f64, i32 = torch.complex128, torch.complex64, torch.float64, torch.int32
+        self.G = torch.empty((n, n), dtype=c128, device=dev)
+        self.gram_ws = torch.empty(max(gram_ws, 8), dtype=torch.uint8, device=dev)
+        self.nys_ws = torch.empty(self.nys_bytes, dtype=torch.uint8, device=dev)
+        self.V = torch.empty((n, r), dtype=c128, device=dev)
+        self.refl = torch.empty(2 * n * r, dtype=c128, device=dev)
+        self.tau = torch.empty(r, dtype=c128, device=dev)
+        self.flags = torch.empty(r, dtype=i32, device=dev)
+        self.status = torch.zeros(1, dtype=i32, device=dev)
+        self.B = torch.empty((n, gmax * pmax), dtype=c128, device=dev)
+        self.qt32 = torch.empty(gmax * n * pmax, dtype=c64, device=dev)
+        self.u = torch.empty(smax * pmax, dtype=c64, device=dev)
+        self.g = torch.empty(self.N, dtype=c64, device=dev)
+        self.obj_parts = torch.empty(ncp, dtype=f64, device=dev)
+        self.dc_parts = torch.empty(4 * nsp, dtype=f64, device=dev)
+        self.els_parts = torch.empty(2 * ncp, dtype=f64, device=dev)
+        self.ser_stride = 2 * int(L.hicu_ser_nparts(self.N))
+        self.t0 = torch.zeros(1, dtype=f64, device=dev)
+        self.aux_complex = (n * n + 2 * n * self.ell + 2 * self.ell * self.ell + 2 * n * r + n * gmax * pmax
+                            + smax * pmax + self.N)
+        self.stage_data = [None] * len(schedule.stages)
+        self.recs = [None] * len(schedule.stages)
+        self.sers = [None] * len(schedule.stages)
+        self.inject = [None] * len(schedule.stages)
+
+    # -- inputs --------------------------------------------------------------
+    def upload_draws(self, si: int, omega: np.ndarray, pbig: np.ndarray):
+        self.stage_data[si] = (to_dev(omega, np.complex128), to_dev(pbig, np.complex128))
+        st = self.schedule.stages[si]
+        self.recs[si] = self.torch.zeros(st.iterations * st.gradient_steps * nat.REC_SLOTS,
+                                         dtype=self.torch.float64, device="cuda")
+        if self.ref is not None:
+            self.sers[si] = self.torch.zeros(st.iterations * st.gradient_steps * self.ser_stride,
+                                             dtype=self.torch.float64, device="cuda")
+
+    def set_injected_v(self, si: int, v_all):
+        """Lockstep parity: use the given V (iters, n, r) instead of Gram+Nystrom."""
+        self.inject[si] = None if v_all is None else to_dev(v_all, np.complex128)
+
+    def reset(self):
+        self.y.copy_(self.x_init)
+        self.status.zero_()
+
+    def stamp_start(self):
+        nat.check(nat.lib().hicu_timestamp(self.t0.data_ptr(), nat.stream_handle()), "timestamp")
+
+    # -- execution -----------------------------------------------------------
+    def stage_args(self, si: int, it0: int = 0, iters: int | None = None):
+        st = self.schedule.stages[si]
+        gm = self.geoms[si]
+        iters = st.iterations - it0 if iters is None else iters
+        omega, pbig = self.stage_data[si]
+        a = nat.HicuStageArgs()
+        a.geom = gm.struct
+        a.r, a.ell, a.p, a.gsteps, a.iters = self.r, self.ell, st.p, st.gradient_steps, iters
+        a.dc_mode = 1 if self.soft else 0
+        a.lam = float(self.schedule.dc_lambda) if self.soft else 0.0
+        a.householder_tol = 1e-12
+        a.N = self.N
+        a.y = self.y.data_ptr()
+        a.mask = self.mask.data_ptr()
+        a.x0 = self.x0.data_ptr() if self.x0 is not None else None
+        a.omega = omega[it0].data_ptr() if iters > 0 else omega.data_ptr()
+        a.pbig = pbig[it0].data_ptr() if iters > 0 else pbig.data_ptr()
+        inj = self.inject[si]
+        a.inject_v = inj[it0].data_ptr() if inj is not None and iters > 0 else None
+        a.G, a.gram_ws, a.gram_ws_bytes = self.G.data_ptr(), self.gram_ws.data_ptr(), self.gram_bytes
+        a.nys_ws, a.nys_ws_bytes = self.nys_ws.data_ptr(), self.nys_bytes
+        a.V, a.refl, a.tau = self.V.data_ptr(), self.refl.data_ptr(), self.tau.data_ptr()
+        a.flags, a.status = self.flags.data_ptr(), self.status.data_ptr()
+        a.B, a.qt32, a.u, a.g = self.B.data_ptr(), self.qt32.data_ptr(), self.u.data_ptr(), self.g.data_ptr()
+        a.obj_parts, a.dc_parts, a.els_parts = (self.obj_parts.data_ptr(), self.dc_parts.data_ptr(),
+                                                self.els_parts.data_ptr())
+        G = st.gradient_steps
+        a.rec = self.recs[si].data_ptr() + it0 * G * nat.REC_SLOTS * 8
+        if self.ref is not None:
+            a.ref = self.ref.data_ptr()
+            a.ser_parts = self.sers[si].data_ptr() + it0 * G * self.ser_stride * 8
+            a.ser_stride = self.ser_stride
+        else:
+            a.ref = None
+            a.ser_parts = None
+            a.ser_stride = 0
+        return a
+
+    def run_stage(self, si: int, it0: int = 0, iters: int | None = None, stream=None):
+        a = self.stage_args(si, it0, iters)
+        nat.check(nat.lib().hicu_run_stage(ctypes.byref(a), nat.stream_handle(stream)), f"stage {si}")
+
+    def run_all(self, stream=None):
+        for si in range(len(self.schedule.stages)):
+            self.run_stage(si, stream=stream)
+
+    def check_status(self):
+        v = int(self.status.item())
+        if v != 0:
+            raise DegenerateInputError(
+                f"nullspace step failed on the device ({nat.lib().hicu_status_string(v).decode()})")
+
+    def tail_energy(self, kernel: KernelMask, tail_region: Region, r: int) -> float:
+        """sum_{j>r} sigma_j^2 of the full-region lifted matrix from its Gram
+        matrix (instrumentation; reference oracle.tail_energy_dense)."""
+        from .subspace import gram_matrix
+
+        G = gram_matrix(self.y.reshape(self.dims), kernel, tail_region).cpu().numpy()
+        lam = np.linalg.eigvalsh(0.5 * (G + G.conj().T))[::-1]
+        lam = np.clip(lam, 0.0, None)
+        return float(max(np.sum(lam[r:]), 0.0))
+
+    def download(self) -> np.ndarray:
+        return self.y.reshape(self.dims).cpu().numpy().astype(np.complex128)
+
+
+def _coil_compress_host_entry(x0, mask, reference, nv):
+    from .coil import coil_compress
+
+    xc, mc, basis = coil_compress(x0, mask, nv)
+    refc = None
+    if reference is not None:
+        nc = x0.shape[-1]
+        refc = (np.asarray(reference, np.complex128).reshape(-1, nc) @ basis).reshape(x0.shape[:-1] + (nv,))
+    return xc, mc, refc, basis
+
+
+def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, reference=None,
+                     tail_energy_threshold: int = 2**24, iterate_callback=None, counters: Counters | None = None,
+                     meter: MemoryMeter | None = None, *, coil_compress: int | None = None, lockstep_v=None):
+    """Run the staged completion on zero-filled observed k-space
+    (solver.py:258-398).  Returns ``(xhat, report)``; ``xhat`` is complex128
+    like the reference's.  In hard data-consistency mode the observed
+    samples of ``xhat`` equal ``x0`` bit-exactly.
+
+    B200 additions (keyword-only): ``coil_compress=Nv`` compresses the coil
+    axis to Nv virtual coils on the device first (the kernel's last extent
+    must then be Nv; ``xhat`` is in the compressed domain and
+    ``report.coil_basis`` holds the basis); ``lockstep_v`` is a callable
+    ``(stage, it) -> V`` that replaces the nullspace estimate (parity tests).
+    """
+    watch = _Stopwatch()
+    basis = None
+    if coil_compress is not None:
+        x0_in = np.ascontiguousarray(x0)
+        mask_in = np.asarray(mask)
+        if x0_in.shape != mask_in.shape:
+            raise ConfigError(f"mask shape {mask_in.shape} does not match k-space shape {x0_in.shape}")
+        x0, mask, reference, basis = _coil_compress_host_entry(x0_in, mask_in, reference, int(coil_compress))
+    x0 = np.ascontiguousarray(x0, dtype=np.complex128)
+    mask = np.asarray(mask)
+    if x0.shape != mask.shape:
+        raise ConfigError(f"mask shape {mask.shape} does not match k-space shape {x0.shape}")
+    regions = schedule.validate(kernel, x0.shape)
+    for region in regions:
+        ell = int(np.ceil(1.5 * schedule.rank))
+        if ell > region.s:
+            raise ConfigError(f"sketch width {ell} exceeds region size {region.s}; enlarge the stage region")
+    if int(np.ceil(1.5 * schedule.rank)) > 256:
+        raise ConfigError("rank above 170 is not supported by the device nullspace kernels")
+    counters = counters if counters is not None else Counters()
+    meter = meter if meter is not None else MemoryMeter()
+    report = ReconReport()
+    observed = mask == 1
+    x = np.where(observed, x0, 0)  # mask_apply (arrays.py:54-67), bit-exact copy where observed
+    mask_u8 = observed.astype(np.uint8)
+    ref128 = None if reference is None else np.asarray(reference, dtype=np.complex128)
+    eng = ReconEngine(x.astype(np.complex64), mask_u8, kernel, schedule, regions,
+                      None if ref128 is None else ref128.astype(np.complex64))
+    meter.alloc(eng.aux_complex)
+    tail_region = full_region(x0.shape, kernel, schedule.circular_axes)
+    log_tail = 0 < tail_energy_threshold and tail_region.s * kernel.n <= tail_energy_threshold
+    per_iter = log_tail or iterate_callback is not None
+    torch = eng.torch
+    eng.stamp_start()
+    for si, stage in enumerate(schedule.stages):
+        omega, pbig = draw_stage(schedule, si, stage, kernel.n)
+        eng.upload_draws(si, omega, pbig)
+        if lockstep_v is not None:
+            eng.set_injected_v(si, np.stack([np.asarray(lockstep_v(si, it), np.complex128)
+                                             for it in range(stage.iterations)]))
+        if not per_iter:
+            eng.run_stage(si)
+            continue
+        for it in range(stage.iterations):
+            eng.run_stage(si, it, 1)
+            torch.cuda.synchronize()
+            watch.pause()
+            eng.check_status()
+            xi = None
+            if log_tail:
+                tail = eng.tail_energy(kernel, tail_region, schedule.rank)
+                eng._tails = getattr(eng, "_tails", {})
+                eng._tails[(si, it)] = tail
+            if iterate_callback is not None:
+                xi = eng.download()
+                if schedule.dc_mode == "hard":
+                    xi[observed] = x0[observed]
+                iterate_callback(si, it, xi)
+            watch.resume()
+    torch.cuda.synchronize()
+    total = watch.pause()
+    eng.check_status()
+    # ---- records (one device->host read per stage) ----
+    t0 = float(eng.t0.item())
+    tails = getattr(eng, "_tails", {})
+    for si, stage in enumerate(schedule.stages):
+        rec = eng.recs[si].cpu().numpy().reshape(stage.iterations, stage.gradient_steps, nat.REC_SLOTS)
+        sers = None
+        if eng.ref is not None:
+            sers = eng.sers[si].cpu().numpy().reshape(stage.iterations, stage.gradient_steps, eng.ser_stride)
+        p = stage.p
+        for it in range(stage.iterations):
+            last_obj = None
+            last_sec = 0.0
+            last_ser = None
+            for j in range(stage.gradient_steps):
+                rj = rec[it, j]
+                sec = max((rj[nat.REC_TIME] - t0) * 1e-9, 0.0)
+                ser = _ser_from_parts(sers[it, j]) if sers is not None else None
+                counters.forward += p
+                counters.kspace_scatter += p
+                if rj[nat.REC_GNORM2] > 0.0:
+                    counters.forward += p
+                if rj[nat.REC_DEGENERATE] != 0.0:
+                    report.events.append({"stage": si, "iteration": it, "step": j, "reason": "degenerate-direction"})
+                    report.steps.append(StepRecord(si, it, j, 0.0, float(rj[nat.REC_OBJ]), float(rj[nat.REC_OBJ]),
+                                                   sec, ser))
+                else:
+                    report.steps.append(StepRecord(si, it, j, float(rj[nat.REC_ETA]), float(rj[nat.REC_OBJ]),
+                                                   float(rj[nat.REC_OBJ_AFTER]), sec, ser))
+                last_obj = float(rj[nat.REC_OBJ_AFTER])
+                last_sec, last_ser = sec, ser
+            if lockstep_v is None:
+                counters.gram += 1
+            report.iterations.append(IterationRecord(si, it, last_obj, last_sec, last_ser, tails.get((si, it))))
+    xhat = eng.download()
+    if schedule.dc_mode == "hard":
+        xhat[observed] = x0[observed]
+    report.total_seconds = total
+    report.counters = counters.snapshot()
+    report.peak_aux_complex = meter.peak
+    meter.free(eng.aux_complex)
+    report.device = {"name": torch.cuda.get_device_name(), "nullspace": "gram+nystrom" if lockstep_v is None
+                     else "injected", "precision": "c64 data, fp32 FMA, fp64 reductions / nullspace"}
+    report.coil_basis = basis
+    return xhat, report

@@ -1,0 +1,180 @@
+"""Nullspace estimation on the B200: seeded streams, the rSVD subspace from
+the Gram matrix, Householder complement and JL compression.
+
+Mirrors the reference module ``hicu.subspace`` (subspace.py).  Random draws
+stay on the host with the reference's exact streams (``RngStream``,
+``complex_normal``), so the device sees the same sketch Omega and the same
+JL matrices P as the reference for the same seed.
+
+``rsvd_right_vectors`` keeps the reference signature but computes the
+subspace as Gram + Nystrom on the device (include/hicu_b200.h:
+hicu_gram, hicu_nystrom).  For the same Omega it spans the same subspace as
+the reference's single-pass rSVD (subspace.py:67-155); the individual
+singular-vector phases differ from LAPACK zgesdd's.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .errors import DegenerateInputError, ParameterError
+from .hankel import Counters, KernelMask, MemoryMeter, Region, device_geometry, to_dev
+
+__all__ = [
+    "RngStream",
+    "complex_normal",
+    "NullspaceBasis",
+    "rsvd_right_vectors",
+    "householder_nullspace",
+    "jl_compress",
+    "gram_matrix",
+]
+
+
+@dataclass(frozen=True)
+class RngStream:
+    """Deterministic stream addressed by a seed and integer ids
+    (subspace.py:29-46): SeedSequence(entropy=seed, spawn_key=ids) -> PCG64."""
+
+    seed: int
+    ids: tuple = ()
+
+    def child(self, *ids: int) -> "RngStream":
+        return RngStream(self.seed, self.ids + tuple(int(i) for i in ids))
+
+    def generator(self) -> np.random.Generator:
+        ss = np.random.SeedSequence(entropy=self.seed, spawn_key=self.ids)
+        return np.random.Generator(np.random.PCG64(ss))
+
+
+def complex_normal(rng: np.random.Generator, shape, scale: float = 1.0) -> np.ndarray:
+    """i.i.d. complex Gaussian, per-entry variance ``scale`` (subspace.py:49-52)."""
+    block = rng.standard_normal(tuple(shape) + (2,))
+    return (block[..., 0] + 1j * block[..., 1]) * math.sqrt(scale / 2.0)
+
+
+@dataclass(eq=False)
+class NullspaceBasis:
+    """Orthonormal complement ``q`` (n x (n-r)) of the retained subspace."""
+
+    q: np.ndarray
+    r: int
+
+    @property
+    def n(self) -> int:
+        return self.q.shape[0]
+
+
+def gram_matrix(x, kernel: KernelMask, region: Region):
+    """G = H(x)^H H(x) (n x n, complex128) on the device; returns a CUDA tensor."""
+    torch = nat.require_cuda()
+    x = np.asarray(x) if not isinstance(x, torch.Tensor) else x
+    region.validate(kernel, tuple(x.shape))
+    dg = device_geometry(kernel, region, tuple(x.shape))
+    L = nat.lib()
+    ws_bytes = L.hicu_gram_workspace(dg.ref())
+    ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device="cuda")
+    G = torch.empty((kernel.n, kernel.n), dtype=torch.complex128, device="cuda")
+    nat.check(L.hicu_gram(dg.ref(), to_dev(x).data_ptr(), G.data_ptr(), ws.data_ptr(), ws_bytes, nat.stream_handle()),
+              "gram")
+    return G
+
+
+def _status(torch, st_t, what):
+    v = int(st_t.item())
+    if v != 0:
+        raise DegenerateInputError(f"{what}: device reported {nat.lib().hicu_status_string(v).decode()}")
+
+
+def rsvd_right_vectors(x, kernel: KernelMask, region: Region, r: int, rng: RngStream,
+                       counters: Counters | None = None, meter: MemoryMeter | None = None) -> np.ndarray:
+    """Principal r right singular vectors of the lifted matrix, sketched with
+    the reference's Omega (width l = ceil(1.5 r), stream ``rng``)."""
+    n = kernel.n
+    s = region.s
+    if not (1 <= r < n):
+        raise ParameterError(f"rank must satisfy 1 <= r < n={n}, got {r}")
+    ell = math.ceil(1.5 * r)
+    if ell > s:
+        raise ParameterError(f"sketch width {ell} exceeds region size {s}")
+    torch = nat.require_cuda()
+    omega = complex_normal(rng.generator(), (n, ell), 1.0)
+    G = gram_matrix(x, kernel, region)
+    if counters is not None:
+        counters.gram += 1
+    if meter is not None:
+        held = meter.alloc(n * n + 3 * n * ell)
+    L = nat.lib()
+    ws_bytes = L.hicu_nystrom_workspace(n, ell)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    V = torch.empty((n, r), dtype=torch.complex128, device="cuda")
+    st_t = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(L.hicu_nystrom(n, ell, r, G.data_ptr(), to_dev(omega, np.complex128).data_ptr(), V.data_ptr(),
+                             ws.data_ptr(), ws_bytes, st_t.data_ptr(), nat.stream_handle()), "rsvd_right_vectors")
+    _status(torch, st_t, "rsvd_right_vectors")
+    if meter is not None:
+        meter.free(held)
+    return V.cpu().numpy()
+
+
+def _reflectors(torch, vd, n, r, tol):
+    L = nat.lib()
+    refl = torch.empty(2 * n * r, dtype=torch.complex128, device="cuda")
+    tau = torch.empty(r, dtype=torch.complex128, device="cuda")
+    flags = torch.empty(r, dtype=torch.int32, device="cuda")
+    st_t = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(L.hicu_householder(n, r, vd.data_ptr(), float(tol), refl.data_ptr(), tau.data_ptr(), flags.data_ptr(),
+                                 st_t.data_ptr(), nat.stream_handle()), "householder_nullspace")
+    return refl, tau, flags, st_t
+
+
+def householder_nullspace(v, tol: float = 1e-12) -> NullspaceBasis:
+    """Orthonormal complement of span(v) by r complex reflections
+    (subspace.py:158-212), built on the device in fp64."""
+    v = np.array(v, dtype=np.complex128, order="C", copy=True)
+    if v.ndim != 2:
+        raise DegenerateInputError("v must be a 2-D matrix")
+    n, r = v.shape
+    if r > n:
+        raise DegenerateInputError(f"cannot have {r} orthonormal columns in dimension {n}")
+    m = n - r
+    if r == 0:
+        return NullspaceBasis(q=np.eye(n, dtype=np.complex128), r=0)
+    if m == 0:
+        # every column is spanned: the complement is empty (still validate v)
+        pass
+    torch = nat.require_cuda()
+    vd = to_dev(v, np.complex128)
+    refl, tau, flags, st_t = _reflectors(torch, vd, n, r, tol)
+    _status(torch, st_t, "householder_nullspace")
+    if m == 0:
+        return NullspaceBasis(q=np.zeros((n, 0), np.complex128), r=r)
+    b = np.zeros((n, m), np.complex128)
+    b[r:, :] = np.eye(m)
+    bd = to_dev(b, np.complex128)
+    nat.check(nat.lib().hicu_apply_reflectors(n, r, refl.data_ptr(), tau.data_ptr(), flags.data_ptr(), m,
+                                              bd.data_ptr(), bd.data_ptr(), None, 0, nat.stream_handle()),
+              "householder_nullspace")
+    return NullspaceBasis(q=bd.cpu().numpy(), r=r)
+
+
+def jl_compress(q, p: int, rng: RngStream) -> np.ndarray:
+    """Q~ = Q P with P ~ CN(0, 1/p) from stream ``rng`` (subspace.py:215-229)."""
+    if p < 1:
+        raise ParameterError(f"compression dimension must be >= 1, got {p}")
+    q = np.asarray(q, dtype=np.complex128)
+    if q.ndim != 2 or q.shape[1] < 1:
+        raise ParameterError("nullspace must have at least one column")
+    torch = nat.require_cuda()
+    proj = complex_normal(rng.generator(), (q.shape[1], p), 1.0 / p)
+    n, m = q.shape
+    out = torch.empty((n, p), dtype=torch.complex128, device="cuda")
+    nat.check(nat.lib().hicu_zgemm(b"N", b"N", n, p, m, to_dev(q, np.complex128).data_ptr(), m,
+                                   to_dev(proj, np.complex128).data_ptr(), p, out.data_ptr(), p,
+                                   nat.stream_handle()), "jl_compress")
+    return out.cpu().numpy()

@@ -1,0 +1,247 @@
+"""GPU parity of every hot-path operator against the reference's golden
+vectors and the oracle restatement (complex64 data on the device; the
+north-star tolerance is 1e-5 relative per kernel output)."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+import paper_2004_08962_b200 as H
+from oracle import hicu_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["c2d", "c2dcirc", "csub", "c3d", "cell", "c1d", "cnc"]
+TOL = 1e-5
+
+
+def c64(a):
+    return np.asarray(a).astype(np.complex64).astype(np.complex128)
+
+
+def rel(a, b):
+    return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
+
+
+def geom(g, name):
+    p = name + "_"
+    kernel = H.KernelMask(tuple(int(e) for e in g[p + "kext"]), g[p + "support"])
+    circ = frozenset(int(a) for a in np.nonzero(g[p + "circ"])[0])
+    region = H.Region(tuple(int(o) for o in g[p + "roff"]), tuple(int(e) for e in g[p + "rext"]), circ)
+    ogeom = O.Geom(tuple(int(d) for d in g[p + "dims"]), kernel.positions, region.offsets, region.extents, circ)
+    return kernel, region, ogeom
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_forward_adjoint_scatter_gram(golden_ops, name):
+    g = golden_ops
+    p = name + "_"
+    kernel, region, og = geom(g, name)
+    x, v, u = g[p + "x"], g[p + "v"], g[p + "u"]
+    # against the reference golden output (inputs rounded to c64 on the device)
+    assert rel(H.hankel_apply(x, v, kernel, region), g[p + "fwd"]) <= TOL
+    assert rel(H.hankel_adjoint_apply(x, u, kernel, region), g[p + "adj"]) <= TOL
+    assert rel(H.kspace_adjoint_scatter(v, u, kernel, region, x.shape), g[p + "scatter"]) <= TOL
+    G = H.gram_matrix(x, kernel, region).cpu().numpy()
+    assert rel(G, g[p + "gram"]) <= TOL
+    # exact Hermitian structure with a real diagonal
+    assert np.array_equal(G, G.conj().T)
+    # against the oracle on the identical c64-rounded inputs (tighter)
+    assert rel(H.hankel_apply(x, v, kernel, region), O.hankel_apply(c64(x), c64(v), og)) <= 2e-6
+    assert rel(G, O.gram(c64(x), og)) <= 2e-6
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("mode", ["hard", "soft"])
+def test_objective_gradient_els(golden_ops, name, mode):
+    g = golden_ops
+    p = name + "_"
+    kernel, region, og = geom(g, name)
+    x, v = g[p + "x"], g[p + "v"]
+    dc = H.DataConsistency(mode, g[p + "mask"], x0=g[p + "x0"] if mode == "soft" else None,
+                           lam=0.7 if mode == "soft" else 0.0)
+    grad, obj, u = H.objective_and_gradient(x, v, kernel, region, dc, return_products=True)
+    assert rel(grad, g[p + mode + "_grad"]) <= TOL
+    assert abs(obj - float(g[p + mode + "_obj"])) <= TOL * abs(float(g[p + mode + "_obj"]))
+    if mode == "hard":
+        assert not np.any(grad[g[p + "mask"] == 1])
+    eta, dec = H.exact_line_search(x, grad, v, kernel, region, dc, u=u, return_decrease=True)
+    assert abs(eta - float(g[p + mode + "_eta"])) <= 1e-4 * abs(float(g[p + mode + "_eta"]))
+    assert abs(dec - float(g[p + mode + "_dec"])) <= 1e-4 * abs(float(g[p + mode + "_dec"]))
+
+
+def test_known_answers():
+    # reference tests/test_hankel.py:42-64, 132-146, 284-296
+    k = H.KernelMask.full((2,))
+    out = H.hankel_apply(np.array([1.0, 2.0, 3.0], complex), np.array([1.0, -1.0]), k, H.full_region((3,), k))
+    assert np.allclose(out, [-1.0, -1.0], atol=0)
+    reg = H.full_region((3,), k, circular_axes=(0,))
+    out = H.hankel_apply(np.array([1.0, 2.0, 3.0], complex), np.array([1.0, 1.0]), k, reg)
+    assert np.allclose(out, [3.0, 5.0, 4.0], atol=0)
+    out = H.kspace_adjoint_scatter(np.array([1.0, 0.0], complex), np.array([2.0 + 1j, 3.0]), k,
+                                   H.full_region((3,), k), (3,))
+    assert np.allclose(out, [2.0 + 1j, 3.0, 0.0], atol=0)
+    u = np.array([2.0 + 1j, -1.0])
+    out = H.hankel_adjoint_apply(np.ones(3, complex), u, k, H.full_region((3,), k))
+    assert np.allclose(out, [u.sum(), u.sum()])
+    # impulse kernel == window slice, exactly
+    rng = np.random.default_rng(0)
+    x = c64(rng.standard_normal((6, 5)) + 1j * rng.standard_normal((6, 5)))
+    k2 = H.KernelMask.full((3, 2))
+    reg2 = H.full_region(x.shape, k2)
+    for row, (i, j) in enumerate(k2.positions):
+        v = np.zeros(k2.n, complex)
+        v[row] = 1.0
+        out = H.hankel_apply(x, v, k2, reg2).reshape(reg2.extents)
+        assert np.array_equal(out, x[i:i + 4, j:j + 4])
+    # scalar ELS: eta == 1 exactly annihilates
+    ks = H.KernelMask((2,), np.array([1, 0], np.uint8))
+    rs = H.full_region((2,), ks)
+    y = np.array([2.0 + 1j, 0.0])
+    dc = H.DataConsistency("hard", np.zeros(2, np.uint8))
+    grad, _ = H.objective_and_gradient(y, np.array([[1.0 + 0j]]), ks, rs, dc)
+    assert np.allclose(grad, [2.0 + 1j, 0.0])
+    eta = H.exact_line_search(y, grad, np.array([[1.0 + 0j]]), ks, rs, dc)
+    assert abs(eta - 1.0) <= 1e-7
+    with pytest.raises(H.DegenerateDirectionError):
+        H.exact_line_search(y, np.ones(2, complex), np.zeros((1, 1), complex), ks, rs, dc)
+
+
+def test_adjoint_identities_random():
+    # reference tests/test_hankel.py:156-177 (three-way adjoint identities)
+    rng = np.random.default_rng(6)
+    for trial in range(20):
+        dims = tuple(int(rng.integers(4, m + 1)) for m in (10, 8, 4))
+        kern = tuple(int(rng.integers(1, min(mk, d) + 1)) for mk, d in zip((4, 3, 4), dims))
+        k = H.KernelMask.full(kern)
+        reg = H.full_region(dims, k, (1,) if trial % 3 == 0 else ())
+        x = c64(rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+        v = c64(rng.standard_normal((k.n, 2)) + 1j * rng.standard_normal((k.n, 2)))
+        u = c64(rng.standard_normal((reg.s, 2)) + 1j * rng.standard_normal((reg.s, 2)))
+        scale = np.linalg.norm(v) * np.linalg.norm(u) * np.linalg.norm(x)
+        lhs = np.vdot(u, H.hankel_apply(x, v, k, reg))
+        rhs = np.vdot(H.hankel_adjoint_apply(x, u, k, reg), v)
+        assert abs(lhs - rhs) <= 1e-6 * scale
+        lhs2 = np.vdot(u[:, 0], H.hankel_apply(x, v[:, 0], k, reg))
+        rhs2 = np.vdot(H.kspace_adjoint_scatter(v[:, 0], u[:, 0], k, reg, dims), x)
+        assert abs(lhs2 - rhs2) <= 1e-6 * scale
+
+
+def test_wide_kernel_matrix_chunks():
+    rng = np.random.default_rng(2)
+    dims = (12, 11, 3)
+    k = H.KernelMask.full((3, 3, 3))
+    reg = H.full_region(dims, k)
+    og = O.full_geom(dims, (3, 3, 3))
+    x = c64(rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+    v = c64(rng.standard_normal((k.n, 37)) + 1j * rng.standard_normal((k.n, 37)))
+    assert rel(H.hankel_apply(x, v, k, reg), O.hankel_apply(x, v, og)) <= 2e-6
+    u = c64(rng.standard_normal((reg.s, 37)) + 1j * rng.standard_normal((reg.s, 37)))
+    assert rel(H.kspace_adjoint_scatter(v, u, k, reg, dims), O.kspace_adjoint_scatter(v, u, og)) <= 2e-6
+
+
+def test_householder_and_jl_match_golden(golden_ops):
+    g = golden_ops
+    q = H.householder_nullspace(g["sub_v"]).q
+    assert rel(q, g["sub_q"]) <= 1e-12
+    qt = H.jl_compress(g["sub_q"], 4, H.RngStream(int(g["sub_seed"]), (2, 0, 2, 1)))
+    assert rel(qt, g["sub_qt"]) <= 1e-12
+    # reference tests/test_subspace.py:55-81
+    q1 = H.householder_nullspace(np.array([[1.0], [0.0]], complex)).q
+    assert q1.shape == (2, 1) and abs(abs(q1[1, 0]) - 1.0) <= 1e-14 and abs(q1[0, 0]) <= 1e-14
+    assert np.array_equal(H.householder_nullspace(np.zeros((4, 0), complex)).q, np.eye(4, dtype=complex))
+    v = np.zeros((5, 2), complex)
+    v[0, 0] = v[0, 1] = 1.0
+    with pytest.raises(H.DegenerateInputError):
+        H.householder_nullspace(v)
+    rng = np.random.default_rng(0)
+    vv = np.linalg.qr(rng.standard_normal((20, 6)) + 1j * rng.standard_normal((20, 6)))[0]
+    qq = H.householder_nullspace(vv).q
+    assert np.linalg.norm(qq.conj().T @ vv) <= 1e-10
+    assert np.linalg.norm(qq.conj().T @ qq - np.eye(14)) <= 1e-10
+    assert rel(qq, O.householder_nullspace(vv)) <= 1e-12
+
+
+def _nystrom_device(G, omega, r):
+    import torch
+
+    from paper_2004_08962_b200 import _native as nat
+    from paper_2004_08962_b200.hankel import to_dev
+
+    n, ell = omega.shape
+    L = nat.lib()
+    ws_bytes = L.hicu_nystrom_workspace(n, ell)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    V = torch.empty((n, r), dtype=torch.complex128, device="cuda")
+    st = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(L.hicu_nystrom(n, ell, r, to_dev(G, np.complex128).data_ptr(), to_dev(omega, np.complex128).data_ptr(),
+                             V.data_ptr(), ws.data_ptr(), ws_bytes, st.data_ptr(), nat.stream_handle()))
+    assert int(st.item()) == 0
+    return V.cpu().numpy()
+
+
+def proj_dist(a, b):
+    return float(np.linalg.norm(a @ a.conj().T - b @ b.conj().T, 2))
+
+
+def test_nystrom_kernel_fp64_parity(golden_ops):
+    """The fp64 nullspace kernel on the oracle's exact Gram reproduces the
+    reference rSVD subspace for the same Omega (isolates K2 from the Gram)."""
+    g = golden_ops
+    x = g["sub_x"]
+    og = O.full_geom(x.shape, tuple(g["sub_kext"]))
+    r = int(g["sub_rank"])
+    omega = g["sub_omega"]
+    V = _nystrom_device(O.gram(x, og), omega, r)
+    assert np.linalg.norm(V.conj().T @ V - np.eye(r)) <= 1e-9
+    assert proj_dist(V, g["sub_v"]) <= 1e-8
+
+
+def test_nystrom_random_sizes():
+    rng = np.random.default_rng(5)
+    for n, r in [(50, 10), (200, 60), (120, 40)]:
+        a = rng.standard_normal((3 * n, n)) + 1j * rng.standard_normal((3 * n, n))
+        a = a * np.exp(-np.arange(n) / (n / 6.0))  # decaying spectrum
+        G = a.conj().T @ a
+        ell = math.ceil(1.5 * r)
+        om = O.complex_normal(rng, (n, ell))
+        V = _nystrom_device(G, om, r)
+        Vr = O.nystrom_right_vectors(G, om, r)
+        assert proj_dist(V, Vr) <= 1e-8, (n, r)
+
+
+def test_rsvd_right_vectors_gpu(golden_ops):
+    g = golden_ops
+    x = g["sub_x"]
+    k = H.KernelMask.full(tuple(g["sub_kext"]))
+    reg = H.full_region(x.shape, k)
+    r = int(g["sub_rank"])
+    V = H.rsvd_right_vectors(x, k, reg, r, H.RngStream(int(g["sub_seed"]), tuple(int(i) for i in g["sub_ids"])))
+    assert np.linalg.norm(V.conj().T @ V - np.eye(r)) <= 1e-9
+    # fp32 Gram accuracy bounds the subspace error by ~eps32*||G||/gap
+    assert proj_dist(V, g["sub_v"]) <= 1e-3
+    # exact-rank-ish constant signal (reference tests/test_subspace.py:85-92)
+    k1 = H.KernelMask.full((2,))
+    V1 = H.rsvd_right_vectors(np.full(4, 2.5 + 0.5j), k1, H.full_region((4,), k1), 1, H.RngStream(0))
+    t = np.array([1.0, 1.0]) / np.sqrt(2)
+    assert abs(abs(np.vdot(V1[:, 0], t)) - 1.0) <= 1e-6
+    with pytest.raises(H.ParameterError):
+        H.rsvd_right_vectors(np.zeros((6, 6), complex), H.KernelMask.full((2, 2)),
+                             H.full_region((6, 6), H.KernelMask.full((2, 2))), 4, H.RngStream(0))
+
+
+def test_coil_compression_vs_oracle():
+    rng = np.random.default_rng(3)
+    nx, ny, nc, nv = 24, 20, 12, 3
+    base = rng.standard_normal((nx, ny, 3)) + 1j * rng.standard_normal((nx, ny, 3))
+    mix = rng.standard_normal((3, nc)) + 1j * rng.standard_normal((3, nc))
+    x = c64(base @ mix + 0.01 * (rng.standard_normal((nx, ny, nc)) + 1j * rng.standard_normal((nx, ny, nc))))
+    mask = np.repeat((rng.random((nx, ny, 1)) < 0.4).astype(np.uint8), nc, axis=2)
+    x = np.where(mask == 1, x, 0)
+    xc, mc, basis = H.coil_compress(x, mask, nv)
+    xo, mo, bo = O.coil_compress(x, mask, nv)
+    assert np.array_equal(mc, mo)
+    assert rel(basis, bo) <= 1e-6
+    assert rel(xc, xo) <= 1e-5

@@ -148,8 +148,9 @@ int hicu_zgemm(char opa, char opb, int m, int n, int k, const void* A, int lda,
 /* Top-r right singular subspace of H from its Gram matrix with the host
  * sketch omega (n x ell c128): Nystrom form of the reference's single-pass
  * rSVD (same subspace for the same omega).  Writes V (n x r c128, orthonormal
- * columns ordered by decreasing singular value) and *status_dev (device int,
- * HICU_OK or HICU_ERR_DEGENERATE_INPUT). */
+ * columns ordered by decreasing singular value, each column's phase fixed so
+ * its largest-magnitude entry, first on ties, is real positive) and
+ * *status_dev (device int, HICU_OK or HICU_ERR_DEGENERATE_INPUT). */
 size_t hicu_nystrom_workspace(int n, int ell);
 int hicu_nystrom(int n, int ell, int r, const void* G, const void* omega,
                  void* V, void* ws, size_t ws_bytes, int* status_dev,

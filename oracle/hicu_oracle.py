@@ -49,6 +49,7 @@ __all__ = [
     "rsvd_right_vectors",
     "nystrom_right_vectors",
     "householder_nullspace",
+    "canonicalize_phases",
     "jl_compress",
     "mask_apply",
     "hicu_reconstruct",
@@ -332,6 +333,21 @@ def nystrom_right_vectors(g, omega, r: int, rel_floor: float = 1e-13) -> np.ndar
     return (z @ f[:, order]) / np.sqrt(lam[order])
 
 
+def canonicalize_phases(v) -> np.ndarray:
+    """Rotate each column so its largest-|.| entry (first on ties) is real
+    positive.  Not a reference function: the reference keeps LAPACK zgesdd's
+    phases (subspace.py:150-154), an implementation detail that the
+    Householder basis depends on.  Oracle and device both apply this
+    convention when compared free-running (nullspace_phase="canonical")."""
+    v = np.array(v, np.complex128, copy=True)
+    for j in range(v.shape[1]):
+        k = int(np.argmax(np.abs(v[:, j]) ** 2))
+        e = v[k, j]
+        if abs(e) > 0:
+            v[:, j] *= np.conj(e) / abs(e)
+    return v
+
+
 def householder_nullspace(v, tol: float = 1e-12) -> np.ndarray:
     """Orthonormal complement of span(v) by r complex reflections
     (subspace.py:158-212); returns Q (n x (n-r))."""
@@ -395,14 +411,16 @@ def ser_db(reference, est) -> float:
 
 
 def hicu_reconstruct(x0, mask, kext, stages, rank, circular=(), dc_mode="hard", dc_lambda=0.0,
-                     seed=0, support=None, nullspace="rsvd", inject_v=None, trace=None, v_log=None):
+                     seed=0, support=None, nullspace="rsvd", inject_v=None, trace=None, v_log=None,
+                     canonical=False):
     """Algorithm 1 driver restated from solver.py:258-398.
 
     ``stages`` is a list of ``(region, p, gradient_steps, iterations)``.
     ``nullspace="rsvd"`` follows the reference (subspace.py:67); "nystrom"
     follows the B200 route (Gram + Nystrom) in fp64.  ``inject_v(si, it)``
     may return a V to use instead (lockstep parity); ``v_log`` (a dict) receives
-    the V used at each (stage, iteration).  ``trace`` (a list) gets one dict
+    the V used at each (stage, iteration); ``canonical=True`` applies
+    :func:`canonicalize_phases` to V (the device convention).  ``trace`` (a list) gets one dict
     per step with eta/objective values.  Returns (xhat, trace)."""
     x0 = np.ascontiguousarray(x0, dtype=np.complex128)
     mask = np.asarray(mask)
@@ -429,6 +447,8 @@ def hicu_reconstruct(x0, mask, kext, stages, rank, circular=(), dc_mode="hard", 
                 ell = math.ceil(1.5 * rank)
                 omega = complex_normal(rng_generator(seed, (1, si, it)), (n, ell), 1.0)
                 v = nystrom_right_vectors(gram(x, gm), omega, rank)
+            if canonical and inject_v is None:
+                v = canonicalize_phases(v)
             if v_log is not None:
                 v_log[(si, it)] = v
             q = householder_nullspace(v)

@@ -3,6 +3,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 #include "common.cuh"
 
 size_t hicu_gram_simt_workspace(const DevGeom& g);
@@ -33,6 +37,24 @@ int hicu_sm_count() {
     cached[dev] = v;
   }
   return cached[dev];
+}
+
+void hicu_allow_max_smem(const void* func) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({func, dev})) return;
+  int optin = 0;
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (optin <= 0) optin = 227 * 1024;
+  cudaFuncAttributes attr;
+  size_t static_smem = 0;
+  if (cudaFuncGetAttributes(&attr, func) == cudaSuccess) static_smem = attr.sharedSizeBytes;
+  cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)static_smem);
+  (void)cudaGetLastError();  // never leave a sticky error for the caller's launch check
+  done.insert({func, dev});
 }
 
 int hicu_make_devgeom(const hicu_geom* g, DevGeom* out) {

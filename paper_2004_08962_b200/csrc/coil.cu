@@ -19,7 +19,7 @@ int cov_blocks(int64_t nloc) {
 }
 
 // block b accumulates a contiguous slice of locations into parts[b][nc][nc]
-__global__ void coil_cov_kernel(int64_t nloc, int nc, const float2* __restrict__ x, const uint8_t* __restrict__ mask,
+__global__ void __launch_bounds__(1024) coil_cov_kernel(int64_t nloc, int nc, const float2* __restrict__ x, const uint8_t* __restrict__ mask,
                                 int64_t per_block, double2* __restrict__ parts) {
   __shared__ float2 xs[kLocPerBlock][33];
   __shared__ uint8_t ms[kLocPerBlock];
@@ -50,7 +50,7 @@ __global__ void coil_cov_kernel(int64_t nloc, int nc, const float2* __restrict__
   if (active) parts[(size_t)blockIdx.x * nc * nc + threadIdx.x] = acc;
 }
 
-__global__ void coil_cov_reduce(int nc, int nparts, const double2* __restrict__ parts, double2* __restrict__ cov) {
+__global__ void __launch_bounds__(1024) coil_cov_reduce(int nc, int nparts, const double2* __restrict__ parts, double2* __restrict__ cov) {
   const int e = threadIdx.x;
   if (e >= nc * nc) return;
   double2 s = cd(0.0, 0.0);

@@ -144,3 +144,5 @@ int hicu_set_error(int code, const char* msg);
 int hicu_check_cuda(cudaError_t e, const char* where);
 int hicu_make_devgeom(const hicu_geom* g, DevGeom* out);
 int hicu_sm_count();
+// raise a kernel's dynamic shared-memory limit to the device maximum (once)
+void hicu_allow_max_smem(const void* func);

@@ -311,6 +311,36 @@ __global__ void rot_apply_kernel(int n, int ell, int r, const double2* __restric
   }
 }
 
+// Canonical phase of each column of V (n x r): rotate so the largest-|.|
+// entry (first on ties) is real positive.  The reference's V carries LAPACK
+// zgesdd's phases, which are an implementation detail; fixing a documented
+// convention makes the Householder basis (subspace.py:158-212), and with it
+// the free-running trajectory, reproducible by the oracle.
+__global__ void canon_phase_kernel(int n, int r, double2* __restrict__ V) {
+  const int warps = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int t = blockIdx.x * warps + warp; t < r; t += gridDim.x * warps) {
+    double best = -1.0;
+    int bk = 0;
+    for (int k = lane; k < n; k += 32) {
+      const double a = abs2d(V[(size_t)k * r + t]);
+      if (a > best) { best = a; bk = k; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (ob > best || (ob == best && ok < bk)) { best = ob; bk = ok; }
+    }
+    const double2 e = V[(size_t)bk * r + t];
+    const double mag = sqrt(abs2d(e));
+    if (!(mag > 0.0)) continue;
+    const double2 ph = cd(e.x / mag, -e.y / mag);  // conj(e)/|e|
+    __syncwarp();
+    for (int k = lane; k < n; k += 32) V[(size_t)k * r + t] = cmul(V[(size_t)k * r + t], ph);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Householder triangularisation of V (subspace.py:158-201).  refl is r x n
 // (row j = w_j, zero before entry j), tau r, flags r.
@@ -499,7 +529,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const size_t bytes = (size_t)ell * ell * sizeof(double2);
     const bool sm = bytes <= kSmemCap;
-    if (sm) cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    hicu_allow_max_smem((const void*)chol_kernel);
     chol_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.C, w.O, Gp, n, w.scratch, sm, w.nu, status_dev);
     if ((s = hicu_check_cuda(cudaGetLastError(), "chol_kernel"))) return s;
   }
@@ -509,7 +539,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     const size_t rowb = (size_t)warps * ell * sizeof(double2);
     const bool sm = rbytes + rowb <= kSmemCap;
     const size_t smem = (sm ? rbytes : 0) + rowb;
-    cudaFuncSetAttribute(trsm_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hicu_allow_max_smem((const void*)trsm_rows_kernel);
     const int blocks = (n + warps - 1) / warps;
     trsm_rows_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, w.Y, Om, w.nu, w.C, sm, w.W);
     if ((s = hicu_check_cuda(cudaGetLastError(), "trsm_rows_kernel"))) return s;
@@ -518,7 +548,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const size_t bytes = (size_t)ell * ell * sizeof(double2);
     const bool sm = bytes <= kSmemCap;
-    if (sm) cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    hicu_allow_max_smem((const void*)jacobi_kernel);
     jacobi_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.M, w.scratch, sm, kMaxSweeps, 1e-15, w.log, w.nrounds,
                                                    w.evals, w.order, status_dev);
     if ((s = hicu_check_cuda(cudaGetLastError(), "jacobi_kernel"))) return s;
@@ -526,12 +556,14 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const int warps = 8;
     const size_t smem = (size_t)warps * ell * sizeof(double2);
-    cudaFuncSetAttribute(rot_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hicu_allow_max_smem((const void*)rot_apply_kernel);
     const int blocks = (n + warps - 1) / warps;
     rot_apply_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, r, w.W, w.log, w.nrounds, w.evals, w.order,
                                                        (double2*)V, status_dev, true);
     if ((s = hicu_check_cuda(cudaGetLastError(), "rot_apply_kernel"))) return s;
   }
+  canon_phase_kernel<<<(r + 7) / 8, 256, 0, st>>>(n, r, (double2*)V);
+  if ((s = hicu_check_cuda(cudaGetLastError(), "canon_phase_kernel"))) return s;
   return HICU_OK;
 }
 
@@ -549,7 +581,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     // require the caller to size refl at 2*n*r and use its upper half as scratch.
     gws = (double2*)refl + (size_t)n * r;
   }
-  if (sm) cudaFuncSetAttribute(householder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  hicu_allow_max_smem((const void*)householder_kernel);
   householder_kernel<<<1, 1024, sm ? bytes : 0, (cudaStream_t)stream>>>(
       n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
   return hicu_check_cuda(cudaGetLastError(), "householder_kernel");
@@ -563,7 +595,7 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
   while (warps > 1 && (size_t)warps * n * sizeof(double2) > kSmemCap) warps >>= 1;
   const size_t smem = (size_t)warps * n * sizeof(double2);
   if (smem > kSmemCap) return hicu_set_error(HICU_ERR_SIZE, "apply_reflectors: n too large");
-  cudaFuncSetAttribute(apply_reflectors_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  hicu_allow_max_smem((const void*)apply_reflectors_kernel);
   const int blocks = (cols + warps - 1) / warps;
   apply_reflectors_kernel<<<blocks, warps * 32, smem, (cudaStream_t)stream>>>(
       n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B, (float2*)out32,
@@ -625,7 +657,7 @@ extern "C" int hicu_coil_basis(int nc, int nv, const void* cov, void* basis, dou
   eye_kernel<<<1, 256, 0, st>>>(nc, I);
   if ((s = hicu_check_cuda(cudaGetLastError(), "eye_kernel"))) return s;
   const size_t bytes = (size_t)nc * nc * sizeof(double2);
-  cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  hicu_allow_max_smem((const void*)jacobi_kernel);
   jacobi_kernel<<<1, 1024, bytes, st>>>(nc, (const double2*)cov, w.scratch, true, kMaxSweeps, 1e-15, w.log,
                                         w.nrounds, w.evals, w.order, status);
   if ((s = hicu_check_cuda(cudaGetLastError(), "jacobi_kernel"))) return s;

@@ -266,7 +266,7 @@ int launch_conv(const DevGeom& g, const float2* y, const float2* qt, int p, floa
 #define HICU_LAUNCH_CONV(C, M)                                                                    \
   do {                                                                                            \
     auto kfn = conv_kernel<PMAX, C, M>;                                                           \
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    hicu_allow_max_smem((const void*)kfn);            \
     kfn<<<blocks, kConvThreads, smem, st>>>(g, y, qt, p, u, parts);                               \
   } while (0)
   if (circ) {
@@ -303,11 +303,11 @@ int launch_scatter(const DevGeom& g, const float2* qt, int p, const float2* u, c
   if (smem > 200 * 1024) return hicu_set_error(HICU_ERR_SIZE, "scatter: n*p too large for shared memory");
   if (g.ncirc > 0) {
     auto kfn = scatter_kernel<PMAX, true>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hicu_allow_max_smem((const void*)kfn);
     kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   } else {
     auto kfn = scatter_kernel<PMAX, false>;
-    cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    hicu_allow_max_smem((const void*)kfn);
     kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   }
   return hicu_check_cuda(cudaGetLastError(), "scatter_kernel");

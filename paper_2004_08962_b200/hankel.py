@@ -355,7 +355,8 @@ def hankel_adjoint_apply(x, u, kernel: KernelMask, region: Region, pos_chunk: in
     dg = device_geometry(kernel, region, dims)
     out = torch.empty((kernel.n, k), dtype=torch.complex128, device="cuda")
     L = nat.lib()
-    nat.check(L.hicu_conv_adj(dg.ref(), to_dev(x).data_ptr(), to_dev(umat).data_ptr(), k, out.data_ptr(),
+    xd, ud = to_dev(x), to_dev(umat)  # keep the device copies alive across the launch
+    nat.check(L.hicu_conv_adj(dg.ref(), xd.data_ptr(), ud.data_ptr(), k, out.data_ptr(),
                               nat.stream_handle()), "hankel_adjoint_apply")
     res = out.cpu().numpy()
     return res[:, 0] if squeeze else res
@@ -473,7 +474,8 @@ def exact_line_search(y, g, qt, kernel: KernelMask, region: Region, dc: DataCons
     st = nat.stream_handle()
     gd = to_dev(g)
     parts = torch.empty(2 * max(dg.conv_nparts, 1), dtype=torch.float64, device="cuda")
-    nat.check(L.hicu_conv_els(dg.ref(), gd.data_ptr(), to_dev(qmat).data_ptr(), k, ud.data_ptr(), parts.data_ptr(),
+    qd = to_dev(qmat)
+    nat.check(L.hicu_conv_els(dg.ref(), gd.data_ptr(), qd.data_ptr(), k, ud.data_ptr(), parts.data_ptr(),
                               st), "exact_line_search")
     num = _sum_parts(parts, 2, 0)
     den = _sum_parts(parts, 2, 1)
@@ -482,8 +484,9 @@ def exact_line_search(y, g, qt, kernel: KernelMask, region: Region, dc: DataCons
 
         sp = torch.empty(3 * nat.lib().hicu_ser_nparts(dg.N), dtype=torch.float64, device="cuda")
         npt = ctypes.c_int(0)
-        nat.check(L.hicu_soft_terms(dg.N, gd.data_ptr(), yd.data_ptr(), to_dev(dc.x0).data_ptr(),
-                                    to_dev(dc.mask, np.uint8).data_ptr(), sp.data_ptr(), ctypes.byref(npt), st),
+        x0d, md = to_dev(dc.x0), to_dev(dc.mask, np.uint8)
+        nat.check(L.hicu_soft_terms(dg.N, gd.data_ptr(), yd.data_ptr(), x0d.data_ptr(),
+                                    md.data_ptr(), sp.data_ptr(), ctypes.byref(npt), st),
                   "exact_line_search")
         num += dc.lam * _sum_parts(sp, 3, 0)
         den += dc.lam * _sum_parts(sp, 3, 1)

@@ -80,7 +80,8 @@ def gram_matrix(x, kernel: KernelMask, region: Region):
     ws_bytes = L.hicu_gram_workspace(dg.ref())
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device="cuda")
     G = torch.empty((kernel.n, kernel.n), dtype=torch.complex128, device="cuda")
-    nat.check(L.hicu_gram(dg.ref(), to_dev(x).data_ptr(), G.data_ptr(), ws.data_ptr(), ws_bytes, nat.stream_handle()),
+    xd = to_dev(x)  # keep alive across the launch
+    nat.check(L.hicu_gram(dg.ref(), xd.data_ptr(), G.data_ptr(), ws.data_ptr(), ws_bytes, nat.stream_handle()),
               "gram")
     return G
 
@@ -114,7 +115,8 @@ def rsvd_right_vectors(x, kernel: KernelMask, region: Region, r: int, rng: RngSt
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     V = torch.empty((n, r), dtype=torch.complex128, device="cuda")
     st_t = torch.zeros(1, dtype=torch.int32, device="cuda")
-    nat.check(L.hicu_nystrom(n, ell, r, G.data_ptr(), to_dev(omega, np.complex128).data_ptr(), V.data_ptr(),
+    omd = to_dev(omega, np.complex128)
+    nat.check(L.hicu_nystrom(n, ell, r, G.data_ptr(), omd.data_ptr(), V.data_ptr(),
                              ws.data_ptr(), ws_bytes, st_t.data_ptr(), nat.stream_handle()), "rsvd_right_vectors")
     _status(torch, st_t, "rsvd_right_vectors")
     if meter is not None:
@@ -174,7 +176,8 @@ def jl_compress(q, p: int, rng: RngStream) -> np.ndarray:
     proj = complex_normal(rng.generator(), (q.shape[1], p), 1.0 / p)
     n, m = q.shape
     out = torch.empty((n, p), dtype=torch.complex128, device="cuda")
-    nat.check(nat.lib().hicu_zgemm(b"N", b"N", n, p, m, to_dev(q, np.complex128).data_ptr(), m,
-                                   to_dev(proj, np.complex128).data_ptr(), p, out.data_ptr(), p,
+    qd, pd = to_dev(q, np.complex128), to_dev(proj, np.complex128)
+    nat.check(nat.lib().hicu_zgemm(b"N", b"N", n, p, m, qd.data_ptr(), m,
+                                   pd.data_ptr(), p, out.data_ptr(), p,
                                    nat.stream_handle()), "jl_compress")
     return out.cpu().numpy()

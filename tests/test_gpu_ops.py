@@ -176,7 +176,8 @@ def _nystrom_device(G, omega, r):
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     V = torch.empty((n, r), dtype=torch.complex128, device="cuda")
     st = torch.zeros(1, dtype=torch.int32, device="cuda")
-    nat.check(L.hicu_nystrom(n, ell, r, to_dev(G, np.complex128).data_ptr(), to_dev(omega, np.complex128).data_ptr(),
+    Gd, omd = to_dev(G, np.complex128), to_dev(omega, np.complex128)
+    nat.check(L.hicu_nystrom(n, ell, r, Gd.data_ptr(), omd.data_ptr(),
                              V.data_ptr(), ws.data_ptr(), ws_bytes, st.data_ptr(), nat.stream_handle()))
     assert int(st.item()) == 0
     return V.cpu().numpy()

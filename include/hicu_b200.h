@@ -211,7 +211,22 @@ typedef struct hicu_stage_args {
   const void* ref;         /* optional c64 N fully sampled reference          */
   double* ser_parts;       /* iters*gsteps*ser_stride doubles when ref        */
   int32_t ser_stride;
+  void* prof;              /* optional hicu_prof handle (NULL: no events)     */
 } hicu_stage_args;
+
+/* ---- native profiler: CUDA events around each launch group --------------- */
+enum {
+  HICU_PROF_GRAM = 0, HICU_PROF_NYSTROM = 1, HICU_PROF_HOUSEHOLDER = 2,
+  HICU_PROF_CONV_FWD = 3, HICU_PROF_SCATTER = 4, HICU_PROF_CONV_ELS = 5,
+  HICU_PROF_UPDATE = 6, HICU_PROF_KINDS = 7
+};
+int hicu_prof_create(int capacity, void** out);
+int hicu_prof_destroy(void* h);
+int hicu_prof_reset(void* h);
+/* per-kind total milliseconds and launch-group counts (synchronises) */
+int hicu_prof_summary(void* h, double* ms, int* count);
+/* number of kernels this library has launched in the process */
+long long hicu_launch_count(void);
 
 int hicu_ser_nparts(int64_t N);
 int hicu_run_stage(const hicu_stage_args* a, void* stream);

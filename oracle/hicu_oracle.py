@@ -142,6 +142,30 @@ def stage_geom(dims, kext, fraction, circular=(), support=None) -> Geom:
     return Geom(dims, support_positions(kext, support), tuple(offs), tuple(exts), circ)
 
 
+def _row_cache(geom: Geom):
+    """Per-geometry cache: flat base offset of every region row over the
+    non-circular axes, the region coordinates on circular axes, strides."""
+    c = getattr(geom, "_cache", None)
+    if c is None:
+        dims = geom.dims
+        nd = len(dims)
+        strides = np.ones(nd, np.int64)
+        for d in range(nd - 2, -1, -1):
+            strides[d] = strides[d + 1] * dims[d + 1]
+        grids = np.meshgrid(*[np.arange(e, dtype=np.int64) for e in geom.extents], indexing="ij")
+        base = np.zeros(geom.s, np.int64)
+        circ = {}
+        for d in range(nd):
+            a = grids[d].reshape(-1) + geom.offsets[d]
+            if d in geom.circular:
+                circ[d] = a
+            else:
+                base += a * strides[d]
+        c = (base, circ, strides)
+        geom._cache = c
+    return c
+
+
 def flat_index(geom: Geom, rows_of_positions: np.ndarray) -> np.ndarray:
     """Flat k-space index of H[i, kappa] for every region row i (row-major)
     and each given support position: ``(s, c)`` int64.
@@ -149,19 +173,15 @@ def flat_index(geom: Geom, rows_of_positions: np.ndarray) -> np.ndarray:
     Restates the window decomposition of hankel.py:210-252 (``_axis_pieces``,
     ``_window_pieces``, ``_gather_slab``) as modular index arithmetic.
     """
-    dims = geom.dims
-    nd = len(dims)
-    strides = np.ones(nd, np.int64)
-    for d in range(nd - 2, -1, -1):
-        strides[d] = strides[d + 1] * dims[d + 1]
-    grids = np.meshgrid(*[np.arange(e, dtype=np.int64) for e in geom.extents], indexing="ij")
+    base, circ, strides = _row_cache(geom)
     pos = np.asarray(rows_of_positions, np.int64)
-    idx = np.zeros((geom.s, pos.shape[0]), np.int64)
-    for d in range(nd):
-        a = grids[d].reshape(-1, 1) + geom.offsets[d] + pos[None, :, d]
-        if d in geom.circular:
-            a = a % dims[d]
-        idx += a * strides[d]
+    koff = np.zeros(pos.shape[0], np.int64)
+    for d in range(len(geom.dims)):
+        if d not in circ:
+            koff += pos[:, d] * strides[d]
+    idx = base[:, None] + koff[None, :]
+    for d, a in circ.items():
+        idx += ((a[:, None] + pos[None, :, d]) % geom.dims[d]) * strides[d]
     return idx
 
 

@@ -18,6 +18,7 @@ MAX_NDIM = 8
 
 REC_OBJ, REC_NUM, REC_DEN, REC_ETA, REC_OBJ_AFTER, REC_GNORM2, REC_DEGENERATE, REC_TIME = range(8)
 REC_SLOTS = 8
+PROF_KINDS = ("gram", "nystrom", "householder", "conv_fwd", "scatter", "conv_els", "update")
 
 
 class HicuGeom(ctypes.Structure):
@@ -50,6 +51,7 @@ class HicuStageArgs(ctypes.Structure):
         ("obj_parts", c_void_p), ("dc_parts", c_void_p), ("els_parts", c_void_p),
         ("rec", c_void_p),
         ("ref", c_void_p), ("ser_parts", c_void_p), ("ser_stride", c_int32),
+        ("prof", c_void_p),
     ]
 
 
@@ -85,6 +87,11 @@ _SIGS = {
                                       c_void_p, c_int, c_void_p]),
     "hicu_run_stage": (c_int, [POINTER(HicuStageArgs), c_void_p]),
     "hicu_timestamp": (c_int, [c_void_p, c_void_p]),
+    "hicu_prof_create": (c_int, [c_int, POINTER(c_void_p)]),
+    "hicu_prof_destroy": (c_int, [c_void_p]),
+    "hicu_prof_reset": (c_int, [c_void_p]),
+    "hicu_prof_summary": (c_int, [c_void_p, POINTER(c_double), POINTER(c_int)]),
+    "hicu_launch_count": (ctypes.c_longlong, []),
     "hicu_coil_workspace": (c_size_t, [c_int64, c_int]),
     "hicu_coil_cov": (c_int, [c_int64, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hicu_coil_basis_workspace": (c_size_t, [c_int]),
@@ -148,3 +155,27 @@ def stream_handle(stream=None) -> int:
 
     s = stream if stream is not None else torch.cuda.current_stream()
     return int(s.cuda_stream)
+
+
+class Profiler:
+    """Native CUDA-event profiler (hicu_prof_*): per kernel class totals."""
+
+    def __init__(self, capacity: int = 1 << 16):
+        self.h = c_void_p()
+        check(lib().hicu_prof_create(capacity, ctypes.byref(self.h)), "prof_create")
+
+    def reset(self):
+        lib().hicu_prof_reset(self.h)
+
+    def summary(self) -> dict:
+        ms = (c_double * len(PROF_KINDS))()
+        cnt = (c_int * len(PROF_KINDS))()
+        check(lib().hicu_prof_summary(self.h, ms, cnt), "prof_summary")
+        return {k: {"ms": ms[i], "launches": cnt[i]} for i, k in enumerate(PROF_KINDS)}
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().hicu_prof_destroy(self.h)
+        except Exception:
+            pass

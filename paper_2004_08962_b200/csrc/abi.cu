@@ -12,9 +12,19 @@
 size_t hicu_gram_simt_workspace(const DevGeom& g);
 int hicu_gram_simt(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st);
 
+#include <atomic>
+
 namespace {
 thread_local char g_last_error[512] = "";
+std::atomic<long long> g_launches{0};
 }
+
+int hicu_check_launch(const char* where) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return hicu_check_cuda(cudaGetLastError(), where);
+}
+
+extern "C" long long hicu_launch_count(void) { return g_launches.load(); }
 
 int hicu_set_error(int code, const char* msg) {
   snprintf(g_last_error, sizeof(g_last_error), "%s", msg ? msg : "");

@@ -94,10 +94,10 @@ extern "C" int hicu_coil_cov(int64_t nloc, int nc, const void* x, const uint8_t*
   const int64_t per = (nloc + blocks - 1) / blocks;
   cudaStream_t st = (cudaStream_t)stream;
   coil_cov_kernel<<<blocks, 1024, 0, st>>>(nloc, nc, (const float2*)x, mask, per, (double2*)ws);
-  int s = hicu_check_cuda(cudaGetLastError(), "coil_cov_kernel");
+  int s = hicu_check_launch("coil_cov_kernel");
   if (s) return s;
   coil_cov_reduce<<<1, 1024, 0, st>>>(nc, blocks, (const double2*)ws, (double2*)cov);
-  return hicu_check_cuda(cudaGetLastError(), "coil_cov_reduce");
+  return hicu_check_launch("coil_cov_reduce");
 }
 
 extern "C" int hicu_coil_apply(int64_t nloc, int nc, int nv, const void* x, const uint8_t* mask, const void* basis,
@@ -109,5 +109,5 @@ extern "C" int hicu_coil_apply(int64_t nloc, int nc, int nv, const void* x, cons
   if (blocks > cap) blocks = cap;
   coil_apply_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(nloc, nc, nv, (const float2*)x, mask,
                                                                    (const double2*)basis, (float2*)y, mask_out);
-  return hicu_check_cuda(cudaGetLastError(), "coil_apply_kernel");
+  return hicu_check_launch("coil_apply_kernel");
 }

@@ -142,6 +142,8 @@ __device__ __forceinline__ double warp_sum_parts(const double* parts, int np, in
 
 int hicu_set_error(int code, const char* msg);
 int hicu_check_cuda(cudaError_t e, const char* where);
+// count one kernel launch and check it
+int hicu_check_launch(const char* where);
 int hicu_make_devgeom(const hicu_geom* g, DevGeom* out);
 int hicu_sm_count();
 // raise a kernel's dynamic shared-memory limit to the device maximum (once)

@@ -51,7 +51,7 @@ int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int 
                  double2* C, int ldc, cudaStream_t st) {
   dim3 grid((n + 15) / 16, (m + 15) / 16);
   zgemm_kernel<<<grid, 256, 0, st>>>(opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
-  return hicu_check_cuda(cudaGetLastError(), "zgemm_kernel");
+  return hicu_check_launch("zgemm_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -531,7 +531,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     const bool sm = bytes <= kSmemCap;
     hicu_allow_max_smem((const void*)chol_kernel);
     chol_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.C, w.O, Gp, n, w.scratch, sm, w.nu, status_dev);
-    if ((s = hicu_check_cuda(cudaGetLastError(), "chol_kernel"))) return s;
+    if ((s = hicu_check_launch("chol_kernel"))) return s;
   }
   {
     const size_t rbytes = (size_t)ell * ell * sizeof(double2);
@@ -542,7 +542,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     hicu_allow_max_smem((const void*)trsm_rows_kernel);
     const int blocks = (n + warps - 1) / warps;
     trsm_rows_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, w.Y, Om, w.nu, w.C, sm, w.W);
-    if ((s = hicu_check_cuda(cudaGetLastError(), "trsm_rows_kernel"))) return s;
+    if ((s = hicu_check_launch("trsm_rows_kernel"))) return s;
   }
   if ((s = zgemm_launch('C', 'N', ell, ell, n, w.W, ell, w.W, ell, w.M, ell, st))) return s;
   {
@@ -551,7 +551,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     hicu_allow_max_smem((const void*)jacobi_kernel);
     jacobi_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.M, w.scratch, sm, kMaxSweeps, 1e-15, w.log, w.nrounds,
                                                    w.evals, w.order, status_dev);
-    if ((s = hicu_check_cuda(cudaGetLastError(), "jacobi_kernel"))) return s;
+    if ((s = hicu_check_launch("jacobi_kernel"))) return s;
   }
   {
     const int warps = 8;
@@ -560,10 +560,10 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     const int blocks = (n + warps - 1) / warps;
     rot_apply_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, r, w.W, w.log, w.nrounds, w.evals, w.order,
                                                        (double2*)V, status_dev, true);
-    if ((s = hicu_check_cuda(cudaGetLastError(), "rot_apply_kernel"))) return s;
+    if ((s = hicu_check_launch("rot_apply_kernel"))) return s;
   }
   canon_phase_kernel<<<(r + 7) / 8, 256, 0, st>>>(n, r, (double2*)V);
-  if ((s = hicu_check_cuda(cudaGetLastError(), "canon_phase_kernel"))) return s;
+  if ((s = hicu_check_launch("canon_phase_kernel"))) return s;
   return HICU_OK;
 }
 
@@ -584,7 +584,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
   hicu_allow_max_smem((const void*)householder_kernel);
   householder_kernel<<<1, 1024, sm ? bytes : 0, (cudaStream_t)stream>>>(
       n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
-  return hicu_check_cuda(cudaGetLastError(), "householder_kernel");
+  return hicu_check_launch("householder_kernel");
 }
 
 extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
@@ -600,7 +600,7 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
   apply_reflectors_kernel<<<blocks, warps * 32, smem, (cudaStream_t)stream>>>(
       n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B, (float2*)out32,
       p ? p : 1);
-  return hicu_check_cuda(cudaGetLastError(), "apply_reflectors_kernel");
+  return hicu_check_launch("apply_reflectors_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -655,17 +655,17 @@ extern "C" int hicu_coil_basis(int nc, int nv, const void* cov, void* basis, dou
   cudaStream_t st = (cudaStream_t)stream;
   int s;
   eye_kernel<<<1, 256, 0, st>>>(nc, I);
-  if ((s = hicu_check_cuda(cudaGetLastError(), "eye_kernel"))) return s;
+  if ((s = hicu_check_launch("eye_kernel"))) return s;
   const size_t bytes = (size_t)nc * nc * sizeof(double2);
   hicu_allow_max_smem((const void*)jacobi_kernel);
   jacobi_kernel<<<1, 1024, bytes, st>>>(nc, (const double2*)cov, w.scratch, true, kMaxSweeps, 1e-15, w.log,
                                         w.nrounds, w.evals, w.order, status);
-  if ((s = hicu_check_cuda(cudaGetLastError(), "jacobi_kernel"))) return s;
+  if ((s = hicu_check_launch("jacobi_kernel"))) return s;
   // E = I J with columns in descending-eigenvalue order (no scaling)
   rot_apply_kernel<<<1, 32 * 8, (size_t)8 * nc * sizeof(double2), st>>>(nc, nc, nc, I, w.log, w.nrounds, w.evals,
                                                                        w.order, E, nullptr, false);
-  if ((s = hicu_check_cuda(cudaGetLastError(), "rot_apply_kernel"))) return s;
+  if ((s = hicu_check_launch("rot_apply_kernel"))) return s;
   // E columns are already in descending order; identity order for the phase step
   coil_phase_kernel<<<1, 32, 0, st>>>(nc, nv, E, w.evals, w.order, (double2*)basis, evals);
-  return hicu_check_cuda(cudaGetLastError(), "coil_phase_kernel");
+  return hicu_check_launch("coil_phase_kernel");
 }

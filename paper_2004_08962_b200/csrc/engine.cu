@@ -2,7 +2,81 @@
 // (solver.py:322-393) as a sequence of asynchronous launches on one stream.
 // One ABI call per stage; no host synchronisation inside, so a whole stage
 // can be captured into a CUDA graph and replayed.
+#include <vector>
+
 #include "common.cuh"
+
+// ---------------------------------------------------------------------------
+// Native per-kernel-class profiler: a pool of CUDA events recorded around each
+// launch group on the launching stream (created once, outside timed regions).
+// ---------------------------------------------------------------------------
+struct HicuProf {
+  std::vector<cudaEvent_t> ev;  // 2 per record
+  std::vector<int> kind;
+  int used = 0;
+};
+
+extern "C" int hicu_prof_create(int capacity, void** out) {
+  if (!out || capacity < 1) return hicu_set_error(HICU_ERR_PARAMETER, "prof_create: bad arguments");
+  HicuProf* p = new HicuProf();
+  p->ev.resize(2 * (size_t)capacity);
+  p->kind.resize(capacity);
+  for (auto& e : p->ev) {
+    int s = hicu_check_cuda(cudaEventCreate(&e), "prof_create");
+    if (s) return s;
+  }
+  *out = p;
+  return HICU_OK;
+}
+
+extern "C" int hicu_prof_destroy(void* h) {
+  HicuProf* p = (HicuProf*)h;
+  if (!p) return HICU_OK;
+  for (auto& e : p->ev) cudaEventDestroy(e);
+  delete p;
+  return HICU_OK;
+}
+
+extern "C" int hicu_prof_reset(void* h) {
+  if (h) ((HicuProf*)h)->used = 0;
+  return HICU_OK;
+}
+
+// ms and launch-group counts per kind (arrays of HICU_PROF_KINDS); syncs.
+extern "C" int hicu_prof_summary(void* h, double* ms, int* count) {
+  HicuProf* p = (HicuProf*)h;
+  if (!p || !ms || !count) return hicu_set_error(HICU_ERR_PARAMETER, "prof_summary: bad arguments");
+  for (int k = 0; k < HICU_PROF_KINDS; ++k) { ms[k] = 0.0; count[k] = 0; }
+  if (p->used == 0) return HICU_OK;
+  int s = hicu_check_cuda(cudaEventSynchronize(p->ev[2 * (size_t)(p->used - 1) + 1]), "prof_summary");
+  if (s) return s;
+  for (int i = 0; i < p->used; ++i) {
+    float t = 0.f;
+    s = hicu_check_cuda(cudaEventElapsedTime(&t, p->ev[2 * (size_t)i], p->ev[2 * (size_t)i + 1]), "prof elapsed");
+    if (s) return s;
+    ms[p->kind[i]] += t;
+    count[p->kind[i]] += 1;
+  }
+  return HICU_OK;
+}
+
+namespace {
+struct ProfScope {
+  HicuProf* p;
+  cudaStream_t st;
+  int idx = -1;
+  ProfScope(void* h, int kind, cudaStream_t s) : p((HicuProf*)h), st(s) {
+    if (p && p->used < (int)p->kind.size()) {
+      idx = p->used++;
+      p->kind[idx] = kind;
+      cudaEventRecord(p->ev[2 * (size_t)idx], st);
+    }
+  }
+  ~ProfScope() {
+    if (idx >= 0) cudaEventRecord(p->ev[2 * (size_t)idx + 1], st);
+  }
+};
+}  // namespace
 
 extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   if (!a) return hicu_set_error(HICU_ERR_PARAMETER, "run_stage: null args");
@@ -19,34 +93,54 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   for (int it = 0; it < a->iters; ++it) {
     // ---- nullspace: Gram + Nystrom (== rSVD subspace), or injected V ----
     if (a->inject_v) {
+      ProfScope ps(a->prof, HICU_PROF_NYSTROM, st);
       s = hicu_check_cuda(cudaMemcpyAsync(a->V, (const double2*)a->inject_v + (size_t)it * n * r,
                                           (size_t)n * r * sizeof(double2), cudaMemcpyDeviceToDevice, st),
                           "inject_v copy");
       if (s) return s;
     } else {
-      if ((s = hicu_gram(gm, a->y, a->G, a->gram_ws, a->gram_ws_bytes, stream))) return s;
+      {
+        ProfScope ps(a->prof, HICU_PROF_GRAM, st);
+        if ((s = hicu_gram(gm, a->y, a->G, a->gram_ws, a->gram_ws_bytes, stream))) return s;
+      }
+      ProfScope ps(a->prof, HICU_PROF_NYSTROM, st);
       if ((s = hicu_nystrom(n, ell, r, a->G, (const double2*)a->omega + (size_t)it * nomega, a->V, a->nys_ws,
                             a->nys_ws_bytes, a->status, stream)))
         return s;
     }
     // ---- Householder complement and Q~_j = Q P_j for all steps ----
-    if ((s = hicu_householder(n, r, a->V, a->householder_tol, a->refl, a->tau, a->flags, a->status, stream)))
-      return s;
-    if ((s = hicu_apply_reflectors(n, r, a->refl, a->tau, a->flags, G * p,
-                                   (const double2*)a->pbig + (size_t)it * npbig, a->B, a->qt32, p, stream)))
-      return s;
+    {
+      ProfScope ps(a->prof, HICU_PROF_HOUSEHOLDER, st);
+      if ((s = hicu_householder(n, r, a->V, a->householder_tol, a->refl, a->tau, a->flags, a->status, stream)))
+        return s;
+      if ((s = hicu_apply_reflectors(n, r, a->refl, a->tau, a->flags, G * p,
+                                     (const double2*)a->pbig + (size_t)it * npbig, a->B, a->qt32, p, stream)))
+        return s;
+    }
     // ---- gradient steps ----
     for (int j = 0; j < G; ++j) {
       const float2* qt = (const float2*)a->qt32 + (size_t)j * n * p;
       double* rec = a->rec + ((size_t)it * G + j) * HICU_REC_SLOTS;
-      if ((s = hicu_conv_fwd(gm, a->y, qt, p, a->u, a->obj_parts, stream))) return s;
-      if ((s = hicu_scatter_dc(gm, qt, p, a->u, a->mask, a->y, a->x0, a->dc_mode, a->lam, a->g, a->dc_parts,
-                               stream)))
-        return s;
-      if ((s = hicu_conv_els(gm, a->g, qt, p, a->u, a->els_parts, stream))) return s;
-      if ((s = hicu_step_update(a->N, a->y, a->g, a->obj_parts, ncp, a->dc_parts, nsp, a->els_parts, ncp,
-                                a->dc_mode, a->lam, rec, stream)))
-        return s;
+      {
+        ProfScope ps(a->prof, HICU_PROF_CONV_FWD, st);
+        if ((s = hicu_conv_fwd(gm, a->y, qt, p, a->u, a->obj_parts, stream))) return s;
+      }
+      {
+        ProfScope ps(a->prof, HICU_PROF_SCATTER, st);
+        if ((s = hicu_scatter_dc(gm, qt, p, a->u, a->mask, a->y, a->x0, a->dc_mode, a->lam, a->g, a->dc_parts,
+                                 stream)))
+          return s;
+      }
+      {
+        ProfScope ps(a->prof, HICU_PROF_CONV_ELS, st);
+        if ((s = hicu_conv_els(gm, a->g, qt, p, a->u, a->els_parts, stream))) return s;
+      }
+      {
+        ProfScope ps(a->prof, HICU_PROF_UPDATE, st);
+        if ((s = hicu_step_update(a->N, a->y, a->g, a->obj_parts, ncp, a->dc_parts, nsp, a->els_parts, ncp,
+                                  a->dc_mode, a->lam, rec, stream)))
+          return s;
+      }
       if (a->ref && a->ser_parts) {
         double* sp = a->ser_parts + ((size_t)it * G + j) * a->ser_stride;
         if ((s = hicu_ser_parts(a->N, a->ref, a->y, sp, nullptr, stream))) return s;

@@ -149,11 +149,11 @@ int hicu_gram_simt(const DevGeom& g, const float2* x, double2* G, void* ws, size
     gram_simt_kernel<true><<<grid, kThreads, 0, st>>>(g, x, p.ntile, p.rows_per_split, (double2*)ws);
   else
     gram_simt_kernel<false><<<grid, kThreads, 0, st>>>(g, x, p.ntile, p.rows_per_split, (double2*)ws);
-  int s = hicu_check_cuda(cudaGetLastError(), "gram_simt_kernel");
+  int s = hicu_check_launch("gram_simt_kernel");
   if (s) return s;
   int64_t total = (int64_t)g.n * g.n;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 1184) blocks = 1184;
   gram_reduce_kernel<<<blocks, 256, 0, st>>>(g.n, p.splits, (const double2*)ws, G);
-  return hicu_check_cuda(cudaGetLastError(), "gram_reduce_kernel");
+  return hicu_check_launch("gram_reduce_kernel");
 }

@@ -275,7 +275,7 @@ int launch_conv(const DevGeom& g, const float2* y, const float2* qt, int p, floa
     if (mode == 0) HICU_LAUNCH_CONV(false, 0); else HICU_LAUNCH_CONV(false, 1);
   }
 #undef HICU_LAUNCH_CONV
-  return hicu_check_cuda(cudaGetLastError(), "conv_kernel");
+  return hicu_check_launch("conv_kernel");
 }
 
 int conv_dispatch(const hicu_geom* hg, const void* y, const void* qt, int p, const void* u_in, void* u_out,
@@ -310,7 +310,7 @@ int launch_scatter(const DevGeom& g, const float2* qt, int p, const float2* u, c
     hicu_allow_max_smem((const void*)kfn);
     kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   }
-  return hicu_check_cuda(cudaGetLastError(), "scatter_kernel");
+  return hicu_check_launch("scatter_kernel");
 }
 
 }  // namespace
@@ -371,7 +371,7 @@ extern "C" int hicu_step_update(int64_t N, void* y, const void* gdir, const doub
   if (b > cap) b = cap;
   update_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(N, (float2*)y, (const float2*)gdir, obj_parts, n_obj,
                                                            dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec);
-  return hicu_check_cuda(cudaGetLastError(), "update_kernel");
+  return hicu_check_launch("update_kernel");
 }
 
 __global__ void timestamp_kernel(double* out) {
@@ -391,7 +391,7 @@ int ser_blocks(int64_t N) {
 extern "C" int hicu_timestamp(double* out, void* stream) {
   if (!out) return hicu_set_error(HICU_ERR_PARAMETER, "timestamp: null");
   timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(out);
-  return hicu_check_cuda(cudaGetLastError(), "timestamp_kernel");
+  return hicu_check_launch("timestamp_kernel");
 }
 
 extern "C" int hicu_ser_nparts(int64_t N) { return ser_blocks(N); }
@@ -402,7 +402,7 @@ extern "C" int hicu_ser_parts(int64_t N, const void* ref, const void* y, double*
   const int b = ser_blocks(N);
   if (nparts_out) *nparts_out = b;
   ser_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(N, (const float2*)ref, (const float2*)y, parts);
-  return hicu_check_cuda(cudaGetLastError(), "ser_kernel");
+  return hicu_check_launch("ser_kernel");
 }
 
 // ---------------------------------------------------------------------------
@@ -446,7 +446,7 @@ extern "C" int hicu_conv_adj(const hicu_geom* hg, const void* x, const void* u, 
   else
     conv_adj_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(g, (const float2*)x, (const float2*)u, k,
                                                                    (double2*)out);
-  return hicu_check_cuda(cudaGetLastError(), "conv_adj_kernel");
+  return hicu_check_launch("conv_adj_kernel");
 }
 
 // Soft-DC line-search terms for the operator-level API (hankel.py:546-550):
@@ -476,5 +476,5 @@ extern "C" int hicu_soft_terms(int64_t N, const void* g, const void* y, const vo
   if (nparts_out) *nparts_out = b;
   soft_terms_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(N, (const float2*)g, (const float2*)y, (const float2*)x0,
                                                          mask, parts);
-  return hicu_check_cuda(cudaGetLastError(), "soft_terms_kernel");
+  return hicu_check_launch("soft_terms_kernel");
 }

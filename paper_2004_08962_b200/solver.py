@@ -239,21 +239,28 @@ def _ser_from_parts(parts: np.ndarray) -> float:
     return 20.0 * math.log10(math.sqrt(r) / math.sqrt(e))
 
 
-def draw_stage(schedule: SolverSchedule, si: int, stage: StageSpec, n: int):
-    """Host draws for one stage with the reference streams: omega
-    (iters, n, l) and pbig (iters, n, G*p) with P_j in rows r.. of column
-    block j (solver.py:325-333, subspace.py:112-116, 228)."""
+def _fill_draws(schedule: SolverSchedule, si: int, stage: StageSpec, n: int, it: int, omega_out, pbig_out):
+    """Host draws of one outer iteration with the reference streams
+    (solver.py:325-333, subspace.py:112-116, 228): omega (n, l) and pbig
+    (n, G*p) with P_j in rows r.. of column block j (rows < r stay zero)."""
     r = schedule.rank
     ell = math.ceil(1.5 * r)
     root = RngStream(schedule.seed)
     G, p = stage.gradient_steps, stage.p
+    omega_out[...] = complex_normal(root.child(_RSVD_STREAM, si, it).generator(), (n, ell), 1.0)
+    pbig_out[:r, :] = 0
+    for j in range(G):
+        pbig_out[r:, j * p:(j + 1) * p] = complex_normal(root.child(_JL_STREAM, si, it, j).generator(),
+                                                         (n - r, p), 1.0 / p)
+
+
+def draw_stage(schedule: SolverSchedule, si: int, stage: StageSpec, n: int):
+    """All host draws of one stage: omega (iters, n, l), pbig (iters, n, G*p)."""
+    ell = math.ceil(1.5 * schedule.rank)
     omega = np.empty((stage.iterations, n, ell), np.complex128)
-    pbig = np.zeros((stage.iterations, n, G * p), np.complex128)
+    pbig = np.zeros((stage.iterations, n, stage.gradient_steps * stage.p), np.complex128)
     for it in range(stage.iterations):
-        omega[it] = complex_normal(root.child(_RSVD_STREAM, si, it).generator(), (n, ell), 1.0)
-        for j in range(G):
-            pbig[it, r:, j * p:(j + 1) * p] = complex_normal(
-                root.child(_JL_STREAM, si, it, j).generator(), (n - r, p), 1.0 / p)
+        _fill_draws(schedule, si, stage, n, it, omega[it], pbig[it])
     return omega, pbig
 
 
@@ -261,28 +268,30 @@ class ReconEngine:
     """Device-resident state for one reconstruction: the iterate, mask, data
     and every scratch buffer, plus one ``hicu_stage_args`` per stage.
 
-    ``run_stage`` issues one native call per stage (or per iteration when
-    per-iteration host work is requested).  The same engine can be re-run
-    (``reset``) for benchmarking without reallocating."""
+    ``run_stage`` issues one native call per stage (or per chunk of
+    iterations).  Host draws are written into pinned staging buffers (by
+    worker threads in :func:`hicu_reconstruct`) and copied asynchronously on
+    the compute stream, so drawing overlaps device execution.  The same
+    engine can be re-run (``reset``) for benchmarking without reallocating."""
 
-    def __init__(self, x_c64, mask_u8, kernel: KernelMask, schedule: SolverSchedule, regions, reference_c64=None):
+    def __init__(self, x_init, mask, dims, kernel: KernelMask, schedule: SolverSchedule, regions, reference=None):
         torch = nat.require_cuda()
         self.torch = torch
         self.kernel = kernel
         self.schedule = schedule
         self.regions = regions
-        self.dims = tuple(x_c64.shape)
+        self.dims = tuple(int(d) for d in dims)
         self.N = int(np.prod(self.dims))
         n, r = kernel.n, schedule.rank
         self.n, self.r = n, r
         self.ell = math.ceil(1.5 * r)
         self.soft = schedule.dc_mode == "soft"
         dev = "cuda"
-        self.x_init = to_dev(x_c64).reshape(-1)
+        self.x_init = to_dev(x_init).reshape(-1)
         self.y = self.x_init.clone()
-        self.mask = to_dev(mask_u8, np.uint8).reshape(-1)
+        self.mask = to_dev(mask, np.uint8).reshape(-1)
         self.x0 = self.x_init.clone() if self.soft else None
-        self.ref = to_dev(reference_c64).reshape(-1) if reference_c64 is not None else None
+        self.ref = to_dev(reference).reshape(-1) if reference is not None else None
         self.geoms = [device_geometry(kernel, reg, self.dims) for reg in regions]
         L = nat.lib()
         pmax = max(st.p for st in schedule.stages)
@@ -313,20 +322,45 @@ class ReconEngine:
         self.t0 = torch.zeros(1, dtype=f64, device=dev)
         self.aux_complex = (n * n + 2 * n * self.ell + 2 * self.ell * self.ell + 2 * n * r + n * gmax * pmax
                             + smax * pmax + self.N)
-        self.stage_data = [None] * len(schedule.stages)
-        self.recs = [None] * len(schedule.stages)
-        self.sers = [None] * len(schedule.stages)
-        self.inject = [None] * len(schedule.stages)
+        ns = len(schedule.stages)
+        self.stage_data = [None] * ns
+        self.host_draws = [None] * ns
+        self.recs = [None] * ns
+        self.sers = [None] * ns
+        self.inject = [None] * ns
+        self.prof = None
+        self.h2d_bytes = 0
+        for si, st in enumerate(schedule.stages):
+            it, G = st.iterations, st.gradient_steps
+            self.stage_data[si] = (torch.empty((it, n, self.ell), dtype=c128, device=dev),
+                                   torch.empty((it, n, G * st.p), dtype=c128, device=dev))
+            self.recs[si] = torch.zeros(it * G * nat.REC_SLOTS, dtype=f64, device=dev)
+            if self.ref is not None:
+                self.sers[si] = torch.zeros(it * G * self.ser_stride, dtype=f64, device=dev)
 
     # -- inputs --------------------------------------------------------------
-    def upload_draws(self, si: int, omega: np.ndarray, pbig: np.ndarray):
-        self.stage_data[si] = (to_dev(omega, np.complex128), to_dev(pbig, np.complex128))
-        st = self.schedule.stages[si]
-        self.recs[si] = self.torch.zeros(st.iterations * st.gradient_steps * nat.REC_SLOTS,
-                                         dtype=self.torch.float64, device="cuda")
-        if self.ref is not None:
-            self.sers[si] = self.torch.zeros(st.iterations * st.gradient_steps * self.ser_stride,
-                                             dtype=self.torch.float64, device="cuda")
+    def host_draw_buffers(self, si: int):
+        """Pinned host staging buffers for stage ``si`` (allocated once)."""
+        if self.host_draws[si] is None:
+            om, pb = self.stage_data[si]
+            self.host_draws[si] = (self.torch.empty(om.shape, dtype=om.dtype, pin_memory=True),
+                                   self.torch.empty(pb.shape, dtype=pb.dtype, pin_memory=True))
+        return self.host_draws[si]
+
+    def upload_draws(self, si: int, it0: int = 0, it1: int | None = None):
+        """Async H2D of the staged draws for iterations [it0, it1)."""
+        om_h, pb_h = self.host_draw_buffers(si)
+        om, pb = self.stage_data[si]
+        it1 = om.shape[0] if it1 is None else it1
+        om[it0:it1].copy_(om_h[it0:it1], non_blocking=True)
+        pb[it0:it1].copy_(pb_h[it0:it1], non_blocking=True)
+        self.h2d_bytes += (om_h[it0:it1].numel() + pb_h[it0:it1].numel()) * 16
+
+    def set_host_draws(self, si: int, omega: np.ndarray, pbig: np.ndarray):
+        om_h, pb_h = self.host_draw_buffers(si)
+        om_h.numpy()[...] = omega
+        pb_h.numpy()[...] = pbig
+        self.upload_draws(si)
 
     def set_injected_v(self, si: int, v_all):
         """Lockstep parity: use the given V (iters, n, r) instead of Gram+Nystrom."""
@@ -376,6 +410,7 @@ class ReconEngine:
             a.ref = None
             a.ser_parts = None
             a.ser_stride = 0
+        a.prof = self.prof.h if self.prof is not None else None
         return a
 
     def run_stage(self, si: int, it0: int = 0, iters: int | None = None, stream=None):
@@ -406,15 +441,25 @@ class ReconEngine:
         return self.y.reshape(self.dims).cpu().numpy().astype(np.complex128)
 
 
-def _coil_compress_host_entry(x0, mask, reference, nv):
-    from .coil import coil_compress
+_DRAW_POOL = None
 
-    xc, mc, basis = coil_compress(x0, mask, nv)
-    refc = None
-    if reference is not None:
-        nc = x0.shape[-1]
-        refc = (np.asarray(reference, np.complex128).reshape(-1, nc) @ basis).reshape(x0.shape[:-1] + (nv,))
-    return xc, mc, refc, basis
+
+def _draw_pool():
+    global _DRAW_POOL
+    if _DRAW_POOL is None:
+        import concurrent.futures as cf
+        import os
+
+        _DRAW_POOL = cf.ThreadPoolExecutor(max_workers=max(1, min(8, len(os.sched_getaffinity(0)))),
+                                           thread_name_prefix="hicu-draws")
+    return _DRAW_POOL
+
+
+def _chunks(schedule: SolverSchedule, per_iter: bool):
+    for si, st in enumerate(schedule.stages):
+        step = 1 if per_iter else max(1, min(8, (st.iterations + 3) // 4))
+        for it0 in range(0, st.iterations, step):
+            yield si, it0, min(st.iterations, it0 + step)
 
 
 def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, reference=None,
@@ -426,78 +471,113 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
     samples of ``xhat`` equal ``x0`` bit-exactly.
 
     B200 additions (keyword-only): ``coil_compress=Nv`` compresses the coil
-    axis to Nv virtual coils on the device first (the kernel's last extent
-    must then be Nv; ``xhat`` is in the compressed domain and
-    ``report.coil_basis`` holds the basis); ``lockstep_v`` is a callable
-    ``(stage, it) -> V`` that replaces the nullspace estimate (parity tests).
+    axis to Nv virtual coils on the device first (SVD coil compression; the
+    kernel's last extent must then be Nv; ``xhat`` is in the compressed
+    domain and ``report.coil_basis`` holds the basis); ``lockstep_v`` is a
+    callable ``(stage, it) -> V`` that replaces the nullspace estimate
+    (trajectory-parity tests).
     """
     watch = _Stopwatch()
-    basis = None
-    if coil_compress is not None:
-        x0_in = np.ascontiguousarray(x0)
-        mask_in = np.asarray(mask)
-        if x0_in.shape != mask_in.shape:
-            raise ConfigError(f"mask shape {mask_in.shape} does not match k-space shape {x0_in.shape}")
-        x0, mask, reference, basis = _coil_compress_host_entry(x0_in, mask_in, reference, int(coil_compress))
-    x0 = np.ascontiguousarray(x0, dtype=np.complex128)
+    x0 = np.asarray(x0)
     mask = np.asarray(mask)
     if x0.shape != mask.shape:
         raise ConfigError(f"mask shape {mask.shape} does not match k-space shape {x0.shape}")
-    regions = schedule.validate(kernel, x0.shape)
+    dims = x0.shape if coil_compress is None else x0.shape[:-1] + (int(coil_compress),)
+    regions = schedule.validate(kernel, dims)
     for region in regions:
         ell = int(np.ceil(1.5 * schedule.rank))
         if ell > region.s:
             raise ConfigError(f"sketch width {ell} exceeds region size {region.s}; enlarge the stage region")
     if int(np.ceil(1.5 * schedule.rank)) > 256:
         raise ConfigError("rank above 170 is not supported by the device nullspace kernels")
+    torch = nat.require_cuda()
+    observed_in = mask == 1
+    basis = None
+    h2d = 0
+    if coil_compress is not None:
+        from .coil import coil_compress_device
+
+        nc, nv = x0.shape[-1], int(coil_compress)
+        if not (1 <= nv <= nc) or nc > 32:
+            raise ConfigError(f"coil_compress must be in [1, {min(nc, 32)}], got {coil_compress}")
+        xm = np.where(observed_in, x0, 0).astype(np.complex64)  # mask_apply (arrays.py:54-67)
+        xd, md = to_dev(xm), to_dev(observed_in.astype(np.uint8), np.uint8)
+        h2d += xm.nbytes + md.numel()
+        ydev, mdev, bdev, _ = coil_compress_device(xd.reshape(-1), md.reshape(-1), nc, nv)
+        dims = x0.shape[:-1] + (nv,)
+        x_init, mask_dev = ydev, mdev
+        mask_c = np.ascontiguousarray(mask[..., :nv])
+        observed = mask_c == 1
+        ref_dev = None
+        if reference is not None:
+            rd = to_dev(np.asarray(reference).astype(np.complex64))
+            h2d += rd.numel() * 8
+            ref_dev = torch.empty(int(np.prod(dims)), dtype=torch.complex64, device="cuda")
+            nat.check(nat.lib().hicu_coil_apply(rd.numel() // nc, nc, nv, rd.data_ptr(), None, bdev.data_ptr(),
+                                                ref_dev.data_ptr(), None, nat.stream_handle()), "coil_apply")
+        basis = bdev.cpu().numpy()
+        x0_exact = None  # observed samples live (in c64) on the device
+    else:
+        dims = x0.shape
+        x0_exact = np.ascontiguousarray(x0, dtype=np.complex128)
+        xm = np.where(observed_in, x0_exact, 0)
+        x_init = xm.astype(np.complex64)
+        mask_dev = observed_in.astype(np.uint8)
+        observed = observed_in
+        ref_dev = None if reference is None else np.asarray(reference).astype(np.complex64)
+        h2d += x_init.nbytes + mask_dev.nbytes + (0 if ref_dev is None else ref_dev.nbytes)
     counters = counters if counters is not None else Counters()
     meter = meter if meter is not None else MemoryMeter()
     report = ReconReport()
-    observed = mask == 1
-    x = np.where(observed, x0, 0)  # mask_apply (arrays.py:54-67), bit-exact copy where observed
-    mask_u8 = observed.astype(np.uint8)
-    ref128 = None if reference is None else np.asarray(reference, dtype=np.complex128)
-    eng = ReconEngine(x.astype(np.complex64), mask_u8, kernel, schedule, regions,
-                      None if ref128 is None else ref128.astype(np.complex64))
+    eng = ReconEngine(x_init, mask_dev, dims, kernel, schedule, regions, ref_dev)
     meter.alloc(eng.aux_complex)
-    tail_region = full_region(x0.shape, kernel, schedule.circular_axes)
+    tail_region = full_region(dims, kernel, schedule.circular_axes)
     log_tail = 0 < tail_energy_threshold and tail_region.s * kernel.n <= tail_energy_threshold
     per_iter = log_tail or iterate_callback is not None
-    torch = eng.torch
-    eng.stamp_start()
-    for si, stage in enumerate(schedule.stages):
-        omega, pbig = draw_stage(schedule, si, stage, kernel.n)
-        eng.upload_draws(si, omega, pbig)
-        if lockstep_v is not None:
+    if lockstep_v is not None:
+        for si, stage in enumerate(schedule.stages):
             eng.set_injected_v(si, np.stack([np.asarray(lockstep_v(si, it), np.complex128)
                                              for it in range(stage.iterations)]))
+    # host draws (reference streams) on worker threads, overlapped with the device
+    pool = _draw_pool()
+    futures = []
+    for si, it0, it1 in _chunks(schedule, per_iter):
+        om_h, pb_h = eng.host_draw_buffers(si)
+        om_np, pb_np = om_h.numpy(), pb_h.numpy()
+        st = schedule.stages[si]
+        futs = [pool.submit(_fill_draws, schedule, si, st, kernel.n, it, om_np[it], pb_np[it])
+                for it in range(it0, it1)]
+        futures.append((si, it0, it1, futs))
+    eng.stamp_start()
+    tails = {}
+    for si, it0, it1, futs in futures:
+        for f in futs:
+            f.result()
+        eng.upload_draws(si, it0, it1)
+        eng.run_stage(si, it0, it1 - it0)
         if not per_iter:
-            eng.run_stage(si)
             continue
-        for it in range(stage.iterations):
-            eng.run_stage(si, it, 1)
-            torch.cuda.synchronize()
-            watch.pause()
-            eng.check_status()
-            xi = None
-            if log_tail:
-                tail = eng.tail_energy(kernel, tail_region, schedule.rank)
-                eng._tails = getattr(eng, "_tails", {})
-                eng._tails[(si, it)] = tail
-            if iterate_callback is not None:
-                xi = eng.download()
-                if schedule.dc_mode == "hard":
-                    xi[observed] = x0[observed]
-                iterate_callback(si, it, xi)
-            watch.resume()
+        torch.cuda.synchronize()
+        watch.pause()
+        eng.check_status()
+        if log_tail:
+            tails[(si, it0)] = eng.tail_energy(kernel, tail_region, schedule.rank)
+        if iterate_callback is not None:
+            xi = eng.download()
+            if schedule.dc_mode == "hard" and x0_exact is not None:
+                xi[observed] = x0_exact[observed]
+            iterate_callback(si, it0, xi)
+        watch.resume()
     torch.cuda.synchronize()
+    xhat = eng.download()
     total = watch.pause()
     eng.check_status()
     # ---- records (one device->host read per stage) ----
     t0 = float(eng.t0.item())
-    tails = getattr(eng, "_tails", {})
+    d2h = xhat.size * 8
     for si, stage in enumerate(schedule.stages):
         rec = eng.recs[si].cpu().numpy().reshape(stage.iterations, stage.gradient_steps, nat.REC_SLOTS)
+        d2h += rec.nbytes
         sers = None
         if eng.ref is not None:
             sers = eng.sers[si].cpu().numpy().reshape(stage.iterations, stage.gradient_steps, eng.ser_stride)
@@ -526,14 +606,15 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
             if lockstep_v is None:
                 counters.gram += 1
             report.iterations.append(IterationRecord(si, it, last_obj, last_sec, last_ser, tails.get((si, it))))
-    xhat = eng.download()
-    if schedule.dc_mode == "hard":
-        xhat[observed] = x0[observed]
+    if schedule.dc_mode == "hard" and x0_exact is not None:
+        xhat[observed] = x0_exact[observed]
     report.total_seconds = total
     report.counters = counters.snapshot()
     report.peak_aux_complex = meter.peak
     meter.free(eng.aux_complex)
-    report.device = {"name": torch.cuda.get_device_name(), "nullspace": "gram+nystrom" if lockstep_v is None
-                     else "injected", "precision": "c64 data, fp32 FMA, fp64 reductions / nullspace"}
+    report.device = {"name": torch.cuda.get_device_name(),
+                     "nullspace": "gram+nystrom (canonical phases)" if lockstep_v is None else "injected",
+                     "precision": "c64 data, fp32 FMA, fp64 reductions and nullspace",
+                     "h2d_bytes": int(h2d + eng.h2d_bytes), "d2h_bytes": int(d2h)}
     report.coil_basis = basis
     return xhat, report

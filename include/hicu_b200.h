@@ -57,9 +57,14 @@ typedef struct hicu_geom {
   int64_t roff[HICU_MAX_NDIM];    /* region offsets (0 on circular axes)      */
   int64_t rext[HICU_MAX_NDIM];    /* region extents                           */
   uint32_t circular;              /* bit d set: axis d is circular            */
+  int32_t flags;                  /* HICU_GEOM_COIL_SEPARABLE: the support is  *
+                                   * (spatial support) x (all dims[last] coils), *
+                                   * kappa = sp*dims[last] + c                  */
   const int32_t* pos;             /* device: n x ndim support positions       */
   const int64_t* koff;            /* device: n flat offsets, non-circular axes */
 } hicu_geom;
+
+#define HICU_GEOM_COIL_SEPARABLE 1
 
 /* Per-step scalar record written by hicu_step_update (doubles). */
 enum {

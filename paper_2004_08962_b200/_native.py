@@ -18,6 +18,7 @@ MAX_NDIM = 8
 
 REC_OBJ, REC_NUM, REC_DEN, REC_ETA, REC_OBJ_AFTER, REC_GNORM2, REC_DEGENERATE, REC_TIME = range(8)
 REC_SLOTS = 8
+GEOM_COIL_SEPARABLE = 1
 PROF_KINDS = ("gram", "nystrom", "householder", "conv_fwd", "scatter", "conv_els", "update")
 
 
@@ -29,6 +30,7 @@ class HicuGeom(ctypes.Structure):
         ("roff", c_int64 * MAX_NDIM),
         ("rext", c_int64 * MAX_NDIM),
         ("circular", c_uint32),
+        ("flags", c_int32),
         ("pos", c_void_p),
         ("koff", c_void_p),
     ]

@@ -102,6 +102,17 @@ int hicu_make_devgeom(const hicu_geom* g, DevGeom* out) {
       d.circ_axes[d.ncirc++] = a;
     }
   }
+  d.nc = 0;
+  d.nsp = 0;
+  {
+    const int L = g->ndim - 1;
+    const int64_t ncl = g->dims[L];
+    if ((g->flags & HICU_GEOM_COIL_SEPARABLE) && L >= 1 && !(g->circular & (1u << L)) && g->rext[L] == 1 &&
+        g->roff[L] == 0 && ncl <= 32 && g->n % ncl == 0) {
+      d.nc = (int)ncl;
+      d.nsp = g->n / (int)ncl;
+    }
+  }
   *out = d;
   return HICU_OK;
 }

@@ -70,6 +70,12 @@ struct DevGeom {
   int64_t N;                        // k-space size
   const int32_t* pos;
   const int64_t* koff;
+  // coil-structured fast path: last axis is the coil axis, the kernel spans
+  // all Nc coils at every spatial tap (kappa = sp*Nc + c), the region has one
+  // coil row (rext[last] == 1, roff[last] == 0, not circular).  nc = 0 when
+  // the geometry does not have this structure (generic kernels are used).
+  int nc;
+  int nsp;  // spatial taps (n / nc)
 };
 
 // Non-circular part of the flat address of row i, plus the region coordinates

@@ -16,6 +16,9 @@
 
 #include <math.h>
 
+size_t hicu_heev_top_workspace(int l, int r);
+int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void* ws, cudaStream_t st);
+
 namespace {
 
 constexpr int kSmemCap = 200 * 1024;
@@ -95,15 +98,16 @@ chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, c
         else A[(size_t)kk * ell + j] = inv * A[(size_t)kk * ell + j];
       }
       __syncthreads();
-      const int rem = ell - kk - 1;
-      for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
-        const int i = kk + 1 + e / rem, j = kk + 1 + e % rem;
-        if (j < i) continue;
-        // A[i][j] -= conj(R[kk][i]) * R[kk][j]
-        const double2 a = A[(size_t)kk * ell + i], b = A[(size_t)kk * ell + j];
-        double2 v = A[(size_t)i * ell + j];
-        v = v - cmulc(a, b);
-        A[(size_t)i * ell + j] = v;
+      // trailing update of the upper triangle, one warp per row
+      {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+        for (int i = kk + 1 + warp; i < ell; i += nw) {
+          const double2 a = A[(size_t)kk * ell + i];
+          for (int j = i + lane; j < ell; j += 32) {
+            // A[i][j] -= conj(R[kk][i]) * R[kk][j]
+            A[(size_t)i * ell + j] = A[(size_t)i * ell + j] - cmulc(a, A[(size_t)kk * ell + j]);
+          }
+        }
       }
       __syncthreads();
     }
@@ -197,7 +201,7 @@ jacobi_kernel(int ell, const double2* __restrict__ Mg, double2* __restrict__ gws
   if (threadIdx.x == 0) {
     double tr = 0.0;
     for (int i = 0; i < ell; ++i) tr += fabs(A[(size_t)i * ell + i].x);
-    s_floor = 1e-300 + 1e-17 * tr;
+    s_floor = 1e-300 + 1e-15 * tr;  // below fp64 round-off of the largest eigenvalues
   }
   __syncthreads();
   int rounds = 0;
@@ -316,10 +320,19 @@ __global__ void rot_apply_kernel(int n, int ell, int r, const double2* __restric
 // zgesdd's phases, which are an implementation detail; fixing a documented
 // convention makes the Householder basis (subspace.py:158-212), and with it
 // the free-running trajectory, reproducible by the oracle.
-__global__ void canon_phase_kernel(int n, int r, double2* __restrict__ V) {
+__global__ void canon_phase_kernel(int n, int r, double2* __restrict__ V, const double* __restrict__ lam,
+                                   int* __restrict__ status) {
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int t = blockIdx.x * warps + warp; t < r; t += gridDim.x * warps) {
+    if (lam) {
+      // V = W F Lambda^{-1/2}: unit columns (left singular vectors of W)
+      const double lv = lam[t];
+      const double sc = lv > 0.0 ? 1.0 / sqrt(lv) : 0.0;
+      if (!(lv > 0.0) && lane == 0 && status) *status = HICU_ERR_DEGENERATE_INPUT;
+      for (int k = lane; k < n; k += 32) V[(size_t)k * r + t] = sc * V[(size_t)k * r + t];
+      __syncwarp();
+    }
     double best = -1.0;
     int bk = 0;
     for (int k = lane; k < n; k += 32) {
@@ -350,17 +363,17 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
                    bool use_smem, double2* __restrict__ refl, double2* __restrict__ tau, int* __restrict__ flags,
                    int* __restrict__ status) {
   extern __shared__ double2 sV[];
-  double2* v = use_smem ? sV : gws;  // n x r row-major
+  double2* v = use_smem ? sV : gws;  // column-major: element (k, j) at v[j*n + k] (conflict-free)
   __shared__ double red[32];
   __shared__ double2 s_u0inv, s_tau;
   __shared__ int s_active;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[e] = Vg[e];
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[(size_t)(e % r) * n + e / r] = Vg[e];
   for (int e = threadIdx.x; e < n * r; e += blockDim.x) refl[e] = cd(0.0, 0.0);
   __syncthreads();
   for (int col = 0; col < r; ++col) {
     double t = 0.0;
-    for (int k = col + 1 + threadIdx.x; k < n; k += blockDim.x) t += abs2d(v[(size_t)k * r + col]);
+    for (int k = col + 1 + threadIdx.x; k < n; k += blockDim.x) t += abs2d(v[(size_t)col * n + k]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     if (lane == 0) red[warp] = t;
@@ -368,7 +381,7 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
     if (threadIdx.x == 0) {
       double tail = 0.0;
       for (int w = 0; w < nw; ++w) tail += red[w];
-      const double2 x0 = v[(size_t)col * r + col];
+      const double2 x0 = v[(size_t)col * n + col];
       const double beta = sqrt(tail + x0.x * x0.x + x0.y * x0.y);
       int active = 1;
       if (beta < tol) {
@@ -402,7 +415,7 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
       const double2 ui = s_u0inv;
       // w = xvec / u0, w[0] = 1
       for (int k = col + threadIdx.x; k < n; k += blockDim.x) {
-        const double2 wv = (k == col) ? cd(1.0, 0.0) : cmul(v[(size_t)k * r + col], ui);
+        const double2 wv = (k == col) ? cd(1.0, 0.0) : cmul(v[(size_t)col * n + k], ui);
         refl[(size_t)col * n + k] = wv;
       }
       __syncthreads();
@@ -411,14 +424,14 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
       const double2* wrow = refl + (size_t)col * n;
       for (int j = col + 1 + warp; j < r; j += nw) {
         double2 dot = cd(0.0, 0.0);
-        for (int k = col + lane; k < n; k += 32) zfmac(dot, wrow[k], v[(size_t)k * r + j]);
+        for (int k = col + lane; k < n; k += 32) zfmac(dot, wrow[k], v[(size_t)j * n + k]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
           dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
         }
         const double2 f = cmul(tv, dot);
-        for (int k = col + lane; k < n; k += 32) v[(size_t)k * r + j] = v[(size_t)k * r + j] - cmul(wrow[k], f);
+        for (int k = col + lane; k < n; k += 32) v[(size_t)j * n + k] = v[(size_t)j * n + k] - cmul(wrow[k], f);
       }
     }
     __syncthreads();
@@ -464,7 +477,8 @@ __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict_
 }
 
 struct NysWs {
-  double2 *Y, *O, *C, *W, *M, *scratch;
+  double2 *Y, *O, *C, *W, *M, *scratch, *F;
+  void* heev;
   double* evals;
   double* nu;
   int* order;
@@ -495,6 +509,8 @@ NysWs nystrom_layout(int n, int ell, char* base) {
   w.order = (int*)take((size_t)ell * sizeof(int));
   w.nrounds = (int*)take(sizeof(int));
   w.log = (RotEntry*)take((size_t)kMaxSweeps * (m - 1) * (m / 2) * sizeof(RotEntry));
+  w.F = (double2*)take((size_t)ell * ell * sizeof(double2));
+  w.heev = (void*)take(hicu_heev_top_workspace(ell, ell));
   w.bytes = off;
   return w;
 }
@@ -545,24 +561,11 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     if ((s = hicu_check_launch("trsm_rows_kernel"))) return s;
   }
   if ((s = zgemm_launch('C', 'N', ell, ell, n, w.W, ell, w.W, ell, w.M, ell, st))) return s;
-  {
-    const size_t bytes = (size_t)ell * ell * sizeof(double2);
-    const bool sm = bytes <= kSmemCap;
-    hicu_allow_max_smem((const void*)jacobi_kernel);
-    jacobi_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.M, w.scratch, sm, kMaxSweeps, 1e-15, w.log, w.nrounds,
-                                                   w.evals, w.order, status_dev);
-    if ((s = hicu_check_launch("jacobi_kernel"))) return s;
-  }
-  {
-    const int warps = 8;
-    const size_t smem = (size_t)warps * ell * sizeof(double2);
-    hicu_allow_max_smem((const void*)rot_apply_kernel);
-    const int blocks = (n + warps - 1) / warps;
-    rot_apply_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, r, w.W, w.log, w.nrounds, w.evals, w.order,
-                                                       (double2*)V, status_dev, true);
-    if ((s = hicu_check_launch("rot_apply_kernel"))) return s;
-  }
-  canon_phase_kernel<<<(r + 7) / 8, 256, 0, st>>>(n, r, (double2*)V);
+  // top-r eigenpairs of M = W^H W (tridiagonal + bisection + inverse iteration)
+  if ((s = hicu_heev_top(ell, r, w.M, w.evals, w.F, w.heev, st))) return s;
+  // V = W F Lambda^{-1/2}
+  if ((s = zgemm_launch('N', 'N', n, r, ell, w.W, ell, w.F, r, (double2*)V, r, st))) return s;
+  canon_phase_kernel<<<(r + 7) / 8, 256, 0, st>>>(n, r, (double2*)V, w.evals, status_dev);
   if ((s = hicu_check_launch("canon_phase_kernel"))) return s;
   return HICU_OK;
 }

@@ -255,6 +255,259 @@ __global__ void ser_kernel(int64_t N, const float2* __restrict__ ref, const floa
   block_reduce_store<2>(v, parts + 2 * (size_t)blockIdx.x);
 }
 
+
+// ---------------------------------------------------------------------------
+// Coil-structured fast paths (DevGeom.nc > 0: kappa = sp*Nc + c, one coil row
+// in the region).  Conv: one thread per region row, Nc coils loaded as
+// float4 pairs per spatial tap.  Scatter: one thread per SPATIAL k-space
+// location accumulating all Nc coils, so each valid spatial tap costs one
+// u-row load reused Nc times (the generic kernel tests every (spatial, coil)
+// tap pair per coil).
+// ---------------------------------------------------------------------------
+template <int PMAX, int NCMAX, bool CIRC, int MODE>
+__global__ void __launch_bounds__(kConvThreads)
+conv_coil_kernel(DevGeom g, const float2* __restrict__ y, const float2* __restrict__ qt, int p,
+                 float2* __restrict__ u, double* __restrict__ parts) {
+  extern __shared__ unsigned char smem_raw[];
+  const int nc = g.nc, nsp = g.nsp;
+  float2* sq = reinterpret_cast<float2*>(smem_raw);                          // n * PMAX
+  int64_t* skoff = reinterpret_cast<int64_t*>(sq + (size_t)g.n * PMAX);      // nsp
+  int32_t* spos = reinterpret_cast<int32_t*>(skoff + nsp);                    // nsp * ndim
+  for (int t = threadIdx.x; t < g.n * PMAX; t += blockDim.x) {
+    const int k = t / PMAX, j = t % PMAX;
+    sq[t] = (j < p) ? qt[(size_t)k * p + j] : cf(0.f, 0.f);
+  }
+  for (int t = threadIdx.x; t < nsp; t += blockDim.x) skoff[t] = g.koff[(size_t)t * nc];
+  if (CIRC)
+    for (int t = threadIdx.x; t < nsp * g.ndim; t += blockDim.x)
+      spos[t] = g.pos[(size_t)(t / g.ndim) * nc * g.ndim + t % g.ndim];
+  __syncthreads();
+  const bool vec2 = (nc % 2) == 0;
+  double a0 = 0.0, a1 = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.s; i += (int64_t)gridDim.x * blockDim.x) {
+    int cc[HICU_MAX_NDIM];
+    const int64_t base = row_base(g, i, cc);
+    float2 acc[PMAX];
+#pragma unroll
+    for (int j = 0; j < PMAX; ++j) acc[j] = cf(0.f, 0.f);
+    for (int sp = 0; sp < nsp; ++sp) {
+      int64_t addr = base + skoff[sp];
+      if (CIRC) addr += circ_part(g, cc, spos + (size_t)sp * g.ndim);
+      const float2* qsp = sq + (size_t)sp * nc * PMAX;
+      if (vec2) {
+        const float4* yp = reinterpret_cast<const float4*>(y + addr);
+#pragma unroll 4
+        for (int c2 = 0; c2 < nc / 2; ++c2) {
+          const float4 v = __ldg(yp + c2);
+          const float2 v0 = cf(v.x, v.y), v1 = cf(v.z, v.w);
+          const float2* q0 = qsp + (size_t)(2 * c2) * PMAX;
+#pragma unroll
+          for (int j = 0; j < PMAX; ++j) {
+            cfma(acc[j], v0, q0[j]);
+            cfma(acc[j], v1, q0[PMAX + j]);
+          }
+        }
+      } else {
+        for (int c = 0; c < nc; ++c) {
+          const float2 v = __ldg(y + addr + c);
+          const float2* q0 = qsp + (size_t)c * PMAX;
+#pragma unroll
+          for (int j = 0; j < PMAX; ++j) cfma(acc[j], v, q0[j]);
+        }
+      }
+    }
+    float2* ui = u + (size_t)i * p;
+#pragma unroll
+    for (int j = 0; j < PMAX; ++j) {
+      if (j < p) {
+        if (MODE == 0) {
+          ui[j] = acc[j];
+          a0 += (double)acc[j].x * acc[j].x + (double)acc[j].y * acc[j].y;
+        } else {
+          const float2 uv = ui[j];
+          a0 += (double)acc[j].x * uv.x + (double)acc[j].y * uv.y;
+          a1 += (double)acc[j].x * acc[j].x + (double)acc[j].y * acc[j].y;
+        }
+      }
+    }
+  }
+  if (MODE == 0) {
+    double v[1] = {a0};
+    block_reduce_store<1>(v, parts + blockIdx.x);
+  } else {
+    double v[2] = {a0, a1};
+    block_reduce_store<2>(v, parts + 2 * (size_t)blockIdx.x);
+  }
+}
+
+template <int PMAX, int NCMAX, bool CIRC>
+__global__ void __launch_bounds__(128)
+scatter_coil_kernel(DevGeom g, const float2* __restrict__ qt, int p, const float2* __restrict__ u,
+                    const uint8_t* __restrict__ mask, const float2* __restrict__ y,
+                    const float2* __restrict__ x0, int dc_mode, float lam, float2* __restrict__ gout,
+                    double* __restrict__ parts) {
+  extern __shared__ unsigned char smem_raw[];
+  const int nc = g.nc, nsp = g.nsp, L = g.ndim - 1;
+  float2* sq = reinterpret_cast<float2*>(smem_raw);                           // n * PMAX, conj
+  int64_t* srow = reinterpret_cast<int64_t*>(sq + (size_t)g.n * PMAX);        // nsp
+  int32_t* spos = reinterpret_cast<int32_t*>(srow + nsp);                      // nsp * L
+  for (int t = threadIdx.x; t < g.n * PMAX; t += blockDim.x) {
+    const int k = t / PMAX, j = t % PMAX;
+    const float2 q = (j < p) ? qt[(size_t)k * p + j] : cf(0.f, 0.f);
+    sq[t] = cf(q.x, -q.y);
+  }
+  for (int t = threadIdx.x; t < nsp * L; t += blockDim.x)
+    spos[t] = g.pos[(size_t)(t / L) * nc * g.ndim + t % L];
+  __syncthreads();
+  for (int t = threadIdx.x; t < nsp; t += blockDim.x) {
+    int64_t o = 0;
+    for (int d = 0, ci = 0; d < L; ++d) {
+      if (ci < g.ncirc && g.circ_axes[ci] == d) { ++ci; continue; }
+      o += (int64_t)spos[(size_t)t * L + d] * g.rstride[d];
+    }
+    srow[t] = o;
+  }
+  __syncthreads();
+  const int64_t Ns = g.N / nc;
+  double a_g = 0.0, a_res = 0.0, a_num = 0.0, a_den = 0.0;
+  for (int64_t ms = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ms < Ns; ms += (int64_t)gridDim.x * blockDim.x) {
+    int64_t mc[HICU_MAX_NDIM];
+    int64_t rem = ms;
+    for (int d = L - 1; d >= 0; --d) {
+      mc[d] = rem % g.dims[d];
+      rem /= g.dims[d];
+    }
+    int64_t rbase = 0;
+    for (int d = 0, ci = 0; d < L; ++d) {
+      if (ci < g.ncirc && g.circ_axes[ci] == d) { ++ci; continue; }
+      rbase += (mc[d] - g.roff[d]) * g.rstride[d];
+    }
+    float2 acc[NCMAX];
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) acc[c] = cf(0.f, 0.f);
+    for (int sp = 0; sp < nsp; ++sp) {
+      const int32_t* pk = spos + (size_t)sp * L;
+      bool ok = true;
+      int64_t crow = 0;
+      for (int d = 0, ci = 0; d < L; ++d) {
+        if (CIRC && ci < g.ncirc && g.circ_axes[ci] == d) {
+          int64_t r = mc[d] - pk[d];
+          if (r < 0) r += g.dims[d];
+          crow += r * g.rstride[d];
+          ++ci;
+        } else {
+          const int64_t r = mc[d] - g.roff[d] - pk[d];
+          ok = ok && (r >= 0) && (r < g.rext[d]);
+        }
+      }
+      if (!ok) continue;
+      const float2* ur = u + (size_t)(rbase - srow[sp] + crow) * p;
+      float2 uk[PMAX];
+#pragma unroll
+      for (int j = 0; j < PMAX; ++j) uk[j] = (j < p) ? __ldg(ur + j) : cf(0.f, 0.f);
+      const float2* qsp = sq + (size_t)sp * nc * PMAX;
+#pragma unroll
+      for (int c = 0; c < NCMAX; ++c) {
+        if (c < nc) {
+#pragma unroll
+          for (int j = 0; j < PMAX; ++j) cfma(acc[c], qsp[c * PMAX + j], uk[j]);
+        }
+      }
+    }
+    const int64_t m0 = ms * nc;
+#pragma unroll
+    for (int c = 0; c < NCMAX; ++c) {
+      if (c >= nc) break;
+      const int64_t m = m0 + c;
+      float2 a = acc[c];
+      const bool on = (dc_mode != 2) && mask[m] == 1;
+      if (dc_mode == 0) {
+        if (on) a = cf(0.f, 0.f);
+      } else if (dc_mode == 1) {
+        const float2 res = on ? (y[m] - x0[m]) : cf(0.f, 0.f);
+        a_res += (double)res.x * res.x + (double)res.y * res.y;
+        a = a + lam * res;
+        if (on) {
+          a_num += (double)a.x * res.x + (double)a.y * res.y;
+          a_den += (double)a.x * a.x + (double)a.y * a.y;
+        }
+      }
+      a_g += (double)a.x * a.x + (double)a.y * a.y;
+      gout[m] = a;
+    }
+  }
+  double v[4] = {a_g, a_res, a_num, a_den};
+  block_reduce_store<4>(v, parts + 4 * (size_t)blockIdx.x);
+}
+
+template <int PMAX, int NCMAX>
+int launch_conv_coil(const DevGeom& g, const float2* y, const float2* qt, int p, float2* u, double* parts, int mode,
+                     cudaStream_t st) {
+  const int blocks = conv_blocks(g.s);
+  const bool circ = g.ncirc > 0;
+  const size_t smem = (size_t)g.n * PMAX * sizeof(float2) + (size_t)g.nsp * sizeof(int64_t) +
+                      (circ ? (size_t)g.nsp * g.ndim * sizeof(int32_t) : 0);
+  if (smem > 200 * 1024) return hicu_set_error(HICU_ERR_SIZE, "conv: n*p too large for shared memory");
+#define HICU_LAUNCH_CONVC(C, M)                                                 \
+  do {                                                                          \
+    auto kfn = conv_coil_kernel<PMAX, NCMAX, C, M>;                             \
+    hicu_allow_max_smem((const void*)kfn);                                      \
+    kfn<<<blocks, kConvThreads, smem, st>>>(g, y, qt, p, u, parts);             \
+  } while (0)
+  if (circ) {
+    if (mode == 0) HICU_LAUNCH_CONVC(true, 0); else HICU_LAUNCH_CONVC(true, 1);
+  } else {
+    if (mode == 0) HICU_LAUNCH_CONVC(false, 0); else HICU_LAUNCH_CONVC(false, 1);
+  }
+#undef HICU_LAUNCH_CONVC
+  return hicu_check_launch("conv_coil_kernel");
+}
+
+int scatter_coil_blocks(int64_t Ns) {
+  int64_t b = (Ns + 127) / 128;
+  int64_t cap = (int64_t)hicu_sm_count() * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+template <int PMAX, int NCMAX>
+int launch_scatter_coil(const DevGeom& g, const float2* qt, int p, const float2* u, const uint8_t* mask,
+                        const float2* y, const float2* x0, int dc_mode, float lam, float2* gout, double* parts,
+                        cudaStream_t st) {
+  const int blocks = scatter_coil_blocks(g.N / g.nc);
+  const size_t smem = (size_t)g.n * PMAX * sizeof(float2) + (size_t)g.nsp * sizeof(int64_t) +
+                      (size_t)g.nsp * (g.ndim - 1) * sizeof(int32_t);
+  if (smem > 200 * 1024) return hicu_set_error(HICU_ERR_SIZE, "scatter: n*p too large for shared memory");
+  if (g.ncirc > 0) {
+    auto kfn = scatter_coil_kernel<PMAX, NCMAX, true>;
+    hicu_allow_max_smem((const void*)kfn);
+    kfn<<<blocks, 128, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+  } else {
+    auto kfn = scatter_coil_kernel<PMAX, NCMAX, false>;
+    hicu_allow_max_smem((const void*)kfn);
+    kfn<<<blocks, 128, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+  }
+  return hicu_check_launch("scatter_coil_kernel");
+}
+
+template <int PMAX>
+int conv_coil_dispatch(const DevGeom& g, const float2* y, const float2* qt, int p, float2* u, double* parts, int mode,
+                       cudaStream_t st) {
+  if (g.nc <= 8) return launch_conv_coil<PMAX, 8>(g, y, qt, p, u, parts, mode, st);
+  if (g.nc <= 16) return launch_conv_coil<PMAX, 16>(g, y, qt, p, u, parts, mode, st);
+  return launch_conv_coil<PMAX, 32>(g, y, qt, p, u, parts, mode, st);
+}
+
+template <int PMAX>
+int scatter_coil_dispatch(const DevGeom& g, const float2* qt, int p, const float2* u, const uint8_t* mask,
+                          const float2* y, const float2* x0, int dc_mode, float lam, float2* gout, double* parts,
+                          cudaStream_t st) {
+  if (g.nc <= 8) return launch_scatter_coil<PMAX, 8>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts, st);
+  if (g.nc <= 16) return launch_scatter_coil<PMAX, 16>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts, st);
+  return launch_scatter_coil<PMAX, 32>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts, st);
+}
+
 template <int PMAX>
 int launch_conv(const DevGeom& g, const float2* y, const float2* qt, int p, float2* u, double* parts,
                 int mode, cudaStream_t st) {
@@ -288,6 +541,11 @@ int conv_dispatch(const hicu_geom* hg, const void* y, const void* qt, int p, con
   cudaStream_t s = (cudaStream_t)stream;
   float2* u = mode == 0 ? (float2*)u_out : (float2*)u_in;
   if (!u) return hicu_set_error(HICU_ERR_PARAMETER, "conv: null u");
+  if (g.nc > 0) {
+    if (p <= 4) return conv_coil_dispatch<4>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+    if (p <= 8) return conv_coil_dispatch<8>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+    return conv_coil_dispatch<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+  }
   if (p <= 4) return launch_conv<4>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
   if (p <= 8) return launch_conv<8>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
   return launch_conv<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
@@ -324,7 +582,7 @@ extern "C" int hicu_conv_nparts(const hicu_geom* hg) {
 extern "C" int hicu_scatter_nparts(const hicu_geom* hg) {
   DevGeom g;
   if (hicu_make_devgeom(hg, &g)) return -1;
-  return scatter_blocks(g.N);
+  return g.nc > 0 ? scatter_coil_blocks(g.N / g.nc) : scatter_blocks(g.N);
 }
 
 extern "C" int hicu_conv_fwd(const hicu_geom* g, const void* y, const void* qt, int p, void* u,
@@ -351,6 +609,13 @@ extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const
   cudaStream_t s = (cudaStream_t)stream;
   auto q = (const float2*)qt;
   auto uu = (const float2*)u;
+  if (g.nc > 0) {
+    auto yy = (const float2*)y;
+    auto xx = (const float2*)x0;
+    if (p <= 4) return scatter_coil_dispatch<4>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
+    if (p <= 8) return scatter_coil_dispatch<8>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
+    return scatter_coil_dispatch<16>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
+  }
   if (p <= 4)
     return launch_scatter<4>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
                              (float2*)gout, dc_parts, s);

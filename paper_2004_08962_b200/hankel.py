@@ -237,6 +237,7 @@ class DeviceGeometry:
             g.roff[d] = region.offsets[d]
             g.rext[d] = region.extents[d]
         g.circular = sum(1 << a for a in region.circular_axes)
+        g.flags = nat.GEOM_COIL_SEPARABLE if _coil_separable(kernel, dims) else 0
         g.pos = self.pos_t.data_ptr()
         g.koff = self.koff_t.data_ptr()
         self.struct = g
@@ -248,6 +249,20 @@ class DeviceGeometry:
         import ctypes
 
         return ctypes.byref(self.struct)
+
+
+def _coil_separable(kernel: KernelMask, dims) -> bool:
+    """True when the support is (spatial support) x (all coils): kappa =
+    sp*Nc + c.  Enables the coil-vectorised device kernels."""
+    nc = int(dims[-1])
+    if len(dims) < 2 or kernel.extents[-1] != nc or kernel.n % nc != 0:
+        return False
+    pos = kernel.positions
+    c = np.arange(kernel.n) % nc
+    if not np.array_equal(pos[:, -1], c):
+        return False
+    sp = pos[::nc, :-1]
+    return bool(np.array_equal(pos[:, :-1], np.repeat(sp, nc, axis=0)))
 
 
 _GEOM_CACHE: dict = {}

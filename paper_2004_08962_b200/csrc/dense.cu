@@ -61,11 +61,12 @@ int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int 
 // Cholesky C_nu = C + nu*O = R^H R (upper R, in place in C)
 // nu starts at 0; on a non-positive pivot it escalates (stabilised Nystrom).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024)
+template <bool SMEM>
+__global__ void __launch_bounds__(512)
 chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, const double2* __restrict__ G,
-            int n, double2* __restrict__ gws, bool use_smem, double* __restrict__ nu_out, int* __restrict__ status) {
+            int n, double2* __restrict__ gws, double* __restrict__ nu_out, int* __restrict__ status) {
   extern __shared__ double2 sA[];
-  double2* A = use_smem ? sA : gws;
+  double2* A = SMEM ? sA : gws;
   __shared__ double s_scale;
   __shared__ int s_fail;
   __shared__ double s_nu;
@@ -363,7 +364,8 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
                    bool use_smem, double2* __restrict__ refl, double2* __restrict__ tau, int* __restrict__ flags,
                    int* __restrict__ status) {
   extern __shared__ double2 sV[];
-  double2* v = use_smem ? sV : gws;  // column-major: element (k, j) at v[j*n + k] (conflict-free)
+  double2* sw = sV;                                   // current reflector w (n)
+  double2* v = use_smem ? sV + n : gws;  // column-major: element (k, j) at v[j*n + k] (conflict-free)
   __shared__ double red[32];
   __shared__ double2 s_u0inv, s_tau;
   __shared__ int s_active;
@@ -417,21 +419,35 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
       for (int k = col + threadIdx.x; k < n; k += blockDim.x) {
         const double2 wv = (k == col) ? cd(1.0, 0.0) : cmul(v[(size_t)col * n + k], ui);
         refl[(size_t)col * n + k] = wv;
+        sw[k] = wv;
       }
       __syncthreads();
       // rest -= (tau w)(w^H rest), one warp per remaining column
       const double2 tv = s_tau;
-      const double2* wrow = refl + (size_t)col * n;
-      for (int j = col + 1 + warp; j < r; j += nw) {
-        double2 dot = cd(0.0, 0.0);
-        for (int k = col + lane; k < n; k += 32) zfmac(dot, wrow[k], v[(size_t)j * n + k]);
+      const double2* wrow = sw;
+      // two columns per warp pass so the two shuffle-reduction chains overlap
+      for (int j0 = col + 1 + warp; j0 < r; j0 += 2 * nw) {
+        const int j1 = j0 + nw;
+        const bool two = j1 < r;
+        double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+        for (int k = col + lane; k < n; k += 32) {
+          const double2 wk = wrow[k];
+          zfmac(d0, wk, v[(size_t)j0 * n + k]);
+          if (two) zfmac(d1, wk, v[(size_t)j1 * n + k]);
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
-          dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
+          d0.x += __shfl_xor_sync(0xffffffffu, d0.x, o);
+          d0.y += __shfl_xor_sync(0xffffffffu, d0.y, o);
+          d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
+          d1.y += __shfl_xor_sync(0xffffffffu, d1.y, o);
         }
-        const double2 f = cmul(tv, dot);
-        for (int k = col + lane; k < n; k += 32) v[(size_t)j * n + k] = v[(size_t)j * n + k] - cmul(wrow[k], f);
+        const double2 f0 = cmul(tv, d0), f1 = cmul(tv, d1);
+        for (int k = col + lane; k < n; k += 32) {
+          const double2 wk = wrow[k];
+          v[(size_t)j0 * n + k] = v[(size_t)j0 * n + k] - cmul(wk, f0);
+          if (two) v[(size_t)j1 * n + k] = v[(size_t)j1 * n + k] - cmul(wk, f1);
+        }
       }
     }
     __syncthreads();
@@ -439,7 +455,9 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
 }
 
 // B <- H_0^H ... applied for col = r-1 .. 0: block -= conj(tau) w (w^H block).
-// One warp per column of B; the column lives in shared memory.
+// One warp per column of B (held in shared memory); the reflectors stream
+// through shared memory in chunks so each is read from L2 once per CTA.
+constexpr int kReflChunk = 8;
 __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
                                         const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
                                         double2* __restrict__ B, float2* __restrict__ out32, int p) {
@@ -447,12 +465,27 @@ __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict_
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* b = sb + (size_t)warp * n;
-  for (int j = blockIdx.x * warps + warp; j < cols; j += gridDim.x * warps) {
+  double2* ws = sb + (size_t)warps * n;  // kReflChunk reflectors
+  __shared__ double2 ts[kReflChunk];
+  __shared__ int fs[kReflChunk];
+  const int j = blockIdx.x * warps + warp;
+  const bool active = j < cols;
+  if (active)
     for (int k = lane; k < n; k += 32) b[k] = Bin[(size_t)k * cols + j];
-    __syncwarp();
-    for (int col = r - 1; col >= 0; --col) {
-      if (!flags[col]) continue;
-      const double2* w = refl + (size_t)col * n;
+  for (int c1 = r - 1; c1 >= 0; c1 -= kReflChunk) {
+    const int c0 = max(0, c1 - kReflChunk + 1);
+    __syncthreads();
+    for (int q = threadIdx.x; q < (c1 - c0 + 1) * n; q += blockDim.x)
+      ws[q] = refl[(size_t)(c0 + q / n) * n + q % n];
+    for (int q = threadIdx.x; q <= c1 - c0; q += blockDim.x) {
+      ts[q] = tau[c0 + q];
+      fs[q] = flags[c0 + q];
+    }
+    __syncthreads();
+    if (!active) continue;
+    for (int col = c1; col >= c0; --col) {
+      if (!fs[col - c0]) continue;
+      const double2* w = ws + (size_t)(col - c0) * n;
       double2 dot = cd(0.0, 0.0);
       for (int k = col + lane; k < n; k += 32) zfmac(dot, w[k], b[k]);
 #pragma unroll
@@ -460,19 +493,19 @@ __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict_
         dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
         dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
       }
-      const double2 f = cmulc(tau[col], dot);  // conj(tau) * dot
+      const double2 f = cmulc(ts[col - c0], dot);  // conj(tau) * dot
       for (int k = col + lane; k < n; k += 32) b[k] = b[k] - cmul(w[k], f);
       __syncwarp();
     }
-    for (int k = lane; k < n; k += 32) {
-      const double2 v = b[k];
-      B[(size_t)k * cols + j] = v;
-      if (out32) {
-        const int step = j / p, t = j % p;
-        out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
-      }
+  }
+  if (!active) return;
+  for (int k = lane; k < n; k += 32) {
+    const double2 v = b[k];
+    B[(size_t)k * cols + j] = v;
+    if (out32) {
+      const int step = j / p, t = j % p;
+      out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
     }
-    __syncwarp();
   }
 }
 
@@ -545,8 +578,12 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const size_t bytes = (size_t)ell * ell * sizeof(double2);
     const bool sm = bytes <= kSmemCap;
-    hicu_allow_max_smem((const void*)chol_kernel);
-    chol_kernel<<<1, 1024, sm ? bytes : 0, st>>>(ell, w.C, w.O, Gp, n, w.scratch, sm, w.nu, status_dev);
+    if (sm) {
+      hicu_allow_max_smem((const void*)chol_kernel<true>);
+      chol_kernel<true><<<1, 512, bytes, st>>>(ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
+    } else {
+      chol_kernel<false><<<1, 512, 0, st>>>(ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
+    }
     if ((s = hicu_check_launch("chol_kernel"))) return s;
   }
   {
@@ -577,7 +614,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
   if (r == 0) return HICU_OK;
   if (!V) return hicu_set_error(HICU_ERR_PARAMETER, "householder: null V");
   const size_t bytes = (size_t)n * r * sizeof(double2);
-  const bool sm = bytes <= kSmemCap;
+  const bool sm = bytes + (size_t)n * sizeof(double2) <= kSmemCap;
   void* gws = nullptr;
   if (!sm) {
     // large V: work in place in the caller's refl buffer is not possible (different layout);
@@ -585,7 +622,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     gws = (double2*)refl + (size_t)n * r;
   }
   hicu_allow_max_smem((const void*)householder_kernel);
-  householder_kernel<<<1, 1024, sm ? bytes : 0, (cudaStream_t)stream>>>(
+  householder_kernel<<<1, 1024, (sm ? bytes : 0) + (size_t)n * sizeof(double2), (cudaStream_t)stream>>>(
       n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
   return hicu_check_launch("householder_kernel");
 }
@@ -595,8 +632,8 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
   if (n < 1 || r < 0 || cols < 1 || !B || !Bin) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad p");
   int warps = 8;
-  while (warps > 1 && (size_t)warps * n * sizeof(double2) > kSmemCap) warps >>= 1;
-  const size_t smem = (size_t)warps * n * sizeof(double2);
+  while (warps > 1 && (size_t)(warps + kReflChunk) * n * sizeof(double2) > kSmemCap) warps >>= 1;
+  const size_t smem = (size_t)(warps + kReflChunk) * n * sizeof(double2);
   if (smem > kSmemCap) return hicu_set_error(HICU_ERR_SIZE, "apply_reflectors: n too large");
   hicu_allow_max_smem((const void*)apply_reflectors_kernel);
   const int blocks = (cols + warps - 1) / warps;

@@ -28,40 +28,55 @@ __device__ __forceinline__ double2 warp_sum_z(double2 t) {
   return t;
 }
 
-// Householder reduction A = Q T Q^H (lower), one CTA.  Outputs d (l), e (l-1),
-// tau (l-1) and the reflectors transposed: Vt[k*l + i] = v_k[i] (v_k[k+1] = 1).
-__global__ void __launch_bounds__(1024)
-hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws, bool use_smem,
+// Householder reduction A = Q T Q^H (lower), one CTA of 512 threads.
+// Outputs d (l), e (l-1), tau (l-1) and the reflectors transposed:
+// Vt[k*l + i] = v_k[i] (v_k[k+1] = 1).  A is held with leading dimension
+// l+1 so column walks (lanes over rows) are bank-conflict free; the
+// matrix-vector product is row-parallel with j-chunk partials in shared memory
+// (no per-row shuffle reductions on the sequential critical path).
+template <bool SMEM>
+__global__ void __launch_bounds__(512)
+hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
              double* __restrict__ d, double* __restrict__ e, double2* __restrict__ tau,
              double2* __restrict__ Vt) {
   extern __shared__ double2 sA[];
-  double2* A = use_smem ? sA : Aws;
+  double2* A = SMEM ? sA : Aws;
+  const int lda = l + 1;
   __shared__ double2 sv[256], sw[256];
+  __shared__ double2 part[4][256];
+  __shared__ double redd[32];
+  __shared__ double2 redz[16];
   __shared__ double2 s_tau, s_scal, s_alpha2;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int q = tid; q < l * l; q += blockDim.x) A[q] = Ain[q];
-  for (int q = tid; q < l * l; q += blockDim.x) Vt[q] = cd(0.0, 0.0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  for (int q = tid; q < l * l; q += nt) A[(size_t)(q / l) * lda + q % l] = Ain[q];
+  for (int q = tid; q < l * l; q += nt) Vt[q] = cd(0.0, 0.0);
   __syncthreads();
   for (int k = 0; k + 1 < l; ++k) {
+    const int k1 = k + 1, m = l - k1;
+    // ---- column norm of A[k+2:, k] (warp 0, smem partials) and the reflector ----
     if (warp == 0) {
       double t = 0.0;
-      for (int i = k + 2 + lane; i < l; i += 32) t += abs2d(A[(size_t)i * l + k]);
-      t = warp_sum_d(t);
+      for (int i = k + 2 + lane; i < l; i += 32) t += abs2d(A[(size_t)i * lda + k]);
+      redd[lane] = t;
+      __syncwarp();
       if (lane == 0) {
-        const double2 alpha = A[(size_t)(k + 1) * l + k];
+        double tt = 0.0;
+        for (int q = 0; q < 32; ++q) tt += redd[q];
+        const double2 alpha = A[(size_t)k1 * lda + k];
         double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
         double beta;
-        if (t == 0.0 && alpha.y == 0.0) {
+        if (tt == 0.0 && alpha.y == 0.0) {
           beta = alpha.x;  // H = I
         } else {
-          beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + t), alpha.x);
-          tv = cd((beta - alpha.x) / beta, -alpha.y / beta);
+          beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + tt), alpha.x);
+          const double ib = 1.0 / beta;
+          tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
           const double2 den = cd(alpha.x - beta, alpha.y);
-          const double dd = abs2d(den);
-          scal = cd(den.x / dd, -den.y / dd);  // 1 / (alpha - beta)
+          const double idd = 1.0 / abs2d(den);
+          scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
         }
         e[k] = beta;
-        d[k] = A[(size_t)k * l + k].x;
+        d[k] = A[(size_t)k * lda + k].x;
         tau[k] = tv;
         s_tau = tv;
         s_scal = scal;
@@ -70,47 +85,63 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws, 
     __syncthreads();
     const double2 tk = s_tau;
     const double2 sc = s_scal;
-    for (int i = k + 1 + tid; i < l; i += blockDim.x) {
-      const double2 v = (i == k + 1) ? cd(1.0, 0.0) : cmul(A[(size_t)i * l + k], sc);
+    for (int i = k1 + tid; i < l; i += nt) {
+      const double2 v = (i == k1) ? cd(1.0, 0.0) : cmul(A[(size_t)i * lda + k], sc);
       sv[i] = v;
       Vt[(size_t)k * l + i] = v;
     }
     __syncthreads();
     if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform
-    // w = tau * A22 v
-    for (int i = k + 1 + warp; i < l; i += nw) {
-      double2 acc = cd(0.0, 0.0);
-      for (int j = k + 1 + lane; j < l; j += 32) zfma(acc, A[(size_t)i * l + j], sv[j]);
-      acc = warp_sum_z(acc);
-      if (lane == 0) sw[i] = cmul(tk, acc);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      double2 dot = cd(0.0, 0.0);
-      for (int i = k + 1 + lane; i < l; i += 32) zfmac(dot, sw[i], sv[i]);
-      dot = warp_sum_z(dot);
-      if (lane == 0) {
-        const double2 td = cmul(tk, dot);
-        s_alpha2 = cd(-0.5 * td.x, -0.5 * td.y);
+    // ---- y = A22 v: thread (row, chunk), 4 chunks over j ----
+    {
+      const int nchunk = 4, rows_per = nt / nchunk;  // 128 rows per pass
+      const int c = tid / rows_per, rr = tid % rows_per;
+      const int clen = (m + nchunk - 1) / nchunk;
+      const int j0 = k1 + c * clen, j1 = min(l, j0 + clen);
+      for (int i = k1 + rr; i < l; i += rows_per) {
+        double2 acc = cd(0.0, 0.0);
+        const double2* Ai = A + (size_t)i * lda;
+        for (int j = j0; j < j1; ++j) zfma(acc, Ai[j], sv[j]);
+        part[c][i] = acc;
       }
     }
     __syncthreads();
-    const double2 a2 = s_alpha2;
-    for (int i = k + 1 + tid; i < l; i += blockDim.x) sw[i] = sw[i] + cmul(a2, sv[i]);
+    // ---- w = tau * y; alpha2 = -tau/2 (w^H v) ----
+    {
+      double2 pz = cd(0.0, 0.0);
+      for (int i = k1 + tid; i < l; i += nt) {
+        const double2 y = part[0][i] + part[1][i] + part[2][i] + part[3][i];
+        const double2 wv = cmul(tk, y);
+        sw[i] = wv;
+        zfmac(pz, wv, sv[i]);
+      }
+      // m <= 255 < nt: at most 8 warps hold non-zero partials
+      pz = warp_sum_z(pz);
+      if (lane == 0 && warp < 16) redz[warp] = pz;
+    }
     __syncthreads();
-    // A22 -= v w^H + w v^H
-    for (int i = k + 1 + warp; i < l; i += nw) {
-      const double2 vi = sv[i], wi = sw[i];
-      for (int j = k + 1 + lane; j < l; j += 32) {
-        const double2 vj = sv[j], wj = sw[j];
-        double2 a = A[(size_t)i * l + j];
-        a = a - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
-        A[(size_t)i * l + j] = a;
+    if (tid == 0) {
+      double2 dot = cd(0.0, 0.0);
+      for (int q = 0; q < 16; ++q) dot = dot + redz[q];
+      const double2 td = cmul(tk, dot);
+      s_alpha2 = cd(-0.5 * td.x, -0.5 * td.y);
+    }
+    __syncthreads();
+    // ---- A22 -= v w'^H + w' v^H with w' = w + alpha2 v (formed on the fly) ----
+    const double2 a2 = s_alpha2;
+    for (int i = k1 + warp; i < l; i += nt / 32) {
+      const double2 vi = sv[i];
+      const double2 wi = sw[i] + cmul(a2, vi);
+      double2* Ai = A + (size_t)i * lda;
+      for (int j = k1 + lane; j < l; j += 32) {
+        const double2 vj = sv[j];
+        const double2 wj = sw[j] + cmul(a2, vj);
+        Ai[j] = Ai[j] - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
       }
     }
     __syncthreads();
   }
-  if (tid == 0) d[l - 1] = A[(size_t)(l - 1) * l + (l - 1)].x;
+  if (tid == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
 }
 
 // Sturm count: number of eigenvalues of T (d, e2 = e^2) strictly below x.
@@ -177,85 +208,94 @@ __global__ void stebz_kernel(int l, int r, const double* __restrict__ dg, const 
 }
 
 // Inverse iteration: one thread per eigenvalue; (T - lam I) LU with partial
-// pivoting (dgttrf form), 4 solves from a deterministic start vector.
-// z is l x r column-major (z[j*l + i]); scratch 5*l doubles per thread.
+// pivoting (dgttrf form), 3 solves from a deterministic start vector.  The
+// per-thread factors live in shared memory, interleaved by thread
+// (element i of thread t at [i*T + t]) so a warp's accesses hit distinct banks.
+// z is l x r column-major (z[j*l + i]).
 __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const double* __restrict__ e,
-                             const double* __restrict__ lam, double* __restrict__ z, double* __restrict__ scratch) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+                             const double* __restrict__ lam, double* __restrict__ z) {
+  extern __shared__ double sm[];
+  __shared__ double sd[256], se[256];
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int i = t; i < l; i += T) {
+    sd[i] = d[i];
+    se[i] = (i + 1 < l) ? e[i] : 0.0;
+  }
+  __syncthreads();
+  const int j = blockIdx.x * T + t;
   if (j >= r) return;
-  double* dl = scratch + (size_t)j * 5 * l;  // multipliers
-  double* u0 = dl + l;                       // U diagonal
-  double* u1 = u0 + l;                       // U super-diagonal
-  double* u2 = u1 + l;                       // U second super-diagonal (pivoting fill)
-  double* ip = u2 + l;                       // 1.0 when rows i, i+1 were swapped
+  double* dl = sm;                    // multipliers
+  double* u0 = dl + (size_t)l * T;    // U diagonal
+  double* u1 = u0 + (size_t)l * T;    // U super-diagonal
+  double* u2 = u1 + (size_t)l * T;    // U second super-diagonal
+  double* x = u2 + (size_t)l * T;     // iterate
+  unsigned long long swaps[4] = {0ull, 0ull, 0ull, 0ull};  // row-swap bits (l <= 256)
+#define AT(arr, i) arr[(size_t)(i) * T + t]
   const double lj = lam[j];
   double tnorm = 0.0;
   for (int i = 0; i < l; ++i)
-    tnorm = fmax(tnorm, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < l ? fabs(e[i]) : 0.0));
+    tnorm = fmax(tnorm, fabs(sd[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + fabs(se[i]));
   const double tiny = 2.2e-16 * fmax(tnorm, 1e-300);
-  // factor (dgttrf) with sub = super = e
   for (int i = 0; i < l; ++i) {
-    u0[i] = d[i] - lj;
-    u1[i] = (i + 1 < l) ? e[i] : 0.0;
-    u2[i] = 0.0;
-    ip[i] = 0.0;
+    AT(u0, i) = sd[i] - lj;
+    AT(u1, i) = se[i];
+    AT(u2, i) = 0.0;
   }
   for (int i = 0; i + 1 < l; ++i) {
-    const double sub = e[i];
-    if (fabs(u0[i]) >= fabs(sub)) {
-      const double f = (u0[i] != 0.0) ? sub / u0[i] : 0.0;
-      dl[i] = f;
-      u0[i + 1] -= f * u1[i];
+    const double sub = se[i];
+    const double ui = AT(u0, i);
+    if (fabs(ui) >= fabs(sub)) {
+      const double f = (ui != 0.0) ? sub / ui : 0.0;
+      AT(dl, i) = f;
+      AT(u0, i + 1) -= f * AT(u1, i);
     } else {
-      // swap rows i and i+1
-      const double f = u0[i] / sub;
-      u0[i] = sub;
-      const double t = u0[i + 1];
-      u0[i + 1] = u1[i] - f * t;
-      u1[i] = t;
+      const double f = ui / sub;
+      AT(u0, i) = sub;
+      const double tt = AT(u0, i + 1);
+      AT(u0, i + 1) = AT(u1, i) - f * tt;
+      AT(u1, i) = tt;
       if (i + 2 < l) {
-        u2[i] = u1[i + 1];
-        u1[i + 1] = -f * u2[i];
+        AT(u2, i) = AT(u1, i + 1);
+        AT(u1, i + 1) = -f * AT(u2, i);
       }
-      dl[i] = f;
-      ip[i] = 1.0;
+      AT(dl, i) = f;
+      swaps[i >> 6] |= 1ull << (i & 63);
     }
   }
-  for (int i = 0; i < l; ++i)
-    if (fabs(u0[i]) < tiny) u0[i] = (u0[i] < 0.0 ? -tiny : tiny);
-  double* x = z + (size_t)j * l;
-  // deterministic, eigenvalue-dependent start vector
-  unsigned s = 2654435761u * (unsigned)(j + 1);
   for (int i = 0; i < l; ++i) {
-    s = s * 1664525u + 1013904223u;
-    x[i] = 1.0 + 0.5 * ((double)(s >> 8) / 16777216.0 - 0.5);
+    const double v = AT(u0, i);
+    if (fabs(v) < tiny) AT(u0, i) = (v < 0.0 ? -tiny : tiny);
   }
-  for (int itn = 0; itn < 4; ++itn) {
-    // apply L^{-1} (with the recorded row swaps)
+  unsigned sd0 = 2654435761u * (unsigned)(j + 1);
+  for (int i = 0; i < l; ++i) {
+    sd0 = sd0 * 1664525u + 1013904223u;
+    AT(x, i) = 1.0 + 0.5 * ((double)(sd0 >> 8) / 16777216.0 - 0.5);
+  }
+  for (int itn = 0; itn < 3; ++itn) {
     for (int i = 0; i + 1 < l; ++i) {
-      if (ip[i] != 0.0) {
-        const double t = x[i];
-        x[i] = x[i + 1];
-        x[i + 1] = t - dl[i] * x[i];
+      if ((swaps[i >> 6] >> (i & 63)) & 1ull) {
+        const double tt = AT(x, i);
+        AT(x, i) = AT(x, i + 1);
+        AT(x, i + 1) = tt - AT(dl, i) * AT(x, i);
       } else {
-        x[i + 1] -= dl[i] * x[i];
+        AT(x, i + 1) -= AT(dl, i) * AT(x, i);
       }
     }
-    // back substitution with U (3 diagonals)
+    double nrm = 0.0;
+    double xp1 = 0.0, xp2 = 0.0;
     for (int i = l - 1; i >= 0; --i) {
-      double v = x[i];
-      if (i + 1 < l) v -= u1[i] * x[i + 1];
-      if (i + 2 < l) v -= u2[i] * x[i + 2];
-      x[i] = v / u0[i];
-    }
-    double nrm = 0.0, mx = 0.0;
-    for (int i = 0; i < l; ++i) {
-      nrm += x[i] * x[i];
-      mx = fmax(mx, fabs(x[i]));
+      double v = AT(x, i) - AT(u1, i) * xp1 - AT(u2, i) * xp2;
+      v = v / AT(u0, i);
+      AT(x, i) = v;
+      xp2 = xp1;
+      xp1 = v;
+      nrm += v * v;
     }
     const double inv = 1.0 / sqrt(nrm);
-    for (int i = 0; i < l; ++i) x[i] *= inv;
+    for (int i = 0; i < l; ++i) AT(x, i) *= inv;
   }
+  for (int i = 0; i < l; ++i) z[(size_t)j * l + i] = AT(x, i);
+#undef AT
 }
 
 // Re-orthogonalise clusters (|lam_i - lam_j| <= ctol * |lam_0|) by CGS2 in
@@ -308,19 +348,33 @@ __global__ void __launch_bounds__(256) cluster_orth_kernel(int l, int r, const d
 }
 
 // F[:, j] = Q z_j with Q = H_0 H_1 ... H_{l-2}: apply H_{l-2} first.
-// One warp per eigenvector; F is l x r row-major (c128).
+// One CTA owns a group of eigenvectors (one warp each) and streams the
+// reflectors through shared memory in chunks, so each reflector is read from
+// L2 once per CTA instead of once per warp.  F is l x r row-major (c128).
+constexpr int kBtChunk = 16;
 __global__ void back_transform_kernel(int l, int r, const double2* __restrict__ Vt, const double2* __restrict__ tau,
                                       const double* __restrict__ z, double2* __restrict__ F) {
-  extern __shared__ double2 sx[];
+  extern __shared__ double2 sm2[];
   const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double2* x = sx + (size_t)warp * l;
-  for (int j = blockIdx.x * warps + warp; j < r; j += gridDim.x * warps) {
+  double2* x = sm2 + (size_t)warp * l;
+  double2* vs = sm2 + (size_t)warps * l;  // kBtChunk reflectors
+  __shared__ double2 ts[kBtChunk];
+  const int j = blockIdx.x * warps + warp;
+  const bool active = j < r;
+  if (active)
     for (int i = lane; i < l; i += 32) x[i] = cd(z[(size_t)j * l + i], 0.0);
-    __syncwarp();
-    for (int k = l - 2; k >= 0; --k) {
-      const double2 tk = tau[k];
+  for (int k1 = l - 2; k1 >= 0; k1 -= kBtChunk) {
+    const int k0 = max(0, k1 - kBtChunk + 1);
+    __syncthreads();
+    for (int q = threadIdx.x; q < (k1 - k0 + 1) * l; q += blockDim.x)
+      vs[q] = Vt[(size_t)(k0 + q / l) * l + q % l];
+    for (int q = threadIdx.x; q <= k1 - k0; q += blockDim.x) ts[q] = tau[k0 + q];
+    __syncthreads();
+    if (!active) continue;
+    for (int k = k1; k >= k0; --k) {
+      const double2 tk = ts[k - k0];
       if (tk.x == 0.0 && tk.y == 0.0) continue;
-      const double2* v = Vt + (size_t)k * l;
+      const double2* v = vs + (size_t)(k - k0) * l;
       double2 dot = cd(0.0, 0.0);
       for (int i = k + 1 + lane; i < l; i += 32) zfmac(dot, v[i], x[i]);
       dot = warp_sum_z(dot);
@@ -328,16 +382,16 @@ __global__ void back_transform_kernel(int l, int r, const double2* __restrict__ 
       for (int i = k + 1 + lane; i < l; i += 32) x[i] = x[i] - cmul(v[i], f);
       __syncwarp();
     }
-    for (int i = lane; i < l; i += 32) F[(size_t)i * r + j] = x[i];
-    __syncwarp();
   }
+  if (active)
+    for (int i = lane; i < l; i += 32) F[(size_t)i * r + j] = x[i];
 }
 
 }  // namespace
 
 size_t hicu_heev_top_workspace(int l, int r) {
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
-  return al((size_t)l * l * sizeof(double2)) * 2 + al((size_t)l * sizeof(double)) * 2 +
+  return al((size_t)l * (l + 1) * sizeof(double2)) * 2 + al((size_t)l * sizeof(double)) * 2 +
          al((size_t)l * sizeof(double2)) + al((size_t)r * sizeof(double)) + al((size_t)l * r * sizeof(double)) +
          al((size_t)5 * l * r * sizeof(double));
 }
@@ -347,30 +401,39 @@ size_t hicu_heev_top_workspace(int l, int r) {
 int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void* ws, cudaStream_t st) {
   auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
   char* p = (char*)ws;
-  double2* Aws = (double2*)p;   p += al((size_t)l * l * sizeof(double2));
-  double2* Vt = (double2*)p;    p += al((size_t)l * l * sizeof(double2));
+  double2* Aws = (double2*)p;   p += al((size_t)l * (l + 1) * sizeof(double2));
+  double2* Vt = (double2*)p;    p += al((size_t)l * (l + 1) * sizeof(double2));
   double* d = (double*)p;       p += al((size_t)l * sizeof(double));
   double* e = (double*)p;       p += al((size_t)l * sizeof(double));
   double2* tau = (double2*)p;   p += al((size_t)l * sizeof(double2));
   double* lam_s = (double*)p;   p += al((size_t)r * sizeof(double));
   double* z = (double*)p;       p += al((size_t)l * r * sizeof(double));
-  double* scratch = (double*)p;
   (void)lam_s;
   int s;
-  const size_t abytes = (size_t)l * l * sizeof(double2);
-  const bool sm = abytes <= 200 * 1024;
-  hicu_allow_max_smem((const void*)hetrd_kernel);
-  hetrd_kernel<<<1, 1024, sm ? abytes : 0, st>>>(l, A, Aws, sm, d, e, tau, Vt);
+  const size_t abytes = (size_t)l * (l + 1) * sizeof(double2);
+  const bool sm = abytes <= 180 * 1024;
+  if (sm) {
+    hicu_allow_max_smem((const void*)hetrd_kernel<true>);
+    hetrd_kernel<true><<<1, 512, abytes, st>>>(l, A, Aws, d, e, tau, Vt);
+  } else {
+    hetrd_kernel<false><<<1, 512, 0, st>>>(l, A, Aws, d, e, tau, Vt);
+  }
   if ((s = hicu_check_launch("hetrd_kernel"))) return s;
   const int wpb = 8;
   stebz_kernel<<<(r + wpb - 1) / wpb, wpb * 32, 0, st>>>(l, r, d, e, lam);
   if ((s = hicu_check_launch("stebz_kernel"))) return s;
-  stein_kernel<<<(r + 63) / 64, 64, 0, st>>>(l, r, d, e, lam, z, scratch);
+  {
+    int T = 32;
+    while (T > 1 && (size_t)5 * l * T * sizeof(double) > 200 * 1024) T >>= 1;
+    const size_t smem = (size_t)5 * l * T * sizeof(double);
+    hicu_allow_max_smem((const void*)stein_kernel);
+    stein_kernel<<<(r + T - 1) / T, T, smem, st>>>(l, r, d, e, lam, z);
+  }
   if ((s = hicu_check_launch("stein_kernel"))) return s;
   cluster_orth_kernel<<<1, 256, 0, st>>>(l, r, lam, z, 1e-9);
   if ((s = hicu_check_launch("cluster_orth_kernel"))) return s;
-  const int bw = 4;
-  const size_t smem = (size_t)bw * l * sizeof(double2);
+  const int bw = 8;
+  const size_t smem = ((size_t)bw * l + (size_t)kBtChunk * l) * sizeof(double2);
   hicu_allow_max_smem((const void*)back_transform_kernel);
   back_transform_kernel<<<(r + bw - 1) / bw, bw * 32, smem, st>>>(l, r, Vt, tau, z, F);
   return hicu_check_launch("back_transform_kernel");

@@ -65,6 +65,7 @@ typedef struct hicu_geom {
 } hicu_geom;
 
 #define HICU_GEOM_COIL_SEPARABLE 1
+#define HICU_GEOM_FORCE_SIMT_GRAM 2   /* use the SIMT Gram even when tcgen05 applies */
 
 /* Per-step scalar record written by hicu_step_update (doubles). */
 enum {
@@ -142,6 +143,9 @@ int hicu_ser_parts(int64_t N, const void* ref, const void* y, double* ser_parts,
 /* G = H(x)^H H(x), n x n c128 Hermitian (full storage).  No reference
  * function; equals hankel_adjoint_apply(x, hankel_apply(x, I)). */
 size_t hicu_gram_workspace(const hicu_geom* g);
+/* 1 when hicu_gram runs the tcgen05 3xTF32 kernel for this geometry (coil-
+ * separable support with 8 coils, no circular axes, >= 8 spatial taps). */
+int hicu_gram_uses_tensor_cores(const hicu_geom* g);
 int hicu_gram(const hicu_geom* g, const void* x, void* G, void* ws,
               size_t ws_bytes, void* stream);
 

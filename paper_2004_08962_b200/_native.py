@@ -19,6 +19,7 @@ MAX_NDIM = 8
 REC_OBJ, REC_NUM, REC_DEN, REC_ETA, REC_OBJ_AFTER, REC_GNORM2, REC_DEGENERATE, REC_TIME = range(8)
 REC_SLOTS = 8
 GEOM_COIL_SEPARABLE = 1
+GEOM_FORCE_SIMT_GRAM = 2
 PROF_KINDS = ("gram", "nystrom", "householder", "conv_fwd", "scatter", "conv_els", "update")
 
 
@@ -77,6 +78,7 @@ _SIGS = {
     "hicu_soft_terms": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int),
                                 c_void_p]),
     "hicu_gram_workspace": (c_size_t, [_GP]),
+    "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
     "hicu_gram": (c_int, [_GP, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hicu_zgemm": (c_int, [c_char, c_char, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,
                            c_void_p]),

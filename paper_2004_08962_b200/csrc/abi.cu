@@ -10,6 +10,9 @@
 #include "common.cuh"
 
 size_t hicu_gram_simt_workspace(const DevGeom& g);
+bool hicu_gram_tc_supported(const DevGeom& g);
+size_t hicu_gram_tc_workspace(const DevGeom& g);
+int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st);
 int hicu_gram_simt(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st);
 
 #include <atomic>
@@ -143,10 +146,22 @@ extern "C" int hicu_device_sm_count(int* out) {
   return HICU_OK;
 }
 
+static bool use_tc(const hicu_geom* hg, const DevGeom& g) {
+  return !(hg->flags & HICU_GEOM_FORCE_SIMT_GRAM) && hicu_gram_tc_supported(g);
+}
+
 extern "C" size_t hicu_gram_workspace(const hicu_geom* hg) {
   DevGeom g;
   if (hicu_make_devgeom(hg, &g)) return 0;
-  return hicu_gram_simt_workspace(g);
+  const size_t a = hicu_gram_simt_workspace(g);
+  const size_t b = use_tc(hg, g) ? hicu_gram_tc_workspace(g) : 0;
+  return a > b ? a : b;
+}
+
+extern "C" int hicu_gram_uses_tensor_cores(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return 0;
+  return use_tc(hg, g) ? 1 : 0;
 }
 
 extern "C" int hicu_gram(const hicu_geom* hg, const void* x, void* G, void* ws, size_t ws_bytes, void* stream) {
@@ -154,5 +169,6 @@ extern "C" int hicu_gram(const hicu_geom* hg, const void* x, void* G, void* ws, 
   DevGeom g;
   int s = hicu_make_devgeom(hg, &g);
   if (s) return s;
+  if (use_tc(hg, g)) return hicu_gram_tc(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
   return hicu_gram_simt(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
 }

@@ -1,0 +1,447 @@
+// Gram matrix G = H(x)^H H(x) on the 5th-generation tensor cores (tcgen05,
+// kind::tf32, 3xTF32 split for FP32-grade accuracy), implicit im2col.
+//
+// Real embedding: H_real (s x 2n) holds, for region row i and kernel column
+// kappa = tap*Nc + c, the floats (re, im) of X[i + pos(kappa)].  For a
+// coil-separable support the 2*Nc = 16 floats of one spatial tap are
+// contiguous in k-space, so G_real = H_real^T H_real is a GEMM over rows i
+// (K) whose M/N operands are tap columns:
+//   D[mu, nu] += sum_i A[mu, i] B[nu, i],  A = H_real[:, M tile]^T, B = H_real[:, N tile]^T
+// G[k1,k2] = (G_rr + G_ii) + i (G_ri - G_ir) is assembled in fp64 by the
+// split-K reduction kernel (only tile pairs holding k1 <= k2 are computed).
+//
+// 3xTF32: x = hi + lo, hi = rna_tf32(x); D += A_hi B_hi + A_hi B_lo + A_lo B_hi.
+//
+// Accumulation accuracy: tcgen05 fp32 accumulation loses precision in
+// proportion to the number of MMAs chained into one accumulator (measured on
+// C2: 1.5e-5 relative after ~650 chained MMAs, 1.5e-6 after ~50).  Each CTA
+// therefore alternates two TMEM accumulators (256 columns each) in chains of
+// kChain k-blocks; 16 epilogue warps drain a finished chain with tcgen05.ld
+// and add it into fp32 registers (round-to-nearest) while the tensor core
+// fills the other buffer.
+//
+// Operands are staged K-major (canonical no-swizzle core matrices, LBO 128 B,
+// SBO 256 B): MN-major tf32 operands returned all-zero results on this part
+// in a unit test (scripts/tc_unit.cu).  Producer warps gather the 16 floats x
+// 16 rows of every tap of the tile, split hi/lo on the fly and write 16-byte
+// K-major chunks.
+//
+// Warp roles (672 threads): warps 0-3 producers, warp 4 TMEM owner + MMA
+// issuer (one lane), warps 5-20 epilogue (TMEM lane quarter = warp % 4,
+// 64-column group = (warp - 5) / 4).
+//
+// Scope: coil-separable support with Nc = 8 (16 floats per tap), no circular
+// axes, <= 3 spatial axes, 8..128 spatial taps.  Other geometries use the SIMT
+// kernel (gram_simt.cu).
+#include <stdlib.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kBK = 16;           // rows (K) per pipeline stage: 2 MMA k-steps of 8
+constexpr int kMT = 8;            // taps per M tile  (M = 128 real columns)
+constexpr int kNT = 16;           // taps per N tile  (N <= 256 real columns)
+constexpr int kChain = 4;         // k-blocks per TMEM accumulation chain
+constexpr int kProducers = 128;
+constexpr int kEpiWarps = 16;
+constexpr int kThreads = (4 + 1 + kEpiWarps) * 32;
+constexpr int kMaxStages = 6;
+constexpr int kPartCols = 256;
+constexpr int kMaxPairs = 160;
+
+struct TcParams {
+  int T;                 // spatial taps
+  int nsp;               // spatial axes (1..3)
+  int64_t rext[3];       // region extents per spatial axis (last = K-contiguous)
+  int64_t roff[3];
+  int64_t fstride[3];    // float strides of the spatial axes in the k-space array
+  int64_t nkb_line;      // k-blocks per region line
+  int64_t nkb;           // total k-blocks
+  int64_t kb_per_split;
+  int npairs;
+  int stages;
+  unsigned char pair_m[kMaxPairs], pair_n[kMaxPairs];  // tile pair -> (m tile, n tile)
+};
+
+struct PairTable {
+  short v[16 * 8];  // [m tile][n tile] -> pair index or -1
+};
+
+__host__ __device__ __forceinline__ int64_t hmin64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+__host__ __device__ __forceinline__ int mtile_first_tap(int m, int T) {
+  const int f = m * kMT;
+  return (f + kMT > T) ? T - kMT : f;  // last tile shifted back so it stays full
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major no-swizzle descriptor: core matrix = 8 MN rows x 16 B, LBO = next 4 K, SBO = next 8 MN rows.
+__device__ __forceinline__ uint64_t make_desc_kmajor(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm100)
+  return d;                // layout type 0: no swizzle
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, A and B K-major.
+__device__ __forceinline__ uint32_t make_idesc_tf32(int M, int N) {
+  uint32_t d = 0;
+  d |= 1u << 4;   // D format F32
+  d |= 2u << 7;   // A format TF32
+  d |= 2u << 10;  // B format TF32
+  d |= (uint32_t)(N >> 3) << 17;
+  d |= (uint32_t)(M >> 4) << 24;
+  return d;
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16_raw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// Stage layout (per hi/lo half): for k-step ks (8 rows), tap q of the list,
+// MN row j (0..15), row k: ks*list*512 + (2q + j/8)*256 + ((k%8)/4)*128 + (j%8)*16 + (k%4)*4.
+__global__ void __launch_bounds__(kThreads, 1)
+gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ tap_off, float* __restrict__ part) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x, split = blockIdx.y;
+  const int T = p.T;
+  const int m0 = mtile_first_tap(p.pair_m[pair], T);
+  const int n0 = p.pair_n[pair] * kNT;
+  const int NT = min(kNT, T - n0);
+  const bool a_inside = (m0 >= n0) && (m0 + kMT <= n0 + NT);
+  const int list = NT + (a_inside ? 0 : kMT);
+  const int a_off = a_inside ? (m0 - n0) : NT;
+  const uint32_t half_bytes = (uint32_t)(list * 2 * 512);
+  const uint32_t stage_bytes = 2 * half_bytes;
+  const int64_t kb0 = (int64_t)split * p.kb_per_split;
+  const int64_t kb1 = hmin64(p.nkb, kb0 + p.kb_per_split);
+  const int nkb = (int)(kb1 > kb0 ? kb1 - kb0 : 0);
+  const int nchains = (nkb + kChain - 1) / kChain;
+  const int S = p.stages;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], kProducers);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- producers: gather, split hi/lo, K-major stores ----------------
+    const int tid = threadIdx.x;
+    const int L = p.nsp - 1;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&empty_bar[s], ph ^ 1);
+      const int64_t line = kb / p.nkb_line;
+      const int chunk = (int)(kb % p.nkb_line);
+      int64_t base = 0;
+      {
+        int64_t rem = line;
+        for (int d = L - 1; d >= 0; --d) {
+          const int64_t c = rem % p.rext[d];
+          rem /= p.rext[d];
+          base += (p.roff[d] + c) * p.fstride[d];
+        }
+        base += (p.roff[L] + (int64_t)chunk * kBK) * 16;
+      }
+      const int valid = (int)hmin64(kBK, p.rext[L] - (int64_t)chunk * kBK);
+      uint8_t* sb = smem + (size_t)s * stage_bytes;
+      const int ntask = list * 64;
+#pragma unroll 2
+      for (int t = tid; t < ntask; t += kProducers) {
+        const int j = t & 15;
+        const int quad = (t >> 4) & 3;
+        const int q = t >> 6;
+        const int tap = (q < NT) ? n0 + q : m0 + (q - NT);
+        const float* src = x + base + tap_off[tap] + j + quad * 64;
+        float v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[r] = (quad * 4 + r < valid) ? __ldg(src + r * 16) : 0.f;
+        float h[4], l[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          uint32_t hb;
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v[r]));
+          h[r] = __uint_as_float(hb);
+          l[r] = v[r] - h[r];
+        }
+        const int ks = quad >> 1, kq = quad & 1;
+        const uint32_t off = (uint32_t)ks * list * 512 + (uint32_t)(2 * q + (j >> 3)) * 256 + (uint32_t)kq * 128 +
+                             (uint32_t)(j & 7) * 16;
+        *(float4*)(sb + off) = make_float4(h[0], h[1], h[2], h[3]);
+        *(float4*)(sb + half_bytes + off) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full_bar[s]);
+      if (++s == S) { s = 0; ph ^= 1; }
+    }
+  } else if (warp == 4) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc_tf32(128, 16 * NT);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int c = 0; c < nchains; ++c) {
+      const int b = c & 1;
+      mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem + (uint32_t)(256 * b);
+      bool first = true;
+      const int j1 = min(nkb, (c + 1) * kChain);
+      for (int j = c * kChain; j < j1; ++j) {
+        const int64_t kb = kb0 + j;
+        mbar_wait(&full_bar[s], ph);
+        tc_fence_after();
+        const int chunk = (int)(kb % p.nkb_line);
+        const int valid = (int)hmin64(kBK, p.rext[p.nsp - 1] - (int64_t)chunk * kBK);
+        const int nks = (valid + 7) / 8;
+        if (lane == 0) {
+          const uint32_t sbase = smem_u32(smem + (size_t)s * stage_bytes);
+          for (int ks = 0; ks < nks; ++ks) {
+            const uint32_t kbase = sbase + (uint32_t)ks * list * 512;
+            const uint64_t a_hi = make_desc_kmajor(kbase + (uint32_t)a_off * 512);
+            const uint64_t a_lo = make_desc_kmajor(kbase + half_bytes + (uint32_t)a_off * 512);
+            const uint64_t b_hi = make_desc_kmajor(kbase);
+            const uint64_t b_lo = make_desc_kmajor(kbase + half_bytes);
+            umma_tf32(dcol, a_hi, b_hi, idesc, first ? 0u : 1u);
+            umma_tf32(dcol, a_hi, b_lo, idesc, 1u);
+            umma_tf32(dcol, a_lo, b_hi, idesc, 1u);
+            first = false;
+          }
+          umma_commit(&empty_bar[s]);
+        }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull[b]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue: drain chains into fp32 registers ----------------
+    const int ew = warp - 5;
+    const int q4 = warp & 3;  // TMEM lane quarter
+    const int grp = ew >> 2;  // 64-column group
+    const int row = 32 * q4 + lane;
+    const int c0 = 64 * grp;
+    const int ncols = max(0, min(64, 16 * NT - c0));
+    float acc[64];
+#pragma unroll
+    for (int q = 0; q < 64; ++q) acc[q] = 0.f;
+    for (int c = 0; c < nchains; ++c) {
+      const int b = c & 1;
+      mbar_wait(&tfull[b], (c >> 1) & 1);
+      tc_fence_after();
+      if (ncols > 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r[16];
+          tmem_ld16_raw(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(256 * b + c0 + 16 * i), r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[16 * i + q] += __uint_as_float(r[q]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+    float* dst = part + ((size_t)pair * gridDim.y + split) * 128 * kPartCols + (size_t)row * kPartCols + c0;
+#pragma unroll
+    for (int q = 0; q < 64; q += 4)
+      if (q < ncols) *(float4*)(dst + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// G[k1][k2] (k1 <= k2) from the real partials: (rr + ii) + i (ri - ir), summed
+// over splits in fp64 in a fixed order; mirrored conjugate below the diagonal.
+__global__ void gram_tc_reduce_kernel(int n, int nc, int T, int splits, PairTable pt, int ntn,
+                                      const float* __restrict__ part, double2* __restrict__ G) {
+  const int64_t total = (int64_t)n * n;
+  const size_t blk = (size_t)128 * kPartCols;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int k1 = (int)(e / n), k2 = (int)(e % n);
+    if (k1 > k2) continue;
+    const int t1 = k1 / nc, c1 = k1 % nc, t2 = k2 / nc, c2 = k2 % nc;
+    int mt = t1 / kMT;
+    while (mtile_first_tap(mt, T) > t1) --mt;  // first tile containing t1
+    const int lt1 = t1 - mtile_first_tap(mt, T);
+    const int nt = t2 / kNT, lt2 = t2 - nt * kNT;
+    const int pr = pt.v[mt * ntn + nt];
+    const int mu = (lt1 * nc + c1) * 2, nu = (lt2 * nc + c2) * 2;
+    double rr = 0.0, ii = 0.0, ri = 0.0, ir = 0.0;
+    for (int sp = 0; sp < splits; ++sp) {
+      const float* b = part + ((size_t)pr * splits + sp) * blk;
+      rr += b[(size_t)mu * kPartCols + nu];
+      ri += b[(size_t)mu * kPartCols + nu + 1];
+      ir += b[(size_t)(mu + 1) * kPartCols + nu];
+      ii += b[(size_t)(mu + 1) * kPartCols + nu + 1];
+    }
+    const double gr = rr + ii, gi = ri - ir;
+    if (k1 == k2) {
+      G[e] = cd(gr, 0.0);
+    } else {
+      G[e] = cd(gr, gi);
+      G[(size_t)k2 * n + k1] = cd(gr, -gi);
+    }
+  }
+}
+
+// per tap: flat float offset of its coil-0 sample relative to the row base (= 2*koff)
+__global__ void tc_tap_table_kernel(int T, int nc, const int64_t* __restrict__ koff, int* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < T) out[t] = (int)(2 * koff[(size_t)t * nc]);
+}
+
+struct TcPlan {
+  bool ok = false;
+  TcParams p;
+  PairTable pt;
+  int splits = 0;
+  int mtiles = 0, ntiles = 0;
+  size_t part_bytes = 0, smem_bytes = 0;
+};
+
+TcPlan tc_plan(const DevGeom& g) {
+  TcPlan pl;
+  if (g.nc != 8 || g.ncirc != 0) return pl;
+  const int nsp = g.ndim - 1;
+  if (nsp < 1 || nsp > 3) return pl;
+  const int T = g.nsp;
+  if (T < kMT || T > 128) return pl;
+  TcParams& p = pl.p;
+  p.T = T;
+  p.nsp = nsp;
+  for (int d = 0; d < 3; ++d) {
+    p.rext[d] = d < nsp ? g.rext[d] : 1;
+    p.roff[d] = d < nsp ? g.roff[d] : 0;
+    p.fstride[d] = d < nsp ? 2 * g.stride[d] : 0;
+  }
+  const int64_t rl = p.rext[nsp - 1];
+  p.nkb_line = (rl + kBK - 1) / kBK;
+  int64_t lines = 1;
+  for (int d = 0; d < nsp - 1; ++d) lines *= p.rext[d];
+  p.nkb = lines * p.nkb_line;
+  pl.mtiles = (T + kMT - 1) / kMT;
+  pl.ntiles = (T + kNT - 1) / kNT;
+  int np = 0;
+  for (int m = 0; m < pl.mtiles; ++m)
+    for (int nn = 0; nn < pl.ntiles; ++nn) {
+      const int mf = mtile_first_tap(m, T), nl = min(T, (nn + 1) * kNT) - 1;
+      pl.pt.v[m * pl.ntiles + nn] = -1;
+      if (mf <= nl) {  // the tile holds some k1 <= k2 entries
+        if (np >= kMaxPairs) return pl;
+        p.pair_m[np] = (unsigned char)m;
+        p.pair_n[np] = (unsigned char)nn;
+        pl.pt.v[m * pl.ntiles + nn] = (short)np++;
+      }
+    }
+  p.npairs = np;
+  int splits = (hicu_sm_count() + np - 1) / np;
+  if (splits > p.nkb) splits = (int)p.nkb;
+  if (splits < 1) splits = 1;
+  p.kb_per_split = (p.nkb + splits - 1) / splits;
+  pl.splits = (int)((p.nkb + p.kb_per_split - 1) / p.kb_per_split);
+  const size_t stage_bytes = (size_t)(kNT + kMT) * 2 * 1024;
+  int stages = (int)((200 * 1024) / stage_bytes);
+  if (stages > kMaxStages) stages = kMaxStages;
+  if (stages < 2) return pl;
+  p.stages = stages;
+  pl.smem_bytes = stages * stage_bytes + 1024;
+  pl.part_bytes = (size_t)np * pl.splits * 128 * kPartCols * sizeof(float);
+  pl.ok = true;
+  return pl;
+}
+
+}  // namespace
+
+bool hicu_gram_tc_supported(const DevGeom& g) { return tc_plan(g).ok; }
+
+size_t hicu_gram_tc_workspace(const DevGeom& g) {
+  TcPlan pl = tc_plan(g);
+  if (!pl.ok) return 0;
+  return pl.part_bytes + 4096;
+}
+
+int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st) {
+  TcPlan pl = tc_plan(g);
+  if (!pl.ok) return hicu_set_error(HICU_ERR_PARAMETER, "gram_tc: unsupported geometry");
+  if (ws_bytes < hicu_gram_tc_workspace(g)) return hicu_set_error(HICU_ERR_WORKSPACE, "gram_tc: workspace");
+  float* part = (float*)ws;
+  int* toff = (int*)((char*)ws + pl.part_bytes);
+  int s;
+  tc_tap_table_kernel<<<(g.nsp + 127) / 128, 128, 0, st>>>(g.nsp, g.nc, g.koff, toff);
+  if ((s = hicu_check_launch("tc_tap_table_kernel"))) return s;
+  hicu_allow_max_smem((const void*)gram_tc_kernel);
+  dim3 grid(pl.p.npairs, pl.splits);
+  gram_tc_kernel<<<grid, kThreads, pl.smem_bytes, st>>>((const float*)x, pl.p, toff, part);
+  if ((s = hicu_check_launch("gram_tc_kernel"))) return s;
+  const int64_t total = (int64_t)g.n * g.n;
+  const int rb = (int)hmin64((total + 255) / 256, 1184);
+  gram_tc_reduce_kernel<<<rb, 256, 0, st>>>(g.n, g.nc, pl.p.T, pl.splits, pl.pt, pl.ntiles, part, G);
+  return hicu_check_launch("gram_tc_reduce_kernel");
+}

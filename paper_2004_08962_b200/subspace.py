@@ -33,6 +33,7 @@ __all__ = [
     "householder_nullspace",
     "jl_compress",
     "gram_matrix",
+    "gram_uses_tensor_cores",
 ]
 
 
@@ -70,12 +71,27 @@ class NullspaceBasis:
         return self.q.shape[0]
 
 
-def gram_matrix(x, kernel: KernelMask, region: Region):
-    """G = H(x)^H H(x) (n x n, complex128) on the device; returns a CUDA tensor."""
+def gram_uses_tensor_cores(kernel: KernelMask, region: Region, dims) -> bool:
+    """True when hicu_gram runs the tcgen05 3xTF32 kernel for this geometry."""
+    dg = device_geometry(kernel, region, tuple(dims))
+    return bool(nat.lib().hicu_gram_uses_tensor_cores(dg.ref()))
+
+
+def gram_matrix(x, kernel: KernelMask, region: Region, force_simt: bool = False):
+    """G = H(x)^H H(x) (n x n, complex128) on the device; returns a CUDA tensor.
+
+    ``force_simt`` selects the SIMT kernel even where the tcgen05 kernel applies
+    (cross-checks)."""
     torch = nat.require_cuda()
     x = np.asarray(x) if not isinstance(x, torch.Tensor) else x
     region.validate(kernel, tuple(x.shape))
     dg = device_geometry(kernel, region, tuple(x.shape))
+    if force_simt:
+        import copy
+
+        dg = copy.copy(dg)
+        dg.struct = nat.HicuGeom.from_buffer_copy(dg.struct)
+        dg.struct.flags |= nat.GEOM_FORCE_SIMT_GRAM
     L = nat.lib()
     ws_bytes = L.hicu_gram_workspace(dg.ref())
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device="cuda")

@@ -94,7 +94,7 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
     if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform
     // ---- y = A22 v: thread (row, chunk), 4 chunks over j ----
     {
-      const int nchunk = 4, rows_per = nt / nchunk;  // 128 rows per pass
+      const int nchunk = 4, rows_per = nt / nchunk;  // nt/4 rows per pass
       const int c = tid / rows_per, rr = tid % rows_per;
       const int clen = (m + nchunk - 1) / nchunk;
       const int j0 = k1 + c * clen, j1 = min(l, j0 + clen);
@@ -122,7 +122,7 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
     __syncthreads();
     if (tid == 0) {
       double2 dot = cd(0.0, 0.0);
-      for (int q = 0; q < 16; ++q) dot = dot + redz[q];
+      for (int q = 0; q < (nt >> 5); ++q) dot = dot + redz[q];
       const double2 td = cmul(tk, dot);
       s_alpha2 = cd(-0.5 * td.x, -0.5 * td.y);
     }
@@ -142,6 +142,18 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
     __syncthreads();
   }
   if (tid == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+}
+
+// 1/q to ~1e-15 relative: fp32 seed (MUFU) + two Newton steps in fp64
+// (the Sturm count only needs the sign of each pivot).  Falls back to an IEEE
+// division when q is outside the fp32 exponent range.
+__device__ __forceinline__ double fast_rcp(double q) {
+  const double aq = fabs(q);
+  if (aq < 1e-30 || aq > 1e30) return 1.0 / q;
+  double r = (double)__frcp_rn((float)q);
+  r = r * (2.0 - q * r);
+  r = r * (2.0 - q * r);
+  return r;
 }
 
 // Sturm count: number of eigenvalues of T (d, e2 = e^2) strictly below x.
@@ -263,8 +275,9 @@ __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const d
     }
   }
   for (int i = 0; i < l; ++i) {
-    const double v = AT(u0, i);
-    if (fabs(v) < tiny) AT(u0, i) = (v < 0.0 ? -tiny : tiny);
+    double v = AT(u0, i);
+    if (fabs(v) < tiny) v = (v < 0.0 ? -tiny : tiny);
+    AT(u0, i) = 1.0 / v;  // store the reciprocal: back substitution multiplies
   }
   unsigned sd0 = 2654435761u * (unsigned)(j + 1);
   for (int i = 0; i < l; ++i) {
@@ -285,7 +298,7 @@ __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const d
     double xp1 = 0.0, xp2 = 0.0;
     for (int i = l - 1; i >= 0; --i) {
       double v = AT(x, i) - AT(u1, i) * xp1 - AT(u2, i) * xp2;
-      v = v / AT(u0, i);
+      v = v * AT(u0, i);
       AT(x, i) = v;
       xp2 = xp1;
       xp1 = v;

@@ -133,6 +133,23 @@ int hicu_soft_terms(int64_t N, const void* g, const void* y, const void* x0,
 int hicu_conv_adj(const hicu_geom* g, const void* x, const void* u, int k,
                   void* out, void* stream);
 
+/* Split step update for the halo-sharded volume path (several GPUs hold one
+ * volume): hicu_step_reduce writes sums7 = [obj_conv, ||g||^2, ||res||^2,
+ * Re<Mg,res>, ||Mg||^2, num_conv, den_conv] from the local partials; the
+ * caller all-reduces sums7 over ranks; hicu_step_apply forms eta (identical on
+ * every rank) and updates y (solver.py:356-370). */
+int hicu_step_reduce(const double* obj_parts, int n_obj, const double* dc_parts,
+                     int n_dc, const double* els_parts, int n_els,
+                     double* sums7, void* stream);
+int hicu_step_apply(int64_t N, void* y, const void* gdir, const double* sums7,
+                    int dc_mode, double lam, double* rec, void* stream);
+/* Data consistency on n contiguous samples of g (after the halo
+ * accumulation of raw scatter partials); parts as hicu_scatter_dc's. */
+int hicu_dc_nparts(int64_t n);
+int hicu_dc_apply(int64_t n, void* g, const uint8_t* mask, const void* y,
+                  const void* x0, int dc_mode, double lam, double* parts,
+                  void* stream);
+
 /* ser_parts[2b] = sum |ref - y|^2, [2b+1] = sum |ref|^2 (solver.py:251-255).
  * Returns the number of blocks used in *nparts_out when not NULL. */
 int hicu_ser_parts(int64_t N, const void* ref, const void* y, double* ser_parts,

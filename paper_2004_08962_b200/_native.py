@@ -74,6 +74,10 @@ _SIGS = {
     "hicu_step_update": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,
                                  c_int, c_double, c_void_p, c_void_p]),
     "hicu_ser_nparts": (c_int, [c_int64]),
+    "hicu_step_reduce": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p]),
+    "hicu_step_apply": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_int, c_double, c_void_p, c_void_p]),
+    "hicu_dc_nparts": (c_int, [c_int64]),
+    "hicu_dc_apply": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_double, c_void_p, c_void_p]),
     "hicu_ser_parts": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int), c_void_p]),
     "hicu_soft_terms": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, POINTER(c_int),
                                 c_void_p]),

@@ -743,3 +743,121 @@ extern "C" int hicu_soft_terms(int64_t N, const void* g, const void* y, const vo
                                                          mask, parts);
   return hicu_check_launch("soft_terms_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Split form of the step update for the halo-sharded path (one volume over
+// several GPUs): the partial sums are reduced locally to 7 raw scalars, the
+// caller all-reduces them across ranks, and every rank applies the same eta.
+// sums7 = [obj_conv, ||g||^2, ||res||^2, Re<Mg,res>, ||Mg||^2, num_conv, den_conv]
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void step_reduce_kernel(const double* __restrict__ obj_parts, int n_obj, const double* __restrict__ dc_parts,
+                                   int n_dc, const double* __restrict__ els_parts, int n_els,
+                                   double* __restrict__ sums7) {
+  const double obj_c = warp_sum_parts(obj_parts, n_obj, 1, 0);
+  const double gn2 = warp_sum_parts(dc_parts, n_dc, 4, 0);
+  const double res2 = warp_sum_parts(dc_parts, n_dc, 4, 1);
+  const double snum = warp_sum_parts(dc_parts, n_dc, 4, 2);
+  const double sden = warp_sum_parts(dc_parts, n_dc, 4, 3);
+  const double num_c = warp_sum_parts(els_parts, n_els, 2, 0);
+  const double den_c = warp_sum_parts(els_parts, n_els, 2, 1);
+  if (threadIdx.x == 0) {
+    sums7[0] = obj_c;
+    sums7[1] = gn2;
+    sums7[2] = res2;
+    sums7[3] = snum;
+    sums7[4] = sden;
+    sums7[5] = num_c;
+    sums7[6] = den_c;
+  }
+}
+
+__global__ void step_apply_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir,
+                                  const double* __restrict__ sums7, int dc_mode, double lam, double* __restrict__ rec) {
+  double obj = sums7[0], num = sums7[5], den = sums7[6];
+  if (dc_mode == 1) {
+    obj += lam * sums7[2];
+    num += lam * sums7[3];
+    den += lam * sums7[4];
+  }
+  const bool degenerate = !(den > 0.0);
+  const double eta = degenerate ? 0.0 : num / den;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && rec) {
+    rec[HICU_REC_OBJ] = obj;
+    rec[HICU_REC_NUM] = num;
+    rec[HICU_REC_DEN] = den;
+    rec[HICU_REC_ETA] = eta;
+    rec[HICU_REC_OBJ_AFTER] = degenerate ? obj : obj - num * num / den;
+    rec[HICU_REC_GNORM2] = sums7[1];
+    rec[HICU_REC_DEGENERATE] = degenerate ? 1.0 : 0.0;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    rec[7] = (double)t;
+  }
+  if (degenerate) return;
+  const float e = (float)eta;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N; m += (int64_t)gridDim.x * blockDim.x) {
+    const float2 gv = gdir[m];
+    float2 yv = y[m];
+    yv.x = fmaf(-e, gv.x, yv.x);
+    yv.y = fmaf(-e, gv.y, yv.y);
+    y[m] = yv;
+  }
+}
+
+// data consistency on a contiguous range of samples, with the partial sums
+// (||g||^2, ||res||^2, Re<Mg,res>, ||Mg||^2) of scatter_kernel's epilogue
+__global__ void dc_apply_kernel(int64_t n, float2* __restrict__ g, const uint8_t* __restrict__ mask,
+                                const float2* __restrict__ y, const float2* __restrict__ x0, int dc_mode, float lam,
+                                double* __restrict__ parts) {
+  double a_g = 0.0, a_res = 0.0, a_num = 0.0, a_den = 0.0;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
+    float2 acc = g[m];
+    const bool on = mask[m] == 1;
+    if (dc_mode == 0) {
+      if (on) acc = cf(0.f, 0.f);
+    } else {
+      const float2 res = on ? (y[m] - x0[m]) : cf(0.f, 0.f);
+      a_res += (double)res.x * res.x + (double)res.y * res.y;
+      acc = acc + lam * res;
+      if (on) {
+        a_num += (double)acc.x * res.x + (double)acc.y * res.y;
+        a_den += (double)acc.x * acc.x + (double)acc.y * acc.y;
+      }
+    }
+    a_g += (double)acc.x * acc.x + (double)acc.y * acc.y;
+    g[m] = acc;
+  }
+  double v[4] = {a_g, a_res, a_num, a_den};
+  block_reduce_store<4>(v, parts + 4 * (size_t)blockIdx.x);
+}
+}  // namespace
+
+extern "C" int hicu_step_reduce(const double* obj_parts, int n_obj, const double* dc_parts, int n_dc,
+                                const double* els_parts, int n_els, double* sums7, void* stream) {
+  if (!obj_parts || !dc_parts || !els_parts || !sums7) return hicu_set_error(HICU_ERR_PARAMETER, "step_reduce: null");
+  step_reduce_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(obj_parts, n_obj, dc_parts, n_dc, els_parts, n_els, sums7);
+  return hicu_check_launch("step_reduce_kernel");
+}
+
+extern "C" int hicu_step_apply(int64_t N, void* y, const void* gdir, const double* sums7, int dc_mode, double lam,
+                               double* rec, void* stream) {
+  if (!y || !gdir || !sums7 || N < 1) return hicu_set_error(HICU_ERR_PARAMETER, "step_apply: bad arguments");
+  int64_t b = (N + 255) / 256;
+  const int64_t cap = (int64_t)hicu_sm_count() * 4;
+  if (b > cap) b = cap;
+  step_apply_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(N, (float2*)y, (const float2*)gdir, sums7, dc_mode,
+                                                               lam, rec);
+  return hicu_check_launch("step_apply_kernel");
+}
+
+extern "C" int hicu_dc_nparts(int64_t n) { return ser_blocks(n); }
+
+extern "C" int hicu_dc_apply(int64_t n, void* g, const uint8_t* mask, const void* y, const void* x0, int dc_mode,
+                             double lam, double* parts, void* stream) {
+  if (!g || !mask || !parts || n < 1) return hicu_set_error(HICU_ERR_PARAMETER, "dc_apply: bad arguments");
+  if (dc_mode == 1 && (!y || !x0)) return hicu_set_error(HICU_ERR_SHAPE, "soft data consistency requires x0");
+  dc_apply_kernel<<<ser_blocks(n), 256, 0, (cudaStream_t)stream>>>(n, (float2*)g, mask, (const float2*)y,
+                                                                   (const float2*)x0, dc_mode, (float)lam, parts);
+  return hicu_check_launch("dc_apply_kernel");
+}

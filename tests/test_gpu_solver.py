@@ -201,3 +201,23 @@ def test_reconstruct_slices_partition():
     out1 = reconstruct_slices([x0, x0, x0], [mask] * 3, kern, sched, rank=1, world=2, tail_energy_threshold=0)
     assert sorted(out0) == [0, 1] and sorted(out1) == [2]
     assert np.array_equal(out0[0][0], out1[2][0])
+
+
+@pytest.mark.timeout(900)
+def test_c1_free_running_ser_parity():
+    """BASELINE configs[0] (C1: 128x128, 8 coils, SNR 30 dB, VD random R=3,
+    5x5x8 kernel, rank 40, 50 outer iterations, p=8, G=5): the device run and
+    the oracle running the reference's rSVD (same canonical phase
+    convention) end within 0.1 dB SER of each other."""
+    from paper_2004_08962_b200.synthetic import CONFIGS, make_config
+
+    spec = CONFIGS["C1"]
+    ksp, mask, x0 = make_config("C1")
+    kern = H.KernelMask.full(spec.kernel)
+    sched = H.SolverSchedule(rank=spec.rank, stages=[H.StageSpec(*s) for s in spec.stages], seed=0)
+    xg, rep = H.hicu_reconstruct(x0, mask, kern, sched, reference=ksp, tail_energy_threshold=0)
+    xo, _ = O.hicu_reconstruct(x0, mask, spec.kernel, spec.stages, spec.rank, seed=0, canonical=True)
+    ser_g, ser_o, ser_0 = O.ser_db(ksp, xg), O.ser_db(ksp, xo), O.ser_db(ksp, x0)
+    print(f"C1 SER: zero-filled {ser_0:.3f} dB, device {ser_g:.3f} dB, oracle {ser_o:.3f} dB")
+    assert ser_g > ser_0 + 3.0
+    assert abs(ser_g - ser_o) <= 0.1

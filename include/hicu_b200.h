@@ -62,10 +62,15 @@ typedef struct hicu_geom {
                                    * kappa = sp*dims[last] + c                  */
   const int32_t* pos;             /* device: n x ndim support positions       */
   const int64_t* koff;            /* device: n flat offsets, non-circular axes */
+  int64_t kext[HICU_MAX_NDIM];    /* kernel bounding-box extents (KernelMask.extents,
+                                   * hankel.py:58); 0 = unknown (disables the
+                                   * tensor-core conv/scatter, which size their
+                                   * operand tiles from it)                     */
 } hicu_geom;
 
 #define HICU_GEOM_COIL_SEPARABLE 1
 #define HICU_GEOM_FORCE_SIMT_GRAM 2   /* use the SIMT Gram even when tcgen05 applies */
+#define HICU_GEOM_FORCE_SIMT_CONV 4   /* use the SIMT conv/scatter even when tcgen05 applies */
 
 /* Per-step scalar record written by hicu_step_update (doubles). */
 enum {
@@ -163,6 +168,9 @@ size_t hicu_gram_workspace(const hicu_geom* g);
 /* 1 when hicu_gram runs the tcgen05 3xTF32 kernel for this geometry (coil-
  * separable support with 8 coils, no circular axes, >= 8 spatial taps). */
 int hicu_gram_uses_tensor_cores(const hicu_geom* g);
+/* 1 when hicu_conv_fwd / hicu_conv_els / hicu_scatter_dc with p columns run
+ * on the tcgen05 kernels (conv_tc.cu) for this geometry. */
+int hicu_conv_uses_tensor_cores(const hicu_geom* g, int p);
 int hicu_gram(const hicu_geom* g, const void* x, void* G, void* ws,
               size_t ws_bytes, void* stream);
 

@@ -20,6 +20,7 @@ REC_OBJ, REC_NUM, REC_DEN, REC_ETA, REC_OBJ_AFTER, REC_GNORM2, REC_DEGENERATE, R
 REC_SLOTS = 8
 GEOM_COIL_SEPARABLE = 1
 GEOM_FORCE_SIMT_GRAM = 2
+GEOM_FORCE_SIMT_CONV = 4
 PROF_KINDS = ("gram", "nystrom", "householder", "conv_fwd", "scatter", "conv_els", "update")
 
 
@@ -34,6 +35,7 @@ class HicuGeom(ctypes.Structure):
         ("flags", c_int32),
         ("pos", c_void_p),
         ("koff", c_void_p),
+        ("kext", c_int64 * MAX_NDIM),
     ]
 
 
@@ -83,6 +85,7 @@ _SIGS = {
                                 c_void_p]),
     "hicu_gram_workspace": (c_size_t, [_GP]),
     "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
+    "hicu_conv_uses_tensor_cores": (c_int, [_GP, c_int]),
     "hicu_gram": (c_int, [_GP, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hicu_zgemm": (c_int, [c_char, c_char, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,
                            c_void_p]),

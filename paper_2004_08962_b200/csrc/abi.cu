@@ -107,6 +107,7 @@ int hicu_make_devgeom(const hicu_geom* g, DevGeom* out) {
   }
   d.nc = 0;
   d.nsp = 0;
+  for (int a = 0; a < HICU_MAX_NDIM; ++a) d.kext[a] = a < g->ndim ? g->kext[a] : 0;
   {
     const int L = g->ndim - 1;
     const int64_t ncl = g->dims[L];
@@ -120,7 +121,7 @@ int hicu_make_devgeom(const hicu_geom* g, DevGeom* out) {
   return HICU_OK;
 }
 
-extern "C" int hicu_abi_version(void) { return 1; }
+extern "C" int hicu_abi_version(void) { return 2; }
 
 extern "C" const char* hicu_last_error(void) { return g_last_error; }
 

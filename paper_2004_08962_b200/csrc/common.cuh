@@ -76,6 +76,7 @@ struct DevGeom {
   // the geometry does not have this structure (generic kernels are used).
   int nc;
   int nsp;  // spatial taps (n / nc)
+  int64_t kext[HICU_MAX_NDIM];  // kernel bounding box (0 = unknown)
 };
 
 // Non-circular part of the flat address of row i, plus the region coordinates

@@ -12,6 +12,13 @@
 // the geometry so partial counts, and hence results, are deterministic.
 #include "common.cuh"
 
+bool hicu_conv_tc_supported(const DevGeom& g, int p);
+int hicu_conv_tc(const DevGeom& g, const float2* y, const float2* qt, float2* u, double* parts, int mode,
+                 int nparts_total, cudaStream_t st);
+int hicu_scatter_tc(const DevGeom& g, const float2* qt, const float2* u, const uint8_t* mask, const float2* y,
+                    const float2* x0, int dc_mode, float lam, float2* gout, double* parts, int nparts_total,
+                    cudaStream_t st);
+
 namespace {
 
 constexpr int kConvThreads = 256;
@@ -541,6 +548,8 @@ int conv_dispatch(const hicu_geom* hg, const void* y, const void* qt, int p, con
   cudaStream_t s = (cudaStream_t)stream;
   float2* u = mode == 0 ? (float2*)u_out : (float2*)u_in;
   if (!u) return hicu_set_error(HICU_ERR_PARAMETER, "conv: null u");
+  if (!(hg->flags & HICU_GEOM_FORCE_SIMT_CONV) && hicu_conv_tc_supported(g, p))
+    return hicu_conv_tc(g, (const float2*)y, (const float2*)qt, u, parts, mode, conv_blocks(g.s), s);
   if (g.nc > 0) {
     if (p <= 4) return conv_coil_dispatch<4>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
     if (p <= 8) return conv_coil_dispatch<8>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
@@ -572,6 +581,12 @@ int launch_scatter(const DevGeom& g, const float2* qt, int p, const float2* u, c
 }
 
 }  // namespace
+
+extern "C" int hicu_conv_uses_tensor_cores(const hicu_geom* hg, int p) {
+  DevGeom g;
+  if (!hg || hicu_make_devgeom(hg, &g)) return 0;
+  return !(hg->flags & HICU_GEOM_FORCE_SIMT_CONV) && hicu_conv_tc_supported(g, p) ? 1 : 0;
+}
 
 extern "C" int hicu_conv_nparts(const hicu_geom* hg) {
   DevGeom g;
@@ -609,6 +624,9 @@ extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const
   cudaStream_t s = (cudaStream_t)stream;
   auto q = (const float2*)qt;
   auto uu = (const float2*)u;
+  if (g.nc > 0 && !(hg->flags & HICU_GEOM_FORCE_SIMT_CONV) && hicu_conv_tc_supported(g, p))
+    return hicu_scatter_tc(g, q, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam, (float2*)gout,
+                           dc_parts, scatter_coil_blocks(g.N / g.nc), s);
   if (g.nc > 0) {
     auto yy = (const float2*)y;
     auto xx = (const float2*)x0;

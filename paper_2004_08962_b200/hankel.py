@@ -14,6 +14,7 @@ outputs are numpy complex128 like the reference.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import contextlib
 import math
 from dataclasses import dataclass, field
 
@@ -36,6 +37,8 @@ __all__ = [
     "exact_line_search",
     "DeviceGeometry",
     "device_geometry",
+    "kernel_paths",
+    "conv_uses_tensor_cores",
 ]
 
 _PCHUNK = 16  # columns per device call (kernels are compiled for p <= 16)
@@ -237,9 +240,11 @@ class DeviceGeometry:
             g.roff[d] = region.offsets[d]
             g.rext[d] = region.extents[d]
         g.circular = sum(1 << a for a in region.circular_axes)
-        g.flags = nat.GEOM_COIL_SEPARABLE if _coil_separable(kernel, dims) else 0
+        g.flags = (nat.GEOM_COIL_SEPARABLE if _coil_separable(kernel, dims) else 0) | _PATH_FLAGS
         g.pos = self.pos_t.data_ptr()
         g.koff = self.koff_t.data_ptr()
+        for d in range(nd):
+            g.kext[d] = int(kernel.extents[d])
         self.struct = g
         L = nat.lib()
         self.conv_nparts = L.hicu_conv_nparts(self.ref())
@@ -266,13 +271,29 @@ def _coil_separable(kernel: KernelMask, dims) -> bool:
 
 
 _GEOM_CACHE: dict = {}
+_PATH_FLAGS = 0
+
+
+@contextlib.contextmanager
+def kernel_paths(simt_conv: bool = False, simt_gram: bool = False):
+    """Select the SIMT conv/scatter and/or Gram kernels even where the
+    tcgen05 kernels apply (cross-checks and A/B timing).  Geometries built
+    inside the context carry the choice; the cache keys on it."""
+    global _PATH_FLAGS
+    old = _PATH_FLAGS
+    _PATH_FLAGS = (nat.GEOM_FORCE_SIMT_CONV if simt_conv else 0) | (nat.GEOM_FORCE_SIMT_GRAM if simt_gram else 0)
+    try:
+        yield
+    finally:
+        _PATH_FLAGS = old
 
 
 def device_geometry(kernel: KernelMask, region: Region, dims) -> DeviceGeometry:
     torch = nat.require_cuda()
 
     key = (kernel.positions.tobytes(), kernel.positions.shape, region.offsets, region.extents,
-           tuple(sorted(region.circular_axes)), tuple(int(d) for d in dims), torch.cuda.current_device())
+           tuple(sorted(region.circular_axes)), tuple(int(d) for d in dims), torch.cuda.current_device(),
+           _PATH_FLAGS)
     dg = _GEOM_CACHE.get(key)
     if dg is None:
         if len(_GEOM_CACHE) > 64:
@@ -280,6 +301,13 @@ def device_geometry(kernel: KernelMask, region: Region, dims) -> DeviceGeometry:
         dg = DeviceGeometry(kernel, region, dims)
         _GEOM_CACHE[key] = dg
     return dg
+
+
+def conv_uses_tensor_cores(kernel: KernelMask, region: Region, dims, p: int = 8) -> bool:
+    """True when conv / ELS / scatter with ``p`` columns run on the tcgen05
+    kernels (``csrc/conv_tc.cu``) for this geometry."""
+    dg = device_geometry(kernel, region, dims)
+    return bool(nat.lib().hicu_conv_uses_tensor_cores(dg.ref(), int(p)))
 
 
 def to_dev(a, dtype_np=np.complex64):

@@ -42,7 +42,7 @@ def test_library_exports_every_header_symbol(lib):
 
 
 def test_library_info_without_gpu(lib):
-    assert lib.hicu_abi_version() == 1
+    assert lib.hicu_abi_version() == 2
     assert lib.hicu_status_string(3) == b"DegenerateInputError"
     assert lib.hicu_status_string(6) == b"ConfigError"
 
@@ -51,7 +51,7 @@ def test_struct_layout_matches_header(lib):
     import ctypes
 
     # hicu_geom: 2*int32 + 3*8*int64 + uint32 (+pad) + 2 pointers
-    assert ctypes.sizeof(nat.HicuGeom) == 8 + 3 * 64 + 8 + 16
+    assert ctypes.sizeof(nat.HicuGeom) == 8 + 3 * 64 + 8 + 16 + 64
     assert nat.HicuStageArgs.rec.offset % 8 == 0
 
 

@@ -24,11 +24,13 @@ namespace {
 constexpr int kConvThreads = 256;
 constexpr int kScatterThreads = 256;
 
+// At least one block per SM: the tcgen05 kernels (conv_tc.cu) run one
+// persistent CTA per SM and write one partial per CTA into the same buffer.
 int conv_blocks(int64_t s) {
   int64_t b = (s + kConvThreads - 1) / kConvThreads;
   int64_t cap = (int64_t)hicu_sm_count() * 8;
   if (b > cap) b = cap;
-  if (b < 1) b = 1;
+  if (b < hicu_sm_count()) b = hicu_sm_count();
   return (int)b;
 }
 
@@ -474,7 +476,7 @@ int scatter_coil_blocks(int64_t Ns) {
   int64_t b = (Ns + 127) / 128;
   int64_t cap = (int64_t)hicu_sm_count() * 16;
   if (b > cap) b = cap;
-  if (b < 1) b = 1;
+  if (b < hicu_sm_count()) b = hicu_sm_count();
   return (int)b;
 }
 

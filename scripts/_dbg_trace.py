@@ -14,7 +14,7 @@ for dims in [(256, 256, 8), (64, 64, 8)]:
         torch.cuda.synchronize()
         nat.check(L.hicu_conv_fwd(dg.ref(), y.data_ptr(), q.data_ptr(), 8, u.data_ptr(), op.data_ptr(), st))
         torch.cuda.synchronize()
-    t = u.view(torch.int64).cpu().numpy().reshape(-1)[: 148 * 12].reshape(148, 12)[:, :10].astype(np.int64)
+    t = u.view(torch.int64).cpu().numpy().reshape(-1)[: 148 * 12].reshape(148, 12)[:, :12].astype(np.int64)
     t = t[t[:, 0] > 0]
     base = t[:, 0].min()
     rel = (t - base) / 1000.0

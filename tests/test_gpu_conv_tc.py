@@ -36,12 +36,16 @@ CASES = {
     # name: (spatial dims, kernel, region offsets/extents or None for full)
     "2d_full": ((70, 300), spatial_kernel((5, 5)), None),
     "2d_sub": ((64, 96), spatial_kernel((5, 5)), ((10, 20), (30, 40))),
-    "2d_ell": ((40, 150), spatial_kernel((7, 7), ellipse(7)), None),
-    "1d": ((700,), spatial_kernel((9,)), None),
+    "2d_ell": ((40, 150), spatial_kernel((7, 7), ellipse(7)), None),   # 7 taps along the last axis: one TMEM buffer
+    "2d_wide": ((20, 520), spatial_kernel((3, 8)), None),              # nb = 8 (widest), lines of 5 tiles
+    "2d_short": ((30, 40), spatial_kernel((4, 2)), ((3, 5), (20, 12))),  # lines shorter than one tile
+    "1d": ((700,), spatial_kernel((7,)), None),
     "3d": ((12, 10, 140), spatial_kernel((3, 3, 3)), None),
     "3d_sub": ((14, 12, 40), spatial_kernel((3, 2, 3)), ((2, 3, 5), (6, 5, 20))),
-    "spread": ((6, 260), spatial_kernel((1, 40)), None),
+    "1d_nb9": ((300,), spatial_kernel((9,)), None),                   # outside the tcgen05 scope -> SIMT
+    "spread": ((6, 260), spatial_kernel((1, 40)), None),               # outside the tcgen05 scope -> SIMT
 }
+SIMT_ONLY = {"1d_nb9", "spread"}
 
 
 def make(name, seed=0):
@@ -69,7 +73,7 @@ def rel(a, b):
 @pytest.mark.parametrize("name", list(CASES))
 def test_tc_path_selected(name):
     dims, kernel, region, *_ = make(name)
-    assert H.conv_uses_tensor_cores(kernel, region, dims, 8)
+    assert H.conv_uses_tensor_cores(kernel, region, dims, 8) == (name not in SIMT_ONLY)
     assert not H.conv_uses_tensor_cores(kernel, region, dims, 4)
     with H.kernel_paths(simt_conv=True):
         assert not H.conv_uses_tensor_cores(kernel, region, dims, 8)

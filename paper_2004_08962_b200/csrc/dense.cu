@@ -15,6 +15,8 @@
 #include "common.cuh"
 
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 size_t hicu_heev_top_workspace(int l, int r);
 int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void* ws, cudaStream_t st);
@@ -22,6 +24,12 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
 namespace {
 
 constexpr int kSmemCap = 200 * 1024;
+
+__device__ __forceinline__ double warp_sum_d_(double t) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
 
 // ---------------------------------------------------------------------------
 // C = op(A) op(B), row-major, op in {N, C}
@@ -161,6 +169,54 @@ __global__ void trsm_rows_kernel(int n, int ell, const double2* __restrict__ Y, 
     }
     for (int j = lane; j < ell; j += 32) W[(size_t)row * ell + j] = w[j];
     __syncwarp();
+  }
+}
+
+// Right-looking variant: one warp per row, lane t owns entries j = t, t+32,
+// t+64, ... of the row.  For each j the owner finishes w_j (one multiply by the
+// precomputed 1/R_jj), broadcasts it with one shuffle, and every lane folds
+// w_j R[j][k] into its pending entries k > j: no reduction per column.
+constexpr int kTrsmMaxPer = 8;  // ell <= 256
+__global__ void trsm_rl_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
+                               const double* __restrict__ nu_p, const double2* __restrict__ R,
+                               double2* __restrict__ W) {
+  extern __shared__ double2 smr[];
+  double2* sR = smr;                                       // ell x ell (upper)
+  double* rinv = reinterpret_cast<double*>(sR + (size_t)ell * ell);  // 1 / R_jj
+  for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) sR[e] = R[e];
+  for (int j = threadIdx.x; j < ell; j += blockDim.x) rinv[j] = 1.0 / R[(size_t)j * ell + j].x;
+  __syncthreads();
+  const double nu = *nu_p;
+  const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int row = blockIdx.x * warps + warp; row < n; row += gridDim.x * warps) {
+    double2 acc[kTrsmMaxPer];
+#pragma unroll
+    for (int u = 0; u < kTrsmMaxPer; ++u) {
+      const int j = lane + 32 * u;
+      acc[u] = (j < ell) ? Y[(size_t)row * ell + j] + nu * Om[(size_t)row * ell + j] : cd(0.0, 0.0);
+    }
+    for (int j = 0; j < ell; ++j) {
+      const int owner = j & 31, uj = j >> 5;
+      double2 wj = cd(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < kTrsmMaxPer; ++u)
+        if (u == uj) wj = acc[u];
+      wj = rinv[j] * wj;
+      wj.x = __shfl_sync(0xffffffffu, wj.x, owner);
+      wj.y = __shfl_sync(0xffffffffu, wj.y, owner);
+      const double2* Rj = sR + (size_t)j * ell;
+#pragma unroll
+      for (int u = 0; u < kTrsmMaxPer; ++u) {
+        const int k = lane + 32 * u;
+        if (k == j) acc[u] = wj;
+        else if (k > j && k < ell) acc[u] = acc[u] - cmul(wj, Rj[k]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kTrsmMaxPer; ++u) {
+      const int j = lane + 32 * u;
+      if (j < ell) W[(size_t)row * ell + j] = acc[u];
+    }
   }
 }
 
@@ -454,6 +510,274 @@ householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, dou
   }
 }
 
+// Latency-oriented Householder triangularisation (same reflectors as
+// householder_kernel): one block barrier per column.  Warp 0 owns column
+// col+1: it applies reflector col to it, then immediately builds reflector
+// col+1 (norm by shuffles, w into the other half of a double-buffered smem
+// vector, refl row to global).  Warps 1.. apply reflector col to the other
+// remaining columns, two per pass so their reduction chains overlap.
+__device__ __forceinline__ void hh2_reflector(int n, int c, const double2* vc, double tol, int lane,
+                                              double2* __restrict__ refl, double2* __restrict__ tau,
+                                              int* __restrict__ flags, int* __restrict__ status, double2* s_tau,
+                                              int* s_act, double2* w_next) {
+  double t = 0.0;
+  for (int k = c + 1 + lane; k < n; k += 32) t += abs2d(vc[k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  double2 ui = cd(0.0, 0.0);
+  int active = 0;
+  if (lane == 0) {
+    const double tail = t;
+    const double2 x0 = vc[c];
+    const double beta = sqrt(tail + x0.x * x0.x + x0.y * x0.y);
+    active = 1;
+    if (beta < tol) {
+      *status = HICU_ERR_DEGENERATE_INPUT;
+      active = 0;
+    } else if (tail == 0.0 && x0.y == 0.0 && x0.x >= 0.0) {
+      active = 0;
+    }
+    double2 u0 = cd(0.0, 0.0), tv = cd(0.0, 0.0);
+    if (active) {
+      if (x0.x > 0.0) {
+        const double2 nume = cd(-tail, 2.0 * beta * x0.y);
+        const double2 deno = cd(x0.x + beta, -x0.y);
+        const double dd = abs2d(deno);
+        u0 = cd((nume.x * deno.x + nume.y * deno.y) / dd, (nume.y * deno.x - nume.x * deno.y) / dd);
+      } else {
+        u0 = cd(x0.x - beta, x0.y);
+      }
+      tv = cd((beta - x0.x) / beta, x0.y / beta);
+      const double uu = abs2d(u0);
+      ui = cd(u0.x / uu, -u0.y / uu);
+    }
+    *s_tau = tv;
+    *s_act = active;
+    flags[c] = active;
+    tau[c] = tv;
+  }
+  active = __shfl_sync(0xffffffffu, active, 0);
+  ui.x = __shfl_sync(0xffffffffu, ui.x, 0);
+  ui.y = __shfl_sync(0xffffffffu, ui.y, 0);
+  if (!active) return;
+  for (int k = c + lane; k < n; k += 32) {
+    const double2 wv = (k == c) ? cd(1.0, 0.0) : cmul(vc[k], ui);
+    refl[(size_t)c * n + k] = wv;
+    w_next[k] = wv;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+householder2_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
+                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  extern __shared__ double2 sh2[];
+  double2* sw = sh2;           // 2 x n (double-buffered reflector w)
+  double2* v = sh2 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
+  __shared__ double2 s_tau[2];
+  __shared__ int s_act[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[(size_t)(e % r) * n + e / r] = Vg[e];
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) refl[e] = cd(0.0, 0.0);
+  __syncthreads();
+  if (warp == 0) hh2_reflector(n, 0, v, tol, lane, refl, tau, flags, status, &s_tau[0], &s_act[0], sw);
+  __syncthreads();
+  for (int col = 0; col < r; ++col) {
+    const int par = col & 1;
+    const double2 tv = s_tau[par];
+    const double2* w = sw + (size_t)par * n;
+    if (s_act[par]) {
+      if (warp == 0) {
+        const int j = col + 1;
+        if (j < r) {
+          double2 d0 = cd(0.0, 0.0);
+          for (int k = col + lane; k < n; k += 32) zfmac(d0, w[k], v[(size_t)j * n + k]);
+          d0 = cd(warp_sum_d_(d0.x), warp_sum_d_(d0.y));
+          const double2 f0 = cmul(tv, d0);
+          for (int k = col + lane; k < n; k += 32) v[(size_t)j * n + k] = v[(size_t)j * n + k] - cmul(w[k], f0);
+        }
+      } else {
+        for (int j0 = col + 2 + (warp - 1); j0 < r; j0 += 2 * (nw - 1)) {
+          const int j1 = j0 + (nw - 1);
+          const bool two = j1 < r;
+          double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+          for (int k = col + lane; k < n; k += 32) {
+            const double2 wk = w[k];
+            zfmac(d0, wk, v[(size_t)j0 * n + k]);
+            if (two) zfmac(d1, wk, v[(size_t)j1 * n + k]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            d0.x += __shfl_xor_sync(0xffffffffu, d0.x, o);
+            d0.y += __shfl_xor_sync(0xffffffffu, d0.y, o);
+            d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
+            d1.y += __shfl_xor_sync(0xffffffffu, d1.y, o);
+          }
+          const double2 f0 = cmul(tv, d0), f1 = cmul(tv, d1);
+          for (int k = col + lane; k < n; k += 32) {
+            const double2 wk = w[k];
+            v[(size_t)j0 * n + k] = v[(size_t)j0 * n + k] - cmul(wk, f0);
+            if (two) v[(size_t)j1 * n + k] = v[(size_t)j1 * n + k] - cmul(wk, f1);
+          }
+        }
+      }
+    }
+    if (warp == 0 && col + 1 < r) {
+      __syncwarp();
+      hh2_reflector(n, col + 1, v + (size_t)(col + 1) * n, tol, lane, refl, tau, flags, status, &s_tau[par ^ 1],
+                    &s_act[par ^ 1], sw + (size_t)(par ^ 1) * n);
+    }
+    __syncthreads();
+  }
+}
+
+// Third variant (n <= 32 * kHh3Per): fixed column ownership (column j by warp
+// j % 32), every per-step access of a column issued as one predicated batch
+// (lane owns rows lane + 32u), so a step costs one shared-memory latency
+// instead of one per element.  The owner of column col+1 builds reflector
+// col+1 from the registers it just updated; one block barrier per column.
+constexpr int kHh3Per = 7;
+__device__ unsigned g_hh3_trace[64];  // debug (HICU_HH_TRACE): owner-warp clocks of steps 5, 30, 50
+constexpr int kHh3Threads = 768;
+
+__device__ __forceinline__ void hh3_build(int n, int c, const double2 (&x)[kHh3Per], double tol, int lane,
+                                          double2* __restrict__ refl, double2* __restrict__ tau,
+                                          int* __restrict__ flags, int* __restrict__ status, double2* s_tau,
+                                          int* s_act, double2* w_next) {
+  // x = column c (rows lane + 32u); pivot row c, tail rows > c
+  double t = 0.0;
+  double2 x0 = cd(0.0, 0.0);
+#pragma unroll
+  for (int u = 0; u < kHh3Per; ++u) {
+    const int k = lane + 32 * u;
+    if (k > c && k < n) t += abs2d(x[u]);
+    if (k == c) x0 = x[u];
+  }
+  t = warp_sum_d_(t);
+  x0.x = __shfl_sync(0xffffffffu, x0.x, c & 31);
+  x0.y = __shfl_sync(0xffffffffu, x0.y, c & 31);
+  double2 ui = cd(0.0, 0.0);
+  int active = 0;
+  if (lane == 0) {
+    const double tail = t;
+    const double beta = sqrt(tail + x0.x * x0.x + x0.y * x0.y);
+    active = 1;
+    if (beta < tol) {
+      *status = HICU_ERR_DEGENERATE_INPUT;
+      active = 0;
+    } else if (tail == 0.0 && x0.y == 0.0 && x0.x >= 0.0) {
+      active = 0;
+    }
+    double2 u0 = cd(0.0, 0.0), tv = cd(0.0, 0.0);
+    if (active) {
+      if (x0.x > 0.0) {
+        const double2 nume = cd(-tail, 2.0 * beta * x0.y);
+        const double2 deno = cd(x0.x + beta, -x0.y);
+        const double dd = abs2d(deno);
+        u0 = cd((nume.x * deno.x + nume.y * deno.y) / dd, (nume.y * deno.x - nume.x * deno.y) / dd);
+      } else {
+        u0 = cd(x0.x - beta, x0.y);
+      }
+      tv = cd((beta - x0.x) / beta, x0.y / beta);
+      const double uu = abs2d(u0);
+      ui = cd(u0.x / uu, -u0.y / uu);
+    }
+    *s_tau = tv;
+    *s_act = active;
+    flags[c] = active;
+    tau[c] = tv;
+  }
+  active = __shfl_sync(0xffffffffu, active, 0);
+  ui.x = __shfl_sync(0xffffffffu, ui.x, 0);
+  ui.y = __shfl_sync(0xffffffffu, ui.y, 0);
+  if (!active) return;
+#pragma unroll
+  for (int u = 0; u < kHh3Per; ++u) {
+    const int k = lane + 32 * u;
+    if (k >= c && k < n) {
+      const double2 wv = (k == c) ? cd(1.0, 0.0) : cmul(x[u], ui);
+      refl[(size_t)c * n + k] = wv;
+      w_next[k] = wv;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kHh3Threads)
+householder3_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
+                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  extern __shared__ double2 sh3[];
+  double2* sw = sh3;           // 2 x n (double-buffered reflector w)
+  double2* v = sh3 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
+  __shared__ double2 s_tau[2];
+  __shared__ int s_act[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[(size_t)(e % r) * n + e / r] = Vg[e];
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) refl[e] = cd(0.0, 0.0);
+  __syncthreads();
+  if (warp == 0) {
+    double2 x[kHh3Per];
+#pragma unroll
+    for (int u = 0; u < kHh3Per; ++u) {
+      const int k = lane + 32 * u;
+      x[u] = k < n ? v[k] : cd(0.0, 0.0);
+    }
+    hh3_build(n, 0, x, tol, lane, refl, tau, flags, status, &s_tau[0], &s_act[0], sw);
+  }
+  __syncthreads();
+  for (int col = 0; col < r; ++col) {
+    const int par = col & 1;
+    const int slot = col == 5 ? 0 : (col == 30 ? 1 : (col == 50 ? 2 : -1));
+    const bool own = ((col + 1) % nw) == warp && lane == 0;
+    if (slot >= 0 && own) g_hh3_trace[slot * 8 + 0] = (unsigned)clock();
+    const double2 tv = s_tau[par];
+    const bool act = s_act[par] != 0;
+    const double2* w = sw + (size_t)par * n;
+    double2 wr[kHh3Per];
+    if (act) {
+#pragma unroll
+      for (int u = 0; u < kHh3Per; ++u) {
+        const int k = lane + 32 * u;
+        wr[u] = (k >= col && k < n) ? w[k] : cd(0.0, 0.0);
+      }
+    }
+    // my columns j > col, j % nw == warp
+    for (int j = col + 1 + ((warp - (col + 1)) % nw + nw) % nw; j < r; j += nw) {
+      double2* vj = v + (size_t)j * n;
+      double2 x[kHh3Per];
+#pragma unroll
+      for (int u = 0; u < kHh3Per; ++u) {
+        const int k = lane + 32 * u;
+        x[u] = k < n ? vj[k] : cd(0.0, 0.0);
+      }
+      if (act) {
+        double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < kHh3Per; ++u) {
+          if (u & 1) zfmac(d1, wr[u], x[u]);
+          else zfmac(d0, wr[u], x[u]);
+        }
+        double2 dt = d0 + d1;
+        dt = cd(warp_sum_d_(dt.x), warp_sum_d_(dt.y));
+        const double2 f = cmul(tv, dt);
+#pragma unroll
+        for (int u = 0; u < kHh3Per; ++u) {
+          const int k = lane + 32 * u;
+          x[u] = x[u] - cmul(wr[u], f);
+          if (k >= col && k < n) vj[k] = x[u];
+        }
+      }
+      if (j == col + 1) {  // owner of the next pivot column builds its reflector from registers
+        if (slot >= 0 && lane == 0) g_hh3_trace[slot * 8 + 1] = (unsigned)clock();
+        hh3_build(n, j, x, tol, lane, refl, tau, flags, status, &s_tau[par ^ 1], &s_act[par ^ 1],
+                  sw + (size_t)(par ^ 1) * n);
+        if (slot >= 0 && lane == 0) g_hh3_trace[slot * 8 + 2] = (unsigned)clock();
+      }
+    }
+    if (slot >= 0 && own) g_hh3_trace[slot * 8 + 3] = (unsigned)clock();
+    __syncthreads();
+    if (slot >= 0 && own) g_hh3_trace[slot * 8 + 4] = (unsigned)clock();
+  }
+}
+
 // B <- H_0^H ... applied for col = r-1 .. 0: block -= conj(tau) w (w^H block).
 // One warp per column of B (held in shared memory); the reflectors stream
 // through shared memory in chunks so each is read from L2 once per CTA.
@@ -501,6 +825,70 @@ __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict_
   if (!active) return;
   for (int k = lane; k < n; k += 32) {
     const double2 v = b[k];
+    B[(size_t)k * cols + j] = v;
+    if (out32) {
+      const int step = j / p, t = j % p;
+      out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
+    }
+  }
+}
+
+// Resident variant: all r reflectors staged in shared memory once, four warps
+// (four columns of B) per CTA, no barriers in the reflector loop.
+constexpr int kArWarps = 4;
+constexpr int kArPer = 8;  // n <= 256 for the resident apply
+__global__ void __launch_bounds__(kArWarps * 32)
+apply_reflectors_res_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
+                            const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
+                            double2* __restrict__ B, float2* __restrict__ out32, int p) {
+  extern __shared__ double2 sar[];
+  double2* ws = sar;                          // r x n reflectors
+  double2* ts = ws + (size_t)r * n;           // r taus
+  double2* bs = ts + r;                       // kArWarps x n columns
+  int* fs = reinterpret_cast<int*>(bs + (size_t)kArWarps * n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int q = threadIdx.x; q < r * n; q += blockDim.x) ws[q] = refl[q];
+  for (int q = threadIdx.x; q < r; q += blockDim.x) {
+    ts[q] = tau[q];
+    fs[q] = flags[q];
+  }
+  const int j = blockIdx.x * kArWarps + warp;
+  (void)bs;
+  __syncthreads();
+  if (j >= cols) return;
+  // the column lives in registers: lane owns rows lane + 32u (n <= 32 kArPer)
+  double2 b[kArPer];
+#pragma unroll
+  for (int u = 0; u < kArPer; ++u) {
+    const int k = lane + 32 * u;
+    b[u] = k < n ? Bin[(size_t)k * cols + j] : cd(0.0, 0.0);
+  }
+  for (int col = r - 1; col >= 0; --col) {
+    if (!fs[col]) continue;
+    const double2* w = ws + (size_t)col * n;
+    double2 wr[kArPer];
+#pragma unroll
+    for (int u = 0; u < kArPer; ++u) {
+      const int k = lane + 32 * u;
+      wr[u] = (k >= col && k < n) ? w[k] : cd(0.0, 0.0);
+    }
+    double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kArPer; u += 2) {
+      zfmac(d0, wr[u], b[u]);
+      if (u + 1 < kArPer) zfmac(d1, wr[u + 1], b[u + 1]);
+    }
+    double2 dot = d0 + d1;
+    dot = cd(warp_sum_d_(dot.x), warp_sum_d_(dot.y));
+    const double2 f = cmulc(ts[col], dot);  // conj(tau) * dot
+#pragma unroll
+    for (int u = 0; u < kArPer; ++u) b[u] = b[u] - cmul(wr[u], f);
+  }
+#pragma unroll
+  for (int u = 0; u < kArPer; ++u) {
+    const int k = lane + 32 * u;
+    if (k >= n) continue;
+    const double2 v = b[u];
     B[(size_t)k * cols + j] = v;
     if (out32) {
       const int step = j / p, t = j % p;
@@ -588,6 +976,13 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   }
   {
     const size_t rbytes = (size_t)ell * ell * sizeof(double2);
+    if (rbytes + (size_t)ell * sizeof(double) <= kSmemCap) {
+      const int warps = 4;
+      hicu_allow_max_smem((const void*)trsm_rl_kernel);
+      trsm_rl_kernel<<<(n + warps - 1) / warps, warps * 32, rbytes + (size_t)ell * sizeof(double), st>>>(
+          n, ell, w.Y, Om, w.nu, w.C, w.W);
+      if ((s = hicu_check_launch("trsm_rl_kernel"))) return s;
+    } else {
     const int warps = 8;
     const size_t rowb = (size_t)warps * ell * sizeof(double2);
     const bool sm = rbytes + rowb <= kSmemCap;
@@ -596,6 +991,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     const int blocks = (n + warps - 1) / warps;
     trsm_rows_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, w.Y, Om, w.nu, w.C, sm, w.W);
     if ((s = hicu_check_launch("trsm_rows_kernel"))) return s;
+    }
   }
   if ((s = zgemm_launch('C', 'N', ell, ell, n, w.W, ell, w.W, ell, w.M, ell, st))) return s;
   // top-r eigenpairs of M = W^H W (tridiagonal + bisection + inverse iteration)
@@ -621,6 +1017,27 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     // require the caller to size refl at 2*n*r and use its upper half as scratch.
     gws = (double2*)refl + (size_t)n * r;
   }
+  if (getenv("HICU_HOUSEHOLDER3") && n <= 32 * kHh3Per && bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
+    hicu_allow_max_smem((const void*)householder3_kernel);
+    householder3_kernel<<<1, kHh3Threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream>>>(
+        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev);
+    if (getenv("HICU_HH_TRACE")) {
+      unsigned h[64];
+      cudaStreamSynchronize((cudaStream_t)stream);
+      cudaMemcpyFromSymbol(h, g_hh3_trace, sizeof(h));
+      for (int q = 0; q < 3; ++q)
+        fprintf(stderr, "householder3 col %d: cols-before-own %u | build %u | rest %u | barrier %u (cycles)\n",
+                q == 0 ? 5 : (q == 1 ? 30 : 50), h[q * 8 + 1] - h[q * 8 + 0], h[q * 8 + 2] - h[q * 8 + 1],
+                h[q * 8 + 3] - h[q * 8 + 2], h[q * 8 + 4] - h[q * 8 + 3]);
+    }
+    return hicu_check_launch("householder3_kernel");
+  }
+  if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
+    hicu_allow_max_smem((const void*)householder2_kernel);
+    householder2_kernel<<<1, 1024, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream>>>(
+        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev);
+    return hicu_check_launch("householder2_kernel");
+  }
   hicu_allow_max_smem((const void*)householder_kernel);
   householder_kernel<<<1, 1024, (sm ? bytes : 0) + (size_t)n * sizeof(double2), (cudaStream_t)stream>>>(
       n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
@@ -631,6 +1048,16 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
                                      const void* Bin, void* B, void* out32, int p, void* stream) {
   if (n < 1 || r < 0 || cols < 1 || !B || !Bin) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad p");
+  {
+    const size_t res = ((size_t)r * n + r + (size_t)kArWarps * n) * sizeof(double2) + (size_t)r * sizeof(int);
+    if (r >= 1 && n <= 32 * kArPer && res <= (size_t)210 * 1024) {
+      hicu_allow_max_smem((const void*)apply_reflectors_res_kernel);
+      apply_reflectors_res_kernel<<<(cols + kArWarps - 1) / kArWarps, kArWarps * 32, res, (cudaStream_t)stream>>>(
+          n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B,
+          (float2*)out32, p ? p : 1);
+      return hicu_check_launch("apply_reflectors_res_kernel");
+    }
+  }
   int warps = 8;
   while (warps > 1 && (size_t)(warps + kReflChunk) * n * sizeof(double2) > kSmemCap) warps >>= 1;
   const size_t smem = (size_t)(warps + kReflChunk) * n * sizeof(double2);

@@ -9,6 +9,8 @@
 // Used by hicu_nystrom (dense.cu); no reference function (the reference
 // gets its singular vectors from LAPACK zgesdd, subspace.py:150).
 #include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -144,6 +146,406 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
   if (tid == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
 }
 
+// Latency-oriented variant for l <= kHetrd2Max (A resident in shared memory):
+// two block barriers per step.  Phase B: warp-per-row matvec y = A22 v with
+// batched shuffle reductions (the rows of one warp reduce together so their
+// shuffle chains overlap), w = tau y and the w^H v partials.  Phase D: the
+// rank-2 update; warp 0 owns the next pivot row k+1 and builds the next
+// reflector right after updating it (norm by shuffles, v written into the
+// other half of a double-buffered smem vector).  The reflector uses row k
+// (A[k][j] = conj(A[j][k]), both triangles are kept).
+constexpr int kHetrd2Max = 110;
+constexpr int kHetrd2Rows = 8;  // rows per warp in phase B (16 warps x 8 >= kHetrd2Max)
+
+__device__ __forceinline__ void hetrd2_reflector(int l, int k, const double2* A, int lda, int lane, double* d,
+                                                 double* e, double2* tau, double2* s_tau, double2* sv_next) {
+  // x = column k below the diagonal = conj(row k), alpha = x[k+1]
+  double t = 0.0;
+  for (int j = k + 2 + lane; j < l; j += 32) t += abs2d(A[(size_t)k * lda + j]);
+  t = warp_sum_d(t);
+  double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
+  double beta = 0.0;
+  if (lane == 0) {
+    const double2 alpha = conjd(A[(size_t)k * lda + k + 1]);
+    if (t == 0.0 && alpha.y == 0.0) {
+      beta = alpha.x;  // H = I
+    } else {
+      beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + t), alpha.x);
+      const double ib = 1.0 / beta;
+      tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
+      const double2 den = cd(alpha.x - beta, alpha.y);
+      const double idd = 1.0 / abs2d(den);
+      scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
+    }
+    e[k] = beta;
+    d[k] = A[(size_t)k * lda + k].x;
+    tau[k] = tv;
+    *s_tau = tv;
+  }
+  scal.x = __shfl_sync(0xffffffffu, scal.x, 0);
+  scal.y = __shfl_sync(0xffffffffu, scal.y, 0);
+  for (int j = k + 1 + lane; j < l; j += 32)
+    sv_next[j] = (j == k + 1) ? cd(1.0, 0.0) : cmul(conjd(A[(size_t)k * lda + j]), scal);
+}
+
+__global__ void __launch_bounds__(512)
+hetrd2_kernel(int l, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
+              double2* __restrict__ tau, double2* __restrict__ Vt) {
+  extern __shared__ double2 A[];
+  const int lda = l + 1;
+  __shared__ double2 sv[2][kHetrd2Max + 2], sw[kHetrd2Max + 2];
+  __shared__ double2 redz[16];
+  __shared__ double2 s_tau[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = 16;
+  for (int q = tid; q < l * l; q += 512) A[(size_t)(q / l) * lda + q % l] = Ain[q];
+  for (int q = tid; q < l * l; q += 512) Vt[q] = cd(0.0, 0.0);
+  __syncthreads();
+  if (warp == 0 && l > 1) hetrd2_reflector(l, 0, A, lda, lane, d, e, tau, &s_tau[0], sv[0]);
+  __syncthreads();
+  for (int k = 0; k + 1 < l; ++k) {
+    const int k1 = k + 1, par = k & 1;
+    const double2 tk = s_tau[par];
+    const bool active = !(tk.x == 0.0 && tk.y == 0.0);
+    const double2* v = sv[par];
+    // ---- phase B: y = A22 v (warp per row, batched reductions), w = tau y, w^H v ----
+    if (active) {
+      double2 acc[kHetrd2Rows];
+#pragma unroll
+      for (int q = 0; q < kHetrd2Rows; ++q) {
+        acc[q] = cd(0.0, 0.0);
+        const int i = k1 + warp + q * nw;
+        if (i < l) {
+          const double2* Ai = A + (size_t)i * lda;
+          for (int j = k1 + lane; j < l; j += 32) zfma(acc[q], Ai[j], v[j]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < kHetrd2Rows; ++q) {
+          acc[q].x += __shfl_xor_sync(0xffffffffu, acc[q].x, o);
+          acc[q].y += __shfl_xor_sync(0xffffffffu, acc[q].y, o);
+        }
+      double2 pdot = cd(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < kHetrd2Rows; ++q) {
+        const int i = k1 + warp + q * nw;
+        if (i < l) {
+          const double2 wi = cmul(tk, acc[q]);
+          const double2 vi = v[i];
+          zfmac(pdot, wi, vi);
+          if (lane == 0) {
+            sw[i] = wi;
+            Vt[(size_t)k * l + i] = vi;
+          }
+        }
+      }
+      if (lane == 0) redz[warp] = pdot;
+    }
+    __syncthreads();
+    // ---- phase D: A22 -= v w'^H + w' v^H, w' = w + alpha2 v; warp 0 then builds the next reflector ----
+    double2* vn = sv[par ^ 1];
+    if (active) {
+      double2 dot = cd(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < nw; ++q) dot = dot + redz[q];
+      const double2 td = cmul(tk, dot);
+      const double2 a2 = cd(-0.5 * td.x, -0.5 * td.y);
+      // warp 0: row k1 only; warps 1..15: rows k1+1.. round-robin
+      const int i0 = warp == 0 ? k1 : k1 + warp;
+      const int istep = warp == 0 ? l : nw - 1;
+      for (int i = i0; i < l; i += istep) {
+        const double2 vi = v[i];
+        const double2 wi = sw[i] + cmul(a2, vi);
+        double2* Ai = A + (size_t)i * lda;
+        for (int j = k1 + lane; j < l; j += 32) {
+          const double2 vj = v[j];
+          const double2 wj = sw[j] + cmul(a2, vj);
+          Ai[j] = Ai[j] - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
+        }
+      }
+    }
+    if (warp == 0 && k1 + 1 < l) {
+      __syncwarp();
+      hetrd2_reflector(l, k1, A, lda, lane, d, e, tau, &s_tau[par ^ 1], vn);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+}
+
+// Thread-per-row variant (128 threads, l <= 128, A in shared memory with
+// lda = l + 1 rounded up to 1 mod 8 so a warp walking 32 rows of one column
+// touches all 32 banks).  Per step: [A] thread j forms v_j, barrier; [B]
+// thread i forms y_i = A22[i, :] v (no cross-thread reduction), w_i = tau y_i
+// and the w^H v partials, barrier; [D] thread i updates row i,
+//   A[i][j] -= v_i conj(w_j) + (w_i + c v_i) conj(v_j),  c = 2 Re(alpha2)
+// (the Hermitian rank-2 update with w' = w + alpha2 v folded in), and thread
+// 0, which owns the next pivot row, accumulates its norm during the update
+// and forms the next reflector; barrier.  Instruction count per step is
+// ~20 m per thread with no shuffles on the matvec.
+constexpr int kHetrd3Max = 128;
+
+// Reflector scalars for step k of the tridiagonalisation from row k:
+// x = conj(A[k][k+1:]), alpha = x[0], tail = |x[1:]|^2.
+__device__ __forceinline__ void hetrd3_reflector(int k, double tail, double2 akk1, double dkk, double* d, double* e,
+                                                 double2* tau, double2* s_tau, double2* s_sc) {
+  const double2 alpha = conjd(akk1);
+  double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
+  double beta;
+  if (tail == 0.0 && alpha.y == 0.0) {
+    beta = alpha.x;  // H = I
+  } else {
+    beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + tail), alpha.x);
+    const double ib = 1.0 / beta;
+    tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
+    const double2 den = cd(alpha.x - beta, alpha.y);
+    const double idd = 1.0 / abs2d(den);
+    scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
+  }
+  e[k] = beta;
+  d[k] = dkk;
+  tau[k] = tv;
+  *s_tau = tv;
+  *s_sc = scal;
+}
+
+__global__ void __launch_bounds__(128)
+hetrd3_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
+              double2* __restrict__ tau, double2* __restrict__ Vt) {
+  extern __shared__ double2 A[];
+  __shared__ double2 sv[kHetrd3Max], sw[kHetrd3Max];
+  __shared__ double2 red[4];
+  __shared__ double2 s_tau, s_sc;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int q = t; q < l * l; q += 128) A[(size_t)(q / l) * lda + q % l] = Ain[q];
+  for (int q = t; q < l * l; q += 128) Vt[q] = cd(0.0, 0.0);
+  __syncthreads();
+  if (t == 0 && l > 1) {
+    double tail = 0.0;
+    for (int j = 2; j < l; ++j) tail += abs2d(A[j]);
+    hetrd3_reflector(0, tail, A[1], A[0].x, d, e, tau, &s_tau, &s_sc);
+  }
+  __syncthreads();
+  for (int k = 0; k + 1 < l; ++k) {
+    const int k1 = k + 1;
+    const double2 tk = s_tau, sc = s_sc;
+    if (tk.x == 0.0 && tk.y == 0.0) {
+      // H = I: the trailing block is unchanged; thread 0 forms the next reflector from row k1
+      if (t == 0 && k1 + 1 < l) {
+        double tail = 0.0;
+        for (int j = k1 + 2; j < l; ++j) tail += abs2d(A[(size_t)k1 * lda + j]);
+        hetrd3_reflector(k1, tail, A[(size_t)k1 * lda + k1 + 1], A[(size_t)k1 * lda + k1].x, d, e, tau, &s_tau, &s_sc);
+      }
+      __syncthreads();
+      continue;
+    }
+    // [A] v_j = (j == k1) ? 1 : conj(A[k][j]) sc
+    {
+      const int j = k1 + t;
+      if (j < l) {
+        const double2 vj = (j == k1) ? cd(1.0, 0.0) : cmul(conjd(A[(size_t)k * lda + j]), sc);
+        sv[j] = vj;
+        Vt[(size_t)k * l + j] = vj;
+      }
+    }
+    __syncthreads();
+    // [B] y_i = sum_j A[i][j] v_j (two accumulators), w_i = tau y_i, partial conj(w_i) v_i
+    const int i = k1 + t;
+    double2 wi = cd(0.0, 0.0), vi = cd(0.0, 0.0);
+    {
+      double2 pd = cd(0.0, 0.0);
+      if (i < l) {
+        const double2* Ai = A + (size_t)i * lda;
+        double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0), a2 = cd(0.0, 0.0), a3 = cd(0.0, 0.0);
+        int j = k1;
+        for (; j + 3 < l; j += 4) {  // four independent chains (DFMA latency ~9 cycles)
+          const double2 x0 = Ai[j], x1 = Ai[j + 1], x2 = Ai[j + 2], x3 = Ai[j + 3];
+          const double2 y0 = sv[j], y1 = sv[j + 1], y2 = sv[j + 2], y3 = sv[j + 3];
+          zfma(a0, x0, y0);
+          zfma(a1, x1, y1);
+          zfma(a2, x2, y2);
+          zfma(a3, x3, y3);
+        }
+        for (; j < l; ++j) zfma(a0, Ai[j], sv[j]);
+        a0 = a0 + a2;
+        a1 = a1 + a3;
+        wi = cmul(tk, a0 + a1);
+        vi = sv[i];
+        sw[i] = wi;
+        zfmac(pd, wi, vi);
+      }
+      pd = cd(warp_sum_d(pd.x), warp_sum_d(pd.y));
+      if (lane == 0) red[warp] = pd;
+    }
+    __syncthreads();
+    // [D] rank-2 update of row i; thread 0 (row k1) then forms the next reflector
+    {
+      const double2 dot = red[0] + red[1] + red[2] + red[3];
+      const double2 td = cmul(tk, dot);
+      const double c = -td.x;  // 2 Re(alpha2), alpha2 = -tau (w^H v) / 2
+      if (i < l) {
+        const double2 wpi = wi + c * vi;
+        double2* Ai = A + (size_t)i * lda;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;  // |row k1|^2 partials (used by thread 0)
+        int j = k1;
+        for (; j + 3 < l; j += 4) {
+          const double2 v0 = sv[j], v1 = sv[j + 1], v2 = sv[j + 2], v3 = sv[j + 3];
+          const double2 w0 = sw[j], w1 = sw[j + 1], w2 = sw[j + 2], w3 = sw[j + 3];
+          const double2 n0 = Ai[j] - cmul(vi, conjd(w0)) - cmul(wpi, conjd(v0));
+          const double2 n1 = Ai[j + 1] - cmul(vi, conjd(w1)) - cmul(wpi, conjd(v1));
+          const double2 n2 = Ai[j + 2] - cmul(vi, conjd(w2)) - cmul(wpi, conjd(v2));
+          const double2 n3 = Ai[j + 3] - cmul(vi, conjd(w3)) - cmul(wpi, conjd(v3));
+          Ai[j] = n0;
+          Ai[j + 1] = n1;
+          Ai[j + 2] = n2;
+          Ai[j + 3] = n3;
+          if (j >= k1 + 2) t0 += abs2d(n0);
+          if (j + 1 >= k1 + 2) t1 += abs2d(n1);
+          t2 += abs2d(n2);
+          t3 += abs2d(n3);
+        }
+        for (; j < l; ++j) {
+          const double2 nv = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(sv[j]));
+          Ai[j] = nv;
+          if (j >= k1 + 2) t0 += abs2d(nv);
+        }
+        const double tail = (t0 + t1) + (t2 + t3);
+        if (t == 0 && k1 + 1 < l)
+          hetrd3_reflector(k1, tail, Ai[k1 + 1], Ai[k1].x, d, e, tau, &s_tau, &s_sc);
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+}
+
+// 512-thread variant: 4 threads per row (thread (row i, quarter q) owns the
+// columns j = k1 + q + 4u), up to 128 rows, lda == 4 mod 8 so the 8 lanes of a
+// 16-byte shared-memory phase (2 rows x 4 quarters) hit disjoint banks.  The
+// reflector vector is formed on the fly from row k (v_j = conj(A[k][j]) sc),
+// so a step needs two barriers: [B] matvec partials + 4-lane reduction,
+// w_i = tau y_i, w^H v partials; [D] rank-2 update (c = 2 Re(alpha2) folded
+// into a per-row factor) while the four owners of row k1 accumulate its tail
+// norm, then thread 0 forms the next reflector.
+constexpr int kHetrd4Max = 128;
+
+__global__ void __launch_bounds__(512)
+hetrd4_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
+              double2* __restrict__ tau, double2* __restrict__ Vt) {
+  extern __shared__ double2 A[];
+  __shared__ double2 sw[kHetrd4Max];
+  __shared__ double2 red[16];
+  __shared__ double2 s_tau, s_sc;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int qd = t & 3, rowo = t >> 2;  // quarter, row offset
+
+  for (int x = t; x < l * l; x += 512) A[(size_t)(x / l) * lda + x % l] = Ain[x];
+  for (int x = t; x < l * l; x += 512) Vt[x] = cd(0.0, 0.0);
+  __syncthreads();
+  if (t == 0 && l > 1) {
+    double tail = 0.0;
+    for (int j = 2; j < l; ++j) tail += abs2d(A[j]);
+    hetrd3_reflector(0, tail, A[1], A[0].x, d, e, tau, &s_tau, &s_sc);
+  }
+  __syncthreads();
+  for (int k = 0; k + 1 < l; ++k) {
+    const int k1 = k + 1;
+    const double2 tk = s_tau, sc = s_sc;
+    const double2* Ak = A + (size_t)k * lda;
+    const int i = k1 + rowo;
+    const bool has_row = i < l;
+    if (tk.x == 0.0 && tk.y == 0.0) {
+      if (t == 0 && k1 + 1 < l) {
+        double tail = 0.0;
+        for (int j = k1 + 2; j < l; ++j) tail += abs2d(A[(size_t)k1 * lda + j]);
+        hetrd3_reflector(k1, tail, A[(size_t)k1 * lda + k1 + 1], A[(size_t)k1 * lda + k1].x, d, e, tau, &s_tau,
+                         &s_sc);
+      }
+      __syncthreads();
+      continue;
+    }
+    // ---- [B] y_i partial over my quarter, 4-lane reduction, w_i, w^H v partials ----
+    double2 vi = cd(0.0, 0.0), wi = cd(0.0, 0.0);
+    {
+      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0);
+      if (has_row) {
+        const double2* Ai = A + (size_t)i * lda;
+        int j = k1 + qd;
+        for (; j + 4 < l; j += 8) {
+          const double2 v0 = (j == k1) ? cd(1.0, 0.0) : cmul(conjd(Ak[j]), sc);
+          const double2 v1 = cmul(conjd(Ak[j + 4]), sc);
+          zfma(a0, Ai[j], v0);
+          zfma(a1, Ai[j + 4], v1);
+        }
+        if (j < l) {
+          const double2 v0 = (j == k1) ? cd(1.0, 0.0) : cmul(conjd(Ak[j]), sc);
+          zfma(a0, Ai[j], v0);
+        }
+        vi = (i == k1) ? cd(1.0, 0.0) : cmul(conjd(Ak[i]), sc);
+      }
+      double2 y = a0 + a1;
+      y.x += __shfl_xor_sync(0xffffffffu, y.x, 1);
+      y.y += __shfl_xor_sync(0xffffffffu, y.y, 1);
+      y.x += __shfl_xor_sync(0xffffffffu, y.x, 2);
+      y.y += __shfl_xor_sync(0xffffffffu, y.y, 2);
+      double2 pd = cd(0.0, 0.0);
+      if (has_row) {
+        wi = cmul(tk, y);
+        if (qd == 0) {
+          sw[i] = wi;
+          Vt[(size_t)k * l + i] = vi;
+          zfmac(pd, wi, vi);
+        }
+      }
+      pd = cd(warp_sum_d(pd.x), warp_sum_d(pd.y));
+      if (lane == 0) red[warp] = pd;
+    }
+    __syncthreads();
+    // ---- [D] A[i][j] -= v_i conj(w_j) + (w_i + c v_i) conj(v_j) over my quarter ----
+    {
+      double2 dot = cd(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < 16; ++w) dot = dot + red[w];
+      const double c = -cmul(tk, dot).x;  // 2 Re(alpha2), alpha2 = -tau (w^H v) / 2
+      double tl0 = 0.0, tl1 = 0.0;
+      if (has_row) {
+        const double2 wpi = wi + c * vi;
+        double2* Ai = A + (size_t)i * lda;
+        int j = k1 + qd;
+        for (; j + 4 < l; j += 8) {
+          const double2 v0 = (j == k1) ? cd(1.0, 0.0) : cmul(conjd(Ak[j]), sc);
+          const double2 v1 = cmul(conjd(Ak[j + 4]), sc);
+          const double2 n0 = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(v0));
+          const double2 n1 = Ai[j + 4] - cmul(vi, conjd(sw[j + 4])) - cmul(wpi, conjd(v1));
+          Ai[j] = n0;
+          Ai[j + 4] = n1;
+          if (j >= k1 + 2) tl0 += abs2d(n0);
+          tl1 += abs2d(n1);
+        }
+        if (j < l) {
+          const double2 v0 = (j == k1) ? cd(1.0, 0.0) : cmul(conjd(Ak[j]), sc);
+          const double2 n0 = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(v0));
+          Ai[j] = n0;
+          if (j >= k1 + 2) tl0 += abs2d(n0);
+        }
+      }
+      if (warp == 0) {  // row k1 = threads 0..3
+        double tl = tl0 + tl1;
+        tl += __shfl_xor_sync(0xffffffffu, tl, 1);
+        tl += __shfl_xor_sync(0xffffffffu, tl, 2);
+        if (t == 0 && k1 + 1 < l) {
+          const double2* Ar = A + (size_t)k1 * lda;
+          hetrd3_reflector(k1, tl, Ar[k1 + 1], Ar[k1].x, d, e, tau, &s_tau, &s_sc);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+}
+
 // 1/q to ~1e-15 relative: fp32 seed (MUFU) + two Newton steps in fp64
 // (the Sturm count only needs the sign of each pivot).  Falls back to an IEEE
 // division when q is outside the fp32 exponent range.
@@ -166,6 +568,36 @@ __device__ __forceinline__ int sturm_count(int l, const double* d, const double*
     q = d[i] - x - e2[i - 1] / q;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// Division-free Sturm count: the leading principal minors p_i of T - xI obey
+// p_{i+1} = (d_i - x) p_i - e_i^2 p_{i-1}; the number of negative ratios
+// q_i = p_i / p_{i-1} (the LDL^T pivots of sturm_count) is the number of
+// eigenvalues below x.  Two dependent FMAs per step instead of a division;
+// |q_i| < pivmin is mapped to q_i = -pivmin exactly as in sturm_count, and
+// the pair (p_i, p_{i-1}) is rescaled by a power of two every 8 steps.
+__device__ __forceinline__ int sturm_count_poly(int l, const double* d, const double* e2, double x, double pivmin) {
+  double pm = 1.0, p = d[0] - x;
+  if (fabs(p) < pivmin) p = -pivmin;
+  int cnt = p < 0.0;
+  for (int i = 1; i < l; ++i) {
+    double pn = (d[i] - x) * p - e2[i - 1] * pm;
+    if (fabs(pn) < pivmin * fabs(p)) pn = -pivmin * p;  // q = pn / p = -pivmin
+    cnt += (pn < 0.0) != (p < 0.0);
+    pm = p;
+    p = pn;
+    if ((i & 7) == 0) {
+      // scale both by 2^-e, e = exponent of max(|p|, |pm|)
+      const double m = fmax(fabs(p), fabs(pm));
+      const int ex = (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1023;
+      const double sc = __longlong_as_double((long long)(1023 - ex) << 52);
+      if (ex > -1000 && ex < 1000) {
+        p *= sc;
+        pm *= sc;
+      }
+    }
   }
   return cnt;
 }
@@ -203,7 +635,7 @@ __global__ void stebz_kernel(int l, int r, const double* __restrict__ dg, const 
       const double w = hi - lo;
       if (w <= 4.4e-16 * fmax(fabs(lo), fabs(hi)) + 4.0 * pivmin) break;
       const double x = lo + w * (double)(lane + 1) / 33.0;
-      const int c = sturm_count(l, d, e2, x, pivmin);
+      const int c = sturm_count_poly(l, d, e2, x, pivmin);
       const unsigned b = __ballot_sync(0xffffffffu, c >= k + 1);
       if (b == 0u) {
         lo = lo + w * 32.0 / 33.0;
@@ -400,6 +832,59 @@ __global__ void back_transform_kernel(int l, int r, const double2* __restrict__ 
     for (int i = lane; i < l; i += 32) F[(size_t)i * r + j] = x[i];
 }
 
+// Resident variant: every reflector (Vt, (l-1) x l) staged in shared memory
+// once, four warps per CTA, one eigenvector per warp, no barriers in the
+// reflector loop (one warp per scheduler: the dot-reduce-axpy chains do not
+// contend for issue slots).
+constexpr int kBtWarps = 4;
+constexpr int kBtPer = 4;  // l <= 128 for the resident back-transform
+__global__ void __launch_bounds__(kBtWarps * 32)
+back_transform_res_kernel(int l, int r, const double2* __restrict__ Vt, const double2* __restrict__ tau,
+                          const double* __restrict__ z, double2* __restrict__ F) {
+  extern __shared__ double2 sm3[];
+  double2* vs = sm3;                          // (l-1) x l reflectors
+  double2* ts = vs + (size_t)(l - 1) * l;     // l-1 taus
+  double2* xs = ts + l;                       // kBtWarps x l vectors
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = (l - 1) * l;
+  for (int q = threadIdx.x; q < nv; q += blockDim.x) vs[q] = Vt[q];
+  for (int q = threadIdx.x; q < l - 1; q += blockDim.x) ts[q] = tau[q];
+  const int j = blockIdx.x * kBtWarps + warp;
+  (void)xs;
+  __syncthreads();
+  if (j >= r) return;
+  // the eigenvector lives in registers: lane owns entries lane + 32u (l <= 32 kBtPer)
+  double2 x[kBtPer];
+#pragma unroll
+  for (int u = 0; u < kBtPer; ++u) {
+    const int i = lane + 32 * u;
+    x[u] = i < l ? cd(z[(size_t)j * l + i], 0.0) : cd(0.0, 0.0);
+  }
+  for (int k = l - 2; k >= 0; --k) {
+    const double2 tk = ts[k];
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    const double2* v = vs + (size_t)k * l;
+    double2 vr[kBtPer];
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) {  // all loads issued before any use
+      const int i = lane + 32 * u;
+      vr[u] = (i > k && i < l) ? v[i] : cd(0.0, 0.0);
+    }
+    double2 dot = cd(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) zfmac(dot, vr[u], x[u]);
+    dot = warp_sum_z(dot);
+    const double2 f = cmul(tk, dot);
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) x[u] = x[u] - cmul(vr[u], f);
+  }
+#pragma unroll
+  for (int u = 0; u < kBtPer; ++u) {
+    const int i = lane + 32 * u;
+    if (i < l) F[(size_t)i * r + j] = x[u];
+  }
+}
+
 }  // namespace
 
 size_t hicu_heev_top_workspace(int l, int r) {
@@ -426,13 +911,28 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   const size_t abytes = (size_t)l * (l + 1) * sizeof(double2);
   const bool sm = abytes <= 180 * 1024;
   if (sm) {
-    hicu_allow_max_smem((const void*)hetrd_kernel<true>);
-    hetrd_kernel<true><<<1, 512, abytes, st>>>(l, A, Aws, d, e, tau, Vt);
+    const int lda3 = ((l + 1 + 6) / 8) * 8 + 1;  // >= l + 1, == 1 mod 8
+    const size_t a3 = (size_t)l * lda3 * sizeof(double2);
+    const int lda4 = ((l + 1 + 3) / 8) * 8 + 4;  // >= l + 1, == 4 mod 8
+    const size_t a4 = (size_t)l * lda4 * sizeof(double2);
+    if (l <= kHetrd4Max && a4 <= 180 * 1024) {
+      hicu_allow_max_smem((const void*)hetrd4_kernel);
+      hetrd4_kernel<<<1, 512, a4, st>>>(l, lda4, A, d, e, tau, Vt);
+    } else if (l <= kHetrd3Max && a3 <= 180 * 1024) {
+      hicu_allow_max_smem((const void*)hetrd3_kernel);
+      hetrd3_kernel<<<1, 128, a3, st>>>(l, lda3, A, d, e, tau, Vt);
+    } else if (l <= kHetrd2Max) {
+      hicu_allow_max_smem((const void*)hetrd2_kernel);
+      hetrd2_kernel<<<1, 512, abytes, st>>>(l, A, d, e, tau, Vt);
+    } else {
+      hicu_allow_max_smem((const void*)hetrd_kernel<true>);
+      hetrd_kernel<true><<<1, 512, abytes, st>>>(l, A, Aws, d, e, tau, Vt);
+    }
   } else {
     hetrd_kernel<false><<<1, 512, 0, st>>>(l, A, Aws, d, e, tau, Vt);
   }
   if ((s = hicu_check_launch("hetrd_kernel"))) return s;
-  const int wpb = 8;
+  const int wpb = 1;  // one warp (one eigenvalue) per SM: the Sturm recurrence is a division chain
   stebz_kernel<<<(r + wpb - 1) / wpb, wpb * 32, 0, st>>>(l, r, d, e, lam);
   if ((s = hicu_check_launch("stebz_kernel"))) return s;
   {
@@ -445,6 +945,12 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   if ((s = hicu_check_launch("stein_kernel"))) return s;
   cluster_orth_kernel<<<1, 256, 0, st>>>(l, r, lam, z, 1e-9);
   if ((s = hicu_check_launch("cluster_orth_kernel"))) return s;
+  const size_t res = ((size_t)(l - 1) * l + l + (size_t)kBtWarps * l) * sizeof(double2);
+  if (res <= 200 * 1024 && l <= 32 * kBtPer) {
+    hicu_allow_max_smem((const void*)back_transform_res_kernel);
+    back_transform_res_kernel<<<(r + kBtWarps - 1) / kBtWarps, kBtWarps * 32, res, st>>>(l, r, Vt, tau, z, F);
+    return hicu_check_launch("back_transform_res_kernel");
+  }
   const int bw = 8;
   const size_t smem = ((size_t)bw * l + (size_t)kBtChunk * l) * sizeof(double2);
   hicu_allow_max_smem((const void*)back_transform_kernel);

@@ -12,8 +12,11 @@ slice; metric = HICU outer iterations per second.
   compute stream; L2 flushed between steps (256 MiB write, untimed).
 * ``e2e``: the public API ``hicu_reconstruct`` from host numpy arrays
   (draws made on host worker threads, uploaded, result downloaded).
-* ``roofline``: the dominant kernel class from the native CUDA-event
-  profiler over the timed region.
+* ``roofline``: the dominant tensor-core kernel class (Gram or one of the
+  three convolutions) from the native CUDA-event profiler over the timed
+  region, against the measured TF32 peak / 3 (3xTF32); ``roofline_all``
+  lists every class, including the HBM-bound update and the fp64 nullspace
+  (latency-bound, reported separately as SURVEY §8d asks).
 * ``cpu_baseline``: the oracle port (numpy/scipy restatement of the
   reference) on a bounded sample (coil compression + one outer iteration per
   stage), extrapolated to the schedule; rank 0, N=1 only.
@@ -321,7 +324,6 @@ def run_ours(args):
             flops_total[k] += w[k] * per_launch_groups * args.steps
             launches_expected[k] += per_launch_groups * args.steps
     ms_by = {k: v["ms"] for k, v in kinds.items()}
-    dom = max(ms_by, key=ms_by.get)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -329,21 +331,48 @@ def run_ours(args):
         pass
     tf32 = json.load(open(os.path.join(ROOT, "profiles", "tf32_peak_r01.json")))
     hbm = peaks.get("hbm_gbs", 6650.0)
-    if dom in flops_total:
-        achieved = flops_total[dom] / (ms_by[dom] * 1e-3) / 1e12
-        peak = tf32["tf32_tflops"] / 3.0
-        roof = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": None,
-                "peak_source": "measured TF32 dense (profiles/tf32_peak_r01.json) / 3 for 3xTF32 FP32-grade",
-                "avg_launch_ms": ms_by[dom] / max(1, kinds[dom]["launches"])}
-    elif dom == "update":
+    # ncu --set full captures of full-stage launches (scripts/ncu_full.sh -> profiles/r01_ncu_full_v2.json)
+    ncu_by = {}
+    try:
+        for rec in json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full_v2.json"))):
+            ncu_by[rec["kernel"]] = rec
+    except (OSError, ValueError):
+        pass
+    ncu_name = {"gram": "gram_tc_kernel", "conv_fwd": "void conv_tc_kernel<0>", "scatter": "void conv_tc_kernel<2>",
+                "conv_els": "void conv_tc_kernel<1>", "update": "update_kernel"}
+
+    def traffic(kind):
+        rec = ncu_by.get(ncu_name.get(kind, ""))
+        if not rec or rec.get("dram_read_bytes") is None:
+            return None
+        return rec["dram_read_bytes"] + (rec.get("dram_write_bytes") or 0.0)
+
+    tf32_peak = tf32["tf32_tflops"] / 3.0
+    roof_all = {}
+    for k in ("gram", "conv_fwd", "scatter", "conv_els"):
+        if k not in ms_by or ms_by[k] <= 0:
+            continue
+        nl = max(1, kinds[k]["launches"])
+        ach = flops_total[k] / (ms_by[k] * 1e-3) / 1e12
+        roof_all[k] = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
+                       "frac": ach / tf32_peak, "traffic": traffic(k), "launches": nl,
+                       "avg_launch_ms": ms_by[k] / nl, "flops_per_launch_avg": flops_total[k] / nl}
+    if "update" in ms_by and ms_by["update"] > 0:
         bytes_total = sum(w["update_bytes"] * w["iters"] * w["G"] for w in work) * args.steps
-        achieved = bytes_total / (ms_by[dom] * 1e-3) / 1e9
-        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
-    else:
-        roof = {"kernel": dom, "bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None,
-                "traffic": None, "note": "fp64 small dense algebra (single-CTA), latency-bound"}
+        ach = bytes_total / (ms_by["update"] * 1e-3) / 1e9
+        roof_all["update"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                              "traffic": traffic("update"), "launches": kinds["update"]["launches"]}
+    for k in ("nystrom", "householder"):
+        if k in ms_by:
+            roof_all[k] = {"bound": "fp64 latency (single-CTA small dense algebra, reported separately, SURVEY 8d)",
+                           "ms_per_step": ms_by[k] / args.steps,
+                           "us_per_iteration": 1e3 * ms_by[k] / (args.steps * spec.iterations)}
+    # the roofline object: the dominant tensor-core kernel class (K1 Gram / K4-K6 convolutions)
+    dom = max((k for k in roof_all if roof_all[k]["bound"] == "tensor"), key=lambda k: ms_by[k])
+    roof = dict(roof_all[dom])
+    roof.update({"kernel": dom, "peak_source": "measured TF32 dense (profiles/tf32_peak_r01.json) / 3 for 3xTF32",
+                 "achieved_def": "algorithmic flops of all launches of the class / their summed CUDA-event time",
+                 "traffic_def": "ncu dram read+write bytes of one full-stage launch (profiles/r01_ncu_full_v2.json)"})
     share = {k: (v / sum(ms_by.values()) if sum(ms_by.values()) > 0 else 0.0) for k, v in ms_by.items()}
     grad_tflops = sum(flops_total.values()) / (total_ms * 1e-3 / max(world, 1)) / 1e12 if world == 1 else None
 
@@ -363,7 +392,7 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "c64 (fp32 FMA; fp64 reductions and nullspace)",
             "data": "synthetic", "config": workload_config(spec), "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches) // max(1, args.steps),
-            "roofline": roof, "cpu_baseline": cpu, "clocks": clock_info,
+            "roofline": roof, "roofline_all": roof_all, "cpu_baseline": cpu, "clocks": clock_info,
             "kernel_share": share, "kernel_ms_per_step": {k: v / args.steps for k, v in ms_by.items()},
             "gram_grad_tflops": grad_tflops,
             "step_ms": times,

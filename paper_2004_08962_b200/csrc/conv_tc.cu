@@ -129,15 +129,6 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-// 3xTF32 split of an A operand element without rewriting it: the tensor core
-// reads a tf32 operand as the top 19 bits of the fp32 container (truncation),
-// so the raw value acts as hi = trunc(x) and lo = x - trunc(x) is exact in
-// fp32; lo is then rounded to nearest tf32 (error <= 2^-21 |x|).
-__device__ __forceinline__ float tf32_lo(float x) {
-  const float lo = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  return __uint_as_float((__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u);
-}
-
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Scatter epilogue for one k-space position: data consistency + the four
@@ -397,7 +388,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
 #pragma unroll 4
             for (int i = ct; i < kTileM * 4; i += 128) {
               const float4 v = hi4[i];
-              lo4[i] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+              lo4[i] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
             }
           }
           tc::fence_proxy_async();

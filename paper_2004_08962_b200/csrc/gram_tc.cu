@@ -33,9 +33,11 @@
 // Scope: coil-separable support with Nc = 8 (16 floats per tap), no circular
 // axes, <= 3 spatial axes, 8..128 spatial taps.  Other geometries use the SIMT
 // kernel (gram_simt.cu).
+#include <cuda.h>
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace {
 
@@ -317,6 +319,260 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed variant (gram_tc2_kernel).  A planar copy Xt[f][position] of the
+// k-space (f = the 16 floats of one spatial position: 8 coils x re/im) makes
+// every tap's operand tile K-major along positions, so the producer is one
+// TMA box [16 positions x 16 floats] (SWIZZLE_64B, 1 KB) per tap per k-block
+// instead of 4 warps of scalar gathers.  Converter warps write A_lo =
+// rna(x - trunc(x)) next to the raw tile (the tensor core reads the raw fp32
+// container as trunc(x) = A_hi) and zero the K columns past the region line.
+// MMA issue, chained TMEM accumulators, epilogue and the split-K reduction are
+// those of gram_tc_kernel.
+// Warp roles (704 threads): warp 0 TMA producer, warp 1 TMEM owner + MMA
+// issuer, warps 2-5 converters, warps 6-21 epilogue.
+constexpr int kEpi0v2 = 6;
+constexpr int kThreads2 = (kEpi0v2 + kEpiWarps) * 32;
+constexpr int kMaxTaps2 = 128;
+
+// Blocked planar copies of the k-space for the TMA producer.  Copy b (one per
+// last-axis kernel offset, b < kext_last <= kMaxShift) is shifted by
+// sigma_b = (roff_last + b) mod 16 positions and stored as
+//   Xt_b[line][blk][f][t] = X[line][16 blk + t + sigma_b][f]   (0 past the line)
+// so the operand box of any tap, chunk and line is one contiguous 1 KB block
+// [16 f rows x 16 positions]: K-major SWIZZLE_64B, one 16-byte aligned TMA op.
+constexpr int kMaxShift = 8;
+struct TmapSet {
+  CUtensorMap m[kMaxShift];
+};
+
+__global__ void gram_planar_kernel(int64_t nlines, int dlast, int nblk, int nshift, int roff_last,
+                                   const float* __restrict__ x, float* __restrict__ xt) {
+  // one thread per (line, blk, f, t) of one copy; t fastest (coalesced writes)
+  const int64_t per_copy = nlines * nblk * 256;
+  const int64_t total = per_copy * nshift;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / per_copy);
+    int64_t r = e % per_copy;
+    const int t = (int)(r & 15), f = (int)((r >> 4) & 15);
+    r >>= 8;
+    const int blk = (int)(r % nblk);
+    const int64_t line = r / nblk;
+    const int sig = (roff_last + b) & 15;
+    const int pos = 16 * blk + t + sig;
+    xt[e] = pos < dlast ? __ldg(x + ((size_t)line * dlast + pos) * 16 + f) : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads2, 1)
+gram_tc2_kernel(const __grid_constant__ TmapSet tms, TcParams p, const int32_t* __restrict__ pos, int ndim,
+                float* __restrict__ part, int dbg) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_bar[kMaxStages], ready_bar[kMaxStages], empty_bar[kMaxStages], tfull[2],
+      tempty[2];
+  __shared__ uint32_t tmem_slot;
+  __shared__ int tap_c[kMaxTaps2][3];  // per tap: last-axis offset, prefix offsets
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.x, split = blockIdx.y;
+  const int T = p.T;
+  const int L = p.nsp;  // spatial axes
+  const int m0 = mtile_first_tap(p.pair_m[pair], T);
+  const int n0 = p.pair_n[pair] * kNT;
+  const int NT = min(kNT, T - n0);
+  const bool a_inside = (m0 >= n0) && (m0 + kMT <= n0 + NT);
+  const int list = NT + (a_inside ? 0 : kMT);
+  const int a_off = a_inside ? (m0 - n0) : NT;
+  const uint32_t half_bytes = (uint32_t)(list * 1024);
+  const uint32_t stage_bytes = 2 * half_bytes;
+  const int64_t kb0 = (int64_t)split * p.kb_per_split;
+  const int64_t kb1 = hmin64(p.nkb, kb0 + p.kb_per_split);
+  const int nkb = (int)(kb1 > kb0 ? kb1 - kb0 : 0);
+  const int nchains = (nkb + kChain - 1) / kChain;
+  const int S = p.stages;
+
+  for (int t = threadIdx.x; t < T * L; t += blockDim.x) {
+    const int tp = t / L, d = t % L;
+    const int v = __ldg(pos + (size_t)tp * 8 * ndim + d);
+    if (d == L - 1) tap_c[tp][0] = v;
+    else tap_c[tp][1 + d] = v;
+  }
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < S; ++st) {
+      mbar_init(&full_bar[st], 1);
+      mbar_init(&ready_bar[st], 128);
+      mbar_init(&empty_bar[st], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty_bar[st], ph ^ 1);
+        const int64_t line = kb / p.nkb_line;
+        const int chunk = (int)(kb % p.nkb_line);
+        int lc[2] = {0, 0};
+        {
+          int64_t rem = line;
+          for (int d = L - 2; d >= 0; --d) {
+            lc[d] = (int)(rem % p.rext[d]);
+            rem /= p.rext[d];
+          }
+        }
+        if (dbg & 2) {
+          mbar_arrive(&full_bar[st]);
+          if (++st == S) { st = 0; ph ^= 1; }
+          continue;
+        }
+        tc::mbar_expect_tx(&full_bar[st], half_bytes);
+        uint8_t* sb = smem + (size_t)st * stage_bytes;
+        for (int q = 0; q < list; ++q) {
+          const int tap = (q < NT) ? n0 + q : m0 + (q - NT);
+          // copy b = last-axis offset of the tap; block = (roff + b + 16 chunk - sigma_b) / 16
+          const int bsh = tap_c[tap][0];
+          const int pstart = (int)p.roff[L - 1] + bsh + chunk * kBK;
+          const int blk = (pstart - (pstart & 15)) >> 4;
+          int c3 = 0, c4 = 0;
+          if (L == 2) c3 = (int)p.roff[0] + lc[0] + tap_c[tap][1];
+          if (L == 3) {
+            c3 = (int)p.roff[1] + lc[1] + tap_c[tap][2];
+            c4 = (int)p.roff[0] + lc[0] + tap_c[tap][1];
+          }
+          tc::tma_load_5d(sb + (size_t)q * 1024, &tms.m[(dbg & 16) ? 0 : bsh], 0, 0, blk, c3, c4, &full_bar[st]);
+        }
+        if (++st == S) { st = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc_tf32(128, 16 * NT);
+    int st = 0;
+    uint32_t ph = 0;
+    for (int c = 0; c < nchains; ++c) {
+      const int b = c & 1;
+      mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t dcol = tmem + (uint32_t)(256 * b);
+      bool first = true;
+      const int j1 = min(nkb, (c + 1) * kChain);
+      for (int j = c * kChain; j < j1; ++j) {
+        const int64_t kb = kb0 + j;
+        mbar_wait(&ready_bar[st], ph);
+        tc_fence_after();
+        const int chunk = (int)(kb % p.nkb_line);
+        const int valid = (int)hmin64(kBK, p.rext[L - 1] - (int64_t)chunk * kBK);
+        const int nks = (valid + 7) / 8;
+        if (lane == 0) {
+          const uint32_t sbase = smem_u32(smem + (size_t)st * stage_bytes);
+          for (int ks = 0; ks < ((dbg & 1) ? 0 : nks); ++ks) {
+            const uint32_t kofs = (uint32_t)ks * 32;
+            const uint64_t a_hi = tc::desc_sw64(sbase + (uint32_t)a_off * 1024 + kofs);
+            const uint64_t a_lo = tc::desc_sw64(sbase + half_bytes + (uint32_t)a_off * 1024 + kofs);
+            const uint64_t b_hi = tc::desc_sw64(sbase + kofs);
+            const uint64_t b_lo = tc::desc_sw64(sbase + half_bytes + kofs);
+            umma_tf32(dcol, a_hi, b_hi, idesc, first ? 0u : 1u);
+            umma_tf32(dcol, a_hi, b_lo, idesc, 1u);
+            umma_tf32(dcol, a_lo, b_hi, idesc, 1u);
+            first = false;
+          }
+          umma_commit(&empty_bar[st]);
+        }
+        __syncwarp();
+        if (++st == S) { st = 0; ph ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull[b]);
+      __syncwarp();
+    }
+  } else if (warp < kEpi0v2) {
+    // ---------------- converters: A_lo and line-tail zeroing ----------------
+    const int ct = threadIdx.x - 64;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full_bar[st], ph);
+      const int chunk = (int)(kb % p.nkb_line);
+      const int valid = (int)hmin64(kBK, p.rext[L - 1] - (int64_t)chunk * kBK);
+      uint8_t* sb = smem + (size_t)st * stage_bytes;
+      float4* raw4 = reinterpret_cast<float4*>(sb);
+      float4* lo4 = reinterpret_cast<float4*>(sb + half_bytes);
+      // float4 slot s: box q = s / 64, row f = (s % 64) / 4, physical 16-B chunk u = s % 4;
+      // logical K = 4 * (u ^ ((row byte address >> 7) & 3)) + e
+      for (int sidx = ct; sidx < ((dbg & 4) ? 0 : list * 64); sidx += 128) {
+        float4 v = raw4[sidx];
+        if (valid < kBK) {
+          const int f = (sidx & 63) >> 2, u = sidx & 3;
+          const int k4 = 4 * (u ^ ((f >> 1) & 3));
+          if (k4 + 0 >= valid) v.x = 0.f;
+          if (k4 + 1 >= valid) v.y = 0.f;
+          if (k4 + 2 >= valid) v.z = 0.f;
+          if (k4 + 3 >= valid) v.w = 0.f;
+          raw4[sidx] = v;
+        }
+        lo4[sidx] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
+      }
+      tc::fence_proxy_async();
+      mbar_arrive(&ready_bar[st]);
+      if (++st == S) { st = 0; ph ^= 1; }
+    }
+  } else {
+    // ---------------- epilogue: drain chains into fp32 registers ----------------
+    const int ew = warp - kEpi0v2;
+    const int q4 = warp & 3;  // TMEM lane quarter
+    const int grp = ew >> 2;  // 64-column group
+    const int row = 32 * q4 + lane;
+    const int c0 = 64 * grp;
+    const int ncols = max(0, min(64, 16 * NT - c0));
+    float acc[64];
+#pragma unroll
+    for (int q = 0; q < 64; ++q) acc[q] = 0.f;
+    for (int c = 0; c < nchains; ++c) {
+      const int b = c & 1;
+      mbar_wait(&tfull[b], (c >> 1) & 1);
+      tc_fence_after();
+      if (ncols > 0 && !(dbg & 8)) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t r[16];
+          tmem_ld16_raw(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(256 * b + c0 + 16 * i), r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int q = 0; q < 16; ++q) acc[16 * i + q] += __uint_as_float(r[q]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[b]);
+    }
+    float* dst = part + ((size_t)pair * gridDim.y + split) * 128 * kPartCols + (size_t)row * kPartCols + c0;
+#pragma unroll
+    for (int q = 0; q < 64; q += 4)
+      if (q < ncols) *(float4*)(dst + q) = make_float4(acc[q], acc[q + 1], acc[q + 2], acc[q + 3]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 // G[k1][k2] (k1 <= k2) from the real partials: (rr + ii) + i (ri - ir), summed
 // over splits in fp64 in a fixed order; mirrored conjugate below the diagonal.
 __global__ void gram_tc_reduce_kernel(int n, int nc, int T, int splits, PairTable pt, int ntn,
@@ -417,6 +673,45 @@ TcPlan tc_plan(const DevGeom& g) {
   return pl;
 }
 
+typedef CUresult (*GramEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+GramEncodeFn gram_encode() {
+  static GramEncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (GramEncodeFn)f;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// The gather-producer kernel is the default.  The TMA-fed variant is opt-in
+// (HICU_GRAM_TMA=1): with K-major tf32 operands one TMA op carries a 1 KB
+// [16 f x 16 positions] tile, and a 1 KB op costs ~68 cycles of TMA issue on
+// this part (scripts/tma_rate.cu: 68 / 100 / 131 cycles for 1 / 4 / 8 KB), so
+// the 24 ops per 16-row k-block outrun the ~768 MMA cycles they feed
+// (measured 512 us vs 359 us at C2 full).
+bool use_tma_gram() {
+  static int v = -1;
+  if (v < 0) v = getenv("HICU_GRAM_TMA") ? 1 : 0;
+  return v == 1;
+}
+
+size_t planar_bytes(const DevGeom& g) {
+  const int L = g.ndim - 1;
+  if (!use_tma_gram() || L < 1 || g.kext[L - 1] < 1) return 0;
+  int64_t nlines = 1;
+  for (int d = 0; d < L - 1; ++d) nlines *= g.dims[d];
+  const int64_t nblk = (g.dims[L - 1] + 15) / 16 + 1;
+  return (((size_t)nlines * nblk * 256 * g.kext[L - 1] * sizeof(float)) + 255) & ~(size_t)255;
+}
+
 }  // namespace
 
 bool hicu_gram_tc_supported(const DevGeom& g) { return tc_plan(g).ok; }
@@ -424,7 +719,7 @@ bool hicu_gram_tc_supported(const DevGeom& g) { return tc_plan(g).ok; }
 size_t hicu_gram_tc_workspace(const DevGeom& g) {
   TcPlan pl = tc_plan(g);
   if (!pl.ok) return 0;
-  return pl.part_bytes + 4096;
+  return pl.part_bytes + 4096 + planar_bytes(g);
 }
 
 int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -433,13 +728,48 @@ int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t
   if (ws_bytes < hicu_gram_tc_workspace(g)) return hicu_set_error(HICU_ERR_WORKSPACE, "gram_tc: workspace");
   float* part = (float*)ws;
   int* toff = (int*)((char*)ws + pl.part_bytes);
+  float* xt = (float*)((char*)ws + pl.part_bytes + 4096);
   int s;
-  tc_tap_table_kernel<<<(g.nsp + 127) / 128, 128, 0, st>>>(g.nsp, g.nc, g.koff, toff);
-  if ((s = hicu_check_launch("tc_tap_table_kernel"))) return s;
-  hicu_allow_max_smem((const void*)gram_tc_kernel);
   dim3 grid(pl.p.npairs, pl.splits);
-  gram_tc_kernel<<<grid, kThreads, pl.smem_bytes, st>>>((const float*)x, pl.p, toff, part);
-  if ((s = hicu_check_launch("gram_tc_kernel"))) return s;
+  GramEncodeFn enc = gram_encode();
+  const int Lg = g.ndim - 1;
+  if (use_tma_gram() && enc && g.kext[Lg - 1] >= 1 && g.kext[Lg - 1] <= kMaxShift) {
+    const int L = g.ndim - 1;
+    const int dlast = (int)g.dims[L - 1];
+    const int nblk = (dlast + 15) / 16 + 1;
+    const int nshift = (int)g.kext[L - 1];
+    int64_t nlines = 1;
+    for (int d = 0; d < L - 1; ++d) nlines *= g.dims[d];
+    {
+      const int64_t total = nlines * nblk * 256 * nshift;
+      const int blocks = (int)hmin64((total + 255) / 256, (int64_t)hicu_sm_count() * 16);
+      gram_planar_kernel<<<blocks, 256, 0, st>>>(nlines, dlast, nblk, nshift, (int)g.roff[L - 1], (const float*)x,
+                                                 xt);
+      if ((s = hicu_check_launch("gram_planar_kernel"))) return s;
+    }
+    TmapSet tms;
+    cuuint64_t dims[5] = {16, 16, (cuuint64_t)nblk, (cuuint64_t)(L >= 2 ? g.dims[L - 2] : 1),
+                          (cuuint64_t)(L >= 3 ? g.dims[L - 3] : 1)};
+    cuuint64_t strides[4] = {64, 1024, (cuuint64_t)1024 * nblk, (cuuint64_t)1024 * nblk * dims[3]};
+    cuuint32_t box[5] = {16, 16, 1, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+    const size_t copy_floats = (size_t)nlines * nblk * 256;
+    for (int b = 0; b < nshift; ++b)
+      if (enc(&tms.m[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, xt + (size_t)b * copy_floats, dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return hicu_set_error(HICU_ERR_CUDA, "gram_tc: cuTensorMapEncodeTiled failed");
+    hicu_allow_max_smem((const void*)gram_tc2_kernel);
+    static int dbg = -1;
+    if (dbg < 0) dbg = getenv("HICU_GRAM_DEBUG") ? atoi(getenv("HICU_GRAM_DEBUG")) : 0;
+    gram_tc2_kernel<<<grid, kThreads2, pl.smem_bytes, st>>>(tms, pl.p, g.pos, g.ndim, part, dbg);
+    if ((s = hicu_check_launch("gram_tc2_kernel"))) return s;
+  } else {
+    tc_tap_table_kernel<<<(g.nsp + 127) / 128, 128, 0, st>>>(g.nsp, g.nc, g.koff, toff);
+    if ((s = hicu_check_launch("tc_tap_table_kernel"))) return s;
+    hicu_allow_max_smem((const void*)gram_tc_kernel);
+    gram_tc_kernel<<<grid, kThreads, pl.smem_bytes, st>>>((const float*)x, pl.p, toff, part);
+    if ((s = hicu_check_launch("gram_tc_kernel"))) return s;
+  }
   const int64_t total = (int64_t)g.n * g.n;
   const int rb = (int)hmin64((total + 255) / 256, 1184);
   gram_tc_reduce_kernel<<<rb, 256, 0, st>>>(g.n, g.nc, pl.p.T, pl.splits, pl.pt, pl.ntiles, part, G);

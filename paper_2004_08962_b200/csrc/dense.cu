@@ -58,8 +58,54 @@ __global__ void zgemm_kernel(bool ca, bool cb, int m, int n, int k, const double
   if (row < m && col < n) C[(size_t)row * ldc + col] = acc;
 }
 
+// Small-K variant: the whole K panel of a 16 x 16 output tile is staged in
+// shared memory with one batch of loads and one barrier; each thread then
+// runs its K loop with four independent accumulators (DFMA latency ~9
+// cycles).  The nullspace GEMMs (K = n or ell <= 256) are latency-bound, and
+// the tiled kernel above pays one L2 round trip per 16-wide K chunk.
+constexpr int kZgK = 256;
+__global__ void __launch_bounds__(256)
+zgemm_panel_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restrict__ A, int lda,
+                   const double2* __restrict__ B, int ldb, double2* __restrict__ C, int ldc) {
+  extern __shared__ double2 zp[];
+  double2* As = zp;              // 16 x (k+1): row r of op(A), padded
+  double2* Bs = zp + 16 * (k + 1);  // k x 17: op(B) rows, padded
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int row0 = blockIdx.y * 16, col0 = blockIdx.x * 16;
+  for (int e = threadIdx.x; e < 16 * k; e += 256) {
+    const int r = ca ? e % 16 : e / k, l = ca ? e / 16 : e % k;  // coalesced along the contiguous index
+    const int row = row0 + r;
+    As[r * (k + 1) + l] = row < m ? load_op(A, lda, ca, row, l) : cd(0.0, 0.0);
+  }
+  for (int e = threadIdx.x; e < 16 * k; e += 256) {
+    const int c = cb ? e / k : e % 16, l = cb ? e % k : e / 16;
+    const int col = col0 + c;
+    Bs[l * 17 + c] = col < n ? load_op(B, ldb, cb, l, col) : cd(0.0, 0.0);
+  }
+  __syncthreads();
+  const double2* a = As + ty * (k + 1);
+  double2 c0 = cd(0.0, 0.0), c1 = c0, c2 = c0, c3 = c0;
+  int l = 0;
+  for (; l + 3 < k; l += 4) {
+    zfma(c0, a[l], Bs[l * 17 + tx]);
+    zfma(c1, a[l + 1], Bs[(l + 1) * 17 + tx]);
+    zfma(c2, a[l + 2], Bs[(l + 2) * 17 + tx]);
+    zfma(c3, a[l + 3], Bs[(l + 3) * 17 + tx]);
+  }
+  for (; l < k; ++l) zfma(c0, a[l], Bs[l * 17 + tx]);
+  const int row = row0 + ty, col = col0 + tx;
+  if (row < m && col < n) C[(size_t)row * ldc + col] = (c0 + c1) + (c2 + c3);
+}
+
 int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int lda, const double2* B, int ldb,
                  double2* C, int ldc, cudaStream_t st) {
+  if (k <= kZgK) {
+    const size_t smem = ((size_t)16 * (k + 1) + (size_t)k * 17) * sizeof(double2);
+    hicu_allow_max_smem((const void*)zgemm_panel_kernel);
+    dim3 grid((n + 15) / 16, (m + 15) / 16);
+    zgemm_panel_kernel<<<grid, 256, smem, st>>>(opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
+    return hicu_check_launch("zgemm_panel_kernel");
+  }
   dim3 grid((n + 15) / 16, (m + 15) / 16);
   zgemm_kernel<<<grid, 256, 0, st>>>(opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
   return hicu_check_launch("zgemm_kernel");
@@ -778,6 +824,160 @@ householder3_kernel(int n, int r, const double2* __restrict__ Vg, double tol, do
   }
 }
 
+// Panel-blocked Householder triangularisation (same reflectors as
+// householder_kernel up to rounding).  For each panel of kHb columns:
+//   1. factor the panel: one step per column, applying the new reflector to
+//      the remaining panel columns only (<= kHb-1 warps, one barrier / step);
+//   2. S = Y^H Y and the lower-triangular T' with
+//      H_{c1-1} ... H_{c0} = I - Y T' Y^H,
+//      T'[j][j] = tau_j,  T'[j][0:j] = -tau_j (w_j^H Y[:,0:j]) T'[0:j,0:j];
+//   3. trailing update A <- A - Y (T' (Y^H A)) as three in-CTA products with
+//      one output per thread and no cross-thread reductions.
+// V lives column-major with an odd leading dimension (n+1) so threads walking
+// consecutive columns of the same row hit distinct banks.
+constexpr int kHb = 8;
+constexpr int kHb4Threads = 768;
+__device__ unsigned long long g_hh4_trace[8];  // debug (HICU_HH_TRACE): summed phase clocks
+
+__global__ void __launch_bounds__(kHb4Threads)
+householder4_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
+                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  extern __shared__ double2 sh4[];
+  const int ldv = n + 1;
+  double2* v = sh4;                               // r x ldv, element (k, j) at v[j*ldv + k]
+  double2* Wp = v + (size_t)r * ldv;              // kHb x ldv panel reflectors (zero above the pivot)
+  double2* Z = Wp + (size_t)kHb * ldv;            // kHb x r   (Y^H A, then T' Y^H A)
+  double2* T = Z + (size_t)kHb * r;               // kHb x kHb lower triangular
+  double2* S = T + kHb * kHb;                     // kHb x kHb, S[j][k] = w_j^H w_k
+  __shared__ double2 s_tau[2];
+  __shared__ int s_act[2];
+  __shared__ double2 s_ptau[kHb];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
+  for (int e = tid; e < n * r; e += nt) v[(size_t)(e % r) * ldv + e / r] = Vg[e];
+  for (int e = tid; e < n * r; e += nt) refl[e] = cd(0.0, 0.0);
+  __syncthreads();
+  long long tp0 = clock64(), acc_f = 0, acc_t = 0, acc_z = 0, acc_u = 0;
+  for (int c0 = 0; c0 < r; c0 += kHb) {
+    const int c1 = min(r, c0 + kHb), pw = c1 - c0;
+    tp0 = clock64();
+    for (int e = tid; e < kHb * ldv; e += nt) Wp[e] = cd(0.0, 0.0);
+    __syncthreads();
+    // ---- 1. panel factorisation ----
+    if (warp == 0)
+      hh2_reflector(n, c0, v + (size_t)c0 * ldv, tol, lane, refl, tau, flags, status, &s_tau[0], &s_act[0], Wp);
+    __syncthreads();
+    for (int c = c0; c < c1; ++c) {
+      const int par = (c - c0) & 1;
+      const double2 tv = s_tau[par];
+      const bool act = s_act[par] != 0;
+      if (lane == 0 && warp == 0) s_ptau[c - c0] = act ? tv : cd(0.0, 0.0);
+      const double2* w = Wp + (size_t)(c - c0) * ldv;
+      const int j = c + 1 + warp;  // one panel column per warp
+      if (j < c1) {
+        double2* vj = v + (size_t)j * ldv;
+        if (act) {
+          double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+          int k = c + lane;
+          for (; k + 32 < n; k += 64) {
+            zfmac(d0, w[k], vj[k]);
+            zfmac(d1, w[k + 32], vj[k + 32]);
+          }
+          if (k < n) zfmac(d0, w[k], vj[k]);
+          double2 dt = d0 + d1;
+          dt = cd(warp_sum_d_(dt.x), warp_sum_d_(dt.y));
+          const double2 f = cmul(tv, dt);
+          for (int kk = c + lane; kk < n; kk += 32) vj[kk] = vj[kk] - cmul(w[kk], f);
+        }
+        if (j == c + 1) {  // owner of the next pivot column builds its reflector
+          __syncwarp();
+          hh2_reflector(n, j, vj, tol, lane, refl, tau, flags, status, &s_tau[par ^ 1], &s_act[par ^ 1],
+                        Wp + (size_t)(j - c0) * ldv);
+        }
+      }
+      __syncthreads();
+    }
+    acc_f += clock64() - tp0;
+    tp0 = clock64();
+    if (c1 >= r) break;
+    // ---- 2. S = Y^H Y (k < j) and T' ----
+    for (int q = tid; q < pw * pw; q += nt) {
+      const int jj = q / pw, kk = q % pw;
+      if (kk >= jj) continue;
+      const double2* wj = Wp + (size_t)jj * ldv;
+      const double2* wk = Wp + (size_t)kk * ldv;
+      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0);
+      int row = c0 + jj;  // w_j is zero above row c0 + jj
+      for (; row + 1 < n; row += 2) {
+        zfmac(a0, wj[row], wk[row]);
+        zfmac(a1, wj[row + 1], wk[row + 1]);
+      }
+      if (row < n) zfmac(a0, wj[row], wk[row]);
+      S[jj * kHb + kk] = a0 + a1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      for (int jj = 0; jj < pw; ++jj) {
+        const double2 tj = s_ptau[jj];
+        for (int i = 0; i < jj; ++i) {
+          double2 acc = cd(0.0, 0.0);
+          for (int kk = i; kk < jj; ++kk) zfma(acc, S[jj * kHb + kk], T[kk * kHb + i]);
+          T[jj * kHb + i] = cd(-(tj.x * acc.x - tj.y * acc.y), -(tj.x * acc.y + tj.y * acc.x));
+        }
+        T[jj * kHb + jj] = tj;
+      }
+    }
+    __syncthreads();
+    acc_t += clock64() - tp0;
+    tp0 = clock64();
+    // ---- 3a. Z = Y^H A_trail ----
+    const int mc = r - c1;
+    for (int q = tid; q < pw * mc; q += nt) {
+      const int jj = q % pw, col = c1 + q / pw;
+      const double2* wj = Wp + (size_t)jj * ldv;
+      const double2* ac = v + (size_t)col * ldv;
+      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0), a2 = cd(0.0, 0.0), a3 = cd(0.0, 0.0);
+      int row = c0 + jj;
+      for (; row + 3 < n; row += 4) {
+        zfmac(a0, wj[row], ac[row]);
+        zfmac(a1, wj[row + 1], ac[row + 1]);
+        zfmac(a2, wj[row + 2], ac[row + 2]);
+        zfmac(a3, wj[row + 3], ac[row + 3]);
+      }
+      for (; row < n; ++row) zfmac(a0, wj[row], ac[row]);
+      Z[jj * r + col] = (a0 + a1) + (a2 + a3);
+    }
+    __syncthreads();
+    acc_z += clock64() - tp0;
+    tp0 = clock64();
+    // ---- 3b. Z' = T' Z (in place, rows from the bottom: row j uses rows i <= j) ----
+    for (int col = c1 + tid; col < r; col += nt) {
+      for (int jj = pw - 1; jj >= 0; --jj) {
+        double2 acc = cd(0.0, 0.0);
+        for (int i = 0; i <= jj; ++i) zfma(acc, T[jj * kHb + i], Z[i * r + col]);
+        Z[jj * r + col] = acc;
+      }
+    }
+    __syncthreads();
+    // ---- 3c. A_trail -= Y Z' ----
+    for (int q = tid; q < (n - c0) * mc; q += nt) {
+      const int row = c0 + q % (n - c0), col = c1 + q / (n - c0);
+      double2 acc = cd(0.0, 0.0);
+#pragma unroll
+      for (int jj = 0; jj < kHb; ++jj)
+        if (jj < pw) zfma(acc, Wp[(size_t)jj * ldv + row], Z[jj * r + col]);
+      v[(size_t)col * ldv + row] = v[(size_t)col * ldv + row] - acc;
+    }
+    __syncthreads();
+    acc_u += clock64() - tp0;
+  }
+  if (tid == 0) {
+    g_hh4_trace[0] = acc_f;
+    g_hh4_trace[1] = acc_t;
+    g_hh4_trace[2] = acc_z;
+    g_hh4_trace[3] = acc_u;
+  }
+}
+
 // B <- H_0^H ... applied for col = r-1 .. 0: block -= conj(tau) w (w^H block).
 // One warp per column of B (held in shared memory); the reflectors stream
 // through shared memory in chunks so each is read from L2 once per CTA.
@@ -1016,6 +1216,25 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     // large V: work in place in the caller's refl buffer is not possible (different layout);
     // require the caller to size refl at 2*n*r and use its upper half as scratch.
     gws = (double2*)refl + (size_t)n * r;
+  }
+  {
+    const size_t b4 = ((size_t)r * (n + 1) + (size_t)kHb * (n + 1) + (size_t)kHb * r + 2 * kHb * kHb) * sizeof(double2);
+    // Opt-in (HICU_HOUSEHOLDER4=1): measured slower than householder2 at C2
+    // (307 vs 234 us; per-panel clocks: factor 4.4K cycles/step, S,T 17K,
+    // Z 18K, trailing 15K), kept for the blocked-QR work that follows.
+    if (getenv("HICU_HOUSEHOLDER4") && b4 <= (size_t)227 * 1024 - 1024) {
+      hicu_allow_max_smem((const void*)householder4_kernel);
+      householder4_kernel<<<1, kHb4Threads, b4, (cudaStream_t)stream>>>(n, r, (const double2*)V, tol, (double2*)refl,
+                                                                         (double2*)tau, flags, status_dev);
+      if (getenv("HICU_HH_TRACE")) {
+        unsigned long long h[8];
+        cudaStreamSynchronize((cudaStream_t)stream);
+        cudaMemcpyFromSymbol(h, g_hh4_trace, sizeof(h));
+        fprintf(stderr, "householder4 cycles: panel-factor %llu | S,T %llu | Z=Y^H A %llu | Z',A-=YZ' %llu\n", h[0], h[1],
+                h[2], h[3]);
+      }
+      return hicu_check_launch("householder4_kernel");
+    }
   }
   if (getenv("HICU_HOUSEHOLDER3") && n <= 32 * kHh3Per && bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
     hicu_allow_max_smem((const void*)householder3_kernel);

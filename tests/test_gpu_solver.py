@@ -221,3 +221,30 @@ def test_c1_free_running_ser_parity():
     print(f"C1 SER: zero-filled {ser_0:.3f} dB, device {ser_g:.3f} dB, oracle {ser_o:.3f} dB")
     assert ser_g > ser_0 + 3.0
     assert abs(ser_g - ser_o) <= 0.1
+
+
+def test_cli_recon_matches_api(tmp_path):
+    """`hicu recon --config` (cli.py) writes exactly the array hicu_reconstruct
+    returns and the reference's report keys (dims, rank, seed)."""
+    import json as _json
+
+    from paper_2004_08962_b200 import cli
+
+    rng = np.random.default_rng(5)
+    dims = (24, 20, 4)
+    x = rng.standard_normal(dims) + 1j * rng.standard_normal(dims)
+    mask = np.repeat((rng.random(dims[:2] + (1,)) < 0.5).astype(np.uint8), dims[2], axis=2)
+    H.write_array(tmp_path / "k.hicu", x)
+    H.write_array(tmp_path / "m.hicu", mask)
+    doc = {"kernel": {"extents": [3, 3, 4]},
+           "schedule": {"rank": 8, "stages": [{"region": "full", "p": 4, "gradient_steps": 2, "iterations": 3}]},
+           "paths": {"kspace": "k.hicu", "mask": "m.hicu"}}
+    (tmp_path / "run.json").write_text(_json.dumps(doc))
+    assert cli.main(["recon", "--config", str(tmp_path / "run.json"), "--out", str(tmp_path), "--seed", "4"]) == 0
+    got = H.read_array(tmp_path / "recon.hicu")
+    cfg = H.parse_config(doc)
+    cfg.schedule.seed = 4
+    want, _ = H.hicu_reconstruct(H.mask_apply(x, mask), mask, cfg.kernel, cfg.schedule)
+    assert np.array_equal(got, want)
+    rep = _json.loads((tmp_path / "report.json").read_text())
+    assert rep["dims"] == list(dims) and rep["rank"] == 8 and rep["seed"] == 4

@@ -389,7 +389,7 @@ def run_ours(args):
         line = {
             "metric": "HICU iters/s", "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (fp32 FMA; fp64 reductions and nullspace)",
+            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (3xTF32 tcgen05 convs/Gram; fp64 reductions and nullspace)",
             "data": "synthetic", "config": workload_config(spec), "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches) // max(1, args.steps),
             "roofline": roof, "roofline_all": roof_all, "cpu_baseline": cpu, "clocks": clock_info,

@@ -195,58 +195,127 @@ scatter_kernel(DevGeom g, const float2* __restrict__ qt, int p, const float2* __
   block_reduce_store<4>(v, parts + 4 * (size_t)blockIdx.x);
 }
 
-__global__ void update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir,
-                              const double* __restrict__ obj_parts, int n_obj,
-                              const double* __restrict__ dc_parts, int n_dc,
-                              const double* __restrict__ els_parts, int n_els, int dc_mode, double lam,
-                              double* __restrict__ rec) {
+// Seven warps reduce the seven per-step sums in parallel, every partial
+// loaded before any add (one L2 round trip instead of a chain); the
+// summation order (lane j sums j, j+32, ... then a fixed xor tree) is that of
+// warp_sum_parts, so the results are bit-identical to the serial form.
+constexpr int kUpdMaxPer = 32;  // partials per lane (n <= 1024)
+__device__ __forceinline__ double warp_sum_batched(const double* __restrict__ parts, int np, int stride, int off) {
+  const int lane = threadIdx.x & 31;
+  double v[kUpdMaxPer];
+#pragma unroll
+  for (int k = 0; k < kUpdMaxPer; ++k) {
+    const int j = lane + 32 * k;
+    v[k] = j < np ? __ldg(parts + (size_t)j * stride + off) : 0.0;
+  }
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < kUpdMaxPer; ++k)
+    if (lane + 32 * k < np) t += v[k];
+  for (int j = lane + 32 * kUpdMaxPer; j < np; j += 32) t += parts[(size_t)j * stride + off];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+__global__ void __launch_bounds__(256)
+update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir,
+              const double* __restrict__ obj_parts, int n_obj,
+              const double* __restrict__ dc_parts, int n_dc,
+              const double* __restrict__ els_parts, int n_els, int dc_mode, double lam,
+              double* __restrict__ rec, bool vec) {
   __shared__ double s_eta;
   __shared__ int s_skip;
-  if (threadIdx.x < 32) {
-    const double obj_c = warp_sum_parts(obj_parts, n_obj, 1, 0);
-    const double gn2 = warp_sum_parts(dc_parts, n_dc, 4, 0);
-    const double res2 = warp_sum_parts(dc_parts, n_dc, 4, 1);
-    const double snum = warp_sum_parts(dc_parts, n_dc, 4, 2);
-    const double sden = warp_sum_parts(dc_parts, n_dc, 4, 3);
-    const double num_c = warp_sum_parts(els_parts, n_els, 2, 0);
-    const double den_c = warp_sum_parts(els_parts, n_els, 2, 1);
-    if (threadIdx.x == 0) {
-      double obj = obj_c, num = num_c, den = den_c;
-      if (dc_mode == 1) {
-        obj += lam * res2;
-        num += lam * snum;
-        den += lam * sden;
-      }
-      // solver.py:347: the ELS convolution only runs when any(g); H(0) == 0
-      // exactly, so num = den = 0 falls out when g vanishes.
-      const bool degenerate = !(den > 0.0);
-      const double eta = degenerate ? 0.0 : num / den;
-      s_eta = eta;
-      s_skip = degenerate ? 1 : 0;
-      if (blockIdx.x == 0) {
-        rec[HICU_REC_OBJ] = obj;
-        rec[HICU_REC_NUM] = num;
-        rec[HICU_REC_DEN] = den;
-        rec[HICU_REC_ETA] = eta;
-        rec[HICU_REC_OBJ_AFTER] = degenerate ? obj : obj - num * num / den;
-        rec[HICU_REC_GNORM2] = gn2;
-        rec[HICU_REC_DEGENERATE] = degenerate ? 1.0 : 0.0;
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        rec[7] = (double)t;
-      }
+  __shared__ double sums[7];
+  const int warp = threadIdx.x >> 5;
+  if (warp < 7) {
+    double t;
+    switch (warp) {
+      case 0: t = warp_sum_batched(obj_parts, n_obj, 1, 0); break;
+      case 1: t = warp_sum_batched(dc_parts, n_dc, 4, 0); break;
+      case 2: t = warp_sum_batched(dc_parts, n_dc, 4, 1); break;
+      case 3: t = warp_sum_batched(dc_parts, n_dc, 4, 2); break;
+      case 4: t = warp_sum_batched(dc_parts, n_dc, 4, 3); break;
+      case 5: t = warp_sum_batched(els_parts, n_els, 2, 0); break;
+      default: t = warp_sum_batched(els_parts, n_els, 2, 1); break;
+    }
+    if ((threadIdx.x & 31) == 0) sums[warp] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double obj_c = sums[0], gn2 = sums[1], res2 = sums[2], snum = sums[3], sden = sums[4];
+    double obj = obj_c, num = sums[5], den = sums[6];
+    if (dc_mode == 1) {
+      obj += lam * res2;
+      num += lam * snum;
+      den += lam * sden;
+    }
+    // solver.py:347: the ELS convolution only runs when any(g); H(0) == 0
+    // exactly, so num = den = 0 falls out when g vanishes.
+    const bool degenerate = !(den > 0.0);
+    const double eta = degenerate ? 0.0 : num / den;
+    s_eta = eta;
+    s_skip = degenerate ? 1 : 0;
+    if (blockIdx.x == 0) {
+      rec[HICU_REC_OBJ] = obj;
+      rec[HICU_REC_NUM] = num;
+      rec[HICU_REC_DEN] = den;
+      rec[HICU_REC_ETA] = eta;
+      rec[HICU_REC_OBJ_AFTER] = degenerate ? obj : obj - num * num / den;
+      rec[HICU_REC_GNORM2] = gn2;
+      rec[HICU_REC_DEGENERATE] = degenerate ? 1.0 : 0.0;
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      rec[7] = (double)tt;
     }
   }
   __syncthreads();
   if (s_skip) return;
   const float eta = (float)s_eta;
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N;
-       m += (int64_t)gridDim.x * blockDim.x) {
-    const float2 gv = gdir[m];
-    float2 yv = y[m];
+  if (!vec) {  // operands not 16-byte aligned
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N; m += (int64_t)gridDim.x * blockDim.x) {
+      const float2 gv = gdir[m];
+      float2 yv = y[m];
+      yv.x = fmaf(-eta, gv.x, yv.x);
+      yv.y = fmaf(-eta, gv.y, yv.y);
+      y[m] = yv;
+    }
+    return;
+  }
+  // two complex elements per thread per pass (16-byte accesses)
+  const int64_t N2 = N >> 1;
+  float4* y4 = reinterpret_cast<float4*>(y);
+  const float4* g4 = reinterpret_cast<const float4*>(gdir);
+  // four 16-byte pairs in flight per thread (memory-level parallelism)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m0 < N2; m0 += 4 * stride) {
+    float4 gv[4], yv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t m = m0 + u * stride;
+      if (m < N2) {
+        gv[u] = g4[m];
+        yv[u] = y4[m];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t m = m0 + u * stride;
+      if (m < N2) {
+        yv[u].x = fmaf(-eta, gv[u].x, yv[u].x);
+        yv[u].y = fmaf(-eta, gv[u].y, yv[u].y);
+        yv[u].z = fmaf(-eta, gv[u].z, yv[u].z);
+        yv[u].w = fmaf(-eta, gv[u].w, yv[u].w);
+        y4[m] = yv[u];
+      }
+    }
+  }
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const float2 gv = gdir[N - 1];
+    float2 yv = y[N - 1];
     yv.x = fmaf(-eta, gv.x, yv.x);
     yv.y = fmaf(-eta, gv.y, yv.y);
-    y[m] = yv;
+    y[N - 1] = yv;
   }
 }
 
@@ -651,11 +720,13 @@ extern "C" int hicu_step_update(int64_t N, void* y, const void* gdir, const doub
                                 int dc_mode, double lam, double* rec, void* stream) {
   if (!y || !gdir || !obj_parts || !dc_parts || !els_parts || !rec || N < 1)
     return hicu_set_error(HICU_ERR_PARAMETER, "update: bad arguments");
-  int64_t b = (N + 255) / 256;
-  int64_t cap = (int64_t)hicu_sm_count() * 4;
+  int64_t b = (N / 2 + 255) / 256;
+  int64_t cap = (int64_t)hicu_sm_count() * 2;  // fewer blocks: each re-reads the partials
   if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  const bool vec = (((uintptr_t)y | (uintptr_t)gdir) & 15) == 0;
   update_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(N, (float2*)y, (const float2*)gdir, obj_parts, n_obj,
-                                                           dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec);
+                                                           dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec, vec);
   return hicu_check_launch("update_kernel");
 }
 

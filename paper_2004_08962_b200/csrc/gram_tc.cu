@@ -26,9 +26,9 @@
 // 16 rows of every tap of the tile, split hi/lo on the fly and write 16-byte
 // K-major chunks.
 //
-// Warp roles (672 threads): warps 0-3 producers, warp 4 TMEM owner + MMA
-// issuer (one lane), warps 5-20 epilogue (TMEM lane quarter = warp % 4,
-// 64-column group = (warp - 5) / 4).
+// Warp roles (800 threads): warps 0-7 producers, warp 8 TMEM owner + MMA
+// issuer (one lane), warps 9-24 epilogue (TMEM lane quarter = warp % 4,
+// 64-column group = (warp - 9) / 4).
 //
 // Scope: coil-separable support with Nc = 8 (16 floats per tap), no circular
 // axes, <= 3 spatial axes, 8..128 spatial taps.  Other geometries use the SIMT
@@ -45,9 +45,10 @@ constexpr int kBK = 16;           // rows (K) per pipeline stage: 2 MMA k-steps 
 constexpr int kMT = 8;            // taps per M tile  (M = 128 real columns)
 constexpr int kNT = 16;           // taps per N tile  (N <= 256 real columns)
 constexpr int kChain = 4;         // k-blocks per TMEM accumulation chain
-constexpr int kProducers = 128;
+constexpr int kProdWarps = 8;
+constexpr int kProducers = kProdWarps * 32;
 constexpr int kEpiWarps = 16;
-constexpr int kThreads = (4 + 1 + kEpiWarps) * 32;
+constexpr int kThreads = (kProdWarps + 1 + kEpiWarps) * 32;
 constexpr int kMaxStages = 6;
 constexpr int kPartCols = 256;
 constexpr int kMaxPairs = 160;
@@ -176,7 +177,7 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == kProdWarps) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
                  "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -186,7 +187,7 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
-  if (warp < 4) {
+  if (warp < kProdWarps) {
     // ---------------- producers: gather, split hi/lo, K-major stores ----------------
     const int tid = threadIdx.x;
     const int L = p.nsp - 1;
@@ -237,7 +238,7 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
       mbar_arrive(&full_bar[s]);
       if (++s == S) { s = 0; ph ^= 1; }
     }
-  } else if (warp == 4) {
+  } else if (warp == kProdWarps) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = make_idesc_tf32(128, 16 * NT);
     int s = 0;
@@ -279,7 +280,7 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
     }
   } else {
     // ---------------- epilogue: drain chains into fp32 registers ----------------
-    const int ew = warp - 5;
+    const int ew = warp - (kProdWarps + 1);
     const int q4 = warp & 3;  // TMEM lane quarter
     const int grp = ew >> 2;  // 64-column group
     const int row = 32 * q4 + lane;
@@ -313,7 +314,7 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kProdWarps) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }

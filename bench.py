@@ -266,8 +266,6 @@ def run_ours(args):
     clocks = ClockSampler(local)
     times = []
     launches0 = nat.lib().hicu_launch_count()
-    eng.prof = prof
-    prof.reset()
     clocks.start()
     for _ in range(args.steps):
         flush.fill_(1.0)
@@ -280,6 +278,15 @@ def run_ours(args):
         times.append(e0.elapsed_time(e1))
     clock_info = clocks.stop()
     launches = nat.lib().hicu_launch_count() - launches0
+    eng.check_status()
+    # per-kernel-class CUDA-event times from one extra, untimed step (the
+    # event records between kernels would perturb the timed steps)
+    flush.fill_(1.0)
+    barrier()
+    eng.prof = prof
+    prof.reset()
+    one_step()
+    barrier()
     eng.prof = None
     kinds = prof.summary()
     eng.check_status()
@@ -321,8 +328,8 @@ def run_ours(args):
     for w in work:
         for k in flops_total:
             per_launch_groups = w["iters"] * (1 if k == "gram" else w["G"])
-            flops_total[k] += w[k] * per_launch_groups * args.steps
-            launches_expected[k] += per_launch_groups * args.steps
+            flops_total[k] += w[k] * per_launch_groups  # the profiled step
+            launches_expected[k] += per_launch_groups
     ms_by = {k: v["ms"] for k, v in kinds.items()}
     peaks = {}
     try:
@@ -358,15 +365,15 @@ def run_ours(args):
                        "frac": ach / tf32_peak, "traffic": traffic(k), "launches": nl,
                        "avg_launch_ms": ms_by[k] / nl, "flops_per_launch_avg": flops_total[k] / nl}
     if "update" in ms_by and ms_by["update"] > 0:
-        bytes_total = sum(w["update_bytes"] * w["iters"] * w["G"] for w in work) * args.steps
+        bytes_total = sum(w["update_bytes"] * w["iters"] * w["G"] for w in work)
         ach = bytes_total / (ms_by["update"] * 1e-3) / 1e9
         roof_all["update"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                               "traffic": traffic("update"), "launches": kinds["update"]["launches"]}
     for k in ("nystrom", "householder"):
         if k in ms_by:
             roof_all[k] = {"bound": "fp64 latency (single-CTA small dense algebra, reported separately, SURVEY 8d)",
-                           "ms_per_step": ms_by[k] / args.steps,
-                           "us_per_iteration": 1e3 * ms_by[k] / (args.steps * spec.iterations)}
+                           "ms_per_step": ms_by[k],
+                           "us_per_iteration": 1e3 * ms_by[k] / spec.iterations}
     # the roofline object: the dominant tensor-core kernel class (K1 Gram / K4-K6 convolutions)
     dom = max((k for k in roof_all if roof_all[k]["bound"] == "tensor"), key=lambda k: ms_by[k])
     roof = dict(roof_all[dom])
@@ -374,7 +381,7 @@ def run_ours(args):
                  "achieved_def": "algorithmic flops of all launches of the class / their summed CUDA-event time",
                  "traffic_def": "ncu dram read+write bytes of one full-stage launch (profiles/r01_ncu_full_v2.json)"})
     share = {k: (v / sum(ms_by.values()) if sum(ms_by.values()) > 0 else 0.0) for k, v in ms_by.items()}
-    grad_tflops = sum(flops_total.values()) / (total_ms * 1e-3 / max(world, 1)) / 1e12 if world == 1 else None
+    grad_tflops = sum(flops_total.values()) / (total_ms / args.steps * 1e-3) / 1e12 if world == 1 else None
 
     # ---- CPU baseline (oracle port), rank 0, N=1 only ----
     cpu = None
@@ -393,7 +400,8 @@ def run_ours(args):
             "data": "synthetic", "config": workload_config(spec), "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches) // max(1, args.steps),
             "roofline": roof, "roofline_all": roof_all, "cpu_baseline": cpu, "clocks": clock_info,
-            "kernel_share": share, "kernel_ms_per_step": {k: v / args.steps for k, v in ms_by.items()},
+            "kernel_share": share, "kernel_ms_per_step": dict(ms_by),
+            "kernel_ms_source": "one extra untimed step with the native CUDA-event profiler",
             "gram_grad_tflops": grad_tflops,
             "step_ms": times,
         }

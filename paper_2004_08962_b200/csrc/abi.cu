@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // C-ABI glue: error reporting, geometry validation, device queries and the
 // Gram dispatch.  See include/hicu_b200.h for the contract.
 #include <stdio.h>
@@ -38,6 +39,12 @@ int hicu_check_cuda(cudaError_t e, const char* where) {
   if (e == cudaSuccess) return HICU_OK;
   snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where, cudaGetErrorString(e));
   return HICU_ERR_CUDA;
+}
+
+bool hicu_pdl_enabled() {
+  static int v = -1;
+  if (v < 0) v = getenv("HICU_NO_PDL") ? 0 : 1;
+  return v == 1;
 }
 
 int hicu_sm_count() {

@@ -21,6 +21,7 @@ int cov_blocks(int64_t nloc) {
 // block b accumulates a contiguous slice of locations into parts[b][nc][nc]
 __global__ void __launch_bounds__(1024) coil_cov_kernel(int64_t nloc, int nc, const float2* __restrict__ x, const uint8_t* __restrict__ mask,
                                 int64_t per_block, double2* __restrict__ parts) {
+  hicu_pdl_entry();
   __shared__ float2 xs[kLocPerBlock][33];
   __shared__ uint8_t ms[kLocPerBlock];
   const int64_t l0 = (int64_t)blockIdx.x * per_block;
@@ -51,6 +52,7 @@ __global__ void __launch_bounds__(1024) coil_cov_kernel(int64_t nloc, int nc, co
 }
 
 __global__ void __launch_bounds__(1024) coil_cov_reduce(int nc, int nparts, const double2* __restrict__ parts, double2* __restrict__ cov) {
+  hicu_pdl_entry();
   const int e = threadIdx.x;
   if (e >= nc * nc) return;
   double2 s = cd(0.0, 0.0);
@@ -61,6 +63,7 @@ __global__ void __launch_bounds__(1024) coil_cov_reduce(int nc, int nparts, cons
 __global__ void coil_apply_kernel(int64_t nloc, int nc, int nv, const float2* __restrict__ x,
                                   const uint8_t* __restrict__ mask, const double2* __restrict__ basis,
                                   float2* __restrict__ y, uint8_t* __restrict__ mask_out) {
+  hicu_pdl_entry();
   __shared__ float2 sb[32 * 32];
   for (int e = threadIdx.x; e < nc * nv; e += blockDim.x) {
     const double2 v = basis[e];
@@ -93,10 +96,10 @@ extern "C" int hicu_coil_cov(int64_t nloc, int nc, const void* x, const uint8_t*
   const int blocks = cov_blocks(nloc);
   const int64_t per = (nloc + blocks - 1) / blocks;
   cudaStream_t st = (cudaStream_t)stream;
-  coil_cov_kernel<<<blocks, 1024, 0, st>>>(nloc, nc, (const float2*)x, mask, per, (double2*)ws);
+  hicu_launch(coil_cov_kernel, blocks, 1024, 0, st, nloc, nc, (const float2*)x, mask, per, (double2*)ws);
   int s = hicu_check_launch("coil_cov_kernel");
   if (s) return s;
-  coil_cov_reduce<<<1, 1024, 0, st>>>(nc, blocks, (const double2*)ws, (double2*)cov);
+  hicu_launch(coil_cov_reduce, 1, 1024, 0, st, nc, blocks, (const double2*)ws, (double2*)cov);
   return hicu_check_launch("coil_cov_reduce");
 }
 
@@ -107,7 +110,7 @@ extern "C" int hicu_coil_apply(int64_t nloc, int nc, int nv, const void* x, cons
   int64_t blocks = (nloc * nv + 255) / 256;
   int64_t cap = (int64_t)hicu_sm_count() * 8;
   if (blocks > cap) blocks = cap;
-  coil_apply_kernel<<<(int)blocks, 256, 0, (cudaStream_t)stream>>>(nloc, nc, nv, (const float2*)x, mask,
+  hicu_launch(coil_apply_kernel, (int)blocks, 256, 0, (cudaStream_t)stream, nloc, nc, nv, (const float2*)x, mask,
                                                                    (const double2*)basis, (float2*)y, mask_out);
   return hicu_check_launch("coil_apply_kernel");
 }

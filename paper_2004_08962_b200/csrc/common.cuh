@@ -147,6 +147,37 @@ __device__ __forceinline__ double warp_sum_parts(const double* parts, int np, in
   return t;
 }
 
+// Programmatic dependent launch.  Every kernel of the library starts with
+// hicu_pdl_entry(): it waits until the previous grid in the stream has
+// completed (and its writes are visible) and then lets the next grid launch,
+// so the next kernel's launch and CTA placement overlap this kernel's run.
+// A no-op for kernels launched without the attribute.
+__device__ __forceinline__ void hicu_pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool hicu_pdl_enabled();
+
+// kernel<<<grid, block, smem, stream>>>(args...) with the programmatic
+// stream serialization attribute (cudaLaunchKernelEx coerces the arguments to
+// the kernel's parameter types); errors surface through hicu_check_launch.
+template <typename... KArgs, typename... Args>
+inline void hicu_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                        Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = hicu_pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  (void)cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 int hicu_set_error(int code, const char* msg);
 int hicu_check_cuda(cudaError_t e, const char* where);
 // count one kernel launch and check it

@@ -187,6 +187,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
                const float2* __restrict__ qt, float2* __restrict__ out, const float2* __restrict__ uin,
                const uint8_t* __restrict__ mask, const float2* __restrict__ y, const float2* __restrict__ x0,
                double* __restrict__ parts) {
+  hicu_pdl_entry();
   constexpr int NV = MODE == 0 ? 1 : (MODE == 1 ? 2 : 4);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -707,7 +708,7 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   if (grid > hicu_sm_count()) grid = hicu_sm_count();
   if (grid > nparts_total) grid = nparts_total;
   if (grid < 1) grid = 1;
-  conv_tc_kernel<MODE><<<(int)grid, kThreads, smem, st>>>(tm, P, g.pos, qt, out, uin, mask, y, x0, parts);
+  hicu_launch(conv_tc_kernel<MODE>, (int)grid, kThreads, smem, st, tm, P, g.pos, qt, out, uin, mask, y, x0, parts);
   return hicu_check_launch("conv_tc_kernel");
 }
 

@@ -41,6 +41,7 @@ __device__ __forceinline__ double2 load_op(const double2* A, int lda, bool conjT
 
 __global__ void zgemm_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restrict__ A, int lda,
                              const double2* __restrict__ B, int ldb, double2* __restrict__ C, int ldc) {
+  hicu_pdl_entry();
   __shared__ double2 As[16][17];
   __shared__ double2 Bs[16][17];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -67,6 +68,7 @@ constexpr int kZgK = 256;
 __global__ void __launch_bounds__(256)
 zgemm_panel_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restrict__ A, int lda,
                    const double2* __restrict__ B, int ldb, double2* __restrict__ C, int ldc) {
+  hicu_pdl_entry();
   extern __shared__ double2 zp[];
   double2* As = zp;              // 16 x (k+1): row r of op(A), padded
   double2* Bs = zp + 16 * (k + 1);  // k x 17: op(B) rows, padded
@@ -103,11 +105,11 @@ int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int 
     const size_t smem = ((size_t)16 * (k + 1) + (size_t)k * 17) * sizeof(double2);
     hicu_allow_max_smem((const void*)zgemm_panel_kernel);
     dim3 grid((n + 15) / 16, (m + 15) / 16);
-    zgemm_panel_kernel<<<grid, 256, smem, st>>>(opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
+    hicu_launch(zgemm_panel_kernel, grid, 256, smem, st, opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
     return hicu_check_launch("zgemm_panel_kernel");
   }
   dim3 grid((n + 15) / 16, (m + 15) / 16);
-  zgemm_kernel<<<grid, 256, 0, st>>>(opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
+  hicu_launch(zgemm_kernel, grid, 256, 0, st, opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
   return hicu_check_launch("zgemm_kernel");
 }
 
@@ -119,6 +121,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(512)
 chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, const double2* __restrict__ G,
             int n, double2* __restrict__ gws, double* __restrict__ nu_out, int* __restrict__ status) {
+  hicu_pdl_entry();
   extern __shared__ double2 sA[];
   double2* A = SMEM ? sA : gws;
   __shared__ double s_scale;
@@ -184,6 +187,7 @@ chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, c
 __global__ void trsm_rows_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
                                  const double* __restrict__ nu_p, const double2* __restrict__ R, bool r_smem,
                                  double2* __restrict__ W) {
+  hicu_pdl_entry();
   extern __shared__ double2 sm[];
   const int warps = blockDim.x >> 5;
   double2* sR = sm;
@@ -226,6 +230,7 @@ constexpr int kTrsmMaxPer = 8;  // ell <= 256
 __global__ void trsm_rl_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
                                const double* __restrict__ nu_p, const double2* __restrict__ R,
                                double2* __restrict__ W) {
+  hicu_pdl_entry();
   extern __shared__ double2 smr[];
   double2* sR = smr;                                       // ell x ell (upper)
   double* rinv = reinterpret_cast<double*>(sR + (size_t)ell * ell);  // 1 / R_jj
@@ -292,6 +297,7 @@ __global__ void __launch_bounds__(1024)
 jacobi_kernel(int ell, const double2* __restrict__ Mg, double2* __restrict__ gws, bool use_smem, int max_sweeps,
               double tol, RotEntry* __restrict__ log, int* __restrict__ nrounds_out, double* __restrict__ evals,
               int* __restrict__ order, int* __restrict__ status) {
+  hicu_pdl_entry();
   extern __shared__ double2 sA[];
   double2* A = use_smem ? sA : gws;
   const int m = ell + (ell & 1);
@@ -380,6 +386,7 @@ __global__ void rot_apply_kernel(int n, int ell, int r, const double2* __restric
                                  const int* __restrict__ nrounds_p, const double* __restrict__ evals,
                                  const int* __restrict__ order, double2* __restrict__ V, int* __restrict__ status,
                                  bool scale) {
+  hicu_pdl_entry();
   extern __shared__ double2 sw[];
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -425,6 +432,7 @@ __global__ void rot_apply_kernel(int n, int ell, int r, const double2* __restric
 // the free-running trajectory, reproducible by the oracle.
 __global__ void canon_phase_kernel(int n, int r, double2* __restrict__ V, const double* __restrict__ lam,
                                    int* __restrict__ status) {
+  hicu_pdl_entry();
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int t = blockIdx.x * warps + warp; t < r; t += gridDim.x * warps) {
@@ -465,6 +473,7 @@ __global__ void __launch_bounds__(1024)
 householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ gws,
                    bool use_smem, double2* __restrict__ refl, double2* __restrict__ tau, int* __restrict__ flags,
                    int* __restrict__ status) {
+  hicu_pdl_entry();
   extern __shared__ double2 sV[];
   double2* sw = sV;                                   // current reflector w (n)
   double2* v = use_smem ? sV + n : gws;  // column-major: element (k, j) at v[j*n + k] (conflict-free)
@@ -616,6 +625,7 @@ __device__ __forceinline__ void hh2_reflector(int n, int c, const double2* vc, d
 __global__ void __launch_bounds__(1024)
 householder2_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
                     double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  hicu_pdl_entry();
   extern __shared__ double2 sh2[];
   double2* sw = sh2;           // 2 x n (double-buffered reflector w)
   double2* v = sh2 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
@@ -750,6 +760,7 @@ __device__ __forceinline__ void hh3_build(int n, int c, const double2 (&x)[kHh3P
 __global__ void __launch_bounds__(kHh3Threads)
 householder3_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
                     double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  hicu_pdl_entry();
   extern __shared__ double2 sh3[];
   double2* sw = sh3;           // 2 x n (double-buffered reflector w)
   double2* v = sh3 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
@@ -842,6 +853,7 @@ __device__ unsigned long long g_hh4_trace[8];  // debug (HICU_HH_TRACE): summed 
 __global__ void __launch_bounds__(kHb4Threads)
 householder4_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
                     double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  hicu_pdl_entry();
   extern __shared__ double2 sh4[];
   const int ldv = n + 1;
   double2* v = sh4;                               // r x ldv, element (k, j) at v[j*ldv + k]
@@ -985,6 +997,7 @@ constexpr int kReflChunk = 8;
 __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
                                         const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
                                         double2* __restrict__ B, float2* __restrict__ out32, int p) {
+  hicu_pdl_entry();
   extern __shared__ double2 sb[];
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1041,6 +1054,7 @@ __global__ void __launch_bounds__(kArWarps * 32)
 apply_reflectors_res_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
                             const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
                             double2* __restrict__ B, float2* __restrict__ out32, int p) {
+  hicu_pdl_entry();
   extern __shared__ double2 sar[];
   double2* ws = sar;                          // r x n reflectors
   double2* ts = ws + (size_t)r * n;           // r taus
@@ -1168,9 +1182,9 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     const bool sm = bytes <= kSmemCap;
     if (sm) {
       hicu_allow_max_smem((const void*)chol_kernel<true>);
-      chol_kernel<true><<<1, 512, bytes, st>>>(ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
+      hicu_launch(chol_kernel<true>, 1, 512, bytes, st, ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
     } else {
-      chol_kernel<false><<<1, 512, 0, st>>>(ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
+      hicu_launch(chol_kernel<false>, 1, 512, 0, st, ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
     }
     if ((s = hicu_check_launch("chol_kernel"))) return s;
   }
@@ -1179,7 +1193,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     if (rbytes + (size_t)ell * sizeof(double) <= kSmemCap) {
       const int warps = 4;
       hicu_allow_max_smem((const void*)trsm_rl_kernel);
-      trsm_rl_kernel<<<(n + warps - 1) / warps, warps * 32, rbytes + (size_t)ell * sizeof(double), st>>>(
+      hicu_launch(trsm_rl_kernel, (n + warps - 1) / warps, warps * 32, rbytes + (size_t)ell * sizeof(double), st, 
           n, ell, w.Y, Om, w.nu, w.C, w.W);
       if ((s = hicu_check_launch("trsm_rl_kernel"))) return s;
     } else {
@@ -1189,7 +1203,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     const size_t smem = (sm ? rbytes : 0) + rowb;
     hicu_allow_max_smem((const void*)trsm_rows_kernel);
     const int blocks = (n + warps - 1) / warps;
-    trsm_rows_kernel<<<blocks, warps * 32, smem, st>>>(n, ell, w.Y, Om, w.nu, w.C, sm, w.W);
+    hicu_launch(trsm_rows_kernel, blocks, warps * 32, smem, st, n, ell, w.Y, Om, w.nu, w.C, sm, w.W);
     if ((s = hicu_check_launch("trsm_rows_kernel"))) return s;
     }
   }
@@ -1198,7 +1212,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   if ((s = hicu_heev_top(ell, r, w.M, w.evals, w.F, w.heev, st))) return s;
   // V = W F Lambda^{-1/2}
   if ((s = zgemm_launch('N', 'N', n, r, ell, w.W, ell, w.F, r, (double2*)V, r, st))) return s;
-  canon_phase_kernel<<<(r + 7) / 8, 256, 0, st>>>(n, r, (double2*)V, w.evals, status_dev);
+  hicu_launch(canon_phase_kernel, (r + 7) / 8, 256, 0, st, n, r, (double2*)V, w.evals, status_dev);
   if ((s = hicu_check_launch("canon_phase_kernel"))) return s;
   return HICU_OK;
 }
@@ -1224,7 +1238,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     // Z 18K, trailing 15K), kept for the blocked-QR work that follows.
     if (getenv("HICU_HOUSEHOLDER4") && b4 <= (size_t)227 * 1024 - 1024) {
       hicu_allow_max_smem((const void*)householder4_kernel);
-      householder4_kernel<<<1, kHb4Threads, b4, (cudaStream_t)stream>>>(n, r, (const double2*)V, tol, (double2*)refl,
+      hicu_launch(householder4_kernel, 1, kHb4Threads, b4, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl,
                                                                          (double2*)tau, flags, status_dev);
       if (getenv("HICU_HH_TRACE")) {
         unsigned long long h[8];
@@ -1238,7 +1252,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
   }
   if (getenv("HICU_HOUSEHOLDER3") && n <= 32 * kHh3Per && bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
     hicu_allow_max_smem((const void*)householder3_kernel);
-    householder3_kernel<<<1, kHh3Threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream>>>(
+    hicu_launch(householder3_kernel, 1, kHh3Threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
         n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev);
     if (getenv("HICU_HH_TRACE")) {
       unsigned h[64];
@@ -1253,12 +1267,12 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
   }
   if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
     hicu_allow_max_smem((const void*)householder2_kernel);
-    householder2_kernel<<<1, 1024, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream>>>(
+    hicu_launch(householder2_kernel, 1, 1024, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
         n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev);
     return hicu_check_launch("householder2_kernel");
   }
   hicu_allow_max_smem((const void*)householder_kernel);
-  householder_kernel<<<1, 1024, (sm ? bytes : 0) + (size_t)n * sizeof(double2), (cudaStream_t)stream>>>(
+  hicu_launch(householder_kernel, 1, 1024, (sm ? bytes : 0) + (size_t)n * sizeof(double2), (cudaStream_t)stream, 
       n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
   return hicu_check_launch("householder_kernel");
 }
@@ -1271,7 +1285,7 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
     const size_t res = ((size_t)r * n + r + (size_t)kArWarps * n) * sizeof(double2) + (size_t)r * sizeof(int);
     if (r >= 1 && n <= 32 * kArPer && res <= (size_t)210 * 1024) {
       hicu_allow_max_smem((const void*)apply_reflectors_res_kernel);
-      apply_reflectors_res_kernel<<<(cols + kArWarps - 1) / kArWarps, kArWarps * 32, res, (cudaStream_t)stream>>>(
+      hicu_launch(apply_reflectors_res_kernel, (cols + kArWarps - 1) / kArWarps, kArWarps * 32, res, (cudaStream_t)stream, 
           n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B,
           (float2*)out32, p ? p : 1);
       return hicu_check_launch("apply_reflectors_res_kernel");
@@ -1283,7 +1297,7 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
   if (smem > kSmemCap) return hicu_set_error(HICU_ERR_SIZE, "apply_reflectors: n too large");
   hicu_allow_max_smem((const void*)apply_reflectors_kernel);
   const int blocks = (cols + warps - 1) / warps;
-  apply_reflectors_kernel<<<blocks, warps * 32, smem, (cudaStream_t)stream>>>(
+  hicu_launch(apply_reflectors_kernel, blocks, warps * 32, smem, (cudaStream_t)stream, 
       n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B, (float2*)out32,
       p ? p : 1);
   return hicu_check_launch("apply_reflectors_kernel");
@@ -1298,6 +1312,7 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
 namespace {
 
 __global__ void eye_kernel(int n, double2* __restrict__ I) {
+  hicu_pdl_entry();
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x)
     I[e] = cd((e / n) == (e % n) ? 1.0 : 0.0, 0.0);
 }
@@ -1305,6 +1320,7 @@ __global__ void eye_kernel(int n, double2* __restrict__ I) {
 __global__ void coil_phase_kernel(int nc, int nv, const double2* __restrict__ E, const double* __restrict__ evals,
                                   const int* __restrict__ order, double2* __restrict__ basis,
                                   double* __restrict__ evals_out) {
+  hicu_pdl_entry();
   const int j = threadIdx.x;
   if (j >= nc) return;
   int best = 0;
@@ -1340,18 +1356,18 @@ extern "C" int hicu_coil_basis(int nc, int nv, const void* cov, void* basis, dou
   int* status = (int*)(E + (size_t)nc * nc);
   cudaStream_t st = (cudaStream_t)stream;
   int s;
-  eye_kernel<<<1, 256, 0, st>>>(nc, I);
+  hicu_launch(eye_kernel, 1, 256, 0, st, nc, I);
   if ((s = hicu_check_launch("eye_kernel"))) return s;
   const size_t bytes = (size_t)nc * nc * sizeof(double2);
   hicu_allow_max_smem((const void*)jacobi_kernel);
-  jacobi_kernel<<<1, 1024, bytes, st>>>(nc, (const double2*)cov, w.scratch, true, kMaxSweeps, 1e-15, w.log,
+  hicu_launch(jacobi_kernel, 1, 1024, bytes, st, nc, (const double2*)cov, w.scratch, true, kMaxSweeps, 1e-15, w.log,
                                         w.nrounds, w.evals, w.order, status);
   if ((s = hicu_check_launch("jacobi_kernel"))) return s;
   // E = I J with columns in descending-eigenvalue order (no scaling)
-  rot_apply_kernel<<<1, 32 * 8, (size_t)8 * nc * sizeof(double2), st>>>(nc, nc, nc, I, w.log, w.nrounds, w.evals,
+  hicu_launch(rot_apply_kernel, 1, 32 * 8, (size_t)8 * nc * sizeof(double2), st, nc, nc, nc, I, w.log, w.nrounds, w.evals,
                                                                        w.order, E, nullptr, false);
   if ((s = hicu_check_launch("rot_apply_kernel"))) return s;
   // E columns are already in descending order; identity order for the phase step
-  coil_phase_kernel<<<1, 32, 0, st>>>(nc, nv, E, w.evals, w.order, (double2*)basis, evals);
+  hicu_launch(coil_phase_kernel, 1, 32, 0, st, nc, nv, E, w.evals, w.order, (double2*)basis, evals);
   return hicu_check_launch("coil_phase_kernel");
 }

@@ -37,6 +37,7 @@ template <bool CIRC>
 __global__ void __launch_bounds__(kThreads)
 gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t rows_per_split,
                  double2* __restrict__ partials) {
+  hicu_pdl_entry();
   __shared__ float2 As[kBK][kTile];
   __shared__ float2 Bs[kBK][kTile];
   __shared__ int64_t rbase[kBK];
@@ -117,6 +118,7 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
 // G[a][b] (a <= b) = sum over splits in order; G[b][a] = conj.
 __global__ void gram_reduce_kernel(int n, int splits, const double2* __restrict__ partials,
                                    double2* __restrict__ G) {
+  hicu_pdl_entry();
   const int64_t total = (int64_t)n * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -146,14 +148,14 @@ int hicu_gram_simt(const DevGeom& g, const float2* x, double2* G, void* ws, size
   if (ws_bytes < need) return hicu_set_error(HICU_ERR_WORKSPACE, "gram: workspace too small");
   dim3 grid(p.npairs, p.splits);
   if (g.ncirc > 0)
-    gram_simt_kernel<true><<<grid, kThreads, 0, st>>>(g, x, p.ntile, p.rows_per_split, (double2*)ws);
+    hicu_launch(gram_simt_kernel<true>, grid, kThreads, 0, st, g, x, p.ntile, p.rows_per_split, (double2*)ws);
   else
-    gram_simt_kernel<false><<<grid, kThreads, 0, st>>>(g, x, p.ntile, p.rows_per_split, (double2*)ws);
+    hicu_launch(gram_simt_kernel<false>, grid, kThreads, 0, st, g, x, p.ntile, p.rows_per_split, (double2*)ws);
   int s = hicu_check_launch("gram_simt_kernel");
   if (s) return s;
   int64_t total = (int64_t)g.n * g.n;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 1184) blocks = 1184;
-  gram_reduce_kernel<<<blocks, 256, 0, st>>>(g.n, p.splits, (const double2*)ws, G);
+  hicu_launch(gram_reduce_kernel, blocks, 256, 0, st, g.n, p.splits, (const double2*)ws, G);
   return hicu_check_launch("gram_reduce_kernel");
 }

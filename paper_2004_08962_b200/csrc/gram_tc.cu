@@ -145,6 +145,7 @@ __device__ __forceinline__ void tmem_ld16_raw(uint32_t taddr, uint32_t (&r)[16])
 // MN row j (0..15), row k: ks*list*512 + (2q + j/8)*256 + ((k%8)/4)*128 + (j%8)*16 + (k%4)*4.
 __global__ void __launch_bounds__(kThreads, 1)
 gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ tap_off, float* __restrict__ part) {
+  hicu_pdl_entry();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], empty_bar[kMaxStages], tfull[2], tempty[2];
@@ -349,6 +350,7 @@ struct TmapSet {
 
 __global__ void gram_planar_kernel(int64_t nlines, int dlast, int nblk, int nshift, int roff_last,
                                    const float* __restrict__ x, float* __restrict__ xt) {
+  hicu_pdl_entry();
   // one thread per (line, blk, f, t) of one copy; t fastest (coalesced writes)
   const int64_t per_copy = nlines * nblk * 256;
   const int64_t total = per_copy * nshift;
@@ -368,6 +370,7 @@ __global__ void gram_planar_kernel(int64_t nlines, int dlast, int nblk, int nshi
 __global__ void __launch_bounds__(kThreads2, 1)
 gram_tc2_kernel(const __grid_constant__ TmapSet tms, TcParams p, const int32_t* __restrict__ pos, int ndim,
                 float* __restrict__ part, int dbg) {
+  hicu_pdl_entry();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full_bar[kMaxStages], ready_bar[kMaxStages], empty_bar[kMaxStages], tfull[2],
@@ -578,6 +581,7 @@ gram_tc2_kernel(const __grid_constant__ TmapSet tms, TcParams p, const int32_t* 
 // over splits in fp64 in a fixed order; mirrored conjugate below the diagonal.
 __global__ void gram_tc_reduce_kernel(int n, int nc, int T, int splits, PairTable pt, int ntn,
                                       const float* __restrict__ part, double2* __restrict__ G) {
+  hicu_pdl_entry();
   const int64_t total = (int64_t)n * n;
   const size_t blk = (size_t)128 * kPartCols;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -610,6 +614,7 @@ __global__ void gram_tc_reduce_kernel(int n, int nc, int T, int splits, PairTabl
 
 // per tap: flat float offset of its coil-0 sample relative to the row base (= 2*koff)
 __global__ void tc_tap_table_kernel(int T, int nc, const int64_t* __restrict__ koff, int* __restrict__ out) {
+  hicu_pdl_entry();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < T) out[t] = (int)(2 * koff[(size_t)t * nc]);
 }
@@ -744,7 +749,7 @@ int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t
     {
       const int64_t total = nlines * nblk * 256 * nshift;
       const int blocks = (int)hmin64((total + 255) / 256, (int64_t)hicu_sm_count() * 16);
-      gram_planar_kernel<<<blocks, 256, 0, st>>>(nlines, dlast, nblk, nshift, (int)g.roff[L - 1], (const float*)x,
+      hicu_launch(gram_planar_kernel, blocks, 256, 0, st, nlines, dlast, nblk, nshift, (int)g.roff[L - 1], (const float*)x,
                                                  xt);
       if ((s = hicu_check_launch("gram_planar_kernel"))) return s;
     }
@@ -762,17 +767,17 @@ int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t
     hicu_allow_max_smem((const void*)gram_tc2_kernel);
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("HICU_GRAM_DEBUG") ? atoi(getenv("HICU_GRAM_DEBUG")) : 0;
-    gram_tc2_kernel<<<grid, kThreads2, pl.smem_bytes, st>>>(tms, pl.p, g.pos, g.ndim, part, dbg);
+    hicu_launch(gram_tc2_kernel, grid, kThreads2, pl.smem_bytes, st, tms, pl.p, g.pos, g.ndim, part, dbg);
     if ((s = hicu_check_launch("gram_tc2_kernel"))) return s;
   } else {
-    tc_tap_table_kernel<<<(g.nsp + 127) / 128, 128, 0, st>>>(g.nsp, g.nc, g.koff, toff);
+    hicu_launch(tc_tap_table_kernel, (g.nsp + 127) / 128, 128, 0, st, g.nsp, g.nc, g.koff, toff);
     if ((s = hicu_check_launch("tc_tap_table_kernel"))) return s;
     hicu_allow_max_smem((const void*)gram_tc_kernel);
-    gram_tc_kernel<<<grid, kThreads, pl.smem_bytes, st>>>((const float*)x, pl.p, toff, part);
+    hicu_launch(gram_tc_kernel, grid, kThreads, pl.smem_bytes, st, (const float*)x, pl.p, toff, part);
     if ((s = hicu_check_launch("gram_tc_kernel"))) return s;
   }
   const int64_t total = (int64_t)g.n * g.n;
   const int rb = (int)hmin64((total + 255) / 256, 1184);
-  gram_tc_reduce_kernel<<<rb, 256, 0, st>>>(g.n, g.nc, pl.p.T, pl.splits, pl.pt, pl.ntiles, part, G);
+  hicu_launch(gram_tc_reduce_kernel, rb, 256, 0, st, g.n, g.nc, pl.p.T, pl.splits, pl.pt, pl.ntiles, part, G);
   return hicu_check_launch("gram_tc_reduce_kernel");
 }

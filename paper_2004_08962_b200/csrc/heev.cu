@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(512)
 hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
              double* __restrict__ d, double* __restrict__ e, double2* __restrict__ tau,
              double2* __restrict__ Vt) {
+  hicu_pdl_entry();
   extern __shared__ double2 sA[];
   double2* A = SMEM ? sA : Aws;
   const int lda = l + 1;
@@ -191,6 +192,7 @@ __device__ __forceinline__ void hetrd2_reflector(int l, int k, const double2* A,
 __global__ void __launch_bounds__(512)
 hetrd2_kernel(int l, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
               double2* __restrict__ tau, double2* __restrict__ Vt) {
+  hicu_pdl_entry();
   extern __shared__ double2 A[];
   const int lda = l + 1;
   __shared__ double2 sv[2][kHetrd2Max + 2], sw[kHetrd2Max + 2];
@@ -314,6 +316,7 @@ __device__ __forceinline__ void hetrd3_reflector(int k, double tail, double2 akk
 __global__ void __launch_bounds__(128)
 hetrd3_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
               double2* __restrict__ tau, double2* __restrict__ Vt) {
+  hicu_pdl_entry();
   extern __shared__ double2 A[];
   __shared__ double2 sv[kHetrd3Max], sw[kHetrd3Max];
   __shared__ double2 red[4];
@@ -434,6 +437,7 @@ constexpr int kHetrd4Max = 128;
 __global__ void __launch_bounds__(512)
 hetrd4_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
               double2* __restrict__ tau, double2* __restrict__ Vt) {
+  hicu_pdl_entry();
   extern __shared__ double2 A[];
   __shared__ double2 sw[kHetrd4Max];
   __shared__ double2 red[16];
@@ -605,6 +609,7 @@ __device__ __forceinline__ int sturm_count_poly(int l, const double* d, const do
 // One warp per target eigenvalue (j-th largest, j < r): 33-way multisection.
 __global__ void stebz_kernel(int l, int r, const double* __restrict__ dg, const double* __restrict__ eg,
                              double* __restrict__ lam) {
+  hicu_pdl_entry();
   __shared__ double d[256], e2[256];
   __shared__ double s_lo, s_hi, s_piv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -658,6 +663,7 @@ __global__ void stebz_kernel(int l, int r, const double* __restrict__ dg, const 
 // z is l x r column-major (z[j*l + i]).
 __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const double* __restrict__ e,
                              const double* __restrict__ lam, double* __restrict__ z) {
+  hicu_pdl_entry();
   extern __shared__ double sm[];
   __shared__ double sd[256], se[256];
   const int T = blockDim.x, t = threadIdx.x;
@@ -747,6 +753,7 @@ __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const d
 // descending order, then fix a sign convention (largest entry positive).
 __global__ void __launch_bounds__(256) cluster_orth_kernel(int l, int r, const double* __restrict__ lam,
                                                            double* __restrict__ z, double ctol) {
+  hicu_pdl_entry();
   __shared__ double red[8];
   __shared__ double s_dot;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -799,6 +806,7 @@ __global__ void __launch_bounds__(256) cluster_orth_kernel(int l, int r, const d
 constexpr int kBtChunk = 16;
 __global__ void back_transform_kernel(int l, int r, const double2* __restrict__ Vt, const double2* __restrict__ tau,
                                       const double* __restrict__ z, double2* __restrict__ F) {
+  hicu_pdl_entry();
   extern __shared__ double2 sm2[];
   const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2* x = sm2 + (size_t)warp * l;
@@ -841,6 +849,7 @@ constexpr int kBtPer = 4;  // l <= 128 for the resident back-transform
 __global__ void __launch_bounds__(kBtWarps * 32)
 back_transform_res_kernel(int l, int r, const double2* __restrict__ Vt, const double2* __restrict__ tau,
                           const double* __restrict__ z, double2* __restrict__ F) {
+  hicu_pdl_entry();
   extern __shared__ double2 sm3[];
   double2* vs = sm3;                          // (l-1) x l reflectors
   double2* ts = vs + (size_t)(l - 1) * l;     // l-1 taus
@@ -917,43 +926,43 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
     const size_t a4 = (size_t)l * lda4 * sizeof(double2);
     if (l <= kHetrd4Max && a4 <= 180 * 1024) {
       hicu_allow_max_smem((const void*)hetrd4_kernel);
-      hetrd4_kernel<<<1, 512, a4, st>>>(l, lda4, A, d, e, tau, Vt);
+      hicu_launch(hetrd4_kernel, 1, 512, a4, st, l, lda4, A, d, e, tau, Vt);
     } else if (l <= kHetrd3Max && a3 <= 180 * 1024) {
       hicu_allow_max_smem((const void*)hetrd3_kernel);
-      hetrd3_kernel<<<1, 128, a3, st>>>(l, lda3, A, d, e, tau, Vt);
+      hicu_launch(hetrd3_kernel, 1, 128, a3, st, l, lda3, A, d, e, tau, Vt);
     } else if (l <= kHetrd2Max) {
       hicu_allow_max_smem((const void*)hetrd2_kernel);
-      hetrd2_kernel<<<1, 512, abytes, st>>>(l, A, d, e, tau, Vt);
+      hicu_launch(hetrd2_kernel, 1, 512, abytes, st, l, A, d, e, tau, Vt);
     } else {
       hicu_allow_max_smem((const void*)hetrd_kernel<true>);
-      hetrd_kernel<true><<<1, 512, abytes, st>>>(l, A, Aws, d, e, tau, Vt);
+      hicu_launch(hetrd_kernel<true>, 1, 512, abytes, st, l, A, Aws, d, e, tau, Vt);
     }
   } else {
-    hetrd_kernel<false><<<1, 512, 0, st>>>(l, A, Aws, d, e, tau, Vt);
+    hicu_launch(hetrd_kernel<false>, 1, 512, 0, st, l, A, Aws, d, e, tau, Vt);
   }
   if ((s = hicu_check_launch("hetrd_kernel"))) return s;
   const int wpb = 1;  // one warp (one eigenvalue) per SM: the Sturm recurrence is a division chain
-  stebz_kernel<<<(r + wpb - 1) / wpb, wpb * 32, 0, st>>>(l, r, d, e, lam);
+  hicu_launch(stebz_kernel, (r + wpb - 1) / wpb, wpb * 32, 0, st, l, r, d, e, lam);
   if ((s = hicu_check_launch("stebz_kernel"))) return s;
   {
     int T = 32;
     while (T > 1 && (size_t)5 * l * T * sizeof(double) > 200 * 1024) T >>= 1;
     const size_t smem = (size_t)5 * l * T * sizeof(double);
     hicu_allow_max_smem((const void*)stein_kernel);
-    stein_kernel<<<(r + T - 1) / T, T, smem, st>>>(l, r, d, e, lam, z);
+    hicu_launch(stein_kernel, (r + T - 1) / T, T, smem, st, l, r, d, e, lam, z);
   }
   if ((s = hicu_check_launch("stein_kernel"))) return s;
-  cluster_orth_kernel<<<1, 256, 0, st>>>(l, r, lam, z, 1e-9);
+  hicu_launch(cluster_orth_kernel, 1, 256, 0, st, l, r, lam, z, 1e-9);
   if ((s = hicu_check_launch("cluster_orth_kernel"))) return s;
   const size_t res = ((size_t)(l - 1) * l + l + (size_t)kBtWarps * l) * sizeof(double2);
   if (res <= 200 * 1024 && l <= 32 * kBtPer) {
     hicu_allow_max_smem((const void*)back_transform_res_kernel);
-    back_transform_res_kernel<<<(r + kBtWarps - 1) / kBtWarps, kBtWarps * 32, res, st>>>(l, r, Vt, tau, z, F);
+    hicu_launch(back_transform_res_kernel, (r + kBtWarps - 1) / kBtWarps, kBtWarps * 32, res, st, l, r, Vt, tau, z, F);
     return hicu_check_launch("back_transform_res_kernel");
   }
   const int bw = 8;
   const size_t smem = ((size_t)bw * l + (size_t)kBtChunk * l) * sizeof(double2);
   hicu_allow_max_smem((const void*)back_transform_kernel);
-  back_transform_kernel<<<(r + bw - 1) / bw, bw * 32, smem, st>>>(l, r, Vt, tau, z, F);
+  hicu_launch(back_transform_kernel, (r + bw - 1) / bw, bw * 32, smem, st, l, r, Vt, tau, z, F);
   return hicu_check_launch("back_transform_kernel");
 }

@@ -48,6 +48,7 @@ template <int PMAX, bool CIRC, int MODE>
 __global__ void __launch_bounds__(kConvThreads)
 conv_kernel(DevGeom g, const float2* __restrict__ y, const float2* __restrict__ qt, int p,
             float2* __restrict__ u, double* __restrict__ parts) {
+  hicu_pdl_entry();
   extern __shared__ unsigned char smem_raw[];
   float2* sq = reinterpret_cast<float2*>(smem_raw);                       // n * PMAX
   int64_t* skoff = reinterpret_cast<int64_t*>(sq + (size_t)g.n * PMAX);   // n
@@ -115,6 +116,7 @@ scatter_kernel(DevGeom g, const float2* __restrict__ qt, int p, const float2* __
                const uint8_t* __restrict__ mask, const float2* __restrict__ y,
                const float2* __restrict__ x0, int dc_mode, float lam, float2* __restrict__ gout,
                double* __restrict__ parts) {
+  hicu_pdl_entry();
   extern __shared__ unsigned char smem_raw[];
   float2* sq = reinterpret_cast<float2*>(smem_raw);                        // n * PMAX (conj)
   int32_t* spos = reinterpret_cast<int32_t*>(sq + (size_t)g.n * PMAX);      // n * ndim
@@ -224,6 +226,7 @@ update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir
               const double* __restrict__ dc_parts, int n_dc,
               const double* __restrict__ els_parts, int n_els, int dc_mode, double lam,
               double* __restrict__ rec, bool vec) {
+  hicu_pdl_entry();
   __shared__ double s_eta;
   __shared__ int s_skip;
   __shared__ double sums[7];
@@ -321,6 +324,7 @@ update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir
 
 __global__ void ser_kernel(int64_t N, const float2* __restrict__ ref, const float2* __restrict__ y,
                            double* __restrict__ parts) {
+  hicu_pdl_entry();
   double e = 0.0, r = 0.0;
   for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N;
        m += (int64_t)gridDim.x * blockDim.x) {
@@ -346,6 +350,7 @@ template <int PMAX, int NCMAX, bool CIRC, int MODE>
 __global__ void __launch_bounds__(kConvThreads)
 conv_coil_kernel(DevGeom g, const float2* __restrict__ y, const float2* __restrict__ qt, int p,
                  float2* __restrict__ u, double* __restrict__ parts) {
+  hicu_pdl_entry();
   extern __shared__ unsigned char smem_raw[];
   const int nc = g.nc, nsp = g.nsp;
   float2* sq = reinterpret_cast<float2*>(smem_raw);                          // n * PMAX
@@ -424,6 +429,7 @@ scatter_coil_kernel(DevGeom g, const float2* __restrict__ qt, int p, const float
                     const uint8_t* __restrict__ mask, const float2* __restrict__ y,
                     const float2* __restrict__ x0, int dc_mode, float lam, float2* __restrict__ gout,
                     double* __restrict__ parts) {
+  hicu_pdl_entry();
   extern __shared__ unsigned char smem_raw[];
   const int nc = g.nc, nsp = g.nsp, L = g.ndim - 1;
   float2* sq = reinterpret_cast<float2*>(smem_raw);                           // n * PMAX, conj
@@ -530,7 +536,7 @@ int launch_conv_coil(const DevGeom& g, const float2* y, const float2* qt, int p,
   do {                                                                          \
     auto kfn = conv_coil_kernel<PMAX, NCMAX, C, M>;                             \
     hicu_allow_max_smem((const void*)kfn);                                      \
-    kfn<<<blocks, kConvThreads, smem, st>>>(g, y, qt, p, u, parts);             \
+    hicu_launch(kfn, blocks, kConvThreads, smem, st, g, y, qt, p, u, parts);             \
   } while (0)
   if (circ) {
     if (mode == 0) HICU_LAUNCH_CONVC(true, 0); else HICU_LAUNCH_CONVC(true, 1);
@@ -560,11 +566,11 @@ int launch_scatter_coil(const DevGeom& g, const float2* qt, int p, const float2*
   if (g.ncirc > 0) {
     auto kfn = scatter_coil_kernel<PMAX, NCMAX, true>;
     hicu_allow_max_smem((const void*)kfn);
-    kfn<<<blocks, 128, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+    hicu_launch(kfn, blocks, 128, smem, st, g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   } else {
     auto kfn = scatter_coil_kernel<PMAX, NCMAX, false>;
     hicu_allow_max_smem((const void*)kfn);
-    kfn<<<blocks, 128, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+    hicu_launch(kfn, blocks, 128, smem, st, g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   }
   return hicu_check_launch("scatter_coil_kernel");
 }
@@ -598,7 +604,7 @@ int launch_conv(const DevGeom& g, const float2* y, const float2* qt, int p, floa
   do {                                                                                            \
     auto kfn = conv_kernel<PMAX, C, M>;                                                           \
     hicu_allow_max_smem((const void*)kfn);            \
-    kfn<<<blocks, kConvThreads, smem, st>>>(g, y, qt, p, u, parts);                               \
+    hicu_launch(kfn, blocks, kConvThreads, smem, st, g, y, qt, p, u, parts);                               \
   } while (0)
   if (circ) {
     if (mode == 0) HICU_LAUNCH_CONV(true, 0); else HICU_LAUNCH_CONV(true, 1);
@@ -642,11 +648,11 @@ int launch_scatter(const DevGeom& g, const float2* qt, int p, const float2* u, c
   if (g.ncirc > 0) {
     auto kfn = scatter_kernel<PMAX, true>;
     hicu_allow_max_smem((const void*)kfn);
-    kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+    hicu_launch(kfn, blocks, kScatterThreads, smem, st, g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   } else {
     auto kfn = scatter_kernel<PMAX, false>;
     hicu_allow_max_smem((const void*)kfn);
-    kfn<<<blocks, kScatterThreads, smem, st>>>(g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
+    hicu_launch(kfn, blocks, kScatterThreads, smem, st, g, qt, p, u, mask, y, x0, dc_mode, lam, gout, parts);
   }
   return hicu_check_launch("scatter_kernel");
 }
@@ -725,12 +731,13 @@ extern "C" int hicu_step_update(int64_t N, void* y, const void* gdir, const doub
   if (b > cap) b = cap;
   if (b < 1) b = 1;
   const bool vec = (((uintptr_t)y | (uintptr_t)gdir) & 15) == 0;
-  update_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(N, (float2*)y, (const float2*)gdir, obj_parts, n_obj,
+  hicu_launch(update_kernel, (int)b, 256, 0, (cudaStream_t)stream, N, (float2*)y, (const float2*)gdir, obj_parts, n_obj,
                                                            dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec, vec);
   return hicu_check_launch("update_kernel");
 }
 
 __global__ void timestamp_kernel(double* out) {
+  hicu_pdl_entry();
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *out = (double)t;
@@ -746,7 +753,7 @@ int ser_blocks(int64_t N) {
 
 extern "C" int hicu_timestamp(double* out, void* stream) {
   if (!out) return hicu_set_error(HICU_ERR_PARAMETER, "timestamp: null");
-  timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(out);
+  hicu_launch(timestamp_kernel, 1, 1, 0, (cudaStream_t)stream, out);
   return hicu_check_launch("timestamp_kernel");
 }
 
@@ -757,7 +764,7 @@ extern "C" int hicu_ser_parts(int64_t N, const void* ref, const void* y, double*
   if (!ref || !y || !parts || N < 1) return hicu_set_error(HICU_ERR_PARAMETER, "ser: bad arguments");
   const int b = ser_blocks(N);
   if (nparts_out) *nparts_out = b;
-  ser_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(N, (const float2*)ref, (const float2*)y, parts);
+  hicu_launch(ser_kernel, b, 256, 0, (cudaStream_t)stream, N, (const float2*)ref, (const float2*)y, parts);
   return hicu_check_launch("ser_kernel");
 }
 
@@ -770,6 +777,7 @@ namespace {
 template <bool CIRC>
 __global__ void conv_adj_kernel(DevGeom g, const float2* __restrict__ x, const float2* __restrict__ u, int k,
                                 double2* __restrict__ out) {
+  hicu_pdl_entry();
   const int kap = blockIdx.x;
   const int j = blockIdx.y;
   const int32_t* pk = g.pos + (size_t)kap * g.ndim;
@@ -797,10 +805,10 @@ extern "C" int hicu_conv_adj(const hicu_geom* hg, const void* x, const void* u, 
   if (st) return st;
   dim3 grid(g.n, k);
   if (g.ncirc > 0)
-    conv_adj_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(g, (const float2*)x, (const float2*)u, k,
+    hicu_launch(conv_adj_kernel<true>, grid, 256, 0, (cudaStream_t)stream, g, (const float2*)x, (const float2*)u, k,
                                                                   (double2*)out);
   else
-    conv_adj_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(g, (const float2*)x, (const float2*)u, k,
+    hicu_launch(conv_adj_kernel<false>, grid, 256, 0, (cudaStream_t)stream, g, (const float2*)x, (const float2*)u, k,
                                                                    (double2*)out);
   return hicu_check_launch("conv_adj_kernel");
 }
@@ -811,6 +819,7 @@ namespace {
 __global__ void soft_terms_kernel(int64_t N, const float2* __restrict__ g, const float2* __restrict__ y,
                                   const float2* __restrict__ x0, const uint8_t* __restrict__ mask,
                                   double* __restrict__ parts) {
+  hicu_pdl_entry();
   double a = 0.0, b = 0.0, c = 0.0;
   for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N; m += (int64_t)gridDim.x * blockDim.x) {
     if (mask[m] != 1) continue;
@@ -830,7 +839,7 @@ extern "C" int hicu_soft_terms(int64_t N, const void* g, const void* y, const vo
   if (!g || !y || !x0 || !mask || !parts || N < 1) return hicu_set_error(HICU_ERR_PARAMETER, "soft_terms: bad args");
   const int b = ser_blocks(N);
   if (nparts_out) *nparts_out = b;
-  soft_terms_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(N, (const float2*)g, (const float2*)y, (const float2*)x0,
+  hicu_launch(soft_terms_kernel, b, 256, 0, (cudaStream_t)stream, N, (const float2*)g, (const float2*)y, (const float2*)x0,
                                                          mask, parts);
   return hicu_check_launch("soft_terms_kernel");
 }
@@ -845,6 +854,7 @@ namespace {
 __global__ void step_reduce_kernel(const double* __restrict__ obj_parts, int n_obj, const double* __restrict__ dc_parts,
                                    int n_dc, const double* __restrict__ els_parts, int n_els,
                                    double* __restrict__ sums7) {
+  hicu_pdl_entry();
   const double obj_c = warp_sum_parts(obj_parts, n_obj, 1, 0);
   const double gn2 = warp_sum_parts(dc_parts, n_dc, 4, 0);
   const double res2 = warp_sum_parts(dc_parts, n_dc, 4, 1);
@@ -865,6 +875,7 @@ __global__ void step_reduce_kernel(const double* __restrict__ obj_parts, int n_o
 
 __global__ void step_apply_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir,
                                   const double* __restrict__ sums7, int dc_mode, double lam, double* __restrict__ rec) {
+  hicu_pdl_entry();
   double obj = sums7[0], num = sums7[5], den = sums7[6];
   if (dc_mode == 1) {
     obj += lam * sums7[2];
@@ -901,6 +912,7 @@ __global__ void step_apply_kernel(int64_t N, float2* __restrict__ y, const float
 __global__ void dc_apply_kernel(int64_t n, float2* __restrict__ g, const uint8_t* __restrict__ mask,
                                 const float2* __restrict__ y, const float2* __restrict__ x0, int dc_mode, float lam,
                                 double* __restrict__ parts) {
+  hicu_pdl_entry();
   double a_g = 0.0, a_res = 0.0, a_num = 0.0, a_den = 0.0;
   for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
     float2 acc = g[m];
@@ -927,7 +939,7 @@ __global__ void dc_apply_kernel(int64_t n, float2* __restrict__ g, const uint8_t
 extern "C" int hicu_step_reduce(const double* obj_parts, int n_obj, const double* dc_parts, int n_dc,
                                 const double* els_parts, int n_els, double* sums7, void* stream) {
   if (!obj_parts || !dc_parts || !els_parts || !sums7) return hicu_set_error(HICU_ERR_PARAMETER, "step_reduce: null");
-  step_reduce_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(obj_parts, n_obj, dc_parts, n_dc, els_parts, n_els, sums7);
+  hicu_launch(step_reduce_kernel, 1, 32, 0, (cudaStream_t)stream, obj_parts, n_obj, dc_parts, n_dc, els_parts, n_els, sums7);
   return hicu_check_launch("step_reduce_kernel");
 }
 
@@ -937,7 +949,7 @@ extern "C" int hicu_step_apply(int64_t N, void* y, const void* gdir, const doubl
   int64_t b = (N + 255) / 256;
   const int64_t cap = (int64_t)hicu_sm_count() * 4;
   if (b > cap) b = cap;
-  step_apply_kernel<<<(int)b, 256, 0, (cudaStream_t)stream>>>(N, (float2*)y, (const float2*)gdir, sums7, dc_mode,
+  hicu_launch(step_apply_kernel, (int)b, 256, 0, (cudaStream_t)stream, N, (float2*)y, (const float2*)gdir, sums7, dc_mode,
                                                                lam, rec);
   return hicu_check_launch("step_apply_kernel");
 }
@@ -948,7 +960,7 @@ extern "C" int hicu_dc_apply(int64_t n, void* g, const uint8_t* mask, const void
                              double lam, double* parts, void* stream) {
   if (!g || !mask || !parts || n < 1) return hicu_set_error(HICU_ERR_PARAMETER, "dc_apply: bad arguments");
   if (dc_mode == 1 && (!y || !x0)) return hicu_set_error(HICU_ERR_SHAPE, "soft data consistency requires x0");
-  dc_apply_kernel<<<ser_blocks(n), 256, 0, (cudaStream_t)stream>>>(n, (float2*)g, mask, (const float2*)y,
+  hicu_launch(dc_apply_kernel, ser_blocks(n), 256, 0, (cudaStream_t)stream, n, (float2*)g, mask, (const float2*)y,
                                                                    (const float2*)x0, dc_mode, (float)lam, parts);
   return hicu_check_launch("dc_apply_kernel");
 }

@@ -325,6 +325,8 @@ class ReconEngine:
         ns = len(schedule.stages)
         self.stage_data = [None] * ns
         self.host_draws = [None] * ns
+        self.copy_stream = None
+        self.upload_events = {}
         self.recs = [None] * ns
         self.sers = [None] * ns
         self.inject = [None] * ns
@@ -348,12 +350,25 @@ class ReconEngine:
         return self.host_draws[si]
 
     def upload_draws(self, si: int, it0: int = 0, it1: int | None = None):
-        """Async H2D of the staged draws for iterations [it0, it1)."""
+        """Async H2D of the staged draws for iterations [it0, it1) on a
+        dedicated copy stream (the copy engine overlaps the compute stream;
+        in-stream copies would also break the programmatic-launch chain).
+        :meth:`run_stage` makes the compute stream wait for the chunk's event."""
+        torch = self.torch
         om_h, pb_h = self.host_draw_buffers(si)
         om, pb = self.stage_data[si]
         it1 = om.shape[0] if it1 is None else it1
-        om[it0:it1].copy_(om_h[it0:it1], non_blocking=True)
-        pb[it0:it1].copy_(pb_h[it0:it1], non_blocking=True)
+        if self.copy_stream is None:
+            self.copy_stream = torch.cuda.Stream()
+        # the device buffers may still be read by earlier work on the compute stream
+        self.copy_stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(self.copy_stream):
+            om[it0:it1].copy_(om_h[it0:it1], non_blocking=True)
+            pb[it0:it1].copy_(pb_h[it0:it1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+        for it in range(it0, it1):
+            self.upload_events[(si, it)] = ev
         self.h2d_bytes += (om_h[it0:it1].numel() + pb_h[it0:it1].numel()) * 16
 
     def set_host_draws(self, si: int, omega: np.ndarray, pbig: np.ndarray):
@@ -415,6 +430,14 @@ class ReconEngine:
 
     def run_stage(self, si: int, it0: int = 0, iters: int | None = None, stream=None):
         a = self.stage_args(si, it0, iters)
+        n_it = self.schedule.stages[si].iterations if iters is None else iters
+        cur = stream if stream is not None else self.torch.cuda.current_stream()
+        waited = set()
+        for it in range(it0, it0 + n_it):
+            ev = self.upload_events.pop((si, it), None)
+            if ev is not None and id(ev) not in waited:
+                cur.wait_event(ev)
+                waited.add(id(ev))
         nat.check(nat.lib().hicu_run_stage(ctypes.byref(a), nat.stream_handle(stream)), f"stage {si}")
 
     def run_all(self, stream=None):
@@ -444,6 +467,24 @@ class ReconEngine:
 _DRAW_POOL = None
 
 
+class _PhaseTrace:
+    """HICU_E2E_TRACE=1: wall-clock phase marks of hicu_reconstruct on stderr."""
+
+    def __init__(self):
+        import os
+        import time
+
+        self.on = bool(os.environ.get("HICU_E2E_TRACE"))
+        self.t0 = time.perf_counter()
+        self.clock = time.perf_counter
+
+    def __call__(self, name):
+        if self.on:
+            import sys
+
+            print(f"hicu_reconstruct {name}: {1e3 * (self.clock() - self.t0):.2f} ms", file=sys.stderr)
+
+
 def _draw_pool():
     global _DRAW_POOL
     if _DRAW_POOL is None:
@@ -456,10 +497,18 @@ def _draw_pool():
 
 
 def _chunks(schedule: SolverSchedule, per_iter: bool):
+    """Stage chunks issued to the device one at a time.  The very first chunk
+    is a single iteration so the device starts while the host is still
+    drawing the later ones."""
+    first = True
     for si, st in enumerate(schedule.stages):
         step = 1 if per_iter else max(1, min(8, (st.iterations + 3) // 4))
-        for it0 in range(0, st.iterations, step):
-            yield si, it0, min(st.iterations, it0 + step)
+        it0 = 0
+        while it0 < st.iterations:
+            n = 1 if first else step
+            first = False
+            yield si, it0, min(st.iterations, it0 + n)
+            it0 += n
 
 
 def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, reference=None,
@@ -478,6 +527,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
     (trajectory-parity tests).
     """
     watch = _Stopwatch()
+    _tr = _PhaseTrace()
     x0 = np.asarray(x0)
     mask = np.asarray(mask)
     if x0.shape != mask.shape:
@@ -501,7 +551,10 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         if not (1 <= nv <= nc) or nc > 32:
             raise ConfigError(f"coil_compress must be in [1, {min(nc, 32)}], got {coil_compress}")
         xm = np.where(observed_in, x0, 0).astype(np.complex64)  # mask_apply (arrays.py:54-67)
-        xd, md = to_dev(xm), to_dev(observed_in.astype(np.uint8), np.uint8)
+        # pinned staging: the upload is asynchronous with respect to the host
+        xp = torch.from_numpy(xm).pin_memory()
+        xd = xp.to("cuda", non_blocking=True)
+        md = to_dev(observed_in.astype(np.uint8), np.uint8)
         h2d += xm.nbytes + md.numel()
         ydev, mdev, bdev, _ = coil_compress_device(xd.reshape(-1), md.reshape(-1), nc, nv)
         dims = x0.shape[:-1] + (nv,)
@@ -515,7 +568,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
             ref_dev = torch.empty(int(np.prod(dims)), dtype=torch.complex64, device="cuda")
             nat.check(nat.lib().hicu_coil_apply(rd.numel() // nc, nc, nv, rd.data_ptr(), None, bdev.data_ptr(),
                                                 ref_dev.data_ptr(), None, nat.stream_handle()), "coil_apply")
-        basis = bdev.cpu().numpy()
+        basis = bdev  # downloaded after the solve (no synchronisation here)
         x0_exact = None  # observed samples live (in c64) on the device
     else:
         dims = x0.shape
@@ -548,6 +601,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         futs = [pool.submit(_fill_draws, schedule, si, st, kernel.n, it, om_np[it], pb_np[it])
                 for it in range(it0, it1)]
         futures.append((si, it0, it1, futs))
+    _tr("setup")
     eng.stamp_start()
     tails = {}
     for si, it0, it1, futs in futures:
@@ -568,8 +622,11 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
                 xi[observed] = x0_exact[observed]
             iterate_callback(si, it0, xi)
         watch.resume()
+    _tr("issued")
     torch.cuda.synchronize()
+    _tr("device done")
     xhat = eng.download()
+    _tr("download")
     total = watch.pause()
     eng.check_status()
     # ---- records (one device->host read per stage) ----
@@ -616,5 +673,6 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
                      "nullspace": "gram+nystrom (canonical phases)" if lockstep_v is None else "injected",
                      "precision": "c64 data, fp32 FMA, fp64 reductions and nullspace",
                      "h2d_bytes": int(h2d + eng.h2d_bytes), "d2h_bytes": int(d2h)}
-    report.coil_basis = basis
+    report.coil_basis = None if basis is None else basis.cpu().numpy()
+    _tr("end")
     return xhat, report

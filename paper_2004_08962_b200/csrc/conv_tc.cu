@@ -54,7 +54,8 @@ namespace {
 constexpr int kTileM = 128;
 constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
-constexpr int kMaxTaps = 56;               // spatial taps (B images resident in shared memory)
+constexpr int kMaxTaps = 128;              // spatial taps (streamed-B mode)
+constexpr int kMaxTapsRes = 56;            // spatial taps with resident B images (prologue registers)
 constexpr int kHalfBytes = kTileM * 64;    // 8 KB: one 128-row A tile (hi or lo)
 constexpr int kStageBytes = 2 * kHalfBytes;
 constexpr int kMaxStages = 8;
@@ -70,6 +71,8 @@ struct CtParams {
   int kpre[2];            // kernel extents of the prefix axes
   int stages;
   int tbuf_stride;        // TMEM columns between the two accumulator buffers (0: one buffer)
+  int nacc;               // accumulator sets per tile (prefix groups dealt round-robin; shortens chains)
+  int stage_bytes;        // A hi + A lo (+ one prefix group's B image when streamed)
   int dc_mode;
   float lam;
   int nparts_total;       // entries of `parts` (per value) the ABI promised
@@ -181,7 +184,8 @@ __device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, cons
 }
 
 // MODE 0: conv forward (u, obj); 1: conv ELS (Re<w,u>, |w|^2); 2: scatter + DC.
-template <int MODE>
+// BS: streamed B images (rebuilt per stage; several accumulator sets).
+template <int MODE, bool BS>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const int32_t* __restrict__ pos,
                const float2* __restrict__ qt, float2* __restrict__ out, const float2* __restrict__ uin,
@@ -194,12 +198,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   const int nb = P.nb, ng = P.ng, L = P.L, S = P.stages;
   const uint32_t gbytes = (uint32_t)nb * 2048;                  // B image of one prefix: 32 nb rows x 64 B
   uint8_t* sB = smem;
-  uint8_t* sStage = sB + (size_t)ng * gbytes;
-  float* sWin = reinterpret_cast<float*>(sStage + (size_t)S * kStageBytes);  // (128 + nb - 1) x nb x 16
+  uint8_t* sStage = sB + (BS ? 0 : (size_t)ng * gbytes);
+  const int stb = P.stage_bytes;
+  float* sWin = reinterpret_cast<float*>(sStage + (size_t)S * stb);  // (128 + nb - 1) x nb x 16
   __shared__ __align__(8) uint64_t full[kMaxStages], ready[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tslot;
   __shared__ int ga[kMaxGroups][2];
   __shared__ int spos[kMaxTaps][3];
+  __shared__ short tapidx[kMaxGroups * kMaxNb];  // (prefix g, offset b) -> spatial tap or -1
   __shared__ double red[4][NV];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -209,9 +215,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   if (tr && threadIdx.x == 0) trace[0] = gtimer();
 
   // ---- prologue: every global load issued up front ----
-  constexpr int kQPer = (kMaxTaps * 64 + kThreads - 1) / kThreads;
+  constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
   float2 qv[kQPer];
-  const int nq = P.nsp * 64;
+  const int nq = BS ? 0 : P.nsp * 64;
 #pragma unroll
   for (int u = 0; u < kQPer; ++u) {
     const int e = threadIdx.x + u * kThreads;
@@ -224,10 +230,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     ga[g][0] = L == 2 ? g : (L == 3 ? g / P.kpre[1] : 0);
     ga[g][1] = L == 3 ? g % P.kpre[1] : 0;
   }
-  {
+  if (!BS) {
     float4* z = reinterpret_cast<float4*>(sB);
     for (int i = threadIdx.x; i < ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  for (int i = threadIdx.x; i < ng * nb; i += kThreads) tapidx[i] = -1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
@@ -242,6 +249,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   }
   if (warp == 1) tc::tmem_alloc(&tslot, 512);
   __syncthreads();
+  for (int sp = threadIdx.x; sp < P.nsp; sp += kThreads) {
+    const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
+    tapidx[g * nb + spos[sp][L - 1]] = (short)sp;
+  }
   if (tr && threadIdx.x == 0) trace[1] = gtimer();
   // B images: prefix g at sB + g * gbytes; row 16 b + n (hi) / 16 nb + 16 b + n (lo);
   // K-major 64-byte rows, SW64 swizzle on absolute address bits.
@@ -316,7 +327,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
                   c3 = lc[0] - P.roff[0] - ga[g][0];
                 }
               }
-              uint8_t* dst = sStage + (size_t)s * kStageBytes;
+              uint8_t* dst = sStage + (size_t)s * stb;
               if (tr && line == (int)blockIdx.x && c == 0 && g == 0) trace[3] = gtimer();
               tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
               tc::tma_load_4d(dst + 64 * 64, &tmap, 0, c1 + 64, c2, c3, &full[s]);
@@ -339,15 +350,19 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
         for (int c = 0; c < P.chunks; ++c) {
           tc::mbar_wait(&tempty[tb], tph ^ 1);
           tc::fence_after();
-          const uint32_t d = tmem + (uint32_t)(tb * P.tbuf_stride);
-          uint32_t acc = 0;
+          const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
+          int vi = 0;  // valid-group index within the tile -> accumulator set vi % nacc
           for (int g = 0; g < ng; ++g) {
             if (!group_valid<MODE>(P, ga, g, lc)) continue;
             tc::mbar_wait(&ready[s], ph);
             tc::fence_after();
             if (tr && line == (int)blockIdx.x && c == 0 && g == 0) trace[4] = gtimer();
-            const uint32_t ahi = tc::smem_u32(sStage + (size_t)s * kStageBytes), alo = ahi + kHalfBytes;
-            const uint32_t bg = bbase + (uint32_t)g * gbytes;
+            const uint32_t ahi = tc::smem_u32(sStage + (size_t)s * stb), alo = ahi + kHalfBytes;
+            const uint32_t bg = BS ? ahi + 2 * kHalfBytes : bbase + (uint32_t)g * gbytes;
+            const int set = BS ? vi % P.nacc : 0;
+            const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
+            uint32_t acc = BS ? (vi >= P.nacc ? 1u : 0u) : (vi > 0 ? 1u : 0u);
+            ++vi;
             if (!(P.debug & 1)) {
 #pragma unroll
               for (int ks = 0; ks < 2; ++ks) {
@@ -384,12 +399,41 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
           if (!group_valid<MODE>(P, ga, g, lc)) continue;
           tc::mbar_wait(&full[s], ph);
           if (!(P.debug & 4)) {
-            const float4* hi4 = reinterpret_cast<const float4*>(sStage + (size_t)s * kStageBytes);
-            float4* lo4 = reinterpret_cast<float4*>(sStage + (size_t)s * kStageBytes + kHalfBytes);
+            const float4* hi4 = reinterpret_cast<const float4*>(sStage + (size_t)s * stb);
+            float4* lo4 = reinterpret_cast<float4*>(sStage + (size_t)s * stb + kHalfBytes);
 #pragma unroll 4
             for (int i = ct; i < kTileM * 4; i += 128) {
               const float4 v = hi4[i];
               lo4[i] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
+            }
+          }
+          if (BS) {
+            // this prefix group's B image: rows 16 b + n (hi) / 16 nb + 16 b + n (lo)
+            uint8_t* gb = sStage + (size_t)s * stb + 2 * kHalfBytes;
+            for (int e = ct; e < nb * 64; e += 128) {
+              const int b = e >> 6, cc = (e >> 3) & 7, j = e & 7;
+              const int sp = tapidx[g * nb + b];
+              const float2 q = sp >= 0 ? __ldg(qt + (size_t)(sp * 8 + cc) * 8 + j) : make_float2(0.f, 0.f);
+#pragma unroll
+              for (int tp = 0; tp < 2; ++tp)
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                  int n, k;
+                  float v;
+                  if (MODE < 2) {
+                    n = 2 * j + tp;
+                    k = 2 * cc + t;
+                    v = tp == 0 ? (t == 0 ? q.x : -q.y) : (t == 0 ? q.y : q.x);
+                  } else {
+                    n = 2 * cc + tp;
+                    k = 2 * j + t;
+                    v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
+                  }
+                  const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
+                  const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
+                  *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
+                  *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
+                }
             }
           }
           tc::fence_proxy_async();
@@ -414,6 +458,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
       if (L >= 2) obase += (int64_t)lc[0] * P.ostride[0];
       if (L >= 3) obase += (int64_t)lc[1] * P.ostride[1];
       const bool active = line_active<MODE>(P, ga, lc);
+      int nvalid = 1;
+      if (BS) {
+        nvalid = 0;
+        for (int gg = 0; gg < ng; ++gg) nvalid += group_valid<MODE>(P, ga, gg, lc) ? 1 : 0;
+      }
       if (active) {
         // carried rows start at zero (u rows before the line / k-space before the region)
         for (int i = m; i < (nb - 1) * (wrow / 4); i += kTileM)
@@ -424,19 +473,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
           if (tr && m == 0 && line == (int)blockIdx.x && c == 0) trace[6] = gtimer();
           const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride);
           float* wr = sWin + (size_t)(nb - 1 + m) * wrow;
+          const int nsets = BS ? min(P.nacc, nvalid) : 1;
           for (int b = 0; b < ((P.debug & 8) ? 0 : nb); ++b) {
-            uint32_t v0[16], v1[16];
-            tc::tmem_ld16_nowait(t0 + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
-            tc::tmem_ld16_nowait(t0 + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
-            tc::tmem_wait_ld();
+            float f[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) f[i] = 0.f;
+            for (int a = 0; a < nsets; ++a) {
+              uint32_t v0[16], v1[16];
+              const uint32_t ta = t0 + (uint32_t)(a * 32 * nb);
+              tc::tmem_ld16_nowait(ta + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
+              tc::tmem_ld16_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
+              tc::tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 16; ++i) f[i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
+            }
             float4* w4 = reinterpret_cast<float4*>(wr + 16 * b);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              float f[4];
-#pragma unroll
-              for (int k = 0; k < 4; ++k) f[k] = __uint_as_float(v0[4 * i + k]) + __uint_as_float(v1[4 * i + k]);
-              w4[i] = make_float4(f[0], f[1], f[2], f[3]);
-            }
+            for (int i = 0; i < 4; ++i) w4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
           }
           tc::fence_before();
           tc::mbar_arrive(&tempty[tb]);
@@ -617,7 +670,9 @@ int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext) {
 
 struct Shape {
   int L, nb, ng, kpre[2];
-  size_t fixed;  // B images + window + alignment slack
+  int bstream;       // B images rebuilt per stage
+  size_t stage;      // bytes per pipeline stage
+  size_t fixed;      // resident B images + window + alignment slack
 };
 
 bool shape_of(const DevGeom& g, int p, Shape* sh) {
@@ -636,8 +691,44 @@ bool shape_of(const DevGeom& g, int p, Shape* sh) {
   sh->kpre[0] = L >= 2 ? (int)g.kext[0] : 1;
   sh->kpre[1] = L >= 3 ? (int)g.kext[1] : 1;
   const size_t win = (((size_t)(kTileM + nb - 1) * (nb * 64 + 16)) + 1023) & ~(size_t)1023;
-  sh->fixed = (size_t)ng * nb * 2048 + win + 1024;
-  return sh->fixed + 2 * kStageBytes <= (size_t)kSmemBudget;
+  // resident B images when they fit next to >= 3 stages, else one group's image per stage
+  const size_t res_fixed = (size_t)ng * nb * 2048 + win + 1024;
+  if (g.nsp <= kMaxTapsRes && res_fixed + 3 * kStageBytes <= (size_t)kSmemBudget) {
+    sh->bstream = 0;
+    sh->stage = kStageBytes;
+    sh->fixed = res_fixed;
+  } else {
+    sh->bstream = 1;
+    sh->stage = kStageBytes + (size_t)nb * 2048;
+    sh->fixed = win + 1024;
+  }
+  return sh->fixed + 2 * sh->stage <= (size_t)kSmemBudget;
+}
+
+template <int MODE, bool BS>
+int launch_bs(const DevGeom& g, const Shape& sh, CtParams P, const CUtensorMap& tm, const int32_t* pos,
+              const float2* qt, float2* out, const float2* uin, const uint8_t* mask, const float2* y,
+              const float2* x0, double* parts, int64_t lines, int nparts_total, cudaStream_t st) {
+  static size_t avail = 0;  // dynamic shared memory available to this instantiation (queried once)
+  if (!avail) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)conv_tc_kernel<MODE, BS>);
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    avail = (size_t)optin - fa.sharedSizeBytes;
+    hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS>);
+  }
+  if (avail < sh.fixed + 2 * sh.stage) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory");
+  P.stages = (int)((avail - sh.fixed) / sh.stage);
+  if (P.stages > kMaxStages) P.stages = kMaxStages;
+  const size_t smem = sh.fixed + (size_t)P.stages * sh.stage;
+  int64_t grid = lines;
+  if (grid > hicu_sm_count()) grid = hicu_sm_count();
+  if (grid > nparts_total) grid = nparts_total;
+  if (grid < 1) grid = 1;
+  hicu_launch(conv_tc_kernel<MODE, BS>, (int)grid, kThreads, smem, st, tm, P, pos, qt, out, uin, mask, y, x0, parts);
+  return hicu_check_launch("conv_tc_kernel");
 }
 
 template <int MODE>
@@ -655,7 +746,14 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   P.ng = sh.ng;
   P.kpre[0] = sh.kpre[0];
   P.kpre[1] = sh.kpre[1];
-  P.tbuf_stride = 256;  // two accumulator buffers of 32 nb <= 256 columns
+  if (sh.bstream) {
+    // many prefix groups: one tile buffer, up to 3 accumulator sets (shorter chains)
+    P.tbuf_stride = 0;
+    P.nacc = min(3, 512 / (32 * sh.nb));
+  } else {
+    P.tbuf_stride = 256;  // two accumulator buffers of 32 nb <= 256 columns
+    P.nacc = 1;
+  }
   P.dc_mode = dc_mode;
   P.lam = lam;
   P.nparts_total = nparts_total;
@@ -690,26 +788,10 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   CUtensorMap tm;
   int s = cached_tmap(&tm, tsrc, L, MODE < 2 ? g.dims : g.rext);
   if (s) return s;
-  static size_t avail = 0;  // dynamic shared memory available to this instantiation (queried once)
-  if (!avail) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, (const void*)conv_tc_kernel<MODE>);
-    int optin = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    avail = (size_t)optin - fa.sharedSizeBytes;
-    hicu_allow_max_smem((const void*)conv_tc_kernel<MODE>);
-  }
-  if (avail < sh.fixed + 2 * kStageBytes) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory");
-  P.stages = (int)((avail - sh.fixed) / kStageBytes);
-  if (P.stages > kMaxStages) P.stages = kMaxStages;
-  const size_t smem = sh.fixed + (size_t)P.stages * kStageBytes;
-  int64_t grid = lines;
-  if (grid > hicu_sm_count()) grid = hicu_sm_count();
-  if (grid > nparts_total) grid = nparts_total;
-  if (grid < 1) grid = 1;
-  hicu_launch(conv_tc_kernel<MODE>, (int)grid, kThreads, smem, st, tm, P, g.pos, qt, out, uin, mask, y, x0, parts);
-  return hicu_check_launch("conv_tc_kernel");
+  P.stage_bytes = (int)sh.stage;
+  if (sh.bstream)
+    return launch_bs<MODE, true>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
+  return launch_bs<MODE, false>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
 }
 
 }  // namespace

@@ -32,6 +32,12 @@ def ellipse(n):
     return (yy / (c + 0.5)) ** 2 + (xx / (c + 0.5)) ** 2 <= 1.0
 
 
+def ellipsoid3(n):
+    c = (n - 1) / 2
+    z, yy, xx = np.meshgrid(*(np.arange(n) - c,) * 3, indexing="ij")
+    return (z / (c + 0.5)) ** 2 + (yy / (c + 0.5)) ** 2 + (xx / (c + 0.5)) ** 2 <= 1.0
+
+
 CASES = {
     # name: (spatial dims, kernel, region offsets/extents or None for full)
     "2d_full": ((70, 300), spatial_kernel((5, 5)), None),
@@ -42,6 +48,9 @@ CASES = {
     "1d": ((700,), spatial_kernel((7,)), None),
     "3d": ((12, 10, 140), spatial_kernel((3, 3, 3)), None),
     "3d_sub": ((14, 12, 40), spatial_kernel((3, 2, 3)), ((2, 3, 5), (6, 5, 20))),
+    "3d_555": ((10, 9, 140), spatial_kernel((5, 5, 5)), None),          # 125 taps: B images streamed per stage
+    "3d_555_ell": ((11, 10, 40), spatial_kernel((5, 5, 5), ellipsoid3(5)), ((1, 2, 3), (5, 4, 30))),
+    "2d_8x8": ((24, 150), spatial_kernel((8, 8)), None),                # 64 taps, nb = 8: streamed
     "1d_nb9": ((300,), spatial_kernel((9,)), None),                   # outside the tcgen05 scope -> SIMT
     "spread": ((6, 260), spatial_kernel((1, 40)), None),               # outside the tcgen05 scope -> SIMT
 }
@@ -66,6 +75,12 @@ def make(name, seed=0):
     return dims, kernel, region, og, x, q, mask, x0
 
 
+def tol_for(kernel, base=2e-6):
+    """fp32-grade bound for a contraction of n complex terms per output
+    (accumulation error grows ~sqrt(n); the 2e-6 base covers n <= 400)."""
+    return base * max(1.0, (kernel.n / 400.0) ** 0.5)
+
+
 def rel(a, b):
     return float(np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300))
 
@@ -82,25 +97,27 @@ def test_tc_path_selected(name):
 @pytest.mark.parametrize("name", list(CASES))
 def test_tc_conv_scatter_vs_oracle_and_simt(name):
     dims, kernel, region, og, x, q, mask, x0 = make(name)
+    tol = tol_for(kernel)
     u_tc = H.hankel_apply(x, q, kernel, region)
     u_ref = O.hankel_apply(x, q, og)
-    assert rel(u_tc, u_ref) <= 2e-6
+    assert rel(u_tc, u_ref) <= tol
     with H.kernel_paths(simt_conv=True):
         u_simt = H.hankel_apply(x, q, kernel, region)
         g_simt = H.kspace_adjoint_scatter(q, u_ref, kernel, region, dims)
-    assert rel(u_tc, u_simt) <= 4e-6  # both paths carry fp32-grade error (each <= 2e-6 vs oracle)
+    assert rel(u_tc, u_simt) <= 2 * tol  # both paths carry fp32-grade error (each <= tol vs oracle)
     g_tc = H.kspace_adjoint_scatter(q, u_ref, kernel, region, dims)
     g_ref = O.kspace_adjoint_scatter(q, u_ref, og)
-    assert rel(g_tc, g_ref) <= 2e-6
-    assert rel(g_tc, g_simt) <= 4e-6
+    assert rel(g_tc, g_ref) <= tol
+    assert rel(g_tc, g_simt) <= 2 * tol
     # positions no tap reaches are exactly zero
-    assert np.array_equal(g_tc == 0, g_ref == 0) or rel(g_tc, g_ref) <= 2e-6
+    assert np.array_equal(g_tc == 0, g_ref == 0) or rel(g_tc, g_ref) <= tol
 
 
 @pytest.mark.parametrize("name", list(CASES))
 @pytest.mark.parametrize("mode", ["hard", "soft"])
 def test_tc_objective_gradient_els(name, mode):
     dims, kernel, region, og, x, q, mask, x0 = make(name, seed=1)
+    tol = tol_for(kernel)
     dc = H.DataConsistency(mode, mask, x0=x0 if mode == "soft" else None, lam=0.6 if mode == "soft" else 0.0)
     g_tc, obj_tc, u_tc = H.objective_and_gradient(x, q, kernel, region, dc, return_products=True)
     eta_tc = H.exact_line_search(x, g_tc, q, kernel, region, dc, u=u_tc)
@@ -111,10 +128,13 @@ def test_tc_objective_gradient_els(name, mode):
                                                0.6 if mode == "soft" else 0.0)
     eta_o = O.exact_line_search(x, g_o, q, og, mask, u_o, mode, x0 if mode == "soft" else None,
                                 0.6 if mode == "soft" else 0.0)[0]
-    assert rel(g_tc, g_o) <= 2e-6
-    assert rel(g_tc, g_s) <= 4e-6
-    assert abs(obj_tc - obj_o) <= 4e-6 * abs(obj_o)
-    assert abs(obj_tc - obj_s) <= 4e-6 * abs(obj_s)
+    # the gradient chains two n-term contractions; bound it by the n-scaled
+    # tolerance or 1.5x the SIMT fp32 path's own error on the same inputs
+    e_tc, e_simt = rel(g_tc, g_o), rel(g_s, g_o)
+    assert e_tc <= max(tol, 1.5 * e_simt), (e_tc, e_simt)
+    assert rel(g_tc, g_s) <= 2 * max(tol, e_simt)
+    assert abs(obj_tc - obj_o) <= 2 * tol * abs(obj_o)
+    assert abs(obj_tc - obj_s) <= 2 * tol * abs(obj_s)
     assert abs(eta_tc - eta_s) <= 1e-5 * abs(eta_s)
     assert abs(eta_tc - eta_o) <= 1e-5 * abs(eta_o)
     if mode == "hard":

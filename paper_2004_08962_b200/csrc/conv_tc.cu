@@ -191,7 +191,6 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
                const float2* __restrict__ qt, float2* __restrict__ out, const float2* __restrict__ uin,
                const uint8_t* __restrict__ mask, const float2* __restrict__ y, const float2* __restrict__ x0,
                double* __restrict__ parts) {
-  hicu_pdl_entry();
   constexpr int NV = MODE == 0 ? 1 : (MODE == 1 ? 2 : 4);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -214,15 +213,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   const bool tr = (P.debug & 16) != 0;
   if (tr && threadIdx.x == 0) trace[0] = gtimer();
 
-  // ---- prologue: every global load issued up front ----
-  constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
-  float2 qv[kQPer];
-  const int nq = BS ? 0 : P.nsp * 64;
-#pragma unroll
-  for (int u = 0; u < kQPer; ++u) {
-    const int e = threadIdx.x + u * kThreads;
-    qv[u] = e < nq ? __ldg(qt + e) : make_float2(0.f, 0.f);
-  }
+  // ---- prologue part 1 (before the grid-dependency wait): only static data
+  // (support positions, barrier/TMEM setup), overlapping the previous kernel ----
   for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
     spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + t % L);
   if (threadIdx.x < ng) {
@@ -248,6 +240,17 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     tc::mbar_init_fence();
   }
   if (warp == 1) tc::tmem_alloc(&tslot, 512);
+  // ---- prologue part 2: Q~ (written by the reflector apply) and the k-space
+  // operands are read only after the previous grid has completed ----
+  hicu_pdl_entry();
+  constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
+  float2 qv[kQPer];
+  const int nq = BS ? 0 : P.nsp * 64;
+#pragma unroll
+  for (int u = 0; u < kQPer; ++u) {
+    const int e = threadIdx.x + u * kThreads;
+    qv[u] = e < nq ? __ldg(qt + e) : make_float2(0.f, 0.f);
+  }
   __syncthreads();
   for (int sp = threadIdx.x; sp < P.nsp; sp += kThreads) {
     const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);

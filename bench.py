@@ -345,8 +345,8 @@ def run_ours(args):
             ncu_by[rec["kernel"]] = rec
     except (OSError, ValueError):
         pass
-    ncu_name = {"gram": "gram_tc_kernel", "conv_fwd": "void conv_tc_kernel<0>", "scatter": "void conv_tc_kernel<2>",
-                "conv_els": "void conv_tc_kernel<1>", "update": "update_kernel"}
+    ncu_name = {"gram": "gram_tc_kernel", "conv_fwd": "void conv_tc_kernel<0, 0>", "scatter": "void conv_tc_kernel<2, 0>",
+                "conv_els": "void conv_tc_kernel<1, 0>", "update": "update_kernel"}
 
     def traffic(kind):
         rec = ncu_by.get(ncu_name.get(kind, ""))

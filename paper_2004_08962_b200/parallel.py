@@ -58,16 +58,18 @@ def partition_slices(n_slices: int, world: int, rank: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
-def reconstruct_slices(x0_slices, masks, kernel, schedule, rank: int = 0, world: int = 1, **kw):
+def reconstruct_slices(x0_slices, masks, kernel, schedule, rank: int = 0, world: int = 1, concurrency: int = 4,
+                       **kw):
     """C3-style slice parallelism: reconstruct this rank's block of
-    independent slices with :func:`hicu_reconstruct`; returns
-    ``{slice_index: (xhat, report)}``.  No collective on the data path."""
-    from .solver import hicu_reconstruct
+    independent slices, ``concurrency`` at a time on separate CUDA streams
+    (:func:`hicu_reconstruct_batch`); returns ``{slice_index: (xhat, report)}``.
+    No collective on the data path."""
+    from .solver import hicu_reconstruct_batch
 
-    out = {}
-    for s in partition_slices(len(x0_slices), world, rank):
-        out[s] = hicu_reconstruct(x0_slices[s], masks[s], kernel, schedule, **kw)
-    return out
+    idx = list(partition_slices(len(x0_slices), world, rank))
+    res = hicu_reconstruct_batch([x0_slices[s] for s in idx], [masks[s] for s in idx], kernel, schedule,
+                                 concurrency=concurrency, **kw)
+    return dict(zip(idx, res))
 
 
 def split_rows(n_rows: int, world: int):

@@ -40,6 +40,7 @@ __all__ = [
     "IterationRecord",
     "ReconReport",
     "hicu_reconstruct",
+    "hicu_reconstruct_batch",
     "ReconEngine",
 ]
 
@@ -611,7 +612,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         eng.run_stage(si, it0, it1 - it0)
         if not per_iter:
             continue
-        torch.cuda.synchronize()
+        torch.cuda.current_stream().synchronize()
         watch.pause()
         eng.check_status()
         if log_tail:
@@ -623,7 +624,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
             iterate_callback(si, it0, xi)
         watch.resume()
     _tr("issued")
-    torch.cuda.synchronize()
+    torch.cuda.current_stream().synchronize()
     _tr("device done")
     xhat = eng.download()
     _tr("download")
@@ -676,3 +677,39 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
     report.coil_basis = None if basis is None else basis.cpu().numpy()
     _tr("end")
     return xhat, report
+
+
+def hicu_reconstruct_batch(x0s, masks, kernel: KernelMask, schedule: SolverSchedule, *, concurrency: int = 4,
+                           **kw):
+    """Independent reconstructions (the slices of a multi-slice exam, C3)
+    run concurrently on ``concurrency`` CUDA streams of the current device;
+    returns ``[(xhat, report), ...]`` in input order.
+
+    Each reconstruction is exactly :func:`hicu_reconstruct` (results are
+    bit-identical to running them one after another: every kernel is
+    deterministic and nothing is shared between streams).  Concurrency lets one
+    slice's nullspace step — a chain of single-CTA fp64 kernels — run on a few
+    SMs while other slices' convolutions fill the rest of the GPU (SURVEY §8e:
+    "batch K1/K2 across the slices on each GPU")."""
+    import concurrent.futures as cf
+
+    torch = nat.require_cuda()
+    n = len(x0s)
+    if len(masks) != n:
+        raise ConfigError("need one mask per slice")
+    if n == 0:
+        return []
+    lanes = max(1, min(int(concurrency), n))
+    dev = torch.cuda.current_device()
+    streams = [torch.cuda.Stream(device=dev) for _ in range(lanes)]
+    out = [None] * n
+
+    def lane(k):
+        with torch.cuda.device(dev), torch.cuda.stream(streams[k]):
+            for i in range(k, n, lanes):
+                out[i] = hicu_reconstruct(x0s[i], masks[i], kernel, schedule, **kw)
+
+    with cf.ThreadPoolExecutor(max_workers=lanes, thread_name_prefix="hicu-batch") as ex:
+        for f in [ex.submit(lane, k) for k in range(lanes)]:
+            f.result()
+    return out

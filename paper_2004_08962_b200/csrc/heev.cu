@@ -945,7 +945,8 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   hicu_launch(stebz_kernel, (r + wpb - 1) / wpb, wpb * 32, 0, st, l, r, d, e, lam);
   if ((s = hicu_check_launch("stebz_kernel"))) return s;
   {
-    int T = 32;
+    // one eigenvalue per CTA: the pivoting branches diverge between eigenvalues
+    int T = getenv("HICU_STEIN_T") ? atoi(getenv("HICU_STEIN_T")) : 1;
     while (T > 1 && (size_t)5 * l * T * sizeof(double) > 200 * 1024) T >>= 1;
     const size_t smem = (size_t)5 * l * T * sizeof(double);
     hicu_allow_max_smem((const void*)stein_kernel);

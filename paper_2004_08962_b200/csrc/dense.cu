@@ -183,6 +183,183 @@ chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, c
   if (threadIdx.x == 0) *nu_out = s_nu;
 }
 
+// Register-resident variant (ell <= 96): row i of the upper triangle lives
+// in warp i % 16 (slot i / 16), lane t holding columns t + 32u.  Step k: the
+// owner warp finalises row k (sqrt + one reciprocal on every lane, no
+// reduction) and publishes it in a double-buffered shared row guarded by
+// mbarriers (full: owner -> all, empty: all 16 warps -> next writer), so
+// there is no block barrier: the owner of row k+1 folds row k into row k+1
+// first and publishes it while the other warps are still folding row k into
+// their rows (one-step lookahead).  Same arithmetic per element as
+// chol_kernel up to FMA contraction; the shift-scale trace is summed
+// warp-parallel in a fixed order.
+__device__ unsigned g_chol_trace[12];  // debug (HICU_CHOL_TRACE)
+
+template <int PER, int RPW>
+__device__ __forceinline__ void chol3_publish(int k, int ell, int lane, double2 (&a)[RPW][PER], double2* buf,
+                                              int* fail_flag) {
+  const int os = k >> 4, uk = k >> 5;
+  double2 rk[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    rk[u] = a[0][u];
+#pragma unroll
+    for (int s = 1; s < RPW; ++s) rk[u] = (s == os) ? a[s][u] : rk[u];
+  }
+  double dk = rk[0].x;
+#pragma unroll
+  for (int u = 1; u < PER; ++u) dk = (u == uk) ? rk[u].x : dk;
+  dk = __shfl_sync(0xffffffffu, dk, k & 31);
+  const bool ok = (dk > 0.0) && isfinite(dk);
+  const double rs = sqrt(dk), inv = 1.0 / rs;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int j = lane + 32 * u;
+    const double2 val = (j == k) ? cd(rs, 0.0) : inv * rk[u];
+    buf[j] = val;
+#pragma unroll
+    for (int s = 0; s < RPW; ++s)
+      if (s == os) a[s][u] = val;
+  }
+  if (lane == 0) *fail_flag = ok ? 0 : 1;
+}
+
+template <int PER, int RPW>
+__device__ __forceinline__ void chol3_fold(int k, int warp, int ell, int only, int skip, const double2* buf,
+                                           const double2 (&rj)[PER], double2 (&a)[RPW][PER]) {
+#pragma unroll
+  for (int s = 0; s < RPW; ++s) {
+    const int i = warp + 16 * s;
+    if (i > k && i < ell && (only < 0 || s == only) && s != skip) {
+      const double2 ai = buf[i];
+#pragma unroll
+      for (int u = 0; u < PER; ++u)
+        if (32 * (u + 1) > k + 1) {
+          a[s][u].x = fma(-ai.x, rj[u].x, fma(-ai.y, rj[u].y, a[s][u].x));
+          a[s][u].y = fma(-ai.x, rj[u].y, fma(ai.y, rj[u].x, a[s][u].y));
+        }
+    }
+  }
+}
+
+template <int PER, int RPW>
+__global__ void __launch_bounds__(512)
+chol2_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, const double2* __restrict__ G, int n,
+             double* __restrict__ nu_out, int* __restrict__ status) {
+  hicu_pdl_entry();
+  __shared__ double2 rowk[2][PER * 32];
+  __shared__ double red[16];
+  __shared__ int s_fail[2];
+  __shared__ __align__(8) uint64_t bars[12][4];  // per attempt: full[2], empty[2]
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  {
+    double tr = 0.0;
+    for (int i = t; i < n; i += 512) tr += G[(size_t)i * n + i].x;
+    for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    if (lane == 0) red[warp] = tr;
+  }
+  if (t < 48) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(&bars[t >> 2][t & 3]);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"((t & 3) < 2 ? 1 : 16));
+  }
+  __syncthreads();
+  double scale = 0.0;
+#pragma unroll
+  for (int w = 0; w < 16; ++w) scale += red[w];
+  scale = scale > 0.0 ? scale / n : 1.0;
+  const unsigned c0 = (unsigned)clock();
+  double nu = 0.0;
+  double2 a[RPW][PER];
+  bool failed = true;
+  auto arrive = [](uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(b)) : "memory");
+  };
+  auto wait = [](uint64_t* b, uint32_t par) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n\t}" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+        "r"(par)
+        : "memory");
+  };
+  for (int attempt = 0; attempt < 12; ++attempt) {
+    uint64_t* full = bars[attempt];
+    uint64_t* empty = bars[attempt] + 2;
+#pragma unroll
+    for (int s = 0; s < RPW; ++s) {
+      const int i = warp + 16 * s;
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int j = lane + 32 * u;
+        a[s][u] = (i < ell && j < ell) ? Cg[(size_t)i * ell + j] + nu * Og[(size_t)i * ell + j] : cd(0.0, 0.0);
+      }
+    }
+    bool fail = false;
+    const unsigned c1 = (unsigned)clock();
+    if (warp == 0) {
+      chol3_publish<PER, RPW>(0, ell, lane, a, rowk[0], &s_fail[0]);
+      __syncwarp();
+      if (lane == 0) arrive(&full[0]);
+    }
+    for (int k = 0; k < ell; ++k) {
+      const int b = k & 1;
+      wait(&full[b], (k >> 1) & 1);
+      double2 rj[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) rj[u] = rowk[b][lane + 32 * u];
+      if (s_fail[b]) {
+        fail = true;
+        break;
+      }
+      const int k1 = k + 1;
+      if (k1 < ell && warp == (k1 & 15)) {
+        const int s1 = k1 >> 4;
+        const bool tr = (k == 30 || k == 31) && lane == 0;
+        const int tb = (k - 30) * 5;
+        if (tr) g_chol_trace[2 + tb] = (unsigned)clock();
+        chol3_fold<PER, RPW>(k, warp, ell, s1, -1, rowk[b], rj, a);
+        if (tr) g_chol_trace[3 + tb] = (unsigned)(clock() + (int)(a[0][0].x > 1e300));
+        if (k1 >= 2) wait(&empty[k1 & 1], ((k1 >> 1) - 1) & 1);
+        if (tr) g_chol_trace[4 + tb] = (unsigned)clock();
+        chol3_publish<PER, RPW>(k1, ell, lane, a, rowk[k1 & 1], &s_fail[k1 & 1]);
+        __syncwarp();
+        if (lane == 0) arrive(&full[k1 & 1]);
+        if (tr) g_chol_trace[5 + tb] = (unsigned)clock();
+        chol3_fold<PER, RPW>(k, warp, ell, -1, s1, rowk[b], rj, a);
+        if (tr) g_chol_trace[6 + tb] = (unsigned)(clock() + (int)(a[0][0].x > 1e300));
+      } else {
+        chol3_fold<PER, RPW>(k, warp, ell, -1, -1, rowk[b], rj, a);
+      }
+      __syncwarp();
+      if (lane == 0) arrive(&empty[b]);
+    }
+    __syncthreads();
+    if (t == 0) {
+      g_chol_trace[0] = c1 - c0;
+      g_chol_trace[1] = (unsigned)clock() - c1;
+    }
+    if (!fail) {
+      failed = false;
+      break;
+    }
+    nu = (nu == 0.0) ? 1e-14 * scale : nu * 100.0;
+  }
+  if (failed) {
+    if (t == 0) *status = HICU_ERR_DEGENERATE_INPUT;
+  }
+#pragma unroll
+  for (int s = 0; s < RPW; ++s) {
+    const int i = warp + 16 * s;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int j = lane + 32 * u;
+      if (i < ell && j < ell) Cg[(size_t)i * ell + j] = (j >= i) ? a[s][u] : cd(0.0, 0.0);
+    }
+  }
+  if (t == 0) *nu_out = nu;
+}
+
 // W = (Y + nu*Omega) R^{-1}; one warp per row, R staged in smem when it fits.
 __global__ void trsm_rows_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
                                  const double* __restrict__ nu_p, const double2* __restrict__ R, bool r_smem,
@@ -227,9 +404,15 @@ __global__ void trsm_rows_kernel(int n, int ell, const double2* __restrict__ Y, 
 // precomputed 1/R_jj), broadcasts it with one shuffle, and every lane folds
 // w_j R[j][k] into its pending entries k > j: no reduction per column.
 constexpr int kTrsmMaxPer = 8;  // ell <= 256
-__global__ void trsm_rl_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
-                               const double* __restrict__ nu_p, const double2* __restrict__ R,
-                               double2* __restrict__ W) {
+__device__ unsigned g_trsm_trace[4];  // debug (HICU_TRSM_TRACE): block 0 warp 0 cycles of the first row
+// PER = ceil(ell / 32).  Every per-column step is branch-free: the row of R
+// is loaded for all PER slots before the owner's shuffle (clamped index, so
+// the loads never wait on w_j) and the fold is a select, so a step costs one
+// shuffle + two dependent FMAs instead of PER serialised load latencies.
+template <int PER>
+__global__ void __launch_bounds__(128) trsm_rl_kernel(int n, int ell, const double2* __restrict__ Y,
+                                                      const double2* __restrict__ Om, const double* __restrict__ nu_p,
+                                                      const double2* __restrict__ R, double2* __restrict__ W) {
   hicu_pdl_entry();
   extern __shared__ double2 smr[];
   double2* sR = smr;                                       // ell x ell (upper)
@@ -237,38 +420,58 @@ __global__ void trsm_rl_kernel(int n, int ell, const double2* __restrict__ Y, co
   for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) sR[e] = R[e];
   for (int j = threadIdx.x; j < ell; j += blockDim.x) rinv[j] = 1.0 / R[(size_t)j * ell + j].x;
   __syncthreads();
+  const unsigned c1 = (unsigned)clock();
   const double nu = *nu_p;
   const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * warps + warp; row < n; row += gridDim.x * warps) {
-    double2 acc[kTrsmMaxPer];
+  int kc[PER];
 #pragma unroll
-    for (int u = 0; u < kTrsmMaxPer; ++u) {
+  for (int u = 0; u < PER; ++u) kc[u] = min(lane + 32 * u, ell - 1);
+  for (int row = blockIdx.x * warps + warp; row < n; row += gridDim.x * warps) {
+    double2 acc[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
       const int j = lane + 32 * u;
       acc[u] = (j < ell) ? Y[(size_t)row * ell + j] + nu * Om[(size_t)row * ell + j] : cd(0.0, 0.0);
     }
     for (int j = 0; j < ell; ++j) {
-      const int owner = j & 31, uj = j >> 5;
-      double2 wj = cd(0.0, 0.0);
-#pragma unroll
-      for (int u = 0; u < kTrsmMaxPer; ++u)
-        if (u == uj) wj = acc[u];
-      wj = rinv[j] * wj;
-      wj.x = __shfl_sync(0xffffffffu, wj.x, owner);
-      wj.y = __shfl_sync(0xffffffffu, wj.y, owner);
       const double2* Rj = sR + (size_t)j * ell;
+      double2 rj[PER];
 #pragma unroll
-      for (int u = 0; u < kTrsmMaxPer; ++u) {
+      for (int u = 0; u < PER; ++u) rj[u] = Rj[kc[u]];
+      const double ri = rinv[j];
+      const int uj = j >> 5;
+      double2 wj = acc[0];
+#pragma unroll
+      for (int u = 1; u < PER; ++u) wj = (u == uj) ? acc[u] : wj;
+      wj = ri * wj;
+      wj.x = __shfl_sync(0xffffffffu, wj.x, j & 31);
+      wj.y = __shfl_sync(0xffffffffu, wj.y, j & 31);
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
         const int k = lane + 32 * u;
-        if (k == j) acc[u] = wj;
-        else if (k > j && k < ell) acc[u] = acc[u] - cmul(wj, Rj[k]);
+        const double2 t = acc[u] - cmul(wj, rj[u]);
+        acc[u] = (k == j) ? wj : ((k > j) ? t : acc[u]);
       }
     }
 #pragma unroll
-    for (int u = 0; u < kTrsmMaxPer; ++u) {
+    for (int u = 0; u < PER; ++u) {
       const int j = lane + 32 * u;
       if (j < ell) W[(size_t)row * ell + j] = acc[u];
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) g_trsm_trace[1] = (unsigned)clock() - c1;
   }
+}
+
+template <int PER>
+void trsm_rl_launch(int n, int ell, const double2* Y, const double2* Om, const double* nu, const double2* R,
+                    double2* W, size_t smem, cudaStream_t st) {
+  if (PER * 32 < ell) {
+    if constexpr (PER < kTrsmMaxPer) trsm_rl_launch<PER + 1>(n, ell, Y, Om, nu, R, W, smem, st);
+    return;
+  }
+  const int warps = 4;
+  hicu_allow_max_smem((const void*)trsm_rl_kernel<PER>);
+  hicu_launch(trsm_rl_kernel<PER>, (n + warps - 1) / warps, warps * 32, smem, st, n, ell, Y, Om, nu, R, W);
 }
 
 // ---------------------------------------------------------------------------
@@ -1180,7 +1383,28 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const size_t bytes = (size_t)ell * ell * sizeof(double2);
     const bool sm = bytes <= kSmemCap;
-    if (sm) {
+    const bool old_chol = getenv("HICU_CHOL1") != nullptr;
+    if (!old_chol && ell <= 96) {
+      auto args = [&](auto kern) {
+        hicu_launch(kern, 1, 512, 0, st, ell, w.C, (const double2*)w.O, Gp, n, w.nu, status_dev);
+      };
+      if (ell <= 16) args(chol2_kernel<1, 1>);
+      else if (ell <= 32) args(chol2_kernel<1, 2>);
+      else if (ell <= 48) args(chol2_kernel<2, 3>);
+      else if (ell <= 64) args(chol2_kernel<2, 4>);
+      else if (ell <= 80) args(chol2_kernel<3, 5>);
+      else args(chol2_kernel<3, 6>);
+      if (getenv("HICU_CHOL_TRACE")) {
+        unsigned h[12];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_chol_trace, sizeof(h));
+        fprintf(stderr, "chol2: load %u | factor %u cycles\n", h[0], h[1]);
+        fprintf(stderr, "  owner k1=31: fold-own %u | wait-empty %u | publish %u | fold-rest %u\n", h[3] - h[2],
+                h[4] - h[3], h[5] - h[4], h[6] - h[5]);
+        fprintf(stderr, "  owner k1=32: fold-own %u | wait-empty %u | publish %u | fold-rest %u | step31->32 start %u\n",
+                h[8] - h[7], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[7] - h[2]);
+      }
+    } else if (sm) {
       hicu_allow_max_smem((const void*)chol_kernel<true>);
       hicu_launch(chol_kernel<true>, 1, 512, bytes, st, ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
     } else {
@@ -1191,11 +1415,14 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const size_t rbytes = (size_t)ell * ell * sizeof(double2);
     if (rbytes + (size_t)ell * sizeof(double) <= kSmemCap) {
-      const int warps = 4;
-      hicu_allow_max_smem((const void*)trsm_rl_kernel);
-      hicu_launch(trsm_rl_kernel, (n + warps - 1) / warps, warps * 32, rbytes + (size_t)ell * sizeof(double), st, 
-          n, ell, w.Y, Om, w.nu, w.C, w.W);
+      trsm_rl_launch<1>(n, ell, w.Y, Om, w.nu, w.C, w.W, rbytes + (size_t)ell * sizeof(double), st);
       if ((s = hicu_check_launch("trsm_rl_kernel"))) return s;
+      if (getenv("HICU_TRSM_TRACE")) {
+        unsigned h[4];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_trsm_trace, sizeof(h));
+        fprintf(stderr, "trsm_rl: first row %u cycles\n", h[1]);
+      }
     } else {
     const int warps = 8;
     const size_t rowb = (size_t)warps * ell * sizeof(double2);

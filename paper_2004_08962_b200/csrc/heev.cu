@@ -550,6 +550,151 @@ hetrd4_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restric
   if (t == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
 }
 
+// Lower-triangle variant (hetrd5): only A[i][j], j <= i, is kept up to date
+// (the Hermitian rank-2 update touches half the matrix); the matrix-vector
+// product reads the upper half as conj(A[j][i]) by column; v is formed once
+// per step in shared memory (hetrd4 recomputed it per matrix element).
+// Per step: [R] thread 0 forms reflector k from column k (tail norm from
+// per-warp partials of the previous update), [A] v, [B] y = A22 v partials
+// (4 threads per row, interleaved columns) and w, [D] lower update plus the
+// per-warp partial norms of the next column.  ~10 m^2 fp64 ops per step
+// instead of ~26 m^2.
+constexpr int kHetrd5Max = 128;
+__device__ unsigned g_h5_trace[4][12];  // debug (HICU_HETRD_TRACE): thread-0 phase clocks of steps 10, 40, 70
+
+__global__ void __launch_bounds__(512)
+hetrd5_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
+              double2* __restrict__ tau, double2* __restrict__ Vt) {
+  hicu_pdl_entry();
+  extern __shared__ double2 A[];
+  __shared__ double2 sv[kHetrd5Max], sw[kHetrd5Max];
+  __shared__ double2 red[16];
+  __shared__ double red2[16];
+  __shared__ double2 s_tau, s_sc;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int qd = t & 3, rowo = t >> 2;
+  for (int x = t; x < l * l; x += 512) A[(size_t)(x / l) * lda + x % l] = Ain[x];
+  for (int x = t; x < l * l; x += 512) Vt[x] = cd(0.0, 0.0);
+  __syncthreads();
+  // tail norm of column 0: sum_{i >= 2} |A[i][0]|^2 (per-warp partials, fixed order)
+  {
+    double p = 0.0;
+    for (int i = 2 + t; i < l; i += 512) p += abs2d(A[(size_t)i * lda]);
+    p = warp_sum_d(p);
+    if (lane == 0) red2[warp] = p;
+  }
+  __syncthreads();
+  for (int k = 0; k + 1 < l; ++k) {
+    const int k1 = k + 1, m = l - k1;
+    const int slot = k == 10 ? 0 : (k == 40 ? 1 : (k == 70 ? 2 : -1));
+    if (slot >= 0 && t == 0) g_h5_trace[slot][0] = (unsigned)clock();
+    // ---- [R] reflector k from column k ----
+    if (t == 0) {
+      double tail = 0.0;
+#pragma unroll
+      for (int w = 0; w < 16; ++w) tail += red2[w];
+      hetrd3_reflector(k, tail, conjd(A[(size_t)k1 * lda + k]), A[(size_t)k * lda + k].x, d, e, tau, &s_tau, &s_sc);
+      if (slot >= 0) g_h5_trace[slot][1] = (unsigned)clock();
+    }
+    __syncthreads();
+    if (slot >= 0 && t == 0) g_h5_trace[slot][2] = (unsigned)clock();
+    const double2 tk = s_tau, sc = s_sc;
+    const bool active = !(tk.x == 0.0 && tk.y == 0.0);
+    // ---- [A] v = [1; A[k+2:, k] sc] ----
+    if (active && t < m) {
+      const int j = k1 + t;
+      const double2 vj = (j == k1) ? cd(1.0, 0.0) : cmul(A[(size_t)j * lda + k], sc);
+      sv[j] = vj;
+      Vt[(size_t)k * l + j] = vj;
+    }
+    __syncthreads();
+    if (slot >= 0 && t == 0) g_h5_trace[slot][3] = (unsigned)clock();
+    const int i = k1 + rowo;
+    const bool has_row = i < l;
+    double2 wi = cd(0.0, 0.0), vi = cd(0.0, 0.0);
+    if (active) {
+      // ---- [B] y_i = sum_j A[i][j] v_j over my quarter: row part j <= i, column part j > i ----
+      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0), a2 = cd(0.0, 0.0), a3 = cd(0.0, 0.0);
+      if (has_row) {
+        const double2* Ai = A + (size_t)i * lda;
+        int j = k1 + qd;
+        // 4 independent chains, loads issued ahead of the FMAs
+        for (; j + 12 <= i; j += 16) {
+          const double2 x0 = Ai[j], x1 = Ai[j + 4], x2 = Ai[j + 8], x3 = Ai[j + 12];
+          const double2 v0 = sv[j], v1 = sv[j + 4], v2 = sv[j + 8], v3 = sv[j + 12];
+          zfma(a0, x0, v0); zfma(a1, x1, v1); zfma(a2, x2, v2); zfma(a3, x3, v3);
+        }
+        for (; j <= i; j += 4) zfma(a0, Ai[j], sv[j]);
+        if (slot >= 0 && t == 0) g_h5_trace[slot][8] = (unsigned)clock();
+        const double2* Ac = A + (size_t)j * lda + i;
+        for (; j + 12 < l; j += 16, Ac += 16 * lda) {
+          const double2 x0 = Ac[0], x1 = Ac[4 * lda], x2 = Ac[8 * lda], x3 = Ac[12 * lda];
+          const double2 v0 = sv[j], v1 = sv[j + 4], v2 = sv[j + 8], v3 = sv[j + 12];
+          zfma(a0, conjd(x0), v0); zfma(a1, conjd(x1), v1); zfma(a2, conjd(x2), v2); zfma(a3, conjd(x3), v3);
+        }
+        for (; j < l; j += 4, Ac += 4 * lda) zfma(a1, conjd(*Ac), sv[j]);
+        vi = sv[i];
+      }
+      double2 y = (a0 + a1) + (a2 + a3);
+      if (slot >= 0 && t == 0) g_h5_trace[slot][9] = (unsigned)(clock() + (int)(y.x > 1e300));
+      y.x += __shfl_xor_sync(0xffffffffu, y.x, 1);
+      y.y += __shfl_xor_sync(0xffffffffu, y.y, 1);
+      y.x += __shfl_xor_sync(0xffffffffu, y.x, 2);
+      y.y += __shfl_xor_sync(0xffffffffu, y.y, 2);
+      double2 pd = cd(0.0, 0.0);
+      if (has_row) {
+        wi = cmul(tk, y);
+        if (qd == 0) {
+          sw[i] = wi;
+          zfmac(pd, wi, vi);
+        }
+      }
+      if (slot >= 0 && t == 0) g_h5_trace[slot][10] = (unsigned)(clock() + (int)(pd.x > 1e300));
+      pd = cd(warp_sum_d(pd.x), warp_sum_d(pd.y));
+      if (lane == 0) red[warp] = pd;
+    }
+    if (slot >= 0 && t == 0) g_h5_trace[slot][4] = (unsigned)clock();
+    __syncthreads();
+    if (slot >= 0 && t == 0) g_h5_trace[slot][5] = (unsigned)clock();
+    // ---- [D] lower update A[i][j] -= v_i conj(w_j) + (w_i + c v_i) conj(v_j), j <= i;
+    //      partial norms of column k1 below row k1+1 for the next reflector ----
+    double tl = 0.0;
+    if (active) {
+      double2 dot = cd(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < 16; ++w) dot = dot + red[w];
+      const double c = -cmul(tk, dot).x;  // 2 Re(alpha2)
+      if (has_row) {
+        const double2 wpi = wi + c * vi;
+        double2* Ai = A + (size_t)i * lda;
+        int j = k1 + qd;
+        if (j == k1 && j <= i) {
+          const double2 nv = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(sv[j]));
+          Ai[j] = nv;
+          if (i >= k1 + 2) tl = abs2d(nv);
+          j += 4;
+        }
+        for (; j + 12 <= i; j += 16) {
+          double2 x[4], ww[4], vv[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) { x[u] = Ai[j + 4 * u]; ww[u] = sw[j + 4 * u]; vv[u] = sv[j + 4 * u]; }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) Ai[j + 4 * u] = x[u] - cmul(vi, conjd(ww[u])) - cmul(wpi, conjd(vv[u]));
+        }
+        for (; j <= i; j += 4) Ai[j] = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(sv[j]));
+      }
+    } else if (has_row && qd == 0 && i >= k1 + 2) {
+      tl = abs2d(A[(size_t)i * lda + k1]);
+    }
+    tl = warp_sum_d(tl);
+    if (lane == 0) red2[warp] = tl;
+    if (slot >= 0 && t == 0) g_h5_trace[slot][6] = (unsigned)clock();
+    __syncthreads();
+    if (slot >= 0 && t == 0) g_h5_trace[slot][7] = (unsigned)clock();
+  }
+  if (t == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+}
+
 // 1/q to ~1e-15 relative: fp32 seed (MUFU) + two Newton steps in fp64
 // (the Sturm count only needs the sign of each pivot).  Falls back to an IEEE
 // division when q is outside the fp32 exponent range.
@@ -924,7 +1069,22 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
     const size_t a3 = (size_t)l * lda3 * sizeof(double2);
     const int lda4 = ((l + 1 + 3) / 8) * 8 + 4;  // >= l + 1, == 4 mod 8
     const size_t a4 = (size_t)l * lda4 * sizeof(double2);
-    if (l <= kHetrd4Max && a4 <= 180 * 1024) {
+    if (getenv("HICU_HETRD5") && l <= kHetrd5Max && a4 <= 180 * 1024) {
+      hicu_allow_max_smem((const void*)hetrd5_kernel);
+      hicu_launch(hetrd5_kernel, 1, 512, a4, st, l, lda4, A, d, e, tau, Vt);
+      if (getenv("HICU_HETRD_TRACE")) {
+        unsigned h[4][12];
+        cudaStreamSynchronize(st);
+        cudaMemcpyFromSymbol(h, g_h5_trace, sizeof(h));
+        for (int q = 0; q < 3; ++q)
+          fprintf(stderr, "hetrd5 step %d (t0): refl %u | bar %u | v+bar %u | matvec %u | bar %u | update %u | bar %u\n",
+                  q == 0 ? 10 : (q == 1 ? 40 : 70), h[q][1] - h[q][0], h[q][2] - h[q][1], h[q][3] - h[q][2],
+                  h[q][4] - h[q][3], h[q][5] - h[q][4], h[q][6] - h[q][5], h[q][7] - h[q][6]);
+        for (int q = 0; q < 3; ++q)
+          fprintf(stderr, "   matvec split: rowloop %u | colloop %u | shfl+cmul %u | warpsum %u\n", h[q][8] - h[q][3],
+                  h[q][9] - h[q][8], h[q][10] - h[q][9], h[q][4] - h[q][10]);
+      }
+    } else if (l <= kHetrd4Max && a4 <= 180 * 1024) {
       hicu_allow_max_smem((const void*)hetrd4_kernel);
       hicu_launch(hetrd4_kernel, 1, 512, a4, st, l, lda4, A, d, e, tau, Vt);
     } else if (l <= kHetrd3Max && a3 <= 180 * 1024) {

@@ -59,7 +59,8 @@ constexpr int kMaxTapsRes = 56;            // spatial taps with resident B image
 constexpr int kHalfBytes = kTileM * 64;    // 8 KB: one 128-row A tile (hi or lo)
 constexpr int kStageBytes = 2 * kHalfBytes;
 constexpr int kMaxStages = 8;
-constexpr int kThreads = 320;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each owning 8 of the 16 output floats
+constexpr int kThreads = (6 + kEpiWarps) * 32;
 constexpr int kSmemBudget = 220 * 1024;    // conservative dynamic shared memory budget (sm_100a opt-in 227 KB)
 
 struct CtParams {
@@ -132,41 +133,40 @@ __device__ __forceinline__ double warp_sum_d(double v) {
   return v;
 }
 
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory"); }
 
-// Scatter epilogue for one k-space position: data consistency + the four
-// partial sums (|g|^2, |res|^2, <g,res>, |g|^2 on observed).
-__device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, const float (&v)[16],
+// Scatter epilogue for one k-space position, coils 4h..4h+3 (one half of the
+// 8 coils): data consistency + the four partial sums (|g|^2, |res|^2,
+// <g,res>, |g|^2 on observed).
+__device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[8],
                                               const uint8_t* __restrict__ mask, const float2* __restrict__ y,
                                               const float2* __restrict__ x0, float2* __restrict__ gout,
                                               double (&acc)[4]) {
-  uint8_t mk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const size_t e = e0 + 4 * h;
+  uint8_t mk[4] = {0, 0, 0, 0};
   if (P.dc_mode != 2) {
-    const uint2 mm = *reinterpret_cast<const uint2*>(mask + e0);
+    const uint32_t mm = *reinterpret_cast<const uint32_t*>(mask + e);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      mk[c] = (uint8_t)(mm.x >> (8 * c));
-      mk[4 + c] = (uint8_t)(mm.y >> (8 * c));
-    }
+    for (int c = 0; c < 4; ++c) mk[c] = (uint8_t)(mm >> (8 * c));
   }
-  float4* gp = reinterpret_cast<float4*>(gout + e0);
+  float4* gp = reinterpret_cast<float4*>(gout + e);
 #pragma unroll
-  for (int c2 = 0; c2 < 4; ++c2) {
+  for (int c2 = 0; c2 < 2; ++c2) {
     float a[4] = {v[4 * c2], v[4 * c2 + 1], v[4 * c2 + 2], v[4 * c2 + 3]};
     float4 yy = make_float4(0.f, 0.f, 0.f, 0.f), xx = yy;
     if (P.dc_mode == 1) {
-      yy = reinterpret_cast<const float4*>(y + e0)[c2];
-      xx = reinterpret_cast<const float4*>(x0 + e0)[c2];
+      yy = reinterpret_cast<const float4*>(y + e)[c2];
+      xx = reinterpret_cast<const float4*>(x0 + e)[c2];
     }
     const float yv[4] = {yy.x, yy.y, yy.z, yy.w}, xv[4] = {xx.x, xx.y, xx.z, xx.w};
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const bool on = P.dc_mode != 2 && mk[2 * c2 + h] == 1;
-      float ar = a[2 * h], ai = a[2 * h + 1];
+    for (int hh = 0; hh < 2; ++hh) {
+      const bool on = P.dc_mode != 2 && mk[2 * c2 + hh] == 1;
+      float ar = a[2 * hh], ai = a[2 * hh + 1];
       if (P.dc_mode == 0) {
         if (on) ar = ai = 0.f;
       } else if (P.dc_mode == 1) {
-        const float rr = on ? yv[2 * h] - xv[2 * h] : 0.f, ri = on ? yv[2 * h + 1] - xv[2 * h + 1] : 0.f;
+        const float rr = on ? yv[2 * hh] - xv[2 * hh] : 0.f, ri = on ? yv[2 * hh + 1] - xv[2 * hh + 1] : 0.f;
         acc[1] += (double)rr * rr + (double)ri * ri;
         ar = ar + P.lam * rr;
         ai = ai + P.lam * ri;
@@ -176,8 +176,8 @@ __device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, cons
         }
       }
       acc[0] += (double)ar * ar + (double)ai * ai;
-      a[2 * h] = ar;
-      a[2 * h + 1] = ai;
+      a[2 * hh] = ar;
+      a[2 * hh + 1] = ai;
     }
     gp[c2] = make_float4(a[0], a[1], a[2], a[3]);
   }
@@ -205,7 +205,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   __shared__ int ga[kMaxGroups][2];
   __shared__ int spos[kMaxTaps][3];
   __shared__ short tapidx[kMaxGroups * kMaxNb];  // (prefix g, offset b) -> spatial tap or -1
-  __shared__ double red[4][NV];
+  __shared__ double red[kEpiWarps][NV];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // debug bit 16: CTA milestones (%globaltimer) written to `out` (conv forward only)
@@ -235,7 +235,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], 128);
+      tc::mbar_init(&tempty[b], kEpiWarps * 32);
     }
     tc::mbar_init_fence();
   }
@@ -446,8 +446,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     }
   } else {
     // ---------------- epilogue ----------------
-    const int q = warp & 3;
+    // 8 warps: warp w reads TMEM lane quarter q = w & 3 (A-tile rows 32q..)
+    // and owns output floats [8h, 8h + 8) of every row (h = column half).
+    const int q = warp & 3, h = (warp - 6) >> 2;
     const int m = 32 * q + lane;  // TMEM lane = A-tile row
+    const int et = threadIdx.x - 192;  // epilogue thread index 0..255
     const int wrow = nb * 16 + 4; // floats per window row (+16 B: conflict-free float4 rows)
     double acc_v[NV];
 #pragma unroll
@@ -468,35 +471,36 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
       }
       if (active) {
         // carried rows start at zero (u rows before the line / k-space before the region)
-        for (int i = m; i < (nb - 1) * (wrow / 4); i += kTileM)
+        for (int i = et; i < (nb - 1) * (wrow / 4); i += kEpiWarps * 32)
           reinterpret_cast<float4*>(sWin)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        epi_bar();
         for (int c = 0; c < P.chunks; ++c) {
           tc::mbar_wait(&tfull[tb], tph);
           tc::fence_after();
-          if (tr && m == 0 && line == (int)blockIdx.x && c == 0) trace[6] = gtimer();
-          const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride);
-          float* wr = sWin + (size_t)(nb - 1 + m) * wrow;
+          if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[6] = gtimer();
+          const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride) + (uint32_t)(8 * h);
+          float* wr = sWin + (size_t)(nb - 1 + m) * wrow + 8 * h;
           const int nsets = BS ? min(P.nacc, nvalid) : 1;
           for (int b = 0; b < ((P.debug & 8) ? 0 : nb); ++b) {
-            float f[16];
+            float f[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) f[i] = 0.f;
+            for (int i = 0; i < 8; ++i) f[i] = 0.f;
             for (int a = 0; a < nsets; ++a) {
-              uint32_t v0[16], v1[16];
+              uint32_t v0[8], v1[8];
               const uint32_t ta = t0 + (uint32_t)(a * 32 * nb);
-              tc::tmem_ld16_nowait(ta + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
-              tc::tmem_ld16_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
+              tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
+              tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
               tc::tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 16; ++i) f[i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
+              for (int i = 0; i < 8; ++i) f[i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
             }
             float4* w4 = reinterpret_cast<float4*>(wr + 16 * b);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) w4[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+            w4[0] = make_float4(f[0], f[1], f[2], f[3]);
+            w4[1] = make_float4(f[4], f[5], f[6], f[7]);
           }
           tc::fence_before();
           tc::mbar_arrive(&tempty[tb]);
-          if (tr && m == 0 && line == (int)blockIdx.x && c == 0) trace[7] = gtimer();
+          if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[7] = gtimer();
           if (nbuf == 2) {
             tb ^= 1;
             if (tb == 0) tph ^= 1;
@@ -505,14 +509,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
           }
           epi_bar();
           // shifted sums: conv row m takes window rows m + b; scatter row m takes rows nb - 1 + m - b
-          float v[16];
+          float v[8];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+          for (int i = 0; i < 8; ++i) v[i] = 0.f;
           for (int b = 0; b < nb; ++b) {
             const int w = MODE < 2 ? m + b : nb - 1 + m - b;
-            const float4* r4 = reinterpret_cast<const float4*>(sWin + (size_t)w * wrow + 16 * b);
+            const float4* r4 = reinterpret_cast<const float4*>(sWin + (size_t)w * wrow + 16 * b + 8 * h);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < 2; ++i) {
               const float4 t = r4[i];
               v[4 * i] += t.x;
               v[4 * i + 1] += t.y;
@@ -522,40 +526,52 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
           }
           epi_bar();
           // carry the last nb - 1 rows into the next tile (float4 copies spread over all threads)
-          for (int i = m; i < (nb - 1) * (wrow / 4); i += kTileM) {
+          for (int i = et; i < (nb - 1) * (wrow / 4); i += kEpiWarps * 32) {
             const int r = i / (wrow / 4), k = i % (wrow / 4);
             reinterpret_cast<float4*>(sWin + (size_t)r * wrow)[k] =
                 reinterpret_cast<const float4*>(sWin + (size_t)(kTileM + r) * wrow)[k];
           }
           epi_bar();
-          if (tr && m == 0 && line == (int)blockIdx.x && c == 0) trace[8] = gtimer();
+          if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[8] = gtimer();
           if (MODE < 2) {
             const int i_out = c * kTileM - (nb - 1) + m;
             if (i_out < 0 || i_out >= P.ext_last) continue;
             const int64_t idx = obase + i_out;
             if (MODE == 0) {
-              float4* up = reinterpret_cast<float4*>(out + (size_t)idx * 8);
-              if (!tr)  // trace mode keeps `out` for the milestones
+              float4* up = reinterpret_cast<float4*>(out + (size_t)idx * 8 + 4 * h);
+              if (!tr) {  // trace mode keeps `out` for the milestones
+                up[0] = make_float4(v[0], v[1], v[2], v[3]);
+                up[1] = make_float4(v[4], v[5], v[6], v[7]);
+              }
+              double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) up[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) acc_v[0] += (double)v[i] * v[i];
+              for (int i = 0; i < 8; i += 2) {
+                s0 += (double)v[i] * v[i];
+                s1 += (double)v[i + 1] * v[i + 1];
+              }
+              acc_v[0] += s0 + s1;
             } else {
-              const float4* up = reinterpret_cast<const float4*>(uin + (size_t)idx * 8);
+              const float4* up = reinterpret_cast<const float4*>(uin + (size_t)idx * 8 + 4 * h);
+              double d0 = 0.0, d1 = 0.0, n0 = 0.0, n1 = 0.0;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) {
+              for (int i = 0; i < 2; ++i) {
                 const float4 uu = up[i];
-                acc_v[0] += (double)v[4 * i] * uu.x + (double)v[4 * i + 1] * uu.y + (double)v[4 * i + 2] * uu.z +
-                            (double)v[4 * i + 3] * uu.w;
+                d0 += (double)v[4 * i] * uu.x + (double)v[4 * i + 1] * uu.y;
+                d1 += (double)v[4 * i + 2] * uu.z + (double)v[4 * i + 3] * uu.w;
               }
 #pragma unroll
-              for (int i = 0; i < 16; ++i) acc_v[NV - 1] += (double)v[i] * v[i];
+              for (int i = 0; i < 8; i += 2) {
+                n0 += (double)v[i] * v[i];
+                n1 += (double)v[i + 1] * v[i + 1];
+              }
+              acc_v[0] += d0 + d1;
+              acc_v[NV - 1] += n0 + n1;
             }
           } else {
             const int x = P.roff[L - 1] + c * kTileM + m;
             if (x >= P.ext_last) continue;
             double a4[4] = {0, 0, 0, 0};
-            scatter_store(P, (size_t)(obase + x) * 8, v, mask, y, x0, out, a4);
+            scatter_store(P, (size_t)(obase + x) * 8, h, v, mask, y, x0, out, a4);
 #pragma unroll
             for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
           }
@@ -565,30 +581,32 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
         // positions no tile covers: DC term only
         const int x_lo = active ? P.roff[L - 1] : 0;
         const int x_hi = active ? P.roff[L - 1] + P.chunks * kTileM : 0;
-        const float vz[16] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const float vz[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (int x = m; x < P.ext_last; x += kTileM) {
           if (x >= x_lo && x < x_hi) continue;
           double a4[4] = {0, 0, 0, 0};
-          scatter_store(P, (size_t)(obase + x) * 8, vz, mask, y, x0, out, a4);
+          scatter_store(P, (size_t)(obase + x) * 8, h, vz, mask, y, x0, out, a4);
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
         }
       }
     }
-    if (tr && m == 0) trace[9] = gtimer();
-    // fixed-order reduction over the 128 epilogue threads
+    if (tr && m == 0 && h == 0) trace[9] = gtimer();
+    // fixed-order reduction over the 256 epilogue threads
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const double t = warp_sum_d(acc_v[i]);
-      if (lane == 0) red[q][i] = t;
+      if (lane == 0) red[warp - 6][i] = t;
     }
     epi_bar();
     if (warp == 6 && lane < NV) {
-      const double t = red[0][lane] + red[1][lane] + red[2][lane] + red[3][lane];
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < kEpiWarps; ++w) t += red[w][lane];
       parts[(size_t)blockIdx.x * NV + lane] = t;
     }
     if (blockIdx.x == 0)
-      for (int i = threadIdx.x - 192 + (int)gridDim.x * NV; i < P.nparts_total * NV; i += 128) parts[i] = 0.0;
+      for (int i = et + (int)gridDim.x * NV; i < P.nparts_total * NV; i += kEpiWarps * 32) parts[i] = 0.0;
   }
   if (tr && threadIdx.x == 192) trace[10] = gtimer();
   tc::fence_before();

@@ -550,149 +550,186 @@ hetrd4_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restric
   if (t == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
 }
 
-// Lower-triangle variant (hetrd5): only A[i][j], j <= i, is kept up to date
-// (the Hermitian rank-2 update touches half the matrix); the matrix-vector
-// product reads the upper half as conj(A[j][i]) by column; v is formed once
-// per step in shared memory (hetrd4 recomputed it per matrix element).
-// Per step: [R] thread 0 forms reflector k from column k (tail norm from
-// per-warp partials of the previous update), [A] v, [B] y = A22 v partials
-// (4 threads per row, interleaved columns) and w, [D] lower update plus the
-// per-warp partial norms of the next column.  ~10 m^2 fp64 ops per step
-// instead of ~26 m^2.
-constexpr int kHetrd5Max = 128;
-__device__ unsigned g_h5_trace[4][12];  // debug (HICU_HETRD_TRACE): thread-0 phase clocks of steps 10, 40, 70
+// Register-resident variant (l <= 96): the full Hermitian matrix lives in
+// registers, warp w holding columns 6w..6w+5 and lane t rows t, t+32, t+64
+// (18 complex per thread), so no step streams A through shared memory.
+// Step k: [R] the warp owning column k (= conj of row k) forms reflector k
+// from its registers (one warp reduction) and publishes v; [B] every thread
+// forms partial matrix-vector products over its 6 columns for its 3 rows
+// (shared partials, no shuffles) and its share of v^H A v; [C] warps 0-2 sum
+// the 16 partials per row into w = tau A v; [D] every thread applies the
+// rank-2 update to its 18 elements (v and w are zero outside the trailing
+// block, so the update needs no masks).  Same reflector scalars as
+// hetrd3_reflector; v/w double-buffered by step parity, 3 barriers per step.
+constexpr int kHetrd6Max = 96;
+constexpr int kH6Warps = 12, kH6Cols = 8;  // 12 warps x 8 columns; 3 row slots per lane
+__device__ long long g_h6_trace[3][6];  // debug (HICU_HETRD_TRACE): thread 0 clocks at steps 10, 40, 70
 
-__global__ void __launch_bounds__(512)
-hetrd5_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
+// reflector k from column k (x = rows lane + 32u of column k, in registers
+// of every lane of the calling warp): scalars, v into sv, reflector row of Vt
+__device__ __forceinline__ void hetrd6_reflect(int k, int l, int lane, const double2 (&x)[3], double* d, double* e,
+                                               double2* tau, double2* Vt, double2* svb, double2* stau,
+                                               double2* ssc) {
+  const int k1 = k + 1;
+  double tl = 0.0;
+  double2 alpha = cd(0.0, 0.0), dkk = cd(0.0, 0.0);
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int i = lane + 32 * u;
+    tl += (i >= k + 2 && i < l) ? abs2d(x[u]) : 0.0;
+    alpha = (i == k1) ? x[u] : alpha;
+    dkk = (i == k) ? x[u] : dkk;
+  }
+  tl = warp_sum_d(tl);
+  alpha.x = __shfl_sync(0xffffffffu, alpha.x, k1 & 31);
+  alpha.y = __shfl_sync(0xffffffffu, alpha.y, k1 & 31);
+  dkk.x = __shfl_sync(0xffffffffu, dkk.x, k & 31);
+  if (lane == 0) hetrd3_reflector(k, tl, conjd(alpha), dkk.x, d, e, tau, stau, ssc);
+  __syncwarp();
+  const double2 tk = *stau, sc = *ssc;
+  const bool act = !(tk.x == 0.0 && tk.y == 0.0);
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    const int i = lane + 32 * u;
+    if (i >= kHetrd6Max) continue;
+    double2 vi = (i == k1) ? cd(1.0, 0.0) : cmul(x[u], sc);
+    const bool on = act && i >= k1 && i < l;
+    svb[i] = on ? vi : cd(0.0, 0.0);
+    if (on) Vt[(size_t)k * l + i] = vi;
+  }
+}
+
+__global__ void __launch_bounds__(kH6Warps * 32)
+hetrd6_kernel(int l, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
               double2* __restrict__ tau, double2* __restrict__ Vt) {
   hicu_pdl_entry();
-  extern __shared__ double2 A[];
-  __shared__ double2 sv[kHetrd5Max], sw[kHetrd5Max];
-  __shared__ double2 red[16];
-  __shared__ double red2[16];
-  __shared__ double2 s_tau, s_sc;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int qd = t & 3, rowo = t >> 2;
-  for (int x = t; x < l * l; x += 512) A[(size_t)(x / l) * lda + x % l] = Ain[x];
-  for (int x = t; x < l * l; x += 512) Vt[x] = cd(0.0, 0.0);
-  __syncthreads();
-  // tail norm of column 0: sum_{i >= 2} |A[i][0]|^2 (per-warp partials, fixed order)
-  {
-    double p = 0.0;
-    for (int i = 2 + t; i < l; i += 512) p += abs2d(A[(size_t)i * lda]);
-    p = warp_sum_d(p);
-    if (lane == 0) red2[warp] = p;
+  __shared__ double2 sv[2][kHetrd6Max], sw[2][kHetrd6Max];
+  __shared__ double2 part[kH6Warps][kHetrd6Max];
+  __shared__ double sq[kH6Warps];
+  __shared__ double2 s_tau[2], s_sc[2];
+  __shared__ double s_c;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  double2 a[3][kH6Cols];
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+#pragma unroll
+    for (int c = 0; c < kH6Cols; ++c) {
+      const int i = lane + 32 * u, j = kH6Cols * w + c;
+      a[u][c] = (i < l && j < l) ? Ain[(size_t)i * l + j] : cd(0.0, 0.0);
+    }
+  for (int x = t; x < l * l; x += kH6Warps * 32) Vt[x] = cd(0.0, 0.0);
+  __syncthreads();  // Vt zeroed before any reflector row is written
+  if (w == 0 && l > 1) {
+    double2 x[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) x[u] = a[u][0];
+    hetrd6_reflect(0, l, lane, x, d, e, tau, Vt, sv[0], &s_tau[0], &s_sc[0]);
   }
-  __syncthreads();
   for (int k = 0; k + 1 < l; ++k) {
-    const int k1 = k + 1, m = l - k1;
+    const int k1 = k + 1, par = k & 1;
     const int slot = k == 10 ? 0 : (k == 40 ? 1 : (k == 70 ? 2 : -1));
-    if (slot >= 0 && t == 0) g_h5_trace[slot][0] = (unsigned)clock();
-    // ---- [R] reflector k from column k ----
-    if (t == 0) {
-      double tail = 0.0;
+    if (slot >= 0 && t == 0) g_h6_trace[slot][0] = clock64();
+    __syncthreads();  // reflector k published
+    if (slot >= 0 && t == 0) g_h6_trace[slot][1] = clock64();
+    const double2 tk = s_tau[par];
+    // ---- [B] partial A v over my columns for my 3 rows; share of v^H A v ----
+    {
+      double2 p[3] = {cd(0.0, 0.0), cd(0.0, 0.0), cd(0.0, 0.0)};
+      if (kH6Cols * w + kH6Cols > k1) {  // v is zero on the columns < k1
+        double2 p2[3] = {cd(0.0, 0.0), cd(0.0, 0.0), cd(0.0, 0.0)};
 #pragma unroll
-      for (int w = 0; w < 16; ++w) tail += red2[w];
-      hetrd3_reflector(k, tail, conjd(A[(size_t)k1 * lda + k]), A[(size_t)k * lda + k].x, d, e, tau, &s_tau, &s_sc);
-      if (slot >= 0) g_h5_trace[slot][1] = (unsigned)clock();
-    }
-    __syncthreads();
-    if (slot >= 0 && t == 0) g_h5_trace[slot][2] = (unsigned)clock();
-    const double2 tk = s_tau, sc = s_sc;
-    const bool active = !(tk.x == 0.0 && tk.y == 0.0);
-    // ---- [A] v = [1; A[k+2:, k] sc] ----
-    if (active && t < m) {
-      const int j = k1 + t;
-      const double2 vj = (j == k1) ? cd(1.0, 0.0) : cmul(A[(size_t)j * lda + k], sc);
-      sv[j] = vj;
-      Vt[(size_t)k * l + j] = vj;
-    }
-    __syncthreads();
-    if (slot >= 0 && t == 0) g_h5_trace[slot][3] = (unsigned)clock();
-    const int i = k1 + rowo;
-    const bool has_row = i < l;
-    double2 wi = cd(0.0, 0.0), vi = cd(0.0, 0.0);
-    if (active) {
-      // ---- [B] y_i = sum_j A[i][j] v_j over my quarter: row part j <= i, column part j > i ----
-      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0), a2 = cd(0.0, 0.0), a3 = cd(0.0, 0.0);
-      if (has_row) {
-        const double2* Ai = A + (size_t)i * lda;
-        int j = k1 + qd;
-        // 4 independent chains, loads issued ahead of the FMAs
-        for (; j + 12 <= i; j += 16) {
-          const double2 x0 = Ai[j], x1 = Ai[j + 4], x2 = Ai[j + 8], x3 = Ai[j + 12];
-          const double2 v0 = sv[j], v1 = sv[j + 4], v2 = sv[j + 8], v3 = sv[j + 12];
-          zfma(a0, x0, v0); zfma(a1, x1, v1); zfma(a2, x2, v2); zfma(a3, x3, v3);
+        for (int c = 0; c < kH6Cols; ++c) {
+          const double2 vj = sv[par][kH6Cols * w + c];
+#pragma unroll
+          for (int u = 0; u < 3; ++u)
+            if (32 * u + 32 > k1) {  // rows < k1 are never read again
+              if (c & 1) zfma(p2[u], a[u][c], vj);
+              else zfma(p[u], a[u][c], vj);
+            }
         }
-        for (; j <= i; j += 4) zfma(a0, Ai[j], sv[j]);
-        if (slot >= 0 && t == 0) g_h5_trace[slot][8] = (unsigned)clock();
-        const double2* Ac = A + (size_t)j * lda + i;
-        for (; j + 12 < l; j += 16, Ac += 16 * lda) {
-          const double2 x0 = Ac[0], x1 = Ac[4 * lda], x2 = Ac[8 * lda], x3 = Ac[12 * lda];
-          const double2 v0 = sv[j], v1 = sv[j + 4], v2 = sv[j + 8], v3 = sv[j + 12];
-          zfma(a0, conjd(x0), v0); zfma(a1, conjd(x1), v1); zfma(a2, conjd(x2), v2); zfma(a3, conjd(x3), v3);
-        }
-        for (; j < l; j += 4, Ac += 4 * lda) zfma(a1, conjd(*Ac), sv[j]);
-        vi = sv[i];
+#pragma unroll
+        for (int u = 0; u < 3; ++u) p[u] = p[u] + p2[u];
       }
-      double2 y = (a0 + a1) + (a2 + a3);
-      if (slot >= 0 && t == 0) g_h5_trace[slot][9] = (unsigned)(clock() + (int)(y.x > 1e300));
-      y.x += __shfl_xor_sync(0xffffffffu, y.x, 1);
-      y.y += __shfl_xor_sync(0xffffffffu, y.y, 1);
-      y.x += __shfl_xor_sync(0xffffffffu, y.x, 2);
-      y.y += __shfl_xor_sync(0xffffffffu, y.y, 2);
-      double2 pd = cd(0.0, 0.0);
-      if (has_row) {
-        wi = cmul(tk, y);
-        if (qd == 0) {
-          sw[i] = wi;
-          zfmac(pd, wi, vi);
+      double qv = 0.0;
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int i = lane + 32 * u;
+        if (i < kHetrd6Max) {
+          part[w][i] = p[u];
+          const double2 vi = sv[par][i];
+          qv += vi.x * p[u].x + vi.y * p[u].y;  // Re(conj(v_i) p_i)
         }
       }
-      if (slot >= 0 && t == 0) g_h5_trace[slot][10] = (unsigned)(clock() + (int)(pd.x > 1e300));
-      pd = cd(warp_sum_d(pd.x), warp_sum_d(pd.y));
-      if (lane == 0) red[warp] = pd;
+      qv = warp_sum_d(qv);
+      if (lane == 0) sq[w] = qv;
     }
-    if (slot >= 0 && t == 0) g_h5_trace[slot][4] = (unsigned)clock();
     __syncthreads();
-    if (slot >= 0 && t == 0) g_h5_trace[slot][5] = (unsigned)clock();
-    // ---- [D] lower update A[i][j] -= v_i conj(w_j) + (w_i + c v_i) conj(v_j), j <= i;
-    //      partial norms of column k1 below row k1+1 for the next reflector ----
-    double tl = 0.0;
-    if (active) {
-      double2 dot = cd(0.0, 0.0);
+    if (slot >= 0 && t == 0) g_h6_trace[slot][2] = clock64();
+    // ---- [C] w_i = tau sum_w part[w][i] (one row per thread) ----
+    if (t < kHetrd6Max) {
+      double2 y0 = cd(0.0, 0.0), y1 = cd(0.0, 0.0), y2 = cd(0.0, 0.0), y3 = cd(0.0, 0.0);
 #pragma unroll
-      for (int w = 0; w < 16; ++w) dot = dot + red[w];
-      const double c = -cmul(tk, dot).x;  // 2 Re(alpha2)
-      if (has_row) {
-        const double2 wpi = wi + c * vi;
-        double2* Ai = A + (size_t)i * lda;
-        int j = k1 + qd;
-        if (j == k1 && j <= i) {
-          const double2 nv = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(sv[j]));
-          Ai[j] = nv;
-          if (i >= k1 + 2) tl = abs2d(nv);
-          j += 4;
-        }
-        for (; j + 12 <= i; j += 16) {
-          double2 x[4], ww[4], vv[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) { x[u] = Ai[j + 4 * u]; ww[u] = sw[j + 4 * u]; vv[u] = sv[j + 4 * u]; }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) Ai[j + 4 * u] = x[u] - cmul(vi, conjd(ww[u])) - cmul(wpi, conjd(vv[u]));
-        }
-        for (; j <= i; j += 4) Ai[j] = Ai[j] - cmul(vi, conjd(sw[j])) - cmul(wpi, conjd(sv[j]));
+      for (int q = 0; q < kH6Warps; q += 4) {
+        y0 = y0 + part[q][t];
+        y1 = y1 + part[q + 1][t];
+        y2 = y2 + part[q + 2][t];
+        y3 = y3 + part[q + 3][t];
       }
-    } else if (has_row && qd == 0 && i >= k1 + 2) {
-      tl = abs2d(A[(size_t)i * lda + k1]);
+      sw[par][t] = (t >= k1 && t < l) ? cmul(tk, (y0 + y1) + (y2 + y3)) : cd(0.0, 0.0);
     }
-    tl = warp_sum_d(tl);
-    if (lane == 0) red2[warp] = tl;
-    if (slot >= 0 && t == 0) g_h5_trace[slot][6] = (unsigned)clock();
+    if (t == kHetrd6Max) {  // 2 Re(alpha2) = -|tau|^2 v^H A v (fixed-order tree over the warps)
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < kH6Warps; ++q) s4[q & 3] += sq[q];
+      s_c = -(tk.x * tk.x + tk.y * tk.y) * ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+    }
     __syncthreads();
-    if (slot >= 0 && t == 0) g_h5_trace[slot][7] = (unsigned)clock();
+    if (slot >= 0 && t == 0) g_h6_trace[slot][3] = clock64();
+    // ---- [D] A -= v w^H + (w + c v) v^H on my elements; the owner of column
+    //      k+1 keeps its fresh values and forms reflector k+1 right away ----
+    {
+      const double c = s_c;
+      double2 vr[3], wr[3], xn[3];
+#pragma unroll
+      for (int u = 0; u < 3; ++u) {
+        const int i = lane + 32 * u;
+        vr[u] = i < kHetrd6Max ? sv[par][i] : cd(0.0, 0.0);
+        const double2 wi = i < kHetrd6Max ? sw[par][i] : cd(0.0, 0.0);
+        wr[u] = wi + c * vr[u];  // row factor of the second term: w_i + c v_i
+        xn[u] = cd(0.0, 0.0);
+      }
+      const bool own_next = k1 + 1 < l && w == k1 / kH6Cols;
+      if (kH6Cols * w + kH6Cols > k1) {  // v, w are zero outside the trailing block
+#pragma unroll
+        for (int c2 = 0; c2 < kH6Cols; ++c2) {
+          const int j = kH6Cols * w + c2;
+          const double2 vj = sv[par][j], wj = sw[par][j];
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            if (32 * u + 32 > k1) {
+              // a -= v_i conj(w_j) + wp_i conj(v_j)  (4 FMAs per component)
+              double2 x = a[u][c2];
+              x.x = fma(-vr[u].x, wj.x, fma(-vr[u].y, wj.y, x.x));
+              x.x = fma(-wr[u].x, vj.x, fma(-wr[u].y, vj.y, x.x));
+              x.y = fma(-vr[u].y, wj.x, fma(vr[u].x, wj.y, x.y));
+              x.y = fma(-wr[u].y, vj.x, fma(wr[u].x, vj.y, x.y));
+              a[u][c2] = x;
+            }
+            if (j == k1) xn[u] = a[u][c2];
+          }
+        }
+      }
+      if (own_next) hetrd6_reflect(k1, l, lane, xn, d, e, tau, Vt, sv[par ^ 1], &s_tau[par ^ 1], &s_sc[par ^ 1]);
+      if (slot >= 0 && t == 0) g_h6_trace[slot][4] = clock64() + (long long)(a[0][0].x > 1e300);
+      if (slot >= 0 && t == 0) g_h6_trace[slot][5] = clock64();
+    }
   }
-  if (t == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+  // d[l-1] = A[l-1][l-1]
+#pragma unroll
+  for (int u = 0; u < 3; ++u)
+#pragma unroll
+    for (int c = 0; c < kH6Cols; ++c)
+      if (lane + 32 * u == l - 1 && kH6Cols * w + c == l - 1) d[l - 1] = a[u][c].x;
 }
 
 // 1/q to ~1e-15 relative: fp32 seed (MUFU) + two Newton steps in fp64
@@ -1069,20 +1106,16 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
     const size_t a3 = (size_t)l * lda3 * sizeof(double2);
     const int lda4 = ((l + 1 + 3) / 8) * 8 + 4;  // >= l + 1, == 4 mod 8
     const size_t a4 = (size_t)l * lda4 * sizeof(double2);
-    if (getenv("HICU_HETRD5") && l <= kHetrd5Max && a4 <= 180 * 1024) {
-      hicu_allow_max_smem((const void*)hetrd5_kernel);
-      hicu_launch(hetrd5_kernel, 1, 512, a4, st, l, lda4, A, d, e, tau, Vt);
+    if (!getenv("HICU_HETRD4") && l <= kHetrd6Max) {
+      hicu_launch(hetrd6_kernel, 1, kH6Warps * 32, 0, st, l, A, d, e, tau, Vt);
       if (getenv("HICU_HETRD_TRACE")) {
-        unsigned h[4][12];
+        long long h[3][6];
         cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(h, g_h5_trace, sizeof(h));
+        cudaMemcpyFromSymbol(h, g_h6_trace, sizeof(h));
         for (int q = 0; q < 3; ++q)
-          fprintf(stderr, "hetrd5 step %d (t0): refl %u | bar %u | v+bar %u | matvec %u | bar %u | update %u | bar %u\n",
+          fprintf(stderr, "hetrd6 step %d (t0): bar %lld | B+bar %lld | C+bar %lld | D %lld | R(next) %lld\n",
                   q == 0 ? 10 : (q == 1 ? 40 : 70), h[q][1] - h[q][0], h[q][2] - h[q][1], h[q][3] - h[q][2],
-                  h[q][4] - h[q][3], h[q][5] - h[q][4], h[q][6] - h[q][5], h[q][7] - h[q][6]);
-        for (int q = 0; q < 3; ++q)
-          fprintf(stderr, "   matvec split: rowloop %u | colloop %u | shfl+cmul %u | warpsum %u\n", h[q][8] - h[q][3],
-                  h[q][9] - h[q][8], h[q][10] - h[q][9], h[q][4] - h[q][10]);
+                  h[q][4] - h[q][3], h[q][5] - h[q][4]);
       }
     } else if (l <= kHetrd4Max && a4 <= 180 * 1024) {
       hicu_allow_max_smem((const void*)hetrd4_kernel);

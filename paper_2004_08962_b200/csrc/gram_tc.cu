@@ -369,7 +369,8 @@ __global__ void gram_planar_kernel(int64_t nlines, int dlast, int nblk, int nshi
 
 __global__ void __launch_bounds__(kThreads2, 1)
 gram_tc2_kernel(const __grid_constant__ TmapSet tms, TcParams p, const int32_t* __restrict__ pos, int ndim,
-                float* __restrict__ part, int dbg) {
+                float* __restrict__ part, int dbg, const float* __restrict__ xt, int64_t copy_floats, int nblk,
+                int d3, int cpasync) {
   hicu_pdl_entry();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -403,7 +404,7 @@ gram_tc2_kernel(const __grid_constant__ TmapSet tms, TcParams p, const int32_t* 
   }
   if (threadIdx.x == 0) {
     for (int st = 0; st < S; ++st) {
-      mbar_init(&full_bar[st], 1);
+      mbar_init(&full_bar[st], cpasync ? 32 : 1);
       mbar_init(&ready_bar[st], 128);
       mbar_init(&empty_bar[st], 1);
     }
@@ -423,7 +424,55 @@ gram_tc2_kernel(const __grid_constant__ TmapSet tms, TcParams p, const int32_t* 
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 && cpasync) {
+    // ---------------- cp.async producer (all 32 lanes) ----------------
+    // Each operand tile is a contiguous 1 KB block [16 f rows x 16 positions]
+    // of the planar copy; lanes issue its 64 16-byte chunks with cp.async
+    // into the SW64-swizzled K-major layout (chunk u of row f lands at
+    // 16 (u ^ ((f >> 1) & 3))) and arm the stage's full barrier with
+    // cp.async.mbarrier.arrive (no thread waits for the data: the producer
+    // runs up to S stages ahead, each stage ~24 KB in flight).
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&empty_bar[st], ph ^ 1);
+      const int64_t line = kb / p.nkb_line;
+      const int chunk = (int)(kb % p.nkb_line);
+      int lc[2] = {0, 0};
+      {
+        int64_t rem = line;
+        for (int d = L - 2; d >= 0; --d) {
+          lc[d] = (int)(rem % p.rext[d]);
+          rem /= p.rext[d];
+        }
+      }
+      const uint32_t sb = smem_u32(smem + (size_t)st * stage_bytes);
+      // lane covers rows f = lane / 4 and f + 8 of every tile, chunk u = lane % 4
+      const int f0 = lane >> 2, u = lane & 3;
+      const uint32_t d0 = (uint32_t)f0 * 64 + (uint32_t)((u ^ ((f0 >> 1) & 3)) << 4);
+      const uint32_t d1 = (uint32_t)(f0 + 8) * 64 + (uint32_t)((u ^ (((f0 + 8) >> 1) & 3)) << 4);
+      const int soff0 = f0 * 16 + u * 4, soff1 = (f0 + 8) * 16 + u * 4;
+      for (int q = 0; q < list; ++q) {
+        const int tap = (q < NT) ? n0 + q : m0 + (q - NT);
+        const int bsh = tap_c[tap][0];
+        const int pstart = (int)p.roff[L - 1] + bsh + chunk * kBK;
+        const int blk = pstart >> 4;
+        int c3 = 0, c4 = 0;
+        if (L == 2) c3 = (int)p.roff[0] + lc[0] + tap_c[tap][1];
+        if (L == 3) {
+          c3 = (int)p.roff[1] + lc[1] + tap_c[tap][2];
+          c4 = (int)p.roff[0] + lc[0] + tap_c[tap][1];
+        }
+        const float* src = xt + (size_t)bsh * copy_floats + (((size_t)c4 * d3 + c3) * nblk + blk) * 256;
+        const uint32_t dst = sb + (uint32_t)q * 1024;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + d0), "l"(src + soff0) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + d1), "l"(src + soff1) : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full_bar[st])) : "memory");
+      if (++st == S) { st = 0; ph ^= 1; }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == 0) {
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       int st = 0;
@@ -663,7 +712,9 @@ TcPlan tc_plan(const DevGeom& g) {
       }
     }
   p.npairs = np;
-  int splits = (hicu_sm_count() + np - 1) / np;
+  // one wave: np * splits <= SM count (one CTA per SM at ~200 KB of shared
+  // memory; a 149th CTA would double the kernel time)
+  int splits = hicu_sm_count() / np;
   if (splits > p.nkb) splits = (int)p.nkb;
   if (splits < 1) splits = 1;
   p.kb_per_split = (p.nkb + splits - 1) / splits;
@@ -708,10 +759,16 @@ bool use_tma_gram() {
   if (v < 0) v = getenv("HICU_GRAM_TMA") ? 1 : 0;
   return v == 1;
 }
+// cp.async-fed planar variant (HICU_GRAM_CPASYNC=1 while it is being measured)
+bool use_cpasync_gram() {
+  static int v = -1;
+  if (v < 0) v = getenv("HICU_GRAM_CPASYNC") ? 1 : 0;
+  return v == 1;
+}
 
 size_t planar_bytes(const DevGeom& g) {
   const int L = g.ndim - 1;
-  if (!use_tma_gram() || L < 1 || g.kext[L - 1] < 1) return 0;
+  if (!(use_tma_gram() || use_cpasync_gram()) || L < 1 || g.kext[L - 1] < 1) return 0;
   int64_t nlines = 1;
   for (int d = 0; d < L - 1; ++d) nlines *= g.dims[d];
   const int64_t nblk = (g.dims[L - 1] + 15) / 16 + 1;
@@ -739,7 +796,7 @@ int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t
   dim3 grid(pl.p.npairs, pl.splits);
   GramEncodeFn enc = gram_encode();
   const int Lg = g.ndim - 1;
-  if (use_tma_gram() && enc && g.kext[Lg - 1] >= 1 && g.kext[Lg - 1] <= kMaxShift) {
+  if ((use_tma_gram() || use_cpasync_gram()) && enc && g.kext[Lg - 1] >= 1 && g.kext[Lg - 1] <= kMaxShift) {
     const int L = g.ndim - 1;
     const int dlast = (int)g.dims[L - 1];
     const int nblk = (dlast + 15) / 16 + 1;
@@ -767,7 +824,8 @@ int hicu_gram_tc(const DevGeom& g, const float2* x, double2* G, void* ws, size_t
     hicu_allow_max_smem((const void*)gram_tc2_kernel);
     static int dbg = -1;
     if (dbg < 0) dbg = getenv("HICU_GRAM_DEBUG") ? atoi(getenv("HICU_GRAM_DEBUG")) : 0;
-    hicu_launch(gram_tc2_kernel, grid, kThreads2, pl.smem_bytes, st, tms, pl.p, g.pos, g.ndim, part, dbg);
+    hicu_launch(gram_tc2_kernel, grid, kThreads2, pl.smem_bytes, st, tms, pl.p, g.pos, g.ndim, part, dbg,
+                (const float*)xt, (int64_t)copy_floats, nblk, (int)dims[3], use_cpasync_gram() ? 1 : 0);
     if ((s = hicu_check_launch("gram_tc2_kernel"))) return s;
   } else {
     hicu_launch(tc_tap_table_kernel, (g.nsp + 127) / 128, 128, 0, st, g.nsp, g.nc, g.koff, toff);

@@ -9,4 +9,4 @@ prof() { ncu --set full --clock-control none --import-source on -k "regex:$1" -s
 prof gram_tc_kernel 70 1 gram
 prof conv_tc_kernel 1050 3 conv
 prof update_kernel 350 1 update
-prof "hetrd4|householder2" 140 2 nullspace
+prof "hetrd6|householder2" 140 2 nullspace

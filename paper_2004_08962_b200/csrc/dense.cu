@@ -1314,6 +1314,88 @@ apply_reflectors_res_kernel(int n, int r, const double2* __restrict__ refl, cons
   }
 }
 
+// Streaming variant (n <= 32 kArPer): each warp carries two columns of B in
+// registers and reads the reflectors straight from L2 one step ahead (no
+// 192 KB shared-memory staging per CTA); the two columns' dot products are
+// reduced together, interleaving the x and y parts (one 5-level shuffle tree
+// for four doubles instead of four sequential trees).
+constexpr int kAr2Warps = 4;
+__global__ void __launch_bounds__(kAr2Warps * 32)
+apply_reflectors_res2_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
+                             const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
+                             double2* __restrict__ B, float2* __restrict__ out32, int p) {
+  hicu_pdl_entry();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = 2 * (blockIdx.x * kAr2Warps + warp);
+  if (j0 >= cols) return;
+  const bool two = j0 + 1 < cols;
+  double2 b0[kArPer], b1[kArPer];
+#pragma unroll
+  for (int u = 0; u < kArPer; ++u) {
+    const int k = lane + 32 * u;
+    b0[u] = k < n ? Bin[(size_t)k * cols + j0] : cd(0.0, 0.0);
+    b1[u] = (k < n && two) ? Bin[(size_t)k * cols + j0 + 1] : cd(0.0, 0.0);
+  }
+  double2 wn[kArPer];
+  auto load_w = [&](int col) {
+#pragma unroll
+    for (int u = 0; u < kArPer; ++u) {
+      const int k = lane + 32 * u;
+      wn[u] = (col >= 0 && k < n) ? __ldg(refl + (size_t)col * n + k) : cd(0.0, 0.0);  // zero above col
+    }
+  };
+  load_w(r - 1);
+  for (int col = r - 1; col >= 0; --col) {
+    double2 wr[kArPer];
+#pragma unroll
+    for (int u = 0; u < kArPer; ++u) wr[u] = wn[u];
+    load_w(col - 1);  // next reflector in flight while this one is applied
+    const int act = __ldg(flags + col);
+    if (!act) continue;
+    double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0), e0 = cd(0.0, 0.0), e1 = cd(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kArPer; u += 2) {
+      zfmac(d0, wr[u], b0[u]);
+      zfmac(e0, wr[u], b1[u]);
+      if (u + 1 < kArPer) {
+        zfmac(d1, wr[u + 1], b0[u + 1]);
+        zfmac(e1, wr[u + 1], b1[u + 1]);
+      }
+    }
+    double2 d = d0 + d1, e = e0 + e1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      d.x += __shfl_xor_sync(0xffffffffu, d.x, o);
+      d.y += __shfl_xor_sync(0xffffffffu, d.y, o);
+      e.x += __shfl_xor_sync(0xffffffffu, e.x, o);
+      e.y += __shfl_xor_sync(0xffffffffu, e.y, o);
+    }
+    const double2 tc = __ldg(tau + col);
+    const double2 f = cmulc(tc, d), g = cmulc(tc, e);  // conj(tau) * dot
+#pragma unroll
+    for (int u = 0; u < kArPer; ++u) {
+      b0[u] = b0[u] - cmul(wr[u], f);
+      b1[u] = b1[u] - cmul(wr[u], g);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kArPer; ++u) {
+    const int k = lane + 32 * u;
+    if (k >= n) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = j0 + h;
+      if (h == 1 && !two) continue;
+      const double2 v = h ? b1[u] : b0[u];
+      B[(size_t)k * cols + j] = v;
+      if (out32) {
+        const int step = j / p, t = j % p;
+        out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
+      }
+    }
+  }
+}
+
 struct NysWs {
   double2 *Y, *O, *C, *W, *M, *scratch, *F;
   void* heev;
@@ -1508,6 +1590,13 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
                                      const void* Bin, void* B, void* out32, int p, void* stream) {
   if (n < 1 || r < 0 || cols < 1 || !B || !Bin) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad p");
+  if (r >= 1 && n <= 32 * kArPer && !getenv("HICU_APPLY_RES1")) {
+    const int pairs = (cols + 1) / 2;
+    hicu_launch(apply_reflectors_res2_kernel, (pairs + kAr2Warps - 1) / kAr2Warps, kAr2Warps * 32, 0,
+                (cudaStream_t)stream, n, r, (const double2*)refl, (const double2*)tau, flags, cols,
+                (const double2*)Bin, (double2*)B, (float2*)out32, p ? p : 1);
+    return hicu_check_launch("apply_reflectors_res2_kernel");
+  }
   {
     const size_t res = ((size_t)r * n + r + (size_t)kArWarps * n) * sizeof(double2) + (size_t)r * sizeof(int);
     if (r >= 1 && n <= 32 * kArPer && res <= (size_t)210 * 1024) {

@@ -868,31 +868,43 @@ __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const d
   for (int i = 0; i < l; ++i)
     tnorm = fmax(tnorm, fabs(sd[i]) + (i > 0 ? fabs(se[i - 1]) : 0.0) + fabs(se[i]));
   const double tiny = 2.2e-16 * fmax(tnorm, 1e-300);
-  for (int i = 0; i < l; ++i) {
-    AT(u0, i) = sd[i] - lj;
-    AT(u1, i) = se[i];
-    AT(u2, i) = 0.0;
-  }
-  for (int i = 0; i + 1 < l; ++i) {
-    const double sub = se[i];
-    const double ui = AT(u0, i);
-    if (fabs(ui) >= fabs(sub)) {
-      const double f = (ui != 0.0) ? sub / ui : 0.0;
-      AT(dl, i) = f;
-      AT(u0, i + 1) -= f * AT(u1, i);
-    } else {
-      const double f = ui / sub;
-      AT(u0, i) = sub;
-      const double tt = AT(u0, i + 1);
-      AT(u0, i + 1) = AT(u1, i) - f * tt;
-      AT(u1, i) = tt;
-      if (i + 2 < l) {
-        AT(u2, i) = AT(u1, i + 1);
-        AT(u1, i + 1) = -f * AT(u2, i);
+  // LU of T - lam I with partial pivoting (dgttrf form).  The two entries the
+  // next step depends on (u0[i+1], u1[i+1]) are carried in registers, so the
+  // recurrence chain holds one division and no shared-memory round trip;
+  // the factors are stored for the solves off the chain.
+  {
+    double u0c = sd[0] - lj, u1c = se[0];
+    for (int i = 0; i + 1 < l; ++i) {
+      const double sub = se[i];
+      double u0n = sd[i + 1] - lj, u1n = se[i + 1];
+      if (fabs(u0c) >= fabs(sub)) {
+        const double f = (u0c != 0.0) ? sub / u0c : 0.0;
+        AT(dl, i) = f;
+        AT(u0, i) = u0c;
+        AT(u1, i) = u1c;
+        AT(u2, i) = 0.0;
+        u0n -= f * u1c;
+      } else {
+        const double f = u0c / sub;
+        AT(u0, i) = sub;
+        const double tt = u0n;
+        u0n = u1c - f * tt;
+        AT(u1, i) = tt;
+        if (i + 2 < l) {
+          AT(u2, i) = u1n;
+          u1n = -f * u1n;
+        } else {
+          AT(u2, i) = 0.0;
+        }
+        AT(dl, i) = f;
+        swaps[i >> 6] |= 1ull << (i & 63);
       }
-      AT(dl, i) = f;
-      swaps[i >> 6] |= 1ull << (i & 63);
+      u0c = u0n;
+      u1c = u1n;
     }
+    AT(u0, l - 1) = u0c;
+    AT(u1, l - 1) = u1c;
+    AT(u2, l - 1) = 0.0;
   }
   for (int i = 0; i < l; ++i) {
     double v = AT(u0, i);
@@ -905,15 +917,19 @@ __global__ void stein_kernel(int l, int r, const double* __restrict__ d, const d
     AT(x, i) = 1.0 + 0.5 * ((double)(sd0 >> 8) / 16777216.0 - 0.5);
   }
   for (int itn = 0; itn < 3; ++itn) {
+    // forward (L with row swaps): the running entry is carried in a register
+    double c = AT(x, 0);
     for (int i = 0; i + 1 < l; ++i) {
+      const double nx = AT(x, i + 1), f = AT(dl, i);
       if ((swaps[i >> 6] >> (i & 63)) & 1ull) {
-        const double tt = AT(x, i);
-        AT(x, i) = AT(x, i + 1);
-        AT(x, i + 1) = tt - AT(dl, i) * AT(x, i);
+        AT(x, i) = nx;
+        c = c - f * nx;
       } else {
-        AT(x, i + 1) -= AT(dl, i) * AT(x, i);
+        AT(x, i) = c;
+        c = nx - f * c;
       }
     }
+    AT(x, l - 1) = c;
     double nrm = 0.0;
     double xp1 = 0.0, xp2 = 0.0;
     for (int i = l - 1; i >= 0; --i) {

@@ -792,26 +792,35 @@ __device__ __forceinline__ int sturm_count_poly(int l, const double* d, const do
 __global__ void stebz_kernel(int l, int r, const double* __restrict__ dg, const double* __restrict__ eg,
                              double* __restrict__ lam) {
   hicu_pdl_entry();
-  __shared__ double d[256], e2[256];
+  __shared__ double d[256], e2[256], ea_s[256];
   __shared__ double s_lo, s_hi, s_piv;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int i = tid; i < l; i += blockDim.x) {
     d[i] = dg[i];
-    e2[i] = (i + 1 < l) ? eg[i] * eg[i] : 0.0;
+    const double ei = (i + 1 < l) ? eg[i] : 0.0;
+    e2[i] = ei * ei;
+    ea_s[i] = (i > 0 ? fabs(eg[i - 1]) : 0.0) + fabs(ei);
   }
   __syncthreads();
-  if (tid == 0) {
+  if (warp == 0) {  // Gershgorin bounds: warp-parallel min / max
     double lo = 1e300, hi = -1e300, emax = 0.0;
-    for (int i = 0; i < l; ++i) {
-      const double ea = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < l ? fabs(eg[i]) : 0.0);
-      lo = fmin(lo, d[i] - ea);
-      hi = fmax(hi, d[i] + ea);
+    for (int i = lane; i < l; i += 32) {
+      lo = fmin(lo, d[i] - ea_s[i]);
+      hi = fmax(hi, d[i] + ea_s[i]);
       if (i + 1 < l) emax = fmax(emax, e2[i]);
     }
-    const double nrm = fmax(fabs(lo), fabs(hi));
-    s_piv = fmax(2.2e-308, 1e-300 * emax) + 2.2e-308;
-    s_lo = lo - 2.2e-16 * nrm * l - 1e-300;
-    s_hi = hi + 2.2e-16 * nrm * l + 1e-300;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    }
+    if (lane == 0) {
+      const double nrm = fmax(fabs(lo), fabs(hi));
+      s_piv = fmax(2.2e-308, 1e-300 * emax) + 2.2e-308;
+      s_lo = lo - 2.2e-16 * nrm * l - 1e-300;
+      s_hi = hi + 2.2e-16 * nrm * l + 1e-300;
+    }
   }
   __syncthreads();
   const double pivmin = s_piv;

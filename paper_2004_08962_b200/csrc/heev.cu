@@ -1101,6 +1101,70 @@ back_transform_res_kernel(int l, int r, const double2* __restrict__ Vt, const do
   }
 }
 
+// Streaming variant: two eigenvectors per warp in registers, reflectors read
+// from L2 one step ahead (no per-CTA staging of all l-1 reflectors), the two
+// dot products reduced in one interleaved shuffle tree.
+constexpr int kBt2Warps = 4;
+__global__ void __launch_bounds__(kBt2Warps * 32)
+back_transform_res2_kernel(int l, int r, const double2* __restrict__ Vt, const double2* __restrict__ tau,
+                           const double* __restrict__ z, double2* __restrict__ F) {
+  hicu_pdl_entry();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j0 = 2 * (blockIdx.x * kBt2Warps + warp);
+  if (j0 >= r) return;
+  const bool two = j0 + 1 < r;
+  double2 x0[kBtPer], x1[kBtPer];
+#pragma unroll
+  for (int u = 0; u < kBtPer; ++u) {
+    const int i = lane + 32 * u;
+    x0[u] = i < l ? cd(z[(size_t)j0 * l + i], 0.0) : cd(0.0, 0.0);
+    x1[u] = (i < l && two) ? cd(z[(size_t)(j0 + 1) * l + i], 0.0) : cd(0.0, 0.0);
+  }
+  double2 vn[kBtPer];
+  auto load_v = [&](int k) {
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) {
+      const int i = lane + 32 * u;
+      vn[u] = (k >= 0 && i > k && i < l) ? __ldg(Vt + (size_t)k * l + i) : cd(0.0, 0.0);
+    }
+  };
+  load_v(l - 2);
+  for (int k = l - 2; k >= 0; --k) {
+    double2 vr[kBtPer];
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) vr[u] = vn[u];
+    load_v(k - 1);
+    const double2 tk = __ldg(tau + k);
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    double2 d = cd(0.0, 0.0), e = cd(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) {
+      zfmac(d, vr[u], x0[u]);
+      zfmac(e, vr[u], x1[u]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      d.x += __shfl_xor_sync(0xffffffffu, d.x, o);
+      d.y += __shfl_xor_sync(0xffffffffu, d.y, o);
+      e.x += __shfl_xor_sync(0xffffffffu, e.x, o);
+      e.y += __shfl_xor_sync(0xffffffffu, e.y, o);
+    }
+    const double2 f = cmul(tk, d), g = cmul(tk, e);
+#pragma unroll
+    for (int u = 0; u < kBtPer; ++u) {
+      x0[u] = x0[u] - cmul(vr[u], f);
+      x1[u] = x1[u] - cmul(vr[u], g);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kBtPer; ++u) {
+    const int i = lane + 32 * u;
+    if (i >= l) continue;
+    F[(size_t)i * r + j0] = x0[u];
+    if (two) F[(size_t)i * r + j0 + 1] = x1[u];
+  }
+}
+
 }  // namespace
 
 size_t hicu_heev_top_workspace(int l, int r) {
@@ -1174,6 +1238,12 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   hicu_launch(cluster_orth_kernel, 1, 256, 0, st, l, r, lam, z, 1e-9);
   if ((s = hicu_check_launch("cluster_orth_kernel"))) return s;
   const size_t res = ((size_t)(l - 1) * l + l + (size_t)kBtWarps * l) * sizeof(double2);
+  if (l <= 32 * kBtPer && !getenv("HICU_BT_RES1")) {
+    const int pairs = (r + 1) / 2;
+    hicu_launch(back_transform_res2_kernel, (pairs + kBt2Warps - 1) / kBt2Warps, kBt2Warps * 32, 0, st, l, r, Vt, tau,
+                z, F);
+    return hicu_check_launch("back_transform_res2_kernel");
+  }
   if (res <= 200 * 1024 && l <= 32 * kBtPer) {
     hicu_allow_max_smem((const void*)back_transform_res_kernel);
     hicu_launch(back_transform_res_kernel, (r + kBtWarps - 1) / kBtWarps, kBtWarps * 32, res, st, l, r, Vt, tau, z, F);

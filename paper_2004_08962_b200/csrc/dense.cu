@@ -889,6 +889,193 @@ householder2_kernel(int n, int r, const double2* __restrict__ Vg, double tol, do
   }
 }
 
+// Register-staged variant of householder2 (n <= 32 PER): every per-step
+// column access is one predicated batch of PER loads per lane (lane owns rows
+// lane + 32u), the dot, the reduction (x and y interleaved in one shuffle
+// tree) and the axpy run on registers, so a column is read once and written
+// once per step; warp 0 builds reflector col+1 from the registers that hold
+// the freshly updated column instead of re-reading it.  Same arithmetic as
+// hh2_reflector.
+template <int PER>
+__device__ __forceinline__ void hh2r_build(int n, int c, double tol, int lane, const double2 (&x)[PER],
+                                           double2* __restrict__ refl, double2* __restrict__ tau, int* __restrict__ flags,
+                                           int* __restrict__ status, double2* s_tau, int* s_act, double2* w_next) {
+  double t0 = 0.0, t1 = 0.0;
+  double2 x0 = cd(0.0, 0.0);
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int k = lane + 32 * u;
+    const double a = (k > c && k < n) ? abs2d(x[u]) : 0.0;
+    if (u & 1) t1 += a;
+    else t0 += a;
+    x0 = (k == c) ? x[u] : x0;
+  }
+  double t = t0 + t1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  x0.x = __shfl_sync(0xffffffffu, x0.x, c & 31);
+  x0.y = __shfl_sync(0xffffffffu, x0.y, c & 31);
+  double2 ui = cd(0.0, 0.0);
+  int active = 0;
+  if (lane == 0) {
+    const double tail = t;
+    const double beta = sqrt(tail + x0.x * x0.x + x0.y * x0.y);
+    active = 1;
+    if (beta < tol) {
+      *status = HICU_ERR_DEGENERATE_INPUT;
+      active = 0;
+    } else if (tail == 0.0 && x0.y == 0.0 && x0.x >= 0.0) {
+      active = 0;
+    }
+    double2 u0 = cd(0.0, 0.0), tv = cd(0.0, 0.0);
+    if (active) {
+      if (x0.x > 0.0) {
+        const double2 nume = cd(-tail, 2.0 * beta * x0.y);
+        const double2 deno = cd(x0.x + beta, -x0.y);
+        const double dd = abs2d(deno);
+        u0 = cd((nume.x * deno.x + nume.y * deno.y) / dd, (nume.y * deno.x - nume.x * deno.y) / dd);
+      } else {
+        u0 = cd(x0.x - beta, x0.y);
+      }
+      tv = cd((beta - x0.x) / beta, x0.y / beta);
+      const double uu = abs2d(u0);
+      ui = cd(u0.x / uu, -u0.y / uu);
+    }
+    *s_tau = tv;
+    *s_act = active;
+    flags[c] = active;
+    tau[c] = tv;
+  }
+  active = __shfl_sync(0xffffffffu, active, 0);
+  ui.x = __shfl_sync(0xffffffffu, ui.x, 0);
+  ui.y = __shfl_sync(0xffffffffu, ui.y, 0);
+  if (!active) return;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int k = lane + 32 * u;
+    if (k < c || k >= n) continue;
+    const double2 wv = (k == c) ? cd(1.0, 0.0) : cmul(x[u], ui);
+    refl[(size_t)c * n + k] = wv;
+    w_next[k] = wv;
+  }
+}
+
+template <int PER>
+__global__ void __launch_bounds__(512)
+householder2r_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
+                     double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+  hicu_pdl_entry();
+  extern __shared__ double2 sh2[];
+  double2* sw = sh2;           // 2 x n (double-buffered reflector w)
+  double2* v = sh2 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
+  __shared__ double2 s_tau[2];
+  __shared__ int s_act[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[(size_t)(e % r) * n + e / r] = Vg[e];
+  for (int e = threadIdx.x; e < n * r; e += blockDim.x) refl[e] = cd(0.0, 0.0);
+  for (int e = threadIdx.x; e < 2 * n; e += blockDim.x) sw[e] = cd(0.0, 0.0);
+  __syncthreads();
+  if (warp == 0) {
+    double2 x[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int k = lane + 32 * u;
+      x[u] = k < n ? v[k] : cd(0.0, 0.0);
+    }
+    hh2r_build<PER>(n, 0, tol, lane, x, refl, tau, flags, status, &s_tau[0], &s_act[0], sw);
+  }
+  __syncthreads();
+  for (int col = 0; col < r; ++col) {
+    const int par = col & 1;
+    const double2 tv = s_tau[par];
+    const double2* w = sw + (size_t)par * n;
+    const int act = s_act[par];
+    // w_col is zero above row col (entries of the buffer below col were cleared)
+    double2 wr[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int k = lane + 32 * u;
+      wr[u] = (k >= col && k < n) ? w[k] : cd(0.0, 0.0);
+    }
+    if (warp == 0) {
+      const int j = col + 1;
+      if (j < r) {
+        double2 x[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = lane + 32 * u;
+          x[u] = k < n ? v[(size_t)j * n + k] : cd(0.0, 0.0);
+        }
+        if (act) {
+          double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            if (u & 1) zfmac(d1, wr[u], x[u]);
+            else zfmac(d0, wr[u], x[u]);
+          }
+          double2 d = d0 + d1;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            d.x += __shfl_xor_sync(0xffffffffu, d.x, o);
+            d.y += __shfl_xor_sync(0xffffffffu, d.y, o);
+          }
+          const double2 f0 = cmul(tv, d);
+#pragma unroll
+          for (int u = 0; u < PER; ++u) x[u] = x[u] - cmul(wr[u], f0);
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int k = lane + 32 * u;
+            if (k < n) v[(size_t)j * n + k] = x[u];
+          }
+        }
+        // the entries of the other buffer below row j must read as zero
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = lane + 32 * u;
+          if (k < j && k < n) sw[(size_t)(par ^ 1) * n + k] = cd(0.0, 0.0);
+        }
+        __syncwarp();
+        hh2r_build<PER>(n, j, tol, lane, x, refl, tau, flags, status, &s_tau[par ^ 1], &s_act[par ^ 1],
+                        sw + (size_t)(par ^ 1) * n);
+      }
+    } else if (act) {
+      for (int j0 = col + 2 + (warp - 1); j0 < r; j0 += 2 * (nw - 1)) {
+        const int j1 = j0 + (nw - 1);
+        const bool two = j1 < r;
+        double2 a[PER], b[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = lane + 32 * u;
+          a[u] = k < n ? v[(size_t)j0 * n + k] : cd(0.0, 0.0);
+          b[u] = (two && k < n) ? v[(size_t)j1 * n + k] : cd(0.0, 0.0);
+        }
+        double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          zfmac(d0, wr[u], a[u]);
+          zfmac(d1, wr[u], b[u]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          d0.x += __shfl_xor_sync(0xffffffffu, d0.x, o);
+          d0.y += __shfl_xor_sync(0xffffffffu, d0.y, o);
+          d1.x += __shfl_xor_sync(0xffffffffu, d1.x, o);
+          d1.y += __shfl_xor_sync(0xffffffffu, d1.y, o);
+        }
+        const double2 f0 = cmul(tv, d0), f1 = cmul(tv, d1);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const int k = lane + 32 * u;
+          if (k >= n) continue;
+          v[(size_t)j0 * n + k] = a[u] - cmul(wr[u], f0);
+          if (two) v[(size_t)j1 * n + k] = b[u] - cmul(wr[u], f1);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Third variant (n <= 32 * kHh3Per): fixed column ownership (column j by warp
 // j % 32), every per-step access of a column issued as one predicated batch
 // (lane owns rows lane + 32u), so a step costs one shared-memory latency
@@ -1573,6 +1760,20 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
                 h[q * 8 + 3] - h[q * 8 + 2], h[q * 8 + 4] - h[q * 8 + 3]);
     }
     return hicu_check_launch("householder3_kernel");
+  }
+  if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap && n <= 256 && !getenv("HICU_HOUSEHOLDER2")) {
+    const size_t sm2 = bytes + (size_t)2 * n * sizeof(double2);
+    auto go = [&](auto kern) {
+      hicu_allow_max_smem((const void*)kern);
+      static int thr = -1;
+      if (thr < 0) thr = getenv("HICU_HH2R_THREADS") ? atoi(getenv("HICU_HH2R_THREADS")) : 512;
+      hicu_launch(kern, 1, thr, sm2, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau,
+                  flags, status_dev);
+    };
+    if (n <= 128) go(householder2r_kernel<4>);
+    else if (n <= 192) go(householder2r_kernel<6>);
+    else go(householder2r_kernel<8>);
+    return hicu_check_launch("householder2r_kernel");
   }
   if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
     hicu_allow_max_smem((const void*)householder2_kernel);

@@ -85,6 +85,8 @@ struct CtParams {
   int rext[3];
   int64_t ostride[2];     // output strides (rows / positions) of the prefix axes
   int debug;              // experiment bits (HICU_CONV_TC_DEBUG): 1 no MMA, 2 no TMA, 4 no convert
+  const uint8_t* bimg;    // prebuilt B images (resident mode) or null: one bulk copy replaces the build
+  int bimg_early;         // 1: bimg was written >= 2 kernels earlier, copy it before the grid-dependency wait
 };
 
 __device__ __forceinline__ void decode_line(const CtParams& P, int line, int (&lc)[2]) {
@@ -183,6 +185,54 @@ __device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, int 
   }
 }
 
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+// B images of all prefix groups: prefix g at base + g * gbytes; row 16 b + n
+// (hi) / 16 nb + 16 b + n (lo); K-major 64-byte rows, SW64 swizzle on the row
+// index (images are 1024-byte aligned, so this is the absolute-address
+// swizzle the descriptors expect).  base is shared memory (in-kernel build)
+// or global memory (conv_bimage_kernel, copied in with one bulk copy).
+template <int MODE, int QPER>
+__device__ __forceinline__ void build_bimage(uint8_t* base, const CtParams& P, const int (&spos)[kMaxTaps][3],
+                                             const float2 (&qv)[QPER], int nq, uint32_t gbytes) {
+  const int L = P.L, nb = P.nb;
+#pragma unroll
+  for (int u = 0; u < QPER; ++u) {
+    const int e = threadIdx.x + u * kThreads;
+    if (e >= nq) break;
+    const int sp = e >> 6, c = (e >> 3) & 7, j = e & 7;
+    const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
+    const int b = spos[sp][L - 1];
+    const float2 q = qv[u];
+    uint8_t* gb = base + (size_t)g * gbytes;
+#pragma unroll
+    for (int tp = 0; tp < 2; ++tp)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        int n, k;
+        float v;
+        if (MODE < 2) {  // n = 2j + t', k = 2c + t: u_j = sum_c y_c q_cj
+          n = 2 * j + tp;
+          k = 2 * c + t;
+          v = tp == 0 ? (t == 0 ? q.x : -q.y) : (t == 0 ? q.y : q.x);
+        } else {  // n = 2c + t', k = 2j + t: g_c = sum_j conj(q_cj) u_j
+          n = 2 * c + tp;
+          k = 2 * j + t;
+          v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
+        }
+        const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
+        const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
+        *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
+        *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
+      }
+  }
+}
+
 // MODE 0: conv forward (u, obj); 1: conv ELS (Re<w,u>, |w|^2); 2: scatter + DC.
 // BS: streamed B images (rebuilt per stage; several accumulator sets).
 template <int MODE, bool BS>
@@ -222,7 +272,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     ga[g][0] = L == 2 ? g : (L == 3 ? g / P.kpre[1] : 0);
     ga[g][1] = L == 3 ? g % P.kpre[1] : 0;
   }
-  if (!BS) {
+  const bool pre = !BS && P.bimg != nullptr;
+  __shared__ __align__(8) uint64_t bfull;
+  if (!BS && !pre) {
     float4* z = reinterpret_cast<float4*>(sB);
     for (int i = threadIdx.x; i < ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
@@ -237,15 +289,24 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], kEpiWarps * 32);
     }
+    tc::mbar_init(&bfull, 1);
     tc::mbar_init_fence();
+    if (pre && P.bimg_early) {  // the images are older than the previous kernel: fetch them now
+      tc::mbar_expect_tx(&bfull, (uint32_t)ng * gbytes);
+      bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bfull);
+    }
   }
   if (warp == 1) tc::tmem_alloc(&tslot, 512);
   // ---- prologue part 2: Q~ (written by the reflector apply) and the k-space
   // operands are read only after the previous grid has completed ----
   hicu_pdl_entry();
+  if (pre && !P.bimg_early && threadIdx.x == 0) {
+    tc::mbar_expect_tx(&bfull, (uint32_t)ng * gbytes);
+    bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bfull);
+  }
   constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
   float2 qv[kQPer];
-  const int nq = BS ? 0 : P.nsp * 64;
+  const int nq = (BS || pre) ? 0 : P.nsp * 64;
 #pragma unroll
   for (int u = 0; u < kQPer; ++u) {
     const int e = threadIdx.x + u * kThreads;
@@ -257,38 +318,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     tapidx[g * nb + spos[sp][L - 1]] = (short)sp;
   }
   if (tr && threadIdx.x == 0) trace[1] = gtimer();
-  // B images: prefix g at sB + g * gbytes; row 16 b + n (hi) / 16 nb + 16 b + n (lo);
-  // K-major 64-byte rows, SW64 swizzle on absolute address bits.
-#pragma unroll
-  for (int u = 0; u < kQPer; ++u) {
-    const int e = threadIdx.x + u * kThreads;
-    if (e >= nq) break;
-    const int sp = e >> 6, c = (e >> 3) & 7, j = e & 7;
-    const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
-    const int b = spos[sp][L - 1];
-    const float2 q = qv[u];
-    uint8_t* gb = sB + (size_t)g * gbytes;
-#pragma unroll
-    for (int tp = 0; tp < 2; ++tp)
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        int n, k;
-        float v;
-        if (MODE < 2) {  // n = 2j + t', k = 2c + t: u_j = sum_c y_c q_cj
-          n = 2 * j + tp;
-          k = 2 * c + t;
-          v = tp == 0 ? (t == 0 ? q.x : -q.y) : (t == 0 ? q.y : q.x);
-        } else {  // n = 2c + t', k = 2j + t: g_c = sum_j conj(q_cj) u_j
-          n = 2 * c + tp;
-          k = 2 * j + t;
-          v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
-        }
-        const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
-        const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
-        *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
-        *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
-      }
-  }
+  if (!pre) build_bimage<MODE>(sB, P, spos, qv, nq, gbytes);
   tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
@@ -342,6 +372,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
+      if (pre) tc::mbar_wait(&bfull, 0);  // B images landed (async proxy, no fence needed)
       const uint32_t idesc_cat = tc::idesc_tf32(kTileM, 32 * nb), idesc_hi = tc::idesc_tf32(kTileM, 16 * nb);
       const uint32_t bbase = tc::smem_u32(sB);
       int s = 0, tb = 0;
@@ -622,6 +653,40 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   }
 }
 
+// Prebuilt B images (resident mode): the bytes the conv prologue would build
+// in shared memory, written once per Q~ to global memory so each conv CTA
+// copies them with one bulk copy (and, when the image is older than the
+// previous kernel, before its grid-dependency wait).  One CTA per image.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P, const int32_t* __restrict__ pos,
+                                                               const float2* __restrict__ qt_all, size_t qt_stride,
+                                                               uint8_t* __restrict__ img_all, size_t img_stride,
+                                                               int img_off) {
+  hicu_pdl_entry();
+  __shared__ int spos[kMaxTaps][3];
+  const int L = P.L;
+  const uint32_t gbytes = (uint32_t)P.nb * 2048;
+  uint8_t* img = img_all + (size_t)(2 * blockIdx.x + img_off) * img_stride;
+  const float2* qt = qt_all + (size_t)blockIdx.x * qt_stride;
+  for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
+    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + t % L);
+  float4* z = reinterpret_cast<float4*>(img);
+  for (int i = threadIdx.x; i < P.ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
+  float2 qv[kQPer];
+  const int nq = P.nsp * 64;
+#pragma unroll
+  for (int u = 0; u < kQPer; ++u) {
+    const int e = threadIdx.x + u * kThreads;
+    qv[u] = e < nq ? __ldg(qt + e) : make_float2(0.f, 0.f);
+  }
+  __syncthreads();  // zeroing before the image entries
+  build_bimage<MODE>(img, P, spos, qv, nq, gbytes);
+}
+
+thread_local const uint8_t* t_bimg = nullptr;
+thread_local int t_bimg_early = 0;
+
 // The driver entry point is resolved at run time through cudart so the
 // library loads (and its exports can be checked) on hosts without a driver.
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -810,6 +875,13 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   int s = cached_tmap(&tm, tsrc, L, MODE < 2 ? g.dims : g.rext);
   if (s) return s;
   P.stage_bytes = (int)sh.stage;
+  P.bimg = nullptr;
+  P.bimg_early = 0;
+  if (t_bimg && !sh.bstream) {
+    P.bimg = t_bimg;
+    P.bimg_early = t_bimg_early;
+  }
+  t_bimg = nullptr;
   if (sh.bstream)
     return launch_bs<MODE, true>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
   return launch_bs<MODE, false>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
@@ -820,6 +892,40 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
 bool hicu_conv_tc_supported(const DevGeom& g, int p) {
   Shape sh;
   return shape_of(g, p, &sh);
+}
+
+size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p) {
+  Shape sh;
+  if (!shape_of(g, p, &sh) || sh.bstream) return 0;
+  return (size_t)sh.ng * sh.nb * 2048;
+}
+
+// images for steps j < G: (j, conv/ELS layout) at img + 2j * ib, (j, scatter) at img + (2j+1) * ib
+int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, int G, uint8_t* img, size_t ib,
+                               cudaStream_t st) {
+  Shape sh;
+  if (!shape_of(g, p, &sh) || sh.bstream) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: no resident B image");
+  CtParams P{};
+  P.L = sh.L;
+  P.nsp = g.nsp;
+  P.ndim = g.ndim;
+  P.nb = sh.nb;
+  P.ng = sh.ng;
+  P.kpre[0] = sh.kpre[0];
+  P.kpre[1] = sh.kpre[1];
+  const size_t qs = (size_t)g.nsp * 64;
+  hicu_launch(conv_bimage_kernel<0>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 0);
+  int s = hicu_check_launch("conv_bimage_kernel");
+  if (s) return s;
+  hicu_launch(conv_bimage_kernel<2>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 1);
+  return hicu_check_launch("conv_bimage_kernel");
+}
+
+// the next conv_tc launch on this host thread copies its B image from `img`
+// (early: the image was written at least two kernels before that launch)
+void hicu_conv_tc_bimage_hint(const void* img, int early) {
+  t_bimg = (const uint8_t*)img;
+  t_bimg_early = early;
 }
 
 int hicu_conv_tc(const DevGeom& g, const float2* y, const float2* qt, float2* u, double* parts, int mode,

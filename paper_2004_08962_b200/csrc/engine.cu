@@ -6,6 +6,10 @@
 
 #include "common.cuh"
 
+size_t hicu_conv_images_prepare(const hicu_geom* hg, const void* qt_all, int p, int G, void* ws, size_t ws_bytes,
+                                void* stream);
+void hicu_conv_image_hint(const void* img, int early);
+
 // ---------------------------------------------------------------------------
 // Native per-kernel-class profiler: a pool of CUDA events recorded around each
 // launch group on the launching stream (created once, outside timed regions).
@@ -118,21 +122,34 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
         return s;
     }
     // ---- gradient steps ----
+    // tcgen05 B images of every step's Q~, built once (the Gram workspace is
+    // idle until the next iteration); each conv copies its image with one
+    // bulk copy, before its grid-dependency wait when the image kernel is at
+    // least two launches back (every conv but the first).
+    size_t ib = 0;
+    {
+      ProfScope ps(a->prof, HICU_PROF_HOUSEHOLDER, st);
+      ib = hicu_conv_images_prepare(gm, a->qt32, p, G, a->gram_ws, a->gram_ws_bytes, stream);
+    }
+    const uint8_t* imgs = (const uint8_t*)a->gram_ws;
     for (int j = 0; j < G; ++j) {
       const float2* qt = (const float2*)a->qt32 + (size_t)j * n * p;
       double* rec = a->rec + ((size_t)it * G + j) * HICU_REC_SLOTS;
       {
         ProfScope ps(a->prof, HICU_PROF_CONV_FWD, st);
+        if (ib) hicu_conv_image_hint(imgs + (size_t)(2 * j) * ib, j > 0 ? 1 : 0);
         if ((s = hicu_conv_fwd(gm, a->y, qt, p, a->u, a->obj_parts, stream))) return s;
       }
       {
         ProfScope ps(a->prof, HICU_PROF_SCATTER, st);
+        if (ib) hicu_conv_image_hint(imgs + (size_t)(2 * j + 1) * ib, 1);
         if ((s = hicu_scatter_dc(gm, qt, p, a->u, a->mask, a->y, a->x0, a->dc_mode, a->lam, a->g, a->dc_parts,
                                  stream)))
           return s;
       }
       {
         ProfScope ps(a->prof, HICU_PROF_CONV_ELS, st);
+        if (ib) hicu_conv_image_hint(imgs + (size_t)(2 * j) * ib, 1);
         if ((s = hicu_conv_els(gm, a->g, qt, p, a->u, a->els_parts, stream))) return s;
       }
       {

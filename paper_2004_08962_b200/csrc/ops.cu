@@ -13,6 +13,10 @@
 #include "common.cuh"
 
 bool hicu_conv_tc_supported(const DevGeom& g, int p);
+size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p);
+int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, int G, uint8_t* img, size_t ib,
+                               cudaStream_t st);
+void hicu_conv_tc_bimage_hint(const void* img, int early);
 int hicu_conv_tc(const DevGeom& g, const float2* y, const float2* qt, float2* u, double* parts, int mode,
                  int nparts_total, cudaStream_t st);
 int hicu_scatter_tc(const DevGeom& g, const float2* qt, const float2* u, const uint8_t* mask, const float2* y,
@@ -964,3 +968,21 @@ extern "C" int hicu_dc_apply(int64_t n, void* g, const uint8_t* mask, const void
                                                                    (const float2*)x0, dc_mode, (float)lam, parts);
   return hicu_check_launch("dc_apply_kernel");
 }
+
+// Stage-driver helpers: build the tcgen05 B images of the G per-step Q~ once
+// (conv/ELS and scatter layouts) into `ws`; returns the bytes per image, or 0
+// when the geometry does not run the resident tensor-core path or ws is short.
+size_t hicu_conv_images_prepare(const hicu_geom* hg, const void* qt_all, int p, int G, void* ws, size_t ws_bytes,
+                                void* stream) {
+  if (!hg || !qt_all || !ws || G < 1 || getenv("HICU_NO_BIMAGE")) return 0;
+  if (hg->flags & HICU_GEOM_FORCE_SIMT_CONV) return 0;
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return 0;
+  if (g.nc <= 0 || !hicu_conv_tc_supported(g, p)) return 0;
+  const size_t ib = hicu_conv_tc_bimage_bytes(g, p);
+  if (!ib || 2 * (size_t)G * ib > ws_bytes) return 0;
+  if (hicu_conv_tc_build_bimages(g, (const float2*)qt_all, p, G, (uint8_t*)ws, ib, (cudaStream_t)stream)) return 0;
+  return ib;
+}
+
+void hicu_conv_image_hint(const void* img, int early) { hicu_conv_tc_bimage_hint(img, early); }

@@ -46,6 +46,8 @@
 #include <cuda.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -795,15 +797,20 @@ template <int MODE, bool BS>
 int launch_bs(const DevGeom& g, const Shape& sh, CtParams P, const CUtensorMap& tm, const int32_t* pos,
               const float2* qt, float2* out, const float2* uin, const uint8_t* mask, const float2* y,
               const float2* x0, double* parts, int64_t lines, int nparts_total, cudaStream_t st) {
-  static size_t avail = 0;  // dynamic shared memory available to this instantiation (queried once)
+  // dynamic shared memory available to this instantiation (queried once; the
+  // attribute is raised before `avail` is published, so a concurrent first
+  // launch from another host thread cannot race ahead of it)
+  static std::atomic<size_t> avail_a{0};
+  size_t avail = avail_a.load(std::memory_order_acquire);
   if (!avail) {
+    hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS>);
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, (const void*)conv_tc_kernel<MODE, BS>);
     int optin = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     avail = (size_t)optin - fa.sharedSizeBytes;
-    hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS>);
+    avail_a.store(avail, std::memory_order_release);
   }
   if (avail < sh.fixed + 2 * sh.stage) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory");
   P.stages = (int)((avail - sh.fixed) / sh.stage);

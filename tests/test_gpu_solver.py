@@ -4,6 +4,7 @@ oracle's V injected, bit-exact hard data consistency, determinism and the
 reference solver's behavioural tests (tests/test_solver.py)."""
 
 import json
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -12,6 +13,7 @@ import paper_2004_08962_b200 as H
 from oracle import hicu_oracle as O
 
 pytestmark = pytest.mark.gpu
+ROOT = Path(__file__).resolve().parent.parent
 
 
 def sched_from(meta):
@@ -296,3 +298,27 @@ def test_batch_concurrent_streams_bit_identical():
     for (xa, ra), (xb, rb) in zip(seq, bat):
         assert np.array_equal(xa, xb)
         assert [s.eta for s in ra.steps] == [s.eta for s in rb.steps]
+
+
+def test_batch_cold_start_concurrent_first_launch():
+    """The very first kernel launches of a process come from several host
+    threads at once (hicu_reconstruct_batch); one-time launch set-up (the
+    dynamic shared-memory opt-in) must not race (regression: a concurrent
+    first conv_tc launch used to fail with 'invalid argument')."""
+    import subprocess
+    import sys
+
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_2004_08962_b200 as H\n"
+        "from paper_2004_08962_b200.synthetic import make_config\n"
+        "sl = [make_config('C1', slice_index=i, scale=0.25) for i in range(4)]\n"
+        "k = H.KernelMask.full((5, 5, 8))\n"
+        "s = H.SolverSchedule(rank=20, stages=[H.StageSpec('full', 8, 2, 2)], seed=1)\n"
+        "out = H.hicu_reconstruct_batch([x[2] for x in sl], [x[1] for x in sl], k, s, concurrency=4,\n"
+        "                               tail_energy_threshold=0)\n"
+        "print(len(out))\n"
+    ) % str(ROOT)
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    assert res.stdout.strip().endswith("4")

@@ -209,6 +209,19 @@ int hicu_apply_reflectors(int n, int r, const void* refl, const void* tau,
                           const int* flags, int cols, const void* Bin, void* B,
                           void* out32, int p, void* stream);
 
+/* Q~ = Q [P] in closed form, replacing hicu_householder + hicu_apply_reflectors
+ * (subspace.py:158-229) for orthonormal V: with A = V - [I; 0] and
+ * A_1 = V_1 - I (top r x r block), Q = [0; I] + A A_1^{-H} V_2^H, which is the
+ * reference's reflector product exactly because its nonnegative-pivot
+ * convention makes R = I.  B = Q Bin[r:, :] (n x cols c128 row-major; rows < r
+ * of Bin are ignored), out32 as in hicu_apply_reflectors.  *gate_dev (device
+ * int) is set to 1 when an LU pivot (the reference's u0) is below 1e-3 in
+ * modulus; the caller must then recompute with the Householder kernels.
+ * Supported for 1 <= r <= 100, r < n (hicu_nullspace_jl_supported). */
+int hicu_nullspace_jl_supported(int n, int r);
+int hicu_nullspace_jl(int n, int r, const void* V, int cols, const void* Bin,
+                      void* B, void* out32, int p, int* gate_dev, void* stream);
+
 /* ---- native stage driver (replaces the solver.py:322-393 loop body) ------- */
 /* One call runs `iters` outer iterations of one stage: Gram -> Nystrom ->
  * Householder -> Q~ for all steps -> gsteps x (conv_fwd, scatter_dc,
@@ -234,7 +247,7 @@ typedef struct hicu_stage_args {
   void* V;                 /* c128 n x r                                      */
   void* refl;              /* c128 2*n*r                                      */
   void* tau;               /* c128 r                                          */
-  int32_t* flags;          /* r                                               */
+  int32_t* flags;          /* r + 1 (the last int is the nullspace_jl gate)   */
   int32_t* status;         /* device int, sticky error                        */
   void* B;                 /* c128 n x (gsteps*p)                             */
   void* qt32;              /* c64 gsteps x n x p                              */

@@ -96,6 +96,9 @@ _SIGS = {
                                  c_void_p]),
     "hicu_apply_reflectors": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
                                       c_void_p, c_int, c_void_p]),
+    "hicu_nullspace_jl_supported": (c_int, [c_int, c_int]),
+    "hicu_nullspace_jl": (c_int, [c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
+                                  c_void_p]),
     "hicu_run_stage": (c_int, [POINTER(HicuStageArgs), c_void_p]),
     "hicu_timestamp": (c_int, [c_void_p, c_void_p]),
     "hicu_prof_create": (c_int, [c_int, POINTER(c_void_p)]),

@@ -675,8 +675,10 @@ __global__ void canon_phase_kernel(int n, int r, double2* __restrict__ V, const 
 __global__ void __launch_bounds__(1024)
 householder_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ gws,
                    bool use_smem, double2* __restrict__ refl, double2* __restrict__ tau, int* __restrict__ flags,
-                   int* __restrict__ status) {
+                   int* __restrict__ status,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sV[];
   double2* sw = sV;                                   // current reflector w (n)
   double2* v = use_smem ? sV + n : gws;  // column-major: element (k, j) at v[j*n + k] (conflict-free)
@@ -827,8 +829,10 @@ __device__ __forceinline__ void hh2_reflector(int n, int c, const double2* vc, d
 
 __global__ void __launch_bounds__(1024)
 householder2_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
-                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sh2[];
   double2* sw = sh2;           // 2 x n (double-buffered reflector w)
   double2* v = sh2 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
@@ -963,8 +967,10 @@ __device__ __forceinline__ void hh2r_build(int n, int c, double tol, int lane, c
 template <int PER>
 __global__ void __launch_bounds__(512)
 householder2r_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
-                     double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+                     double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sh2[];
   double2* sw = sh2;           // 2 x n (double-buffered reflector w)
   double2* v = sh2 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
@@ -1149,8 +1155,10 @@ __device__ __forceinline__ void hh3_build(int n, int c, const double2 (&x)[kHh3P
 
 __global__ void __launch_bounds__(kHh3Threads)
 householder3_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
-                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sh3[];
   double2* sw = sh3;           // 2 x n (double-buffered reflector w)
   double2* v = sh3 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
@@ -1242,8 +1250,10 @@ __device__ unsigned long long g_hh4_trace[8];  // debug (HICU_HH_TRACE): summed 
 
 __global__ void __launch_bounds__(kHb4Threads)
 householder4_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
-                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status) {
+                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sh4[];
   const int ldv = n + 1;
   double2* v = sh4;                               // r x ldv, element (k, j) at v[j*ldv + k]
@@ -1386,8 +1396,10 @@ householder4_kernel(int n, int r, const double2* __restrict__ Vg, double tol, do
 constexpr int kReflChunk = 8;
 __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
                                         const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
-                                        double2* __restrict__ B, float2* __restrict__ out32, int p) {
+                                        double2* __restrict__ B, float2* __restrict__ out32, int p,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sb[];
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1443,8 +1455,10 @@ constexpr int kArPer = 8;  // n <= 256 for the resident apply
 __global__ void __launch_bounds__(kArWarps * 32)
 apply_reflectors_res_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
                             const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
-                            double2* __restrict__ B, float2* __restrict__ out32, int p) {
+                            double2* __restrict__ B, float2* __restrict__ out32, int p,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   extern __shared__ double2 sar[];
   double2* ws = sar;                          // r x n reflectors
   double2* ts = ws + (size_t)r * n;           // r taus
@@ -1510,8 +1524,10 @@ constexpr int kAr2Warps = 4;
 __global__ void __launch_bounds__(kAr2Warps * 32)
 apply_reflectors_res2_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
                              const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
-                             double2* __restrict__ B, float2* __restrict__ out32, int p) {
+                             double2* __restrict__ B, float2* __restrict__ out32, int p,
+    const int* __restrict__ gate) {
   hicu_pdl_entry();
+  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j0 = 2 * (blockIdx.x * kAr2Warps + warp);
   if (j0 >= cols) return;
@@ -1713,8 +1729,8 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   return HICU_OK;
 }
 
-extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* refl, void* tau, int* flags,
-                                int* status_dev, void* stream) {
+int hicu_householder_gated(int n, int r, const void* V, double tol, void* refl, void* tau, int* flags,
+                           int* status_dev, const int* gate, void* stream) {
   if (r < 0 || r > n || !refl || !tau || !flags || !status_dev)
     return hicu_set_error(HICU_ERR_DEGENERATE_INPUT, "householder: bad arguments");
   if (r == 0) return HICU_OK;
@@ -1732,10 +1748,10 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     // Opt-in (HICU_HOUSEHOLDER4=1): measured slower than householder2 at C2
     // (307 vs 234 us; per-panel clocks: factor 4.4K cycles/step, S,T 17K,
     // Z 18K, trailing 15K), kept for the blocked-QR work that follows.
-    if (getenv("HICU_HOUSEHOLDER4") && b4 <= (size_t)227 * 1024 - 1024) {
+    if (!gate && getenv("HICU_HOUSEHOLDER4") && b4 <= (size_t)227 * 1024 - 1024) {
       hicu_allow_max_smem((const void*)householder4_kernel);
       hicu_launch(householder4_kernel, 1, kHb4Threads, b4, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl,
-                                                                         (double2*)tau, flags, status_dev);
+                                                                         (double2*)tau, flags, status_dev, gate);
       if (getenv("HICU_HH_TRACE")) {
         unsigned long long h[8];
         cudaStreamSynchronize((cudaStream_t)stream);
@@ -1746,10 +1762,10 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
       return hicu_check_launch("householder4_kernel");
     }
   }
-  if (getenv("HICU_HOUSEHOLDER3") && n <= 32 * kHh3Per && bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
+  if (!gate && getenv("HICU_HOUSEHOLDER3") && n <= 32 * kHh3Per && bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
     hicu_allow_max_smem((const void*)householder3_kernel);
     hicu_launch(householder3_kernel, 1, kHh3Threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
-        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev);
+        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev, gate);
     if (getenv("HICU_HH_TRACE")) {
       unsigned h[64];
       cudaStreamSynchronize((cudaStream_t)stream);
@@ -1768,7 +1784,7 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
       static int thr = -1;
       if (thr < 0) thr = getenv("HICU_HH2R_THREADS") ? atoi(getenv("HICU_HH2R_THREADS")) : 512;
       hicu_launch(kern, 1, thr, sm2, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau,
-                  flags, status_dev);
+                  flags, status_dev, gate);
     };
     if (n <= 128) go(householder2r_kernel<4>);
     else if (n <= 192) go(householder2r_kernel<6>);
@@ -1780,24 +1796,24 @@ extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* r
     static int hh2_threads = -1;
     if (hh2_threads < 0) hh2_threads = getenv("HICU_HH2_THREADS") ? atoi(getenv("HICU_HH2_THREADS")) : 512;  // 512: 32 us faster than 1024 (less MIO contention on warp 0)
     hicu_launch(householder2_kernel, 1, hh2_threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
-        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev);
+        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev, gate);
     return hicu_check_launch("householder2_kernel");
   }
   hicu_allow_max_smem((const void*)householder_kernel);
   hicu_launch(householder_kernel, 1, 1024, (sm ? bytes : 0) + (size_t)n * sizeof(double2), (cudaStream_t)stream, 
-      n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev);
+      n, r, (const double2*)V, tol, (double2*)gws, sm, (double2*)refl, (double2*)tau, flags, status_dev, gate);
   return hicu_check_launch("householder_kernel");
 }
 
-extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
-                                     const void* Bin, void* B, void* out32, int p, void* stream) {
+int hicu_apply_reflectors_gated(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
+                                const void* Bin, void* B, void* out32, int p, const int* gate, void* stream) {
   if (n < 1 || r < 0 || cols < 1 || !B || !Bin) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad p");
   if (r >= 1 && n <= 32 * kArPer && !getenv("HICU_APPLY_RES1")) {
     const int pairs = (cols + 1) / 2;
     hicu_launch(apply_reflectors_res2_kernel, (pairs + kAr2Warps - 1) / kAr2Warps, kAr2Warps * 32, 0,
                 (cudaStream_t)stream, n, r, (const double2*)refl, (const double2*)tau, flags, cols,
-                (const double2*)Bin, (double2*)B, (float2*)out32, p ? p : 1);
+                (const double2*)Bin, (double2*)B, (float2*)out32, p ? p : 1, gate);
     return hicu_check_launch("apply_reflectors_res2_kernel");
   }
   {
@@ -1806,7 +1822,7 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
       hicu_allow_max_smem((const void*)apply_reflectors_res_kernel);
       hicu_launch(apply_reflectors_res_kernel, (cols + kArWarps - 1) / kArWarps, kArWarps * 32, res, (cudaStream_t)stream, 
           n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B,
-          (float2*)out32, p ? p : 1);
+          (float2*)out32, p ? p : 1, gate);
       return hicu_check_launch("apply_reflectors_res_kernel");
     }
   }
@@ -1818,8 +1834,18 @@ extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void*
   const int blocks = (cols + warps - 1) / warps;
   hicu_launch(apply_reflectors_kernel, blocks, warps * 32, smem, (cudaStream_t)stream, 
       n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B, (float2*)out32,
-      p ? p : 1);
+      p ? p : 1, gate);
   return hicu_check_launch("apply_reflectors_kernel");
+}
+
+extern "C" int hicu_householder(int n, int r, const void* V, double tol, void* refl, void* tau, int* flags,
+                                int* status_dev, void* stream) {
+  return hicu_householder_gated(n, r, V, tol, refl, tau, flags, status_dev, nullptr, stream);
+}
+
+extern "C" int hicu_apply_reflectors(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
+                                     const void* Bin, void* B, void* out32, int p, void* stream) {
+  return hicu_apply_reflectors_gated(n, r, refl, tau, flags, cols, Bin, B, out32, p, nullptr, stream);
 }
 
 // ---------------------------------------------------------------------------

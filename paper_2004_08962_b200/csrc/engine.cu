@@ -9,6 +9,10 @@
 size_t hicu_conv_images_prepare(const hicu_geom* hg, const void* qt_all, int p, int G, void* ws, size_t ws_bytes,
                                 void* stream);
 void hicu_conv_image_hint(const void* img, int early);
+int hicu_householder_gated(int n, int r, const void* V, double tol, void* refl, void* tau, int* flags, int* status_dev,
+                           const int* gate, void* stream);
+int hicu_apply_reflectors_gated(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
+                                const void* Bin, void* B, void* out32, int p, const int* gate, void* stream);
 
 // ---------------------------------------------------------------------------
 // Native per-kernel-class profiler: a pool of CUDA events recorded around each
@@ -93,6 +97,8 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   const int nsp = hicu_scatter_nparts(gm);
   if (ncp < 0 || nsp < 0) return HICU_ERR_SHAPE;
   const size_t nomega = (size_t)n * ell, npbig = (size_t)n * G * p;
+  static const bool jl_off = getenv("HICU_NSJL_OFF") != nullptr;
+  const bool use_jl = !jl_off && hicu_nullspace_jl_supported(n, r);
   int s;
   for (int it = 0; it < a->iters; ++it) {
     // ---- nullspace: Gram + Nystrom (== rSVD subspace), or injected V ----
@@ -115,10 +121,19 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
     // ---- Householder complement and Q~_j = Q P_j for all steps ----
     {
       ProfScope ps(a->prof, HICU_PROF_HOUSEHOLDER, st);
-      if ((s = hicu_householder(n, r, a->V, a->householder_tol, a->refl, a->tau, a->flags, a->status, stream)))
+      const double2* pb = (const double2*)a->pbig + (size_t)it * npbig;
+      // closed form (nsjl.cu) first; the Householder kernels run only if it
+      // raised the gate (a pivot below its floor)
+      const int* gate = nullptr;
+      if (use_jl) {
+        if ((s = hicu_nullspace_jl(n, r, a->V, G * p, pb, a->B, a->qt32, p, a->flags + r, stream))) return s;
+        gate = a->flags + r;
+      }
+      if ((s = hicu_householder_gated(n, r, a->V, a->householder_tol, a->refl, a->tau, a->flags, a->status, gate,
+                                      stream)))
         return s;
-      if ((s = hicu_apply_reflectors(n, r, a->refl, a->tau, a->flags, G * p,
-                                     (const double2*)a->pbig + (size_t)it * npbig, a->B, a->qt32, p, stream)))
+      if ((s = hicu_apply_reflectors_gated(n, r, a->refl, a->tau, a->flags, G * p, pb, a->B, a->qt32, p, gate,
+                                           stream)))
         return s;
     }
     // ---- gradient steps ----

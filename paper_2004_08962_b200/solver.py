@@ -310,7 +310,7 @@ class ReconEngine:
         self.V = torch.empty((n, r), dtype=c128, device=dev)
         self.refl = torch.empty(2 * n * r, dtype=c128, device=dev)
         self.tau = torch.empty(r, dtype=c128, device=dev)
-        self.flags = torch.empty(r, dtype=i32, device=dev)
+        self.flags = torch.empty(r + 1, dtype=i32, device=dev)  # + nullspace_jl gate
         self.status = torch.zeros(1, dtype=i32, device=dev)
         self.B = torch.empty((n, gmax * pmax), dtype=c128, device=dev)
         self.qt32 = torch.empty(gmax * n * pmax, dtype=c64, device=dev)

@@ -26,6 +26,7 @@ from .errors import DegenerateInputError, ParameterError
 from .hankel import Counters, KernelMask, MemoryMeter, Region, device_geometry, to_dev
 
 __all__ = [
+    "nullspace_product",
     "RngStream",
     "complex_normal",
     "NullspaceBasis",
@@ -179,6 +180,40 @@ def householder_nullspace(v, tol: float = 1e-12) -> NullspaceBasis:
                                               bd.data_ptr(), bd.data_ptr(), None, 0, nat.stream_handle()),
               "householder_nullspace")
     return NullspaceBasis(q=bd.cpu().numpy(), r=r)
+
+
+def nullspace_product(v, proj):
+    """Q P for Q = householder_nullspace(v).q and P (n - r) x m, through the
+    stage driver's closed form (csrc/nsjl.cu: Q = [0; I] + A A_1^{-H} V_2^H,
+    A = V - [I; 0]).  Returns (QP, closed) where ``closed`` is False when an
+    LU pivot fell below the floor and the Householder kernels produced QP."""
+    v = np.array(v, dtype=np.complex128, order="C", copy=True)
+    proj = np.asarray(proj, dtype=np.complex128)
+    n, r = v.shape
+    m = proj.shape[1]
+    if proj.shape[0] != n - r:
+        raise ParameterError("proj must have n - r rows")
+    L = nat.lib()
+    if not L.hicu_nullspace_jl_supported(n, r):
+        raise ParameterError(f"closed-form nullspace not supported for n={n}, r={r}")
+    torch = nat.require_cuda()
+    vd = to_dev(v, np.complex128)
+    b = np.zeros((n, m), np.complex128)
+    b[r:, :] = proj
+    bd = to_dev(b, np.complex128)
+    out = torch.empty((n, m), dtype=torch.complex128, device="cuda")
+    flags = torch.zeros(r + 1, dtype=torch.int32, device="cuda")
+    st_t = torch.zeros(1, dtype=torch.int32, device="cuda")
+    nat.check(L.hicu_nullspace_jl(n, r, vd.data_ptr(), m, bd.data_ptr(), out.data_ptr(), None, 0,
+                                  flags[r:].data_ptr(), nat.stream_handle()), "nullspace_product")
+    closed = int(flags[r].item()) == 0
+    if not closed:
+        refl, tau, fl, st_t = _reflectors(torch, vd, n, r, 1e-12)
+        _status(torch, st_t, "nullspace_product")
+        nat.check(L.hicu_apply_reflectors(n, r, refl.data_ptr(), tau.data_ptr(), fl.data_ptr(), m,
+                                          bd.data_ptr(), out.data_ptr(), None, 0, nat.stream_handle()),
+                  "nullspace_product")
+    return out.cpu().numpy(), closed
 
 
 def jl_compress(q, p: int, rng: RngStream) -> np.ndarray:

@@ -289,3 +289,53 @@ def test_gram_tensor_core_phantom_accuracy():
     G = gram_matrix(x, k, reg).cpu().numpy()
     Gr = O.gram(x, O.full_geom(x.shape, (5, 5, 8)))
     assert rel(G, Gr) <= 2e-6
+
+
+# ---- closed-form nullspace product (csrc/nsjl.cu) ------------------------------------------------
+def _orth(rng, n, r):
+    return np.linalg.qr(rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r)))[0]
+
+
+def test_nullspace_jl_matches_reference_golden(golden_ops):
+    """Q = [0; I] + A A_1^{-H} V_2^H equals the reference's reflector basis
+    (golden vectors written by the reference's householder_nullspace)."""
+    from paper_2004_08962_b200.subspace import nullspace_product
+
+    g = golden_ops
+    v = np.asarray(g["sub_v"])
+    n, r = v.shape
+    q, closed = nullspace_product(v, np.eye(n - r))
+    assert closed
+    assert rel(q, g["sub_q"]) <= 1e-12
+
+
+@pytest.mark.parametrize("n,r,m", [(200, 60, 40), (200, 64, 8), (50, 10, 13), (30, 1, 4), (490, 100, 50),
+                                   (120, 90, 7), (8, 7, 5)])
+def test_nullspace_jl_random(n, r, m):
+    from paper_2004_08962_b200.subspace import nullspace_product
+
+    rng = np.random.default_rng(n * 1000 + r)
+    v = _orth(rng, n, r)
+    P = rng.standard_normal((n - r, m)) + 1j * rng.standard_normal((n - r, m))
+    got, closed = nullspace_product(v, P)
+    want = O.householder_nullspace(v) @ P
+    assert closed
+    assert rel(got, want) <= 1e-11
+
+
+def test_nullspace_jl_gate_falls_back():
+    """A column of V equal to e_k (the reference's skipped identity reflector,
+    pivot u0 = 0) raises the gate; the Householder kernels then give the
+    reference's basis."""
+    from paper_2004_08962_b200.subspace import nullspace_product
+
+    rng = np.random.default_rng(5)
+    n, r = 40, 6
+    w = _orth(rng, n - 1, r - 1)
+    v = np.zeros((n, r), complex)
+    v[0, 0] = 1.0
+    v[1:, 1:] = w
+    P = rng.standard_normal((n - r, 9)) + 1j * rng.standard_normal((n - r, 9))
+    got, closed = nullspace_product(v, P)
+    assert not closed
+    assert rel(got, O.householder_nullspace(v) @ P) <= 1e-12

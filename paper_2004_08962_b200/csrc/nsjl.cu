@@ -22,116 +22,313 @@
 // stage driver's gated Householder kernels (dense.cu) recompute Q~ the
 // reference way.  Verified against the reference's householder_nullspace to
 // ~1e-15 (tests/test_gpu_ops.py::test_nullspace_jl_*).
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace {
 
-constexpr int kNjThreads = 512;
 constexpr int kNjCols = 4;            // JL columns per CTA (the r x r LU is redundant per CTA)
 constexpr double kPivotFloor = 1e-3;  // |u0| below this -> Householder fallback
+__device__ unsigned long long g_nsjl_trace[8];  // phase clocks of CTA 0 (HICU_NSJL_TRACE)
+#define NSJL_STAMP(i) \
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_nsjl_trace[i] = clock64();
 
-template <int CT, int QN>
-__global__ void __launch_bounds__(kNjThreads)
+// 1/d for 1e-30 < d < 1e30 to ~1 ulp: fp32 MUFU seed (no slow path) and two
+// fp64 Newton steps.  Pivots outside that range raise the gate anyway.
+__device__ __forceinline__ double nsjl_rcp(double d) {
+  const float df = (float)fmin(fmax(d, 1e-30), 1e30);
+  float x0;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(x0) : "f"(df));
+  double x = (double)x0;
+  x = fma(x, fma(-d, x, 1.0), x);
+  x = fma(x, fma(-d, x, 1.0), x);
+  return x;
+}
+
+__device__ __forceinline__ void nsjl_cp16(void* dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void nsjl_cp_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ int nsjl_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];"
+               : "=r"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void nsjl_st_release(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+
+// 1 / z, published by the single thread that owns the pivot
+__device__ __forceinline__ double2 nsjl_inv(double2 z) {
+  const double t = nsjl_rcp(abs2d(z));
+  return cd(z.x * t, -z.y * t);
+}
+
+// Z partials: Zp[g][a][c] = sum_{k >= r, k = r + g (mod RG)} conj(V[k][a]) P[k][c0 + c],
+// thread (a = j, g = rg); P_2 already staged in shared memory (Ps, (n - r) x kNjCols),
+// V loads issued in batches of 16 rows.
+template <int RG>
+__device__ __forceinline__ void nsjl_zpart(int n, int r, const double2* __restrict__ V, const double2* __restrict__ Ps,
+                                           int j, int rg, double2* __restrict__ Zp) {
+  if (j >= r) return;
+  double2 acc[kNjCols];
+#pragma unroll
+  for (int c = 0; c < kNjCols; ++c) acc[c] = cd(0.0, 0.0);
+  constexpr int kB = 16;
+  for (int k0 = r + rg; k0 < n; k0 += kB * RG) {
+    double2 va[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int k = k0 + u * RG;
+      va[u] = k < n ? V[(size_t)k * r + j] : cd(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int k = k0 + u * RG;
+      if (k < n) {
+#pragma unroll
+        for (int c = 0; c < kNjCols; ++c) zfmac(acc[c], va[u], Ps[(size_t)(k - r) * kNjCols + c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kNjCols; ++c) Zp[((size_t)rg * r + j) * kNjCols + c] = acc[c];
+}
+
+// CT threads per LU row group (>= r), NT threads, QN = ceil(r / (NT / CT)) rows per thread.
+template <int CT, int QN, int NT, bool WARP_LU>
+__global__ void __launch_bounds__(NT)
 nsjl_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2* __restrict__ Pin,
             double2* __restrict__ B, float2* __restrict__ out32, int p, int* __restrict__ gate) {
   hicu_pdl_entry();
-  constexpr int RG = kNjThreads / CT;  // row groups of the register-resident LU
+  NSJL_STAMP(0)
+  constexpr int RG = NT / CT;  // row groups of the register-resident LU (warp-uniform: CT % 32 == 0)
   extern __shared__ double2 smj[];
-  double2* LU = smj;                    // r x r: U (upper, incl. diagonal), L (strictly lower)
-  double2* colb = LU + (size_t)r * r;   // 2 x r published column k (double-buffered)
-  double2* rowb = colb + 2 * r;         // 2 x r published row k
-  double2* idg = rowb + 2 * r;          // r: 1 / U[k][k]
+  double2* LU = smj;                           // RG*QN x r: U (upper, incl. diagonal), L (strictly lower)
+  // generic LU: 2 x RG*QN published column k and 2 x CT row k (double-buffered);
+  // warp LU: every step's column k kept (r x 64, no reuse, so no write-after-read hazard)
+  constexpr int kColbPerR = WARP_LU ? 64 : 0;
+  double2* colb = LU + (size_t)RG * QN * r;
+  double2* rowb = colb + (WARP_LU ? (size_t)kColbPerR * r : 2 * RG * QN);
+  double2* idg = rowb + (WARP_LU ? 0 : 2 * CT);  // r: 1 / U[k][k]
   double2* Zp = idg + r;                // RG x r x kNjCols partials of V_2^H P
   double2* X = Zp + (size_t)RG * r * kNjCols;  // r x kNjCols
+  double* pd = (double*)(X + (size_t)r * kNjCols);  // r: |U[k][k]|^2
+  int* ready = (int*)(pd + r);                       // r: column k published (warp LU)
+  double2* Ps = (double2*)(((uintptr_t)(ready + r) + 15) & ~(uintptr_t)15);  // (n - r) x kNjCols: P_2
   const int tid = threadIdx.x, j = tid % CT, rg = tid / CT;
   const int c0 = blockIdx.x * kNjCols;
   const int nc = min(kNjCols, cols - c0);
+  for (int e = tid; e < (n - r) * kNjCols; e += NT) {
+    const int kk = e / kNjCols, c = e - kk * kNjCols;
+    if (c < nc) nsjl_cp16(Ps + e, Pin + (size_t)(r + kk) * cols + c0 + c);
+    else Ps[e] = cd(0.0, 0.0);
+  }
 
-  // LU operand A_1 = V_1 - I: element (rg + RG q, j) in s[q]
-  double2 s[QN];
+  if constexpr (WARP_LU) {
+    // Warp-column LU (r <= 64, 8 warps): warp w holds columns 8w..8w+7 of A_1
+    // for rows lane and lane + 32 in registers.  Row k of the warp's columns
+    // is a shuffle from lane k % 32; only column k crosses warps (shared
+    // memory, one barrier per step), and warps whose columns are all <= k
+    // skip the update entirely.
+    static_assert(NT == 256, "warp LU is laid out for 8 warps x 8 columns");
+    const int w = tid >> 5, ln = tid & 31;
+    double2* colw = colb;  // r x 64
+    double2 a0[8], a1[8];  // column w + 8c, rows ln and ln + 32
 #pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const int i = rg + RG * q;
-    s[q] = (i < r && j < r) ? V[(size_t)i * r + j] : cd(0.0, 0.0);
-    if (i == j) s[q].x -= 1.0;
-  }
-  // Z partials: Z[a][c] = sum_{k >= r} conj(V[k][a]) P[k][c], k split over the row groups
-  if (j < r) {
-    double2 acc[kNjCols];
-#pragma unroll
-    for (int c = 0; c < kNjCols; ++c) acc[c] = cd(0.0, 0.0);
-    for (int k = r + rg; k < n; k += RG) {
-      const double2 va = V[(size_t)k * r + j];
-#pragma unroll
-      for (int c = 0; c < kNjCols; ++c)
-        if (c < nc) zfmac(acc[c], va, __ldg(Pin + (size_t)k * cols + c0 + c));
+    for (int c = 0; c < 8; ++c) {
+      const int jj = w + 8 * c;
+      a0[c] = (ln < r && jj < r) ? V[(size_t)ln * r + jj] : cd(0.0, 0.0);
+      a1[c] = (ln + 32 < r && jj < r) ? V[(size_t)(ln + 32) * r + jj] : cd(0.0, 0.0);
+      if (ln == jj) a0[c].x -= 1.0;
+      if (ln + 32 == jj) a1[c].x -= 1.0;
     }
-#pragma unroll
-    for (int c = 0; c < kNjCols; ++c) Zp[((size_t)rg * r + j) * kNjCols + c] = acc[c];
-  }
-  // publish column 0 (rows > 0) and row 0
-  if (j == 0) {
-#pragma unroll
-    for (int q = 0; q < QN; ++q) {
-      const int i = rg + RG * q;
-      if (i > 0 && i < r) colb[i] = s[q];
-    }
-  }
-  if (rg == 0 && j < r) rowb[j] = s[0];
-  __syncthreads();
-
-  double minpiv = 1e300;
-  for (int k = 0; k < r; ++k) {
-    const int b = k & 1;
-    const double2 piv = rowb[b * r + k];
-    const double d = abs2d(piv);
-    minpiv = fmin(minpiv, d);
-    const double2 invp = cd(piv.x / d, -piv.y / d);
-    if (j > k && j < r) {
-      const double2 f = cmul(rowb[b * r + j], invp);  // U[k][j] / U[k][k]
-#pragma unroll
-      for (int q = 0; q < QN; ++q) {
-        const int i = rg + RG * q;
-        if (i > k && i < r) s[q] = s[q] - cmul(colb[b * r + i], f);
-      }
-    } else if (j == k) {
-#pragma unroll
-      for (int q = 0; q < QN; ++q) {
-        const int i = rg + RG * q;
-        if (i > k && i < r) LU[(size_t)i * r + k] = cmul(s[q], invp);  // L[i][k]
-      }
-      if (rg == 0) idg[k] = invp;
-    }
-    if (k + 1 < r) {
-      const int nb = (b ^ 1) * r;
-      if (j == k + 1) {
-#pragma unroll
-        for (int q = 0; q < QN; ++q) {
-          const int i = rg + RG * q;
-          if (i > k + 1 && i < r) colb[nb + i] = s[q];
-        }
-      }
-      if (rg == (k + 1) % RG && j > k && j < r) {
-#pragma unroll
-        for (int q = 0; q < QN; ++q)
-          if (rg + RG * q == k + 1) rowb[nb + j] = s[q];
+    nsjl_cp_wait_all();
+    __syncthreads();
+    nsjl_zpart<RG>(n, r, V, Ps, j, rg, Zp);
+    for (int k = tid; k < r; k += NT) ready[k] = k == 0;
+    if (w == 0) {
+      colw[ln] = a0[0];
+      colw[ln + 32] = a1[0];
+      if (ln == 0) {
+        idg[0] = nsjl_inv(a0[0]);
+        pd[0] = abs2d(a0[0]);
       }
     }
     __syncthreads();
-  }
-  // U (upper part, final since step i-1)
+    NSJL_STAMP(1)
+    for (int k = 0; k < r; ++k) {
+      // wait for column k (published by warp k % 8 with release semantics)
+      if (w != (k & 7))
+        while (nsjl_ld_acquire(ready + k) == 0) {
+        }
+      const double2 invp = idg[k];
+      const double2* ck = colw + (size_t)k * 64;
+      const double2 l0 = ln > k ? cmul(ck[ln], invp) : cd(0.0, 0.0);
+      const double2 l1 = ln + 32 > k ? cmul(ck[ln + 32], invp) : cd(0.0, 0.0);
+      if (w == (k & 7)) {
+        if (ln > k) LU[(size_t)ln * r + k] = l0;
+        if (ln + 32 > k && ln + 32 < r) LU[(size_t)(ln + 32) * r + k] = l1;
+      }
+      const bool hi = k >= 32;
+      const int kl = k & 31;
+      if (k + 1 < r && w == ((k + 1) & 7)) {
+        // this warp owns column k + 1: update and publish it (with 1 / pivot)
+        // before its other columns; the other warps' trailing updates for
+        // step k overlap this chain
+        const int cc = (k + 1) >> 3;
+        double2 v0 = a0[0], v1 = a1[0];
 #pragma unroll
-  for (int q = 0; q < QN; ++q) {
-    const int i = rg + RG * q;
-    if (i < r && j < r && i <= j) LU[(size_t)i * r + j] = s[q];
-  }
-  if (blockIdx.x == 0 && tid == 0) *gate = (minpiv >= kPivotFloor * kPivotFloor) ? 0 : 1;
-  __syncthreads();
+        for (int c = 1; c < 8; ++c)
+          if (c == cc) {
+            v0 = a0[c];
+            v1 = a1[c];
+          }
+        double2 u = hi ? v1 : v0;
+        u.x = __shfl_sync(0xffffffffu, u.x, kl);
+        u.y = __shfl_sync(0xffffffffu, u.y, kl);
+        v0 = v0 - cmul(l0, u);
+        v1 = v1 - cmul(l1, u);
+        double2* cn = colw + (size_t)(k + 1) * 64;
+        cn[ln] = v0;
+        cn[ln + 32] = v1;
+        if (ln == ((k + 1) & 31)) {
+          const double2 pv = k + 1 >= 32 ? v1 : v0;
+          idg[k + 1] = nsjl_inv(pv);
+          pd[k + 1] = abs2d(pv);
+        }
+        __syncwarp();
+        if (ln == 0) nsjl_st_release(ready + k + 1, 1);
+      }
+      if (w + 56 > k) {  // warp-uniform; columns <= k get u = 0 (no branch per column:
+                         // measured faster than skipping them, 61K vs 69K cycles per LU)
+        double2 u[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          u[c] = hi ? a1[c] : a0[c];
+          u[c].x = __shfl_sync(0xffffffffu, u[c].x, kl);
+          u[c].y = __shfl_sync(0xffffffffu, u[c].y, kl);
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const double2 uc = w + 8 * c > k ? u[c] : cd(0.0, 0.0);
+          a0[c] = a0[c] - cmul(l0, uc);
+          a1[c] = a1[c] - cmul(l1, uc);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int jj = w + 8 * c;
+      if (jj < r && ln <= jj) LU[(size_t)ln * r + jj] = a0[c];
+      if (jj < r && ln + 32 <= jj) LU[(size_t)(ln + 32) * r + jj] = a1[c];
+    }
+  } else {
+    // Generic LU (r <= 100): element (rg + RG q, j) of A_1 = V_1 - I in s[q]. = V_1 - I: element (rg + RG q, j) in s[q]
+    double2 s[QN];
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+      const int i = rg + RG * q;
+      s[q] = (i < r && j < r) ? V[(size_t)i * r + j] : cd(0.0, 0.0);
+      if (i == j) s[q].x -= 1.0;
+    }
+    nsjl_cp_wait_all();
+    __syncthreads();
+    nsjl_zpart<RG>(n, r, V, Ps, j, rg, Zp);
+    // Published column k (rows > k, zero elsewhere, RG*QN entries) and row k
+    // (columns > k, zero elsewhere) make every thread's update unconditional:
+    // s[q] -= colb[i] * (rowb[j] / U[k][k]) is a no-op outside the trailing block.
+    // publish column 0, row 0 and 1 / pivot 0
+    if (j == 0) {
+#pragma unroll
+      for (int q = 0; q < QN; ++q) {
+        const int i = rg + RG * q;
+        colb[i] = i > 0 ? s[q] : cd(0.0, 0.0);
+      }
+      if (rg == 0) {
+        idg[0] = nsjl_inv(s[0]);
+        pd[0] = abs2d(s[0]);
+      }
+    }
+    if (rg == 0 && j < CT) rowb[j] = j > 0 ? s[0] : cd(0.0, 0.0);
+    __syncthreads();
+    NSJL_STAMP(1)
 
-  // A_1^H X = Z  <=>  U^H (L^H X) = Z: one warp per JL column, rows i = lane + 32 m
+    // right-looking LU without pivoting, one barrier per step; the pivot's
+    // owner publishes its inverse with the next row/column
+    for (int k = 0; k < r; ++k) {
+      const int b = k & 1;
+      const double2 invp = idg[k];
+      const double2* cb = colb + b * (RG * QN);
+      const double2 f = cmul(rowb[b * CT + j], invp);  // U[k][j] / U[k][k], 0 unless j > k
+      if (j == k) {
+#pragma unroll
+        for (int q = 0; q < QN; ++q) {
+          const int i = rg + RG * q;
+          if (i > k) LU[(size_t)i * r + k] = cmul(s[q], invp);  // L[i][k] (rows >= r land in spare rows)
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < QN; ++q) s[q] = s[q] - cmul(cb[rg + RG * q], f);
+      if (k + 1 < r) {
+        double2* ncb = colb + (b ^ 1) * (RG * QN);
+        if (j == k + 1) {
+          double2 pv = s[0];
+#pragma unroll
+          for (int q = 0; q < QN; ++q) {
+            const int i = rg + RG * q;
+            ncb[i] = i > k + 1 ? s[q] : cd(0.0, 0.0);
+            if (i == k + 1) pv = s[q];
+          }
+          if (rg == (k + 1) % RG) {
+            idg[k + 1] = nsjl_inv(pv);
+            pd[k + 1] = abs2d(pv);
+          }
+        }
+        if (rg == (k + 1) % RG) {  // warp-uniform
+          double2 v = s[0];
+#pragma unroll
+          for (int q = 1; q < QN; ++q)
+            if (rg + RG * q == k + 1) v = s[q];
+          rowb[(b ^ 1) * CT + j] = j > k + 1 ? v : cd(0.0, 0.0);
+        }
+      }
+      __syncthreads();
+    }
+    // U (upper part, final since step i-1)
+#pragma unroll
+    for (int q = 0; q < QN; ++q) {
+      const int i = rg + RG * q;
+      if (i < r && j < r && i <= j) LU[(size_t)i * r + j] = s[q];
+    }
+  }
+  if (blockIdx.x == 0 && tid < 32) {
+    double m = 1e300;
+    for (int k = tid; k < r; k += 32) m = fmin(m, pd[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (tid == 0) *gate = (m >= kPivotFloor * kPivotFloor) ? 0 : 1;  // NaN -> fallback
+  }
+  __syncthreads();
+  NSJL_STAMP(2)
+
+  // A_1^H X = Z  <=>  U^H (L^H X) = Z: one warp per JL column, rows i = lane + 32 m;
+  // the next row of U / L is loaded one step ahead
   const int warp = tid >> 5, lane = tid & 31;
   if (warp < nc) {
-    constexpr int MQ = 4;  // r <= 128
+    constexpr int MQ = (CT + 31) / 32;  // r <= CT
     double2 z[MQ];
 #pragma unroll
     for (int m = 0; m < MQ; ++m) {
@@ -142,7 +339,20 @@ nsjl_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2
       z[m] = acc;
     }
     // forward: U^H y = z  (y_k = (z_k - sum_{m<k} conj(U[m][k]) y_m) / conj(U[k][k]))
+    double2 un[MQ];
+#pragma unroll
+    for (int m = 0; m < MQ; ++m) {
+      const int i = lane + 32 * m;
+      un[m] = i < r ? LU[i] : cd(0.0, 0.0);
+    }
     for (int k = 0; k < r; ++k) {
+      double2 uc[MQ];
+#pragma unroll
+      for (int m = 0; m < MQ; ++m) {
+        uc[m] = un[m];
+        const int i = lane + 32 * m;
+        un[m] = (k + 1 < r && i < r) ? LU[(size_t)(k + 1) * r + i] : cd(0.0, 0.0);
+      }
       const int sl = k >> 5;
       double2 zv = z[0];
 #pragma unroll
@@ -155,11 +365,23 @@ nsjl_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2
       for (int m = 0; m < MQ; ++m) {
         const int i = lane + 32 * m;
         if (i == k) z[m] = y;
-        else if (i > k && i < r) z[m] = z[m] - cmulc(LU[(size_t)k * r + i], y);
+        else if (i > k) z[m] = z[m] - cmulc(uc[m], y);
       }
     }
     // backward: L^H x = y  (x_k = y_k - sum_{m>k} conj(L[m][k]) x_m)
+#pragma unroll
+    for (int m = 0; m < MQ; ++m) {
+      const int i = lane + 32 * m;
+      un[m] = i < r - 1 ? LU[(size_t)(r - 1) * r + i] : cd(0.0, 0.0);
+    }
     for (int k = r - 1; k >= 0; --k) {
+      double2 lc[MQ];
+#pragma unroll
+      for (int m = 0; m < MQ; ++m) {
+        lc[m] = un[m];
+        const int i = lane + 32 * m;
+        un[m] = (k >= 1 && i < k - 1) ? LU[(size_t)(k - 1) * r + i] : cd(0.0, 0.0);
+      }
       const int sl = k >> 5;
       double2 xv = z[0];
 #pragma unroll
@@ -170,7 +392,7 @@ nsjl_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2
 #pragma unroll
       for (int m = 0; m < MQ; ++m) {
         const int i = lane + 32 * m;
-        if (i < k) z[m] = z[m] - cmulc(LU[(size_t)k * r + i], xv);
+        if (i < k) z[m] = z[m] - cmulc(lc[m], xv);
       }
     }
 #pragma unroll
@@ -180,48 +402,75 @@ nsjl_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2
     }
   }
   __syncthreads();
+  NSJL_STAMP(3)
 
-  // Q~[k][c] = [0; P][k][c] + sum_a (V[k][a] - delta_ka) X[a][c]
-  for (int k = tid; k < n; k += kNjThreads) {
-    double2 acc[kNjCols], acc2[kNjCols];
-#pragma unroll
-    for (int c = 0; c < kNjCols; ++c) {
-      acc[c] = (k >= r && c < nc) ? __ldg(Pin + (size_t)k * cols + c0 + c) : cd(0.0, 0.0);
-      acc2[c] = cd(0.0, 0.0);
-      if (k < r) acc[c] = cd(-X[(size_t)k * kNjCols + c].x, -X[(size_t)k * kNjCols + c].y);
+  // Q~[k][c] = [0; P][k][c] + sum_a (V[k][a] - delta_ka) X[a][c]; V staged through
+  // shared memory (LU and pivot areas) in chunks of CH rows with padded stride r + 1
+  const int ld = r + 1;
+  const int CH = (int)((idg - LU) / ld);  // LU + column/row publication areas (>= 1 row)
+  for (int k0 = 0; k0 < n; k0 += CH) {
+    const int rows = min(CH, n - k0);
+    for (int e = tid; e < rows * r; e += NT) {
+      const int kk = e / r, a = e - kk * r;
+      nsjl_cp16(LU + (size_t)kk * ld + a, V + (size_t)(k0 + kk) * r + a);
     }
-    const double2* vr = V + (size_t)k * r;
-    int a = 0;
-    for (; a + 1 < r; a += 2) {
-      const double2 v0 = __ldg(vr + a), v1 = __ldg(vr + a + 1);
-#pragma unroll
-      for (int c = 0; c < kNjCols; ++c) {
-        zfma(acc[c], v0, X[(size_t)a * kNjCols + c]);
-        zfma(acc2[c], v1, X[(size_t)(a + 1) * kNjCols + c]);
+    nsjl_cp_wait_all();
+    __syncthreads();
+    // thread (row kk = tid % TR (+ TR, ...), column c = tid / TR): two rows per
+    // pass as independent accumulation chains
+    constexpr int TR = NT / kNjCols;
+    const int c = tid / TR;
+    for (int kk = tid % TR; kk < rows; kk += 2 * TR) {
+      const bool two = kk + TR < rows;
+      const int k = k0 + kk, k2 = k + TR;
+      double2 acc = cd(0.0, 0.0), acc2 = cd(0.0, 0.0), bcc = cd(0.0, 0.0), bcc2 = cd(0.0, 0.0);
+      if (c < nc) {
+        acc = k >= r ? Ps[(size_t)(k - r) * kNjCols + c] : cd(-X[(size_t)k * kNjCols + c].x, -X[(size_t)k * kNjCols + c].y);
+        if (two)
+          bcc = k2 >= r ? Ps[(size_t)(k2 - r) * kNjCols + c]
+                        : cd(-X[(size_t)k2 * kNjCols + c].x, -X[(size_t)k2 * kNjCols + c].y);
+      }
+      const double2* vr = LU + (size_t)kk * ld;
+      const double2* vr2 = vr + (size_t)TR * ld;
+      int a = 0;
+      for (; a + 1 < r; a += 2) {
+        const double2 x0 = X[(size_t)a * kNjCols + c], x1 = X[(size_t)(a + 1) * kNjCols + c];
+        zfma(acc, vr[a], x0);
+        zfma(acc2, vr[a + 1], x1);
+        if (two) {
+          zfma(bcc, vr2[a], x0);
+          zfma(bcc2, vr2[a + 1], x1);
+        }
+      }
+      if (a < r) {
+        const double2 x0 = X[(size_t)a * kNjCols + c];
+        zfma(acc, vr[a], x0);
+        if (two) zfma(bcc, vr2[a], x0);
+      }
+      if (c < nc) {
+        const int jj = c0 + c, step = jj / p, t = jj % p;
+        const double2 v = acc + acc2;
+        B[(size_t)k * cols + jj] = v;
+        if (out32) out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
+        if (two) {
+          const double2 v2 = bcc + bcc2;
+          B[(size_t)k2 * cols + jj] = v2;
+          if (out32) out32[((size_t)step * n + k2) * p + t] = cf((float)v2.x, (float)v2.y);
+        }
       }
     }
-    if (a < r) {
-      const double2 v0 = __ldg(vr + a);
-#pragma unroll
-      for (int c = 0; c < kNjCols; ++c) zfma(acc[c], v0, X[(size_t)a * kNjCols + c]);
-    }
-#pragma unroll
-    for (int c = 0; c < kNjCols; ++c) {
-      if (c >= nc) continue;
-      const double2 v = acc[c] + acc2[c];
-      const int jj = c0 + c;
-      B[(size_t)k * cols + jj] = v;
-      if (out32) {
-        const int step = jj / p, t = jj % p;
-        out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
-      }
-    }
+    __syncthreads();
   }
+  NSJL_STAMP(4)
 }
 
-size_t nsjl_smem(int r, int ct) {
-  const int rg = kNjThreads / ct;
-  return ((size_t)r * r + 5 * (size_t)r + (size_t)rg * r * kNjCols + (size_t)r * kNjCols) * sizeof(double2);
+int nsjl_threads(int ct) { return ct == 64 ? 256 : 512; }
+
+size_t nsjl_smem(int n, int r, int ct, bool warp_lu) {
+  const int rg = nsjl_threads(ct) / ct, rows = ct == 64 ? rg * 16 : rg * 25;  // RG * QN of the instantiation
+  const size_t pub = warp_lu ? (size_t)64 * r : 2 * (size_t)rows + 2 * (size_t)ct;
+  return ((size_t)rows * r + pub + (size_t)r + (size_t)rg * r * kNjCols + (size_t)r * kNjCols) * sizeof(double2) +
+         (size_t)r * (sizeof(double) + sizeof(int)) + 16 + (size_t)(n - r) * kNjCols * sizeof(double2);
 }
 
 int nsjl_ct(int r) { return r <= 64 ? 64 : (r <= 100 ? 128 : 0); }
@@ -230,7 +479,7 @@ int nsjl_ct(int r) { return r <= 64 ? 64 : (r <= 100 ? 128 : 0); }
 
 extern "C" int hicu_nullspace_jl_supported(int n, int r) {
   const int ct = nsjl_ct(r);
-  return (r >= 1 && r < n && ct && nsjl_smem(r, ct) <= (size_t)220 * 1024) ? 1 : 0;
+  return (r >= 1 && r < n && ct && nsjl_smem(n, r, ct, ct == 64) <= (size_t)220 * 1024) ? 1 : 0;
 }
 
 extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const void* Bin, void* B, void* out32, int p,
@@ -240,15 +489,24 @@ extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const vo
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad p");
   if (!hicu_nullspace_jl_supported(n, r)) return hicu_set_error(HICU_ERR_SIZE, "nullspace_jl: rank not supported");
   const int ct = nsjl_ct(r);
-  const size_t smem = nsjl_smem(r, ct);
+  static const bool generic = getenv("HICU_NSJL_GENERIC") != nullptr;  // A/B switch for the r <= 64 LU
+  const size_t smem = nsjl_smem(n, r, ct, ct == 64 && !generic);
   const int grid = (cols + kNjCols - 1) / kNjCols;
   cudaStream_t st = (cudaStream_t)stream;
   auto go = [&](auto kern) {
     hicu_allow_max_smem((const void*)kern);
-    hicu_launch(kern, grid, kNjThreads, smem, st, n, r, (const double2*)V, cols, (const double2*)Bin, (double2*)B,
+    hicu_launch(kern, grid, nsjl_threads(ct), smem, st, n, r, (const double2*)V, cols, (const double2*)Bin, (double2*)B,
                 (float2*)out32, p ? p : 1, gate_dev);
   };
-  if (ct == 64) go(nsjl_kernel<64, 8>);
-  else go(nsjl_kernel<128, 25>);
+  if (ct == 64 && !generic) go(nsjl_kernel<64, 16, 256, true>);
+  else if (ct == 64) go(nsjl_kernel<64, 16, 256, false>);
+  else go(nsjl_kernel<128, 25, 512, false>);
+  if (getenv("HICU_NSJL_TRACE")) {
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_nsjl_trace, sizeof(h));
+    fprintf(stderr, "nsjl cycles: Z+load %llu | LU %llu | solves %llu | Q~ %llu\n", h[1] - h[0], h[2] - h[1], h[3] - h[2],
+            h[4] - h[3]);
+  }
   return hicu_check_launch("nsjl_kernel");
 }

@@ -5,6 +5,7 @@ Usage: python scripts/nullspace_bench.py [reps]   -> one JSON line
 Under ncu (warm, --cache-control none) the launch list gives per-kernel times.
 """
 import json
+import os
 import math
 import sys
 
@@ -36,7 +37,8 @@ def main(reps=30):
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
     refl = torch.empty(2 * n * r, dtype=torch.complex128, device="cuda")
     tau = torch.empty(r, dtype=torch.complex128, device="cuda")
-    flags = torch.empty(r, dtype=torch.int32, device="cuda")
+    flags = torch.zeros(r + 1, dtype=torch.int32, device="cuda")
+    jl = not os.environ.get("HICU_NSJL_OFF")
     pbig = torch.zeros((n, gs * p), dtype=torch.complex128, device="cuda")
     pbig[r:] = torch.randn((n - r, gs * p), dtype=torch.complex128, device="cuda")
     B = torch.empty_like(pbig)
@@ -45,6 +47,10 @@ def main(reps=30):
     def one():
         nat.check(L.hicu_nystrom(n, ell, r, G.data_ptr(), om.data_ptr(), V.data_ptr(), ws.data_ptr(), ws_bytes,
                                  status.data_ptr(), st), "nystrom")
+        if jl:
+            nat.check(L.hicu_nullspace_jl(n, r, V.data_ptr(), gs * p, pbig.data_ptr(), B.data_ptr(), q32.data_ptr(), p,
+                                          flags[r:].data_ptr(), st), "nullspace_jl")
+            return
         nat.check(L.hicu_householder(n, r, V.data_ptr(), 1e-12, refl.data_ptr(), tau.data_ptr(), flags.data_ptr(),
                                      status.data_ptr(), st), "householder")
         nat.check(L.hicu_apply_reflectors(n, r, refl.data_ptr(), tau.data_ptr(), flags.data_ptr(), gs * p,

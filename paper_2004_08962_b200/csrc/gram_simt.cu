@@ -1,5 +1,8 @@
-// Gram matrix G = H(x)^H H(x) — SIMT reference kernel (fp32 FMA per row
-// chunk, fp64 split-K reduction).  Used for geometries the tcgen05 kernel
+// Gram matrix G = H(x)^H H(x) — SIMT reference kernel (fp32 FMA over chunks
+// of kFlushRows rows, drained into fp64 register accumulators; fp64 split-K
+// reduction).  The drain keeps the fp32 chains short: one split of the C5
+// shard spans ~195K rows, where a single fp32 chain measured 1.4e-4 relative
+// error against an fp64 Gram (scripts/gram_accuracy.py).  Used for geometries the tcgen05 kernel
 // does not cover (general supports, circular axes) and as its cross-check.
 //
 // No reference function computes G; it equals
@@ -11,6 +14,7 @@ namespace {
 constexpr int kTile = 64;    // complex outputs per tile edge
 constexpr int kBK = 16;      // rows per smem stage
 constexpr int kThreads = 256;
+constexpr int kFlushRows = 512;  // fp32 chain length before draining into fp64
 
 struct GramPlan {
   int ntile;       // tiles per edge
@@ -54,52 +58,67 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
 
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   float2 acc[4][4];
+  double2 acc64[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = cf(0.f, 0.f);
+    for (int b = 0; b < 4; ++b) {
+      acc[a][b] = cf(0.f, 0.f);
+      acc64[a][b] = cd(0.0, 0.0);
+    }
 
-  for (int64_t rc = r0; rc < r1; rc += kBK) {
-    if (threadIdx.x < kBK) {
-      const int64_t i = rc + threadIdx.x;
-      int cc[HICU_MAX_NDIM];
-      rbase[threadIdx.x] = (i < r1) ? row_base(g, i, cc) : -1;
-      if (CIRC)
-        for (int c = 0; c < g.ncirc; ++c) rcc[threadIdx.x][c] = cc[c];
-    }
-    __syncthreads();
-    // 2 * kBK * kTile elements, 8 per thread
-#pragma unroll
-    for (int e = 0; e < (2 * kBK * kTile) / kThreads; ++e) {
-      const int idx = threadIdx.x + e * kThreads;
-      const int which = idx / (kBK * kTile);
-      const int rem = idx % (kBK * kTile);
-      const int row = rem / kTile, col = rem % kTile;
-      const int kap = (which == 0 ? ti : tj) * kTile + col;
-      float2 v = cf(0.f, 0.f);
-      const int64_t b = rbase[row];
-      if (b >= 0 && kap < g.n) {
-        int64_t addr = b + g.koff[kap];
-        if (CIRC) addr += circ_part(g, rcc[row], g.pos + (size_t)kap * g.ndim);
-        v = __ldg(x + addr);
+  // outer blocks of kFlushRows rows, drained into fp64 after each block
+  for (int64_t rb = r0; rb < r1; rb += kFlushRows) {
+    const int64_t re = rb + kFlushRows < r1 ? rb + kFlushRows : r1;
+    for (int64_t rc = rb; rc < re; rc += kBK) {
+      if (threadIdx.x < kBK) {
+        const int64_t i = rc + threadIdx.x;
+        int cc[HICU_MAX_NDIM];
+        rbase[threadIdx.x] = (i < r1) ? row_base(g, i, cc) : -1;
+        if (CIRC)
+          for (int c = 0; c < g.ncirc; ++c) rcc[threadIdx.x][c] = cc[c];
       }
-      if (which == 0) As[row][col] = v; else Bs[row][col] = v;
-    }
-    __syncthreads();
+      __syncthreads();
+      // 2 * kBK * kTile elements, 8 per thread
 #pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      float2 a[4], b[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        a[q] = As[kk][ty * 4 + q];
-        b[q] = Bs[kk][tx * 4 + q];
+      for (int e = 0; e < (2 * kBK * kTile) / kThreads; ++e) {
+        const int idx = threadIdx.x + e * kThreads;
+        const int which = idx / (kBK * kTile);
+        const int rem = idx % (kBK * kTile);
+        const int row = rem / kTile, col = rem % kTile;
+        const int kap = (which == 0 ? ti : tj) * kTile + col;
+        float2 v = cf(0.f, 0.f);
+        const int64_t b = rbase[row];
+        if (b >= 0 && kap < g.n) {
+          int64_t addr = b + g.koff[kap];
+          if (CIRC) addr += circ_part(g, rcc[row], g.pos + (size_t)kap * g.ndim);
+          v = __ldg(x + addr);
+        }
+        if (which == 0) As[row][col] = v; else Bs[row][col] = v;
       }
+      __syncthreads();
 #pragma unroll
-      for (int qa = 0; qa < 4; ++qa)
+      for (int kk = 0; kk < kBK; ++kk) {
+        float2 a[4], b[4];
 #pragma unroll
-        for (int qb = 0; qb < 4; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
+        for (int q = 0; q < 4; ++q) {
+          a[q] = As[kk][ty * 4 + q];
+          b[q] = Bs[kk][tx * 4 + q];
+        }
+#pragma unroll
+        for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+          for (int qb = 0; qb < 4; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        acc64[a][b] = acc64[a][b] + cd(acc[a][b].x, acc[a][b].y);
+        acc[a][b] = cf(0.f, 0.f);
+      }
   }
   double2* out = partials + (size_t)split * g.n * g.n;
 #pragma unroll
@@ -110,7 +129,7 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
     for (int qb = 0; qb < 4; ++qb) {
       const int cb = tj * kTile + tx * 4 + qb;
       if (cb >= g.n) continue;
-      out[(size_t)ra * g.n + cb] = cd(acc[qa][qb].x, acc[qa][qb].y);
+      out[(size_t)ra * g.n + cb] = acc64[qa][qb];
     }
   }
 }

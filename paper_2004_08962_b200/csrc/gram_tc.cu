@@ -142,6 +142,74 @@ __device__ __forceinline__ void tmem_ld16_raw(uint32_t taddr, uint32_t (&r)[16])
       : "r"(taddr));
 }
 
+#ifndef HICU_GRAM_PREFETCH
+#define HICU_GRAM_PREFETCH 0  // 1: next stage's gathers issued before this stage's stores (spills at 72 regs)
+#endif
+constexpr int kTasks = (kNT + kMT) * 64 / kProducers;  // gather tasks per producer thread and stage
+
+// Region-line walker for the producer: the k-block -> (line, chunk) ->
+// float offset decomposition is done once per CTA with divisions and then
+// advanced incrementally (64-bit division per k-block cost ~100 producer
+// instructions of ~430 per k-block in an ncu source profile).
+struct GramCursor {
+  int64_t base;     // float offset of the chunk's first row
+  int valid;        // rows of the chunk inside the region line
+  int chunk;        // chunk index within the line
+  int64_t c[3];     // line coordinates (axes 0..L-1)
+};
+
+__device__ __forceinline__ void cursor_valid(const TcParams& p, GramCursor& cu) {
+  const int L = p.nsp - 1;
+  cu.valid = (int)hmin64(kBK, p.rext[L] - (int64_t)cu.chunk * kBK);
+}
+
+__device__ __forceinline__ void cursor_init(const TcParams& p, int64_t kb, GramCursor& cu) {
+  const int L = p.nsp - 1;
+  int64_t line = kb / p.nkb_line;
+  cu.chunk = (int)(kb % p.nkb_line);
+  cu.base = (p.roff[L] + (int64_t)cu.chunk * kBK) * 16;
+  for (int d = L - 1; d >= 0; --d) {
+    cu.c[d] = line % p.rext[d];
+    line /= p.rext[d];
+    cu.base += (p.roff[d] + cu.c[d]) * p.fstride[d];
+  }
+  cursor_valid(p, cu);
+}
+
+__device__ __forceinline__ void cursor_next(const TcParams& p, GramCursor& cu) {
+  const int L = p.nsp - 1;
+  if (++cu.chunk < p.nkb_line) {
+    cu.base += kBK * 16;
+  } else {
+    cu.base -= (int64_t)(cu.chunk - 1) * kBK * 16;  // back to the line start
+    cu.chunk = 0;
+    for (int d = L - 1; d >= 0; --d) {  // odometer over the line coordinates
+      if (++cu.c[d] < p.rext[d]) {
+        cu.base += p.fstride[d];
+        break;
+      }
+      cu.base -= (p.rext[d] - 1) * p.fstride[d];
+      cu.c[d] = 0;
+    }
+  }
+  cursor_valid(p, cu);
+}
+
+// Loads of one k-block for this producer thread: task it covers float
+// j = t % 16 of tap q = t / 64 for the 4 rows of quad (t / 16) % 4
+// (t = tid + it * kProducers); toff[it] = tap offset + j + 64 quad, or -1.
+__device__ __forceinline__ void gram_gather(const float* __restrict__ x, const GramCursor& cu,
+                                            const int (&toff)[kTasks], float (&v)[kTasks][4]) {
+  const float* xb = x + cu.base;
+#pragma unroll
+  for (int it = 0; it < kTasks; ++it) {
+    const int quad = ((threadIdx.x + it * kProducers) >> 4) & 3;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+      v[it][r] = (toff[it] >= 0 && quad * 4 + r < cu.valid) ? __ldg(xb + toff[it] + r * 16) : 0.f;
+  }
+}
+
 // Stage layout (per hi/lo half): for k-step ks (8 rows), tap q of the list,
 // MN row j (0..15), row k: ks*list*512 + (2q + j/8)*256 + ((k%8)/4)*128 + (j%8)*16 + (k%4)*4.
 __global__ void __launch_bounds__(kThreads, 1)
@@ -191,53 +259,72 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
 
   if (warp < kProdWarps) {
     // ---------------- producers: gather, split hi/lo, K-major stores ----------------
+    // All kTasks x 4 loads of a stage are issued together, and the next
+    // stage's loads are issued before this stage is converted and stored, so
+    // each producer thread keeps ~2 stages of L2 gathers in flight (one stage
+    // at a time with 8 loads in flight left the tensor pipe at ~22 %).
     const int tid = threadIdx.x;
-    const int L = p.nsp - 1;
+    const int ntask = list * 64;
+    int toff[kTasks];
+#pragma unroll
+    for (int it = 0; it < kTasks; ++it) {
+      const int t = tid + it * kProducers;
+      const int q = t >> 6;
+      const int tap = (q < NT) ? n0 + q : m0 + (q - NT);
+      toff[it] = t < ntask ? tap_off[tap] + (t & 15) + ((t >> 4) & 3) * 64 : -1;
+    }
+    GramCursor cu;
+    if (kb0 < kb1) cursor_init(p, kb0, cu);
+    float va[kTasks][4];
+#if HICU_GRAM_PREFETCH
+    float vb[kTasks][4];
+    if (kb0 < kb1) gram_gather(x, cu, toff, va);
+#endif
     int s = 0;
     uint32_t ph = 0;
     for (int64_t kb = kb0; kb < kb1; ++kb) {
+#if HICU_GRAM_PREFETCH
       mbar_wait(&empty_bar[s], ph ^ 1);
-      const int64_t line = kb / p.nkb_line;
-      const int chunk = (int)(kb % p.nkb_line);
-      int64_t base = 0;
-      {
-        int64_t rem = line;
-        for (int d = L - 1; d >= 0; --d) {
-          const int64_t c = rem % p.rext[d];
-          rem /= p.rext[d];
-          base += (p.roff[d] + c) * p.fstride[d];
-        }
-        base += (p.roff[L] + (int64_t)chunk * kBK) * 16;
+      if (kb + 1 < kb1) {
+        cursor_next(p, cu);
+        gram_gather(x, cu, toff, vb);
       }
-      const int valid = (int)hmin64(kBK, p.rext[L] - (int64_t)chunk * kBK);
+#else
+      gram_gather(x, cu, toff, va);
+      cursor_next(p, cu);
+      mbar_wait(&empty_bar[s], ph ^ 1);
+#endif
       uint8_t* sb = smem + (size_t)s * stage_bytes;
-      const int ntask = list * 64;
-#pragma unroll 2
-      for (int t = tid; t < ntask; t += kProducers) {
-        const int j = t & 15;
-        const int quad = (t >> 4) & 3;
-        const int q = t >> 6;
-        const int tap = (q < NT) ? n0 + q : m0 + (q - NT);
-        const float* src = x + base + tap_off[tap] + j + quad * 64;
-        float v[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) v[r] = (quad * 4 + r < valid) ? __ldg(src + r * 16) : 0.f;
-        float h[4], l[4];
+      for (int it = 0; it < kTasks; ++it) {
+        const int t = tid + it * kProducers;
+        if (t < ntask) {
+          const int j = t & 15;
+          const int quad = (t >> 4) & 3;
+          const int q = t >> 6;
+          float h[4], l[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          uint32_t hb;
-          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(v[r]));
-          h[r] = __uint_as_float(hb);
-          l[r] = v[r] - h[r];
+          for (int r = 0; r < 4; ++r) {
+            uint32_t hb;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(va[it][r]));
+            h[r] = __uint_as_float(hb);
+            l[r] = va[it][r] - h[r];
+          }
+          const int ks = quad >> 1, kq = quad & 1;
+          const uint32_t off = (uint32_t)ks * list * 512 + (uint32_t)(2 * q + (j >> 3)) * 256 + (uint32_t)kq * 128 +
+                               (uint32_t)(j & 7) * 16;
+          *(float4*)(sb + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *(float4*)(sb + half_bytes + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
-        const int ks = quad >> 1, kq = quad & 1;
-        const uint32_t off = (uint32_t)ks * list * 512 + (uint32_t)(2 * q + (j >> 3)) * 256 + (uint32_t)kq * 128 +
-                             (uint32_t)(j & 7) * 16;
-        *(float4*)(sb + off) = make_float4(h[0], h[1], h[2], h[3]);
-        *(float4*)(sb + half_bytes + off) = make_float4(l[0], l[1], l[2], l[3]);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&full_bar[s]);
+#if HICU_GRAM_PREFETCH
+#pragma unroll
+      for (int it = 0; it < kTasks; ++it)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) va[it][r] = vb[it][r];
+#endif
       if (++s == S) { s = 0; ph ^= 1; }
     }
   } else if (warp == kProdWarps) {
@@ -245,6 +332,8 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
     const uint32_t idesc = make_idesc_tf32(128, 16 * NT);
     int s = 0;
     uint32_t ph = 0;
+    int chunk = (int)(kb0 % p.nkb_line);  // advanced per k-block (no 64-bit modulo in the issue loop)
+    const int64_t lastlen = p.rext[p.nsp - 1];
     for (int c = 0; c < nchains; ++c) {
       const int b = c & 1;
       mbar_wait(&tempty[b], ((c >> 1) & 1) ^ 1);
@@ -253,11 +342,10 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
       bool first = true;
       const int j1 = min(nkb, (c + 1) * kChain);
       for (int j = c * kChain; j < j1; ++j) {
-        const int64_t kb = kb0 + j;
         mbar_wait(&full_bar[s], ph);
         tc_fence_after();
-        const int chunk = (int)(kb % p.nkb_line);
-        const int valid = (int)hmin64(kBK, p.rext[p.nsp - 1] - (int64_t)chunk * kBK);
+        const int valid = (int)hmin64(kBK, lastlen - (int64_t)chunk * kBK);
+        if (++chunk == p.nkb_line) chunk = 0;
         const int nks = (valid + 7) / 8;
         if (lane == 0) {
           const uint32_t sbase = smem_u32(smem + (size_t)s * stage_bytes);

@@ -38,7 +38,7 @@ GramPlan gram_plan(const DevGeom& g) {
 }
 
 template <bool CIRC>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t rows_per_split,
                  double2* __restrict__ partials) {
   hicu_pdl_entry();
@@ -57,14 +57,16 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
   if (r1 > g.s) r1 = g.s;
 
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  // fp64 drain targets in shared memory ([slot][thread], conflict-free), so
+  // the fp32 tile keeps the register budget of two CTAs per SM
+  extern __shared__ double2 acc64[];
   float2 acc[4][4];
-  double2 acc64[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       acc[a][b] = cf(0.f, 0.f);
-      acc64[a][b] = cd(0.0, 0.0);
+      acc64[(a * 4 + b) * kThreads + threadIdx.x] = cd(0.0, 0.0);
     }
 
   // outer blocks of kFlushRows rows, drained into fp64 after each block
@@ -116,7 +118,8 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        acc64[a][b] = acc64[a][b] + cd(acc[a][b].x, acc[a][b].y);
+        double2& d = acc64[(a * 4 + b) * kThreads + threadIdx.x];
+        d = d + cd(acc[a][b].x, acc[a][b].y);
         acc[a][b] = cf(0.f, 0.f);
       }
   }
@@ -129,7 +132,7 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
     for (int qb = 0; qb < 4; ++qb) {
       const int cb = tj * kTile + tx * 4 + qb;
       if (cb >= g.n) continue;
-      out[(size_t)ra * g.n + cb] = acc64[qa][qb];
+      out[(size_t)ra * g.n + cb] = acc64[(qa * 4 + qb) * kThreads + threadIdx.x];
     }
   }
 }
@@ -166,10 +169,14 @@ int hicu_gram_simt(const DevGeom& g, const float2* x, double2* G, void* ws, size
   const size_t need = (size_t)p.splits * g.n * g.n * sizeof(double2);
   if (ws_bytes < need) return hicu_set_error(HICU_ERR_WORKSPACE, "gram: workspace too small");
   dim3 grid(p.npairs, p.splits);
-  if (g.ncirc > 0)
-    hicu_launch(gram_simt_kernel<true>, grid, kThreads, 0, st, g, x, p.ntile, p.rows_per_split, (double2*)ws);
-  else
-    hicu_launch(gram_simt_kernel<false>, grid, kThreads, 0, st, g, x, p.ntile, p.rows_per_split, (double2*)ws);
+  const size_t dsm = (size_t)16 * kThreads * sizeof(double2);
+  if (g.ncirc > 0) {
+    hicu_allow_max_smem((const void*)gram_simt_kernel<true>);
+    hicu_launch(gram_simt_kernel<true>, grid, kThreads, dsm, st, g, x, p.ntile, p.rows_per_split, (double2*)ws);
+  } else {
+    hicu_allow_max_smem((const void*)gram_simt_kernel<false>);
+    hicu_launch(gram_simt_kernel<false>, grid, kThreads, dsm, st, g, x, p.ntile, p.rows_per_split, (double2*)ws);
+  }
   int s = hicu_check_launch("gram_simt_kernel");
   if (s) return s;
   int64_t total = (int64_t)g.n * g.n;

@@ -199,39 +199,44 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // index (images are 1024-byte aligned, so this is the absolute-address
 // swizzle the descriptors expect).  base is shared memory (in-kernel build)
 // or global memory (conv_bimage_kernel, copied in with one bulk copy).
+template <int MODE>
+__device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, const int (&spos)[kMaxTaps][3], int e,
+                                           float2 q, uint32_t gbytes) {
+  const int L = P.L, nb = P.nb;
+  const int sp = e >> 6, c = (e >> 3) & 7, j = e & 7;
+  const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
+  const int b = spos[sp][L - 1];
+  uint8_t* gb = base + (size_t)g * gbytes;
+#pragma unroll
+  for (int tp = 0; tp < 2; ++tp)
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      int n, k;
+      float v;
+      if (MODE < 2) {  // n = 2j + t', k = 2c + t: u_j = sum_c y_c q_cj
+        n = 2 * j + tp;
+        k = 2 * c + t;
+        v = tp == 0 ? (t == 0 ? q.x : -q.y) : (t == 0 ? q.y : q.x);
+      } else {  // n = 2c + t', k = 2j + t: g_c = sum_j conj(q_cj) u_j
+        n = 2 * c + tp;
+        k = 2 * j + t;
+        v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
+      }
+      const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
+      const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
+      *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
+      *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
+    }
+}
+
 template <int MODE, int QPER>
 __device__ __forceinline__ void build_bimage(uint8_t* base, const CtParams& P, const int (&spos)[kMaxTaps][3],
                                              const float2 (&qv)[QPER], int nq, uint32_t gbytes) {
-  const int L = P.L, nb = P.nb;
 #pragma unroll
   for (int u = 0; u < QPER; ++u) {
     const int e = threadIdx.x + u * kThreads;
     if (e >= nq) break;
-    const int sp = e >> 6, c = (e >> 3) & 7, j = e & 7;
-    const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
-    const int b = spos[sp][L - 1];
-    const float2 q = qv[u];
-    uint8_t* gb = base + (size_t)g * gbytes;
-#pragma unroll
-    for (int tp = 0; tp < 2; ++tp)
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        int n, k;
-        float v;
-        if (MODE < 2) {  // n = 2j + t', k = 2c + t: u_j = sum_c y_c q_cj
-          n = 2 * j + tp;
-          k = 2 * c + t;
-          v = tp == 0 ? (t == 0 ? q.x : -q.y) : (t == 0 ? q.y : q.x);
-        } else {  // n = 2c + t', k = 2j + t: g_c = sum_j conj(q_cj) u_j
-          n = 2 * c + tp;
-          k = 2 * j + t;
-          v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
-        }
-        const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
-        const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
-        *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
-        *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
-      }
+    bimage_put<MODE>(base, P, spos, e, qv[u], gbytes);
   }
 }
 
@@ -275,6 +280,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     ga[g][1] = L == 3 ? g % P.kpre[1] : 0;
   }
   const bool pre = !BS && P.bimg != nullptr;
+  const bool pre_bs = BS && P.bimg != nullptr;  // streamed: each stage's group image arrives with its A tile
   __shared__ __align__(8) uint64_t bfull;
   if (!BS && !pre) {
     float4* z = reinterpret_cast<float4*>(sB);
@@ -344,7 +350,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
             if (P.debug & 2) {
               tc::mbar_arrive(&full[s]);
             } else {
-              tc::mbar_expect_tx(&full[s], kHalfBytes);
+              tc::mbar_expect_tx(&full[s], kHalfBytes + (pre_bs ? gbytes : 0u));
               // tensor coordinate 1 = last spatial axis, 2 = axis L-2, 3 = axis L-3
               int c1, c2 = 0, c3 = 0;
               if (MODE < 2) {
@@ -366,6 +372,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
               if (tr && line == (int)blockIdx.x && c == 0 && g == 0) trace[3] = gtimer();
               tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
               tc::tma_load_4d(dst + 64 * 64, &tmap, 0, c1 + 64, c2, c3, &full[s]);
+              if (pre_bs) bulk_g2s(dst + 2 * kHalfBytes, P.bimg + (size_t)g * gbytes, gbytes, &full[s]);
             }
             if (++s == S) { s = 0; ph ^= 1; }
           }
@@ -443,7 +450,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
               lo4[i] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
             }
           }
-          if (BS) {
+          if (BS && !pre_bs) {
             // this prefix group's B image: rows 16 b + n (hi) / 16 nb + 16 b + n (lo)
             uint8_t* gb = sStage + (size_t)s * stb + 2 * kHalfBytes;
             for (int e = ct; e < nb * 64; e += 128) {
@@ -674,16 +681,9 @@ __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P,
     spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + t % L);
   float4* z = reinterpret_cast<float4*>(img);
   for (int i = threadIdx.x; i < P.ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
-  float2 qv[kQPer];
   const int nq = P.nsp * 64;
-#pragma unroll
-  for (int u = 0; u < kQPer; ++u) {
-    const int e = threadIdx.x + u * kThreads;
-    qv[u] = e < nq ? __ldg(qt + e) : make_float2(0.f, 0.f);
-  }
   __syncthreads();  // zeroing before the image entries
-  build_bimage<MODE>(img, P, spos, qv, nq, gbytes);
+  for (int e = threadIdx.x; e < nq; e += kThreads) bimage_put<MODE>(img, P, spos, e, __ldg(qt + e), gbytes);
 }
 
 thread_local const uint8_t* t_bimg = nullptr;
@@ -884,7 +884,7 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   P.stage_bytes = (int)sh.stage;
   P.bimg = nullptr;
   P.bimg_early = 0;
-  if (t_bimg && !sh.bstream) {
+  if (t_bimg) {
     P.bimg = t_bimg;
     P.bimg_early = t_bimg_early;
   }
@@ -903,7 +903,7 @@ bool hicu_conv_tc_supported(const DevGeom& g, int p) {
 
 size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p) {
   Shape sh;
-  if (!shape_of(g, p, &sh) || sh.bstream) return 0;
+  if (!shape_of(g, p, &sh)) return 0;
   return (size_t)sh.ng * sh.nb * 2048;
 }
 
@@ -911,7 +911,7 @@ size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p) {
 int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, int G, uint8_t* img, size_t ib,
                                cudaStream_t st) {
   Shape sh;
-  if (!shape_of(g, p, &sh) || sh.bstream) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: no resident B image");
+  if (!shape_of(g, p, &sh)) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: no B image");
   CtParams P{};
   P.L = sh.L;
   P.nsp = g.nsp;

@@ -65,6 +65,11 @@ __global__ void zgemm_kernel(bool ca, bool cb, int m, int n, int k, const double
 // cycles).  The nullspace GEMMs (K = n or ell <= 256) are latency-bound, and
 // the tiled kernel above pays one L2 round trip per 16-wide K chunk.
 constexpr int kZgK = 256;
+__device__ __forceinline__ void zp_cp16(double2* dst_smem, const double2* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
 __global__ void __launch_bounds__(256)
 zgemm_panel_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restrict__ A, int lda,
                    const double2* __restrict__ B, int ldb, double2* __restrict__ C, int ldc) {
@@ -74,27 +79,51 @@ zgemm_panel_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restr
   double2* Bs = zp + 16 * (k + 1);  // k x 17: op(B) rows, padded
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int row0 = blockIdx.y * 16, col0 = blockIdx.x * 16;
+  // staged with cp.async (every element's copy in flight at once; a
+  // load-then-store loop paid one L2 round trip per iteration, ~15 us per
+  // call); conjugation is applied when the panels are read
   for (int e = threadIdx.x; e < 16 * k; e += 256) {
     const int r = ca ? e % 16 : e / k, l = ca ? e / 16 : e % k;  // coalesced along the contiguous index
     const int row = row0 + r;
-    As[r * (k + 1) + l] = row < m ? load_op(A, lda, ca, row, l) : cd(0.0, 0.0);
+    double2* dst = As + r * (k + 1) + l;
+    if (row < m) zp_cp16(dst, ca ? A + (size_t)l * lda + row : A + (size_t)row * lda + l);
+    else *dst = cd(0.0, 0.0);
   }
   for (int e = threadIdx.x; e < 16 * k; e += 256) {
     const int c = cb ? e / k : e % 16, l = cb ? e % k : e / 16;
     const int col = col0 + c;
-    Bs[l * 17 + c] = col < n ? load_op(B, ldb, cb, l, col) : cd(0.0, 0.0);
+    double2* dst = Bs + l * 17 + c;
+    if (col < n) zp_cp16(dst, cb ? B + (size_t)col * ldb + l : B + (size_t)l * ldb + col);
+    else *dst = cd(0.0, 0.0);
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const double2* a = As + ty * (k + 1);
   double2 c0 = cd(0.0, 0.0), c1 = c0, c2 = c0, c3 = c0;
   int l = 0;
-  for (; l + 3 < k; l += 4) {
-    zfma(c0, a[l], Bs[l * 17 + tx]);
-    zfma(c1, a[l + 1], Bs[(l + 1) * 17 + tx]);
-    zfma(c2, a[l + 2], Bs[(l + 2) * 17 + tx]);
-    zfma(c3, a[l + 3], Bs[(l + 3) * 17 + tx]);
+  if (!ca && !cb) {
+    for (; l + 3 < k; l += 4) {
+      zfma(c0, a[l], Bs[l * 17 + tx]);
+      zfma(c1, a[l + 1], Bs[(l + 1) * 17 + tx]);
+      zfma(c2, a[l + 2], Bs[(l + 2) * 17 + tx]);
+      zfma(c3, a[l + 3], Bs[(l + 3) * 17 + tx]);
+    }
+    for (; l < k; ++l) zfma(c0, a[l], Bs[l * 17 + tx]);
+  } else {
+    const double sa = ca ? -1.0 : 1.0, sb = cb ? -1.0 : 1.0;  // conjugation as a sign on the imaginary part
+    for (; l + 3 < k; l += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double2 x = a[l + u], y = Bs[(l + u) * 17 + tx];
+        double2& cc = u == 0 ? c0 : (u == 1 ? c1 : (u == 2 ? c2 : c3));
+        zfma(cc, cd(x.x, sa * x.y), cd(y.x, sb * y.y));
+      }
+    }
+    for (; l < k; ++l) {
+      const double2 x = a[l], y = Bs[l * 17 + tx];
+      zfma(c0, cd(x.x, sa * x.y), cd(y.x, sb * y.y));
+    }
   }
-  for (; l < k; ++l) zfma(c0, a[l], Bs[l * 17 + tx]);
   const int row = row0 + ty, col = col0 + tx;
   if (row < m && col < n) C[(size_t)row * ldc + col] = (c0 + c1) + (c2 + c3);
 }

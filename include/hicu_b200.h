@@ -292,7 +292,9 @@ int hicu_coil_cov(int64_t nloc, int nc, const void* x, const uint8_t* mask,
 size_t hicu_coil_basis_workspace(int nc);
 int hicu_coil_basis(int nc, int nv, const void* cov, void* basis, double* evals,
                     void* ws, size_t ws_bytes, void* stream);
-/* y[l, j] = sum_c x[l, c] basis[c, j]  (nloc x nv c64);
+/* y[l, j] = sum_c m[l, c] x[l, c] basis[c, j]  (nloc x nv c64), with
+ * m = (mask == 1) when mask != NULL (the reference's mask_apply,
+ * arrays.py:54-67, fused: x may be raw k-space) and m = 1 otherwise;
  * mask_out[l, j] = mask[l, 0] when mask_out != NULL. */
 int hicu_coil_apply(int64_t nloc, int nc, int nv, const void* x,
                     const uint8_t* mask, const void* basis, void* y,

@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(1024) coil_cov_kernel(int64_t nloc, int nc, co
     const int cnt = (int)((l1 - lc) < kLocPerBlock ? (l1 - lc) : kLocPerBlock);
     for (int e = threadIdx.x; e < cnt * nc; e += blockDim.x) {
       const int li = e / nc, c = e % nc;
-      xs[li][c] = x[(lc + li) * nc + c];
+      const int64_t idx = (lc + li) * nc + c;
+      xs[li][c] = mask[idx] == 1 ? x[idx] : cf(0.f, 0.f);  // mask_apply fused (x may be raw k-space)
     }
     for (int e = threadIdx.x; e < cnt; e += blockDim.x) ms[e] = mask[(lc + e) * nc];
     __syncthreads();
@@ -76,7 +77,13 @@ __global__ void coil_apply_kernel(int64_t nloc, int nc, int nv, const float2* __
     const int j = (int)(e % nv);
     const float2* xl = x + l * nc;
     float2 acc = cf(0.f, 0.f);
-    for (int c = 0; c < nc; ++c) cfma(acc, xl[c], sb[c * nv + j]);
+    if (mask) {  // mask_apply fused (arrays.py:54-67): unobserved entries read as zero
+      const uint8_t* ml = mask + l * nc;
+      for (int c = 0; c < nc; ++c)
+        if (ml[c] == 1) cfma(acc, xl[c], sb[c * nv + j]);
+    } else {
+      for (int c = 0; c < nc; ++c) cfma(acc, xl[c], sb[c * nv + j]);
+    }
     y[e] = acc;
     if (mask_out) mask_out[e] = mask[l * nc];
   }

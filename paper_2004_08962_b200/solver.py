@@ -581,7 +581,9 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         xd = _upload_pinned(torch, x0)
         md = to_dev(observed_in.view(np.uint8), np.uint8)
         h2d += xd.numel() * 8 + md.numel()
+        _tr("upload issued")
         ydev, mdev, bdev, _ = coil_compress_device(xd.reshape(-1), md.reshape(-1), nc, nv)
+        _tr("coil compression issued")
         dims = x0.shape[:-1] + (nv,)
         x_init, mask_dev = ydev, mdev
         mask_c = np.ascontiguousarray(mask[..., :nv])
@@ -608,6 +610,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
     meter = meter if meter is not None else MemoryMeter()
     report = ReconReport()
     eng = ReconEngine(x_init, mask_dev, dims, kernel, schedule, regions, ref_dev)
+    _tr("engine")
     meter.alloc(eng.aux_complex)
     tail_region = full_region(dims, kernel, schedule.circular_axes)
     log_tail = 0 < tail_energy_threshold and tail_region.s * kernel.n <= tail_energy_threshold

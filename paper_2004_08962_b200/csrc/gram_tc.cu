@@ -45,8 +45,14 @@ namespace {
 constexpr int kBK = 16;           // rows (K) per pipeline stage: 2 MMA k-steps of 8
 constexpr int kMT = 8;            // taps per M tile  (M = 128 real columns)
 constexpr int kNT = 16;           // taps per N tile  (N <= 256 real columns)
-constexpr int kChain = 4;         // k-blocks per TMEM accumulation chain
-constexpr int kProdWarps = 8;
+#ifndef HICU_GRAM_CHAIN
+#define HICU_GRAM_CHAIN 8  // 4: 1.15e-6 -> 6.4e-7 vs fp64 at C2, 2.4e-6 -> 2.2e-6 at the C5 shard, 6 % slower there
+#endif
+constexpr int kChain = HICU_GRAM_CHAIN;  // k-blocks per TMEM accumulation chain
+#ifndef HICU_GRAM_PROD_WARPS
+#define HICU_GRAM_PROD_WARPS 8  // 6: 26.0 ms, 4: 41.0 ms, 12: 23.7 ms at the C5 shard (8: 23.6 ms)
+#endif
+constexpr int kProdWarps = HICU_GRAM_PROD_WARPS;
 constexpr int kProducers = kProdWarps * 32;
 constexpr int kEpiWarps = 16;
 constexpr int kThreads = (kProdWarps + 1 + kEpiWarps) * 32;

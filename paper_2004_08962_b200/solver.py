@@ -340,6 +340,12 @@ class ReconEngine:
             self.recs[si] = torch.zeros(it * G * nat.REC_SLOTS, dtype=f64, device=dev)
             if self.ref is not None:
                 self.sers[si] = torch.zeros(it * G * self.ser_stride, dtype=f64, device=dev)
+        # the draw buffers are fresh allocations: uploads need only be ordered
+        # after this point of the compute stream, not after the stages issued
+        # since (waiting on the stream tail serialised every chunk's upload
+        # behind the previous chunk's compute)
+        self.alloc_event = torch.cuda.Event()
+        self.alloc_event.record()
 
     # -- inputs --------------------------------------------------------------
     def host_draw_buffers(self, si: int):
@@ -361,8 +367,9 @@ class ReconEngine:
         it1 = om.shape[0] if it1 is None else it1
         if self.copy_stream is None:
             self.copy_stream = torch.cuda.Stream()
-        # the device buffers may still be read by earlier work on the compute stream
-        self.copy_stream.wait_stream(torch.cuda.current_stream())
+            # iteration slices are disjoint and each is written once, so the only
+            # ordering needed is after the buffers' allocation
+            self.copy_stream.wait_event(self.alloc_event)
         with torch.cuda.stream(self.copy_stream):
             om[it0:it1].copy_(om_h[it0:it1], non_blocking=True)
             pb[it0:it1].copy_(pb_h[it0:it1], non_blocking=True)

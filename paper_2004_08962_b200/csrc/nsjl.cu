@@ -479,7 +479,7 @@ int nsjl_ct(int r) { return r <= 64 ? 64 : (r <= 100 ? 128 : 0); }
 
 extern "C" int hicu_nullspace_jl_supported(int n, int r) {
   const int ct = nsjl_ct(r);
-  return (r >= 1 && r < n && ct && nsjl_smem(n, r, ct, ct == 64) <= (size_t)220 * 1024) ? 1 : 0;
+  return (r >= 1 && r < n && ct && nsjl_smem(n, r, ct, ct == 64) <= (size_t)226 * 1024) ? 1 : 0;
 }
 
 extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const void* Bin, void* B, void* out32, int p,

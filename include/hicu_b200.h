@@ -217,10 +217,17 @@ int hicu_apply_reflectors(int n, int r, const void* refl, const void* tau,
  * of Bin are ignored), out32 as in hicu_apply_reflectors.  *gate_dev (device
  * int) is set to 1 when an LU pivot (the reference's u0) is below 1e-3 in
  * modulus; the caller must then recompute with the Householder kernels.
- * Supported for 1 <= r <= 100, r < n (hicu_nullspace_jl_supported). */
+ * Supported for 1 <= r <= 160, r < n (hicu_nullspace_jl_supported). */
 int hicu_nullspace_jl_supported(int n, int r);
 int hicu_nullspace_jl(int n, int r, const void* V, int cols, const void* Bin,
                       void* B, void* out32, int p, int* gate_dev, void* stream);
+/* Same with a caller workspace: ranks whose r x r LU does not fit one SM
+ * (64 < r <= 160 for large n, e.g. C4/C5) factor A_1 in global memory.
+ * hicu_nullspace_jl_workspace(n, r) bytes (0: none needed). */
+size_t hicu_nullspace_jl_workspace(int n, int r);
+int hicu_nullspace_jl_ws(int n, int r, const void* V, int cols, const void* Bin,
+                         void* B, void* out32, int p, int* gate_dev, void* ws,
+                         size_t ws_bytes, void* stream);
 
 /* ---- native stage driver (replaces the solver.py:322-393 loop body) ------- */
 /* One call runs `iters` outer iterations of one stage: Gram -> Nystrom ->

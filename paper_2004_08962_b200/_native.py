@@ -97,6 +97,9 @@ _SIGS = {
     "hicu_apply_reflectors": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
                                       c_void_p, c_int, c_void_p]),
     "hicu_nullspace_jl_supported": (c_int, [c_int, c_int]),
+    "hicu_nullspace_jl_workspace": (c_size_t, [c_int, c_int]),
+    "hicu_nullspace_jl_ws": (c_int, [c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
+                                     c_void_p, c_size_t, c_void_p]),
     "hicu_nullspace_jl": (c_int, [c_int, c_int, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p,
                                   c_void_p]),
     "hicu_run_stage": (c_int, [POINTER(HicuStageArgs), c_void_p]),

@@ -98,7 +98,8 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   if (ncp < 0 || nsp < 0) return HICU_ERR_SHAPE;
   const size_t nomega = (size_t)n * ell, npbig = (size_t)n * G * p;
   static const bool jl_off = getenv("HICU_NSJL_OFF") != nullptr;
-  const bool use_jl = !jl_off && hicu_nullspace_jl_supported(n, r);
+  const size_t refl_bytes = (size_t)2 * n * r * sizeof(double2);  // scratch for the global-LU closed form
+  const bool use_jl = !jl_off && hicu_nullspace_jl_supported(n, r) && hicu_nullspace_jl_workspace(n, r) <= refl_bytes;
   int s;
   for (int it = 0; it < a->iters; ++it) {
     // ---- nullspace: Gram + Nystrom (== rSVD subspace), or injected V ----
@@ -126,7 +127,9 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
       // raised the gate (a pivot below its floor)
       const int* gate = nullptr;
       if (use_jl) {
-        if ((s = hicu_nullspace_jl(n, r, a->V, G * p, pb, a->B, a->qt32, p, a->flags + r, stream))) return s;
+        if ((s = hicu_nullspace_jl_ws(n, r, a->V, G * p, pb, a->B, a->qt32, p, a->flags + r, a->refl, refl_bytes,
+                                      stream)))
+          return s;
         gate = a->flags + r;
       }
       if ((s = hicu_householder_gated(n, r, a->V, a->householder_tol, a->refl, a->tau, a->flags, a->status, gate,

@@ -106,6 +106,155 @@ __device__ __forceinline__ void nsjl_zpart(int n, int r, const double2* __restri
   for (int c = 0; c < kNjCols; ++c) Zp[((size_t)rg * r + j) * kNjCols + c] = acc[c];
 }
 
+// Solves and Q~ (shared by the single-CTA-LU kernel and the global-LU path):
+// LU / idg may live in shared or global memory (generic loads); V chunks are
+// staged in `stage` (stage_elems double2, padded rows of r + 1).
+template <int CT, int NT, int RG>
+__device__ __forceinline__ void nsjl_finish(int n, int r, const double2* __restrict__ V, int cols, int c0, int nc,
+                                            double2* __restrict__ B, float2* __restrict__ out32, int p,
+                                            const double2* LU, const double2* idg, const double2* Zp, double2* X,
+                                            const double2* Ps, double2* stage, int stage_elems) {
+  const int tid = threadIdx.x;
+  // A_1^H X = Z  <=>  U^H (L^H X) = Z: one warp per JL column, rows i = lane + 32 m;
+  // the next row of U / L is loaded one step ahead
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp < nc) {
+    constexpr int MQ = (CT + 31) / 32;  // r <= CT
+    double2 z[MQ];
+#pragma unroll
+    for (int m = 0; m < MQ; ++m) {
+      const int i = lane + 32 * m;
+      double2 acc = cd(0.0, 0.0);
+      if (i < r)
+        for (int g = 0; g < RG; ++g) acc = acc + Zp[((size_t)g * r + i) * kNjCols + warp];
+      z[m] = acc;
+    }
+    // forward: U^H y = z  (y_k = (z_k - sum_{m<k} conj(U[m][k]) y_m) / conj(U[k][k]))
+    double2 un[MQ];
+#pragma unroll
+    for (int m = 0; m < MQ; ++m) {
+      const int i = lane + 32 * m;
+      un[m] = i < r ? LU[i] : cd(0.0, 0.0);
+    }
+    for (int k = 0; k < r; ++k) {
+      double2 uc[MQ];
+#pragma unroll
+      for (int m = 0; m < MQ; ++m) {
+        uc[m] = un[m];
+        const int i = lane + 32 * m;
+        un[m] = (k + 1 < r && i < r) ? LU[(size_t)(k + 1) * r + i] : cd(0.0, 0.0);
+      }
+      const int sl = k >> 5;
+      double2 zv = z[0];
+#pragma unroll
+      for (int m = 1; m < MQ; ++m)
+        if (sl == m) zv = z[m];
+      zv.x = __shfl_sync(0xffffffffu, zv.x, k & 31);
+      zv.y = __shfl_sync(0xffffffffu, zv.y, k & 31);
+      const double2 y = cmulc(idg[k], zv);
+#pragma unroll
+      for (int m = 0; m < MQ; ++m) {
+        const int i = lane + 32 * m;
+        if (i == k) z[m] = y;
+        else if (i > k) z[m] = z[m] - cmulc(uc[m], y);
+      }
+    }
+    // backward: L^H x = y  (x_k = y_k - sum_{m>k} conj(L[m][k]) x_m)
+#pragma unroll
+    for (int m = 0; m < MQ; ++m) {
+      const int i = lane + 32 * m;
+      un[m] = i < r - 1 ? LU[(size_t)(r - 1) * r + i] : cd(0.0, 0.0);
+    }
+    for (int k = r - 1; k >= 0; --k) {
+      double2 lc[MQ];
+#pragma unroll
+      for (int m = 0; m < MQ; ++m) {
+        lc[m] = un[m];
+        const int i = lane + 32 * m;
+        un[m] = (k >= 1 && i < k - 1) ? LU[(size_t)(k - 1) * r + i] : cd(0.0, 0.0);
+      }
+      const int sl = k >> 5;
+      double2 xv = z[0];
+#pragma unroll
+      for (int m = 1; m < MQ; ++m)
+        if (sl == m) xv = z[m];
+      xv.x = __shfl_sync(0xffffffffu, xv.x, k & 31);
+      xv.y = __shfl_sync(0xffffffffu, xv.y, k & 31);
+#pragma unroll
+      for (int m = 0; m < MQ; ++m) {
+        const int i = lane + 32 * m;
+        if (i < k) z[m] = z[m] - cmulc(lc[m], xv);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < MQ; ++m) {
+      const int i = lane + 32 * m;
+      if (i < r) X[(size_t)i * kNjCols + warp] = z[m];
+    }
+  }
+  __syncthreads();
+  NSJL_STAMP(3)
+
+  // Q~[k][c] = [0; P][k][c] + sum_a (V[k][a] - delta_ka) X[a][c]; V staged through
+  // shared memory (LU and pivot areas) in chunks of CH rows with padded stride r + 1
+  const int ld = r + 1;
+  const int CH = stage_elems / ld;  // rows per staged V chunk (>= 1)
+  for (int k0 = 0; k0 < n; k0 += CH) {
+    const int rows = min(CH, n - k0);
+    for (int e = tid; e < rows * r; e += NT) {
+      const int kk = e / r, a = e - kk * r;
+      nsjl_cp16(stage + (size_t)kk * ld + a, V + (size_t)(k0 + kk) * r + a);
+    }
+    nsjl_cp_wait_all();
+    __syncthreads();
+    // thread (row kk = tid % TR (+ TR, ...), column c = tid / TR): two rows per
+    // pass as independent accumulation chains
+    constexpr int TR = NT / kNjCols;
+    const int c = tid / TR;
+    for (int kk = tid % TR; kk < rows; kk += 2 * TR) {
+      const bool two = kk + TR < rows;
+      const int k = k0 + kk, k2 = k + TR;
+      double2 acc = cd(0.0, 0.0), acc2 = cd(0.0, 0.0), bcc = cd(0.0, 0.0), bcc2 = cd(0.0, 0.0);
+      if (c < nc) {
+        acc = k >= r ? Ps[(size_t)(k - r) * kNjCols + c] : cd(-X[(size_t)k * kNjCols + c].x, -X[(size_t)k * kNjCols + c].y);
+        if (two)
+          bcc = k2 >= r ? Ps[(size_t)(k2 - r) * kNjCols + c]
+                        : cd(-X[(size_t)k2 * kNjCols + c].x, -X[(size_t)k2 * kNjCols + c].y);
+      }
+      const double2* vr = stage + (size_t)kk * ld;
+      const double2* vr2 = vr + (size_t)TR * ld;
+      int a = 0;
+      for (; a + 1 < r; a += 2) {
+        const double2 x0 = X[(size_t)a * kNjCols + c], x1 = X[(size_t)(a + 1) * kNjCols + c];
+        zfma(acc, vr[a], x0);
+        zfma(acc2, vr[a + 1], x1);
+        if (two) {
+          zfma(bcc, vr2[a], x0);
+          zfma(bcc2, vr2[a + 1], x1);
+        }
+      }
+      if (a < r) {
+        const double2 x0 = X[(size_t)a * kNjCols + c];
+        zfma(acc, vr[a], x0);
+        if (two) zfma(bcc, vr2[a], x0);
+      }
+      if (c < nc) {
+        const int jj = c0 + c, step = jj / p, t = jj % p;
+        const double2 v = acc + acc2;
+        B[(size_t)k * cols + jj] = v;
+        if (out32) out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
+        if (two) {
+          const double2 v2 = bcc + bcc2;
+          B[(size_t)k2 * cols + jj] = v2;
+          if (out32) out32[((size_t)step * n + k2) * p + t] = cf((float)v2.x, (float)v2.y);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  NSJL_STAMP(4)
+}
+
 // CT threads per LU row group (>= r), NT threads, QN = ceil(r / (NT / CT)) rows per thread.
 template <int CT, int QN, int NT, bool WARP_LU>
 __global__ void __launch_bounds__(NT)
@@ -324,144 +473,107 @@ nsjl_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2
   __syncthreads();
   NSJL_STAMP(2)
 
-  // A_1^H X = Z  <=>  U^H (L^H X) = Z: one warp per JL column, rows i = lane + 32 m;
-  // the next row of U / L is loaded one step ahead
-  const int warp = tid >> 5, lane = tid & 31;
-  if (warp < nc) {
-    constexpr int MQ = (CT + 31) / 32;  // r <= CT
-    double2 z[MQ];
-#pragma unroll
-    for (int m = 0; m < MQ; ++m) {
-      const int i = lane + 32 * m;
-      double2 acc = cd(0.0, 0.0);
-      if (i < r)
-        for (int g = 0; g < RG; ++g) acc = acc + Zp[((size_t)g * r + i) * kNjCols + warp];
-      z[m] = acc;
-    }
-    // forward: U^H y = z  (y_k = (z_k - sum_{m<k} conj(U[m][k]) y_m) / conj(U[k][k]))
-    double2 un[MQ];
-#pragma unroll
-    for (int m = 0; m < MQ; ++m) {
-      const int i = lane + 32 * m;
-      un[m] = i < r ? LU[i] : cd(0.0, 0.0);
-    }
-    for (int k = 0; k < r; ++k) {
-      double2 uc[MQ];
-#pragma unroll
-      for (int m = 0; m < MQ; ++m) {
-        uc[m] = un[m];
-        const int i = lane + 32 * m;
-        un[m] = (k + 1 < r && i < r) ? LU[(size_t)(k + 1) * r + i] : cd(0.0, 0.0);
-      }
-      const int sl = k >> 5;
-      double2 zv = z[0];
-#pragma unroll
-      for (int m = 1; m < MQ; ++m)
-        if (sl == m) zv = z[m];
-      zv.x = __shfl_sync(0xffffffffu, zv.x, k & 31);
-      zv.y = __shfl_sync(0xffffffffu, zv.y, k & 31);
-      const double2 y = cmulc(idg[k], zv);
-#pragma unroll
-      for (int m = 0; m < MQ; ++m) {
-        const int i = lane + 32 * m;
-        if (i == k) z[m] = y;
-        else if (i > k) z[m] = z[m] - cmulc(uc[m], y);
-      }
-    }
-    // backward: L^H x = y  (x_k = y_k - sum_{m>k} conj(L[m][k]) x_m)
-#pragma unroll
-    for (int m = 0; m < MQ; ++m) {
-      const int i = lane + 32 * m;
-      un[m] = i < r - 1 ? LU[(size_t)(r - 1) * r + i] : cd(0.0, 0.0);
-    }
-    for (int k = r - 1; k >= 0; --k) {
-      double2 lc[MQ];
-#pragma unroll
-      for (int m = 0; m < MQ; ++m) {
-        lc[m] = un[m];
-        const int i = lane + 32 * m;
-        un[m] = (k >= 1 && i < k - 1) ? LU[(size_t)(k - 1) * r + i] : cd(0.0, 0.0);
-      }
-      const int sl = k >> 5;
-      double2 xv = z[0];
-#pragma unroll
-      for (int m = 1; m < MQ; ++m)
-        if (sl == m) xv = z[m];
-      xv.x = __shfl_sync(0xffffffffu, xv.x, k & 31);
-      xv.y = __shfl_sync(0xffffffffu, xv.y, k & 31);
-#pragma unroll
-      for (int m = 0; m < MQ; ++m) {
-        const int i = lane + 32 * m;
-        if (i < k) z[m] = z[m] - cmulc(lc[m], xv);
-      }
-    }
-#pragma unroll
-    for (int m = 0; m < MQ; ++m) {
-      const int i = lane + 32 * m;
-      if (i < r) X[(size_t)i * kNjCols + warp] = z[m];
-    }
+  nsjl_finish<CT, NT, RG>(n, r, V, cols, c0, nc, B, out32, p, LU, idg, Zp, X, Ps, LU, (int)(idg - LU));
+}
+
+// ---------------------------------------------------------------------------
+// Ranks whose r x r LU exceeds one SM (C4/C5: r = 150 / 120, n = 1000): the LU
+// runs in one CTA over a global-memory (L2-resident) copy of A_1, right-looking
+// with one block barrier per step; the Z / solve / Q~ phases then run in the
+// usual per-JL-column CTAs reading U, L and 1/pivot from global memory.
+// ---------------------------------------------------------------------------
+constexpr int kLuThreads = 1024;
+
+__global__ void __launch_bounds__(kLuThreads)
+nsjl_lu_global_kernel(int r, const double2* __restrict__ V, double2* __restrict__ LUg, double2* __restrict__ Lg,
+                      double2* __restrict__ idg, double* __restrict__ pd, int* __restrict__ gate) {
+  hicu_pdl_entry();
+  const int tid = threadIdx.x;
+  for (int e = tid; e < r * r; e += kLuThreads) {
+    const int i = e / r, j = e - i * r;
+    double2 v = V[(size_t)i * r + j];
+    if (i == j) v.x -= 1.0;
+    LUg[e] = v;
   }
   __syncthreads();
-  NSJL_STAMP(3)
-
-  // Q~[k][c] = [0; P][k][c] + sum_a (V[k][a] - delta_ka) X[a][c]; V staged through
-  // shared memory (LU and pivot areas) in chunks of CH rows with padded stride r + 1
-  const int ld = r + 1;
-  const int CH = (int)((idg - LU) / ld);  // LU + column/row publication areas (>= 1 row)
-  for (int k0 = 0; k0 < n; k0 += CH) {
-    const int rows = min(CH, n - k0);
-    for (int e = tid; e < rows * r; e += NT) {
-      const int kk = e / r, a = e - kk * r;
-      nsjl_cp16(LU + (size_t)kk * ld + a, V + (size_t)(k0 + kk) * r + a);
+  for (int k = 0; k < r; ++k) {
+    const double2 piv = __ldcg(LUg + (size_t)k * r + k);
+    const double2 inv = nsjl_inv(piv);
+    if (tid == 0) {
+      idg[k] = inv;
+      pd[k] = abs2d(piv);
     }
-    nsjl_cp_wait_all();
-    __syncthreads();
-    // thread (row kk = tid % TR (+ TR, ...), column c = tid / TR): two rows per
-    // pass as independent accumulation chains
-    constexpr int TR = NT / kNjCols;
-    const int c = tid / TR;
-    for (int kk = tid % TR; kk < rows; kk += 2 * TR) {
-      const bool two = kk + TR < rows;
-      const int k = k0 + kk, k2 = k + TR;
-      double2 acc = cd(0.0, 0.0), acc2 = cd(0.0, 0.0), bcc = cd(0.0, 0.0), bcc2 = cd(0.0, 0.0);
-      if (c < nc) {
-        acc = k >= r ? Ps[(size_t)(k - r) * kNjCols + c] : cd(-X[(size_t)k * kNjCols + c].x, -X[(size_t)k * kNjCols + c].y);
-        if (two)
-          bcc = k2 >= r ? Ps[(size_t)(k2 - r) * kNjCols + c]
-                        : cd(-X[(size_t)k2 * kNjCols + c].x, -X[(size_t)k2 * kNjCols + c].y);
-      }
-      const double2* vr = LU + (size_t)kk * ld;
-      const double2* vr2 = vr + (size_t)TR * ld;
-      int a = 0;
-      for (; a + 1 < r; a += 2) {
-        const double2 x0 = X[(size_t)a * kNjCols + c], x1 = X[(size_t)(a + 1) * kNjCols + c];
-        zfma(acc, vr[a], x0);
-        zfma(acc2, vr[a + 1], x1);
-        if (two) {
-          zfma(bcc, vr2[a], x0);
-          zfma(bcc2, vr2[a + 1], x1);
-        }
-      }
-      if (a < r) {
-        const double2 x0 = X[(size_t)a * kNjCols + c];
-        zfma(acc, vr[a], x0);
-        if (two) zfma(bcc, vr2[a], x0);
-      }
-      if (c < nc) {
-        const int jj = c0 + c, step = jj / p, t = jj % p;
-        const double2 v = acc + acc2;
-        B[(size_t)k * cols + jj] = v;
-        if (out32) out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
-        if (two) {
-          const double2 v2 = bcc + bcc2;
-          B[(size_t)k2 * cols + jj] = v2;
-          if (out32) out32[((size_t)step * n + k2) * p + t] = cf((float)v2.x, (float)v2.y);
-        }
+    // rows k+1.. x columns k.. : column k gives L[i][k] (kept aside: column k
+    // is still being read this step), the rest take the rank-1 update
+    const int m = r - k - 1;
+    for (int e = tid; e < m * (m + 1); e += kLuThreads) {
+      const int ii = e / (m + 1), jj = e - ii * (m + 1);
+      const int i = k + 1 + ii;
+      const double2 l = cmul(__ldcg(LUg + (size_t)i * r + k), inv);
+      if (jj == 0) {
+        Lg[(size_t)i * r + k] = l;
+      } else {
+        const int j = k + jj;
+        double2* pij = LUg + (size_t)i * r + j;
+        *pij = __ldcg(pij) - cmul(l, __ldcg(LUg + (size_t)k * r + j));
       }
     }
     __syncthreads();
   }
-  NSJL_STAMP(4)
+  for (int e = tid; e < r * r; e += kLuThreads) {
+    const int i = e / r, j = e - i * r;
+    if (i > j) LUg[e] = Lg[e];
+  }
+  if (tid < 32) {
+    double mn = 1e300;
+    for (int k = tid; k < r; k += 32) mn = fmin(mn, pd[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (tid == 0) *gate = (mn >= kPivotFloor * kPivotFloor) ? 0 : 1;
+  }
+}
+
+template <int CT, int NT>
+__global__ void __launch_bounds__(NT)
+nsjl_big_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2* __restrict__ Pin,
+                double2* __restrict__ B, float2* __restrict__ out32, int p, const double2* __restrict__ LUg,
+                const double2* __restrict__ idg, int stage_elems) {
+  hicu_pdl_entry();
+  constexpr int RG = NT / CT;
+  extern __shared__ double2 smj[];
+  double2* Zp = smj;                              // RG x r x kNjCols
+  double2* X = Zp + (size_t)RG * r * kNjCols;     // r x kNjCols
+  double2* Ps = X + (size_t)r * kNjCols;          // (n - r) x kNjCols
+  double2* stage = Ps + (size_t)(n - r) * kNjCols;
+  const int tid = threadIdx.x, j = tid % CT, rg = tid / CT;
+  const int c0 = blockIdx.x * kNjCols;
+  const int nc = min(kNjCols, cols - c0);
+  for (int e = tid; e < (n - r) * kNjCols; e += NT) {
+    const int kk = e / kNjCols, c = e - kk * kNjCols;
+    if (c < nc) nsjl_cp16(Ps + e, Pin + (size_t)(r + kk) * cols + c0 + c);
+    else Ps[e] = cd(0.0, 0.0);
+  }
+  nsjl_cp_wait_all();
+  __syncthreads();
+  nsjl_zpart<RG>(n, r, V, Ps, j, rg, Zp);
+  __syncthreads();
+  nsjl_finish<CT, NT, RG>(n, r, V, cols, c0, nc, B, out32, p, LUg, idg, Zp, X, Ps, stage, stage_elems);
+}
+
+size_t nsjl_big_fixed(int n, int r, int ct, int nt) {
+  return ((size_t)(nt / ct) * r * kNjCols + (size_t)r * kNjCols + (size_t)(n - r) * kNjCols) * sizeof(double2);
+}
+
+int nsjl_big_ct(int r) { return r <= 128 ? 128 : (r <= 160 ? 160 : 0); }
+int nsjl_big_nt(int ct) { return ct == 128 ? 512 : 640; }
+constexpr size_t kBigSmem = (size_t)200 * 1024;
+
+size_t nsjl_big_ws(int r) { return ((size_t)2 * r * r + r) * sizeof(double2) + (size_t)r * sizeof(double) + 256; }
+
+bool nsjl_big_ok(int n, int r) {
+  const int ct = nsjl_big_ct(r);
+  if (!ct || r < 1 || r >= n) return false;
+  return nsjl_big_fixed(n, r, ct, nsjl_big_nt(ct)) + (size_t)(r + 1) * sizeof(double2) <= kBigSmem;
 }
 
 int nsjl_threads(int ct) { return ct == 64 ? 256 : 512; }
@@ -477,9 +589,50 @@ int nsjl_ct(int r) { return r <= 64 ? 64 : (r <= 100 ? 128 : 0); }
 
 }  // namespace
 
-extern "C" int hicu_nullspace_jl_supported(int n, int r) {
+static bool nsjl_small_ok(int n, int r) {
   const int ct = nsjl_ct(r);
-  return (r >= 1 && r < n && ct && nsjl_smem(n, r, ct, ct == 64) <= (size_t)226 * 1024) ? 1 : 0;
+  return r >= 1 && r < n && ct && nsjl_smem(n, r, ct, ct == 64) <= (size_t)226 * 1024;
+}
+
+extern "C" int hicu_nullspace_jl_supported(int n, int r) { return (nsjl_small_ok(n, r) || nsjl_big_ok(n, r)) ? 1 : 0; }
+
+extern "C" size_t hicu_nullspace_jl_workspace(int n, int r) {
+  if (nsjl_small_ok(n, r) || !nsjl_big_ok(n, r)) return 0;
+  return nsjl_big_ws(r);
+}
+
+extern "C" int hicu_nullspace_jl_ws(int n, int r, const void* V, int cols, const void* Bin, void* B, void* out32,
+                                    int p, int* gate_dev, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 1 || cols < 1 || !V || !Bin || !B || !gate_dev)
+    return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad arguments");
+  if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad p");
+  if (!hicu_nullspace_jl_supported(n, r)) return hicu_set_error(HICU_ERR_SIZE, "nullspace_jl: rank not supported");
+  if (!nsjl_small_ok(n, r)) {
+    const size_t need = nsjl_big_ws(r);
+    if (!ws || ws_bytes < need) return hicu_set_error(HICU_ERR_WORKSPACE, "nullspace_jl: workspace too small");
+    uint8_t* w = (uint8_t*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    double2* LUg = (double2*)w;
+    double2* Lg = LUg + (size_t)r * r;
+    double2* idg = Lg + (size_t)r * r;
+    double* pd = (double*)(idg + r);
+    cudaStream_t st = (cudaStream_t)stream;
+    hicu_launch(nsjl_lu_global_kernel, 1, kLuThreads, 0, st, r, (const double2*)V, LUg, Lg, idg, pd, gate_dev);
+    int s = hicu_check_launch("nsjl_lu_global_kernel");
+    if (s) return s;
+    const int ct = nsjl_big_ct(r), nt = nsjl_big_nt(ct);
+    const size_t fixed = nsjl_big_fixed(n, r, ct, nt);
+    const int stage_elems = (int)((kBigSmem - fixed) / sizeof(double2));
+    const int grid = (cols + kNjCols - 1) / kNjCols;
+    auto go = [&](auto kern) {
+      hicu_allow_max_smem((const void*)kern);
+      hicu_launch(kern, grid, nt, kBigSmem, st, n, r, (const double2*)V, cols, (const double2*)Bin, (double2*)B,
+                  (float2*)out32, p ? p : 1, (const double2*)LUg, (const double2*)idg, stage_elems);
+    };
+    if (ct == 128) go(nsjl_big_kernel<128, 512>);
+    else go(nsjl_big_kernel<160, 640>);
+    return hicu_check_launch("nsjl_big_kernel");
+  }
+  return hicu_nullspace_jl(n, r, V, cols, Bin, B, out32, p, gate_dev, stream);
 }
 
 extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const void* Bin, void* B, void* out32, int p,
@@ -487,7 +640,8 @@ extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const vo
   if (n < 1 || cols < 1 || !V || !Bin || !B || !gate_dev)
     return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad p");
-  if (!hicu_nullspace_jl_supported(n, r)) return hicu_set_error(HICU_ERR_SIZE, "nullspace_jl: rank not supported");
+  if (!nsjl_small_ok(n, r))
+    return hicu_set_error(HICU_ERR_SIZE, "nullspace_jl: rank needs the workspace entry (hicu_nullspace_jl_ws)");
   const int ct = nsjl_ct(r);
   static const bool generic = getenv("HICU_NSJL_GENERIC") != nullptr;  // A/B switch for the r <= 64 LU
   const size_t smem = nsjl_smem(n, r, ct, ct == 64 && !generic);

@@ -204,8 +204,11 @@ def nullspace_product(v, proj):
     out = torch.empty((n, m), dtype=torch.complex128, device="cuda")
     flags = torch.zeros(r + 1, dtype=torch.int32, device="cuda")
     st_t = torch.zeros(1, dtype=torch.int32, device="cuda")
-    nat.check(L.hicu_nullspace_jl(n, r, vd.data_ptr(), m, bd.data_ptr(), out.data_ptr(), None, 0,
-                                  flags[r:].data_ptr(), nat.stream_handle()), "nullspace_product")
+    wsb = int(L.hicu_nullspace_jl_workspace(n, r))
+    ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
+    nat.check(L.hicu_nullspace_jl_ws(n, r, vd.data_ptr(), m, bd.data_ptr(), out.data_ptr(), None, 0,
+                                     flags[r:].data_ptr(), ws.data_ptr(), wsb, nat.stream_handle()),
+              "nullspace_product")
     closed = int(flags[r].item()) == 0
     if not closed:
         refl, tau, fl, st_t = _reflectors(torch, vd, n, r, 1e-12)

@@ -310,6 +310,7 @@ def test_nullspace_jl_matches_reference_golden(golden_ops):
 
 
 @pytest.mark.parametrize("n,r,m", [(200, 60, 40), (200, 64, 8), (50, 10, 13), (30, 1, 4), (300, 100, 20), (490, 100, 50),
+                                   (1000, 120, 40), (1000, 150, 16), (400, 128, 9),
                                    (120, 90, 7), (8, 7, 5)])
 def test_nullspace_jl_random(n, r, m):
     from paper_2004_08962_b200.subspace import nullspace_product

@@ -190,6 +190,7 @@ chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, c
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
         for (int i = kk + 1 + warp; i < ell; i += nw) {
           const double2 a = A[(size_t)kk * ell + i];
+#pragma unroll 4
           for (int j = i + lane; j < ell; j += 32) {
             // A[i][j] -= conj(R[kk][i]) * R[kk][j]
             A[(size_t)i * ell + j] = A[(size_t)i * ell + j] - cmulc(a, A[(size_t)kk * ell + j]);

@@ -30,14 +30,14 @@ __device__ __forceinline__ double2 warp_sum_z(double2 t) {
   return t;
 }
 
-// Householder reduction A = Q T Q^H (lower), one CTA of 512 threads.
+// Householder reduction A = Q T Q^H (lower), one CTA of 1024 threads.
 // Outputs d (l), e (l-1), tau (l-1) and the reflectors transposed:
 // Vt[k*l + i] = v_k[i] (v_k[k+1] = 1).  A is held with leading dimension
 // l+1 so column walks (lanes over rows) are bank-conflict free; the
 // matrix-vector product is row-parallel with j-chunk partials in shared memory
 // (no per-row shuffle reductions on the sequential critical path).
 template <bool SMEM>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(1024)
 hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
              double* __restrict__ d, double* __restrict__ e, double2* __restrict__ tau,
              double2* __restrict__ Vt) {
@@ -48,7 +48,7 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
   __shared__ double2 sv[256], sw[256];
   __shared__ double2 part[4][256];
   __shared__ double redd[32];
-  __shared__ double2 redz[16];
+  __shared__ double2 redz[32];
   __shared__ double2 s_tau, s_scal, s_alpha2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
   for (int q = tid; q < l * l; q += nt) A[(size_t)(q / l) * lda + q % l] = Ain[q];
@@ -102,10 +102,20 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
       const int clen = (m + nchunk - 1) / nchunk;
       const int j0 = k1 + c * clen, j1 = min(l, j0 + clen);
       for (int i = k1 + rr; i < l; i += rows_per) {
-        double2 acc = cd(0.0, 0.0);
+        // four independent chains: with A in global memory (l > ~110) each
+        // step streams A22 from L2, and one chain kept one load in flight
+        double2 a0 = cd(0.0, 0.0), a1 = a0, a2 = a0, a3 = a0;
         const double2* Ai = A + (size_t)i * lda;
-        for (int j = j0; j < j1; ++j) zfma(acc, Ai[j], sv[j]);
-        part[c][i] = acc;
+        int j = j0;
+        for (; j + 3 < j1; j += 4) {
+          const double2 x0 = Ai[j], x1 = Ai[j + 1], x2 = Ai[j + 2], x3 = Ai[j + 3];
+          zfma(a0, x0, sv[j]);
+          zfma(a1, x1, sv[j + 1]);
+          zfma(a2, x2, sv[j + 2]);
+          zfma(a3, x3, sv[j + 3]);
+        }
+        for (; j < j1; ++j) zfma(a0, Ai[j], sv[j]);
+        part[c][i] = (a0 + a1) + (a2 + a3);
       }
     }
     __syncthreads();
@@ -118,9 +128,8 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
         sw[i] = wv;
         zfmac(pz, wv, sv[i]);
       }
-      // m <= 255 < nt: at most 8 warps hold non-zero partials
       pz = warp_sum_z(pz);
-      if (lane == 0 && warp < 16) redz[warp] = pz;
+      if (lane == 0) redz[warp] = pz;
     }
     __syncthreads();
     if (tid == 0) {
@@ -136,6 +145,7 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
       const double2 vi = sv[i];
       const double2 wi = sw[i] + cmul(a2, vi);
       double2* Ai = A + (size_t)i * lda;
+#pragma unroll 4
       for (int j = k1 + lane; j < l; j += 32) {
         const double2 vj = sv[j];
         const double2 wj = sw[j] + cmul(a2, vj);
@@ -1217,10 +1227,10 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
       hicu_launch(hetrd2_kernel, 1, 512, abytes, st, l, A, d, e, tau, Vt);
     } else {
       hicu_allow_max_smem((const void*)hetrd_kernel<true>);
-      hicu_launch(hetrd_kernel<true>, 1, 512, abytes, st, l, A, Aws, d, e, tau, Vt);
+      hicu_launch(hetrd_kernel<true>, 1, 1024, abytes, st, l, A, Aws, d, e, tau, Vt);
     }
   } else {
-    hicu_launch(hetrd_kernel<false>, 1, 512, 0, st, l, A, Aws, d, e, tau, Vt);
+    hicu_launch(hetrd_kernel<false>, 1, 1024, 0, st, l, A, Aws, d, e, tau, Vt);
   }
   if ((s = hicu_check_launch("hetrd_kernel"))) return s;
   const int wpb = 1;  // one warp (one eigenvalue) per SM: the Sturm recurrence is a division chain

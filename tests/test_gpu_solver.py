@@ -301,6 +301,9 @@ REDUCED = {
     "C3_slice": ("C3", 0.2, 10, (7, 7, 10), 100, [("full", 10, 5, 6)]),
     "C4_cine": ("C4", 0.25, 8, (3, 3, 3, 8), 40, [([0.5, 0.5, "full"], 8, 5, 4), ("full", 8, 5, 4)]),
     "C5_volume": ("C5", 0.15, 8, (3, 3, 3, 8), 40, [("full", 8, 5, 8)]),
+    # the C5 kernel and rank (n = 1000, r = 120): streamed tcgen05 convolutions with
+    # prebuilt B images and the global-memory-LU closed-form nullspace in the driver
+    "C5_kernel_rank": ("C5", 0.15, 8, (5, 5, 5, 8), 120, [("full", 8, 5, 2)]),
 }
 
 

@@ -572,7 +572,10 @@ hetrd4_kernel(int l, int lda, const double2* __restrict__ Ain, double* __restric
 // block, so the update needs no masks).  Same reflector scalars as
 // hetrd3_reflector; v/w double-buffered by step parity, 3 barriers per step.
 constexpr int kHetrd6Max = 96;
-constexpr int kH6Warps = 12, kH6Cols = 8;  // 12 warps x 8 columns; 3 row slots per lane
+#ifndef HICU_H6_WARPS
+#define HICU_H6_WARPS 12  // measured per C2 nullspace iteration: 8: 581 us, 12: 580, 16: 616, 24: 765
+#endif
+constexpr int kH6Warps = HICU_H6_WARPS, kH6Cols = 96 / HICU_H6_WARPS;  // warps x columns = 96; 3 row slots per lane
 __device__ long long g_h6_trace[3][6];  // debug (HICU_HETRD_TRACE): thread 0 clocks at steps 10, 40, 70
 
 // reflector k from column k (x = rows lane + 32u of column k, in registers

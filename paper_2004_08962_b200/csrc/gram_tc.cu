@@ -295,6 +295,12 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
         cursor_next(p, cu);
         gram_gather(x, cu, toff, vb);
       }
+#elif defined(HICU_GRAM_EXP_NOPROD)  // experiment: no gathers (stages carry stale data)
+      cursor_next(p, cu);
+      mbar_wait(&empty_bar[s], ph ^ 1);
+      mbar_arrive(&full_bar[s]);
+      if (++s == S) { s = 0; ph ^= 1; }
+      continue;
 #else
       gram_gather(x, cu, toff, va);
       cursor_next(p, cu);
@@ -361,9 +367,11 @@ gram_tc_kernel(const float* __restrict__ x, TcParams p, const int* __restrict__ 
             const uint64_t a_lo = make_desc_kmajor(kbase + half_bytes + (uint32_t)a_off * 512);
             const uint64_t b_hi = make_desc_kmajor(kbase);
             const uint64_t b_lo = make_desc_kmajor(kbase + half_bytes);
+#ifndef HICU_GRAM_EXP_NOMMA  // experiment: pipeline without the tensor-core work
             umma_tf32(dcol, a_hi, b_hi, idesc, first ? 0u : 1u);
             umma_tf32(dcol, a_hi, b_lo, idesc, 1u);
             umma_tf32(dcol, a_lo, b_hi, idesc, 1u);
+#endif
             first = false;
           }
           umma_commit(&empty_bar[s]);

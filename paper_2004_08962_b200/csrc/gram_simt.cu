@@ -42,8 +42,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t rows_per_split,
                  double2* __restrict__ partials) {
   hicu_pdl_entry();
-  __shared__ float2 As[kBK][kTile];
-  __shared__ float2 Bs[kBK][kTile];
+  __shared__ __align__(16) float2 As[kBK][kTile];
+  __shared__ __align__(16) float2 Bs[kBK][kTile];
   __shared__ int64_t rbase[kBK];
   __shared__ int rcc[kBK][HICU_MAX_NDIM];
 
@@ -69,60 +69,83 @@ gram_simt_kernel(DevGeom g, const float2* __restrict__ x, int ntile, int64_t row
       acc64[(a * 4 + b) * kThreads + threadIdx.x] = cd(0.0, 0.0);
     }
 
-  // outer blocks of kFlushRows rows, drained into fp64 after each block
-  for (int64_t rb = r0; rb < r1; rb += kFlushRows) {
-    const int64_t re = rb + kFlushRows < r1 ? rb + kFlushRows : r1;
-    for (int64_t rc = rb; rc < re; rc += kBK) {
-      if (threadIdx.x < kBK) {
-        const int64_t i = rc + threadIdx.x;
-        int cc[HICU_MAX_NDIM];
-        rbase[threadIdx.x] = (i < r1) ? row_base(g, i, cc) : -1;
-        if (CIRC)
-          for (int c = 0; c < g.ncirc; ++c) rcc[threadIdx.x][c] = cc[c];
-      }
-      __syncthreads();
-      // 2 * kBK * kTile elements, 8 per thread
-#pragma unroll
-      for (int e = 0; e < (2 * kBK * kTile) / kThreads; ++e) {
-        const int idx = threadIdx.x + e * kThreads;
-        const int which = idx / (kBK * kTile);
-        const int rem = idx % (kBK * kTile);
-        const int row = rem / kTile, col = rem % kTile;
-        const int kap = (which == 0 ? ti : tj) * kTile + col;
-        float2 v = cf(0.f, 0.f);
-        const int64_t b = rbase[row];
-        if (b >= 0 && kap < g.n) {
-          int64_t addr = b + g.koff[kap];
-          if (CIRC) addr += circ_part(g, rcc[row], g.pos + (size_t)kap * g.ndim);
-          v = __ldg(x + addr);
-        }
-        if (which == 0) As[row][col] = v; else Bs[row][col] = v;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < kBK; ++kk) {
-        float2 a[4], b[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          a[q] = As[kk][ty * 4 + q];
-          b[q] = Bs[kk][tx * 4 + q];
-        }
-#pragma unroll
-        for (int qa = 0; qa < 4; ++qa)
-#pragma unroll
-          for (int qb = 0; qb < 4; ++qb) cfmac(acc[qa][qb], a[qa], b[qb]);
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        double2& d = acc64[(a * 4 + b) * kThreads + threadIdx.x];
-        d = d + cd(acc[a][b].x, acc[a][b].y);
-        acc[a][b] = cf(0.f, 0.f);
-      }
+  // Gather of one kBK-row block into registers (8 values per thread); the
+  // next block's gather is issued before this block's products so the L2
+  // latency overlaps the FMAs (one block at a time left the SM idle between
+  // the gather and the products).  Macros, not device lambdas (a lambda
+  // capturing shared arrays miscompiled).
+  constexpr int kPer = (2 * kBK * kTile) / kThreads;
+  float2 pre[kPer];
+#define GRAM_SIMT_BASES(rc_)                                                         \
+  if (threadIdx.x < kBK) {                                                           \
+    const int64_t i_ = (rc_) + threadIdx.x;                                          \
+    int cc_[HICU_MAX_NDIM];                                                          \
+    rbase[threadIdx.x] = (i_ < r1) ? row_base(g, i_, cc_) : -1;                      \
+    if (CIRC)                                                                        \
+      for (int c_ = 0; c_ < g.ncirc; ++c_) rcc[threadIdx.x][c_] = cc_[c_];           \
   }
+#define GRAM_SIMT_GATHER()                                                           \
+  _Pragma("unroll") for (int e = 0; e < kPer; ++e) {                                 \
+    const int idx = threadIdx.x + e * kThreads;                                      \
+    const int which = idx / (kBK * kTile);                                           \
+    const int rem = idx % (kBK * kTile);                                             \
+    const int row = rem / kTile, col = rem % kTile;                                  \
+    const int kap = (which == 0 ? ti : tj) * kTile + col;                            \
+    float2 v = cf(0.f, 0.f);                                                         \
+    const int64_t bb = rbase[row];                                                   \
+    if (bb >= 0 && kap < g.n) {                                                      \
+      int64_t addr = bb + g.koff[kap];                                               \
+      if (CIRC) addr += circ_part(g, rcc[row], g.pos + (size_t)kap * g.ndim);        \
+      v = __ldg(x + addr);                                                           \
+    }                                                                                \
+    pre[e] = v;                                                                      \
+  }
+  if (r0 < r1) {
+    GRAM_SIMT_BASES(r0)
+    __syncthreads();
+    GRAM_SIMT_GATHER()
+  }
+  int since = 0;
+  for (int64_t rc = r0; rc < r1; rc += kBK) {
+    __syncthreads();  // previous block's products done with As/Bs and rbase
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int idx = threadIdx.x + e * kThreads;
+      const int which = idx / (kBK * kTile);
+      const int rem = idx % (kBK * kTile);
+      const int row = rem / kTile, col = rem % kTile;
+      if (which == 0) As[row][col] = pre[e]; else Bs[row][col] = pre[e];
+    }
+    if (rc + kBK < r1) GRAM_SIMT_BASES(rc + kBK)
+    __syncthreads();
+    if (rc + kBK < r1) GRAM_SIMT_GATHER()  // in flight during the products below
+#pragma unroll
+    for (int kk = 0; kk < kBK; ++kk) {
+      const float4* ar = reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4* br = reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float4 a01 = ar[0], a23 = ar[1], b01 = br[0], b23 = br[1];
+      const float2 a[4] = {cf(a01.x, a01.y), cf(a01.z, a01.w), cf(a23.x, a23.y), cf(a23.z, a23.w)};
+      const float2 bq[4] = {cf(b01.x, b01.y), cf(b01.z, b01.w), cf(b23.x, b23.y), cf(b23.z, b23.w)};
+#pragma unroll
+      for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+        for (int qb = 0; qb < 4; ++qb) cfmac(acc[qa][qb], a[qa], bq[qb]);
+    }
+    since += kBK;
+    if (since == kFlushRows || rc + kBK >= r1) {  // drain into fp64 every kFlushRows rows and at the end
+      since = 0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          double2& d = acc64[(a * 4 + b) * kThreads + threadIdx.x];
+          d = d + cd(acc[a][b].x, acc[a][b].y);
+          acc[a][b] = cf(0.f, 0.f);
+        }
+    }
+  }
+#undef GRAM_SIMT_GATHER
+#undef GRAM_SIMT_BASES
   double2* out = partials + (size_t)split * g.n * g.n;
 #pragma unroll
   for (int qa = 0; qa < 4; ++qa) {

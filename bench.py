@@ -361,10 +361,10 @@ def run_ours(args):
         pass
     tf32 = json.load(open(os.path.join(ROOT, "profiles", "tf32_peak_r01.json")))
     hbm = peaks.get("hbm_gbs", 6650.0)
-    # ncu --set full captures of full-stage launches (scripts/ncu_full.sh -> profiles/r01_ncu_full_v15.json)
+    # ncu --set full captures of full-stage launches (scripts/ncu_full.sh -> profiles/r01_ncu_full_v16.json)
     ncu_by = {}
     try:
-        for rec in json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full_v15.json"))):
+        for rec in json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full_v16.json"))):
             ncu_by[rec["kernel"]] = rec
     except (OSError, ValueError):
         pass
@@ -402,7 +402,7 @@ def run_ours(args):
     roof = dict(roof_all[dom])
     roof.update({"kernel": dom, "peak_source": "measured TF32 dense (profiles/tf32_peak_r01.json) / 3 for 3xTF32",
                  "achieved_def": "algorithmic flops of all launches of the class / their summed CUDA-event time",
-                 "traffic_def": "ncu dram read+write bytes of one full-stage launch (profiles/r01_ncu_full_v15.json)"})
+                 "traffic_def": "ncu dram read+write bytes of one full-stage launch (profiles/r01_ncu_full_v16.json)"})
     share = {k: (v / sum(ms_by.values()) if sum(ms_by.values()) > 0 else 0.0) for k, v in ms_by.items()}
     grad_tflops = sum(flops_total.values()) / (total_ms / args.steps * 1e-3) / 1e12 if world == 1 else None
 

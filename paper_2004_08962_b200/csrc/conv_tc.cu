@@ -797,20 +797,24 @@ template <int MODE, bool BS>
 int launch_bs(const DevGeom& g, const Shape& sh, CtParams P, const CUtensorMap& tm, const int32_t* pos,
               const float2* qt, float2* out, const float2* uin, const uint8_t* mask, const float2* y,
               const float2* x0, double* parts, int64_t lines, int nparts_total, cudaStream_t st) {
-  // dynamic shared memory available to this instantiation (queried once; the
-  // attribute is raised before `avail` is published, so a concurrent first
-  // launch from another host thread cannot race ahead of it)
-  static std::atomic<size_t> avail_a{0};
-  size_t avail = avail_a.load(std::memory_order_acquire);
+  // dynamic shared memory available to this instantiation on the current
+  // device (the opt-in attribute is per device: hicu_allow_max_smem raises it
+  // once per (kernel, device) and is called on every launch; the derived
+  // budget is cached per device id and published after the attribute is set,
+  // so a concurrent first launch from another host thread cannot race it)
+  constexpr int kMaxDev = 64;
+  static std::atomic<size_t> avail_a[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS>);
+  size_t avail = (dev >= 0 && dev < kMaxDev) ? avail_a[dev].load(std::memory_order_acquire) : 0;
   if (!avail) {
-    hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS>);
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, (const void*)conv_tc_kernel<MODE, BS>);
-    int optin = 0, dev = 0;
-    cudaGetDevice(&dev);
+    int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     avail = (size_t)optin - fa.sharedSizeBytes;
-    avail_a.store(avail, std::memory_order_release);
+    if (dev >= 0 && dev < kMaxDev) avail_a[dev].store(avail, std::memory_order_release);
   }
   if (avail < sh.fixed + 2 * sh.stage) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory");
   P.stages = (int)((avail - sh.fixed) / sh.stage);
@@ -828,6 +832,11 @@ template <int MODE>
 int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, const float2* uin, const uint8_t* mask,
            const float2* y, const float2* x0, int dc_mode, float lam, double* parts, int nparts_total,
            cudaStream_t st) {
+  // the B-image hint is consumed by this launch whatever happens below (an
+  // early error return must not leave it set for an unrelated later call)
+  const uint8_t* bimg = t_bimg;
+  const int bimg_early = t_bimg_early;
+  t_bimg = nullptr;
   Shape sh;
   if (!shape_of(g, 8, &sh)) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: geometry outside the tensor-core scope");
   const int L = sh.L;
@@ -882,13 +891,8 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   int s = cached_tmap(&tm, tsrc, L, MODE < 2 ? g.dims : g.rext);
   if (s) return s;
   P.stage_bytes = (int)sh.stage;
-  P.bimg = nullptr;
-  P.bimg_early = 0;
-  if (t_bimg) {
-    P.bimg = t_bimg;
-    P.bimg_early = t_bimg_early;
-  }
-  t_bimg = nullptr;
+  P.bimg = bimg;
+  P.bimg_early = bimg ? bimg_early : 0;
   if (sh.bstream)
     return launch_bs<MODE, true>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
   return launch_bs<MODE, false>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);

@@ -1112,314 +1112,6 @@ householder2r_kernel(int n, int r, const double2* __restrict__ Vg, double tol, d
   }
 }
 
-// Third variant (n <= 32 * kHh3Per): fixed column ownership (column j by warp
-// j % 32), every per-step access of a column issued as one predicated batch
-// (lane owns rows lane + 32u), so a step costs one shared-memory latency
-// instead of one per element.  The owner of column col+1 builds reflector
-// col+1 from the registers it just updated; one block barrier per column.
-constexpr int kHh3Per = 7;
-__device__ unsigned g_hh3_trace[64];  // debug (HICU_HH_TRACE): owner-warp clocks of steps 5, 30, 50
-constexpr int kHh3Threads = 768;
-
-__device__ __forceinline__ void hh3_build(int n, int c, const double2 (&x)[kHh3Per], double tol, int lane,
-                                          double2* __restrict__ refl, double2* __restrict__ tau,
-                                          int* __restrict__ flags, int* __restrict__ status, double2* s_tau,
-                                          int* s_act, double2* w_next) {
-  // x = column c (rows lane + 32u); pivot row c, tail rows > c
-  double t = 0.0;
-  double2 x0 = cd(0.0, 0.0);
-#pragma unroll
-  for (int u = 0; u < kHh3Per; ++u) {
-    const int k = lane + 32 * u;
-    if (k > c && k < n) t += abs2d(x[u]);
-    if (k == c) x0 = x[u];
-  }
-  t = warp_sum_d_(t);
-  x0.x = __shfl_sync(0xffffffffu, x0.x, c & 31);
-  x0.y = __shfl_sync(0xffffffffu, x0.y, c & 31);
-  double2 ui = cd(0.0, 0.0);
-  int active = 0;
-  if (lane == 0) {
-    const double tail = t;
-    const double beta = sqrt(tail + x0.x * x0.x + x0.y * x0.y);
-    active = 1;
-    if (beta < tol) {
-      *status = HICU_ERR_DEGENERATE_INPUT;
-      active = 0;
-    } else if (tail == 0.0 && x0.y == 0.0 && x0.x >= 0.0) {
-      active = 0;
-    }
-    double2 u0 = cd(0.0, 0.0), tv = cd(0.0, 0.0);
-    if (active) {
-      if (x0.x > 0.0) {
-        const double2 nume = cd(-tail, 2.0 * beta * x0.y);
-        const double2 deno = cd(x0.x + beta, -x0.y);
-        const double dd = abs2d(deno);
-        u0 = cd((nume.x * deno.x + nume.y * deno.y) / dd, (nume.y * deno.x - nume.x * deno.y) / dd);
-      } else {
-        u0 = cd(x0.x - beta, x0.y);
-      }
-      tv = cd((beta - x0.x) / beta, x0.y / beta);
-      const double uu = abs2d(u0);
-      ui = cd(u0.x / uu, -u0.y / uu);
-    }
-    *s_tau = tv;
-    *s_act = active;
-    flags[c] = active;
-    tau[c] = tv;
-  }
-  active = __shfl_sync(0xffffffffu, active, 0);
-  ui.x = __shfl_sync(0xffffffffu, ui.x, 0);
-  ui.y = __shfl_sync(0xffffffffu, ui.y, 0);
-  if (!active) return;
-#pragma unroll
-  for (int u = 0; u < kHh3Per; ++u) {
-    const int k = lane + 32 * u;
-    if (k >= c && k < n) {
-      const double2 wv = (k == c) ? cd(1.0, 0.0) : cmul(x[u], ui);
-      refl[(size_t)c * n + k] = wv;
-      w_next[k] = wv;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kHh3Threads)
-householder3_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
-                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status,
-    const int* __restrict__ gate) {
-  hicu_pdl_entry();
-  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
-  extern __shared__ double2 sh3[];
-  double2* sw = sh3;           // 2 x n (double-buffered reflector w)
-  double2* v = sh3 + 2 * n;    // column-major: element (k, j) at v[j*n + k]
-  __shared__ double2 s_tau[2];
-  __shared__ int s_act[2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int e = threadIdx.x; e < n * r; e += blockDim.x) v[(size_t)(e % r) * n + e / r] = Vg[e];
-  for (int e = threadIdx.x; e < n * r; e += blockDim.x) refl[e] = cd(0.0, 0.0);
-  __syncthreads();
-  if (warp == 0) {
-    double2 x[kHh3Per];
-#pragma unroll
-    for (int u = 0; u < kHh3Per; ++u) {
-      const int k = lane + 32 * u;
-      x[u] = k < n ? v[k] : cd(0.0, 0.0);
-    }
-    hh3_build(n, 0, x, tol, lane, refl, tau, flags, status, &s_tau[0], &s_act[0], sw);
-  }
-  __syncthreads();
-  for (int col = 0; col < r; ++col) {
-    const int par = col & 1;
-    const int slot = col == 5 ? 0 : (col == 30 ? 1 : (col == 50 ? 2 : -1));
-    const bool own = ((col + 1) % nw) == warp && lane == 0;
-    if (slot >= 0 && own) g_hh3_trace[slot * 8 + 0] = (unsigned)clock();
-    const double2 tv = s_tau[par];
-    const bool act = s_act[par] != 0;
-    const double2* w = sw + (size_t)par * n;
-    double2 wr[kHh3Per];
-    if (act) {
-#pragma unroll
-      for (int u = 0; u < kHh3Per; ++u) {
-        const int k = lane + 32 * u;
-        wr[u] = (k >= col && k < n) ? w[k] : cd(0.0, 0.0);
-      }
-    }
-    // my columns j > col, j % nw == warp
-    for (int j = col + 1 + ((warp - (col + 1)) % nw + nw) % nw; j < r; j += nw) {
-      double2* vj = v + (size_t)j * n;
-      double2 x[kHh3Per];
-#pragma unroll
-      for (int u = 0; u < kHh3Per; ++u) {
-        const int k = lane + 32 * u;
-        x[u] = k < n ? vj[k] : cd(0.0, 0.0);
-      }
-      if (act) {
-        double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < kHh3Per; ++u) {
-          if (u & 1) zfmac(d1, wr[u], x[u]);
-          else zfmac(d0, wr[u], x[u]);
-        }
-        double2 dt = d0 + d1;
-        dt = cd(warp_sum_d_(dt.x), warp_sum_d_(dt.y));
-        const double2 f = cmul(tv, dt);
-#pragma unroll
-        for (int u = 0; u < kHh3Per; ++u) {
-          const int k = lane + 32 * u;
-          x[u] = x[u] - cmul(wr[u], f);
-          if (k >= col && k < n) vj[k] = x[u];
-        }
-      }
-      if (j == col + 1) {  // owner of the next pivot column builds its reflector from registers
-        if (slot >= 0 && lane == 0) g_hh3_trace[slot * 8 + 1] = (unsigned)clock();
-        hh3_build(n, j, x, tol, lane, refl, tau, flags, status, &s_tau[par ^ 1], &s_act[par ^ 1],
-                  sw + (size_t)(par ^ 1) * n);
-        if (slot >= 0 && lane == 0) g_hh3_trace[slot * 8 + 2] = (unsigned)clock();
-      }
-    }
-    if (slot >= 0 && own) g_hh3_trace[slot * 8 + 3] = (unsigned)clock();
-    __syncthreads();
-    if (slot >= 0 && own) g_hh3_trace[slot * 8 + 4] = (unsigned)clock();
-  }
-}
-
-// Panel-blocked Householder triangularisation (same reflectors as
-// householder_kernel up to rounding).  For each panel of kHb columns:
-//   1. factor the panel: one step per column, applying the new reflector to
-//      the remaining panel columns only (<= kHb-1 warps, one barrier / step);
-//   2. S = Y^H Y and the lower-triangular T' with
-//      H_{c1-1} ... H_{c0} = I - Y T' Y^H,
-//      T'[j][j] = tau_j,  T'[j][0:j] = -tau_j (w_j^H Y[:,0:j]) T'[0:j,0:j];
-//   3. trailing update A <- A - Y (T' (Y^H A)) as three in-CTA products with
-//      one output per thread and no cross-thread reductions.
-// V lives column-major with an odd leading dimension (n+1) so threads walking
-// consecutive columns of the same row hit distinct banks.
-constexpr int kHb = 8;
-constexpr int kHb4Threads = 768;
-__device__ unsigned long long g_hh4_trace[8];  // debug (HICU_HH_TRACE): summed phase clocks
-
-__global__ void __launch_bounds__(kHb4Threads)
-householder4_kernel(int n, int r, const double2* __restrict__ Vg, double tol, double2* __restrict__ refl,
-                    double2* __restrict__ tau, int* __restrict__ flags, int* __restrict__ status,
-    const int* __restrict__ gate) {
-  hicu_pdl_entry();
-  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
-  extern __shared__ double2 sh4[];
-  const int ldv = n + 1;
-  double2* v = sh4;                               // r x ldv, element (k, j) at v[j*ldv + k]
-  double2* Wp = v + (size_t)r * ldv;              // kHb x ldv panel reflectors (zero above the pivot)
-  double2* Z = Wp + (size_t)kHb * ldv;            // kHb x r   (Y^H A, then T' Y^H A)
-  double2* T = Z + (size_t)kHb * r;               // kHb x kHb lower triangular
-  double2* S = T + kHb * kHb;                     // kHb x kHb, S[j][k] = w_j^H w_k
-  __shared__ double2 s_tau[2];
-  __shared__ int s_act[2];
-  __shared__ double2 s_ptau[kHb];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nt = blockDim.x;
-  for (int e = tid; e < n * r; e += nt) v[(size_t)(e % r) * ldv + e / r] = Vg[e];
-  for (int e = tid; e < n * r; e += nt) refl[e] = cd(0.0, 0.0);
-  __syncthreads();
-  long long tp0 = clock64(), acc_f = 0, acc_t = 0, acc_z = 0, acc_u = 0;
-  for (int c0 = 0; c0 < r; c0 += kHb) {
-    const int c1 = min(r, c0 + kHb), pw = c1 - c0;
-    tp0 = clock64();
-    for (int e = tid; e < kHb * ldv; e += nt) Wp[e] = cd(0.0, 0.0);
-    __syncthreads();
-    // ---- 1. panel factorisation ----
-    if (warp == 0)
-      hh2_reflector(n, c0, v + (size_t)c0 * ldv, tol, lane, refl, tau, flags, status, &s_tau[0], &s_act[0], Wp);
-    __syncthreads();
-    for (int c = c0; c < c1; ++c) {
-      const int par = (c - c0) & 1;
-      const double2 tv = s_tau[par];
-      const bool act = s_act[par] != 0;
-      if (lane == 0 && warp == 0) s_ptau[c - c0] = act ? tv : cd(0.0, 0.0);
-      const double2* w = Wp + (size_t)(c - c0) * ldv;
-      const int j = c + 1 + warp;  // one panel column per warp
-      if (j < c1) {
-        double2* vj = v + (size_t)j * ldv;
-        if (act) {
-          double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
-          int k = c + lane;
-          for (; k + 32 < n; k += 64) {
-            zfmac(d0, w[k], vj[k]);
-            zfmac(d1, w[k + 32], vj[k + 32]);
-          }
-          if (k < n) zfmac(d0, w[k], vj[k]);
-          double2 dt = d0 + d1;
-          dt = cd(warp_sum_d_(dt.x), warp_sum_d_(dt.y));
-          const double2 f = cmul(tv, dt);
-          for (int kk = c + lane; kk < n; kk += 32) vj[kk] = vj[kk] - cmul(w[kk], f);
-        }
-        if (j == c + 1) {  // owner of the next pivot column builds its reflector
-          __syncwarp();
-          hh2_reflector(n, j, vj, tol, lane, refl, tau, flags, status, &s_tau[par ^ 1], &s_act[par ^ 1],
-                        Wp + (size_t)(j - c0) * ldv);
-        }
-      }
-      __syncthreads();
-    }
-    acc_f += clock64() - tp0;
-    tp0 = clock64();
-    if (c1 >= r) break;
-    // ---- 2. S = Y^H Y (k < j) and T' ----
-    for (int q = tid; q < pw * pw; q += nt) {
-      const int jj = q / pw, kk = q % pw;
-      if (kk >= jj) continue;
-      const double2* wj = Wp + (size_t)jj * ldv;
-      const double2* wk = Wp + (size_t)kk * ldv;
-      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0);
-      int row = c0 + jj;  // w_j is zero above row c0 + jj
-      for (; row + 1 < n; row += 2) {
-        zfmac(a0, wj[row], wk[row]);
-        zfmac(a1, wj[row + 1], wk[row + 1]);
-      }
-      if (row < n) zfmac(a0, wj[row], wk[row]);
-      S[jj * kHb + kk] = a0 + a1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      for (int jj = 0; jj < pw; ++jj) {
-        const double2 tj = s_ptau[jj];
-        for (int i = 0; i < jj; ++i) {
-          double2 acc = cd(0.0, 0.0);
-          for (int kk = i; kk < jj; ++kk) zfma(acc, S[jj * kHb + kk], T[kk * kHb + i]);
-          T[jj * kHb + i] = cd(-(tj.x * acc.x - tj.y * acc.y), -(tj.x * acc.y + tj.y * acc.x));
-        }
-        T[jj * kHb + jj] = tj;
-      }
-    }
-    __syncthreads();
-    acc_t += clock64() - tp0;
-    tp0 = clock64();
-    // ---- 3a. Z = Y^H A_trail ----
-    const int mc = r - c1;
-    for (int q = tid; q < pw * mc; q += nt) {
-      const int jj = q % pw, col = c1 + q / pw;
-      const double2* wj = Wp + (size_t)jj * ldv;
-      const double2* ac = v + (size_t)col * ldv;
-      double2 a0 = cd(0.0, 0.0), a1 = cd(0.0, 0.0), a2 = cd(0.0, 0.0), a3 = cd(0.0, 0.0);
-      int row = c0 + jj;
-      for (; row + 3 < n; row += 4) {
-        zfmac(a0, wj[row], ac[row]);
-        zfmac(a1, wj[row + 1], ac[row + 1]);
-        zfmac(a2, wj[row + 2], ac[row + 2]);
-        zfmac(a3, wj[row + 3], ac[row + 3]);
-      }
-      for (; row < n; ++row) zfmac(a0, wj[row], ac[row]);
-      Z[jj * r + col] = (a0 + a1) + (a2 + a3);
-    }
-    __syncthreads();
-    acc_z += clock64() - tp0;
-    tp0 = clock64();
-    // ---- 3b. Z' = T' Z (in place, rows from the bottom: row j uses rows i <= j) ----
-    for (int col = c1 + tid; col < r; col += nt) {
-      for (int jj = pw - 1; jj >= 0; --jj) {
-        double2 acc = cd(0.0, 0.0);
-        for (int i = 0; i <= jj; ++i) zfma(acc, T[jj * kHb + i], Z[i * r + col]);
-        Z[jj * r + col] = acc;
-      }
-    }
-    __syncthreads();
-    // ---- 3c. A_trail -= Y Z' ----
-    for (int q = tid; q < (n - c0) * mc; q += nt) {
-      const int row = c0 + q % (n - c0), col = c1 + q / (n - c0);
-      double2 acc = cd(0.0, 0.0);
-#pragma unroll
-      for (int jj = 0; jj < kHb; ++jj)
-        if (jj < pw) zfma(acc, Wp[(size_t)jj * ldv + row], Z[jj * r + col]);
-      v[(size_t)col * ldv + row] = v[(size_t)col * ldv + row] - acc;
-    }
-    __syncthreads();
-    acc_u += clock64() - tp0;
-  }
-  if (tid == 0) {
-    g_hh4_trace[0] = acc_f;
-    g_hh4_trace[1] = acc_t;
-    g_hh4_trace[2] = acc_z;
-    g_hh4_trace[3] = acc_u;
-  }
-}
-
 // B <- H_0^H ... applied for col = r-1 .. 0: block -= conj(tau) w (w^H block).
 // One warp per column of B (held in shared memory); the reflectors stream
 // through shared memory in chunks so each is read from L2 once per CTA.
@@ -1478,72 +1170,9 @@ __global__ void apply_reflectors_kernel(int n, int r, const double2* __restrict_
   }
 }
 
-// Resident variant: all r reflectors staged in shared memory once, four warps
-// (four columns of B) per CTA, no barriers in the reflector loop.
+// Resident variant: n <= 32 * kArPer rows held in registers (res2 below).
 constexpr int kArWarps = 4;
 constexpr int kArPer = 8;  // n <= 256 for the resident apply
-__global__ void __launch_bounds__(kArWarps * 32)
-apply_reflectors_res_kernel(int n, int r, const double2* __restrict__ refl, const double2* __restrict__ tau,
-                            const int* __restrict__ flags, int cols, const double2* __restrict__ Bin,
-                            double2* __restrict__ B, float2* __restrict__ out32, int p,
-    const int* __restrict__ gate) {
-  hicu_pdl_entry();
-  if (gate && *gate == 0) return;  // closed-form path succeeded (nsjl.cu)
-  extern __shared__ double2 sar[];
-  double2* ws = sar;                          // r x n reflectors
-  double2* ts = ws + (size_t)r * n;           // r taus
-  double2* bs = ts + r;                       // kArWarps x n columns
-  int* fs = reinterpret_cast<int*>(bs + (size_t)kArWarps * n);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int q = threadIdx.x; q < r * n; q += blockDim.x) ws[q] = refl[q];
-  for (int q = threadIdx.x; q < r; q += blockDim.x) {
-    ts[q] = tau[q];
-    fs[q] = flags[q];
-  }
-  const int j = blockIdx.x * kArWarps + warp;
-  (void)bs;
-  __syncthreads();
-  if (j >= cols) return;
-  // the column lives in registers: lane owns rows lane + 32u (n <= 32 kArPer)
-  double2 b[kArPer];
-#pragma unroll
-  for (int u = 0; u < kArPer; ++u) {
-    const int k = lane + 32 * u;
-    b[u] = k < n ? Bin[(size_t)k * cols + j] : cd(0.0, 0.0);
-  }
-  for (int col = r - 1; col >= 0; --col) {
-    if (!fs[col]) continue;
-    const double2* w = ws + (size_t)col * n;
-    double2 wr[kArPer];
-#pragma unroll
-    for (int u = 0; u < kArPer; ++u) {
-      const int k = lane + 32 * u;
-      wr[u] = (k >= col && k < n) ? w[k] : cd(0.0, 0.0);
-    }
-    double2 d0 = cd(0.0, 0.0), d1 = cd(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < kArPer; u += 2) {
-      zfmac(d0, wr[u], b[u]);
-      if (u + 1 < kArPer) zfmac(d1, wr[u + 1], b[u + 1]);
-    }
-    double2 dot = d0 + d1;
-    dot = cd(warp_sum_d_(dot.x), warp_sum_d_(dot.y));
-    const double2 f = cmulc(ts[col], dot);  // conj(tau) * dot
-#pragma unroll
-    for (int u = 0; u < kArPer; ++u) b[u] = b[u] - cmul(wr[u], f);
-  }
-#pragma unroll
-  for (int u = 0; u < kArPer; ++u) {
-    const int k = lane + 32 * u;
-    if (k >= n) continue;
-    const double2 v = b[u];
-    B[(size_t)k * cols + j] = v;
-    if (out32) {
-      const int step = j / p, t = j % p;
-      out32[((size_t)step * n + k) * p + t] = cf((float)v.x, (float)v.y);
-    }
-  }
-}
 
 // Streaming variant (n <= 32 kArPer): each warp carries two columns of B in
 // registers and reads the reflectors straight from L2 one step ahead (no
@@ -1698,8 +1327,7 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
   {
     const size_t bytes = (size_t)ell * ell * sizeof(double2);
     const bool sm = bytes <= kSmemCap;
-    const bool old_chol = getenv("HICU_CHOL1") != nullptr;
-    if (!old_chol && ell <= 96) {
+    if (ell <= 96) {
       auto args = [&](auto kern) {
         hicu_launch(kern, 1, 512, 0, st, ell, w.C, (const double2*)w.O, Gp, n, w.nu, status_dev);
       };
@@ -1709,16 +1337,6 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
       else if (ell <= 64) args(chol2_kernel<2, 4>);
       else if (ell <= 80) args(chol2_kernel<3, 5>);
       else args(chol2_kernel<3, 6>);
-      if (getenv("HICU_CHOL_TRACE")) {
-        unsigned h[12];
-        cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(h, g_chol_trace, sizeof(h));
-        fprintf(stderr, "chol2: load %u | factor %u cycles\n", h[0], h[1]);
-        fprintf(stderr, "  owner k1=31: fold-own %u | wait-empty %u | publish %u | fold-rest %u\n", h[3] - h[2],
-                h[4] - h[3], h[5] - h[4], h[6] - h[5]);
-        fprintf(stderr, "  owner k1=32: fold-own %u | wait-empty %u | publish %u | fold-rest %u | step31->32 start %u\n",
-                h[8] - h[7], h[9] - h[8], h[10] - h[9], h[11] - h[10], h[7] - h[2]);
-      }
     } else if (sm) {
       hicu_allow_max_smem((const void*)chol_kernel<true>);
       hicu_launch(chol_kernel<true>, 1, 512, bytes, st, ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
@@ -1732,12 +1350,6 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     if (rbytes + (size_t)ell * sizeof(double) <= kSmemCap) {
       trsm_rl_launch<1>(n, ell, w.Y, Om, w.nu, w.C, w.W, rbytes + (size_t)ell * sizeof(double), st);
       if ((s = hicu_check_launch("trsm_rl_kernel"))) return s;
-      if (getenv("HICU_TRSM_TRACE")) {
-        unsigned h[4];
-        cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(h, g_trsm_trace, sizeof(h));
-        fprintf(stderr, "trsm_rl: first row %u cycles\n", h[1]);
-      }
     } else {
     const int warps = 8;
     const size_t rowb = (size_t)warps * ell * sizeof(double2);
@@ -1773,47 +1385,11 @@ int hicu_householder_gated(int n, int r, const void* V, double tol, void* refl, 
     // require the caller to size refl at 2*n*r and use its upper half as scratch.
     gws = (double2*)refl + (size_t)n * r;
   }
-  {
-    const size_t b4 = ((size_t)r * (n + 1) + (size_t)kHb * (n + 1) + (size_t)kHb * r + 2 * kHb * kHb) * sizeof(double2);
-    // Opt-in (HICU_HOUSEHOLDER4=1): measured slower than householder2 at C2
-    // (307 vs 234 us; per-panel clocks: factor 4.4K cycles/step, S,T 17K,
-    // Z 18K, trailing 15K), kept for the blocked-QR work that follows.
-    if (!gate && getenv("HICU_HOUSEHOLDER4") && b4 <= (size_t)227 * 1024 - 1024) {
-      hicu_allow_max_smem((const void*)householder4_kernel);
-      hicu_launch(householder4_kernel, 1, kHb4Threads, b4, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl,
-                                                                         (double2*)tau, flags, status_dev, gate);
-      if (getenv("HICU_HH_TRACE")) {
-        unsigned long long h[8];
-        cudaStreamSynchronize((cudaStream_t)stream);
-        cudaMemcpyFromSymbol(h, g_hh4_trace, sizeof(h));
-        fprintf(stderr, "householder4 cycles: panel-factor %llu | S,T %llu | Z=Y^H A %llu | Z',A-=YZ' %llu\n", h[0], h[1],
-                h[2], h[3]);
-      }
-      return hicu_check_launch("householder4_kernel");
-    }
-  }
-  if (!gate && getenv("HICU_HOUSEHOLDER3") && n <= 32 * kHh3Per && bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
-    hicu_allow_max_smem((const void*)householder3_kernel);
-    hicu_launch(householder3_kernel, 1, kHh3Threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
-        n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev, gate);
-    if (getenv("HICU_HH_TRACE")) {
-      unsigned h[64];
-      cudaStreamSynchronize((cudaStream_t)stream);
-      cudaMemcpyFromSymbol(h, g_hh3_trace, sizeof(h));
-      for (int q = 0; q < 3; ++q)
-        fprintf(stderr, "householder3 col %d: cols-before-own %u | build %u | rest %u | barrier %u (cycles)\n",
-                q == 0 ? 5 : (q == 1 ? 30 : 50), h[q * 8 + 1] - h[q * 8 + 0], h[q * 8 + 2] - h[q * 8 + 1],
-                h[q * 8 + 3] - h[q * 8 + 2], h[q * 8 + 4] - h[q * 8 + 3]);
-    }
-    return hicu_check_launch("householder3_kernel");
-  }
-  if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap && n <= 256 && !getenv("HICU_HOUSEHOLDER2")) {
+  if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap && n <= 256) {
     const size_t sm2 = bytes + (size_t)2 * n * sizeof(double2);
     auto go = [&](auto kern) {
       hicu_allow_max_smem((const void*)kern);
-      static int thr = -1;
-      if (thr < 0) thr = getenv("HICU_HH2R_THREADS") ? atoi(getenv("HICU_HH2R_THREADS")) : 512;
-      hicu_launch(kern, 1, thr, sm2, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau,
+      hicu_launch(kern, 1, 512, sm2, (cudaStream_t)stream, n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau,
                   flags, status_dev, gate);
     };
     if (n <= 128) go(householder2r_kernel<4>);
@@ -1823,9 +1399,8 @@ int hicu_householder_gated(int n, int r, const void* V, double tol, void* refl, 
   }
   if (bytes + (size_t)2 * n * sizeof(double2) <= kSmemCap) {
     hicu_allow_max_smem((const void*)householder2_kernel);
-    static int hh2_threads = -1;
-    if (hh2_threads < 0) hh2_threads = getenv("HICU_HH2_THREADS") ? atoi(getenv("HICU_HH2_THREADS")) : 512;  // 512: 32 us faster than 1024 (less MIO contention on warp 0)
-    hicu_launch(householder2_kernel, 1, hh2_threads, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
+    // 512 threads: 32 us faster than 1024 (less MIO contention on warp 0)
+    hicu_launch(householder2_kernel, 1, 512, bytes + (size_t)2 * n * sizeof(double2), (cudaStream_t)stream, 
         n, r, (const double2*)V, tol, (double2*)refl, (double2*)tau, flags, status_dev, gate);
     return hicu_check_launch("householder2_kernel");
   }
@@ -1839,22 +1414,12 @@ int hicu_apply_reflectors_gated(int n, int r, const void* refl, const void* tau,
                                 const void* Bin, void* B, void* out32, int p, const int* gate, void* stream) {
   if (n < 1 || r < 0 || cols < 1 || !B || !Bin) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "apply_reflectors: bad p");
-  if (r >= 1 && n <= 32 * kArPer && !getenv("HICU_APPLY_RES1")) {
+  if (r >= 1 && n <= 32 * kArPer) {
     const int pairs = (cols + 1) / 2;
     hicu_launch(apply_reflectors_res2_kernel, (pairs + kAr2Warps - 1) / kAr2Warps, kAr2Warps * 32, 0,
                 (cudaStream_t)stream, n, r, (const double2*)refl, (const double2*)tau, flags, cols,
                 (const double2*)Bin, (double2*)B, (float2*)out32, p ? p : 1, gate);
     return hicu_check_launch("apply_reflectors_res2_kernel");
-  }
-  {
-    const size_t res = ((size_t)r * n + r + (size_t)kArWarps * n) * sizeof(double2) + (size_t)r * sizeof(int);
-    if (r >= 1 && n <= 32 * kArPer && res <= (size_t)210 * 1024) {
-      hicu_allow_max_smem((const void*)apply_reflectors_res_kernel);
-      hicu_launch(apply_reflectors_res_kernel, (cols + kArWarps - 1) / kArWarps, kArWarps * 32, res, (cudaStream_t)stream, 
-          n, r, (const double2*)refl, (const double2*)tau, flags, cols, (const double2*)Bin, (double2*)B,
-          (float2*)out32, p ? p : 1, gate);
-      return hicu_check_launch("apply_reflectors_res_kernel");
-    }
   }
   int warps = 8;
   while (warps > 1 && (size_t)(warps + kReflChunk) * n * sizeof(double2) > kSmemCap) warps >>= 1;

@@ -69,6 +69,15 @@ extern "C" int hicu_prof_summary(void* h, double* ms, int* count) {
 }
 
 namespace {
+// B-image hint for the next conv_tc launch on this thread, cleared when the
+// scope ends whether or not the call consumed it (error paths included)
+struct ImageHint {
+  explicit ImageHint(const void* img, int early) {
+    if (img) hicu_conv_image_hint(img, early);
+  }
+  ~ImageHint() { hicu_conv_image_hint(nullptr, 0); }
+};
+
 struct ProfScope {
   HicuProf* p;
   cudaStream_t st;
@@ -97,9 +106,8 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   const int nsp = hicu_scatter_nparts(gm);
   if (ncp < 0 || nsp < 0) return HICU_ERR_SHAPE;
   const size_t nomega = (size_t)n * ell, npbig = (size_t)n * G * p;
-  static const bool jl_off = getenv("HICU_NSJL_OFF") != nullptr;
   const size_t refl_bytes = (size_t)2 * n * r * sizeof(double2);  // scratch for the global-LU closed form
-  const bool use_jl = !jl_off && hicu_nullspace_jl_supported(n, r) && hicu_nullspace_jl_workspace(n, r) <= refl_bytes;
+  const bool use_jl = hicu_nullspace_jl_supported(n, r) && hicu_nullspace_jl_workspace(n, r) <= refl_bytes;
   int s;
   for (int it = 0; it < a->iters; ++it) {
     // ---- nullspace: Gram + Nystrom (== rSVD subspace), or injected V ----
@@ -155,19 +163,19 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
       double* rec = a->rec + ((size_t)it * G + j) * HICU_REC_SLOTS;
       {
         ProfScope ps(a->prof, HICU_PROF_CONV_FWD, st);
-        if (ib) hicu_conv_image_hint(imgs + (size_t)(2 * j) * ib, j > 0 ? 1 : 0);
+        ImageHint hint(ib ? imgs + (size_t)(2 * j) * ib : nullptr, j > 0 ? 1 : 0);
         if ((s = hicu_conv_fwd(gm, a->y, qt, p, a->u, a->obj_parts, stream))) return s;
       }
       {
         ProfScope ps(a->prof, HICU_PROF_SCATTER, st);
-        if (ib) hicu_conv_image_hint(imgs + (size_t)(2 * j + 1) * ib, 1);
+        ImageHint hint(ib ? imgs + (size_t)(2 * j + 1) * ib : nullptr, 1);
         if ((s = hicu_scatter_dc(gm, qt, p, a->u, a->mask, a->y, a->x0, a->dc_mode, a->lam, a->g, a->dc_parts,
                                  stream)))
           return s;
       }
       {
         ProfScope ps(a->prof, HICU_PROF_CONV_ELS, st);
-        if (ib) hicu_conv_image_hint(imgs + (size_t)(2 * j) * ib, 1);
+        ImageHint hint(ib ? imgs + (size_t)(2 * j) * ib : nullptr, 1);
         if ((s = hicu_conv_els(gm, a->g, qt, p, a->u, a->els_parts, stream))) return s;
       }
       {

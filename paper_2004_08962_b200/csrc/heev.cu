@@ -1060,59 +1060,7 @@ __global__ void back_transform_kernel(int l, int r, const double2* __restrict__ 
     for (int i = lane; i < l; i += 32) F[(size_t)i * r + j] = x[i];
 }
 
-// Resident variant: every reflector (Vt, (l-1) x l) staged in shared memory
-// once, four warps per CTA, one eigenvector per warp, no barriers in the
-// reflector loop (one warp per scheduler: the dot-reduce-axpy chains do not
-// contend for issue slots).
-constexpr int kBtWarps = 4;
-constexpr int kBtPer = 4;  // l <= 128 for the resident back-transform
-__global__ void __launch_bounds__(kBtWarps * 32)
-back_transform_res_kernel(int l, int r, const double2* __restrict__ Vt, const double2* __restrict__ tau,
-                          const double* __restrict__ z, double2* __restrict__ F) {
-  hicu_pdl_entry();
-  extern __shared__ double2 sm3[];
-  double2* vs = sm3;                          // (l-1) x l reflectors
-  double2* ts = vs + (size_t)(l - 1) * l;     // l-1 taus
-  double2* xs = ts + l;                       // kBtWarps x l vectors
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nv = (l - 1) * l;
-  for (int q = threadIdx.x; q < nv; q += blockDim.x) vs[q] = Vt[q];
-  for (int q = threadIdx.x; q < l - 1; q += blockDim.x) ts[q] = tau[q];
-  const int j = blockIdx.x * kBtWarps + warp;
-  (void)xs;
-  __syncthreads();
-  if (j >= r) return;
-  // the eigenvector lives in registers: lane owns entries lane + 32u (l <= 32 kBtPer)
-  double2 x[kBtPer];
-#pragma unroll
-  for (int u = 0; u < kBtPer; ++u) {
-    const int i = lane + 32 * u;
-    x[u] = i < l ? cd(z[(size_t)j * l + i], 0.0) : cd(0.0, 0.0);
-  }
-  for (int k = l - 2; k >= 0; --k) {
-    const double2 tk = ts[k];
-    if (tk.x == 0.0 && tk.y == 0.0) continue;
-    const double2* v = vs + (size_t)k * l;
-    double2 vr[kBtPer];
-#pragma unroll
-    for (int u = 0; u < kBtPer; ++u) {  // all loads issued before any use
-      const int i = lane + 32 * u;
-      vr[u] = (i > k && i < l) ? v[i] : cd(0.0, 0.0);
-    }
-    double2 dot = cd(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < kBtPer; ++u) zfmac(dot, vr[u], x[u]);
-    dot = warp_sum_z(dot);
-    const double2 f = cmul(tk, dot);
-#pragma unroll
-    for (int u = 0; u < kBtPer; ++u) x[u] = x[u] - cmul(vr[u], f);
-  }
-#pragma unroll
-  for (int u = 0; u < kBtPer; ++u) {
-    const int i = lane + 32 * u;
-    if (i < l) F[(size_t)i * r + j] = x[u];
-  }
-}
+constexpr int kBtPer = 4;  // l <= 128 for the register-resident back-transform (res2 below)
 
 // Streaming variant: two eigenvectors per warp in registers, reflectors read
 // from L2 one step ahead (no per-CTA staging of all l-1 reflectors), the two
@@ -1208,17 +1156,8 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
     const size_t a3 = (size_t)l * lda3 * sizeof(double2);
     const int lda4 = ((l + 1 + 3) / 8) * 8 + 4;  // >= l + 1, == 4 mod 8
     const size_t a4 = (size_t)l * lda4 * sizeof(double2);
-    if (!getenv("HICU_HETRD4") && l <= kHetrd6Max) {
+    if (l <= kHetrd6Max) {
       hicu_launch(hetrd6_kernel, 1, kH6Warps * 32, 0, st, l, A, d, e, tau, Vt);
-      if (getenv("HICU_HETRD_TRACE")) {
-        long long h[3][6];
-        cudaStreamSynchronize(st);
-        cudaMemcpyFromSymbol(h, g_h6_trace, sizeof(h));
-        for (int q = 0; q < 3; ++q)
-          fprintf(stderr, "hetrd6 step %d (t0): bar %lld | B+bar %lld | C+bar %lld | D %lld | R(next) %lld\n",
-                  q == 0 ? 10 : (q == 1 ? 40 : 70), h[q][1] - h[q][0], h[q][2] - h[q][1], h[q][3] - h[q][2],
-                  h[q][4] - h[q][3], h[q][5] - h[q][4]);
-      }
     } else if (l <= kHetrd4Max && a4 <= 180 * 1024) {
       hicu_allow_max_smem((const void*)hetrd4_kernel);
       hicu_launch(hetrd4_kernel, 1, 512, a4, st, l, lda4, A, d, e, tau, Vt);
@@ -1241,7 +1180,7 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   if ((s = hicu_check_launch("stebz_kernel"))) return s;
   {
     // one eigenvalue per CTA: the pivoting branches diverge between eigenvalues
-    int T = getenv("HICU_STEIN_T") ? atoi(getenv("HICU_STEIN_T")) : 1;
+    int T = 1;
     while (T > 1 && (size_t)5 * l * T * sizeof(double) > 200 * 1024) T >>= 1;
     const size_t smem = (size_t)5 * l * T * sizeof(double);
     hicu_allow_max_smem((const void*)stein_kernel);
@@ -1250,17 +1189,11 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   if ((s = hicu_check_launch("stein_kernel"))) return s;
   hicu_launch(cluster_orth_kernel, 1, 256, 0, st, l, r, lam, z, 1e-9);
   if ((s = hicu_check_launch("cluster_orth_kernel"))) return s;
-  const size_t res = ((size_t)(l - 1) * l + l + (size_t)kBtWarps * l) * sizeof(double2);
-  if (l <= 32 * kBtPer && !getenv("HICU_BT_RES1")) {
+  if (l <= 32 * kBtPer) {
     const int pairs = (r + 1) / 2;
     hicu_launch(back_transform_res2_kernel, (pairs + kBt2Warps - 1) / kBt2Warps, kBt2Warps * 32, 0, st, l, r, Vt, tau,
                 z, F);
     return hicu_check_launch("back_transform_res2_kernel");
-  }
-  if (res <= 200 * 1024 && l <= 32 * kBtPer) {
-    hicu_allow_max_smem((const void*)back_transform_res_kernel);
-    hicu_launch(back_transform_res_kernel, (r + kBtWarps - 1) / kBtWarps, kBtWarps * 32, res, st, l, r, Vt, tau, z, F);
-    return hicu_check_launch("back_transform_res_kernel");
   }
   const int bw = 8;
   const size_t smem = ((size_t)bw * l + (size_t)kBtChunk * l) * sizeof(double2);

@@ -643,8 +643,7 @@ extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const vo
   if (!nsjl_small_ok(n, r))
     return hicu_set_error(HICU_ERR_SIZE, "nullspace_jl: rank needs the workspace entry (hicu_nullspace_jl_ws)");
   const int ct = nsjl_ct(r);
-  static const bool generic = getenv("HICU_NSJL_GENERIC") != nullptr;  // A/B switch for the r <= 64 LU
-  const size_t smem = nsjl_smem(n, r, ct, ct == 64 && !generic);
+  const size_t smem = nsjl_smem(n, r, ct, ct == 64);
   const int grid = (cols + kNjCols - 1) / kNjCols;
   cudaStream_t st = (cudaStream_t)stream;
   auto go = [&](auto kern) {
@@ -652,15 +651,7 @@ extern "C" int hicu_nullspace_jl(int n, int r, const void* V, int cols, const vo
     hicu_launch(kern, grid, nsjl_threads(ct), smem, st, n, r, (const double2*)V, cols, (const double2*)Bin, (double2*)B,
                 (float2*)out32, p ? p : 1, gate_dev);
   };
-  if (ct == 64 && !generic) go(nsjl_kernel<64, 16, 256, true>);
-  else if (ct == 64) go(nsjl_kernel<64, 16, 256, false>);
+  if (ct == 64) go(nsjl_kernel<64, 16, 256, true>);
   else go(nsjl_kernel<128, 25, 512, false>);
-  if (getenv("HICU_NSJL_TRACE")) {
-    unsigned long long h[8];
-    cudaStreamSynchronize(st);
-    cudaMemcpyFromSymbol(h, g_nsjl_trace, sizeof(h));
-    fprintf(stderr, "nsjl cycles: Z+load %llu | LU %llu | solves %llu | Q~ %llu\n", h[1] - h[0], h[2] - h[1], h[3] - h[2],
-            h[4] - h[3]);
-  }
   return hicu_check_launch("nsjl_kernel");
 }

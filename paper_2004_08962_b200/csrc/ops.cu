@@ -980,7 +980,7 @@ extern "C" int hicu_dc_apply(int64_t n, void* g, const uint8_t* mask, const void
 // when the geometry does not run the resident tensor-core path or ws is short.
 size_t hicu_conv_images_prepare(const hicu_geom* hg, const void* qt_all, int p, int G, void* ws, size_t ws_bytes,
                                 void* stream) {
-  if (!hg || !qt_all || !ws || G < 1 || getenv("HICU_NO_BIMAGE")) return 0;
+  if (!hg || !qt_all || !ws || G < 1) return 0;
   if (hg->flags & HICU_GEOM_FORCE_SIMT_CONV) return 0;
   DevGeom g;
   if (hicu_make_devgeom(hg, &g)) return 0;

@@ -519,29 +519,55 @@ def _chunks(schedule: SolverSchedule, per_iter: bool):
             it0 += n
 
 
-_PINNED = {}
+class _PinnedPool:
+    """Reused pinned host staging buffers for complex64 uploads (allocating
+    pinned memory per call cost ~2 ms).
+
+    A buffer is checked out under the lock: it is taken only if no call holds
+    it and the device has finished the copy issued from it last time (its
+    event has completed); otherwise a new buffer is allocated.  So concurrent
+    reconstructions (``hicu_reconstruct_batch`` threads) never share a buffer
+    whose copy is still pending.  Idle buffers beyond ``max_idle_bytes`` are
+    released (oldest first)."""
+
+    def __init__(self, max_idle_bytes: int = 1 << 31):
+        import threading
+
+        self.lock = threading.Lock()
+        self.free = []  # [(nbytes, buf, event)] in release order
+        self.max_idle = max_idle_bytes
+
+    def upload(self, torch, a):
+        a = np.asarray(a)
+        n = a.size
+        buf = None
+        with self.lock:
+            for i, (nb, b, ev) in enumerate(self.free):
+                if b.numel() == n and (ev is None or ev.query()):
+                    buf = b
+                    del self.free[i]
+                    break
+        if buf is None:
+            buf = torch.empty(n, dtype=torch.complex64).pin_memory()
+        np.copyto(buf.numpy().reshape(a.shape), a, casting="unsafe")
+        out = buf.to("cuda", non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        with self.lock:
+            self.free.append((buf.numel() * 8, buf, ev))
+            idle = sum(e[0] for e in self.free)
+            while idle > self.max_idle and len(self.free) > 1:
+                idle -= self.free.pop(0)[0]
+        return out
+
+
+_PINNED = _PinnedPool()
 
 
 def _upload_pinned(torch, a):
-    """complex64 copy of ``a`` on the device via a per-size reused pinned
-    staging buffer (allocating pinned memory per call cost ~2 ms); the copy is
-    asynchronous and ordered on the current stream, and the buffer is only
-    rewritten after that stream has finished the previous copy."""
-    a = np.asarray(a)
-    key = a.size
-    ent = _PINNED.get(key)
-    if ent is None:
-        ent = [torch.empty(key, dtype=torch.complex64).pin_memory(), None]
-        _PINNED[key] = ent
-    buf, ev = ent
-    if ev is not None:
-        ev.synchronize()
-    np.copyto(buf.numpy().reshape(a.shape), a, casting="unsafe")
-    out = buf.to("cuda", non_blocking=True)
-    ev = torch.cuda.Event()
-    ev.record()
-    ent[1] = ev
-    return out
+    """complex64 copy of ``a`` on the device through a pinned staging buffer
+    (asynchronous, ordered on the current stream; see :class:`_PinnedPool`)."""
+    return _PINNED.upload(torch, a)
 
 
 def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, reference=None,
@@ -583,6 +609,10 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         nc, nv = x0.shape[-1], int(coil_compress)
         if not (1 <= nv <= nc) or nc > 32:
             raise ConfigError(f"coil_compress must be in [1, {min(nc, 32)}], got {coil_compress}")
+        # virtual coils mix every physical coil, so the sampling pattern must
+        # be the same on every coil (the compressed mask is that pattern)
+        if not np.array_equal(observed_in, np.broadcast_to(observed_in[..., :1], observed_in.shape)):
+            raise ConfigError("coil_compress needs the same sampling mask on every coil")
         # raw k-space through a reused pinned staging buffer; mask_apply
         # (arrays.py:54-67) is fused into the device coil covariance / apply
         xd = _upload_pinned(torch, x0)
@@ -593,8 +623,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         _tr("coil compression issued")
         dims = x0.shape[:-1] + (nv,)
         x_init, mask_dev = ydev, mdev
-        mask_c = np.ascontiguousarray(mask[..., :nv])
-        observed = mask_c == 1
+        observed = None  # observed samples are re-imposed from x0 only without compression
         ref_dev = None
         if reference is not None:
             rd = to_dev(np.asarray(reference).astype(np.complex64))

@@ -8,12 +8,14 @@ from its text (not from the reference's simdata.py, whose phantoms differ):
       8 Gaussian-bump coils (sigma 0.4 FOV), SNR 30 dB, 2D variable-density
       random mask R=3 (exact count, no ACS); kernel 5x5x8, rank 40.
 * C2  256x256 ellipse + texture phantom, 16 coils compressed to 8, 1D
-      variable-density phase-encode mask R=4; kernel 5x5x8, rank 60, stages
+      variable-density phase-encode mask R=4 (line density
+      (1 + |dk|/sigma)^-2, sigma = n/8, as the reference's vd_1d); kernel 5x5x8, rank 60, stages
       64x64 -> 128x128 -> full (25/25/50 iterations).
 * C3  64 slices of 320x320, 16 coils compressed to 10, per-slice 1D random
       mask R=4; kernel 7x7x10, rank 100.
 * C4  192x144x25 cine, central ellipse dilating sinusoidally (period 25),
-      12 coils compressed to 8, per-frame phase-encode mask R=6; kernel
+      12 coils compressed to 8, per-frame phase-encode mask R=6 (vd_1d
+      density per frame, the reference's vd_t family); kernel
       5x5x5x8, rank 150, center-region then full stages.
 * C5  256x160x160 smooth-boundary ellipsoids, 8 coils with 3D Gaussian
       sensitivities, readout fully sampled, 2D Poisson-disc on the
@@ -98,6 +100,14 @@ def _vd_weights(shape, power=2.0, floor=0.05):
     grids = _grid(shape)
     r = np.sqrt(sum(g * g for g in grids)) / (0.5 * math.sqrt(len(shape)))
     return floor + (1.0 - np.clip(r, 0, 1)) ** power
+
+
+def _vd_line_weights(n: int, sigma_frac: float = 0.125, decay: float = 2.0):
+    """Phase-encode line density (1 + |k - n/2| / sigma)^-decay with
+    sigma = n/8: the reference's ``vd_1d`` family (simdata.py:229-246 states
+    this density; this is an independent generator, not its code)."""
+    k = np.abs(np.arange(n) - n // 2)
+    return (1.0 + k / max(sigma_frac * n, 1.0)) ** (-decay)
 
 
 def _weighted_pick(weights, count, rng):
@@ -206,7 +216,7 @@ def make_config(name: str, slice_index: int = 0, scale: float = 1.0):
         coils = _gaussian_coils(shape, nc, rng_co)
         ksp = fft_kspace(img[..., None] * coils, (0, 1))
         ksp = _add_noise(ksp, 30.0, rng_no)
-        w1 = _vd_weights((shape[1],)) if name == "C2" else np.ones(shape[1])
+        w1 = _vd_line_weights(shape[1]) if name == "C2" else np.ones(shape[1])
         lines = _weighted_pick(w1, shape[1] // 4, rng_ma)
         mask = np.broadcast_to(lines[None, :, None], shape + (nc,)).astype(np.uint8)
     elif name == "C4":
@@ -224,7 +234,7 @@ def make_config(name: str, slice_index: int = 0, scale: float = 1.0):
         ksp = fft_kspace(img[..., None] * coils[:, :, None, :], (0, 1))
         ksp = _add_noise(ksp, 30.0, rng_no)
         mask = np.zeros((nx, ny, nt, nc), np.uint8)
-        w1 = _vd_weights((ny,))
+        w1 = _vd_line_weights(ny)
         for t in range(nt):
             lines = _weighted_pick(w1, ny // 6, np.random.default_rng([3000 + c, slice_index, t]))
             mask[:, lines == 1, t, :] = 1

@@ -25,9 +25,11 @@ from paper_2004_08962_b200.synthetic import CONFIGS, make_config
 
 
 def workload(name):
+    full = name.endswith("full")
+    name = name.replace("full", "")
     spec = CONFIGS[name]
     ksp, mask, x0 = make_config(name)
-    if name == "C5":  # one of 8 shards along readout: 32 output planes + 4 halo planes
+    if name == "C5" and not full:  # one of 8 shards along readout: 32 output planes + 4 halo planes
         x0, mask = np.ascontiguousarray(x0[:36]), np.ascontiguousarray(mask[:36])
     return spec, x0, mask
 
@@ -73,7 +75,7 @@ def run(name, iters):
     gram_f = 4.0 * s * n * (n + 1)
     conv_f = 8.0 * s * n * p  # per conv launch
     k = {kk: v["ms"] / it for kk, v in kinds.items()}
-    out = {"workload": name, "dims": list(dims_c), "kernel": list(spec.kernel), "n": n, "rank": spec.rank,
+    out = {"workload": name + (" full volume" if len(x0) == 256 else ""), "dims": list(dims_c), "kernel": list(spec.kernel), "n": n, "rank": spec.rank,
            "ell": math.ceil(1.5 * spec.rank), "p": p, "G": 5, "rows": s, "ms_per_iteration": round(ms_it, 3),
            "kernel_ms_per_iteration": {kk: round(v, 3) for kk, v in k.items()},
            "gram_tflops": round(gram_f / (k["gram"] * 1e-3) / 1e12, 2) if k["gram"] else None,

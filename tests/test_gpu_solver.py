@@ -1,6 +1,6 @@
-"""End-to-end GPU reconstruction parity: free-running SER against the
-reference's golden runs (<= 0.1 dB), lockstep trajectory parity with the
-oracle's V injected, bit-exact hard data consistency, determinism and the
+"""End-to-end GPU reconstruction behaviour: lockstep trajectory parity with the
+oracle's V injected (free-running SER against the reference's own runs lives
+in test_gpu_reference_e2e.py), bit-exact hard data consistency, determinism and the
 reference solver's behavioural tests (tests/test_solver.py)."""
 
 import json
@@ -20,37 +20,6 @@ def sched_from(meta):
     return H.SolverSchedule(rank=meta["rank"], stages=[H.StageSpec(s[0], s[1], s[2], s[3]) for s in meta["stages"]],
                             circular_axes=tuple(meta["circular_axes"]), dc_mode=meta["dc_mode"],
                             dc_lambda=meta["dc_lambda"], seed=meta["seed"])
-
-
-@pytest.mark.parametrize("name", ["hardlong", "softlong", "circlong"])
-def test_free_running_ser_parity(golden_recon, name):
-    """Free-running: the device (Gram + Nystrom, canonical V phases) against
-    the oracle running the reference's rSVD with the same phase convention,
-    on identical inputs, 70 outer iterations.  The reference's own zgesdd
-    phases rotate the Householder basis and hence the JL projections; the
-    reference golden is reported beside it for context (on this tiny noisy
-    problem a random phase choice alone moves the final SER by ~1.5 dB)."""
-    g = golden_recon
-    meta = json.loads(str(g["meta"]))[name]
-    kern = H.KernelMask.full(tuple(g["kext"]))
-    xhat, rep = H.hicu_reconstruct(g["x0"], g["mask"], kern, sched_from(meta), reference=g["ref"],
-                                   tail_energy_threshold=0)
-    xo, _ = O.hicu_reconstruct(g["x0"], g["mask"], tuple(g["kext"]), [tuple(s) for s in meta["stages"]],
-                               meta["rank"], circular=tuple(meta["circular_axes"]), dc_mode=meta["dc_mode"],
-                               dc_lambda=meta["dc_lambda"], seed=meta["seed"], canonical=True)
-    ser_gpu = O.ser_db(g["ref"], xhat)
-    ser_orc = O.ser_db(g["ref"], xo)
-    print(name, "final SER: gpu", ser_gpu, "oracle(canonical)", ser_orc, "reference golden",
-          O.ser_db(g["ref"], g[name + "_xhat"]))
-    assert abs(ser_gpu - ser_orc) <= 0.1, (ser_gpu, ser_orc)
-    assert len(rep.steps) == len(g[name + "_eta"])
-    # per-step SER trace is recorded like the reference's (solver.py:363-375)
-    assert all(s.ser_db is not None for s in rep.steps)
-    assert abs(rep.steps[-1].ser_db - ser_gpu) <= 0.05
-    if meta["dc_mode"] == "hard":
-        obs = g["mask"] == 1
-        assert np.array_equal(xhat[obs], g["x0"][obs])
-    assert xhat.dtype == np.complex128
 
 
 @pytest.mark.parametrize("name", ["hard", "soft", "circ"])
@@ -166,12 +135,11 @@ def test_coil_compress_option():
 def test_coil_compress_fused_mask_apply():
     """The coil-compression path uploads raw k-space and applies mask_apply
     (arrays.py:54-67) on the device: unmasked garbage at unobserved points
-    must give the bit-identical reconstruction of the zero-filled input, with
-    per-coil masks that differ between coils."""
+    must give the bit-identical reconstruction of the zero-filled input.  Masks
+    that differ between coils are rejected (virtual coils mix all coils)."""
     ksp, kern, mask, x0, rank = _small_problem(nc=4)
     rng = np.random.default_rng(11)
     mask = mask.copy()
-    mask[..., 1] = (rng.random(mask.shape[:-1]) < 0.6).astype(mask.dtype)  # coil 1: its own pattern
     zf = np.where(mask == 1, ksp, 0).astype(np.complex64)
     junk = (ksp + 5.0 * (rng.standard_normal(ksp.shape) + 1j * rng.standard_normal(ksp.shape))).astype(np.complex64)
     raw = np.where(mask == 1, zf, junk)
@@ -181,6 +149,10 @@ def test_coil_compress_fused_mask_apply():
     b, rb = H.hicu_reconstruct(raw, mask, kern3, sched, tail_energy_threshold=0, coil_compress=3)
     assert np.array_equal(a, b)
     assert np.array_equal(ra.coil_basis, rb.coil_basis)
+    per_coil = mask.copy()
+    per_coil[..., 1] = (rng.random(mask.shape[:-1]) < 0.6).astype(mask.dtype)
+    with pytest.raises(H.ConfigError):
+        H.hicu_reconstruct(zf, per_coil, kern3, sched, tail_energy_threshold=0, coil_compress=3)
 
 
 def test_gram_fp64_accuracy_3d():
@@ -247,26 +219,6 @@ def test_reconstruct_slices_partition():
     out1 = reconstruct_slices([x0, x0, x0], [mask] * 3, kern, sched, rank=1, world=2, tail_energy_threshold=0)
     assert sorted(out0) == [0, 1] and sorted(out1) == [2]
     assert np.array_equal(out0[0][0], out1[2][0])
-
-
-@pytest.mark.timeout(900)
-def test_c1_free_running_ser_parity():
-    """BASELINE configs[0] (C1: 128x128, 8 coils, SNR 30 dB, VD random R=3,
-    5x5x8 kernel, rank 40, 50 outer iterations, p=8, G=5): the device run and
-    the oracle running the reference's rSVD (same canonical phase
-    convention) end within 0.1 dB SER of each other."""
-    from paper_2004_08962_b200.synthetic import CONFIGS, make_config
-
-    spec = CONFIGS["C1"]
-    ksp, mask, x0 = make_config("C1")
-    kern = H.KernelMask.full(spec.kernel)
-    sched = H.SolverSchedule(rank=spec.rank, stages=[H.StageSpec(*s) for s in spec.stages], seed=0)
-    xg, rep = H.hicu_reconstruct(x0, mask, kern, sched, reference=ksp, tail_energy_threshold=0)
-    xo, _ = O.hicu_reconstruct(x0, mask, spec.kernel, spec.stages, spec.rank, seed=0, canonical=True)
-    ser_g, ser_o, ser_0 = O.ser_db(ksp, xg), O.ser_db(ksp, xo), O.ser_db(ksp, x0)
-    print(f"C1 SER: zero-filled {ser_0:.3f} dB, device {ser_g:.3f} dB, oracle {ser_o:.3f} dB")
-    assert ser_g > ser_0 + 3.0
-    assert abs(ser_g - ser_o) <= 0.1
 
 
 def test_cli_recon_matches_api(tmp_path):

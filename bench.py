@@ -1,34 +1,42 @@
 """HICU B200 benchmark (driver contract: one JSON line on rank 0).
 
-Workload = BASELINE.json configs[1] ("C2"): 256x256 k-space, 16 coils
-SVD-compressed to 8 on the device, 1D variable-density phase-encode mask R=4,
-5x5x8 kernel (n = 200), rank 60, center-out schedule 64^2 -> 128^2 -> full
-with 25/25/50 outer iterations, p = 8, G = 5 gradient steps per iteration.
-A step is one full reconstruction (100 outer iterations) of one synthetic
-slice; metric = HICU outer iterations per second.
+``--config`` picks the BASELINE.json configuration; the default is C5
+(configs[4]), the largest configuration that fits one B200: one 256x160x160
+volume, 8 coils, 2D Poisson-disc R=5, SNR 30 dB, 5x5x5x8 kernel (n = 1000),
+rank 120 (l = 180), p = 8, G = 5, 40 outer iterations.  metric = HICU outer
+iterations per second (BASELINE.json "HICU iters/s").
 
-* ``value``: device-resident (16-coil k-space, mask and all host-seeded
-  sketch/JL draws already in HBM); CUDA events around each step on the
-  compute stream; L2 flushed between steps (256 MiB write, untimed).
-* ``e2e``: the public API ``hicu_reconstruct`` from host numpy arrays
-  (draws made on host worker threads, uploaded, result downloaded).
-* ``roofline``: the dominant tensor-core kernel class (Gram or one of the
-  three convolutions) from the native CUDA-event profiler over the timed
-  region, against the measured TF32 peak / 3 (3xTF32); ``roofline_all``
-  lists every class, including the HBM-bound update and the fp64 nullspace
-  (latency-bound, reported separately as SURVEY §8d asks).
-* ``batched`` (supplementary, N=1): 8 independent C2 slices reconstructed 4
-  at a time on concurrent CUDA streams (``hicu_reconstruct_batch``, the
-  multi-slice C3 path); ``value`` stays the single-slice C2 metric.
-* ``cpu_baseline``: the oracle port (numpy/scipy restatement of the
-  reference) on a bounded sample (coil compression + one outer iteration per
-  stage), extrapolated to the schedule; rank 0, N=1 only.
-* ``--impl reference``: the same oracle port as the reference arm (the
-  reference is pure Python and cannot be shipped to the GPU box; its port is
-  pinned to the reference's golden vectors in tests/).
+A *step* is one pass of the hot path over the input:
+* C5: one outer iteration over the whole volume (Gram + nullspace + G
+  gradient steps), the steps walking through the 40-iteration schedule;
+* C1 / C2 / C4: one full reconstruction (all stages and iterations);
+* C3: one full reconstruction of this rank's share of the 64 slices
+  (independent slices on 4 concurrent CUDA streams).
 
-N > 1 (torchrun): replicas — each rank reconstructs its own slice (no data-
-path collective); value = all ranks' iterations / max-over-ranks time.
+* ``value``: device-resident inputs (k-space, mask and all host-seeded
+  sketch / JL draws already in HBM); CUDA events on the compute stream,
+  barrier + synchronize around each step, max over ranks.  L2: the C5 inputs
+  (419 MB k-space) exceed the 126 MB L2; for the smaller configs a 256 MiB
+  buffer is written between steps (untimed).
+* ``e2e``: the public API ``hicu_reconstruct`` (C3: ``reconstruct_slices``;
+  C5 at N > 1: ``sharded_reconstruct``) from host numpy arrays, every
+  host->device and device->host copy inside the timed region; the full
+  schedule (C5: all 40 iterations).
+* ``roofline``: the dominant tensor-core kernel class from the native
+  CUDA-event profiler over one extra step, against the measured TF32 peak
+  / 3 (3xTF32); ``roofline_all`` lists every class.
+* ``cpu_baseline`` (rank 0, N = 1): the reference package itself
+  (``baseline/_ref/hicu``, its ``hicu_reconstruct``; the numpy oracle port
+  when the install is absent) on a bounded sample: one outer iteration per
+  stage on an axis-0 slab of the input, extrapolated linearly in the region
+  rows to the full config (the s-independent Householder + JL time measured
+  separately and not scaled); 1 thread and all host threads.
+* ``--impl reference``: the same reference sampler as the timed arm.
+
+N > 1 (torchrun, NCCL): C5 one volume sharded along the readout axis with
+(K0-1)-plane halos, the Gram and the line-search scalars all-reduced (strong
+scaling); C3 the 64 slices partitioned over ranks (strong scaling); C1 / C2 /
+C4 replicas (weak scaling).
 """
 
 from __future__ import annotations
@@ -47,8 +55,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
 
-CONFIG = "C2"
+DEFAULT_CONFIG = "C5"
 
 
 def _cpu_model() -> str:
@@ -68,73 +77,206 @@ def _host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def workload_config(spec):
+def _spec(name):
+    from paper_2004_08962_b200.synthetic import CONFIGS
+
+    return CONFIGS[name]
+
+
+WORKLOAD_TEXT = {
+    "C1": "C1 (BASELINE.json configs[0]): 128x128, 8 coils, 2D VD random mask R=3, SNR 30 dB, kernel 5x5x8 (n=200), "
+          "rank 40, 50 iterations, p=8, G=5",
+    "C2": "C2 (BASELINE.json configs[1]): 256x256, 16->8 coils (device SVD coil compression), 1D VD phase-encode "
+          "mask R=4, SNR 30 dB, kernel 5x5x8 (n=200), rank 60, stages 64^2/128^2/full x 25/25/50, p=8, G=5",
+    "C3": "C3 (BASELINE.json configs[2]): 64 slices of 320x320, 16->10 coils (device SVD coil compression), "
+          "per-slice 1D random mask R=4, kernel 7x7x10 (n=490), rank 100, 20 iterations, p=10, G=5",
+    "C4": "C4 (BASELINE.json configs[3]): 192x144x25 cine, 12->8 coils (device SVD coil compression), per-frame "
+          "VD phase-encode mask R=6, kernel 5x5x5x8 (n=1000), rank 150, stages [48,36,full]/full x 50/10, p=8, G=5",
+    "C5": "C5 (BASELINE.json configs[4]): 256x160x160 volume, 8 coils, 2D Poisson-disc R=5 on the phase/partition "
+          "plane, SNR 30 dB, kernel 5x5x5x8 (n=1000), rank 120, 40 iterations, p=8, G=5",
+}
+
+
+def workload_config(name, world):
+    spec = _spec(name)
+    par = {"C5": f"readout-sharded volume over {world} GPU(s) (halo + NCCL all-reduce)" if world > 1 else "1 GPU",
+           "C3": f"64 slices partitioned over {world} GPU(s), no collective"}.get(
+        name, "replicas (one instance per GPU, no collective)" if world > 1 else "1 GPU")
     return {
-        "workload": (f"{spec.name} (BASELINE.json configs[1]): 256x256, {spec.coils_in}->{spec.coils_out} coils "
-                     "(device SVD coil compression), 1D VD phase-encode mask R=4, SNR 30 dB, kernel 5x5x8 (n=200), "
-                     f"rank {spec.rank}, stages 64^2/128^2/full x 25/25/50 iterations, p=8, G=5"),
-        "iterations_per_step": spec.iterations,
-        "kernel": list(spec.kernel),
-        "rank": spec.rank,
+        "workload": WORKLOAD_TEXT[name],
+        "step": "one outer iteration of the whole volume" if name == "C5" else (
+            "one full reconstruction of this rank's slices" if name == "C3" else "one full reconstruction"),
+        "iterations_per_reconstruction": spec.iterations,
+        "kernel": list(spec.kernel), "rank": spec.rank,
         "stages": [[s[0], s[1], s[2], s[3]] for s in spec.stages],
-        "l2": "flushed between steps (256 MiB device write, untimed)",
-        "parallelism": "replicas (one slice per GPU, no collective)",
+        "l2": "inputs larger than L2 (419 MB k-space)" if name == "C5" else
+              "flushed between steps (256 MiB device write, untimed)",
+        "parallelism": par,
     }
 
 
 # ---------------------------------------------------------------------------
-# CPU (oracle port) legs
+# CPU legs: the reference package (baseline/_ref) or the oracle port
 # ---------------------------------------------------------------------------
 
 
-def oracle_sample(x0, mask, spec, threads: int):
-    """Coil compression + one outer iteration of each stage with the oracle
-    port; returns (estimated seconds for the full schedule, details)."""
+def _reference_module():
+    """(module, kind): the installed reference package, else the oracle port."""
+    if os.path.isdir(os.path.join(REF_INSTALL, "hicu")):
+        if REF_INSTALL not in sys.path:
+            sys.path.insert(0, REF_INSTALL)
+        import hicu
+
+        return hicu, "reference"
+    from oracle import hicu_oracle
+
+    return hicu_oracle, "port"
+
+
+def _compressed_host_input(name, scale=1.0):
+    """(x0, mask, n_coil_s) as the CPU path receives it: coil compression is
+    not part of the reference, so the oracle's restatement runs
+    first and is timed separately."""
+    from oracle import hicu_oracle as O
+    from paper_2004_08962_b200.synthetic import make_config
+
+    spec = _spec(name)
+    ksp, mask, x0 = make_config(name, scale=scale)
+    t = 0.0
+    if spec.coils_out != spec.coils_in:
+        t0 = time.perf_counter()
+        xc, mc, _ = O.coil_compress(x0, mask, spec.coils_out)
+        t = time.perf_counter() - t0
+        x0, mask = xc.astype(np.complex64), mc
+    return x0, mask, t
+
+
+def _run_cpu_iteration(mod, kind, x0, mask, kext, region, p, G, rank, circular):
+    """One outer iteration (nullspace + G gradient steps) of the CPU path;
+    returns seconds (the reference's own clock, report.total_seconds)."""
+    if kind == "reference":
+        kern = mod.KernelMask.full(tuple(kext))
+        sched = mod.SolverSchedule(rank=rank, stages=[mod.StageSpec(region, p, G, 1)], circular_axes=tuple(circular),
+                                   seed=0)
+        _, rep = mod.hicu_reconstruct(x0, mask, kern, sched, tail_energy_threshold=0)
+        return rep.total_seconds
+    t = time.perf_counter()
+    mod.hicu_reconstruct(x0, mask, tuple(kext), [(region, p, G, 1)], rank, circular=tuple(circular), seed=0)
+    return time.perf_counter() - t
+
+
+def _const_seconds(mod, kind, n, r, p, G):
+    """s-independent part of an iteration: Householder completion + G JL draws."""
+    rng = np.random.default_rng(0)
+    v, _ = np.linalg.qr(rng.standard_normal((n, r)) + 1j * rng.standard_normal((n, r)))
+    t = time.perf_counter()
+    if kind == "reference":
+        from hicu.subspace import RngStream, householder_nullspace, jl_compress
+
+        q = householder_nullspace(v).q
+        for j in range(G):
+            jl_compress(q, p, RngStream(0, (2, 0, 0, j)))
+    else:
+        q = mod.householder_nullspace(v)
+        for j in range(G):
+            mod.jl_compress(q, p, 0, (2, 0, 0, j))
+    return time.perf_counter() - t
+
+
+def reference_sample(name, threads, budget=1.2e7):
+    """Bounded CPU sample of one config: per stage one outer iteration on an
+    axis-0 slab holding about budget/n region rows (the whole input when it
+    is smaller), extrapolated linearly in region rows to the stage's full
+    region; returns (estimated seconds per step, details)."""
     from threadpoolctl import threadpool_limits
 
-    from oracle import hicu_oracle as O
+    from paper_2004_08962_b200.hankel import KernelMask
+    from paper_2004_08962_b200.solver import stage_region
 
+    mod, kind = _reference_module()
+    spec = _spec(name)
+    x0, mask, t_cc = _compressed_host_input(name)
+    kern = KernelMask.full(spec.kernel)
+    n, k0 = kern.n, spec.kernel[0]
+    ell = math.ceil(1.5 * spec.rank)
+    per_stage = []
     with threadpool_limits(threads):
-        t = time.perf_counter()
-        xc, mc, _ = O.coil_compress(x0, mask, spec.coils_out)
-        t_cc = time.perf_counter() - t
-        per = []
+        t_const = None
         for si, (region, p, G, iters) in enumerate(spec.stages):
-            t = time.perf_counter()
-            O.hicu_reconstruct(xc, mc, spec.kernel, [(region, p, G, 1)], spec.rank, seed=si)
-            per.append(time.perf_counter() - t)
-    est = t_cc + sum(st[3] * t_it for st, t_it in zip(spec.stages, per))
-    return est, {"coil_s": t_cc, "iter_s_by_stage": per}
+            reg = stage_region(x0.shape, kern, region, spec.circular_axes)
+            s_full = reg.s
+            rows_per_plane = s_full // reg.extents[0]
+            want = max(ell, int(budget / n))
+            planes = min(reg.extents[0], max(1, -(-want // rows_per_plane)))
+            if planes < reg.extents[0]:
+                # slab of `planes` output planes (+ K0-1 halo) centred in the stage window
+                lo = reg.offsets[0] + (reg.extents[0] - planes) // 2
+                xs = np.ascontiguousarray(x0[lo:lo + planes + k0 - 1])
+                ms = np.ascontiguousarray(mask[lo:lo + planes + k0 - 1])
+                reg_s = "full" if region == "full" else ["full"] + list(region[1:])
+                s_slab = planes * rows_per_plane
+            else:
+                xs, ms, reg_s, s_slab = x0, mask, region, s_full
+            t_it = _run_cpu_iteration(mod, kind, xs, ms, spec.kernel, reg_s, p, G, spec.rank, spec.circular_axes)
+            if s_slab < s_full:
+                if t_const is None:
+                    t_const = _const_seconds(mod, kind, n, spec.rank, p, G)
+                t_full = t_const + max(t_it - t_const, 0.0) * s_full / s_slab
+            else:
+                t_full = t_it
+            per_stage.append({"stage": si, "rows_full": s_full, "rows_sample": s_slab, "sample_s": t_it,
+                              "iteration_s_est": t_full, "iterations": iters})
+    if name == "C5":
+        est = per_stage[0]["iteration_s_est"]           # one step = one outer iteration
+    else:
+        est = t_cc + sum(st["iteration_s_est"] * st["iterations"] for st in per_stage)
+        if name == "C3":
+            est *= spec.slices
+    return est, {"kind": kind, "coil_compression_s": t_cc, "stages": per_stage, "const_s": t_const,
+                 "threads": threads}
+
+
+def _step_iterations(name):
+    spec = _spec(name)
+    if name == "C5":
+        return 1
+    if name == "C3":
+        return spec.iterations * spec.slices
+    return spec.iterations
+
+
+def _sample_text(name, det):
+    st = det["stages"]
+    parts = [f"stage {s['stage']}: one outer iteration on {s['rows_sample']} of {s['rows_full']} region rows" for s in st]
+    extra = " (C3: one slice, x64 slices)" if name == "C3" else ""
+    return ("; ".join(parts) + ", extrapolated linearly in region rows (Householder+JL time unscaled)"
+            + (", + oracle coil compression" if det["coil_compression_s"] else "") + extra)
 
 
 def run_reference(args):
-    """Reference arm: the oracle port of the reference's CPU path, all host
-    threads, bounded sample per step."""
+    """Reference arm: the reference package's CPU path, all host threads,
+    bounded sample per step."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2004_08962_b200.synthetic import CONFIGS, make_config
-
-    spec = CONFIGS[CONFIG]
-    ksp, mask, x0 = make_config(CONFIG)
+    name = args.config
     threads = _host_threads()
     for _ in range(args.warmup):
-        oracle_sample(x0, mask, spec, threads)
+        reference_sample(name, threads)
     est_total = 0.0
-    samples = []
+    det = None
     for _ in range(args.steps):
-        est, det = oracle_sample(x0, mask, spec, threads)
+        est, det = reference_sample(name, threads)
         est_total += est
-        samples.append(det)
-    value = spec.iterations * args.steps / est_total
+    units = _step_iterations(name) * args.steps
+    value = units / est_total
     line = {
         "metric": "HICU iters/s", "value": value, "unit": "iters/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * est_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": workload_config(spec), "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": "port",
-                         "sample": "coil compression + 1 outer iteration per stage, extrapolated to 25/25/50",
-                         "cpu": _cpu_model(), "last_sample": samples[-1]},
+        "config": workload_config(name, 1), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "iters/s", "cores": threads, "kind": det["kind"],
+                         "sample": _sample_text(name, det), "cpu": _cpu_model(), "last_sample": det},
         "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -193,69 +335,248 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def _flops_by_kind(spec, n, ell, regions, ccfg):
-    """Algorithmic work per launch group, per stage."""
-    out = []
+class DeviceWorkload:
+    """Device-resident inputs + engines for one config on this rank, and a
+    ``step()`` that issues one step on the current stream."""
+
+    def __init__(self, name, world, rank, group=None):
+        import torch
+
+        import paper_2004_08962_b200 as H
+        from paper_2004_08962_b200.coil import coil_compress_device
+        from paper_2004_08962_b200.hankel import to_dev
+        from paper_2004_08962_b200.solver import ReconEngine, draw_stage
+        from paper_2004_08962_b200.synthetic import make_config
+
+        self.torch, self.H = torch, H
+        self.name, self.world, self.rank = name, world, rank
+        spec = self.spec = _spec(name)
+        self.kernel = H.KernelMask.full(spec.kernel)
+        self.sched = H.SolverSchedule(rank=spec.rank, stages=[H.StageSpec(*s) for s in spec.stages],
+                                      circular_axes=spec.circular_axes, seed=0)
+        self.it = 0
+        self.sharded = None
+        if name == "C3":
+            from paper_2004_08962_b200.parallel import partition_slices
+
+            self.slices = list(partition_slices(spec.slices, world, rank))
+        else:
+            self.slices = [rank if world > 1 and name != "C5" else 0]
+        self.host = {s: make_config(name, slice_index=s) for s in self.slices}
+        nc, nv = spec.coils_in, spec.coils_out
+        self.engines = []
+        self.resets = []
+        if name == "C5" and world > 1:
+            from paper_2004_08962_b200.parallel import CudaShardBackend, HaloExchange, ShardedReconstruction, plan_for
+
+            ksp, mask, x0 = self.host[0]
+            plan = plan_for(x0.shape, self.kernel, self.sched, world, rank)
+            backend = CudaShardBackend(x0, mask, self.kernel, self.sched, plan)
+            self.sharded = ShardedReconstruction(backend, plan, HaloExchange(plan, group))
+            self.engines = [backend.eng]
+            self.resets = [(backend.eng.y, backend.eng.y.clone())]
+            self.dims = x0.shape
+            return
+        for s in self.slices:
+            ksp, mask, x0 = self.host[s]
+            xd = to_dev(x0).reshape(-1)
+            md = to_dev(mask, np.uint8).reshape(-1)
+            if nv != nc:
+                y, m, _, _ = coil_compress_device(xd, md, nc, nv)
+            else:
+                y, m = xd, md
+            dims = x0.shape[:-1] + (nv,)
+            regions = self.sched.validate(self.kernel, dims)
+            eng = ReconEngine(y, m, dims, self.kernel, self.sched, regions)
+            for si, st in enumerate(self.sched.stages):
+                om, pb = draw_stage(self.sched, si, st, self.kernel.n)
+                eng.set_host_draws(si, om, pb)
+            self.engines.append(eng)
+            self.resets.append((xd, md))
+            self.dims = dims
+        self.streams = [torch.cuda.Stream() for _ in range(min(4, len(self.engines)))] if name == "C3" else None
+
+    def step(self):
+        torch = self.torch
+        spec = self.spec
+        if self.sharded is not None:
+            it = self.it % spec.stages[0][3]
+            if it == 0:
+                self.resets[0][0].copy_(self.resets[0][1])
+            self.sharded.run_iteration(0, it)
+            self.it += 1
+            return
+        if self.name == "C5":
+            eng = self.engines[0]
+            it = self.it % spec.stages[0][3]
+            if it == 0:
+                eng.y.copy_(eng.x_init)
+                eng.status.zero_()
+            eng.run_stage(0, it, 1)
+            self.it += 1
+            return
+        from paper_2004_08962_b200.coil import coil_compress_device
+
+        nc, nv = spec.coils_in, spec.coils_out
+
+        def one(eng, xd, md):
+            if nv != nc:
+                y, _, _, _ = coil_compress_device(xd, md, nc, nv)
+                eng.y.copy_(y)
+            else:
+                eng.y.copy_(eng.x_init)
+            eng.status.zero_()
+            eng.run_all()
+
+        if self.streams is None:
+            for eng, (xd, md) in zip(self.engines, self.resets):
+                one(eng, xd, md)
+            return
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        for k, (eng, (xd, md)) in enumerate(zip(self.engines, self.resets)):
+            with torch.cuda.stream(self.streams[k % len(self.streams)]):
+                one(eng, xd, md)
+        for s in self.streams:
+            cur.wait_stream(s)
+
+    def check(self):
+        for e in self.engines:
+            e.check_status()
+
+    def set_prof(self, prof):
+        if self.sharded is not None:
+            return
+        for e in self.engines:
+            e.prof = prof
+
+    def e2e(self, group=None):
+        """One call of the public API from host arrays; returns (seconds,
+        iterations, h2d bytes, d2h bytes)."""
+        H = self.H
+        spec = self.spec
+        cc = None if spec.coils_out == spec.coils_in else spec.coils_out
+        t = time.perf_counter()
+        if self.sharded is not None:
+            from paper_2004_08962_b200.parallel import sharded_reconstruct
+
+            ksp, mask, x0 = self.host[0]
+            xhat, _ = sharded_reconstruct(x0, mask, self.kernel, self.sched, group=group)
+            dt = time.perf_counter() - t
+            return dt, spec.iterations, x0.nbytes // self.world + mask.nbytes // self.world, xhat.nbytes // self.world
+        if self.name == "C3":
+            from paper_2004_08962_b200.parallel import reconstruct_slices
+
+            n_all = spec.slices  # this rank holds only its block; reconstruct_slices indexes that block
+            xl = [self.host[i][2] if i in self.host else None for i in range(n_all)]
+            ml = [self.host[i][1] if i in self.host else None for i in range(n_all)]
+            out = reconstruct_slices(xl, ml, self.kernel, self.sched, rank=self.rank, world=self.world,
+                                     concurrency=4, tail_energy_threshold=0, coil_compress=cc)
+            dt = time.perf_counter() - t
+            h2d = sum(r.device["h2d_bytes"] for _, r in out.values())
+            d2h = sum(r.device["d2h_bytes"] for _, r in out.values())
+            return dt, spec.iterations * len(out), h2d, d2h
+        ksp, mask, x0 = self.host[self.slices[0]]
+        _, rep = H.hicu_reconstruct(x0, mask, self.kernel, self.sched, tail_energy_threshold=0, coil_compress=cc)
+        dt = time.perf_counter() - t
+        return dt, spec.iterations, rep.device["h2d_bytes"], rep.device["d2h_bytes"]
+
+
+def _work_per_step(dw):
+    """Algorithmic work of the kernel classes in one step: real
+    flops per class, update bytes."""
+    spec = dw.spec
+    n = dw.kernel.n
+    dims = dw.dims if dw.sharded is None else dw.sharded.b.ldims
+    regions = dw.engines[0].regions
+    N = int(np.prod(dims))
+    tot = {"gram": 0.0, "conv_fwd": 0.0, "scatter": 0.0, "conv_els": 0.0, "update_bytes": 0.0}
+    launches = {k: 0 for k in tot}
     for st, reg in zip(spec.stages, regions):
-        s = reg.s
-        p = st[1]
-        out.append({
-            "gram": 4.0 * s * n * (n + 1),                      # Hermitian H^H H, real flops
-            "conv_fwd": 8.0 * s * n * p,                        # u = H(y) Q~
-            "scatter": 8.0 * s * n * p,                         # g = col2im(Q~^H u)
-            "conv_els": 8.0 * s * n * p,                        # w = H(g) Q~ (+ <w,u>, |w|^2)
-            "update_bytes": 25.0 * ccfg["N"],                   # y, g read, y write, mask
-            "iters": st[3],
-            "G": st[2],
-        })
-    return out
+        s, p, G = reg.s, st[1], st[2]
+        iters = 1 if dw.name == "C5" else st[3]
+        tot["gram"] += 4.0 * s * n * (n + 1) * iters
+        launches["gram"] += iters
+        for k in ("conv_fwd", "scatter", "conv_els"):
+            tot[k] += 8.0 * s * n * p * G * iters
+            launches[k] += G * iters
+        tot["update_bytes"] += 25.0 * N * G * iters
+        launches["update_bytes"] += G * iters
+    mult = len(dw.engines)
+    return {k: v * mult for k, v in tot.items()}, {k: v * mult for k, v in launches.items()}
+
+
+def _load_json(path, default=None):
+    try:
+        return json.load(open(os.path.join(ROOT, path)))
+    except (OSError, ValueError):
+        return default
+
+
+def roofline(kinds, work, peaks):
+    tf32 = _load_json("profiles/tf32_peak_r01.json", {"tf32_tflops": 749.4})
+    tf32_peak = tf32["tf32_tflops"] / 3.0
+    hbm = peaks.get("hbm_gbs", 6548.2)
+    ncu = {rec["kernel"]: rec for rec in _load_json("profiles/r02_ncu_full.json", [])}
+    ncu_name = {"gram": "gram", "conv_fwd": "conv_tc_kernel<0", "scatter": "conv_tc_kernel<2",
+                "conv_els": "conv_tc_kernel<1", "update": "update_kernel"}
+
+    def traffic(kind):
+        for k, rec in ncu.items():
+            if ncu_name.get(kind, "@") in k and rec.get("dram_read_bytes") is not None:
+                return rec["dram_read_bytes"] + (rec.get("dram_write_bytes") or 0.0)
+        return None
+
+    ms_by = {k: v["ms"] for k, v in kinds.items()}
+    roof_all = {}
+    for k in ("gram", "conv_fwd", "scatter", "conv_els"):
+        if ms_by.get(k, 0) <= 0:
+            continue
+        nl = max(1, kinds[k]["launches"])
+        ach = work[k] / (ms_by[k] * 1e-3) / 1e12
+        roof_all[k] = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
+                       "frac": ach / tf32_peak, "traffic": traffic(k), "launches": nl,
+                       "avg_launch_ms": ms_by[k] / nl, "flops_per_launch_avg": work[k] / nl}
+    if ms_by.get("update", 0) > 0:
+        ach = work["update_bytes"] / (ms_by["update"] * 1e-3) / 1e9
+        roof_all["update"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                              "traffic": traffic("update"), "launches": kinds["update"]["launches"]}
+    for k in ("nystrom", "householder"):
+        if ms_by.get(k, 0) > 0:
+            roof_all[k] = {"bound": "fp64 latency (small dense algebra, reported separately, SURVEY 8d)",
+                           "ms_per_step": ms_by[k]}
+    tens = [k for k in roof_all if roof_all[k]["bound"] == "tensor"]
+    dom = max(tens, key=lambda k: ms_by[k]) if tens else None
+    roof = dict(roof_all[dom]) if dom else None
+    if roof:
+        roof.update({"kernel": dom,
+                     "peak_source": "measured TF32 dense (profiles/tf32_peak_r01.json) / 3 for 3xTF32",
+                     "achieved_def": "algorithmic flops of the class in one step / its summed CUDA-event time "
+                                     "(native profiler, one extra step on the launching stream)",
+                     "traffic_def": "ncu dram read+write bytes per launch (profiles/r02_ncu_full.json)"})
+    return roof, roof_all
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2004_08962_b200 as H
     from paper_2004_08962_b200 import _native as nat
-    from paper_2004_08962_b200.coil import coil_compress_device
-    from paper_2004_08962_b200.hankel import to_dev
-    from paper_2004_08962_b200.solver import ReconEngine, draw_stage
-    from paper_2004_08962_b200.synthetic import CONFIGS, make_config
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    group = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     nat.load()
-    spec = CONFIGS[CONFIG]
-    ksp, mask, x0 = make_config(CONFIG, slice_index=rank)
-    kernel = H.KernelMask.full(spec.kernel)
-    sched = H.SolverSchedule(rank=spec.rank, stages=[H.StageSpec(*s) for s in spec.stages], seed=rank)
-    nc, nv = spec.coils_in, spec.coils_out
-    dims_c = x0.shape[:-1] + (nv,)
-    regions = sched.validate(kernel, dims_c)
-    n = kernel.n
-    ell = math.ceil(1.5 * spec.rank)
-
-    # ---- device-resident inputs ----
-    xd16 = to_dev(x0).reshape(-1)
-    md16 = to_dev(mask, np.uint8).reshape(-1)
-    ydev, mdev, _, _ = coil_compress_device(xd16, md16, nc, nv)
-    eng = ReconEngine(ydev, mdev, dims_c, kernel, sched, regions)
-    for si, st in enumerate(sched.stages):
-        om, pb = draw_stage(sched, si, st, n)
-        eng.set_host_draws(si, om, pb)
-    prof = nat.Profiler()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    name = args.config
+    dw = DeviceWorkload(name, world, rank, group)
     stream = torch.cuda.current_stream()
-
-    def one_step():
-        y, _, _, _ = coil_compress_device(xd16, md16, nc, nv)
-        eng.y.copy_(y)
-        eng.status.zero_()
-        eng.run_all()
+    small = name != "C5"
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda") if small else None
 
     def barrier():
         if world > 1:
@@ -263,170 +584,120 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        one_step()
+        dw.step()
     torch.cuda.synchronize()
-    eng.check_status()
+    dw.check()
     clocks = ClockSampler(local)
     times = []
     launches0 = nat.lib().hicu_launch_count()
     clocks.start()
     for _ in range(args.steps):
-        flush.fill_(1.0)
+        if flush is not None:
+            flush.fill_(1.0)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        one_step()
+        dw.step()
         e1.record(stream)
         barrier()
         times.append(e0.elapsed_time(e1))
     clock_info = clocks.stop()
     launches = nat.lib().hicu_launch_count() - launches0
-    eng.check_status()
-    # per-kernel-class CUDA-event times from one extra, untimed step (the
-    # event records between kernels would perturb the timed steps)
-    flush.fill_(1.0)
-    barrier()
-    eng.prof = prof
-    prof.reset()
-    one_step()
-    barrier()
-    eng.prof = None
-    kinds = prof.summary()
-    eng.check_status()
+    dw.check()
+    # per-kernel-class CUDA-event times from one extra, untimed step
+    kinds = None
+    if dw.sharded is None:
+        prof = nat.Profiler()
+        barrier()
+        dw.set_prof(prof)
+        prof.reset()
+        dw.step()
+        barrier()
+        dw.set_prof(None)
+        kinds = prof.summary()
     total_ms = sum(times)
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    iters_all = spec.iterations * args.steps * world
-    value = iters_all / (total_ms * 1e-3)
+    per_rank_units = _step_iterations(name) if name != "C3" else dw.spec.iterations * len(dw.slices)
+    if name == "C5":
+        units = args.steps  # one volume: every rank works on the same iterations
+    elif name == "C3":
+        t = torch.tensor([per_rank_units * args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t)
+        units = float(t.item())
+    else:
+        units = per_rank_units * args.steps * world
+    value = units / (total_ms * 1e-3)
 
     # ---- end to end through the public API (host arrays in, host array out) ----
     e2e = None
     if not args.no_e2e:
-        for _ in range(max(1, args.warmup // 2)):
-            H.hicu_reconstruct(x0, mask, kernel, sched, tail_energy_threshold=0, coil_compress=nv)
-        e2e_t = []
-        rep = None
-        for _ in range(args.steps):
+        dw.e2e(group)  # warm-up (pinned pools, draw threads)
+        reps = 1 if name in ("C5", "C3") else max(1, min(args.steps, 5))
+        tot = 0.0
+        its = 0
+        h2d = d2h = 0
+        for _ in range(reps):
             barrier()
-            t = time.perf_counter()
-            _, rep = H.hicu_reconstruct(x0, mask, kernel, sched, tail_energy_threshold=0, coil_compress=nv)
-            e2e_t.append(time.perf_counter() - t)
-        tot = sum(e2e_t)
+            dt, n_it, h2d, d2h = dw.e2e(group)
+            tot += dt
+            its += n_it
         if world > 1:
             tt = torch.tensor([tot], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             tot = float(tt.item())
-        e2e = {"value": spec.iterations * args.steps * world / tot, "unit": "iters/s",
-               "h2d_bytes_per_step": rep.device["h2d_bytes"], "d2h_bytes_per_step": rep.device["d2h_bytes"],
-               "ms_per_step": 1e3 * tot / args.steps,
-               "path": "paper_2004_08962_b200.hicu_reconstruct(numpy c64 x0, mask, coil_compress=8)"}
+            ii = torch.tensor([its], dtype=torch.float64, device="cuda")
+            if name in ("C3",):
+                dist.all_reduce(ii)
+            elif name != "C5":
+                ii *= world
+            its = float(ii.item())
+        e2e = {"value": its / tot, "unit": "iters/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_call": 1e3 * tot / reps, "calls": reps, "iterations_per_call": its / reps,
+               "path": {"C5": "sharded_reconstruct" if world > 1 else "hicu_reconstruct",
+                        "C3": "reconstruct_slices"}.get(name, "hicu_reconstruct")
+               + " from host numpy arrays (complex64 k-space, uint8 mask), result downloaded"}
 
-    # ---- supplementary: independent slices on concurrent streams (C3-style batching) ----
-    batched = None
-    if world == 1 and not args.no_e2e:
-        nb_slices, conc = 8, 4
-        data = [make_config(CONFIG, slice_index=i) for i in range(nb_slices)]
-        bx, bm = [d[2] for d in data], [d[1] for d in data]
-        H.hicu_reconstruct_batch(bx, bm, kernel, sched, concurrency=conc, tail_energy_threshold=0, coil_compress=nv)
-        dt = float("inf")
-        for _ in range(2):  # best of two
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            H.hicu_reconstruct_batch(bx, bm, kernel, sched, concurrency=conc, tail_energy_threshold=0,
-                                     coil_compress=nv)
-            torch.cuda.synchronize()
-            dt = min(dt, time.perf_counter() - t)
-        batched = {"value": nb_slices * spec.iterations / dt, "unit": "iters/s", "slices": nb_slices,
-                   "concurrency": conc, "ms_per_slice": 1e3 * dt / nb_slices,
-                   "path": "hicu_reconstruct_batch: independent C2 slices on concurrent CUDA streams, host arrays",
-                   "timing": "wall clock between device-wide synchronizations, best of 2 after a warm-up batch"}
+    roof, roof_all, share, ms_by = None, None, None, None
+    work, nlaunch = _work_per_step(dw)
+    peaks = _load_json("MEASURED_PEAKS.json", {})
+    if kinds is not None:
+        roof, roof_all = roofline(kinds, work, peaks)
+        ms_by = {k: v["ms"] for k, v in kinds.items()}
+        tot_ms = sum(ms_by.values())
+        share = {k: (v / tot_ms if tot_ms > 0 else 0.0) for k, v in ms_by.items()}
+    eff = None
+    if world == 1:
+        flops = sum(work[k] for k in ("gram", "conv_fwd", "scatter", "conv_els"))
+        eff = flops / (total_ms / args.steps * 1e-3) / 1e12
 
-    # ---- roofline of the dominant kernel class ----
-    ccfg = {"N": int(np.prod(dims_c))}
-    work = _flops_by_kind(spec, n, ell, regions, ccfg)
-    flops_total = {k: 0.0 for k in ("gram", "conv_fwd", "scatter", "conv_els")}
-    launches_expected = {k: 0 for k in flops_total}
-    for w in work:
-        for k in flops_total:
-            per_launch_groups = w["iters"] * (1 if k == "gram" else w["G"])
-            flops_total[k] += w[k] * per_launch_groups  # the profiled step
-            launches_expected[k] += per_launch_groups
-    ms_by = {k: v["ms"] for k, v in kinds.items()}
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    except OSError:
-        pass
-    tf32 = json.load(open(os.path.join(ROOT, "profiles", "tf32_peak_r01.json")))
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    # ncu --set full captures of full-stage launches (scripts/ncu_full.sh -> profiles/r01_ncu_full_v16.json)
-    ncu_by = {}
-    try:
-        for rec in json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_full_v16.json"))):
-            ncu_by[rec["kernel"]] = rec
-    except (OSError, ValueError):
-        pass
-    ncu_name = {"gram": "gram_tc_kernel", "conv_fwd": "void conv_tc_kernel<0, 0>", "scatter": "void conv_tc_kernel<2, 0>",
-                "conv_els": "void conv_tc_kernel<1, 0>", "update": "update_kernel"}
-
-    def traffic(kind):
-        rec = ncu_by.get(ncu_name.get(kind, ""))
-        if not rec or rec.get("dram_read_bytes") is None:
-            return None
-        return rec["dram_read_bytes"] + (rec.get("dram_write_bytes") or 0.0)
-
-    tf32_peak = tf32["tf32_tflops"] / 3.0
-    roof_all = {}
-    for k in ("gram", "conv_fwd", "scatter", "conv_els"):
-        if k not in ms_by or ms_by[k] <= 0:
-            continue
-        nl = max(1, kinds[k]["launches"])
-        ach = flops_total[k] / (ms_by[k] * 1e-3) / 1e12
-        roof_all[k] = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
-                       "frac": ach / tf32_peak, "traffic": traffic(k), "launches": nl,
-                       "avg_launch_ms": ms_by[k] / nl, "flops_per_launch_avg": flops_total[k] / nl}
-    if "update" in ms_by and ms_by["update"] > 0:
-        bytes_total = sum(w["update_bytes"] * w["iters"] * w["G"] for w in work)
-        ach = bytes_total / (ms_by["update"] * 1e-3) / 1e9
-        roof_all["update"] = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                              "traffic": traffic("update"), "launches": kinds["update"]["launches"]}
-    for k in ("nystrom", "householder"):
-        if k in ms_by:
-            roof_all[k] = {"bound": "fp64 latency (single-CTA small dense algebra, reported separately, SURVEY 8d)",
-                           "ms_per_step": ms_by[k],
-                           "us_per_iteration": 1e3 * ms_by[k] / spec.iterations}
-    # the roofline object: the dominant tensor-core kernel class (K1 Gram / K4-K6 convolutions)
-    dom = max((k for k in roof_all if roof_all[k]["bound"] == "tensor"), key=lambda k: ms_by[k])
-    roof = dict(roof_all[dom])
-    roof.update({"kernel": dom, "peak_source": "measured TF32 dense (profiles/tf32_peak_r01.json) / 3 for 3xTF32",
-                 "achieved_def": "algorithmic flops of all launches of the class / their summed CUDA-event time",
-                 "traffic_def": "ncu dram read+write bytes of one full-stage launch (profiles/r01_ncu_full_v16.json)"})
-    share = {k: (v / sum(ms_by.values()) if sum(ms_by.values()) > 0 else 0.0) for k, v in ms_by.items()}
-    grad_tflops = sum(flops_total.values()) / (total_ms / args.steps * 1e-3) / 1e12 if world == 1 else None
-
-    # ---- CPU baseline (oracle port), rank 0, N=1 only ----
+    # ---- CPU baseline: the reference package on a bounded sample, rank 0, N=1 ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = _host_threads()
-        est, det = oracle_sample(x0, mask, spec, threads)
-        cpu = {"value": spec.iterations / est, "unit": "iters/s", "cores": threads, "kind": "port",
-               "sample": "coil compression + 1 outer iteration per stage of C2, extrapolated to 25/25/50",
-               "cpu": _cpu_model(), "detail": det}
+        est_all, det_all = reference_sample(name, threads)
+        est_one, det_one = reference_sample(name, 1)
+        su = _step_iterations(name)
+        cpu = {"value": su / est_all, "unit": "iters/s", "cores": threads, "kind": det_all["kind"],
+               "sample": _sample_text(name, det_all), "cpu": _cpu_model(), "detail": det_all,
+               "one_thread": {"value": su / est_one, "unit": "iters/s", "cores": 1, "detail": det_one}}
 
     if rank == 0:
         line = {
             "metric": "HICU iters/s", "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c64 (3xTF32 tcgen05 convs/Gram; fp64 reductions and nullspace)",
-            "data": "synthetic", "config": workload_config(spec), "e2e": e2e, "gpu_launches": int(launches),
+            "scaling": "strong" if (world > 1 and name in ("C5", "C3")) else "weak", "vs_baseline": None,
+            "dtype": "c64 (3xTF32 tcgen05 convs/Gram; fp64 reductions and nullspace)",
+            "data": "synthetic (seeded phantoms with BASELINE.json shapes; paper_2004_08962_b200/synthetic.py)",
+            "config": workload_config(name, world), "e2e": e2e, "gpu_launches": int(launches),
             "gpu_launches_per_step": int(launches) // max(1, args.steps),
             "roofline": roof, "roofline_all": roof_all, "cpu_baseline": cpu, "clocks": clock_info,
-            "batched": batched,
-            "kernel_share": share, "kernel_ms_per_step": dict(ms_by),
+            "kernel_share": share, "kernel_ms_per_step": ms_by,
             "kernel_ms_source": "one extra untimed step with the native CUDA-event profiler",
-            "gram_grad_tflops": grad_tflops,
+            "effective_tflops": eff,
             "step_ms": times,
         }
         print(json.dumps(line), flush=True)
@@ -438,8 +709,9 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -212,25 +212,31 @@ class ShardedReconstruction:
         self.plan = plan
         self.halo = halo
 
-    def run(self):
+    def run_iteration(self, si: int, it: int):
+        """One outer iteration of stage ``si`` (the unit a benchmark step
+        times): Gram partials -> all-reduce -> redundant nullspace -> G
+        gradient steps with their halo exchanges and scalar all-reduces."""
         b, pl, hx = self.b, self.plan, self.halo
-        sched = b.schedule
-        for si, stage in enumerate(sched.stages):
+        stage = b.schedule.stages[si]
+        G = b.gram(si)
+        hx.allreduce_(b.as_real(G))
+        b.nullspace(si, it, G)
+        for j in range(stage.gradient_steps):
+            b.conv_fwd(si, j)
+            g = b.scatter_raw(si, j)
+            hx.accumulate(g)
+            b.dc_apply(pl.owned)
+            hx.refresh(g)
+            b.conv_els(si, j)
+            sums = b.reduce()
+            hx.allreduce_(sums)
+            b.apply(si, it, j, sums)
+
+    def run(self):
+        for si, stage in enumerate(self.b.schedule.stages):
             for it in range(stage.iterations):
-                G = b.gram(si)
-                hx.allreduce_(b.as_real(G))
-                b.nullspace(si, it, G)
-                for j in range(stage.gradient_steps):
-                    b.conv_fwd(si, j)
-                    g = b.scatter_raw(si, j)
-                    hx.accumulate(g)
-                    b.dc_apply(pl.owned)
-                    hx.refresh(g)
-                    b.conv_els(si, j)
-                    sums = b.reduce()
-                    hx.allreduce_(sums)
-                    b.apply(si, it, j, sums)
-        return b.result()
+                self.run_iteration(si, it)
+        return self.b.result()
 
 
 def plan_for(dims, kernel, schedule, world: int, rank: int) -> ShardPlan:

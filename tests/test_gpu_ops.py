@@ -200,17 +200,20 @@ def test_nystrom_kernel_fp64_parity(golden_ops):
     assert proj_dist(V, g["sub_v"]) <= 1e-8
 
 
-def test_nystrom_random_sizes():
-    rng = np.random.default_rng(5)
-    for n, r in [(50, 10), (200, 60), (120, 40)]:
-        a = rng.standard_normal((3 * n, n)) + 1j * rng.standard_normal((3 * n, n))
-        a = a * np.exp(-np.arange(n) / (n / 6.0))  # decaying spectrum
-        G = a.conj().T @ a
-        ell = math.ceil(1.5 * r)
-        om = O.complex_normal(rng, (n, ell))
-        V = _nystrom_device(G, om, r)
-        Vr = O.nystrom_right_vectors(G, om, r)
-        assert proj_dist(V, Vr) <= 1e-8, (n, r)
+@pytest.mark.parametrize("n,r", [(50, 10), (200, 60), (120, 40), (490, 100), (1000, 120), (1000, 150)])
+def test_nystrom_random_sizes(n, r):
+    """fp64 nullspace kernel vs the numpy Nystrom on the same Gram and Omega,
+    including the large-l path (l = 150 / 180 / 225: C3 / C5 / C4)."""
+    rng = np.random.default_rng(5 + n + r)
+    a = rng.standard_normal((3 * n, n)) + 1j * rng.standard_normal((3 * n, n))
+    a = a * np.exp(-np.arange(n) / (n / 6.0))  # decaying spectrum
+    G = a.conj().T @ a
+    ell = math.ceil(1.5 * r)
+    om = O.complex_normal(rng, (n, ell))
+    V = _nystrom_device(G, om, r)
+    Vr = O.nystrom_right_vectors(G, om, r)
+    assert np.linalg.norm(V.conj().T @ V - np.eye(r)) <= 1e-9
+    assert proj_dist(V, Vr) <= 1e-8, (n, r, proj_dist(V, Vr))
 
 
 def test_rsvd_right_vectors_gpu(golden_ops):
@@ -222,7 +225,8 @@ def test_rsvd_right_vectors_gpu(golden_ops):
     V = H.rsvd_right_vectors(x, k, reg, r, H.RngStream(int(g["sub_seed"]), tuple(int(i) for i in g["sub_ids"])))
     assert np.linalg.norm(V.conj().T @ V - np.eye(r)) <= 1e-9
     # fp32 Gram accuracy bounds the subspace error by ~eps32*||G||/gap
-    assert proj_dist(V, g["sub_v"]) <= 1e-3
+    print("rsvd projector distance vs reference", proj_dist(V, g["sub_v"]))
+    assert proj_dist(V, g["sub_v"]) <= 1e-5  # measured 2.0e-6 (3xTF32 Gram, fp64 nullspace)
     # exact-rank-ish constant signal (reference tests/test_subspace.py:85-92)
     k1 = H.KernelMask.full((2,))
     V1 = H.rsvd_right_vectors(np.full(4, 2.5 + 0.5j), k1, H.full_region((4,), k1), 1, H.RngStream(0))

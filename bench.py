@@ -133,15 +133,22 @@ def _reference_module():
     return hicu_oracle, "port"
 
 
+_HOST_CACHE = {}
+
+
 def _compressed_host_input(name, scale=1.0):
-    """(x0, mask, n_coil_s) as the CPU path receives it: coil compression is
-    not part of the reference, so the oracle's restatement runs
-    first and is timed separately."""
+    """(x0, mask, coil-compression seconds) as the CPU path receives it: coil
+    compression is not part of the reference, so the oracle's
+    restatement runs first and is timed separately.  The synthetic k-space is
+    generated once per process (C5 takes ~16 s)."""
     from oracle import hicu_oracle as O
     from paper_2004_08962_b200.synthetic import make_config
 
     spec = _spec(name)
-    ksp, mask, x0 = make_config(name, scale=scale)
+    key = (name, scale)
+    if key not in _HOST_CACHE:
+        _HOST_CACHE[key] = make_config(name, scale=scale)
+    ksp, mask, x0 = _HOST_CACHE[key]
     t = 0.0
     if spec.coils_out != spec.coils_in:
         t0 = time.perf_counter()
@@ -574,6 +581,8 @@ def run_ours(args):
     nat.load()
     name = args.config
     dw = DeviceWorkload(name, world, rank, group)
+    if name != "C3":
+        _HOST_CACHE[(name, 1.0)] = dw.host[dw.slices[0]]  # the CPU sampler reuses the generated k-space
     stream = torch.cuda.current_stream()
     small = name != "C5"
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda") if small else None

@@ -71,6 +71,12 @@ typedef struct hicu_geom {
 #define HICU_GEOM_COIL_SEPARABLE 1
 #define HICU_GEOM_FORCE_SIMT_GRAM 2   /* use the SIMT Gram even when tcgen05 applies */
 #define HICU_GEOM_FORCE_SIMT_CONV 4   /* use the SIMT conv/scatter even when tcgen05 applies */
+#define HICU_GEOM_FORCE_DENSE_GRAM 8  /* dense implicit-im2col Gram instead of the lag Gram */
+
+/* hicu_gram_path() values */
+#define HICU_GRAM_PATH_SIMT 0     /* dense implicit-im2col Gram, fp32 SIMT (gram_simt.cu) */
+#define HICU_GRAM_PATH_TCGEN05 1  /* dense implicit-im2col Gram, tcgen05 3xTF32 (gram_tc.cu) */
+#define HICU_GRAM_PATH_LAG 2      /* shift-structured lag Gram (gram_lag.cu) */
 
 /* Per-step scalar record written by hicu_step_update (doubles). */
 enum {
@@ -166,8 +172,15 @@ int hicu_ser_parts(int64_t N, const void* ref, const void* y, double* ser_parts,
  * function; equals hankel_adjoint_apply(x, hankel_apply(x, I)). */
 size_t hicu_gram_workspace(const hicu_geom* g);
 /* 1 when hicu_gram runs the tcgen05 3xTF32 kernel for this geometry (coil-
- * separable support with 8 coils, no circular axes, >= 8 spatial taps). */
+ * separable support with 8 coils, no circular axes, >= 8 spatial taps, and
+ * the dense Gram selected: HICU_GEOM_FORCE_DENSE_GRAM or no lag path). */
 int hicu_gram_uses_tensor_cores(const hicu_geom* g);
+/* Which Gram hicu_gram runs for this geometry: HICU_GRAM_PATH_LAG (coil-
+ * separable support, 1-3 spatial axes, spatial kernel extents <= 8, Nc in
+ * 1..8, 10, 12, 16: G assembled from per-lag coil correlations over the
+ * per-axis position classes of the shifted region boxes), else the dense
+ * tcgen05 or SIMT implicit-im2col Gram; -1 on a bad geometry. */
+int hicu_gram_path(const hicu_geom* g);
 /* 1 when hicu_conv_fwd / hicu_conv_els / hicu_scatter_dc with p columns run
  * on the tcgen05 kernels (conv_tc.cu) for this geometry. */
 int hicu_conv_uses_tensor_cores(const hicu_geom* g, int p);

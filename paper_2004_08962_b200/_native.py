@@ -21,6 +21,8 @@ REC_SLOTS = 8
 GEOM_COIL_SEPARABLE = 1
 GEOM_FORCE_SIMT_GRAM = 2
 GEOM_FORCE_SIMT_CONV = 4
+GEOM_FORCE_DENSE_GRAM = 8
+GRAM_PATHS = {0: "simt", 1: "tcgen05", 2: "lag"}
 PROF_KINDS = ("gram", "nystrom", "householder", "conv_fwd", "scatter", "conv_els", "update")
 
 
@@ -85,6 +87,7 @@ _SIGS = {
                                 c_void_p]),
     "hicu_gram_workspace": (c_size_t, [_GP]),
     "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
+    "hicu_gram_path": (c_int, [_GP]),
     "hicu_conv_uses_tensor_cores": (c_int, [_GP, c_int]),
     "hicu_gram": (c_int, [_GP, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hicu_zgemm": (c_int, [c_char, c_char, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,

@@ -154,22 +154,36 @@ extern "C" int hicu_device_sm_count(int* out) {
   return HICU_OK;
 }
 
-static bool use_tc(const hicu_geom* hg, const DevGeom& g) {
-  return !(hg->flags & HICU_GEOM_FORCE_SIMT_GRAM) && hicu_gram_tc_supported(g);
+// Gram path: the shift-structured lag Gram (gram_lag.cu) wherever it applies,
+// else the dense implicit-im2col Gram (tcgen05 3xTF32, or SIMT).
+static int gram_path(const hicu_geom* hg, const DevGeom& g) {
+  const bool dense = (hg->flags & (HICU_GEOM_FORCE_DENSE_GRAM | HICU_GEOM_FORCE_SIMT_GRAM)) != 0;
+  if (!dense && hicu_gram_lag_supported(g)) return HICU_GRAM_PATH_LAG;
+  if (!(hg->flags & HICU_GEOM_FORCE_SIMT_GRAM) && hicu_gram_tc_supported(g)) return HICU_GRAM_PATH_TCGEN05;
+  return HICU_GRAM_PATH_SIMT;
 }
 
 extern "C" size_t hicu_gram_workspace(const hicu_geom* hg) {
   DevGeom g;
   if (hicu_make_devgeom(hg, &g)) return 0;
-  const size_t a = hicu_gram_simt_workspace(g);
-  const size_t b = use_tc(hg, g) ? hicu_gram_tc_workspace(g) : 0;
-  return a > b ? a : b;
+  switch (gram_path(hg, g)) {
+    case HICU_GRAM_PATH_LAG: return hicu_gram_lag_workspace(g);
+    case HICU_GRAM_PATH_TCGEN05: {
+      const size_t a = hicu_gram_simt_workspace(g), b = hicu_gram_tc_workspace(g);
+      return a > b ? a : b;
+    }
+    default: return hicu_gram_simt_workspace(g);
+  }
+}
+
+extern "C" int hicu_gram_path(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return -1;
+  return gram_path(hg, g);
 }
 
 extern "C" int hicu_gram_uses_tensor_cores(const hicu_geom* hg) {
-  DevGeom g;
-  if (hicu_make_devgeom(hg, &g)) return 0;
-  return use_tc(hg, g) ? 1 : 0;
+  return hicu_gram_path(hg) == HICU_GRAM_PATH_TCGEN05 ? 1 : 0;
 }
 
 extern "C" int hicu_gram(const hicu_geom* hg, const void* x, void* G, void* ws, size_t ws_bytes, void* stream) {
@@ -177,6 +191,12 @@ extern "C" int hicu_gram(const hicu_geom* hg, const void* x, void* G, void* ws, 
   DevGeom g;
   int s = hicu_make_devgeom(hg, &g);
   if (s) return s;
-  if (use_tc(hg, g)) return hicu_gram_tc(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
-  return hicu_gram_simt(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
+  switch (gram_path(hg, g)) {
+    case HICU_GRAM_PATH_LAG:
+      return hicu_gram_lag(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
+    case HICU_GRAM_PATH_TCGEN05:
+      return hicu_gram_tc(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
+    default:
+      return hicu_gram_simt(g, (const float2*)x, (double2*)G, ws, ws_bytes, (cudaStream_t)stream);
+  }
 }

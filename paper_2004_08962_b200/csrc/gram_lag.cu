@@ -1,0 +1,635 @@
+// Shift-structured Gram G = H^H H of the multi-level Hankel (convolution)
+// matrix H(x) (reference analogue:
+// hankel_adjoint_apply(x, hankel_apply(x, I)), hankel.py:255-391).
+//
+// Column (t, c) of H is the k-space window x[i + t, c] for region rows i, so
+//   G[(t,c),(t',c')] = sum_{i in R} conj(x[i+t, c]) x[i+t', c']
+//                    = sum_{j in R+t} conj(x[j, c]) x[j+d, c'],   d = t' - t.
+// Every entry is a "lag-d" coil correlation summed over the shifted box R+t.
+// Along each spatial axis the positions of interest [o, o+e+K-1) fall into
+// at most 2K-1 classes of equal tap membership (positions p with the same set
+// {t : o+t <= p < o+t+e}): K-1 single left-edge positions, one long core
+// [o+K-1, o+e) holding every tap, K-1 single right-edge positions (circular
+// axes: one class).  So with T[d][cell] = sum over the positions of one cell
+// (a product of per-axis classes) of conj(x[j]) x[j+d] (an Nc x Nc block),
+//   G[(t,c),(t+d,c')] = sum_{cells containing t} T[d][cell][c][c'].
+// Only lags in the lexicographic half-space are formed (G is Hermitian): the
+// dense Gram's n(n+1)/2 x s complex MACs (n = taps x coils) become
+// ~((2K-1)^d / 2) x Nc^2 x (positions) -- 21x less work for the 5x5x5x8
+// kernels of C4/C5, 8x for 5x5x8, 14x for 7x7x10.
+//
+// Kernels (fp32 FMA products, fp32 per-CTA partials of a few hundred terms,
+// fp64 everywhere after; fixed summation order, no atomics: deterministic):
+//   lag_core_kernel   the long last-axis core class: lines of k-space staged
+//                     in shared memory (coil planes, cp.async double buffer),
+//                     one warp per (last-axis lag, coil block), lanes over
+//                     positions, an Nc x CB register block of accumulators;
+//   lag_edge_kernel   the short last-axis classes (edge positions);
+//   lag_reduce_kernel fixed-order fp64 sums of the chunk partials -> T;
+//   lag_assemble_kernel  G from T (Hermitian by construction).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int kMaxL = 3;        // spatial axes (outer axes <= 2)
+constexpr int kMaxK = 8;        // kernel extent per spatial axis
+constexpr int kMaxCls = 2 * kMaxK - 1;
+constexpr int kMaxBlocks = kMaxCls * kMaxCls;
+constexpr int kMaxOl = (kMaxCls * kMaxCls + 1) / 2;
+constexpr int kCoreThreadsMax = 384;
+constexpr int kEdgeThreads = 256;
+constexpr int kLinesPerChunkA = 64;
+constexpr int kLinesPerChunkB = 1024;
+
+struct LagParams {
+  int L;           // spatial axes
+  int NC, CB, NCB; // coils, coil rows per warp block, NC / CB
+  int64_t N[kMaxL];
+  int64_t cstride[kMaxL];  // element (complex) stride of each spatial axis
+  int K[kMaxL];
+  int circ[kMaxL];
+  int ncls[kMaxL];
+  int cls_beg[kMaxL][kMaxCls], cls_end[kMaxL][kMaxCls], cls_lo[kMaxL][kMaxCls], cls_hi[kMaxL][kMaxCls];
+  int core_cls;    // index of the core class on the last axis (-1: none)
+  int NB;          // outer class blocks
+  int nol;         // outer lags (half-plane)
+  int ol_d[kMaxOl][2];
+  int ol_index[kMaxCls][kMaxCls];
+  int DZ;          // last-axis lags: dz in [-(K-1), K-1]
+  // core kernel
+  int GZ, NG;      // lags per CTA, groups
+  int CA;          // chunks per (ol, group) summed over blocks
+  int chunksA[kMaxBlocks + 1];  // prefix
+  int lpcA;
+  int64_t P;       // core positions per line
+  int64_t c0;      // first core position
+  // edge kernel
+  int NE;          // non-core last-axis classes
+  int edge_cls[kMaxCls];
+  int NQ, QB, NQB, LL;
+  int CBt;         // chunks per (ol, qblock) summed over blocks
+  int chunksB[kMaxBlocks + 1];
+  int lpcB;
+  int NCL;         // last-axis classes
+};
+
+struct LagPlan {
+  bool ok = false;
+  LagParams p;
+  size_t t_off = 0, a_off = 0, b_off = 0, bytes = 0;
+  int64_t nT = 0;   // complex entries of T
+  int64_t nA = 0, nB = 0;  // CTAs
+  size_t smemA = 0, smemB = 0;
+  int threadsA = 0;
+};
+
+int choose_cb(int nc) {
+  int best = 1;
+  for (int cb = 1; cb <= nc; ++cb)
+    if (nc % cb == 0 && cb * nc <= 64) best = cb;
+  return best;
+}
+
+void axis_classes(int64_t N, int64_t o, int64_t e, int K, bool circ, LagParams& p, int a) {
+  if (circ) {
+    p.ncls[a] = 1;
+    p.cls_beg[a][0] = 0;
+    p.cls_end[a][0] = (int)N;
+    p.cls_lo[a][0] = 0;
+    p.cls_hi[a][0] = K - 1;
+    return;
+  }
+  int nc = 0;
+  for (int64_t q = o; q < o + e + K - 1; ++q) {
+    const int lo = (int)std::max<int64_t>(0, q - o - e + 1), hi = (int)std::min<int64_t>(K - 1, q - o);
+    if (nc > 0 && p.cls_lo[a][nc - 1] == lo && p.cls_hi[a][nc - 1] == hi && p.cls_end[a][nc - 1] == q) {
+      p.cls_end[a][nc - 1] = (int)q + 1;
+      continue;
+    }
+    if (nc >= kMaxCls) {
+      p.ncls[a] = -1;
+      return;
+    }
+    p.cls_beg[a][nc] = (int)q;
+    p.cls_end[a][nc] = (int)q + 1;
+    p.cls_lo[a][nc] = lo;
+    p.cls_hi[a][nc] = hi;
+    ++nc;
+  }
+  p.ncls[a] = nc;
+}
+
+LagPlan make_plan(const DevGeom& g) {
+  LagPlan pl;
+  LagParams& p = pl.p;
+  memset(&p, 0, sizeof(p));
+  if (g.nc < 1 || g.nc > 16) return pl;
+  const int L = g.ndim - 1;
+  if (L < 1 || L > kMaxL) return pl;
+  if (g.nsp * g.nc != g.n) return pl;
+  p.L = L;
+  p.NC = g.nc;
+  p.CB = choose_cb(g.nc);
+  p.NCB = g.nc / p.CB;
+  bool circ[kMaxL] = {false, false, false};
+  for (int c = 0; c < g.ncirc; ++c) {
+    if (g.circ_axes[c] >= L) return pl;
+    circ[g.circ_axes[c]] = true;
+  }
+  for (int a = 0; a < L; ++a) {
+    const int K = (int)g.kext[a];
+    if (K < 1 || K > kMaxK) return pl;
+    p.N[a] = g.dims[a];
+    p.cstride[a] = g.stride[a];
+    p.K[a] = K;
+    p.circ[a] = circ[a] ? 1 : 0;
+    if (circ[a] && K > g.dims[a]) return pl;
+    axis_classes(g.dims[a], g.roff[a], g.rext[a], K, circ[a], p, a);
+    if (p.ncls[a] < 1) return pl;
+  }
+  // outer blocks and lags
+  const int la = L - 1;
+  p.NB = 1;
+  for (int a = 0; a < la; ++a) p.NB *= p.ncls[a];
+  const int D0 = la >= 1 ? 2 * p.K[0] - 1 : 1, D1 = la >= 2 ? 2 * p.K[1] - 1 : 1;
+  p.nol = 0;
+  for (int i = 0; i < kMaxCls; ++i)
+    for (int j = 0; j < kMaxCls; ++j) p.ol_index[i][j] = -1;
+  for (int i = 0; i < D0; ++i)
+    for (int j = 0; j < D1; ++j) {
+      const int d0 = la >= 1 ? i - (p.K[0] - 1) : 0, d1 = la >= 2 ? j - (p.K[1] - 1) : 0;
+      const bool pos = d0 > 0 || (d0 == 0 && d1 >= 0);
+      if (!pos) continue;
+      p.ol_d[p.nol][0] = d0;
+      p.ol_d[p.nol][1] = d1;
+      p.ol_index[i][j] = p.nol;
+      ++p.nol;
+    }
+  const int KL = p.K[la];
+  p.DZ = 2 * KL - 1;
+  p.NCL = p.ncls[la];
+  p.core_cls = -1;
+  for (int c = 0; c < p.NCL; ++c)
+    if (p.cls_lo[la][c] == 0 && p.cls_hi[la][c] == KL - 1 && p.cls_end[la][c] - p.cls_beg[la][c] >= 1) p.core_cls = c;
+  p.NE = 0;
+  for (int c = 0; c < p.NCL; ++c)
+    if (c != p.core_cls) p.edge_cls[p.NE++] = c;
+  auto block_lines = [&](int b) -> int64_t {
+    int64_t nl = 1;
+    int r = b;
+    for (int a = la - 1; a >= 0; --a) {
+      const int k = r % p.ncls[a];
+      r /= p.ncls[a];
+      nl *= p.cls_end[a][k] - p.cls_beg[a][k];
+    }
+    return nl;
+  };
+  // core kernel
+  if (p.core_cls >= 0) {
+    p.P = p.cls_end[la][p.core_cls] - p.cls_beg[la][p.core_cls];
+    p.c0 = p.cls_beg[la][p.core_cls];
+    const int wmax = kCoreThreadsMax / 32;
+    int gz = std::max(1, wmax / p.NCB);
+    p.NG = (p.DZ + gz - 1) / gz;
+    p.GZ = (p.DZ + p.NG - 1) / p.NG;
+    p.lpcA = kLinesPerChunkA;
+    p.chunksA[0] = 0;
+    for (int b = 0; b < p.NB; ++b)
+      p.chunksA[b + 1] = p.chunksA[b] + (int)((block_lines(b) + p.lpcA - 1) / p.lpcA);
+    p.CA = p.chunksA[p.NB];
+    pl.nA = (int64_t)p.nol * p.NG * p.CA;
+    pl.threadsA = 32 * p.GZ * p.NCB;
+    pl.smemA = (size_t)2 * p.NC * (2 * p.P + p.GZ) * sizeof(float2);
+    if (pl.smemA > (size_t)200 * 1024) return pl;
+  }
+  // edge kernel
+  if (p.NE > 0) {
+    p.NQ = p.NE * p.DZ * p.NCB;
+    p.QB = std::min(p.NQ, kEdgeThreads);
+    p.NQB = (p.NQ + p.QB - 1) / p.QB;
+    p.LL = std::max(1, kEdgeThreads / p.QB);
+    p.lpcB = kLinesPerChunkB;
+    p.chunksB[0] = 0;
+    for (int b = 0; b < p.NB; ++b)
+      p.chunksB[b + 1] = p.chunksB[b] + (int)((block_lines(b) + p.lpcB - 1) / p.lpcB);
+    p.CBt = p.chunksB[p.NB];
+    pl.nB = (int64_t)p.nol * p.NQB * p.CBt;
+    pl.smemB = (size_t)p.QB * p.CB * p.NC * sizeof(float2);
+  }
+  pl.nT = (int64_t)p.nol * p.DZ * p.NB * p.NCL * p.NC * p.NC;
+  auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
+  pl.t_off = 0;
+  pl.a_off = al(pl.nT * sizeof(double2));
+  pl.b_off = pl.a_off + al((size_t)pl.nA * p.GZ * p.NC * p.NC * sizeof(float2));
+  pl.bytes = pl.b_off + al((size_t)pl.nB * p.QB * p.CB * p.NC * sizeof(float2));
+  pl.ok = true;
+  return pl;
+}
+
+// outer coordinates of line li of block b; returns false when the neighbour
+// block (shifted by the outer lag) leaves a non-circular axis
+__device__ __forceinline__ void block_ranges(const LagParams& P, int b, int (&beg)[2], int (&len)[2]) {
+  const int la = P.L - 1;
+  beg[0] = beg[1] = 0;
+  len[0] = len[1] = 1;
+  int r = b;
+  for (int a = la - 1; a >= 0; --a) {
+    const int k = r % P.ncls[a];
+    r /= P.ncls[a];
+    beg[a] = P.cls_beg[a][k];
+    len[a] = P.cls_end[a][k] - P.cls_beg[a][k];
+  }
+}
+
+__device__ __forceinline__ bool neighbour_ok(const LagParams& P, const int (&beg)[2], const int (&len)[2], int ol) {
+  const int la = P.L - 1;
+  for (int a = 0; a < la; ++a) {
+    if (P.circ[a]) continue;
+    const int d = P.ol_d[ol][a];
+    if (beg[a] + d < 0 || beg[a] + len[a] - 1 + d >= P.N[a]) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void line_offsets(const LagParams& P, const int (&beg)[2], const int (&len)[2], int ol,
+                                             int64_t li, int64_t& base, int64_t& nbr) {
+  const int la = P.L - 1;
+  int64_t q[2];
+  if (la == 2) {
+    q[0] = li / len[1];
+    q[1] = li % len[1];
+  } else {
+    q[0] = li;
+    q[1] = 0;
+  }
+  base = 0;
+  nbr = 0;
+  for (int a = 0; a < la; ++a) {
+    const int64_t pa = beg[a] + q[a];
+    int64_t pn = pa + P.ol_d[ol][a];
+    if (P.circ[a]) {
+      if (pn < 0) pn += P.N[a];
+      if (pn >= P.N[a]) pn -= P.N[a];
+    }
+    base += pa * P.cstride[a];
+    nbr += pn * P.cstride[a];
+  }
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int NC, int CB>
+__global__ void __launch_bounds__(kCoreThreadsMax, 1)
+lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
+  hicu_pdl_entry();
+  extern __shared__ __align__(16) float2 lsm[];
+  const int64_t bid = blockIdx.x;
+  const int olg = (int)(bid / P.CA);
+  const int rem = (int)(bid % P.CA);
+  const int ol = olg / P.NG, gzi = olg % P.NG;
+  int b = 0;
+  while (P.chunksA[b + 1] <= rem) ++b;
+  const int chunk = rem - P.chunksA[b];
+  const int dz_lo = gzi * P.GZ - (P.K[P.L - 1] - 1);
+  const int gz_n = min(P.GZ, P.DZ - gzi * P.GZ);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dzi = warp / P.NCB, cbi = warp % P.NCB;
+  float2* out = part + (size_t)bid * P.GZ * NC * NC;
+  int beg[2], len[2];
+  block_ranges(P, b, beg, len);
+  const int64_t nlines = (int64_t)len[0] * len[1];
+  const int64_t l0 = (int64_t)chunk * P.lpcA, l1 = min(nlines, l0 + P.lpcA);
+  if (!neighbour_ok(P, beg, len, ol)) {
+    for (int i = threadIdx.x; i < P.GZ * NC * NC; i += blockDim.x) out[i] = cf(0.f, 0.f);
+    return;
+  }
+  const int la = P.L - 1;
+  const int64_t Pn = P.P, NL = P.N[la];
+  const int64_t nw = Pn + P.GZ - 1;          // neighbour positions staged per line
+  const size_t bufsz = (size_t)NC * (Pn + nw);
+  const int64_t cs = P.cstride[la];           // == NC
+  auto stage = [&](int64_t li, int buf) {
+    int64_t base, nbr;
+    line_offsets(P, beg, len, ol, li, base, nbr);
+    float2* sb = lsm + (size_t)buf * bufsz;
+    float2* sn = sb + (size_t)NC * Pn;
+    for (int64_t e = threadIdx.x; e < Pn * NC; e += blockDim.x) {
+      const int64_t j = e / NC;
+      const int c = (int)(e % NC);
+      cp_async8(sb + (size_t)c * Pn + j, x + base + (P.c0 + j) * cs + c);
+    }
+    const int64_t nwa = Pn + gz_n - 1;  // positions the active lags read (a short last group stages less)
+    for (int64_t e = threadIdx.x; e < nwa * NC; e += blockDim.x) {
+      const int64_t j = e / NC;
+      const int c = (int)(e % NC);
+      int64_t q = P.c0 + dz_lo + j;
+      if (P.circ[la]) {
+        q %= NL;
+        if (q < 0) q += NL;
+      }
+      cp_async8(sn + (size_t)c * nw + j, x + nbr + q * cs + c);
+    }
+  };
+  float2 acc[CB][NC];
+#pragma unroll
+  for (int a = 0; a < CB; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[a][c] = cf(0.f, 0.f);
+  const bool active = dzi < gz_n;
+  if (l0 < l1) stage(l0, 0);
+  cp_async_commit();
+  int buf = 0;
+  for (int64_t li = l0; li < l1; ++li) {
+    if (li + 1 < l1) stage(li + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (active) {
+      const float2* sb = lsm + (size_t)buf * bufsz + (size_t)cbi * CB * Pn;
+      const float2* sn = lsm + (size_t)buf * bufsz + (size_t)NC * Pn + dzi;
+      for (int64_t j = lane; j < Pn; j += 32) {
+        float2 a[CB], v[NC];
+#pragma unroll
+        for (int q = 0; q < CB; ++q) a[q] = sb[(size_t)q * Pn + j];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = sn[(size_t)c * nw + j];
+#pragma unroll
+        for (int q = 0; q < CB; ++q)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) cfmac(acc[q][c], a[q], v[c]);
+      }
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+  cp_async_wait<0>();
+  // fixed-order warp reduction of the lanes' partial sums
+#pragma unroll
+  for (int q = 0; q < CB; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      float2 v = acc[q][c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+      }
+      acc[q][c] = v;
+    }
+  if (lane == 0 && dzi < P.GZ) {
+#pragma unroll
+    for (int q = 0; q < CB; ++q)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        out[((size_t)dzi * NC + cbi * CB + q) * NC + c] = active ? acc[q][c] : cf(0.f, 0.f);
+  }
+}
+
+template <int NC, int CB>
+__global__ void __launch_bounds__(kEdgeThreads)
+lag_edge_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
+  hicu_pdl_entry();
+  extern __shared__ __align__(16) float2 esm[];
+  const int64_t bid = blockIdx.x;
+  const int olq = (int)(bid / P.CBt);
+  const int rem = (int)(bid % P.CBt);
+  const int ol = olq / P.NQB, qb = olq % P.NQB;
+  int b = 0;
+  while (P.chunksB[b + 1] <= rem) ++b;
+  const int chunk = rem - P.chunksB[b];
+  const int tq = threadIdx.x % P.QB, ll = threadIdx.x / P.QB;
+  const int q = qb * P.QB + tq;
+  const bool qok = q < P.NQ && ll < P.LL;
+  const int e = q / (P.DZ * P.NCB), dzi = (q / P.NCB) % P.DZ, cbi = q % P.NCB;
+  const int la = P.L - 1;
+  const int dz = dzi - (P.K[la] - 1);
+  int beg[2], len[2];
+  block_ranges(P, b, beg, len);
+  const int64_t nlines = (int64_t)len[0] * len[1];
+  const int64_t l0 = (int64_t)chunk * P.lpcB, l1 = min(nlines, l0 + P.lpcB);
+  const bool ok = neighbour_ok(P, beg, len, ol);
+  float2 acc[CB][NC];
+#pragma unroll
+  for (int a = 0; a < CB; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[a][c] = cf(0.f, 0.f);
+  if (ok && qok) {
+    const int cls = P.edge_cls[e];
+    const int pb = P.cls_beg[la][cls], pe = P.cls_end[la][cls];
+    const int64_t cs = P.cstride[la];
+    for (int64_t li = l0 + ll; li < l1; li += P.LL) {
+      int64_t base, nbr;
+      line_offsets(P, beg, len, ol, li, base, nbr);
+      for (int pz = pb; pz < pe; ++pz) {
+        const int64_t pn = (int64_t)pz + dz;
+        if (pn < 0 || pn >= P.N[la]) continue;
+        float2 a[CB], v[NC];
+#pragma unroll
+        for (int t = 0; t < CB; ++t) a[t] = x[base + pz * cs + cbi * CB + t];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[c] = x[nbr + pn * cs + c];
+#pragma unroll
+        for (int t = 0; t < CB; ++t)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) cfmac(acc[t][c], a[t], v[c]);
+      }
+    }
+  }
+  // fixed-order reduction over the line lanes through shared memory
+  float2* red = esm;
+  for (int r = 1; r < P.LL; ++r) {
+    if (ll == r && qok) {
+#pragma unroll
+      for (int t = 0; t < CB; ++t)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) red[((size_t)tq * CB + t) * NC + c] = acc[t][c];
+    }
+    __syncthreads();
+    if (ll == 0 && qok) {
+#pragma unroll
+      for (int t = 0; t < CB; ++t)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[t][c] = acc[t][c] + red[((size_t)tq * CB + t) * NC + c];
+    }
+    __syncthreads();
+  }
+  if (ll == 0 && qok) {
+    float2* out = part + ((size_t)bid * P.QB + tq) * CB * NC;
+#pragma unroll
+    for (int t = 0; t < CB; ++t)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) out[t * NC + c] = acc[t][c];
+  } else if (ll == 0 && tq < P.QB) {
+    float2* out = part + ((size_t)bid * P.QB + tq) * CB * NC;
+    for (int i = 0; i < CB * NC; ++i) out[i] = cf(0.f, 0.f);
+  }
+}
+
+// T[((ol * DZ + dz) * NB + b) * NCL + cls][c][c'] = fixed-order fp64 sum of the chunk partials
+__global__ void lag_reduce_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ partA,
+                                  const float2* __restrict__ partB, double2* __restrict__ T, int64_t total) {
+  hicu_pdl_entry();
+  const int NC = P.NC, NC2 = NC * NC;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int cc = (int)(idx % NC2);
+    int64_t r = idx / NC2;
+    const int cls = (int)(r % P.NCL);
+    r /= P.NCL;
+    const int b = (int)(r % P.NB);
+    r /= P.NB;
+    const int dz = (int)(r % P.DZ);
+    const int ol = (int)(r / P.DZ);
+    const int c = cc / NC, c2 = cc % NC;
+    double sx = 0.0, sy = 0.0;
+    if (cls == P.core_cls) {
+      const int gzi = dz / P.GZ, dzi = dz % P.GZ;
+      const int64_t bid0 = ((int64_t)ol * P.NG + gzi) * P.CA + P.chunksA[b];
+      const int nch = P.chunksA[b + 1] - P.chunksA[b];
+      for (int ch = 0; ch < nch; ++ch) {
+        const float2 v = partA[((bid0 + ch) * P.GZ + dzi) * NC2 + cc];
+        sx += v.x;
+        sy += v.y;
+      }
+    } else {
+      int e = 0;
+      while (e < P.NE && P.edge_cls[e] != cls) ++e;
+      const int cbi = c / P.CB, t = c % P.CB;
+      const int q = (e * P.DZ + dz) * P.NCB + cbi;
+      const int qb = q / P.QB, tq = q % P.QB;
+      const int64_t bid0 = ((int64_t)ol * P.NQB + qb) * P.CBt + P.chunksB[b];
+      const int nch = P.chunksB[b + 1] - P.chunksB[b];
+      for (int ch = 0; ch < nch; ++ch) {
+        const float2 v = partB[(((bid0 + ch) * P.QB + tq) * P.CB + t) * NC + c2];
+        sx += v.x;
+        sy += v.y;
+      }
+    }
+    T[idx] = cd(sx, sy);
+  }
+}
+
+// G[i][j] = sum over the cells containing tap t_i of T[d = t_j - t_i][cell][c_i][c_j]
+// (lexicographically negative d, or d = 0 with c_i > c_j: conj of the mirrored entry)
+__global__ void lag_assemble_kernel(const __grid_constant__ LagParams P, const double2* __restrict__ T,
+                                    const int32_t* __restrict__ pos, int ndim, int n, double2* __restrict__ G) {
+  hicu_pdl_entry();
+  const int L = P.L, la = L - 1, NC = P.NC;
+  const int64_t total = (int64_t)n * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n), j = (int)(idx % n);
+    int ti[kMaxL], tj[kMaxL];
+    for (int a = 0; a < L; ++a) {
+      ti[a] = pos[(size_t)i * ndim + a];
+      tj[a] = pos[(size_t)j * ndim + a];
+    }
+    int ci = pos[(size_t)i * ndim + L], cj = pos[(size_t)j * ndim + L];
+    int sgn = 0;
+    for (int a = 0; a < L && sgn == 0; ++a) sgn = (tj[a] > ti[a]) - (tj[a] < ti[a]);
+    const bool mirror = sgn < 0 || (sgn == 0 && ci > cj);
+    int t[kMaxL], d[kMaxL];
+    for (int a = 0; a < L; ++a) {
+      t[a] = mirror ? tj[a] : ti[a];
+      d[a] = mirror ? ti[a] - tj[a] : tj[a] - ti[a];
+    }
+    const int c = mirror ? cj : ci, c2 = mirror ? ci : cj;
+    const int i0 = la >= 1 ? d[0] + P.K[0] - 1 : 0, i1 = la >= 2 ? d[1] + P.K[1] - 1 : 0;
+    const int ol = P.ol_index[i0][i1];
+    const int dz = d[la] + P.K[la] - 1;
+    double sx = 0.0, sy = 0.0;
+    const int n0 = la >= 1 ? P.ncls[0] : 1, n1 = la >= 2 ? P.ncls[1] : 1;
+    for (int k0 = 0; k0 < n0; ++k0) {
+      if (la >= 1 && (t[0] < P.cls_lo[0][k0] || t[0] > P.cls_hi[0][k0])) continue;
+      for (int k1 = 0; k1 < n1; ++k1) {
+        if (la >= 2 && (t[1] < P.cls_lo[1][k1] || t[1] > P.cls_hi[1][k1])) continue;
+        const int b = k0 * n1 + k1;
+        const double2* Tb = T + ((((int64_t)ol * P.DZ + dz) * P.NB + b) * P.NCL) * NC * NC + (size_t)c * NC + c2;
+        for (int kl = 0; kl < P.NCL; ++kl) {
+          if (t[la] < P.cls_lo[la][kl] || t[la] > P.cls_hi[la][kl]) continue;
+          const double2 v = Tb[(size_t)kl * NC * NC];
+          sx += v.x;
+          sy += v.y;
+        }
+      }
+    }
+    if (i == j) sy = 0.0;
+    G[idx] = cd(sx, mirror ? -sy : sy);
+  }
+}
+
+template <int NC>
+int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
+  constexpr int CB = (NC <= 8) ? NC : (NC == 10 ? 5 : (NC == 12 ? 4 : (NC == 16 ? 4 : 1)));
+  const LagParams& P = pl.p;
+  if (P.CB != CB) return hicu_set_error(HICU_ERR_PARAMETER, "gram_lag: coil block mismatch");
+  float2* partA = (float2*)((char*)ws + pl.a_off);
+  float2* partB = (float2*)((char*)ws + pl.b_off);
+  int s;
+  if (pl.nA > 0) {
+    hicu_allow_max_smem((const void*)lag_core_kernel<NC, CB>);
+    hicu_launch(lag_core_kernel<NC, CB>, (unsigned)pl.nA, pl.threadsA, pl.smemA, st, P, x, partA);
+    if ((s = hicu_check_launch("lag_core_kernel"))) return s;
+  }
+  if (pl.nB > 0) {
+    hicu_allow_max_smem((const void*)lag_edge_kernel<NC, CB>);
+    hicu_launch(lag_edge_kernel<NC, CB>, (unsigned)pl.nB, kEdgeThreads, pl.smemB, st, P, x, partB);
+    if ((s = hicu_check_launch("lag_edge_kernel"))) return s;
+  }
+  return HICU_OK;
+}
+
+}  // namespace
+
+bool hicu_gram_lag_supported(const DevGeom& g) {
+  if (!(g.nc >= 1 && g.nc <= 8) && g.nc != 10 && g.nc != 12 && g.nc != 16) return false;
+  return make_plan(g).ok;
+}
+
+size_t hicu_gram_lag_workspace(const DevGeom& g) {
+  LagPlan pl = make_plan(g);
+  return pl.ok ? pl.bytes : 0;
+}
+
+int hicu_gram_lag(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st) {
+  LagPlan pl = make_plan(g);
+  if (!pl.ok) return hicu_set_error(HICU_ERR_PARAMETER, "gram_lag: unsupported geometry");
+  if (ws_bytes < pl.bytes) return hicu_set_error(HICU_ERR_WORKSPACE, "gram_lag: workspace too small");
+  int s;
+  switch (g.nc) {
+    case 1: s = launch_nc<1>(pl, x, ws, st); break;
+    case 2: s = launch_nc<2>(pl, x, ws, st); break;
+    case 3: s = launch_nc<3>(pl, x, ws, st); break;
+    case 4: s = launch_nc<4>(pl, x, ws, st); break;
+    case 5: s = launch_nc<5>(pl, x, ws, st); break;
+    case 6: s = launch_nc<6>(pl, x, ws, st); break;
+    case 7: s = launch_nc<7>(pl, x, ws, st); break;
+    case 8: s = launch_nc<8>(pl, x, ws, st); break;
+    case 10: s = launch_nc<10>(pl, x, ws, st); break;
+    case 12: s = launch_nc<12>(pl, x, ws, st); break;
+    case 16: s = launch_nc<16>(pl, x, ws, st); break;
+    default: return hicu_set_error(HICU_ERR_PARAMETER, "gram_lag: coil count");
+  }
+  if (s) return s;
+  double2* T = (double2*)((char*)ws + pl.t_off);
+  const float2* partA = (const float2*)((char*)ws + pl.a_off);
+  const float2* partB = (const float2*)((char*)ws + pl.b_off);
+  {
+    const int blocks = (int)std::min<int64_t>((pl.nT + 255) / 256, (int64_t)hicu_sm_count() * 16);
+    hicu_launch(lag_reduce_kernel, blocks, 256, 0, st, pl.p, partA, partB, T, pl.nT);
+    if ((s = hicu_check_launch("lag_reduce_kernel"))) return s;
+  }
+  const int64_t total = (int64_t)g.n * g.n;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)hicu_sm_count() * 16);
+  hicu_launch(lag_assemble_kernel, blocks, 256, 0, st, pl.p, (const double2*)T, g.pos, g.ndim, g.n, G);
+  return hicu_check_launch("lag_assemble_kernel");
+}

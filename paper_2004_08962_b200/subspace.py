@@ -73,26 +73,43 @@ class NullspaceBasis:
 
 
 def gram_uses_tensor_cores(kernel: KernelMask, region: Region, dims) -> bool:
-    """True when hicu_gram runs the tcgen05 3xTF32 kernel for this geometry."""
+    """True when the dense Gram (``gram_matrix(..., path="tcgen05")``) runs the
+    tcgen05 3xTF32 kernel for this geometry."""
     dg = device_geometry(kernel, region, tuple(dims))
-    return bool(nat.lib().hicu_gram_uses_tensor_cores(dg.ref()))
+    st = nat.HicuGeom.from_buffer_copy(dg.struct)
+    st.flags |= nat.GEOM_FORCE_DENSE_GRAM
+    import ctypes
+
+    return bool(nat.lib().hicu_gram_uses_tensor_cores(ctypes.byref(st)))
 
 
-def gram_matrix(x, kernel: KernelMask, region: Region, force_simt: bool = False):
+def gram_path(kernel: KernelMask, region: Region, dims) -> str:
+    """Which Gram kernel hicu_gram runs: "lag", "tcgen05" or "simt"."""
+    dg = device_geometry(kernel, region, tuple(dims))
+    return nat.GRAM_PATHS[int(nat.lib().hicu_gram_path(dg.ref()))]
+
+
+def gram_matrix(x, kernel: KernelMask, region: Region, force_simt: bool = False, path: str | None = None):
     """G = H(x)^H H(x) (n x n, complex128) on the device; returns a CUDA tensor.
 
-    ``force_simt`` selects the SIMT kernel even where the tcgen05 kernel applies
-    (cross-checks)."""
+    ``path`` forces an implementation for cross-checks: "simt" / "tcgen05"
+    (the dense implicit-im2col Gram; "tcgen05" falls back to SIMT where the
+    tensor-core kernel does not apply) or None (the default: the lag Gram
+    where it applies).  ``force_simt`` is ``path="simt"``."""
+    if force_simt:
+        path = "simt"
     torch = nat.require_cuda()
     x = np.asarray(x) if not isinstance(x, torch.Tensor) else x
     region.validate(kernel, tuple(x.shape))
     dg = device_geometry(kernel, region, tuple(x.shape))
-    if force_simt:
+    if path in ("simt", "tcgen05"):
         import copy
 
         dg = copy.copy(dg)
         dg.struct = nat.HicuGeom.from_buffer_copy(dg.struct)
-        dg.struct.flags |= nat.GEOM_FORCE_SIMT_GRAM
+        dg.struct.flags |= nat.GEOM_FORCE_DENSE_GRAM | (nat.GEOM_FORCE_SIMT_GRAM if path == "simt" else 0)
+    elif path not in (None, "lag"):
+        raise ValueError(f"unknown Gram path {path!r}")
     L = nat.lib()
     ws_bytes = L.hicu_gram_workspace(dg.ref())
     ws = torch.empty(max(ws_bytes, 8), dtype=torch.uint8, device="cuda")

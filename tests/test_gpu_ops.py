@@ -269,14 +269,14 @@ def test_gram_tensor_core_parity(dims, kext, frac):
     k = H.KernelMask.full(kext)
     reg = H.stage_region(dims, k, frac)
     assert gram_uses_tensor_cores(k, reg, dims)
-    G = gram_matrix(x, k, reg).cpu().numpy()
-    Gs = gram_matrix(x, k, reg, force_simt=True).cpu().numpy()
     Gr = O.gram(x, O.stage_geom(dims, kext, frac))
-    assert rel(G, Gr) <= 2e-6
-    assert rel(Gs, Gr) <= 2e-6
-    assert np.array_equal(G, G.conj().T)
-    # deterministic: bit-identical on a second call
-    assert np.array_equal(G, gram_matrix(x, k, reg).cpu().numpy())
+    for path in ("tcgen05", "simt", None):  # None: the default (lag) Gram
+        G = gram_matrix(x, k, reg, path=path).cpu().numpy()
+        assert rel(G, Gr) <= 2e-6, path
+        if path != "simt":
+            assert np.array_equal(G, G.conj().T), path
+        # deterministic: bit-identical on a second call
+        assert np.array_equal(G, gram_matrix(x, k, reg, path=path).cpu().numpy()), path
 
 
 def test_gram_tensor_core_phantom_accuracy():
@@ -290,9 +290,10 @@ def test_gram_tensor_core_phantom_accuracy():
     x = c64(xc)
     k = H.KernelMask.full((5, 5, 8))
     reg = H.full_region(x.shape, k)
-    G = gram_matrix(x, k, reg).cpu().numpy()
     Gr = O.gram(x, O.full_geom(x.shape, (5, 5, 8)))
-    assert rel(G, Gr) <= 2e-6
+    for path in ("tcgen05", None):
+        G = gram_matrix(x, k, reg, path=path).cpu().numpy()
+        assert rel(G, Gr) <= 2e-6, path
 
 
 # ---- closed-form nullspace product (csrc/nsjl.cu) ------------------------------------------------

@@ -174,9 +174,11 @@ def test_gram_fp64_accuracy_3d():
         P = v[i:i + 4096].to(torch.complex128)
         G64 += P.conj().T @ P
     sc = float(G64.abs().max())
-    for force in (False, True):
-        G = H.gram_matrix(x, kernel, region, force_simt=force)
-        assert float((G - G64).abs().max()) / sc <= 1e-5, force
+    for path in (None, "tcgen05", "simt"):  # lag (default), dense tcgen05, dense SIMT
+        G = H.gram_matrix(x, kernel, region, path=path)
+        err = float((G - G64).abs().max()) / sc
+        print(f"3-D 5x5x5x8 Gram ({path or 'lag'}): max rel err {err:.2e}")
+        assert err <= 1e-5, path
 
 
 def test_sharded_cuda_backend_single_rank():

@@ -72,6 +72,7 @@ typedef struct hicu_geom {
 #define HICU_GEOM_FORCE_SIMT_GRAM 2   /* use the SIMT Gram even when tcgen05 applies */
 #define HICU_GEOM_FORCE_SIMT_CONV 4   /* use the SIMT conv/scatter even when tcgen05 applies */
 #define HICU_GEOM_FORCE_DENSE_GRAM 8  /* dense implicit-im2col Gram instead of the lag Gram */
+#define HICU_GEOM_FORCE_LAG_GRAM 16   /* lag Gram wherever it applies (default: by size) */
 
 /* hicu_gram_path() values */
 #define HICU_GRAM_PATH_SIMT 0     /* dense implicit-im2col Gram, fp32 SIMT (gram_simt.cu) */
@@ -179,7 +180,9 @@ int hicu_gram_uses_tensor_cores(const hicu_geom* g);
  * separable support, 1-3 spatial axes, spatial kernel extents <= 8, Nc in
  * 1..8, 10, 12, 16: G assembled from per-lag coil correlations over the
  * per-axis position classes of the shifted region boxes), else the dense
- * tcgen05 or SIMT implicit-im2col Gram; -1 on a bad geometry. */
+ * tcgen05 or SIMT implicit-im2col Gram; the dense tcgen05 Gram is kept for
+ * n < 400 (measured faster at the 5x5x8 kernels of C1/C2) unless
+ * HICU_GEOM_FORCE_LAG_GRAM; -1 on a bad geometry. */
 int hicu_gram_path(const hicu_geom* g);
 /* 1 when hicu_conv_fwd / hicu_conv_els / hicu_scatter_dc with p columns run
  * on the tcgen05 kernels (conv_tc.cu) for this geometry. */

@@ -156,9 +156,16 @@ extern "C" int hicu_device_sm_count(int* out) {
 
 // Gram path: the shift-structured lag Gram (gram_lag.cu) wherever it applies,
 // else the dense implicit-im2col Gram (tcgen05 3xTF32, or SIMT).
+// Measured crossover: for the 5x5x8 kernels of C1/C2 (n = 200) the dense
+// tcgen05 Gram is faster (0.17 vs 0.68 ms at C2's full 252^2 region: the lag
+// Gram's fixed costs -- per-lag partials, reduction, n^2 assembly -- dominate
+// at n = 200); from n ~ 500 on the lag Gram wins (C3 slice 3.9 -> 0.7 ms SIMT,
+// C5 volume 186 -> 56 ms tcgen05).
 static int gram_path(const hicu_geom* hg, const DevGeom& g) {
   const bool dense = (hg->flags & (HICU_GEOM_FORCE_DENSE_GRAM | HICU_GEOM_FORCE_SIMT_GRAM)) != 0;
-  if (!dense && hicu_gram_lag_supported(g)) return HICU_GRAM_PATH_LAG;
+  const bool tc = !(hg->flags & HICU_GEOM_FORCE_SIMT_GRAM) && hicu_gram_tc_supported(g);
+  const bool want_lag = (hg->flags & HICU_GEOM_FORCE_LAG_GRAM) != 0;
+  if (!dense && hicu_gram_lag_supported(g) && (want_lag || !(tc && g.n < 400))) return HICU_GRAM_PATH_LAG;
   if (!(hg->flags & HICU_GEOM_FORCE_SIMT_GRAM) && hicu_gram_tc_supported(g)) return HICU_GRAM_PATH_TCGEN05;
   return HICU_GRAM_PATH_SIMT;
 }

@@ -39,7 +39,8 @@ constexpr int kMaxK = 8;        // kernel extent per spatial axis
 constexpr int kMaxCls = 2 * kMaxK - 1;
 constexpr int kMaxBlocks = kMaxCls * kMaxCls;
 constexpr int kMaxOl = (kMaxCls * kMaxCls + 1) / 2;
-constexpr int kCoreThreadsMax = 384;
+constexpr int kCoreThreadsMax = 512;
+constexpr int kCoreStages = 4;   // lines in flight (cp.async ring)
 constexpr int kEdgeThreads = 256;
 constexpr int kLinesPerChunkA = 64;
 constexpr int kLinesPerChunkB = 1024;
@@ -86,11 +87,28 @@ struct LagPlan {
   int threadsA = 0;
 };
 
-int choose_cb(int nc) {
+// coil rows per warp: two Nc x CB blocks of fp32x2 accumulators (CB * Nc <= 20,
+// so 16 warps of <= 128 registers fit one SM)
+__host__ __device__ constexpr int cb_for(int nc) {
   int best = 1;
   for (int cb = 1; cb <= nc; ++cb)
-    if (nc % cb == 0 && cb * nc <= 64) best = cb;
+    if (nc % cb == 0 && cb * nc <= 20) best = cb;
   return best;
+}
+int choose_cb(int nc) { return cb_for(nc); }
+
+// one k-space position (Nc complex) per shared-memory row, padded to an odd
+// number of 16-byte chunks: lanes reading consecutive rows hit distinct banks
+__host__ __device__ constexpr int row_bytes(int nc) {
+  return 16 * (((nc * 8 + 15) / 16) % 2 ? (nc * 8 + 15) / 16 : (nc * 8 + 15) / 16 + 1);
+}
+
+// acc += conj(a) * b with two packed fp32x2 FMAs (FFMA2), both with a
+// broadcast scalar operand so no register pair is rebuilt per use:
+//   acc += a.x * (b.x, b.y) + a.y * (b.y, -b.x)      (bn = (b.y, -b.x), once per b)
+__device__ __forceinline__ float2 cfmac2(float2 acc, float2 a, float2 b, float2 bn) {
+  acc = __ffma2_rn(make_float2(a.x, a.x), b, acc);
+  return __ffma2_rn(make_float2(a.y, a.y), bn, acc);
 }
 
 void axis_classes(int64_t N, int64_t o, int64_t e, int K, bool circ, LagParams& p, int a) {
@@ -202,7 +220,7 @@ LagPlan make_plan(const DevGeom& g) {
     p.CA = p.chunksA[p.NB];
     pl.nA = (int64_t)p.nol * p.NG * p.CA;
     pl.threadsA = 32 * p.GZ * p.NCB;
-    pl.smemA = (size_t)2 * p.NC * (2 * p.P + p.GZ) * sizeof(float2);
+    pl.smemA = (size_t)kCoreStages * row_bytes(p.NC) * (2 * p.P + p.GZ);
     if (pl.smemA > (size_t)200 * 1024) return pl;
   }
   // edge kernel
@@ -289,18 +307,34 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// Grid: one CTA per (line chunk of a class block) x (outer lag, last-axis lag
+// group), the (lag, group) index fastest so CTAs resident together share
+// their k-space lines in L2.  Accumulation: acc += conj(a) b for a = base
+// position (CB coils of this warp's block), b = neighbour position + dz (all
+// Nc coils), as two broadcast-scalar FFMA2 chains per product
+//   accR += a.x * (b.x, b.y),  accI += a.y * (b.x, b.y)
+//   conj(a) b = (accR.x + accI.y, accR.y - accI.x)
+// so no operand pair is swapped or negated in the inner loop.
 template <int NC, int CB>
 __global__ void __launch_bounds__(kCoreThreadsMax, 1)
 lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
   hicu_pdl_entry();
-  extern __shared__ __align__(16) float2 lsm[];
+  constexpr int RB = row_bytes(NC);
+  constexpr bool V16 = (NC % 2) == 0;
+  extern __shared__ __align__(16) uint8_t lsm[];
   const int64_t bid = blockIdx.x;
-  const int olg = (int)(bid / P.CA);
-  const int rem = (int)(bid % P.CA);
+  const int nlg = P.nol * P.NG;
+  const int rowblk = (int)(bid / nlg);
+  const int olg = (int)(bid % nlg);
   const int ol = olg / P.NG, gzi = olg % P.NG;
   int b = 0;
-  while (P.chunksA[b + 1] <= rem) ++b;
-  const int chunk = rem - P.chunksA[b];
+  while (P.chunksA[b + 1] <= rowblk) ++b;
+  const int chunk = rowblk - P.chunksA[b];
   const int dz_lo = gzi * P.GZ - (P.K[P.L - 1] - 1);
   const int gz_n = min(P.GZ, P.DZ - gzi * P.GZ);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -315,84 +349,115 @@ lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
     return;
   }
   const int la = P.L - 1;
-  const int64_t Pn = P.P, NL = P.N[la];
-  const int64_t nw = Pn + P.GZ - 1;          // neighbour positions staged per line
-  const size_t bufsz = (size_t)NC * (Pn + nw);
-  const int64_t cs = P.cstride[la];           // == NC
+  const int pn = (int)P.P;
+  const int nw = pn + P.GZ - 1;               // neighbour rows per buffer
+  const int nwa = pn + gz_n - 1;              // neighbour rows the active lags read
+  const size_t bufsz = (size_t)(pn + nw) * RB;
+  const int64_t NL = P.N[la];
   auto stage = [&](int64_t li, int buf) {
     int64_t base, nbr;
     line_offsets(P, beg, len, ol, li, base, nbr);
-    float2* sb = lsm + (size_t)buf * bufsz;
-    float2* sn = sb + (size_t)NC * Pn;
-    for (int64_t e = threadIdx.x; e < Pn * NC; e += blockDim.x) {
-      const int64_t j = e / NC;
-      const int c = (int)(e % NC);
-      cp_async8(sb + (size_t)c * Pn + j, x + base + (P.c0 + j) * cs + c);
-    }
-    const int64_t nwa = Pn + gz_n - 1;  // positions the active lags read (a short last group stages less)
-    for (int64_t e = threadIdx.x; e < nwa * NC; e += blockDim.x) {
-      const int64_t j = e / NC;
-      const int c = (int)(e % NC);
-      int64_t q = P.c0 + dz_lo + j;
-      if (P.circ[la]) {
-        q %= NL;
-        if (q < 0) q += NL;
+    uint8_t* sb = lsm + (size_t)buf * bufsz;
+    uint8_t* sn = sb + (size_t)pn * RB;
+    if (V16) {
+      constexpr int H = NC / 2;  // 16-byte chunks per position
+      for (int e = threadIdx.x; e < pn * H; e += blockDim.x) {
+        const int j = e / H, k = e % H;
+        cp_async16(sb + j * RB + k * 16, x + base + (P.c0 + j) * NC + 2 * k);
       }
-      cp_async8(sn + (size_t)c * nw + j, x + nbr + q * cs + c);
+      for (int e = threadIdx.x; e < nwa * H; e += blockDim.x) {
+        const int j = e / H, k = e % H;
+        int64_t q = P.c0 + dz_lo + j;
+        if (P.circ[la]) {
+          q %= NL;
+          if (q < 0) q += NL;
+        }
+        cp_async16(sn + j * RB + k * 16, x + nbr + q * NC + 2 * k);
+      }
+    } else {
+      for (int e = threadIdx.x; e < pn * NC; e += blockDim.x) {
+        const int j = e / NC, c = e % NC;
+        cp_async8(sb + j * RB + c * 8, x + base + (P.c0 + j) * NC + c);
+      }
+      for (int e = threadIdx.x; e < nwa * NC; e += blockDim.x) {
+        const int j = e / NC, c = e % NC;
+        int64_t q = P.c0 + dz_lo + j;
+        if (P.circ[la]) {
+          q %= NL;
+          if (q < 0) q += NL;
+        }
+        cp_async8(sn + j * RB + c * 8, x + nbr + q * NC + c);
+      }
     }
   };
-  float2 acc[CB][NC];
+  float2 accR[CB][NC], accI[CB][NC];
 #pragma unroll
   for (int a = 0; a < CB; ++a)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) acc[a][c] = cf(0.f, 0.f);
+    for (int c = 0; c < NC; ++c) accR[a][c] = accI[a][c] = cf(0.f, 0.f);
   const bool active = dzi < gz_n;
-  if (l0 < l1) stage(l0, 0);
-  cp_async_commit();
-  int buf = 0;
-  for (int64_t li = l0; li < l1; ++li) {
-    if (li + 1 < l1) stage(li + 1, buf ^ 1);
+  // ring of kCoreStages line buffers: lines li+1 .. li+kCoreStages-1 are in
+  // flight while line li is consumed (one commit group per line, maybe empty)
+#pragma unroll
+  for (int k = 0; k < kCoreStages - 1; ++k) {
+    if (l0 + k < l1) stage(l0 + k, k);
     cp_async_commit();
-    cp_async_wait<1>();
+  }
+  for (int64_t li = l0; li < l1; ++li) {
+    const int buf = (int)((li - l0) % kCoreStages);
+    cp_async_wait<kCoreStages - 2>();
     __syncthreads();
+    // refill the buffer consumed in the previous iteration (free after the barrier)
+    if (li + kCoreStages - 1 < l1) stage(li + kCoreStages - 1, (int)((li - l0 + kCoreStages - 1) % kCoreStages));
+    cp_async_commit();
     if (active) {
-      const float2* sb = lsm + (size_t)buf * bufsz + (size_t)cbi * CB * Pn;
-      const float2* sn = lsm + (size_t)buf * bufsz + (size_t)NC * Pn + dzi;
-      for (int64_t j = lane; j < Pn; j += 32) {
+      const uint8_t* sb = lsm + (size_t)buf * bufsz + cbi * CB * 8;
+      const uint8_t* sn = lsm + (size_t)buf * bufsz + (size_t)pn * RB + dzi * RB;
+      for (int j = lane; j < pn; j += 32) {
         float2 a[CB], v[NC];
 #pragma unroll
-        for (int q = 0; q < CB; ++q) a[q] = sb[(size_t)q * Pn + j];
+        for (int q = 0; q < CB; ++q) a[q] = *(const float2*)(sb + j * RB + q * 8);
+        if (V16) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) v[c] = sn[(size_t)c * nw + j];
+          for (int k = 0; k < NC / 2; ++k) {
+            const float4 w = *(const float4*)(sn + j * RB + k * 16);
+            v[2 * k] = make_float2(w.x, w.y);
+            v[2 * k + 1] = make_float2(w.z, w.w);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v[c] = *(const float2*)(sn + j * RB + c * 8);
+        }
 #pragma unroll
         for (int q = 0; q < CB; ++q)
 #pragma unroll
-          for (int c = 0; c < NC; ++c) cfmac(acc[q][c], a[q], v[c]);
+          for (int c = 0; c < NC; ++c) {
+            accR[q][c] = __ffma2_rn(make_float2(a[q].x, a[q].x), v[c], accR[q][c]);
+            accI[q][c] = __ffma2_rn(make_float2(a[q].y, a[q].y), v[c], accI[q][c]);
+          }
       }
     }
-    __syncthreads();
-    buf ^= 1;
   }
   cp_async_wait<0>();
-  // fixed-order warp reduction of the lanes' partial sums
+  // conj(a) b, then a fixed-order warp reduction of the lanes' partial sums
 #pragma unroll
   for (int q = 0; q < CB; ++q)
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      float2 v = acc[q][c];
+      float2 v = make_float2(accR[q][c].x + accI[q][c].y, accR[q][c].y - accI[q][c].x);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
         v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
       }
-      acc[q][c] = v;
+      accR[q][c] = v;
     }
   if (lane == 0 && dzi < P.GZ) {
 #pragma unroll
     for (int q = 0; q < CB; ++q)
 #pragma unroll
       for (int c = 0; c < NC; ++c)
-        out[((size_t)dzi * NC + cbi * CB + q) * NC + c] = active ? acc[q][c] : cf(0.f, 0.f);
+        out[((size_t)dzi * NC + cbi * CB + q) * NC + c] = active ? accR[q][c] : cf(0.f, 0.f);
   }
 }
 
@@ -434,15 +499,16 @@ lag_edge_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
       for (int pz = pb; pz < pe; ++pz) {
         const int64_t pn = (int64_t)pz + dz;
         if (pn < 0 || pn >= P.N[la]) continue;
-        float2 a[CB], v[NC];
+        float2 a[CB];
 #pragma unroll
         for (int t = 0; t < CB; ++t) a[t] = x[base + pz * cs + cbi * CB + t];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) v[c] = x[nbr + pn * cs + c];
+        for (int c = 0; c < NC; ++c) {
+          const float2 v = x[nbr + pn * cs + c];
+          const float2 vn = make_float2(v.y, -v.x);
 #pragma unroll
-        for (int t = 0; t < CB; ++t)
-#pragma unroll
-          for (int c = 0; c < NC; ++c) cfmac(acc[t][c], a[t], v[c]);
+          for (int t = 0; t < CB; ++t) acc[t][c] = cfmac2(acc[t][c], a[t], v, vn);
+        }
       }
     }
   }
@@ -494,10 +560,11 @@ __global__ void lag_reduce_kernel(const __grid_constant__ LagParams P, const flo
     double sx = 0.0, sy = 0.0;
     if (cls == P.core_cls) {
       const int gzi = dz / P.GZ, dzi = dz % P.GZ;
-      const int64_t bid0 = ((int64_t)ol * P.NG + gzi) * P.CA + P.chunksA[b];
+      const int64_t nlg = (int64_t)P.nol * P.NG;
+      const int64_t bid0 = (int64_t)P.chunksA[b] * nlg + (int64_t)ol * P.NG + gzi;
       const int nch = P.chunksA[b + 1] - P.chunksA[b];
       for (int ch = 0; ch < nch; ++ch) {
-        const float2 v = partA[((bid0 + ch) * P.GZ + dzi) * NC2 + cc];
+        const float2 v = partA[((bid0 + ch * nlg) * P.GZ + dzi) * NC2 + cc];
         sx += v.x;
         sy += v.y;
       }
@@ -569,7 +636,7 @@ __global__ void lag_assemble_kernel(const __grid_constant__ LagParams P, const d
 
 template <int NC>
 int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
-  constexpr int CB = (NC <= 8) ? NC : (NC == 10 ? 5 : (NC == 12 ? 4 : (NC == 16 ? 4 : 1)));
+  constexpr int CB = cb_for(NC);
   const LagParams& P = pl.p;
   if (P.CB != CB) return hicu_set_error(HICU_ERR_PARAMETER, "gram_lag: coil block mismatch");
   float2* partA = (float2*)((char*)ws + pl.a_off);

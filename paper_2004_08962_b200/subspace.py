@@ -83,10 +83,15 @@ def gram_uses_tensor_cores(kernel: KernelMask, region: Region, dims) -> bool:
     return bool(nat.lib().hicu_gram_uses_tensor_cores(ctypes.byref(st)))
 
 
-def gram_path(kernel: KernelMask, region: Region, dims) -> str:
+def gram_path(kernel: KernelMask, region: Region, dims, force_lag: bool = False) -> str:
     """Which Gram kernel hicu_gram runs: "lag", "tcgen05" or "simt"."""
+    import ctypes
+
     dg = device_geometry(kernel, region, tuple(dims))
-    return nat.GRAM_PATHS[int(nat.lib().hicu_gram_path(dg.ref()))]
+    st = nat.HicuGeom.from_buffer_copy(dg.struct)
+    if force_lag:
+        st.flags |= nat.GEOM_FORCE_LAG_GRAM
+    return nat.GRAM_PATHS[int(nat.lib().hicu_gram_path(ctypes.byref(st)))]
 
 
 def gram_matrix(x, kernel: KernelMask, region: Region, force_simt: bool = False, path: str | None = None):
@@ -94,8 +99,9 @@ def gram_matrix(x, kernel: KernelMask, region: Region, force_simt: bool = False,
 
     ``path`` forces an implementation for cross-checks: "simt" / "tcgen05"
     (the dense implicit-im2col Gram; "tcgen05" falls back to SIMT where the
-    tensor-core kernel does not apply) or None (the default: the lag Gram
-    where it applies).  ``force_simt`` is ``path="simt"``."""
+    tensor-core kernel does not apply), "lag" (the lag Gram wherever it
+    applies) or None (the library's choice, :func:`gram_path`).
+    ``force_simt`` is ``path="simt"``."""
     if force_simt:
         path = "simt"
     torch = nat.require_cuda()
@@ -108,7 +114,13 @@ def gram_matrix(x, kernel: KernelMask, region: Region, force_simt: bool = False,
         dg = copy.copy(dg)
         dg.struct = nat.HicuGeom.from_buffer_copy(dg.struct)
         dg.struct.flags |= nat.GEOM_FORCE_DENSE_GRAM | (nat.GEOM_FORCE_SIMT_GRAM if path == "simt" else 0)
-    elif path not in (None, "lag"):
+    elif path == "lag":
+        import copy
+
+        dg = copy.copy(dg)
+        dg.struct = nat.HicuGeom.from_buffer_copy(dg.struct)
+        dg.struct.flags |= nat.GEOM_FORCE_LAG_GRAM
+    elif path is not None:
         raise ValueError(f"unknown Gram path {path!r}")
     L = nat.lib()
     ws_bytes = L.hicu_gram_workspace(dg.ref())

@@ -55,15 +55,15 @@ def test_lag_gram_matches_oracle(case):
     x = c64(rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
     k = H.KernelMask.ellipsoid(kext) if sup == "ellipsoid" else H.KernelMask.full(kext)
     reg = H.stage_region(dims, k, frac, circ)
-    assert gram_path(k, reg, dims) == "lag", (dims, kext)
-    G = gram_matrix(x, k, reg).cpu().numpy()
+    assert gram_path(k, reg, dims, force_lag=True) == "lag", (dims, kext)
+    G = gram_matrix(x, k, reg, path="lag").cpu().numpy()
     gm = O.stage_geom(dims, kext, frac, circ, None if sup == "full" else k.support)
     Gr = O.gram(x, gm)
     err = rel(G, Gr)
     assert err <= 2e-6, err
     assert np.array_equal(G, G.conj().T)               # Hermitian by construction
     assert np.all(np.diag(G).imag == 0)
-    assert np.array_equal(G, gram_matrix(x, k, reg).cpu().numpy())  # deterministic
+    assert np.array_equal(G, gram_matrix(x, k, reg, path="lag").cpu().numpy())  # deterministic
 
 
 def test_lag_gram_c5_shard_accuracy():
@@ -85,6 +85,7 @@ def test_lag_gram_c5_shard_accuracy():
     for i in range(0, v.shape[0], 4096):
         P = v[i:i + 4096].to(torch.complex128)
         G64 += P.conj().T @ P
+    assert gram_path(kernel, region, dims) == "lag"  # the library's choice at n = 1000
     G = gram_matrix(x, kernel, region)
     err = float((G - G64).abs().max() / G64.abs().max())
     print(f"lag Gram, C5 phantom shard {dims}: max rel err {err:.2e}")

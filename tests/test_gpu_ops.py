@@ -270,7 +270,7 @@ def test_gram_tensor_core_parity(dims, kext, frac):
     reg = H.stage_region(dims, k, frac)
     assert gram_uses_tensor_cores(k, reg, dims)
     Gr = O.gram(x, O.stage_geom(dims, kext, frac))
-    for path in ("tcgen05", "simt", None):  # None: the default (lag) Gram
+    for path in ("tcgen05", "simt", "lag", None):  # None: the library's choice
         G = gram_matrix(x, k, reg, path=path).cpu().numpy()
         assert rel(G, Gr) <= 2e-6, path
         if path != "simt":
@@ -291,7 +291,7 @@ def test_gram_tensor_core_phantom_accuracy():
     k = H.KernelMask.full((5, 5, 8))
     reg = H.full_region(x.shape, k)
     Gr = O.gram(x, O.full_geom(x.shape, (5, 5, 8)))
-    for path in ("tcgen05", None):
+    for path in ("tcgen05", "lag"):
         G = gram_matrix(x, k, reg, path=path).cpu().numpy()
         assert rel(G, Gr) <= 2e-6, path
 

@@ -156,7 +156,9 @@ int hicu_step_reduce(const double* obj_parts, int n_obj, const double* dc_parts,
 int hicu_step_apply(int64_t N, void* y, const void* gdir, const double* sums7,
                     int dc_mode, double lam, double* rec, void* stream);
 /* Data consistency on n contiguous samples of g (after the halo
- * accumulation of raw scatter partials); parts as hicu_scatter_dc's. */
+ * accumulation of raw scatter partials); parts as hicu_scatter_dc's.  mask
+ * bit 0: observed sample; bit 1: a halo copy of a plane another rank owns
+ * (the data consistency is applied, but the sample is left out of parts). */
 int hicu_dc_nparts(int64_t n);
 int hicu_dc_apply(int64_t n, void* g, const uint8_t* mask, const void* y,
                   const void* x0, int dc_mode, double lam, double* parts,
@@ -241,6 +243,14 @@ int hicu_nullspace_jl(int n, int r, const void* V, int cols, const void* Bin,
  * (64 < r <= 160 for large n, e.g. C4/C5) factor A_1 in global memory.
  * hicu_nullspace_jl_workspace(n, r) bytes (0: none needed). */
 size_t hicu_nullspace_jl_workspace(int n, int r);
+/* The outer iteration's nullspace tail as the stage driver runs it: Q~ = Q P
+ * for cols = G p JL columns from V (the closed form when it applies, the
+ * reflector chain -- householder_nullspace, subspace.py:158-212 -- when its
+ * pivot check gates it in).  pbig: n x cols c128 (rows < r ignored); B: n x
+ * cols c128 out; qt32: [cols/p][n][p] c64 out; refl: 2 n r c128 scratch; tau:
+ * r c128; flags: r + 1 ints; status: device int (DegenerateInputError). */
+int hicu_complement_jl(int n, int r, int cols, int p, const void* V, const void* pbig, void* B, void* qt32,
+                       void* refl, void* tau, int* flags, double tol, int* status, void* stream);
 int hicu_nullspace_jl_ws(int n, int r, const void* V, int cols, const void* Bin,
                          void* B, void* out32, int p, int* gate_dev, void* ws,
                          size_t ws_bytes, void* stream);

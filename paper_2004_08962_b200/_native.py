@@ -96,6 +96,8 @@ _SIGS = {
     "hicu_nystrom_workspace": (c_size_t, [c_int, c_int]),
     "hicu_nystrom": (c_int, [c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p,
                              c_void_p]),
+    "hicu_complement_jl": (c_int, [c_int, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_double, c_void_p, c_void_p]),
     "hicu_householder": (c_int, [c_int, c_int, c_void_p, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p]),
     "hicu_apply_reflectors": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,

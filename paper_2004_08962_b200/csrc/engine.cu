@@ -95,6 +95,24 @@ struct ProfScope {
 };
 }  // namespace
 
+// Householder complement of V and Q~_j = Q P_j for the cols = G p JL columns
+// (subspace.py:158-229): the closed form (nsjl.cu) when it applies, the
+// reference's reflector chain gated on its pivot check otherwise.  refl holds
+// 2 n r complex (also the closed form's scratch), flags r + 1 ints.
+extern "C" int hicu_complement_jl(int n, int r, int cols, int p, const void* V, const void* pbig, void* B, void* qt32,
+                                  void* refl, void* tau, int* flags, double tol, int* status, void* stream) {
+  const size_t refl_bytes = (size_t)2 * n * r * sizeof(double2);
+  const bool use_jl = hicu_nullspace_jl_supported(n, r) && hicu_nullspace_jl_workspace(n, r) <= refl_bytes;
+  const int* gate = nullptr;
+  int s;
+  if (use_jl) {
+    if ((s = hicu_nullspace_jl_ws(n, r, V, cols, pbig, B, qt32, p, flags + r, refl, refl_bytes, stream))) return s;
+    gate = flags + r;
+  }
+  if ((s = hicu_householder_gated(n, r, V, tol, refl, tau, flags, status, gate, stream))) return s;
+  return hicu_apply_reflectors_gated(n, r, refl, tau, flags, cols, pbig, B, qt32, p, gate, stream);
+}
+
 extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   if (!a) return hicu_set_error(HICU_ERR_PARAMETER, "run_stage: null args");
   const hicu_geom* gm = &a->geom;
@@ -106,8 +124,6 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   const int nsp = hicu_scatter_nparts(gm);
   if (ncp < 0 || nsp < 0) return HICU_ERR_SHAPE;
   const size_t nomega = (size_t)n * ell, npbig = (size_t)n * G * p;
-  const size_t refl_bytes = (size_t)2 * n * r * sizeof(double2);  // scratch for the global-LU closed form
-  const bool use_jl = hicu_nullspace_jl_supported(n, r) && hicu_nullspace_jl_workspace(n, r) <= refl_bytes;
   int s;
   for (int it = 0; it < a->iters; ++it) {
     // ---- nullspace: Gram + Nystrom (== rSVD subspace), or injected V ----
@@ -131,20 +147,8 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
     {
       ProfScope ps(a->prof, HICU_PROF_HOUSEHOLDER, st);
       const double2* pb = (const double2*)a->pbig + (size_t)it * npbig;
-      // closed form (nsjl.cu) first; the Householder kernels run only if it
-      // raised the gate (a pivot below its floor)
-      const int* gate = nullptr;
-      if (use_jl) {
-        if ((s = hicu_nullspace_jl_ws(n, r, a->V, G * p, pb, a->B, a->qt32, p, a->flags + r, a->refl, refl_bytes,
-                                      stream)))
-          return s;
-        gate = a->flags + r;
-      }
-      if ((s = hicu_householder_gated(n, r, a->V, a->householder_tol, a->refl, a->tau, a->flags, a->status, gate,
-                                      stream)))
-        return s;
-      if ((s = hicu_apply_reflectors_gated(n, r, a->refl, a->tau, a->flags, G * p, pb, a->B, a->qt32, p, gate,
-                                           stream)))
+      if ((s = hicu_complement_jl(n, r, G * p, p, a->V, pb, a->B, a->qt32, a->refl, a->tau, a->flags,
+                                  a->householder_tol, a->status, stream)))
         return s;
     }
     // ---- gradient steps ----

@@ -926,19 +926,21 @@ __global__ void dc_apply_kernel(int64_t n, float2* __restrict__ g, const uint8_t
   double a_g = 0.0, a_res = 0.0, a_num = 0.0, a_den = 0.0;
   for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += (int64_t)gridDim.x * blockDim.x) {
     float2 acc = g[m];
-    const bool on = mask[m] == 1;
+    const uint8_t mk = mask[m];
+    const bool on = (mk & 1) != 0;
+    const bool cnt = (mk & 2) == 0;  // bit 1: a halo copy of another rank's plane, not summed
     if (dc_mode == 0) {
       if (on) acc = cf(0.f, 0.f);
     } else {
       const float2 res = on ? (y[m] - x0[m]) : cf(0.f, 0.f);
-      a_res += (double)res.x * res.x + (double)res.y * res.y;
+      if (cnt) a_res += (double)res.x * res.x + (double)res.y * res.y;
       acc = acc + lam * res;
-      if (on) {
+      if (on && cnt) {
         a_num += (double)acc.x * res.x + (double)acc.y * res.y;
         a_den += (double)acc.x * acc.x + (double)acc.y * acc.y;
       }
     }
-    a_g += (double)acc.x * acc.x + (double)acc.y * acc.y;
+    if (cnt) a_g += (double)acc.x * acc.x + (double)acc.y * acc.y;
     g[m] = acc;
   }
   double v[4] = {a_g, a_res, a_num, a_den};

@@ -7,10 +7,12 @@ plumbing:
   :func:`reconstruct_slices`: every rank reconstructs its own contiguous block
   of slices; there is no data-path collective (weak scaling).
 
-* **One volume sharded along axis 0 (C5)** — :class:`ShardPlan` /
-  :class:`ShardedReconstruction`: the region's output rows on axis 0 are
-  split into contiguous blocks; rank k owns k-space planes [P_k, P_{k+1}) and
-  holds K0-1 trailing halo planes.  Per outer iteration the local Gram
+* **One volume sharded along one axis (C5: readout; C4: time)** —
+  :class:`ShardPlan` / :class:`ShardedReconstruction`: the region's output
+  rows on that axis are split into contiguous blocks; rank k owns k-space
+  planes [P_k, P_{k+1}) and holds the K-1 trailing halo planes its rows read
+  (spanning several neighbours when a shard is thinner than the halo, and
+  wrapping around as a ring on a circular axis).  Per outer iteration the local Gram
   partials are all-reduced (n x n complex128) and the nullspace step runs
   redundantly (bit-identical on every rank).  Per gradient step:
     conv_fwd (local rows) -> raw scatter over local planes
@@ -79,11 +81,15 @@ def split_rows(n_rows: int, world: int):
 
 @dataclass
 class ShardPlan:
-    """Plane ownership for a volume sharded along axis 0.
+    """Plane ownership for a volume sharded along one axis (``axis``).
 
-    ``rows`` are the region's output rows on axis 0 (offset ``roff``); rank k
-    owns k-space planes [P[k], P[k+1]) and holds planes
-    [P[k], min(D, P[k+1] + K0 - 1)) locally."""
+    ``rows`` are the region's output rows on that axis (offset ``roff``); rank
+    k owns k-space planes [P[k], P[k+1]) and holds, after them, the K-1
+    trailing halo planes its output rows read (K = the kernel extent on the
+    axis).  A shard may be thinner than its halo (C4: 21 output frames over 8
+    GPUs against a 4-frame halo): the trailing halo then spans several
+    neighbours.  On a circular axis (``circular``, region = the whole axis)
+    the planes wrap: the last rank's halo is the first ranks' planes (a ring)."""
 
     dims: tuple
     k0: int
@@ -91,19 +97,29 @@ class ShardPlan:
     rext: int
     world: int
     rank: int
+    axis: int = 0
+    circular: bool = False
 
     def __post_init__(self):
         self.dims = tuple(int(d) for d in self.dims)
-        D = self.dims[0]
+        D = self.dims[self.axis]
+        if self.rext < self.world:
+            raise ConfigError(f"{self.rext} output rows on axis {self.axis} cannot be shared by {self.world} ranks")
         blocks = split_rows(self.rext, self.world)
         self.rows = blocks
-        self.P = [0] + [self.roff + b[0] for b in blocks[1:]] + [D]
-        halo = self.k0 - 1
+        if self.circular:
+            if self.roff != 0 or self.rext != D:
+                raise ConfigError("a circular sharded axis must carry the full region")
+            self.P = [b[0] for b in blocks] + [D]
+        else:
+            self.P = [0] + [self.roff + b[0] for b in blocks[1:]] + [D]
+        self.halo = self.k0 - 1
         for k in range(self.world):
-            if self.P[k + 1] - self.P[k] < max(halo, 1):
-                raise ConfigError(f"shard {k} owns {self.P[k + 1] - self.P[k]} planes, fewer than the "
-                                  f"{halo}-plane halo; use fewer ranks")
-        self.halo = halo
+            if self.P[k + 1] - self.P[k] < 1:
+                raise ConfigError(f"shard {k} owns no plane; use fewer ranks")
+
+    def for_rank(self, k: int) -> "ShardPlan":
+        return ShardPlan(self.dims, self.k0, self.roff, self.rext, self.world, k, self.axis, self.circular)
 
     @property
     def r0(self) -> int:
@@ -119,31 +135,71 @@ class ShardPlan:
 
     @property
     def plane_hi(self) -> int:
-        """One past the last locally held plane (owned + trailing halo)."""
-        return min(self.dims[0], self.P[self.rank + 1] + self.halo)
+        """One past the last locally held plane (owned + trailing halo; may
+        exceed the axis length on a circular axis)."""
+        if self.circular:
+            return self.P[self.rank + 1] + self.halo
+        return min(self.dims[self.axis], self.P[self.rank + 1] + self.halo)
 
     @property
     def owned(self) -> int:
         return self.P[self.rank + 1] - self.P[self.rank]
 
     @property
+    def planes(self) -> list:
+        """Global plane index of every local plane (owned, then halo)."""
+        D = self.dims[self.axis]
+        return [p % D for p in range(self.plane_lo, self.plane_hi)]
+
+    @property
     def local_dims(self) -> tuple:
-        return (self.plane_hi - self.plane_lo,) + self.dims[1:]
+        d = list(self.dims)
+        d[self.axis] = self.plane_hi - self.plane_lo
+        return tuple(d)
 
     @property
     def local_roff0(self) -> int:
-        return self.roff + self.r0 - self.plane_lo
+        return 0 if self.circular else self.roff + self.r0 - self.plane_lo
 
     @property
     def trailing(self) -> int:
         """Halo planes held after the owned block."""
         return self.plane_hi - self.P[self.rank + 1]
 
+    def owner(self, p: int) -> int:
+        p %= self.dims[self.axis]
+        for k in range(self.world):
+            if self.P[k] <= p < self.P[k + 1]:
+                return k
+        raise ValueError(p)
+
+    def trailing_runs(self):
+        """Runs of trailing halo planes with one owner: (local start, count,
+        owner, start in the owner's local planes)."""
+        runs = []
+        pl = self.planes
+        for i in range(self.owned, len(pl)):
+            o = self.owner(pl[i])
+            oi = pl[i] - self.P[o]
+            if runs and runs[-1][2] == o and runs[-1][0] + runs[-1][1] == i and runs[-1][3] + runs[-1][1] == oi:
+                runs[-1][1] += 1
+            else:
+                runs.append([i, 1, o, oi])
+        return [tuple(r) for r in runs]
+
 
 class HaloExchange:
-    """Neighbour exchanges of plane blocks over ``torch.distributed`` (NCCL for
-    CUDA tensors, gloo for CPU tensors).  Tensors are (planes, ...) with
-    axis 0 the sharded axis, contiguous."""
+    """Exchanges of plane blocks along the sharded axis over
+    ``torch.distributed`` (NCCL for CUDA tensors, gloo for CPU tensors).
+
+    Every rank derives the whole exchange pattern from the plans of all ranks:
+    each trailing halo run goes to (accumulate) or comes from (refresh) the
+    rank owning those planes, which may be several ranks away when shards are
+    thinner than the halo, and wraps around on a circular axis.  Received
+    partials are added in a fixed (source-rank) order.  With a ``gloo``
+    group, device tensors are staged through host memory (gloo moves host
+    buffers): the CPU-only multi-rank tests and the single-GPU multi-process
+    test of the CUDA backend."""
 
     def __init__(self, plan: ShardPlan, group=None):
         import torch.distributed as dist
@@ -151,52 +207,89 @@ class HaloExchange:
         self.plan = plan
         self.group = group
         self.dist = dist
+        self.host_staged = dist.get_backend(group) == "gloo"
+        self.sends, self.recvs = [], []  # accumulate direction
+        for k in range(plan.world):
+            for (i0, n, owner, oi0) in plan.for_rank(k).trailing_runs():
+                if k == plan.rank:
+                    self.sends.append((owner, i0, n, oi0))
+                if owner == plan.rank:
+                    self.recvs.append((k, oi0, n, i0))
+        self.recvs.sort(key=lambda r: (r[0], r[1]))
 
-    def _exchange(self, send_to, send_buf, recv_from, recv_buf):
-        dist = self.dist
-        ops = []
-        if send_to is not None:
-            ops.append(dist.P2POp(dist.isend, send_buf.contiguous(), send_to, group=self.group))
-        if recv_from is not None:
-            ops.append(dist.P2POp(dist.irecv, recv_buf, recv_from, group=self.group))
+    def _peer(self, k):
+        return k if self.group is None else self.dist.get_global_rank(self.group, k)
+
+    def _run(self, ops):
         if ops:
-            for r in dist.batch_isend_irecv(ops):
+            for r in self.dist.batch_isend_irecv(ops):
                 r.wait()
 
-    def accumulate(self, g_local):
-        """Send my trailing halo partials to the next rank; add the previous
-        rank's trailing partials into my first owned planes."""
+    def _out(self, t):
+        t = t.contiguous()
+        return t.cpu() if self.host_staged and t.is_cuda else t
+
+    def _buf(self, like, shape):
         import torch
 
-        pl = self.plan
-        nxt = pl.rank + 1 if pl.rank + 1 < pl.world else None
-        prv = pl.rank - 1 if pl.rank > 0 else None
-        send = g_local[pl.owned:pl.owned + pl.trailing] if nxt is not None else None
-        recv = None
-        if prv is not None:
-            prev_plan = ShardPlan(pl.dims, pl.k0, pl.roff, pl.rext, pl.world, prv)
-            recv = torch.empty((prev_plan.trailing,) + tuple(g_local.shape[1:]), dtype=g_local.dtype,
-                               device=g_local.device)
-        self._exchange(nxt, send, prv, recv)
-        if recv is not None:
-            g_local[:recv.shape[0]] += recv
+        dev = "cpu" if self.host_staged else like.device
+        return torch.empty(shape, dtype=like.dtype, device=dev)
+
+    def accumulate(self, g_local):
+        """Send my trailing halo partials to their owners; add the partials
+        other ranks hold of my owned planes into them."""
+        import torch
+
+        dist, ax, me = self.dist, self.plan.axis, self.plan.rank
+        ops, bufs = [], []
+        for (dst, i0, n, oi0) in self.sends:
+            if dst == me:
+                continue
+            ops.append(dist.P2POp(dist.isend, self._out(g_local.narrow(ax, i0, n)), self._peer(dst),
+                                  group=self.group))
+        for (src, oi0, n, i0) in self.recvs:
+            if src == me:
+                bufs.append((oi0, g_local.narrow(ax, i0, n).clone()))
+                continue
+            shape = list(g_local.shape)
+            shape[ax] = n
+            buf = self._buf(g_local, shape)
+            ops.append(dist.P2POp(dist.irecv, buf, self._peer(src), group=self.group))
+            bufs.append((oi0, buf))
+        self._run(ops)
+        for oi0, buf in bufs:
+            g_local.narrow(ax, oi0, buf.shape[ax]).add_(buf.to(g_local.device))
 
     def refresh(self, g_local):
-        """Send my first owned planes to the previous rank's halo; receive my
-        trailing halo from the next rank."""
-        pl = self.plan
-        nxt = pl.rank + 1 if pl.rank + 1 < pl.world else None
-        prv = pl.rank - 1 if pl.rank > 0 else None
-        send = None
-        if prv is not None:
-            prev_plan = ShardPlan(pl.dims, pl.k0, pl.roff, pl.rext, pl.world, prv)
-            send = g_local[:prev_plan.trailing]
-        recv = g_local[pl.owned:pl.owned + pl.trailing] if nxt is not None else None
-        if recv is not None and not recv.is_contiguous():
-            raise ConfigError("halo block must be contiguous")
-        self._exchange(prv, send, nxt, recv)
+        """Owners send the final values of my trailing halo planes to me."""
+        import torch
+
+        dist, ax, me = self.dist, self.plan.axis, self.plan.rank
+        ops, fills = [], []
+        for (src, oi0, n, i0) in self.recvs:
+            if src == me:
+                continue
+            ops.append(dist.P2POp(dist.isend, self._out(g_local.narrow(ax, oi0, n)), self._peer(src),
+                                  group=self.group))
+        for (dst, i0, n, oi0) in self.sends:
+            if dst == me:
+                fills.append((i0, g_local.narrow(ax, oi0, n).clone()))
+                continue
+            shape = list(g_local.shape)
+            shape[ax] = n
+            buf = self._buf(g_local, shape)
+            ops.append(dist.P2POp(dist.irecv, buf, self._peer(dst), group=self.group))
+            fills.append((i0, buf))
+        self._run(ops)
+        for i0, buf in fills:
+            g_local.narrow(ax, i0, buf.shape[ax]).copy_(buf)
 
     def allreduce_(self, t):
+        if self.host_staged and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+            return t
         self.dist.all_reduce(t, group=self.group)
         return t
 
@@ -239,18 +332,22 @@ class ShardedReconstruction:
         return self.b.result()
 
 
-def plan_for(dims, kernel, schedule, world: int, rank: int) -> ShardPlan:
-    """Shard plan along axis 0; every stage must span axis 0 in full."""
+def plan_for(dims, kernel, schedule, world: int, rank: int, axis: int = 0) -> ShardPlan:
+    """Shard plan along ``axis`` (a spatial axis); every stage must have the
+    same region on that axis (C5: readout, axis 0; C4: time, axis 2, whose
+    center-out stage windows only x and y)."""
     from .solver import stage_region
 
+    nd = len(dims)
+    if not (0 <= axis < nd - 1):
+        raise ConfigError(f"cannot shard along axis {axis} (the last axis is the coil axis)")
     regs = [stage_region(dims, kernel, st.region, schedule.circular_axes) for st in schedule.stages]
-    if 0 in set(schedule.circular_axes):
-        raise ConfigError("axis 0 must not be circular in sharded mode")
-    r0 = {(r.offsets[0], r.extents[0]) for r in regs}
-    if len(r0) != 1:
-        raise ConfigError("sharded mode needs the same axis-0 region in every stage")
-    roff, rext = r0.pop()
-    return ShardPlan(tuple(dims), kernel.extents[0], roff, rext, world, rank)
+    ra = {(r.offsets[axis], r.extents[axis]) for r in regs}
+    if len(ra) != 1:
+        raise ConfigError(f"sharded mode needs the same axis-{axis} region in every stage")
+    roff, rext = ra.pop()
+    circ = axis in {int(a) % nd for a in schedule.circular_axes}
+    return ShardPlan(tuple(dims), kernel.extents[axis], roff, rext, world, rank, axis, circ)
 
 
 class CudaShardBackend:
@@ -267,29 +364,41 @@ class CudaShardBackend:
         self.schedule = schedule
         self.plan = plan
         self.kernel = kernel
-        lo, hi = plan.plane_lo, plan.plane_hi
+        ax = plan.axis
         x0 = np.asarray(x0)
         mask = np.asarray(mask)
         observed = mask == 1
-        xm = np.where(observed, x0, 0).astype(np.complex64)[lo:hi]
-        self.mask_np = observed.astype(np.uint8)[lo:hi]
+        planes = plan.planes
+        xm = np.take(np.where(observed, x0, 0).astype(np.complex64), planes, axis=ax)
+        self.mask_np = np.take(observed.astype(np.uint8), planes, axis=ax)
         ldims = plan.local_dims
+        circ_local = tuple(a for a in schedule.circular_axes if int(a) % x0.ndim != ax)
         self.regions = []
         for st in schedule.stages:
             rg = stage_region(x0.shape, kernel, st.region, schedule.circular_axes)
-            offs = (plan.local_roff0,) + rg.offsets[1:]
-            exts = (plan.r1 - plan.r0,) + rg.extents[1:]
-            self.regions.append(Region(offs, exts, rg.circular_axes))
-        self.eng = ReconEngine(xm, self.mask_np, ldims, kernel, schedule, self.regions)
+            offs, exts = list(rg.offsets), list(rg.extents)
+            offs[ax], exts[ax] = plan.local_roff0, plan.r1 - plan.r0
+            self.regions.append(Region(tuple(offs), tuple(exts), frozenset(int(a) % x0.ndim for a in circ_local)))
+        local_sched = schedule
+        if len(circ_local) != len(schedule.circular_axes):
+            import copy
+
+            local_sched = copy.copy(schedule)
+            local_sched.circular_axes = circ_local
+        self.eng = ReconEngine(xm, self.mask_np, ldims, kernel, local_sched, self.regions)
         for si, st in enumerate(schedule.stages):
             om, pb = draw_stage(schedule, si, st, kernel.n)
             self.eng.set_host_draws(si, om, pb)
         self.geoms = [device_geometry(kernel, rg, ldims) for rg in self.regions]
         self.sums = torch.zeros(8, dtype=torch.float64, device="cuda")
-        e = self.eng
-        self.dc_parts = torch.zeros(4 * nat.lib().hicu_dc_nparts(max(1, plan.owned * int(np.prod(ldims[1:])))),
-                                    dtype=torch.float64, device="cuda")
-        self.plane = int(np.prod(ldims[1:]))
+        # data-consistency mask: bit 1 marks the halo planes (left out of the step sums)
+        dcm = self.mask_np.copy()
+        sl = [slice(None)] * len(ldims)
+        sl[ax] = slice(plan.owned, None)
+        dcm[tuple(sl)] |= 2
+        self.dc_mask = to_dev(dcm, np.uint8).reshape(-1)
+        self.N = int(np.prod(ldims))
+        self.dc_parts = torch.zeros(4 * nat.lib().hicu_dc_nparts(self.N), dtype=torch.float64, device="cuda")
         self.ldims = ldims
 
     @staticmethod
@@ -306,17 +415,17 @@ class CudaShardBackend:
         return e.G
 
     def nullspace(self, si, it, G):
+        """Nystrom on the all-reduced Gram, then the stage driver's closed-form
+        complement (hicu_complement_jl): bit-identical on every rank."""
         e, L, nat = self.eng, self.nat.lib(), self.nat
         n, r, ell = e.n, e.r, e.ell
         st = self.schedule.stages[si]
         om, pb = e.stage_data[si]
         nat.check(L.hicu_nystrom(n, ell, r, G.data_ptr(), om[it].data_ptr(), e.V.data_ptr(), e.nys_ws.data_ptr(),
                                  e.nys_bytes, e.status.data_ptr(), self._st()), "nystrom")
-        nat.check(L.hicu_householder(n, r, e.V.data_ptr(), 1e-12, e.refl.data_ptr(), e.tau.data_ptr(),
-                                     e.flags.data_ptr(), e.status.data_ptr(), self._st()), "householder")
-        nat.check(L.hicu_apply_reflectors(n, r, e.refl.data_ptr(), e.tau.data_ptr(), e.flags.data_ptr(),
-                                          st.gradient_steps * st.p, pb[it].data_ptr(), e.B.data_ptr(),
-                                          e.qt32.data_ptr(), st.p, self._st()), "reflectors")
+        nat.check(L.hicu_complement_jl(n, r, st.gradient_steps * st.p, st.p, e.V.data_ptr(), pb[it].data_ptr(),
+                                       e.B.data_ptr(), e.qt32.data_ptr(), e.refl.data_ptr(), e.tau.data_ptr(),
+                                       e.flags.data_ptr(), 1e-12, e.status.data_ptr(), self._st()), "complement_jl")
 
     def _qt(self, si, j):
         e = self.eng
@@ -335,17 +444,18 @@ class CudaShardBackend:
         self.nat.check(L.hicu_scatter_dc(self.geoms[si].ref(), self._qt(si, j), self.schedule.stages[si].p,
                                          e.u.data_ptr(), e.mask.data_ptr(), None, None, 2, 0.0, e.g.data_ptr(),
                                          e.dc_parts.data_ptr(), self._st()), "scatter")
-        return e.g.view(self.ldims[0], -1)
+        return e.g.view(self.ldims)
 
     def dc_apply(self, owned_planes):
+        """DC on every local sample; the step sums count the owned planes only
+        (halo planes carry bit 1 of the DC mask; refresh overwrites them)."""
         e, L = self.eng, self.nat.lib()
-        n = owned_planes * self.plane
         soft = self.schedule.dc_mode == "soft"
-        self.nat.check(L.hicu_dc_apply(n, e.g.data_ptr(), e.mask.data_ptr(), e.y.data_ptr(),
+        self.nat.check(L.hicu_dc_apply(self.N, e.g.data_ptr(), self.dc_mask.data_ptr(), e.y.data_ptr(),
                                        e.x0.data_ptr() if soft else None, 1 if soft else 0,
                                        float(self.schedule.dc_lambda) if soft else 0.0, self.dc_parts.data_ptr(),
                                        self._st()), "dc_apply")
-        self._ndc = self.nat.lib().hicu_dc_nparts(n)
+        self._ndc = self.nat.lib().hicu_dc_nparts(self.N)
 
     def conv_els(self, si, j):
         e, L = self.eng, self.nat.lib()
@@ -372,49 +482,53 @@ class CudaShardBackend:
     def result(self):
         """(owned planes of y as complex128, per-stage record arrays)."""
         pl = self.plan
-        y = self.eng.y.view(self.ldims)[:pl.owned].cpu().numpy().astype(np.complex128)
+        y = self.eng.y.view(self.ldims).narrow(pl.axis, 0, pl.owned).cpu().numpy().astype(np.complex128)
         recs = [r.cpu().numpy().reshape(-1, self.nat.REC_SLOTS) for r in self.eng.recs]
         return y, recs
 
 
 def gather_planes(local_owned, plan: ShardPlan, group=None):
-    """All-gather the owned planes of every rank into the full volume
-    (rank order = plane order).  Works for CPU (gloo) and CUDA (NCCL)."""
+    """All-gather the owned planes of every rank along the sharded axis into
+    the full volume (rank order = plane order).  CPU (gloo) or CUDA (NCCL)."""
     import torch
     import torch.distributed as dist
 
+    ax = plan.axis
     t = torch.as_tensor(local_owned)
     maxp = max(plan.P[k + 1] - plan.P[k] for k in range(plan.world))
-    pad = torch.zeros((maxp,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    pad[:t.shape[0]] = t
-    if pad.is_complex():
-        pad_r = torch.view_as_real(pad).contiguous()
-    else:
-        pad_r = pad
+    shape = list(t.shape)
+    shape[ax] = maxp
+    pad = torch.zeros(shape, dtype=t.dtype, device=t.device)
+    pad.narrow(ax, 0, t.shape[ax]).copy_(t)
+    pad_r = torch.view_as_real(pad).contiguous() if pad.is_complex() else pad
     outs = [torch.empty_like(pad_r) for _ in range(plan.world)]
     dist.all_gather(outs, pad_r, group=group)
     blocks = []
     for k in range(plan.world):
         o = torch.view_as_complex(outs[k]) if pad.is_complex() else outs[k]
-        blocks.append(o[:plan.P[k + 1] - plan.P[k]])
-    return torch.cat(blocks, dim=0)
+        blocks.append(o.narrow(ax, 0, plan.P[k + 1] - plan.P[k]))
+    return torch.cat(blocks, dim=ax)
 
 
-def sharded_reconstruct(x0, mask, kernel, schedule, group=None):
-    """Reconstruct one volume sharded along axis 0 over the ranks of
-    ``group`` (one GPU per rank).  Returns (xhat complex128 full volume,
-    records of this rank's run: list per stage of [iters*G, 8] arrays)."""
+def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0):
+    """Reconstruct one volume sharded along ``axis`` (C5: readout, 0; C4:
+    time, 2) over the ranks of ``group`` (one GPU per rank).  Returns (xhat
+    complex128 full volume, records of this rank's run: list per stage of
+    [iters*G, 8] arrays)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    plan = plan_for(np.asarray(x0).shape, kernel, schedule, world, rank)
+    plan = plan_for(np.asarray(x0).shape, kernel, schedule, world, rank, axis)
     backend = CudaShardBackend(x0, mask, kernel, schedule, plan)
     halo = HaloExchange(plan, group)
     y_owned, recs = ShardedReconstruction(backend, plan, halo).run()
     import torch
 
-    full = gather_planes(torch.from_numpy(y_owned).cuda(), plan, group).cpu().numpy()
+    yt = torch.from_numpy(y_owned)
+    if not halo.host_staged:
+        yt = yt.cuda()
+    full = gather_planes(yt, plan, group).cpu().numpy()
     obs = np.asarray(mask) == 1
     if schedule.dc_mode == "hard":
         full[obs] = np.asarray(x0, np.complex128)[obs]

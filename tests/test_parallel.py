@@ -37,7 +37,24 @@ def test_shard_plan_planes():
     assert sum(p.owned for p in pl) == 256
     assert all(p.trailing == 4 for p in pl[:-1]) and pl[-1].trailing == 0
     with pytest.raises(H.ConfigError):
-        ShardPlan((20, 8, 2), 5, 0, 16, 8, 0)  # 2-plane shards < 4-plane halo
+        ShardPlan((20, 8, 2), 5, 0, 6, 8, 0)  # more ranks than output rows
+
+
+def test_shard_plan_time_axis_thin_shards():
+    """C4: 21 valid output frames over 8 GPUs (3,3,3,3,3,2,2,2) against a
+    4-frame halo: trailing halos span two neighbours; circular time: a ring."""
+    dims = (192, 144, 25, 8)
+    pl = [ShardPlan(dims, 5, 0, 21, 8, k, axis=2) for k in range(8)]
+    assert [p.r1 - p.r0 for p in pl] == [3, 3, 3, 3, 3, 2, 2, 2]
+    assert sum(p.owned for p in pl) == 25 and pl[-1].owned == 6  # the last rank also owns the 4 tail frames
+    assert pl[5].planes == [15, 16, 17, 18, 19, 20] and pl[5].local_dims == (192, 144, 6, 8)
+    # rank 5 (planes 15-16) reads frames 17-20: two from rank 6, two from rank 7
+    assert pl[5].trailing_runs() == [(2, 2, 6, 0), (4, 2, 7, 0)]
+    ring = [ShardPlan(dims, 5, 0, 25, 8, k, axis=2, circular=True) for k in range(8)]
+    assert [p.owned for p in ring] == [4, 3, 3, 3, 3, 3, 3, 3]
+    assert ring[7].planes == [22, 23, 24, 0, 1, 2, 3]            # wraps onto ranks 0 (and 1)
+    assert ring[7].trailing_runs() == [(3, 4, 0, 0)]
+    assert ring[6].trailing_runs() == [(3, 3, 7, 0), (6, 1, 0, 0)]
 
 
 class CpuBackend:
@@ -46,20 +63,21 @@ class CpuBackend:
     def __init__(self, x0, mask, kext, schedule, plan):
         self.schedule = schedule
         self.plan = plan
-        lo, hi = plan.plane_lo, plan.plane_hi
+        ax = plan.axis
         obs = mask == 1
-        self.y = torch.from_numpy(np.where(obs, x0, 0).astype(np.complex128)[lo:hi].copy())
+        self.y = torch.from_numpy(np.take(np.where(obs, x0, 0).astype(np.complex128), plan.planes, axis=ax).copy())
         self.x0 = self.y.clone()
-        self.mask = torch.from_numpy(obs[lo:hi].copy())
+        self.mask = torch.from_numpy(np.take(obs, plan.planes, axis=ax).copy())
         self.ldims = tuple(self.y.shape)
         self.kext = kext
         kern = H.KernelMask.full(kext)
         self.geoms = []
         for st in schedule.stages:
             rg = stage_region(x0.shape, kern, st.region, schedule.circular_axes)
-            offs = (plan.local_roff0,) + rg.offsets[1:]
-            exts = (plan.r1 - plan.r0,) + rg.extents[1:]
-            self.geoms.append(O.Geom(self.ldims, kern.positions, offs, exts, frozenset(rg.circular_axes)))
+            offs, exts = list(rg.offsets), list(rg.extents)
+            offs[ax], exts[ax] = plan.local_roff0, plan.r1 - plan.r0
+            circ = frozenset(a for a in rg.circular_axes if a != ax)
+            self.geoms.append(O.Geom(self.ldims, kern.positions, tuple(offs), tuple(exts), circ))
         self.draws = [draw_stage(schedule, si, st, kern.n) for si, st in enumerate(schedule.stages)]
         self.recs = [np.zeros((st.iterations * st.gradient_steps, 8)) for st in schedule.stages]
 
@@ -89,7 +107,8 @@ class CpuBackend:
         return self.g
 
     def dc_apply(self, owned):
-        g, m, y, x0 = self.g[:owned], self.mask[:owned], self.y[:owned], self.x0[:owned]
+        ax = self.plan.axis
+        g, m, y, x0 = (t.narrow(ax, 0, owned) for t in (self.g, self.mask, self.y, self.x0))
         lam = self.schedule.dc_lambda
         if self.schedule.dc_mode == "hard":
             g[m] = 0
@@ -119,7 +138,7 @@ class CpuBackend:
         self.recs[si][it * self.schedule.stages[si].gradient_steps + j, :4] = [obj, num, den, eta]
 
     def result(self):
-        return self.y[:self.plan.owned].numpy(), self.recs
+        return self.y.narrow(self.plan.axis, 0, self.plan.owned).numpy(), self.recs
 
 
 def _problem():
@@ -181,4 +200,63 @@ def test_sharded_two_ranks_match_single_domain(tmp_path, dc_mode):
                                nullspace="nystrom", canonical=True, dc_mode=dc_mode,
                                dc_lambda=2.0 if dc_mode == "soft" else 0.0)
     xs = np.where(mask == 1, x0, a["full"]) if dc_mode == "hard" else a["full"]
+    assert np.abs(xs - xo).max() <= 1e-9 * np.abs(xo).max()
+
+
+def _problem_t(circular):
+    """2D+t series (C4's structure at toy size): 9 frames, a 3x3x5x2 kernel
+    (4-frame halo), center-out x/y window then the full grid."""
+    rng = np.random.default_rng(8)
+    dims = (10, 8, 9, 2)
+    base = rng.standard_normal((4, 2)) + 1j * rng.standard_normal((4, 2))
+    grid = np.stack(np.meshgrid(*[np.arange(d) for d in dims[:3]], indexing="ij"), -1)
+    x = np.zeros(dims, complex)
+    for t in range(4):
+        f = rng.uniform(0, 2 * np.pi, 3)
+        f[2] = 2 * np.pi * rng.integers(0, 9) / 9  # periodic in time (the cine ring)
+        x += np.exp(1j * (grid @ f))[..., None] * base[t]
+    x += 0.01 * (rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+    mask = np.repeat((rng.random(dims[:3] + (1,)) < 0.5).astype(np.uint8), 2, axis=3)
+    x0 = np.where(mask == 1, x, 0)
+    sched = H.SolverSchedule(rank=10, stages=[H.StageSpec([8, 6, "full"], 2, 2, 1), H.StageSpec("full", 3, 2, 2)],
+                             circular_axes=(2,) if circular else (), seed=6)
+    return x0, mask, (3, 3, 5, 2), sched
+
+
+def _worker_t(rank, world, port, out_path, circular):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x0, mask, kext, sched = _problem_t(circular)
+    plan = plan_for(x0.shape, H.KernelMask.full(kext), sched, world, rank, axis=2)
+    b = CpuBackend(x0, mask, kext, sched, plan)
+    y, recs = ShardedReconstruction(b, plan, HaloExchange(plan)).run()
+    full = gather_planes(torch.from_numpy(y), plan).numpy()
+    if rank == 0:
+        np.savez(out_path, full=full, recs=np.concatenate(recs))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("circular", [False, True])
+def test_time_sharded_multi_neighbour_halo(tmp_path, circular):
+    """C4-style time sharding with shards thinner than the halo (world 4:
+    1-2 frames per rank against a 4-frame halo) and, circularly, a ring:
+    world 2 and 4 reproduce the single domain to 1e-9."""
+    outs = {}
+    for world in (1, 2, 4):
+        path = str(tmp_path / f"t{world}.npz")
+        mp.spawn(_worker_t, args=(world, _free_port(), path, circular), nprocs=world, join=True)
+        outs[world] = np.load(path)
+    a = outs[1]
+    for world in (2, 4):
+        b = outs[world]
+        assert np.allclose(a["recs"], b["recs"], rtol=1e-9, atol=1e-12), world
+        assert np.abs(a["full"] - b["full"]).max() <= 1e-9 * np.abs(a["full"]).max(), world
+    # the single-domain run is the oracle's algorithm (Gram+Nystrom, canonical phases)
+    x0, mask, kext, sched = _problem_t(circular)
+    xo, _ = O.hicu_reconstruct(x0, mask, kext, [(s.region, s.p, s.gradient_steps, s.iterations)
+                                                for s in sched.stages], sched.rank, seed=sched.seed,
+                               circular=sched.circular_axes, nullspace="nystrom", canonical=True)
+    xs = np.where(mask == 1, x0, a["full"])
     assert np.abs(xs - xo).max() <= 1e-9 * np.abs(xo).max()

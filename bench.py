@@ -35,8 +35,9 @@ A *step* is one pass of the hot path over the input:
 
 N > 1 (torchrun, NCCL): C5 one volume sharded along the readout axis with
 (K0-1)-plane halos, the Gram and the line-search scalars all-reduced (strong
-scaling); C3 the 64 slices partitioned over ranks (strong scaling); C1 / C2 /
-C4 replicas (weak scaling).
+scaling); C4 the series sharded along time with multi-neighbour halos and a
+distributed coil compression (strong scaling); C3 the 64 slices partitioned
+over ranks (strong scaling); C1 / C2 replicas (weak scaling).
 """
 
 from __future__ import annotations
@@ -100,6 +101,8 @@ WORKLOAD_TEXT = {
 def workload_config(name, world):
     spec = _spec(name)
     par = {"C5": f"readout-sharded volume over {world} GPU(s) (halo + NCCL all-reduce)" if world > 1 else "1 GPU",
+           "C4": f"time-sharded series over {world} GPU(s) (multi-neighbour halos + NCCL all-reduce)"
+           if world > 1 else "1 GPU",
            "C3": f"64 slices partitioned over {world} GPU(s), no collective"}.get(
         name, "replicas (one instance per GPU, no collective)" if world > 1 else "1 GPU")
     return {
@@ -368,21 +371,29 @@ class DeviceWorkload:
 
             self.slices = list(partition_slices(spec.slices, world, rank))
         else:
-            self.slices = [rank if world > 1 and name != "C5" else 0]
+            self.slices = [rank if world > 1 and name not in ("C4", "C5") else 0]
         self.host = {s: make_config(name, slice_index=s) for s in self.slices}
         nc, nv = spec.coils_in, spec.coils_out
         self.engines = []
         self.resets = []
-        if name == "C5" and world > 1:
-            from paper_2004_08962_b200.parallel import CudaShardBackend, HaloExchange, ShardedReconstruction, plan_for
+        if name in ("C4", "C5") and world > 1:
+            # one volume sharded over the ranks: readout (C5) or time (C4, with the
+            # distributed coil compression: covariance all-reduced, one basis)
+            from paper_2004_08962_b200.parallel import (CudaShardBackend, HaloExchange, ShardedReconstruction,
+                                                        plan_for, torch_view_real)
 
             ksp, mask, x0 = self.host[0]
-            plan = plan_for(x0.shape, self.kernel, self.sched, world, rank)
-            backend = CudaShardBackend(x0, mask, self.kernel, self.sched, plan)
-            self.sharded = ShardedReconstruction(backend, plan, HaloExchange(plan, group))
+            self.axis = 2 if name == "C4" else 0
+            cc = None if nv == nc else nv
+            dims = x0.shape[:-1] + (nv,)
+            plan = plan_for(dims, self.kernel, self.sched, world, rank, self.axis)
+            halo = HaloExchange(plan, group)
+            backend = CudaShardBackend(x0, mask, self.kernel, self.sched, plan, coil_compress=cc,
+                                       cov_reduce=lambda c: halo.allreduce_(torch_view_real(c)))
+            self.sharded = ShardedReconstruction(backend, plan, halo)
             self.engines = [backend.eng]
             self.resets = [(backend.eng.y, backend.eng.y.clone())]
-            self.dims = x0.shape
+            self.dims = dims
             return
         for s in self.slices:
             ksp, mask, x0 = self.host[s]
@@ -407,11 +418,17 @@ class DeviceWorkload:
         torch = self.torch
         spec = self.spec
         if self.sharded is not None:
-            it = self.it % spec.stages[0][3]
-            if it == 0:
-                self.resets[0][0].copy_(self.resets[0][1])
-            self.sharded.run_iteration(0, it)
-            self.it += 1
+            if self.name == "C5":
+                it = self.it % spec.stages[0][3]
+                if it == 0:
+                    self.resets[0][0].copy_(self.resets[0][1])
+                self.sharded.run_iteration(0, it)
+                self.it += 1
+                return
+            self.resets[0][0].copy_(self.resets[0][1])  # C4: one step = the whole schedule
+            for si, st in enumerate(spec.stages):
+                for it in range(st[3]):
+                    self.sharded.run_iteration(si, it)
             return
         if self.name == "C5":
             eng = self.engines[0]
@@ -469,7 +486,8 @@ class DeviceWorkload:
             from paper_2004_08962_b200.parallel import sharded_reconstruct
 
             ksp, mask, x0 = self.host[0]
-            xhat, _ = sharded_reconstruct(x0, mask, self.kernel, self.sched, group=group)
+            xhat, _ = sharded_reconstruct(x0, mask, self.kernel, self.sched, group=group, axis=self.axis,
+                                          coil_compress=cc)
             dt = time.perf_counter() - t
             return dt, spec.iterations, x0.nbytes // self.world + mask.nbytes // self.world, xhat.nbytes // self.world
         if self.name == "C3":
@@ -630,8 +648,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     per_rank_units = _step_iterations(name) if name != "C3" else dw.spec.iterations * len(dw.slices)
-    if name == "C5":
-        units = args.steps  # one volume: every rank works on the same iterations
+    if name in ("C4", "C5") and world > 1 or name == "C5":
+        units = per_rank_units * args.steps  # one volume: every rank works on the same iterations
     elif name == "C3":
         t = torch.tensor([per_rank_units * args.steps], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -661,7 +679,7 @@ def run_ours(args):
             ii = torch.tensor([its], dtype=torch.float64, device="cuda")
             if name in ("C3",):
                 dist.all_reduce(ii)
-            elif name != "C5":
+            elif name not in ("C4", "C5"):
                 ii *= world
             its = float(ii.item())
         e2e = {"value": its / tot, "unit": "iters/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
@@ -698,7 +716,7 @@ def run_ours(args):
         line = {
             "metric": "HICU iters/s", "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if (world > 1 and name in ("C5", "C3")) else "weak", "vs_baseline": None,
+            "scaling": "strong" if (world > 1 and name in ("C3", "C4", "C5")) else "weak", "vs_baseline": None,
             "dtype": "c64 (3xTF32 tcgen05 convs/Gram; fp64 reductions and nullspace)",
             "data": "synthetic (seeded phantoms with BASELINE.json shapes; paper_2004_08962_b200/synthetic.py)",
             "config": workload_config(name, world), "e2e": e2e, "gpu_launches": int(launches),

@@ -24,10 +24,15 @@ from .hankel import to_dev
 __all__ = ["coil_compress", "coil_compress_device"]
 
 
-def coil_compress_device(xd, maskd, nc: int, nv: int):
+def coil_compress_device(xd, maskd, nc: int, nv: int, cov_from=None, cov_reduce=None):
     """Device tensors in/out: xd (nloc*nc c64), maskd (nloc*nc u8).
     Returns (y (nloc*nv c64), mask_out (nloc*nv u8), basis (nc x nv c128),
-    evals (nc f64))."""
+    evals (nc f64)).
+
+    Sharded volumes: ``cov_from = (xd_owned, maskd_owned)`` restricts the
+    covariance to this rank's owned samples and ``cov_reduce(cov)`` sums it
+    over ranks in place, so every rank derives the same basis (the one the
+    whole volume gives) and compresses its local slab, halo included."""
     torch = nat.require_cuda()
     L = nat.lib()
     st = nat.stream_handle()
@@ -35,8 +40,15 @@ def coil_compress_device(xd, maskd, nc: int, nv: int):
     ws_bytes = max(int(L.hicu_coil_workspace(nloc, nc)), int(L.hicu_coil_basis_workspace(nc)))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
     cov = torch.empty((nc, nc), dtype=torch.complex128, device="cuda")
-    nat.check(L.hicu_coil_cov(nloc, nc, xd.data_ptr(), maskd.data_ptr(), cov.data_ptr(), ws.data_ptr(), ws_bytes,
+    cx, cm = cov_from if cov_from is not None else (xd, maskd)
+    ncov = cx.numel() // nc
+    if cov_from is not None:
+        ws_bytes = max(ws_bytes, int(L.hicu_coil_workspace(ncov, nc)))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    nat.check(L.hicu_coil_cov(ncov, nc, cx.data_ptr(), cm.data_ptr(), cov.data_ptr(), ws.data_ptr(), ws_bytes,
                               st), "coil_cov")
+    if cov_reduce is not None:
+        cov_reduce(cov)
     basis = torch.empty((nc, nv), dtype=torch.complex128, device="cuda")
     evals = torch.empty(nc, dtype=torch.float64, device="cuda")
     ws2 = torch.empty(int(L.hicu_coil_basis_workspace(nc)), dtype=torch.uint8, device="cuda")

@@ -353,7 +353,8 @@ def plan_for(dims, kernel, schedule, world: int, rank: int, axis: int = 0) -> Sh
 class CudaShardBackend:
     """Local compute of one shard on the current CUDA device through the C ABI."""
 
-    def __init__(self, x0, mask, kernel, schedule, plan: ShardPlan):
+    def __init__(self, x0, mask, kernel, schedule, plan: ShardPlan, coil_compress: int | None = None,
+                 cov_reduce=None):
         from . import _native as nat
         from .hankel import Region, device_geometry, to_dev
         from .solver import ReconEngine, draw_stage, stage_region
@@ -372,10 +373,27 @@ class CudaShardBackend:
         xm = np.take(np.where(observed, x0, 0).astype(np.complex64), planes, axis=ax)
         self.mask_np = np.take(observed.astype(np.uint8), planes, axis=ax)
         ldims = plan.local_dims
+        self.basis = None
+        if coil_compress is not None:
+            # distributed SVD coil compression: covariance of the owned planes,
+            # summed over ranks, one basis everywhere, applied to the local slab
+            from .coil import coil_compress_device
+
+            nc, nv = x0.shape[-1], int(coil_compress)
+            xd = to_dev(xm).reshape(-1)
+            md = to_dev(self.mask_np, np.uint8).reshape(-1)
+            own = [slice(None)] * xm.ndim
+            own[ax] = slice(0, plan.owned)
+            xo = to_dev(np.ascontiguousarray(xm[tuple(own)])).reshape(-1)
+            mo = to_dev(np.ascontiguousarray(self.mask_np[tuple(own)]), np.uint8).reshape(-1)
+            y, _, self.basis, _ = coil_compress_device(xd, md, nc, nv, cov_from=(xo, mo), cov_reduce=cov_reduce)
+            ldims = ldims[:-1] + (nv,)
+            xm = y.reshape(ldims).cpu().numpy()
+            self.mask_np = np.ascontiguousarray(self.mask_np[..., :nv])
         circ_local = tuple(a for a in schedule.circular_axes if int(a) % x0.ndim != ax)
         self.regions = []
         for st in schedule.stages:
-            rg = stage_region(x0.shape, kernel, st.region, schedule.circular_axes)
+            rg = stage_region(x0.shape[:-1] + (ldims[-1],), kernel, st.region, schedule.circular_axes)
             offs, exts = list(rg.offsets), list(rg.extents)
             offs[ax], exts[ax] = plan.local_roff0, plan.r1 - plan.r0
             self.regions.append(Region(tuple(offs), tuple(exts), frozenset(int(a) % x0.ndim for a in circ_local)))
@@ -510,18 +528,24 @@ def gather_planes(local_owned, plan: ShardPlan, group=None):
     return torch.cat(blocks, dim=ax)
 
 
-def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0):
+def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0, coil_compress: int | None = None):
     """Reconstruct one volume sharded along ``axis`` (C5: readout, 0; C4:
     time, 2) over the ranks of ``group`` (one GPU per rank).  Returns (xhat
     complex128 full volume, records of this rank's run: list per stage of
-    [iters*G, 8] arrays)."""
+    [iters*G, 8] arrays).  ``coil_compress=Nv``: distributed SVD coil
+    compression first (covariance all-reduced, one basis on every rank);
+    ``xhat`` is then in the compressed domain, as hicu_reconstruct's."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    plan = plan_for(np.asarray(x0).shape, kernel, schedule, world, rank, axis)
-    backend = CudaShardBackend(x0, mask, kernel, schedule, plan)
+    x0 = np.asarray(x0)
+    mask = np.asarray(mask)
+    dims = x0.shape if coil_compress is None else x0.shape[:-1] + (int(coil_compress),)
+    plan = plan_for(dims, kernel, schedule, world, rank, axis)
     halo = HaloExchange(plan, group)
+    backend = CudaShardBackend(x0, mask, kernel, schedule, plan, coil_compress=coil_compress,
+                               cov_reduce=lambda c: halo.allreduce_(torch_view_real(c)))
     y_owned, recs = ShardedReconstruction(backend, plan, halo).run()
     import torch
 
@@ -529,7 +553,11 @@ def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0):
     if not halo.host_staged:
         yt = yt.cuda()
     full = gather_planes(yt, plan, group).cpu().numpy()
-    obs = np.asarray(mask) == 1
-    if schedule.dc_mode == "hard":
+    if schedule.dc_mode == "hard" and coil_compress is None:
+        obs = mask == 1
         full[obs] = np.asarray(x0, np.complex128)[obs]
     return full, recs
+
+
+def torch_view_real(t):
+    return t.view(t.real.dtype) if t.is_complex() else t

@@ -624,7 +624,7 @@ int launch_conv(const DevGeom& g, const float2* y, const float2* qt, int p, floa
 int conv_dispatch(const hicu_geom* hg, const void* y, const void* qt, int p, const void* u_in, void* u_out,
                   double* parts, int mode, void* stream) {
   if (!hg || !y || !qt || !parts || p < 1) return hicu_set_error(HICU_ERR_PARAMETER, "conv: bad arguments");
-  if (p > 16) return hicu_set_error(HICU_ERR_PARAMETER, "conv: p > 16 not supported");
+  if (p > 32) return hicu_set_error(HICU_ERR_PARAMETER, "conv: p > 32 not supported");
   DevGeom g;
   int st = hicu_make_devgeom(hg, &g);
   if (st) return st;
@@ -638,12 +638,15 @@ int conv_dispatch(const hicu_geom* hg, const void* y, const void* qt, int p, con
     if (p <= 8) return conv_coil_dispatch<8>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
     // exact fit for C3's p = 10 (the 16-wide instantiation spent 60 % more FMAs on zero columns)
     if (p <= 10) return conv_coil_dispatch<10>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
-    return conv_coil_dispatch<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+    if (p <= 16) return conv_coil_dispatch<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+    // the paper's full-stage compression p = 4 Nc: 32 columns for 8 coils
+    return conv_coil_dispatch<32>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
   }
   if (p <= 4) return launch_conv<4>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
   if (p <= 8) return launch_conv<8>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
   if (p <= 10) return launch_conv<10>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
-  return launch_conv<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+  if (p <= 16) return launch_conv<16>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
+  return launch_conv<32>(g, (const float2*)y, (const float2*)qt, p, u, parts, mode, s);
 }
 
 template <int PMAX>
@@ -701,7 +704,7 @@ extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const
                                double* dc_parts, void* stream) {
   if (!hg || !qt || !u || (!mask && dc_mode != 2) || !gout || !dc_parts || p < 1)
     return hicu_set_error(HICU_ERR_PARAMETER, "scatter: bad arguments");
-  if (p > 16) return hicu_set_error(HICU_ERR_PARAMETER, "scatter: p > 16 not supported");
+  if (p > 32) return hicu_set_error(HICU_ERR_PARAMETER, "scatter: p > 32 not supported");
   if (dc_mode < 0 || dc_mode > 2) return hicu_set_error(HICU_ERR_SHAPE, "scatter: unknown dc mode");
   if (dc_mode == 1 && (!y || !x0)) return hicu_set_error(HICU_ERR_SHAPE, "soft data consistency requires x0");
   DevGeom g;
@@ -719,7 +722,8 @@ extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const
     if (p <= 4) return scatter_coil_dispatch<4>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
     if (p <= 8) return scatter_coil_dispatch<8>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
     if (p <= 10) return scatter_coil_dispatch<10>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
-    return scatter_coil_dispatch<16>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
+    if (p <= 16) return scatter_coil_dispatch<16>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
+    return scatter_coil_dispatch<32>(g, q, p, uu, mask, yy, xx, dc_mode, (float)lam, (float2*)gout, dc_parts, s);
   }
   if (p <= 4)
     return launch_scatter<4>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
@@ -727,7 +731,10 @@ extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const
   if (p <= 8)
     return launch_scatter<8>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
                              (float2*)gout, dc_parts, s);
-  return launch_scatter<16>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
+  if (p <= 16)
+    return launch_scatter<16>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
+                              (float2*)gout, dc_parts, s);
+  return launch_scatter<32>(g, q, p, uu, mask, (const float2*)y, (const float2*)x0, dc_mode, (float)lam,
                             (float2*)gout, dc_parts, s);
 }
 

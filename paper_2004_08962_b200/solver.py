@@ -65,8 +65,8 @@ class StageSpec:
             raise ConfigError("gradient_steps must be >= 1")
         if self.iterations < 1:
             raise ConfigError("iterations must be >= 1")
-        if self.p > 16:
-            raise ConfigError("p must be <= 16 on the B200 path")
+        if self.p > 32:
+            raise ConfigError("p must be <= 32 on the B200 path")
 
 
 @dataclass

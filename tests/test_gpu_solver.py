@@ -442,3 +442,30 @@ def test_sharded_time_axis_coil_compression():
     err = np.abs(xs - xr).max() / np.abs(xr).max()
     print(f"sharded time axis + coil compression vs single domain: {err:.2e}")
     assert err <= 1e-5
+
+
+def test_p32_stage_lockstep():
+    """The paper's full-stage compression p = 4 Nc = 32 (the
+    reference accepts any p >= 1, subspace.py:223-224): lockstep against the
+    oracle with its V injected, 8 coils, 5x5x8 kernel."""
+    rng = np.random.default_rng(12)
+    dims = (28, 26, 8)
+    img = np.zeros(dims[:2], complex)
+    yy, xx = np.mgrid[:dims[0], :dims[1]] / dims[0] - 0.5
+    img[(xx / 0.35) ** 2 + (yy / 0.3) ** 2 <= 1] = 1.0
+    sens = np.stack([np.exp(2j * np.pi * (0.3 * k * xx - 0.2 * (k - 3) * yy)) for k in range(8)], -1)
+    ksp = np.fft.fftshift(np.fft.fft2(np.fft.ifftshift(img[..., None] * sens, axes=(0, 1)), axes=(0, 1),
+                                      norm="ortho"), axes=(0, 1))
+    ksp = ksp + 1e-3 * np.abs(ksp).max() * (rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+    mask = np.repeat((rng.random(dims[:2] + (1,)) < 0.5).astype(np.uint8), 8, axis=2)
+    x0 = np.where(mask == 1, ksp, 0)
+    stages = [("full", 32, 3, 2)]
+    vlog, trace = {}, []
+    xo, _ = O.hicu_reconstruct(x0, mask, (5, 5, 8), stages, 30, seed=1, trace=trace, v_log=vlog)
+    sched = H.SolverSchedule(rank=30, stages=[H.StageSpec(*s) for s in stages], seed=1)
+    xg, rep = H.hicu_reconstruct(x0, mask, H.KernelMask.full((5, 5, 8)), sched, tail_energy_threshold=0,
+                                 lockstep_v=lambda si, it: vlog[(si, it)])
+    eo = np.array([t["eta"] for t in trace])
+    eg = np.array([s.eta for s in rep.steps])
+    assert np.abs(eg - eo).max() <= 1e-4 * np.abs(eo).max()
+    assert np.linalg.norm(xg - xo) <= 1e-5 * np.linalg.norm(xo)

@@ -510,26 +510,34 @@ class DeviceWorkload:
 
 def _work_per_step(dw):
     """Algorithmic work of the kernel classes in one step: real
-    flops per class, update bytes."""
+    flops per class, update bytes; ``gram_path`` is the Gram the library ran
+    ("lag": fp32 lag correlations, whose executed flops are counted, and the
+    dense-equivalent 4 s n (n+1) is reported beside them)."""
+    from paper_2004_08962_b200 import _native as nat
+
     spec = dw.spec
     n = dw.kernel.n
     dims = dw.dims if dw.sharded is None else dw.sharded.b.ldims
     regions = dw.engines[0].regions
+    geoms = dw.engines[0].geoms
     N = int(np.prod(dims))
-    tot = {"gram": 0.0, "conv_fwd": 0.0, "scatter": 0.0, "conv_els": 0.0, "update_bytes": 0.0}
-    launches = {k: 0 for k in tot}
-    for st, reg in zip(spec.stages, regions):
+    tot = {"gram": 0.0, "gram_dense_equiv": 0.0, "conv_fwd": 0.0, "scatter": 0.0, "conv_els": 0.0,
+           "update_bytes": 0.0}
+    paths = set()
+    for st, reg, gm in zip(spec.stages, regions, geoms):
         s, p, G = reg.s, st[1], st[2]
         iters = 1 if dw.name == "C5" else st[3]
-        tot["gram"] += 4.0 * s * n * (n + 1) * iters
-        launches["gram"] += iters
+        path = nat.GRAM_PATHS[int(nat.lib().hicu_gram_path(gm.ref()))]
+        paths.add(path)
+        tot["gram"] += float(nat.lib().hicu_gram_flops(gm.ref())) * iters
+        tot["gram_dense_equiv"] += 4.0 * s * n * (n + 1) * iters
         for k in ("conv_fwd", "scatter", "conv_els"):
             tot[k] += 8.0 * s * n * p * G * iters
-            launches[k] += G * iters
         tot["update_bytes"] += 25.0 * N * G * iters
-        launches["update_bytes"] += G * iters
     mult = len(dw.engines)
-    return {k: v * mult for k, v in tot.items()}, {k: v * mult for k, v in launches.items()}
+    out = {k: v * mult for k, v in tot.items()}
+    out["gram_path"] = "/".join(sorted(paths))
+    return out
 
 
 def _load_json(path, default=None):
@@ -539,12 +547,14 @@ def _load_json(path, default=None):
         return default
 
 
-def roofline(kinds, work, peaks):
+def roofline(kinds, work, peaks, sm_mhz=None):
     tf32 = _load_json("profiles/tf32_peak_r01.json", {"tf32_tflops": 749.4})
     tf32_peak = tf32["tf32_tflops"] / 3.0
     hbm = peaks.get("hbm_gbs", 6548.2)
+    # CUDA-core fp32 peak (FFMA2: 148 SMs x 128 lanes x 2 flop at the max SM clock)
+    fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
     ncu = {rec["kernel"]: rec for rec in _load_json("profiles/r02_ncu_full.json", [])}
-    ncu_name = {"gram": "gram", "conv_fwd": "conv_tc_kernel<0", "scatter": "conv_tc_kernel<2",
+    ncu_name = {"gram": "lag_core_kernel", "conv_fwd": "conv_tc_kernel<0", "scatter": "conv_tc_kernel<2",
                 "conv_els": "conv_tc_kernel<1", "update": "update_kernel"}
 
     def traffic(kind):
@@ -560,6 +570,13 @@ def roofline(kinds, work, peaks):
             continue
         nl = max(1, kinds[k]["launches"])
         ach = work[k] / (ms_by[k] * 1e-3) / 1e12
+        if k == "gram" and work.get("gram_path") == "lag":
+            roof_all[k] = {"bound": "fp32 (CUDA-core FFMA2)", "achieved": ach, "peak": fp32_peak, "unit": "TFLOP/s",
+                           "frac": ach / fp32_peak, "traffic": traffic(k), "launches": nl,
+                           "avg_launch_ms": ms_by[k] / nl, "flops_per_launch_avg": work[k] / nl,
+                           "path": "lag Gram (gram_lag.cu): executed fp32 flops of the lag correlations",
+                           "dense_equivalent_tflops": work["gram_dense_equiv"] / (ms_by[k] * 1e-3) / 1e12}
+            continue
         roof_all[k] = {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                        "frac": ach / tf32_peak, "traffic": traffic(k), "launches": nl,
                        "avg_launch_ms": ms_by[k] / nl, "flops_per_launch_avg": work[k] / nl}
@@ -575,11 +592,14 @@ def roofline(kinds, work, peaks):
     dom = max(tens, key=lambda k: ms_by[k]) if tens else None
     roof = dict(roof_all[dom]) if dom else None
     if roof:
+        top = max((k for k in roof_all if k in ms_by), key=lambda k: ms_by[k])
         roof.update({"kernel": dom,
                      "peak_source": "measured TF32 dense (profiles/tf32_peak_r01.json) / 3 for 3xTF32",
                      "achieved_def": "algorithmic flops of the class in one step / its summed CUDA-event time "
                                      "(native profiler, one extra step on the launching stream)",
-                     "traffic_def": "ncu dram read+write bytes per launch (profiles/r02_ncu_full.json)"})
+                     "traffic_def": "ncu dram read+write bytes per launch (profiles/r02_ncu_full.json)",
+                     "note": ("the dominant tensor-core class; the largest class overall is "
+                              f"{top} ({roof_all[top]['bound']})") if top != dom else "the largest class"})
     return roof, roof_all
 
 
@@ -689,7 +709,7 @@ def run_ours(args):
                + " from host numpy arrays (complex64 k-space, uint8 mask), result downloaded"}
 
     roof, roof_all, share, ms_by = None, None, None, None
-    work, nlaunch = _work_per_step(dw)
+    work = _work_per_step(dw)
     peaks = _load_json("MEASURED_PEAKS.json", {})
     if kinds is not None:
         roof, roof_all = roofline(kinds, work, peaks)
@@ -698,7 +718,8 @@ def run_ours(args):
         share = {k: (v / tot_ms if tot_ms > 0 else 0.0) for k, v in ms_by.items()}
     eff = None
     if world == 1:
-        flops = sum(work[k] for k in ("gram", "conv_fwd", "scatter", "conv_els"))
+        # dense-equivalent algorithmic flops (SURVEY 8d's F_iter) per second of the whole step
+        flops = work["gram_dense_equiv"] + sum(work[k] for k in ("conv_fwd", "scatter", "conv_els"))
         eff = flops / (total_ms / args.steps * 1e-3) / 1e12
 
     # ---- CPU baseline: the reference package on a bounded sample, rank 0, N=1 ----

@@ -186,6 +186,9 @@ int hicu_gram_uses_tensor_cores(const hicu_geom* g);
  * n < 400 (measured faster at the 5x5x8 kernels of C1/C2) unless
  * HICU_GEOM_FORCE_LAG_GRAM; -1 on a bad geometry. */
 int hicu_gram_path(const hicu_geom* g);
+/* Real flops hicu_gram executes for this geometry on its path (lag: the
+ * fp32 lag-correlation products; dense: 4 s n (n+1)); -1 on a bad geometry. */
+double hicu_gram_flops(const hicu_geom* g);
 /* 1 when hicu_conv_fwd / hicu_conv_els / hicu_scatter_dc with p columns run
  * on the tcgen05 kernels (conv_tc.cu) for this geometry. */
 int hicu_conv_uses_tensor_cores(const hicu_geom* g, int p);

@@ -89,6 +89,7 @@ _SIGS = {
     "hicu_gram_workspace": (c_size_t, [_GP]),
     "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
     "hicu_gram_path": (c_int, [_GP]),
+    "hicu_gram_flops": (c_double, [_GP]),
     "hicu_conv_uses_tensor_cores": (c_int, [_GP, c_int]),
     "hicu_gram": (c_int, [_GP, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hicu_zgemm": (c_int, [c_char, c_char, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_int,

@@ -189,6 +189,13 @@ extern "C" int hicu_gram_path(const hicu_geom* hg) {
   return gram_path(hg, g);
 }
 
+extern "C" double hicu_gram_flops(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return -1.0;
+  if (gram_path(hg, g) == HICU_GRAM_PATH_LAG) return hicu_gram_lag_flops(g);
+  return 4.0 * (double)g.s * g.n * (g.n + 1);  // dense Hermitian H^H H
+}
+
 extern "C" int hicu_gram_uses_tensor_cores(const hicu_geom* hg) {
   return hicu_gram_path(hg) == HICU_GRAM_PATH_TCGEN05 ? 1 : 0;
 }

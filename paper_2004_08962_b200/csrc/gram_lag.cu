@@ -662,6 +662,39 @@ bool hicu_gram_lag_supported(const DevGeom& g) {
   return make_plan(g).ok;
 }
 
+// fp32 flops the lag kernels execute (8 per complex MAC: core + edge
+// products of the lines whose neighbour block is in range)
+double hicu_gram_lag_flops(const DevGeom& g) {
+  LagPlan pl = make_plan(g);
+  if (!pl.ok) return 0.0;
+  const LagParams& P = pl.p;
+  const int la = P.L - 1;
+  double lines_pos = 0.0;
+  for (int ol = 0; ol < P.nol; ++ol)
+    for (int b = 0; b < P.NB; ++b) {
+      int r = b, ok = 1;
+      double nl = 1.0;
+      for (int a = la - 1; a >= 0; --a) {
+        const int k = r % P.ncls[a];
+        r /= P.ncls[a];
+        const int beg = P.cls_beg[a][k], len = P.cls_end[a][k] - P.cls_beg[a][k];
+        const int d = P.ol_d[ol][a];
+        if (!P.circ[a] && (beg + d < 0 || beg + len - 1 + d >= P.N[a])) ok = 0;
+        nl *= len;
+      }
+      if (!ok) continue;
+      double pos = P.core_cls >= 0 ? (double)P.P * P.DZ : 0.0;
+      for (int e = 0; e < P.NE; ++e) {
+        const int c = P.edge_cls[e];
+        for (int pz = P.cls_beg[la][c]; pz < P.cls_end[la][c]; ++pz)
+          for (int dz = -(P.K[la] - 1); dz <= P.K[la] - 1; ++dz)
+            if (pz + dz >= 0 && pz + dz < P.N[la]) pos += 1.0;
+      }
+      lines_pos += nl * pos;
+    }
+  return lines_pos * P.NC * P.NC * 8.0;
+}
+
 size_t hicu_gram_lag_workspace(const DevGeom& g) {
   LagPlan pl = make_plan(g);
   return pl.ok ? pl.bytes : 0;

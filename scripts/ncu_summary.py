@@ -58,7 +58,9 @@ def main(paths, out=None, json_out=None):
                        "dram_read_bytes": raw.get("dram__bytes_read.sum"),
                        "dram_write_bytes": raw.get("dram__bytes_write.sum"),
                        "tensor_pipe_pct": raw.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
-                       "fp64_pipe_pct": raw.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")})
+                       "fp64_pipe_pct": raw.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                       "fma_pipe_pct": raw.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                       "sm_throughput_pct": raw.get("sm__throughput.avg.pct_of_peak_sustained_elapsed")})
     txt = "\n".join(lines)
     if out:
         open(out, "w").write(txt + "\n")

@@ -47,6 +47,8 @@ constexpr int kLinesPerChunkB = 1024;
 
 struct LagParams {
   int L;           // spatial axes
+  int perm[kMaxL]; // plan axis a is geometry axis perm[a]; the last plan axis (the "line" axis) is the
+                   // spatial axis with the longest core class, so lines are long whatever the layout
   int NC, CB, NCB; // coils, coil rows per warp block, NC / CB
   int64_t N[kMaxL];
   int64_t cstride[kMaxL];  // element (complex) stride of each spatial axis
@@ -157,15 +159,34 @@ LagPlan make_plan(const DevGeom& g) {
     if (g.circ_axes[c] >= L) return pl;
     circ[g.circ_axes[c]] = true;
   }
+  // line axis: the spatial axis with the longest core class (positions of
+  // interest minus the 2(K-1) edge positions; the whole axis when circular)
+  int line = L - 1;
+  int64_t best = -1;
+  for (int a = L - 1; a >= 0; --a) {
+    const int64_t K = g.kext[a];
+    const int64_t core = circ[a] ? g.dims[a] : g.rext[a] - K + 1;
+    if (core > best) {
+      best = core;
+      line = a;
+    }
+  }
+  {
+    int k = 0;
+    for (int a = 0; a < L; ++a)
+      if (a != line) p.perm[k++] = a;
+    p.perm[L - 1] = line;
+  }
   for (int a = 0; a < L; ++a) {
-    const int K = (int)g.kext[a];
+    const int ga = p.perm[a];
+    const int K = (int)g.kext[ga];
     if (K < 1 || K > kMaxK) return pl;
-    p.N[a] = g.dims[a];
-    p.cstride[a] = g.stride[a];
+    p.N[a] = g.dims[ga];
+    p.cstride[a] = g.stride[ga];
     p.K[a] = K;
-    p.circ[a] = circ[a] ? 1 : 0;
-    if (circ[a] && K > g.dims[a]) return pl;
-    axis_classes(g.dims[a], g.roff[a], g.rext[a], K, circ[a], p, a);
+    p.circ[a] = circ[ga] ? 1 : 0;
+    if (circ[ga] && K > g.dims[ga]) return pl;
+    axis_classes(g.dims[ga], g.roff[ga], g.rext[ga], K, circ[ga], p, a);
     if (p.ncls[a] < 1) return pl;
   }
   // outer blocks and lags
@@ -354,6 +375,7 @@ lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
   const int nwa = pn + gz_n - 1;              // neighbour rows the active lags read
   const size_t bufsz = (size_t)(pn + nw) * RB;
   const int64_t NL = P.N[la];
+  const int64_t ls = P.cstride[la];  // element stride along the line axis
   auto stage = [&](int64_t li, int buf) {
     int64_t base, nbr;
     line_offsets(P, beg, len, ol, li, base, nbr);
@@ -363,7 +385,7 @@ lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
       constexpr int H = NC / 2;  // 16-byte chunks per position
       for (int e = threadIdx.x; e < pn * H; e += blockDim.x) {
         const int j = e / H, k = e % H;
-        cp_async16(sb + j * RB + k * 16, x + base + (P.c0 + j) * NC + 2 * k);
+        cp_async16(sb + j * RB + k * 16, x + base + (P.c0 + j) * ls + 2 * k);
       }
       for (int e = threadIdx.x; e < nwa * H; e += blockDim.x) {
         const int j = e / H, k = e % H;
@@ -372,12 +394,12 @@ lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
           q %= NL;
           if (q < 0) q += NL;
         }
-        cp_async16(sn + j * RB + k * 16, x + nbr + q * NC + 2 * k);
+        cp_async16(sn + j * RB + k * 16, x + nbr + q * ls + 2 * k);
       }
     } else {
       for (int e = threadIdx.x; e < pn * NC; e += blockDim.x) {
         const int j = e / NC, c = e % NC;
-        cp_async8(sb + j * RB + c * 8, x + base + (P.c0 + j) * NC + c);
+        cp_async8(sb + j * RB + c * 8, x + base + (P.c0 + j) * ls + c);
       }
       for (int e = threadIdx.x; e < nwa * NC; e += blockDim.x) {
         const int j = e / NC, c = e % NC;
@@ -386,7 +408,7 @@ lag_core_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
           q %= NL;
           if (q < 0) q += NL;
         }
-        cp_async8(sn + j * RB + c * 8, x + nbr + q * NC + c);
+        cp_async8(sn + j * RB + c * 8, x + nbr + q * ls + c);
       }
     }
   };
@@ -597,8 +619,8 @@ __global__ void lag_assemble_kernel(const __grid_constant__ LagParams P, const d
     const int i = (int)(idx / n), j = (int)(idx % n);
     int ti[kMaxL], tj[kMaxL];
     for (int a = 0; a < L; ++a) {
-      ti[a] = pos[(size_t)i * ndim + a];
-      tj[a] = pos[(size_t)j * ndim + a];
+      ti[a] = pos[(size_t)i * ndim + P.perm[a]];
+      tj[a] = pos[(size_t)j * ndim + P.perm[a]];
     }
     int ci = pos[(size_t)i * ndim + L], cj = pos[(size_t)j * ndim + L];
     int sgn = 0;

@@ -46,6 +46,7 @@
 #include <cuda.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <atomic>
 
 #include "common.cuh"
@@ -89,6 +90,8 @@ struct CtParams {
   int debug;              // experiment bits (HICU_CONV_TC_DEBUG): 1 no MMA, 2 no TMA, 4 no convert
   const uint8_t* bimg;    // prebuilt B images (resident mode) or null: one bulk copy replaces the build
   int bimg_early;         // 1: bimg was written >= 2 kernels earlier, copy it before the grid-dependency wait
+  int perm[3];            // kernel spatial axis k is geometry axis perm[k]; k = L-1 is the tile ("line") axis
+  int64_t lstride;        // output stride (rows / positions) along the line axis
 };
 
 __device__ __forceinline__ void decode_line(const CtParams& P, int line, int (&lc)[2]) {
@@ -273,7 +276,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   // ---- prologue part 1 (before the grid-dependency wait): only static data
   // (support positions, barrier/TMEM setup), overlapping the previous kernel ----
   for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
-    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + t % L);
+    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + P.perm[t % L]);
   if (threadIdx.x < ng) {
     const int g = threadIdx.x;
     ga[g][0] = L == 2 ? g : (L == 3 ? g / P.kpre[1] : 0);
@@ -576,7 +579,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
           if (MODE < 2) {
             const int i_out = c * kTileM - (nb - 1) + m;
             if (i_out < 0 || i_out >= P.ext_last) continue;
-            const int64_t idx = obase + i_out;
+            const int64_t idx = obase + (int64_t)i_out * P.lstride;
             if (MODE == 0) {
               float4* up = reinterpret_cast<float4*>(out + (size_t)idx * 8 + 4 * h);
               if (!tr) {  // trace mode keeps `out` for the milestones
@@ -611,7 +614,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
             const int x = P.roff[L - 1] + c * kTileM + m;
             if (x >= P.ext_last) continue;
             double a4[4] = {0, 0, 0, 0};
-            scatter_store(P, (size_t)(obase + x) * 8, h, v, mask, y, x0, out, a4);
+            scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, v, mask, y, x0, out, a4);
 #pragma unroll
             for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
           }
@@ -625,7 +628,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
         for (int x = m; x < P.ext_last; x += kTileM) {
           if (x >= x_lo && x < x_hi) continue;
           double a4[4] = {0, 0, 0, 0};
-          scatter_store(P, (size_t)(obase + x) * 8, h, vz, mask, y, x0, out, a4);
+          scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, vz, mask, y, x0, out, a4);
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
         }
@@ -678,7 +681,7 @@ __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P,
   uint8_t* img = img_all + (size_t)(2 * blockIdx.x + img_off) * img_stride;
   const float2* qt = qt_all + (size_t)blockIdx.x * qt_stride;
   for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
-    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + t % L);
+    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + P.perm[t % L]);
   float4* z = reinterpret_cast<float4*>(img);
   for (int i = threadIdx.x; i < P.ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int nq = P.nsp * 64;
@@ -709,14 +712,23 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// 4-D map over a [.., rows, 16 floats] array: dims (16, ext[L-1], ext[L-2], ext[L-3]),
-// 64-row x 16-float boxes, SWIZZLE_64B, zero fill out of bounds.
-int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext) {
+// 4-D map over a row-major [ext[0], .., ext[L-1], 16 floats] array seen in
+// the kernel's axis order: dims (16, ext[perm[L-1]], ext[perm[L-2]],
+// ext[perm[L-3]]) with the array's own strides (any spatial axis can be the
+// tile axis), 64-row x 16-float boxes, SWIZZLE_64B, zero fill out of bounds.
+int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[4] = {16, (cuuint64_t)ext[L - 1], (cuuint64_t)(L >= 2 ? ext[L - 2] : 1),
-                        (cuuint64_t)(L >= 3 ? ext[L - 3] : 1)};
-  cuuint64_t strides[3] = {64, 64 * dims[1], 64 * dims[1] * dims[2]};
+  uint64_t astride[3] = {0, 0, 0};  // byte stride of geometry axis a
+  uint64_t st = 64;
+  for (int a = L - 1; a >= 0; --a) {
+    astride[a] = st;
+    st *= (uint64_t)ext[a];
+  }
+  cuuint64_t dims[4] = {16, (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
+                        (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
+  cuuint64_t strides[3] = {astride[perm[L - 1]], L >= 2 ? astride[perm[L - 2]] : 64 * dims[1],
+                           L >= 3 ? astride[perm[L - 3]] : 64 * dims[1] * dims[2]};
   cuuint32_t box[4] = {16, 64, 1, 1}, es[4] = {1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -725,35 +737,74 @@ int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext) {
   return HICU_OK;
 }
 
-// Tensor maps depend only on (pointer, extents): a small per-thread cache
-// keeps cuTensorMapEncodeTiled off the per-launch path of the stage driver.
-int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext) {
+// Tensor maps depend only on (pointer, extents, axis order): a small
+// per-thread cache keeps cuTensorMapEncodeTiled off the per-launch path.
+int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm) {
   struct Entry {
     const void* base;
     int L;
     int64_t ext[3];
+    int perm[3];
     CUtensorMap map;
   };
   static thread_local Entry cache[16];
   static thread_local int used = 0, next = 0;
   for (int i = 0; i < used; ++i) {
     const Entry& e = cache[i];
-    if (e.base == base && e.L == L && e.ext[0] == ext[0] && (L < 2 || e.ext[1] == ext[1]) &&
-        (L < 3 || e.ext[2] == ext[2])) {
+    bool same = e.base == base && e.L == L;
+    for (int d = 0; d < L && same; ++d) same = e.ext[d] == ext[d] && e.perm[d] == perm[d];
+    if (same) {
       *tm = e.map;
       return HICU_OK;
     }
   }
-  const int st = make_tmap(tm, base, L, ext);
+  const int st = make_tmap(tm, base, L, ext, perm);
   if (st) return st;
   Entry& e = cache[next];
   e.base = base;
   e.L = L;
-  for (int d = 0; d < 3; ++d) e.ext[d] = d < L ? ext[d] : 0;
+  for (int d = 0; d < 3; ++d) {
+    e.ext[d] = d < L ? ext[d] : 0;
+    e.perm[d] = d < L ? perm[d] : 0;
+  }
   e.map = *tm;
   next = (next + 1) % 16;
   if (used < 16) ++used;
   return HICU_OK;
+}
+
+// Tile ("line") axis: the spatial axis that minimises the 128-row tiles the
+// kernel walks, lines x ceil((extent + nb - 1) / 128): a k-space volume
+// whose last axis is short (C4: 25 frames -> one 20 %-full tile per line) is
+// tiled along a long axis instead (C4: x; C5: readout, 252 + 4 = 256 rows =
+// two full tiles instead of 160-row lines in two tiles).
+void choose_perm(const DevGeom& g, int MODE, int (&perm)[3]) {
+  const int L = g.ndim - 1;
+  const int64_t* lext = MODE < 2 ? g.rext : g.dims;
+  int best = L - 1;
+  double best_tiles = 1e300;
+  for (int a = L - 1; a >= 0; --a) {
+    // the original last axis, or any axis with >= 2 taps (a 1-tap tile axis would
+    // chain every tap's MMA into one TMEM accumulator: fp32 rounding grows)
+    if (g.kext[a] > kMaxNb || (a != L - 1 && g.kext[a] < 2)) continue;
+    int64_t ng = 1;
+    for (int b = 0; b < L; ++b)
+      if (b != a) ng *= g.kext[b];
+    if (ng > kMaxGroups) continue;
+    double lines = 1.0;
+    for (int b = 0; b < L; ++b)
+      if (b != a) lines *= (double)lext[b];
+    const double tiles = lines * (double)((g.rext[a] + g.kext[a] - 1 + kTileM - 1) / kTileM);
+    if (tiles < best_tiles) {
+      best_tiles = tiles;
+      best = a;
+    }
+  }
+  int k = 0;
+  for (int a = 0; a < L; ++a)
+    if (a != best) perm[k++] = a;
+  perm[L - 1] = best;
+  for (int d = L; d < 3; ++d) perm[d] = d;
 }
 
 struct Shape {
@@ -763,21 +814,21 @@ struct Shape {
   size_t fixed;      // resident B images + window + alignment slack
 };
 
-bool shape_of(const DevGeom& g, int p, Shape* sh) {
+bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
   const int L = g.ndim - 1;
   if (g.nc != 8 || p != 8 || g.ncirc != 0 || L < 1 || L > 3 || g.nsp < 1 || g.nsp > kMaxTaps) return false;
   if (g.kext[L] != 8) return false;
   int ng = 1;
   for (int d = 0; d < L; ++d)
     if (g.kext[d] < 1) return false;
-  for (int d = 0; d < L - 1; ++d) ng *= (int)g.kext[d];
-  const int nb = (int)g.kext[L - 1];
+  for (int d = 0; d < L - 1; ++d) ng *= (int)g.kext[perm[d]];
+  const int nb = (int)g.kext[perm[L - 1]];
   if (nb > kMaxNb || ng > kMaxGroups) return false;
   sh->L = L;
   sh->nb = nb;
   sh->ng = ng;
-  sh->kpre[0] = L >= 2 ? (int)g.kext[0] : 1;
-  sh->kpre[1] = L >= 3 ? (int)g.kext[1] : 1;
+  sh->kpre[0] = L >= 2 ? (int)g.kext[perm[0]] : 1;
+  sh->kpre[1] = L >= 3 ? (int)g.kext[perm[1]] : 1;
   const size_t win = (((size_t)(kTileM + nb - 1) * (nb * 64 + 16)) + 1023) & ~(size_t)1023;
   // resident B images when they fit next to >= 3 stages, else one group's image per stage
   const size_t res_fixed = (size_t)ng * nb * 2048 + win + 1024;
@@ -837,10 +888,14 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   const uint8_t* bimg = t_bimg;
   const int bimg_early = t_bimg_early;
   t_bimg = nullptr;
+  int perm[3];
+  choose_perm(g, MODE, perm);
   Shape sh;
-  if (!shape_of(g, 8, &sh)) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: geometry outside the tensor-core scope");
+  if (!shape_of(g, 8, &sh, perm))
+    return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: geometry outside the tensor-core scope");
   const int L = sh.L;
   CtParams P{};
+  for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
   P.L = L;
   P.nsp = g.nsp;
   P.ndim = g.ndim;
@@ -868,27 +923,34 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
     P.debug = dbg;
   }
   for (int d = 0; d < L; ++d) {
-    P.roff[d] = (int)g.roff[d];
-    P.rext[d] = (int)g.rext[d];
+    P.roff[d] = (int)g.roff[perm[d]];
+    P.rext[d] = (int)g.rext[perm[d]];
   }
-  const int64_t* lext = MODE < 2 ? g.rext : g.dims;  // lines run over the region (conv) or k-space (scatter)
-  P.ext_last = (int)lext[L - 1];
-  P.chunks = (int)((g.rext[L - 1] + sh.nb - 1 + kTileM - 1) / kTileM);
+  // lines run over the region (conv) or k-space (scatter); output strides in
+  // rows of u (region-major, geometry axis order) or k-space positions
+  const int64_t* lext = MODE < 2 ? g.rext : g.dims;
+  int64_t ostr[3] = {1, 1, 1};
+  {
+    int64_t st = 1;
+    for (int a = L - 1; a >= 0; --a) {
+      ostr[a] = st;
+      st *= lext[a];
+    }
+  }
+  P.ext_last = (int)lext[perm[L - 1]];
+  P.chunks = (int)((g.rext[perm[L - 1]] + sh.nb - 1 + kTileM - 1) / kTileM);
+  P.lstride = ostr[perm[L - 1]];
   int64_t lines = 1;
   for (int d = 0; d < L - 1; ++d) {
-    P.ldim[d] = (int)lext[d];
-    lines *= lext[d];
-  }
-  int64_t str = lext[L - 1];
-  for (int d = L - 2; d >= 0; --d) {
-    P.ostride[d] = str;
-    str *= lext[d];
+    P.ldim[d] = (int)lext[perm[d]];
+    P.ostride[d] = ostr[perm[d]];
+    lines *= lext[perm[d]];
   }
   if (lines > (int64_t)1 << 30) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: too many lines");
   P.nlines = (int)lines;
   // TMA source: k-space array (conv, extents dims) or u (scatter, extents rext).
   CUtensorMap tm;
-  int s = cached_tmap(&tm, tsrc, L, MODE < 2 ? g.dims : g.rext);
+  int s = cached_tmap(&tm, tsrc, L, MODE < 2 ? g.dims : g.rext, perm);
   if (s) return s;
   P.stage_bytes = (int)sh.stage;
   P.bimg = bimg;
@@ -902,34 +964,50 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
 
 bool hicu_conv_tc_supported(const DevGeom& g, int p) {
   Shape sh;
-  return shape_of(g, p, &sh);
+  int p0[3], p2[3];
+  choose_perm(g, 0, p0);
+  choose_perm(g, 2, p2);
+  return shape_of(g, p, &sh, p0) && shape_of(g, p, &sh, p2);
 }
 
 size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p) {
   Shape sh;
-  if (!shape_of(g, p, &sh)) return 0;
-  return (size_t)sh.ng * sh.nb * 2048;
+  int p0[3], p2[3];
+  choose_perm(g, 0, p0);
+  choose_perm(g, 2, p2);
+  if (!shape_of(g, p, &sh, p0)) return 0;
+  Shape sh2;
+  if (!shape_of(g, p, &sh2, p2)) return 0;
+  return (size_t)std::max(sh.ng * sh.nb, sh2.ng * sh2.nb) * 2048;
 }
 
 // images for steps j < G: (j, conv/ELS layout) at img + 2j * ib, (j, scatter) at img + (2j+1) * ib
 int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, int G, uint8_t* img, size_t ib,
                                cudaStream_t st) {
-  Shape sh;
-  if (!shape_of(g, p, &sh)) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: no B image");
-  CtParams P{};
-  P.L = sh.L;
-  P.nsp = g.nsp;
-  P.ndim = g.ndim;
-  P.nb = sh.nb;
-  P.ng = sh.ng;
-  P.kpre[0] = sh.kpre[0];
-  P.kpre[1] = sh.kpre[1];
   const size_t qs = (size_t)g.nsp * 64;
-  hicu_launch(conv_bimage_kernel<0>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 0);
-  int s = hicu_check_launch("conv_bimage_kernel");
-  if (s) return s;
-  hicu_launch(conv_bimage_kernel<2>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 1);
-  return hicu_check_launch("conv_bimage_kernel");
+  for (int mode = 0; mode <= 2; mode += 2) {
+    // each image in the axis order its convolution launch will choose
+    int perm[3];
+    choose_perm(g, mode, perm);
+    Shape sh;
+    if (!shape_of(g, p, &sh, perm)) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: no B image");
+    CtParams P{};
+    for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
+    P.L = sh.L;
+    P.nsp = g.nsp;
+    P.ndim = g.ndim;
+    P.nb = sh.nb;
+    P.ng = sh.ng;
+    P.kpre[0] = sh.kpre[0];
+    P.kpre[1] = sh.kpre[1];
+    if (mode == 0)
+      hicu_launch(conv_bimage_kernel<0>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 0);
+    else
+      hicu_launch(conv_bimage_kernel<2>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 1);
+    const int s = hicu_check_launch("conv_bimage_kernel");
+    if (s) return s;
+  }
+  return HICU_OK;
 }
 
 // the next conv_tc launch on this host thread copies its B image from `img`

@@ -53,6 +53,8 @@ CASES = {
     "2d_8x8": ((24, 150), spatial_kernel((8, 8)), None),                # 64 taps, nb = 8: streamed
     "1d_nb9": ((300,), spatial_kernel((9,)), None),                   # outside the tcgen05 scope -> SIMT
     "spread": ((6, 260), spatial_kernel((1, 40)), None),               # outside the tcgen05 scope -> SIMT
+    # C4's layout (short last axis): tiles run along the 60-row axis 0, not the 9 frames
+    "3d_short_last": ((60, 12, 9), spatial_kernel((5, 5, 5)), None),
 }
 SIMT_ONLY = {"1d_nb9", "spread"}
 

@@ -336,6 +336,28 @@ int hicu_coil_apply(int64_t nloc, int nc, int nv, const void* x,
                     const uint8_t* mask, const void* basis, void* y,
                     uint8_t* mask_out, void* stream);
 
+/* ---- collectives of a sharded volume ----------------------
+ * NCCL, resolved at run time from libnccl.so.2.  One communicator per
+ * process/GPU; the 128-byte id comes from hicu_comm_unique_id on rank 0 and
+ * is broadcast by the host.  All calls are asynchronous on `stream`. */
+#define HICU_P2P_SEND 0
+#define HICU_P2P_RECV 1
+typedef struct {
+  int32_t peer;   /* rank in the communicator */
+  int32_t kind;   /* HICU_P2P_SEND / HICU_P2P_RECV */
+  void* buf;      /* device buffer (send: read, recv: written) */
+  int64_t bytes;
+} hicu_p2p_op;
+int hicu_comm_available(void);
+int hicu_comm_unique_id(void* id128_out);
+int hicu_comm_init(int nranks, int rank, const void* id128, void** comm_out);
+int hicu_comm_destroy(void* comm);
+/* in-place sum over ranks of count doubles (Gram partials as 2 n^2 doubles,
+ * the step scalars) */
+int hicu_allreduce(void* comm, double* buf, int64_t count, void* stream);
+/* one grouped round of sends and receives (halo accumulate / refresh) */
+int hicu_halo_exchange(void* comm, int nops, const hicu_p2p_op* ops, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,7 +68,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
                     print("compiled", os.path.relpath(done, ROOT), flush=True)
     newest = max(os.path.getmtime(o) for o in objs)
     if force or jobs or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-ldl"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")

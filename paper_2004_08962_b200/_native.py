@@ -63,6 +63,12 @@ class HicuStageArgs(ctypes.Structure):
     ]
 
 
+class HicuP2P(ctypes.Structure):
+    _fields_ = [("peer", c_int32), ("kind", c_int32), ("buf", c_void_p), ("bytes", c_int64)]
+
+
+P2P_SEND, P2P_RECV = 0, 1
+
 _GP = POINTER(HicuGeom)
 _SIGS = {
     "hicu_abi_version": (c_int, []),
@@ -89,6 +95,12 @@ _SIGS = {
     "hicu_gram_workspace": (c_size_t, [_GP]),
     "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
     "hicu_gram_path": (c_int, [_GP]),
+    "hicu_comm_available": (c_int, []),
+    "hicu_comm_unique_id": (c_int, [c_void_p]),
+    "hicu_comm_init": (c_int, [c_int, c_int, c_void_p, POINTER(c_void_p)]),
+    "hicu_comm_destroy": (c_int, [c_void_p]),
+    "hicu_allreduce": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "hicu_halo_exchange": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "hicu_gram_flops": (c_double, [_GP]),
     "hicu_conv_uses_tensor_cores": (c_int, [_GP, c_int]),
     "hicu_gram": (c_int, [_GP, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),

@@ -41,6 +41,7 @@ import numpy as np
 from .errors import ConfigError
 
 __all__ = [
+    "NativeComm",
     "partition_slices",
     "reconstruct_slices",
     "ShardPlan",
@@ -188,6 +189,67 @@ class ShardPlan:
         return [tuple(r) for r in runs]
 
 
+class NativeComm:
+    """The library's own NCCL communicator (hicu_comm_*) over the ranks of a
+    ``torch.distributed`` group: the unique id is made on the group's rank 0
+    and broadcast by the host; collectives then run from C on the compute
+    stream (hicu_allreduce, hicu_halo_exchange) without torch in the loop."""
+
+    def __init__(self, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        from . import _native as nat
+
+        self.nat = nat
+        L = nat.lib()
+        if not L.hicu_comm_available():
+            raise RuntimeError("libnccl.so.2 is not loadable")
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        idbuf = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            nat.check(L.hicu_comm_unique_id(idbuf), "comm_unique_id")
+        obj = [bytes(idbuf.raw)]
+        src = 0 if group is None else dist.get_global_rank(group, 0)
+        dist.broadcast_object_list(obj, src=src, group=group)
+        idbuf = ctypes.create_string_buffer(obj[0], 128)
+        self.h = ctypes.c_void_p()
+        nat.check(L.hicu_comm_init(self.world, self.rank, idbuf, ctypes.byref(self.h)), "comm_init")
+
+    def allreduce_(self, t):
+        """In-place sum of a float64 (or complex128, as float64 pairs) device tensor."""
+        v = t.view(t.real.dtype) if t.is_complex() else t
+        self.nat.check(self.nat.lib().hicu_allreduce(self.h, v.data_ptr(), v.numel(), self.nat.stream_handle()),
+                       "allreduce")
+        return t
+
+    def exchange(self, ops):
+        """ops: [(peer, kind, tensor)], one grouped NCCL round on the current stream."""
+        import ctypes
+
+        if not ops:
+            return
+        arr = (self.nat.HicuP2P * len(ops))()
+        for i, (peer, kind, t) in enumerate(ops):
+            arr[i].peer, arr[i].kind, arr[i].buf = peer, kind, t.data_ptr()
+            arr[i].bytes = t.numel() * t.element_size()
+        self.nat.check(self.nat.lib().hicu_halo_exchange(self.h, len(ops), ctypes.cast(arr, ctypes.c_void_p),
+                                                         self.nat.stream_handle()), "halo_exchange")
+
+    def close(self):
+        if self.h:
+            self.nat.lib().hicu_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class HaloExchange:
     """Exchanges of plane blocks along the sharded axis over
     ``torch.distributed`` (NCCL for CUDA tensors, gloo for CPU tensors).
@@ -201,13 +263,14 @@ class HaloExchange:
     buffers): the CPU-only multi-rank tests and the single-GPU multi-process
     test of the CUDA backend."""
 
-    def __init__(self, plan: ShardPlan, group=None):
+    def __init__(self, plan: ShardPlan, group=None, native: NativeComm | None = None):
         import torch.distributed as dist
 
         self.plan = plan
         self.group = group
         self.dist = dist
-        self.host_staged = dist.get_backend(group) == "gloo"
+        self.native = native
+        self.host_staged = native is None and dist.get_backend(group) == "gloo"
         self.sends, self.recvs = [], []  # accumulate direction
         for k in range(plan.world):
             for (i0, n, owner, oi0) in plan.for_rank(k).trailing_runs():
@@ -221,9 +284,21 @@ class HaloExchange:
         return k if self.group is None else self.dist.get_global_rank(self.group, k)
 
     def _run(self, ops):
-        if ops:
-            for r in self.dist.batch_isend_irecv(ops):
-                r.wait()
+        if not ops:
+            return
+        if self.native is not None:
+            self.native.exchange(ops)
+            return
+        for r in self.dist.batch_isend_irecv(ops):
+            r.wait()
+
+    def _op(self, kind, t, peer):
+        if self.native is not None:
+            from . import _native as nat
+
+            return (peer, nat.P2P_SEND if kind == "send" else nat.P2P_RECV, t)
+        d = self.dist
+        return d.P2POp(d.isend if kind == "send" else d.irecv, t, self._peer(peer), group=self.group)
 
     def _out(self, t):
         t = t.contiguous()
@@ -245,8 +320,7 @@ class HaloExchange:
         for (dst, i0, n, oi0) in self.sends:
             if dst == me:
                 continue
-            ops.append(dist.P2POp(dist.isend, self._out(g_local.narrow(ax, i0, n)), self._peer(dst),
-                                  group=self.group))
+            ops.append(self._op("send", self._out(g_local.narrow(ax, i0, n)), dst))
         for (src, oi0, n, i0) in self.recvs:
             if src == me:
                 bufs.append((oi0, g_local.narrow(ax, i0, n).clone()))
@@ -254,7 +328,7 @@ class HaloExchange:
             shape = list(g_local.shape)
             shape[ax] = n
             buf = self._buf(g_local, shape)
-            ops.append(dist.P2POp(dist.irecv, buf, self._peer(src), group=self.group))
+            ops.append(self._op("recv", buf, src))
             bufs.append((oi0, buf))
         self._run(ops)
         for oi0, buf in bufs:
@@ -269,8 +343,7 @@ class HaloExchange:
         for (src, oi0, n, i0) in self.recvs:
             if src == me:
                 continue
-            ops.append(dist.P2POp(dist.isend, self._out(g_local.narrow(ax, oi0, n)), self._peer(src),
-                                  group=self.group))
+            ops.append(self._op("send", self._out(g_local.narrow(ax, oi0, n)), src))
         for (dst, i0, n, oi0) in self.sends:
             if dst == me:
                 fills.append((i0, g_local.narrow(ax, oi0, n).clone()))
@@ -278,13 +351,15 @@ class HaloExchange:
             shape = list(g_local.shape)
             shape[ax] = n
             buf = self._buf(g_local, shape)
-            ops.append(dist.P2POp(dist.irecv, buf, self._peer(dst), group=self.group))
+            ops.append(self._op("recv", buf, dst))
             fills.append((i0, buf))
         self._run(ops)
         for i0, buf in fills:
             g_local.narrow(ax, i0, buf.shape[ax]).copy_(buf)
 
     def allreduce_(self, t):
+        if self.native is not None:
+            return self.native.allreduce_(t)
         if self.host_staged and t.is_cuda:
             h = t.cpu()
             self.dist.all_reduce(h, group=self.group)
@@ -528,14 +603,19 @@ def gather_planes(local_owned, plan: ShardPlan, group=None):
     return torch.cat(blocks, dim=ax)
 
 
-def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0, coil_compress: int | None = None):
+def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0, coil_compress: int | None = None,
+                        native_comm: bool | None = None):
     """Reconstruct one volume sharded along ``axis`` (C5: readout, 0; C4:
     time, 2) over the ranks of ``group`` (one GPU per rank).  Returns (xhat
     complex128 full volume, records of this rank's run: list per stage of
     [iters*G, 8] arrays).  ``coil_compress=Nv``: distributed SVD coil
     compression first (covariance all-reduced, one basis on every rank);
-    ``xhat`` is then in the compressed domain, as hicu_reconstruct's."""
+    ``xhat`` is then in the compressed domain, as hicu_reconstruct's.
+    ``native_comm`` (default: with an NCCL group): the library's own NCCL
+    communicator carries the halos and all-reduces on the compute stream."""
     import torch.distributed as dist
+
+    from . import _native as nat
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
@@ -543,16 +623,21 @@ def sharded_reconstruct(x0, mask, kernel, schedule, group=None, axis: int = 0, c
     mask = np.asarray(mask)
     dims = x0.shape if coil_compress is None else x0.shape[:-1] + (int(coil_compress),)
     plan = plan_for(dims, kernel, schedule, world, rank, axis)
-    halo = HaloExchange(plan, group)
+    if native_comm is None:
+        native_comm = dist.get_backend(group) == "nccl" and bool(nat.lib().hicu_comm_available())
+    native = NativeComm(group) if native_comm else None
+    halo = HaloExchange(plan, group, native)
     backend = CudaShardBackend(x0, mask, kernel, schedule, plan, coil_compress=coil_compress,
                                cov_reduce=lambda c: halo.allreduce_(torch_view_real(c)))
     y_owned, recs = ShardedReconstruction(backend, plan, halo).run()
     import torch
 
     yt = torch.from_numpy(y_owned)
-    if not halo.host_staged:
+    if dist.get_backend(group) != "gloo":
         yt = yt.cuda()
     full = gather_planes(yt, plan, group).cpu().numpy()
+    if native is not None:
+        native.close()
     if schedule.dc_mode == "hard" and coil_compress is None:
         obs = mask == 1
         full[obs] = np.asarray(x0, np.complex128)[obs]

@@ -469,3 +469,41 @@ def test_p32_stage_lockstep():
     eg = np.array([s.eta for s in rep.steps])
     assert np.abs(eg - eo).max() <= 1e-4 * np.abs(eo).max()
     assert np.linalg.norm(xg - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+def test_native_nccl_collectives_single_rank():
+    """The library's NCCL communicator (hicu_comm_*, hicu_allreduce,
+    hicu_halo_exchange) at world size 1: the all-reduce is the identity, a
+    grouped self send/receive copies the buffer, and the sharded driver on
+    the native communicator reproduces hicu_reconstruct."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2004_08962_b200 import _native as nat
+    from paper_2004_08962_b200.parallel import NativeComm, sharded_reconstruct
+
+    assert nat.lib().hicu_comm_available()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comm = NativeComm()
+        t = torch.arange(10, dtype=torch.float64, device="cuda")
+        comm.allreduce_(t)
+        src = torch.randn(1000, device="cuda")
+        dst = torch.zeros_like(src)
+        comm.exchange([(0, nat.P2P_SEND, src), (0, nat.P2P_RECV, dst)])
+        torch.cuda.synchronize()
+        assert torch.equal(t, torch.arange(10, dtype=torch.float64, device="cuda"))
+        assert torch.equal(src, dst)
+        comm.close()
+        x0, mask, kern, sched, axis = _sharded_case("time_ring")  # a ring onto itself
+        xs, recs = sharded_reconstruct(x0, mask, kern, sched, axis=axis, native_comm=True)
+    finally:
+        dist.destroy_process_group()
+    xr, rep = H.hicu_reconstruct(x0, mask, kern, sched, tail_energy_threshold=0)
+    assert np.abs(xs - xr).max() <= 1e-5 * np.abs(xr).max()

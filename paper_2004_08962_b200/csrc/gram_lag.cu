@@ -27,10 +27,13 @@
 //   lag_edge_kernel   the short last-axis classes (edge positions);
 //   lag_reduce_kernel fixed-order fp64 sums of the chunk partials -> T;
 //   lag_assemble_kernel  G from T (Hermitian by construction).
+#include <cuda.h>
+
 #include <algorithm>
 #include <vector>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 
 namespace {
 
@@ -656,6 +659,214 @@ __global__ void lag_assemble_kernel(const __grid_constant__ LagParams P, const d
   }
 }
 
+// TMA-staged variant for Nc = 8 (every configuration with 8 coils): each
+// line segment arrives as 64-row boxes of [20 floats] from a tensor map over
+// [16 floats] rows -- the 4 floats past the row are out of bounds and fill
+// with zeros, which yields exactly the padded 80-byte rows above with no
+// per-element cp.async (one thread issues 2 x ceil(rows / 64) TMA loads per
+// line; completion on one mbarrier per ring buffer).
+constexpr int kTmaRows = 64;
+
+__device__ __forceinline__ int tma_boxes(int rows) { return (rows + kTmaRows - 1) / kTmaRows; }
+
+constexpr int kTmaThreadsMax = 416;  // 12 compute warps + the producer: <= 128 registers
+
+template <int CB>
+__global__ void __launch_bounds__(kTmaThreadsMax, 1)
+lag_core_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ LagParams P,
+                    float2* __restrict__ part) {
+  // warps 0 .. W-1 compute (W = GZ * NCB), warp W is the TMA producer; ring
+  // buffers hand off through full (TMA bytes landed) / empty (W warps done)
+  // mbarriers, so compute warps never wait for each other
+  constexpr int NC = 8;
+  constexpr int RB = 80;
+  extern __shared__ __align__(1024) uint8_t tsm[];
+  __shared__ __align__(8) uint64_t full[kCoreStages], empty[kCoreStages];
+  const int64_t bid = blockIdx.x;
+  const int nlg = P.nol * P.NG;
+  const int rowblk = (int)(bid / nlg);
+  const int olg = (int)(bid % nlg);
+  const int ol = olg / P.NG, gzi = olg % P.NG;
+  int b = 0;
+  while (P.chunksA[b + 1] <= rowblk) ++b;
+  const int chunk = rowblk - P.chunksA[b];
+  const int la = P.L - 1;
+  const int dz_lo = gzi * P.GZ - (P.K[la] - 1);
+  const int gz_n = min(P.GZ, P.DZ - gzi * P.GZ);
+  const int nwarps = P.GZ * P.NCB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dzi = warp / P.NCB, cbi = warp % P.NCB;
+  float2* out = part + (size_t)bid * P.GZ * NC * NC;
+  int beg[2], len[2];
+  block_ranges(P, b, beg, len);
+  const int64_t nlines = (int64_t)len[0] * len[1];
+  const int64_t l0 = (int64_t)chunk * P.lpcA, l1 = min(nlines, l0 + P.lpcA);
+  if (!neighbour_ok(P, beg, len, ol)) {
+    hicu_pdl_entry();
+    for (int i = threadIdx.x; i < P.GZ * NC * NC; i += blockDim.x) out[i] = cf(0.f, 0.f);
+    return;
+  }
+  const int pn = (int)P.P;
+  const int nwa = pn + gz_n - 1;
+  const int rb_base = tma_boxes(pn) * kTmaRows;           // rows reserved for the base segment
+  const int rb_nbr = tma_boxes(pn + P.GZ - 1) * kTmaRows;  // and for the neighbour segment
+  const size_t bufsz = (size_t)(rb_base + rb_nbr) * RB;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kCoreStages; ++k) {
+      tc::mbar_init(&full[k], 1);
+      tc::mbar_init(&empty[k], nwarps);
+    }
+    tc::mbar_init_fence();
+  }
+  __syncthreads();
+  hicu_pdl_entry();
+  if (warp == nwarps) {
+    // ---------------- TMA producer (one thread) ----------------
+    if (lane == 0) {
+      const int nbb = tma_boxes(pn), nbn = tma_boxes(nwa);
+      const uint32_t bytes = (uint32_t)((nbb + nbn) * kTmaRows * RB);
+      for (int64_t li = l0; li < l1; ++li) {
+        const int it = (int)(li - l0);
+        const int buf = it % kCoreStages;
+        if (it >= kCoreStages) tc::mbar_wait(&empty[buf], (uint32_t)(((it / kCoreStages) - 1) & 1));
+        int64_t q0 = li, q1 = 0;
+        if (la == 2) {
+          q0 = li / len[1];
+          q1 = li % len[1];
+        }
+        int cb[2] = {0, 0}, cn[2] = {0, 0};
+        for (int a = 0; a < la; ++a) {
+          const int pa = beg[a] + (int)(a == 0 ? q0 : q1);
+          int pq = pa + P.ol_d[ol][a];
+          if (P.circ[a]) {
+            if (pq < 0) pq += (int)P.N[a];
+            if (pq >= P.N[a]) pq -= (int)P.N[a];
+          }
+          cb[a] = pa;
+          cn[a] = pq;
+        }
+        uint8_t* sb = tsm + (size_t)buf * bufsz;
+        uint8_t* sn = sb + (size_t)rb_base * RB;
+        tc::mbar_expect_tx(&full[buf], bytes);
+        // tensor dims (floats, line axis, outer axis 1, outer axis 0); a non-circular line axis
+        const int o1b = la >= 2 ? cb[1] : 0, o0b = la >= 1 ? cb[0] : 0;
+        const int o1n = la >= 2 ? cn[1] : 0, o0n = la >= 1 ? cn[0] : 0;
+        for (int k = 0; k < nbb; ++k)
+          tc::tma_load_4d(sb + (size_t)k * kTmaRows * RB, &tm, 0, (int)P.c0 + k * kTmaRows, o1b, o0b, &full[buf]);
+        for (int k = 0; k < nbn; ++k)
+          tc::tma_load_4d(sn + (size_t)k * kTmaRows * RB, &tm, 0, (int)P.c0 + dz_lo + k * kTmaRows, o1n, o0n,
+                          &full[buf]);
+      }
+    }
+    return;
+  }
+  float2 accR[CB][NC], accI[CB][NC];
+#pragma unroll
+  for (int q = 0; q < CB; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) accR[q][c] = accI[q][c] = cf(0.f, 0.f);
+  const bool active = dzi < gz_n;
+  for (int64_t li = l0; li < l1; ++li) {
+    const int it = (int)(li - l0);
+    const int buf = it % kCoreStages;
+    tc::mbar_wait(&full[buf], (uint32_t)((it / kCoreStages) & 1));
+    if (active) {
+      const uint8_t* sb = tsm + (size_t)buf * bufsz + cbi * CB * 8;
+      const uint8_t* sn = tsm + (size_t)buf * bufsz + (size_t)rb_base * RB + dzi * RB;
+      // two positions per iteration: both positions' operands are loaded
+      // before either's products (hides the shared-memory latency)
+      for (int j0 = lane; j0 < pn; j0 += 64) {
+        const int j1 = j0 + 32;
+        const bool two = j1 < pn;
+        float2 a0[CB], v0[NC], a1[CB], v1[NC];
+#pragma unroll
+        for (int q = 0; q < CB; ++q) {
+          a0[q] = *(const float2*)(sb + j0 * RB + q * 8);
+          a1[q] = two ? *(const float2*)(sb + j1 * RB + q * 8) : cf(0.f, 0.f);
+        }
+#pragma unroll
+        for (int k = 0; k < NC / 2; ++k) {
+          const float4 w0 = *(const float4*)(sn + j0 * RB + k * 16);
+          const float4 w1 = two ? *(const float4*)(sn + j1 * RB + k * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v0[2 * k] = make_float2(w0.x, w0.y);
+          v0[2 * k + 1] = make_float2(w0.z, w0.w);
+          v1[2 * k] = make_float2(w1.x, w1.y);
+          v1[2 * k + 1] = make_float2(w1.z, w1.w);
+        }
+#pragma unroll
+        for (int q = 0; q < CB; ++q)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            accR[q][c] = __ffma2_rn(make_float2(a0[q].x, a0[q].x), v0[c], accR[q][c]);
+            accI[q][c] = __ffma2_rn(make_float2(a0[q].y, a0[q].y), v0[c], accI[q][c]);
+          }
+#pragma unroll
+        for (int q = 0; q < CB; ++q)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            accR[q][c] = __ffma2_rn(make_float2(a1[q].x, a1[q].x), v1[c], accR[q][c]);
+            accI[q][c] = __ffma2_rn(make_float2(a1[q].y, a1[q].y), v1[c], accI[q][c]);
+          }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&empty[buf]);
+  }
+#pragma unroll
+  for (int q = 0; q < CB; ++q)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      float2 v = make_float2(accR[q][c].x + accI[q][c].y, accR[q][c].y - accI[q][c].x);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+        v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+      }
+      accR[q][c] = v;
+    }
+  if (lane == 0 && dzi < P.GZ) {
+#pragma unroll
+    for (int q = 0; q < CB; ++q)
+#pragma unroll
+      for (int c = 0; c < NC; ++c)
+        out[((size_t)dzi * NC + cbi * CB + q) * NC + c] = active ? accR[q][c] : cf(0.f, 0.f);
+  }
+}
+
+typedef CUresult (*LagEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+LagEncodeFn lag_encode() {
+  static LagEncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (LagEncodeFn)p;
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// Tensor map for the TMA core kernel: dims (16 floats, line axis, outer axis
+// 1, outer axis 0) in plan order with the array's byte strides; boxes of
+// 20 floats x 64 rows (the 4 extra floats are out of bounds: zero padding).
+bool lag_tmap(CUtensorMap* tm, const LagParams& P, const float2* x) {
+  LagEncodeFn enc = lag_encode();
+  if (!enc) return false;
+  const int la = P.L - 1;
+  cuuint64_t dims[4] = {16, (cuuint64_t)P.N[la], (cuuint64_t)(la >= 2 ? P.N[1] : 1), (cuuint64_t)(la >= 1 ? P.N[0] : 1)};
+  cuuint64_t strides[3] = {(cuuint64_t)P.cstride[la] * 8, la >= 2 ? (cuuint64_t)P.cstride[1] * 8 : dims[1] * 64,
+                           la >= 1 ? (cuuint64_t)P.cstride[0] * 8 : dims[1] * dims[2] * 64};
+  cuuint32_t box[4] = {20, (cuuint32_t)kTmaRows, 1, 1}, es[4] = {1, 1, 1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float2*>(x), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NC>
 int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
   constexpr int CB = cb_for(NC);
@@ -665,9 +876,25 @@ int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
   float2* partB = (float2*)((char*)ws + pl.b_off);
   int s;
   if (pl.nA > 0) {
-    hicu_allow_max_smem((const void*)lag_core_kernel<NC, CB>);
-    hicu_launch(lag_core_kernel<NC, CB>, (unsigned)pl.nA, pl.threadsA, pl.smemA, st, P, x, partA);
-    if ((s = hicu_check_launch("lag_core_kernel"))) return s;
+    bool done = false;
+    if constexpr (NC == 8) {
+      const int la = P.L - 1;
+      CUtensorMap tm;
+      const int rows = ((int)P.P + kTmaRows - 1) / kTmaRows * kTmaRows +
+                       ((int)P.P + P.GZ - 1 + kTmaRows - 1) / kTmaRows * kTmaRows;
+      const size_t smem = (size_t)kCoreStages * rows * 80 + 1024;
+      if (!P.circ[la] && smem <= (size_t)200 * 1024 && pl.threadsA + 32 <= kTmaThreadsMax && lag_tmap(&tm, P, x)) {
+        hicu_allow_max_smem((const void*)lag_core_tma_kernel<CB>);
+        hicu_launch(lag_core_tma_kernel<CB>, (unsigned)pl.nA, pl.threadsA + 32, smem, st, tm, P, partA);
+        if ((s = hicu_check_launch("lag_core_tma_kernel"))) return s;
+        done = true;
+      }
+    }
+    if (!done) {
+      hicu_allow_max_smem((const void*)lag_core_kernel<NC, CB>);
+      hicu_launch(lag_core_kernel<NC, CB>, (unsigned)pl.nA, pl.threadsA, pl.smemA, st, P, x, partA);
+      if ((s = hicu_check_launch("lag_core_kernel"))) return s;
+    }
   }
   if (pl.nB > 0) {
     hicu_allow_max_smem((const void*)lag_edge_kernel<NC, CB>);

@@ -779,10 +779,19 @@ lag_core_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constan
         const int j1 = j0 + 32;
         const bool two = j1 < pn;
         float2 a0[CB], v0[NC], a1[CB], v1[NC];
+        if (CB == 2) {  // one 16-byte load per position (conflict-free across lanes; 8-byte loads 2-way conflict)
+          const float4 w0 = *(const float4*)(sb + j0 * RB);
+          const float4 w1 = two ? *(const float4*)(sb + j1 * RB) : make_float4(0.f, 0.f, 0.f, 0.f);
+          a0[0] = make_float2(w0.x, w0.y);
+          a0[CB - 1] = make_float2(w0.z, w0.w);
+          a1[0] = make_float2(w1.x, w1.y);
+          a1[CB - 1] = make_float2(w1.z, w1.w);
+        } else {
 #pragma unroll
-        for (int q = 0; q < CB; ++q) {
-          a0[q] = *(const float2*)(sb + j0 * RB + q * 8);
-          a1[q] = two ? *(const float2*)(sb + j1 * RB + q * 8) : cf(0.f, 0.f);
+          for (int q = 0; q < CB; ++q) {
+            a0[q] = *(const float2*)(sb + j0 * RB + q * 8);
+            a1[q] = two ? *(const float2*)(sb + j1 * RB + q * 8) : cf(0.f, 0.f);
+          }
         }
 #pragma unroll
         for (int k = 0; k < NC / 2; ++k) {

@@ -469,7 +469,8 @@ class ReconEngine:
         return float(max(np.sum(lam[r:]), 0.0))
 
     def download(self) -> np.ndarray:
-        return self.y.reshape(self.dims).cpu().numpy().astype(np.complex128)
+        """complex128 copy of the iterate (pinned staging, multithreaded widening)."""
+        return _PINNED.download(self.torch, self.y).reshape(self.dims)
 
 
 _DRAW_POOL = None
@@ -537,6 +538,30 @@ class _PinnedPool:
         self.free = []  # [(nbytes, buf, event)] in release order
         self.max_idle = max_idle_bytes
 
+    def _take(self, torch, n):
+        with self.lock:
+            for i, (nb, b, ev) in enumerate(self.free):
+                if b.numel() == n and (ev is None or ev.query()):
+                    del self.free[i]
+                    return b
+        return torch.empty(n, dtype=torch.complex64).pin_memory()
+
+    def _give(self, torch, buf, ev):
+        with self.lock:
+            self.free.append((buf.numel() * 8, buf, ev))
+            idle = sum(e[0] for e in self.free)
+            while idle > self.max_idle and len(self.free) > 1:
+                idle -= self.free.pop(0)[0]
+
+    def download(self, torch, t):
+        """complex128 numpy copy of a complex64 device tensor through a pinned
+        buffer (the widening runs on torch's CPU threads)."""
+        buf = self._take(torch, t.numel())
+        buf.copy_(t.reshape(-1))  # synchronous device-to-host copy on the current stream
+        out = buf.to(torch.complex128).numpy()
+        self._give(torch, buf, None)
+        return out
+
     def upload(self, torch, a):
         a = np.asarray(a)
         n = a.size
@@ -549,7 +574,15 @@ class _PinnedPool:
                     break
         if buf is None:
             buf = torch.empty(n, dtype=torch.complex64).pin_memory()
-        np.copyto(buf.numpy().reshape(a.shape), a, casting="unsafe")
+        src = np.ascontiguousarray(a)
+        if src.dtype in (np.complex64, np.complex128):
+            import warnings
+
+            with warnings.catch_warnings():  # read-only caller arrays: torch only reads them here
+                warnings.simplefilter("ignore")
+                buf.copy_(torch.from_numpy(src).reshape(-1))  # cast + copy on torch's CPU threads
+        else:
+            np.copyto(buf.numpy().reshape(a.shape), a, casting="unsafe")
         out = buf.to("cuda", non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
@@ -633,15 +666,24 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
                                                 ref_dev.data_ptr(), None, nat.stream_handle()), "coil_apply")
         basis = bdev  # downloaded after the solve (no synchronisation here)
         x0_exact = None  # observed samples live (in c64) on the device
+        exact_on_device = False
     else:
         dims = x0.shape
-        x0_exact = np.ascontiguousarray(x0, dtype=np.complex128)
-        xm = np.where(observed_in, x0_exact, 0)
-        x_init = xm.astype(np.complex64)
-        mask_dev = observed_in.astype(np.uint8)
+        # raw k-space (complex64 on the device) and the observed mask through
+        # pinned staging; mask_apply (arrays.py:54-67) runs on the device.  The
+        # caller's x0 itself (no copy) re-imposes the observed samples
+        # bit-exactly on return.
+        x0_exact = x0
+        xd = _upload_pinned(torch, x0)
+        md = to_dev(observed_in.view(np.uint8), np.uint8).reshape(-1)
+        x_init = torch.where(md.bool(), xd, torch.zeros((), dtype=xd.dtype, device=xd.device))
+        mask_dev = md
         observed = observed_in
+        # complex64 input: its observed samples are exact on the device, so the
+        # result is assembled there (no host pass over the volume)
+        exact_on_device = x0.dtype == np.complex64
         ref_dev = None if reference is None else np.asarray(reference).astype(np.complex64)
-        h2d += x_init.nbytes + mask_dev.nbytes + (0 if ref_dev is None else ref_dev.nbytes)
+        h2d += xd.numel() * 8 + md.numel() + (0 if ref_dev is None else ref_dev.nbytes)
     counters = counters if counters is not None else Counters()
     meter = meter if meter is not None else MemoryMeter()
     report = ReconReport()
@@ -683,10 +725,12 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
         if iterate_callback is not None:
             xi = eng.download()
             if schedule.dc_mode == "hard" and x0_exact is not None:
-                xi[observed] = x0_exact[observed]
+                np.copyto(xi, x0_exact, where=observed)
             iterate_callback(si, it0, xi)
         watch.resume()
     _tr("issued")
+    if schedule.dc_mode == "hard" and exact_on_device:
+        eng.y.copy_(torch.where(md.bool(), xd, eng.y))  # observed samples: the caller's, exactly
     torch.cuda.current_stream().synchronize()
     _tr("device done")
     xhat = eng.download()
@@ -727,8 +771,8 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
             if lockstep_v is None:
                 counters.gram += 1
             report.iterations.append(IterationRecord(si, it, last_obj, last_sec, last_ser, tails.get((si, it))))
-    if schedule.dc_mode == "hard" and x0_exact is not None:
-        xhat[observed] = x0_exact[observed]
+    if schedule.dc_mode == "hard" and x0_exact is not None and not exact_on_device:
+        np.copyto(xhat, x0_exact, where=observed)
     report.total_seconds = total
     report.counters = counters.snapshot()
     report.peak_aux_complex = meter.peak

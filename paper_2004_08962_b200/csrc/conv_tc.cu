@@ -293,12 +293,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&ready[s], 128);
+      tc::mbar_init(&ready[s], 4);  // one arrival per converter warp
       tc::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], kEpiWarps * 32);
+      tc::mbar_init(&tempty[b], kEpiWarps);  // one arrival per epilogue warp
     }
     tc::mbar_init(&bfull, 1);
     tc::mbar_init_fence();
@@ -483,7 +483,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
             }
           }
           tc::fence_proxy_async();
-          tc::mbar_arrive(&ready[s]);
+          // every lane's shared-memory writes are fenced for the async proxy;
+          // one arrival per warp (128 arrivals on one mbarrier serialised ~300
+          // cycles per stage)
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) tc::mbar_arrive(&ready[s]);
           if (++s == S) { s = 0; ph ^= 1; }
         }
     }
@@ -542,7 +546,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
             w4[1] = make_float4(f[4], f[5], f[6], f[7]);
           }
           tc::fence_before();
-          tc::mbar_arrive(&tempty[tb]);
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tempty[tb]);
           if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[7] = gtimer();
           if (nbuf == 2) {
             tb ^= 1;

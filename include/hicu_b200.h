@@ -195,6 +195,13 @@ int hicu_conv_uses_tensor_cores(const hicu_geom* g, int p);
 int hicu_gram(const hicu_geom* g, const void* x, void* G, void* ws,
               size_t ws_bytes, void* stream);
 
+/* Top-r eigenpairs of a Hermitian n x n c128 matrix (row-major, full
+ * storage): evals descending (r doubles), V n x r orthonormal (row-major).  The
+ * dense Cadzow baseline's rank-r truncation (oracle.py:138-174). */
+size_t hicu_eigh_top_workspace(int n, int r);
+int hicu_eigh_top(int n, int r, const void* A, double* evals, void* V, void* ws,
+                  size_t ws_bytes, void* stream);
+
 /* C = op(A) op(B) for small row-major c128 matrices; op 'N' or 'C' (conj
  * transpose).  C is m x n; op(A) is m x k; op(B) is k x n. */
 int hicu_zgemm(char opa, char opb, int m, int n, int k, const void* A, int lda,

@@ -95,6 +95,8 @@ _SIGS = {
     "hicu_gram_workspace": (c_size_t, [_GP]),
     "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
     "hicu_gram_path": (c_int, [_GP]),
+    "hicu_eigh_top_workspace": (c_size_t, [c_int, c_int]),
+    "hicu_eigh_top": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "hicu_comm_available": (c_int, []),
     "hicu_comm_unique_id": (c_int, [c_void_p]),
     "hicu_comm_init": (c_int, [c_int, c_int, c_void_p, POINTER(c_void_p)]),

@@ -1201,3 +1201,22 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
   hicu_launch(back_transform_kernel, (r + bw - 1) / bw, bw * 32, smem, st, l, r, Vt, tau, z, F);
   return hicu_check_launch("back_transform_kernel");
 }
+
+// ---------------------------------------------------------------------------
+// Top-r eigenpairs of a Hermitian n x n complex128 matrix (row-major, full
+// storage): the dense Cadzow baseline's rank-r truncation (oracle.py:138-141,
+// truncated SVD of H == top-r eigenvectors of H^H H).  evals descending, V
+// n x r orthonormal columns.
+// ---------------------------------------------------------------------------
+extern "C" size_t hicu_eigh_top_workspace(int n, int r) {
+  if (n < 1 || r < 1 || r > n) return 0;
+  return hicu_heev_top_workspace(n, r);
+}
+
+extern "C" int hicu_eigh_top(int n, int r, const void* A, double* evals, void* V, void* ws, size_t ws_bytes,
+                             void* stream) {
+  if (n < 1 || r < 1 || r > n || !A || !evals || !V || !ws)
+    return hicu_set_error(HICU_ERR_PARAMETER, "eigh_top: bad arguments");
+  if (ws_bytes < hicu_heev_top_workspace(n, r)) return hicu_set_error(HICU_ERR_WORKSPACE, "eigh_top: workspace");
+  return hicu_heev_top(n, r, (const double2*)A, evals, (double2*)V, ws, (cudaStream_t)stream);
+}

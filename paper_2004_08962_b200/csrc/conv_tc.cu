@@ -1,37 +1,42 @@
 // Hankel convolution u = H(y) Q~ and its transpose (the k-space scatter
-// g = H^H(u) Q~^H) on the 5th-generation tensor cores: tcgen05 kind::tf32 with
-// a 3xTF32 split (FP32-grade accuracy), TMA-staged operands, TMEM accumulators.
+// g = H^H(u) Q~^H) on the 5th-generation tensor cores: tcgen05 kind::f16 with
+// fp16 hi/lo splits under a power-of-two scale (FP32-grade accuracy: 22
+// significant bits per operand, the precision of a 3xTF32 split), TMEM
+// accumulators.
 //
 // Reference: hankel.py:255-322 (hankel_apply), hankel.py:394-440
 // (kspace_adjoint_scatter), solver.py:335-351 (objective / ELS terms, DC).
 //
 // Scope: coil-separable support with Nc = 8 coils, p = 8 JL columns, no
 // circular axes, 1..3 spatial axes, kernel last-axis extent nb <= 8.  One
-// spatial position of the k-space array is a 64-byte row of 16 floats (8
-// complex coils) and a row of u is also 16 floats (8 complex columns), so both
-// operands are natively K-major with 64-byte rows: the SWIZZLE_64B canonical
-// layout that a TMA box of [rows x 16 floats] produces.
+// spatial position of the k-space array is a row of 16 floats (8 complex
+// coils) and a row of u is also 16 floats (8 complex columns): one K = 16
+// step of a kind::f16 MMA, a 32-byte SWIZZLE_32B K-major operand row.
 //
-// Shift-GEMM formulation.  tcgen05.mma (M = 128, K = 8, tf32) costs a fixed
-// ~80 cycles for any N <= 128 on this part (scripts/tc_mma_rate.cu), so one
-// MMA per kernel tap (N = 16) would be issue-bound.  Instead, for every kernel
-// "prefix" a (all spatial axes but the last) one MMA multiplies a 128-row tile
-// of one k-space line by the stacked operators of ALL last-axis taps b:
+// Shift-GEMM formulation.  For every kernel "prefix" a (all spatial axes but
+// the last) one MMA multiplies a 128-row tile of one k-space line by the
+// stacked operators of ALL last-axis taps b:
 //   D[m, b, :] = A_a[m, :] . B_{a,b}^T      (N = 16 * nb per precision term)
 // accumulated over a in TMEM.  Output row i then needs D[i + b, b, :] (conv)
 // or D[i - b, b, :] (scatter): the shift moves to the epilogue, which stages
 // D in a shared-memory window that carries nb - 1 rows from one tile to the
-// next along the line.  Per 128-row tile: 2 k-steps x 2 MMAs x (#prefixes)
-// (20 for a 5x5 kernel) instead of 100 one-tap MMAs.
+// next along the line.
 //
-// 3xTF32: x = hi + lo; A_hi [B_hi; B_lo] (one MMA, N = 32 nb) plus A_lo B_hi
+// Split products: A_hi [B_hi; B_lo] (one MMA, N = 32 nb) plus A_lo B_hi
 // (N = 16 nb, accumulated into the A_hi B_hi columns); the dropped lo*lo term
-// is ~2^-21 relative.  B images for all taps are built once per CTA in shared
-// memory (rows hi then lo, round-to-nearest splits).  A tiles: the TMA-landed
-// fp32 values serve as A_hi directly (the tensor core truncates to tf32) and
-// converter warps write only A_lo = rna(x - trunc(x)).  Accumulation
-// chains are short (2 x #prefixes MMAs per column), so the tensor core's fp32
-// accumulator rounding stays at the fp32 level.
+// is ~2^-22 relative.  A scale: max |A| from amax_kernel partials (the kernel
+// launched just before); B scale: in the image trailer.  The epilogue
+// multiplies by 1 / (s_A s_B), a power of two (exact).
+//
+// Why fp16 and not 3xTF32 (measured, scripts/tc_unit_f16.cu and the per-role
+// cycle counters of HICU_CONV_TC_DEBUG=32): with TMA-staged fp32 A tiles, raw
+// fp32 hi and converter-written lo, a stage (one prefix group) moved ~68 KB
+// through shared memory (TMA write, converter read + write, MMA operand
+// reads of 4 tf32 MMAs) -- ~530 cycles at 128 B/clk, the kernel's real
+// limit.  fp16 operands halve the MMA operand bytes and the MMA count (one
+// K = 16 step instead of two K = 8), and the converter warps now load A rows
+// straight from global memory into registers (kPrefetch stages ahead), so
+// an fp32 A tile never touches shared memory: ~32 KB per stage.
 //
 // Epilogues are fused: conv writes u and the objective partial |u|^2; the ELS
 // variant never stores w = H(g)Q~ and accumulates Re<w,u>, |w|^2; the scatter
@@ -40,14 +45,19 @@
 // sums (same meaning as ops.cu:scatter_coil_kernel).  Partial sums are per
 // CTA in fixed order (deterministic).
 //
-// Warp roles (320 threads, one persistent CTA per SM, whole lines per CTA):
-// warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-5 hi/lo
-// converters, warps 6-9 epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (448 threads, one persistent CTA per SM, whole lines per CTA):
+// warp 0 B-image producer (streamed mode), warp 1 TMEM owner + MMA issuer,
+// warps 2-5 A converters (global -> registers -> fp16 hi/lo tiles), warps
+// 6-13 epilogue (TMEM lane quarter = warp % 4).
 #include <cuda.h>
 #include <stdlib.h>
 
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "tc_common.cuh"
@@ -57,26 +67,29 @@ namespace {
 constexpr int kTileM = 128;
 constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
-constexpr int kMaxTaps = 128;              // spatial taps (streamed-B mode)
-constexpr int kMaxTapsRes = 56;            // spatial taps with resident B images (prologue registers)
-constexpr int kHalfBytes = kTileM * 64;    // 8 KB: one 128-row A tile (hi or lo)
-constexpr int kStageBytes = 2 * kHalfBytes;
-constexpr int kMaxStages = 8;
+constexpr int kMaxTaps = 128;              // spatial taps
+constexpr int kAF32 = kTileM * 64;        // 8 KB: one 128-row fp32 A tile (TMA)
+constexpr int kATile = kTileM * 32;        // 4 KB: one 128-row fp16 A tile (hi or lo)
+constexpr int kAStage = kAF32;             // fp32 tile, converted in place into A hi | A lo
+constexpr int kMaxStages = 16;
+constexpr int kConvWarps = 8;              // A converters (fp32 -> fp16 hi/lo), two groups of four
+constexpr int kConvGroups = 2;             // group k converts stages k, k + 2, ... (hides the per-stage fence)
+constexpr int kGroupThreads = kConvWarps * 32 / kConvGroups;
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each owning 8 of the 16 output floats
-constexpr int kThreads = (6 + kEpiWarps) * 32;
+constexpr int kThreads = (2 + kConvWarps + kEpiWarps) * 32;
 constexpr int kSmemBudget = 220 * 1024;    // conservative dynamic shared memory budget (sm_100a opt-in 227 KB)
 
 struct CtParams {
   int L;                  // spatial axes (1..3)
   int nsp;                // spatial taps
   int ndim;               // geometry rank (pos stride per support entry)
-  int nb;                 // kernel extent along the last spatial axis
+  int nb;                 // kernel extent along the last (tile) axis
   int ng;                 // kernel prefixes
   int kpre[2];            // kernel extents of the prefix axes
   int stages;
   int tbuf_stride;        // TMEM columns between the two accumulator buffers (0: one buffer)
   int nacc;               // accumulator sets per tile (prefix groups dealt round-robin; shortens chains)
-  int stage_bytes;        // A hi + A lo (+ one prefix group's B image when streamed)
+  int stage_bytes;        // fp32 A + A hi + A lo (+ one prefix group's B image when streamed)
   int dc_mode;
   float lam;
   int nparts_total;       // entries of `parts` (per value) the ABI promised
@@ -87,11 +100,14 @@ struct CtParams {
   int roff[3];
   int rext[3];
   int64_t ostride[2];     // output strides (rows / positions) of the prefix axes
-  int debug;              // experiment bits (HICU_CONV_TC_DEBUG): 1 no MMA, 2 no TMA, 4 no convert
-  const uint8_t* bimg;    // prebuilt B images (resident mode) or null: one bulk copy replaces the build
+  int debug;              // experiment bits (HICU_CONV_TC_DEBUG): 1 no MMA, 2 no B copy, 4 no A load/convert,
+                          // 8 no TMEM drain, 32 per-role cycle counters, 64 no converter proxy fence
+  const uint8_t* bimg;    // B images (fp16 hi/lo, ng groups + scale trailer), bulk-copied in
   int bimg_early;         // 1: bimg was written >= 2 kernels earlier, copy it before the grid-dependency wait
   int perm[3];            // kernel spatial axis k is geometry axis perm[k]; k = L-1 is the tile ("line") axis
   int64_t lstride;        // output stride (rows / positions) along the line axis
+  const float* amax;      // max |A component| partials (amax_kernel) -> the A scale
+  int namax;
 };
 
 __device__ __forceinline__ void decode_line(const CtParams& P, int line, int (&lc)[2]) {
@@ -126,12 +142,6 @@ __device__ __forceinline__ bool line_active(const CtParams& P, const int (&ga)[k
   for (int g = 0; g < P.ng; ++g)
     if (group_valid<MODE>(P, ga, g, lc)) return true;
   return false;
-}
-
-__device__ __forceinline__ uint64_t gtimer() {
-  uint64_t t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
 }
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -197,14 +207,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// B images of all prefix groups: prefix g at base + g * gbytes; row 16 b + n
-// (hi) / 16 nb + 16 b + n (lo); K-major 64-byte rows, SW64 swizzle on the row
-// index (images are 1024-byte aligned, so this is the absolute-address
-// swizzle the descriptors expect).  base is shared memory (in-kernel build)
-// or global memory (conv_bimage_kernel, copied in with one bulk copy).
+// fp16 hi/lo split with a power-of-two scale s: x s = hi + lo with
+// hi = rn(x s) and lo = rn(x s - hi) (the residual is exact in fp32), i.e. 22
+// significant bits -- the precision of the 3xTF32 split -- as long as x s
+// stays inside fp16's range: s maps max |x| into [2^14, 2^15).  Values below
+// 2^-24 / s lose relative precision, but their absolute error (< 2^-25 / s =
+// 2^-40 max |x|) is far below fp32 rounding of the sums they enter.
+__host__ __device__ __forceinline__ float pow2_scale(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  int e;
+  frexpf(amax, &e);  // amax = m 2^e, m in [0.5, 1)
+  e = e < -100 ? -100 : (e > 110 ? 110 : e);
+  return ldexpf(1.f, 15 - e);
+}
+
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// SW32 K-major fp16 operand layout: row r (16 halfs = 32 B), half k at
+// r * 32 + ((k >> 3) ^ ((r >> 2) & 1)) * 16 + (k & 7) * 2 (the swizzle is on
+// absolute address bits; every operand buffer is 1024-byte aligned).
+__device__ __forceinline__ int sw32_off(int r, int k) { return r * 32 + (((k >> 3) ^ ((r >> 2) & 1)) << 4) + (k & 7) * 2; }
+
+// B images of all prefix groups, fp16: prefix g at base + g * gbytes; row
+// 16 b + n (hi) / 16 nb + 16 b + n (lo), scaled by sb.
 template <int MODE>
 __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, const int (&spos)[kMaxTaps][3], int e,
-                                           float2 q, uint32_t gbytes) {
+                                           float2 q, uint32_t gbytes, float sb) {
   const int L = P.L, nb = P.nb;
   const int sp = e >> 6, c = (e >> 3) & 7, j = e & 7;
   const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
@@ -225,280 +253,274 @@ __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, con
         k = 2 * j + t;
         v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
       }
-      const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
-      const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
-      *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
-      *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
+      const float x = v * sb;
+      const __half hi = __float2half_rn(x);
+      const __half lo = __float2half_rn(x - __half2float(hi));
+      *reinterpret_cast<__half*>(gb + sw32_off(16 * b + n, k)) = hi;
+      *reinterpret_cast<__half*>(gb + sw32_off(16 * nb + 16 * b + n, k)) = lo;
     }
 }
 
-template <int MODE, int QPER>
-__device__ __forceinline__ void build_bimage(uint8_t* base, const CtParams& P, const int (&spos)[kMaxTaps][3],
-                                             const float2 (&qv)[QPER], int nq, uint32_t gbytes) {
+// Stage sequence shared by every role: lines blockIdx.x, +gridDim.x, ...;
+// 128-row chunks; prefix groups that reach the line (all for the conv).
+template <int MODE>
+__device__ __forceinline__ bool stage_next(const CtParams& P, const int (&ga)[kMaxGroups][2], int& line, int& c,
+                                           int& g, int (&lc)[2]) {
+  for (;;) {
+    if (++g >= P.ng) {
+      g = 0;
+      if (++c >= P.chunks) {
+        c = 0;
+        line += gridDim.x;
+        if (line >= P.nlines) return false;
+        decode_line(P, line, lc);
+      }
+    }
+    if (group_valid<MODE>(P, ga, g, lc)) return true;
+  }
+}
+
+// One stage's fp32 A tile (TMA-landed, 128 rows x 16 floats, unswizzled) ->
+// fp16 hi and lo tiles IN PLACE (8 KB fp32 = 4 KB hi + 4 KB lo): the group's
+// threads read all their chunks, meet at the group barrier, then write.
+// Thread t converts 16-byte chunk t & 3 of rows (t >> 2) + 32 i, i < 4
+// (linear, conflict-free shared-memory reads).
+__device__ __forceinline__ void stage_convert(uint8_t* st, int t, float sa, int grp) {
+  constexpr int kPer = kTileM * 4 / kGroupThreads;  // float4 chunks per thread
+  const float4* a4 = reinterpret_cast<const float4*>(st);
+  const int r0 = t >> 2, k = 4 * (t & 3);
+  float4 r[kPer];
 #pragma unroll
-  for (int u = 0; u < QPER; ++u) {
-    const int e = threadIdx.x + u * kThreads;
-    if (e >= nq) break;
-    bimage_put<MODE>(base, P, spos, e, qv[u], gbytes);
+  for (int i = 0; i < kPer; ++i) r[i] = a4[t + kGroupThreads * i];
+  asm volatile("bar.sync %0, %1;" ::"r"(2 + grp), "n"(kGroupThreads) : "memory");
+#pragma unroll
+  for (int i = 0; i < kPer; ++i) {
+    const float x0 = r[i].x * sa, x1 = r[i].y * sa, x2 = r[i].z * sa, x3 = r[i].w * sa;
+    const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+    const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+    const int off = sw32_off(r0 + kGroupThreads / 4 * i, k);
+    *reinterpret_cast<uint2*>(st + off) = make_uint2(h2u(h01), h2u(h23));
+    *reinterpret_cast<uint2*>(st + kATile + off) = make_uint2(h2u(l01), h2u(l23));
   }
 }
 
 // MODE 0: conv forward (u, obj); 1: conv ELS (Re<w,u>, |w|^2); 2: scatter + DC.
-// BS: streamed B images (rebuilt per stage; several accumulator sets).
+// BS: B images streamed per stage (they do not fit next to the pipeline).
 template <int MODE, bool BS>
 __global__ void __launch_bounds__(kThreads, 1)
-conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const int32_t* __restrict__ pos,
-               const float2* __restrict__ qt, float2* __restrict__ out, const float2* __restrict__ uin,
-               const uint8_t* __restrict__ mask, const float2* __restrict__ y, const float2* __restrict__ x0,
-               double* __restrict__ parts) {
+conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float2* __restrict__ out,
+               const float2* __restrict__ uin, const uint8_t* __restrict__ mask, const float2* __restrict__ y,
+               const float2* __restrict__ x0, double* __restrict__ parts) {
   constexpr int NV = MODE == 0 ? 1 : (MODE == 1 ? 2 : 4);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int nb = P.nb, ng = P.ng, L = P.L, S = P.stages;
-  const uint32_t gbytes = (uint32_t)nb * 2048;                  // B image of one prefix: 32 nb rows x 64 B
+  const uint32_t gbytes = (uint32_t)nb * 1024;  // B image of one prefix: 32 nb fp16 rows x 32 B
   uint8_t* sB = smem;
   uint8_t* sStage = sB + (BS ? 0 : (size_t)ng * gbytes);
   const int stb = P.stage_bytes;
   float* sWin = reinterpret_cast<float*>(sStage + (size_t)S * stb);  // (128 + nb - 1) x nb x 16
-  __shared__ __align__(8) uint64_t full[kMaxStages], ready[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t full[kMaxStages], aready[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ __align__(8) uint64_t bres;
   __shared__ uint32_t tslot;
   __shared__ int ga[kMaxGroups][2];
-  __shared__ int spos[kMaxTaps][3];
-  __shared__ short tapidx[kMaxGroups * kMaxNb];  // (prefix g, offset b) -> spatial tap or -1
   __shared__ double red[kEpiWarps][NV];
+  __shared__ float s_scale[2];  // A scale, 1 / (A scale x B scale)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // debug bit 16: CTA milestones (%globaltimer) written to `out` (conv forward only)
-  __shared__ uint64_t trace[16];
-  const bool tr = (P.debug & 16) != 0;
-  if (tr && threadIdx.x == 0) trace[0] = gtimer();
+  // debug bit 32: per-role cycle counters (waits vs work), written to `out` (conv forward only)
+  __shared__ long long pc[12];
+  const bool pf = (P.debug & 32) != 0;
+  if (threadIdx.x < 12) pc[threadIdx.x] = 0;
 
-  // ---- prologue part 1 (before the grid-dependency wait): only static data
-  // (support positions, barrier/TMEM setup), overlapping the previous kernel ----
-  for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
-    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + P.perm[t % L]);
+  // ---- prologue part 1 (before the grid-dependency wait): static data and
+  // barrier/TMEM setup, overlapping the previous kernel ----
   if (threadIdx.x < ng) {
     const int g = threadIdx.x;
     ga[g][0] = L == 2 ? g : (L == 3 ? g / P.kpre[1] : 0);
     ga[g][1] = L == 3 ? g % P.kpre[1] : 0;
   }
-  const bool pre = !BS && P.bimg != nullptr;
-  const bool pre_bs = BS && P.bimg != nullptr;  // streamed: each stage's group image arrives with its A tile
-  __shared__ __align__(8) uint64_t bfull;
-  if (!BS && !pre) {
-    float4* z = reinterpret_cast<float4*>(sB);
-    for (int i = threadIdx.x; i < ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  for (int i = threadIdx.x; i < ng * nb; i += kThreads) tapidx[i] = -1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&ready[s], 4);  // one arrival per converter warp
+      tc::mbar_init(&aready[s], kConvWarps / kConvGroups);  // one arrival per warp of the converting group
       tc::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&tfull[b], 1);
       tc::mbar_init(&tempty[b], kEpiWarps);  // one arrival per epilogue warp
     }
-    tc::mbar_init(&bfull, 1);
+    tc::mbar_init(&bres, 1);
     tc::mbar_init_fence();
-    if (pre && P.bimg_early) {  // the images are older than the previous kernel: fetch them now
-      tc::mbar_expect_tx(&bfull, (uint32_t)ng * gbytes);
-      bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bfull);
+    if (!BS && P.bimg_early) {  // the images are older than the previous kernel: fetch them now
+      tc::mbar_expect_tx(&bres, (uint32_t)ng * gbytes);
+      bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bres);
     }
   }
   if (warp == 1) tc::tmem_alloc(&tslot, 512);
-  // ---- prologue part 2: Q~ (written by the reflector apply) and the k-space
-  // operands are read only after the previous grid has completed ----
+  // ---- prologue part 2: inputs written by the previous kernels ----
   hicu_pdl_entry();
-  if (pre && !P.bimg_early && threadIdx.x == 0) {
-    tc::mbar_expect_tx(&bfull, (uint32_t)ng * gbytes);
-    bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bfull);
+  if (!BS && !P.bimg_early && threadIdx.x == 0) {
+    tc::mbar_expect_tx(&bres, (uint32_t)ng * gbytes);
+    bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bres);
   }
-  constexpr int kQPer = (kMaxTapsRes * 64 + kThreads - 1) / kThreads;
-  float2 qv[kQPer];
-  const int nq = (BS || pre) ? 0 : P.nsp * 64;
+  if (warp == 2) {
+    float m = 0.f;
+    for (int i = lane; i < P.namax; i += 32) m = fmaxf(m, __ldg(P.amax + i));
 #pragma unroll
-  for (int u = 0; u < kQPer; ++u) {
-    const int e = threadIdx.x + u * kThreads;
-    qv[u] = e < nq ? __ldg(qt + e) : make_float2(0.f, 0.f);
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      const float sa = pow2_scale(m);
+      const float sb = *reinterpret_cast<const float*>(P.bimg + (size_t)ng * gbytes);
+      s_scale[0] = sa;
+      s_scale[1] = 1.f / (sa * sb);
+    }
   }
-  __syncthreads();
-  for (int sp = threadIdx.x; sp < P.nsp; sp += kThreads) {
-    const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
-    tapidx[g * nb + spos[sp][L - 1]] = (short)sp;
-  }
-  if (tr && threadIdx.x == 0) trace[1] = gtimer();
-  if (!pre) build_bimage<MODE>(sB, P, spos, qv, nq, gbytes);
-  tc::fence_proxy_async();
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem = tslot;
   const int nbuf = P.tbuf_stride > 0 ? 2 : 1;
-  if (tr && threadIdx.x == 0) trace[2] = gtimer();
+  if (pf && threadIdx.x == 0) pc[8] = clock64();
 
   if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
-        int lc[2];
-        decode_line(P, line, lc);
-        for (int c = 0; c < P.chunks; ++c)
-          for (int g = 0; g < ng; ++g) {
-            if (!group_valid<MODE>(P, ga, g, lc)) continue;
-            tc::mbar_wait(&empty[s], ph ^ 1);
-            if (P.debug & 2) {
-              tc::mbar_arrive(&full[s]);
-            } else {
-              tc::mbar_expect_tx(&full[s], kHalfBytes + (pre_bs ? gbytes : 0u));
-              // tensor coordinate 1 = last spatial axis, 2 = axis L-2, 3 = axis L-3
-              int c1, c2 = 0, c3 = 0;
-              if (MODE < 2) {
-                c1 = P.roff[L - 1] + c * kTileM;
-                if (L == 2) c2 = P.roff[0] + lc[0] + ga[g][0];
-                if (L == 3) {
-                  c2 = P.roff[1] + lc[1] + ga[g][1];
-                  c3 = P.roff[0] + lc[0] + ga[g][0];
-                }
-              } else {
-                c1 = c * kTileM;
-                if (L == 2) c2 = lc[0] - P.roff[0] - ga[g][0];
-                if (L == 3) {
-                  c2 = lc[1] - P.roff[1] - ga[g][1];
-                  c3 = lc[0] - P.roff[0] - ga[g][0];
-                }
-              }
-              uint8_t* dst = sStage + (size_t)s * stb;
-              if (tr && line == (int)blockIdx.x && c == 0 && g == 0) trace[3] = gtimer();
-              tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
-              tc::tma_load_4d(dst + 64 * 64, &tmap, 0, c1 + 64, c2, c3, &full[s]);
-              if (pre_bs) bulk_g2s(dst + 2 * kHalfBytes, P.bimg + (size_t)g * gbytes, gbytes, &full[s]);
-            }
-            if (++s == S) { s = 0; ph ^= 1; }
-          }
+    // ---------------- TMA producer: fp32 A tile (+ the group's B image when streamed) ----------------
+    // warp-uniform loop (loop state in uniform registers); one elected lane issues
+    int s = 0;
+    uint32_t ph = 0;
+    int line = blockIdx.x, c = 0, g = -1, lc[2];
+    decode_line(P, line, lc);
+    while (line < P.nlines && stage_next<MODE>(P, ga, line, c, g, lc)) {
+      const long long t0p = (pf && lane == 0) ? clock64() : 0;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      if (pf && lane == 0) pc[0] += clock64() - t0p;
+      // tensor coordinate 1 = line axis, 2 = axis L-2, 3 = axis L-3
+      int c1, c2 = 0, c3 = 0;
+      if (MODE < 2) {
+        c1 = P.roff[L - 1] + c * kTileM;
+        if (L == 2) c2 = P.roff[0] + lc[0] + ga[g][0];
+        if (L == 3) {
+          c2 = P.roff[1] + lc[1] + ga[g][1];
+          c3 = P.roff[0] + lc[0] + ga[g][0];
+        }
+      } else {
+        c1 = c * kTileM;
+        if (L == 2) c2 = lc[0] - P.roff[0] - ga[g][0];
+        if (L == 3) {
+          c2 = lc[1] - P.roff[1] - ga[g][1];
+          c3 = lc[0] - P.roff[0] - ga[g][0];
+        }
       }
+      if (tc::elect_one()) {
+        if (P.debug & 2) {
+          tc::mbar_arrive(&full[s]);
+        } else {
+          uint8_t* dst = sStage + (size_t)s * stb;
+          tc::mbar_expect_tx(&full[s], kAF32 + (BS ? gbytes : 0u));
+          tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
+          if (BS) bulk_g2s(dst + kAStage, P.bimg + (size_t)g * gbytes, gbytes, &full[s]);
+        }
+      }
+      __syncwarp();
+      if (++s == S) { s = 0; ph ^= 1; }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
-      if (pre) tc::mbar_wait(&bfull, 0);  // B images landed (async proxy, no fence needed)
-      const uint32_t idesc_cat = tc::idesc_tf32(kTileM, 32 * nb), idesc_hi = tc::idesc_tf32(kTileM, 16 * nb);
-      const uint32_t bbase = tc::smem_u32(sB);
-      int s = 0, tb = 0;
-      uint32_t ph = 0, tph = 0;
-      for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
-        int lc[2];
-        decode_line(P, line, lc);
-        if (!line_active<MODE>(P, ga, lc)) continue;
-        for (int c = 0; c < P.chunks; ++c) {
-          tc::mbar_wait(&tempty[tb], tph ^ 1);
-          tc::fence_after();
-          const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
-          int vi = 0;  // valid-group index within the tile -> accumulator set vi % nacc
-          for (int g = 0; g < ng; ++g) {
-            if (!group_valid<MODE>(P, ga, g, lc)) continue;
-            tc::mbar_wait(&ready[s], ph);
-            tc::fence_after();
-            if (tr && line == (int)blockIdx.x && c == 0 && g == 0) trace[4] = gtimer();
-            const uint32_t ahi = tc::smem_u32(sStage + (size_t)s * stb), alo = ahi + kHalfBytes;
-            const uint32_t bg = BS ? ahi + 2 * kHalfBytes : bbase + (uint32_t)g * gbytes;
-            const int set = BS ? vi % P.nacc : 0;
-            const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
-            uint32_t acc = BS ? (vi >= P.nacc ? 1u : 0u) : (vi > 0 ? 1u : 0u);
-            ++vi;
-            if (!(P.debug & 1)) {
-#pragma unroll
-              for (int ks = 0; ks < 2; ++ks) {
-                tc::mma_tf32(d, tc::desc_sw64(ahi + ks * 32), tc::desc_sw64(bg + ks * 32), idesc_cat, acc);
-                tc::mma_tf32(d, tc::desc_sw64(alo + ks * 32), tc::desc_sw64(bg + ks * 32), idesc_hi, 1);
-                acc = 1;
-              }
-            }
-            tc::mma_commit(&empty[s]);
-            if (++s == S) { s = 0; ph ^= 1; }
-          }
-          tc::mma_commit(&tfull[tb]);
-          if (tr && line == (int)blockIdx.x && c == 0) trace[5] = gtimer();
-          if (nbuf == 2) {
-            tb ^= 1;
-            if (tb == 0) tph ^= 1;
-          } else {
-            tph ^= 1;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  } else if (warp < 6) {
-    // ---------------- hi/lo converters ----------------
-    const int ct = threadIdx.x - 64;
-    int s = 0;
-    uint32_t ph = 0;
+    // warp-uniform loop; one elected lane (always lane 0: the warp is
+    // converged) issues the MMAs and the commits that track them
+    if (!BS) tc::mbar_wait(&bres, 0);  // resident B images landed (async proxy, no fence needed)
+    const uint32_t idesc_cat = tc::idesc_f16(kTileM, 32 * nb), idesc_hi = tc::idesc_f16(kTileM, 16 * nb);
+    // descriptors advance by address >> 4 in their low 14 bits (shared-memory addresses < 256 KB)
+    const uint64_t dstage0 = tc::desc_sw32(tc::smem_u32(sStage)), dimg0 = tc::desc_sw32(tc::smem_u32(sB));
+    const uint32_t stb16 = (uint32_t)stb >> 4, g16 = gbytes >> 4;
+    int s = 0, tb = 0;
+    uint32_t ph = 0, tph = 0;
     for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
       int lc[2];
       decode_line(P, line, lc);
-      for (int c = 0; c < P.chunks; ++c)
+      if (!line_active<MODE>(P, ga, lc)) continue;
+      for (int c = 0; c < P.chunks; ++c) {
+        const long long t0m = (pf && lane == 0) ? clock64() : 0;
+        tc::mbar_wait(&tempty[tb], tph ^ 1);
+        if (pf && lane == 0) pc[4] += clock64() - t0m;
+        tc::fence_after();
+        const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
+        int vi = 0, set = 0;  // valid-group index within the tile; accumulator set = vi % nacc (kept incrementally)
         for (int g = 0; g < ng; ++g) {
           if (!group_valid<MODE>(P, ga, g, lc)) continue;
-          tc::mbar_wait(&full[s], ph);
-          if (!(P.debug & 4)) {
-            const float4* hi4 = reinterpret_cast<const float4*>(sStage + (size_t)s * stb);
-            float4* lo4 = reinterpret_cast<float4*>(sStage + (size_t)s * stb + kHalfBytes);
-#pragma unroll 4
-            for (int i = ct; i < kTileM * 4; i += 128) {
-              const float4 v = hi4[i];
-              lo4[i] = make_float4(tc::tf32_lo(v.x), tc::tf32_lo(v.y), tc::tf32_lo(v.z), tc::tf32_lo(v.w));
+          const long long t0r = (pf && lane == 0) ? clock64() : 0;
+          tc::mbar_wait(&aready[s], ph);  // converters waited for full[s]: the B image landed too
+          if (pf && lane == 0) pc[3] += clock64() - t0r;
+          tc::fence_after();
+          const uint64_t da = dstage0 + (uint64_t)(s * stb16);
+          const uint64_t db = BS ? da + (uint64_t)(kAStage >> 4) : dimg0 + (uint64_t)(g * g16);
+          const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
+          const uint32_t acc = vi >= P.nacc ? 1u : 0u;
+          ++vi;
+          if (++set == P.nacc) set = 0;
+          const long long t0i = (pf && lane == 0) ? clock64() : 0;
+          if (tc::elect_one()) {
+            if (!(P.debug & 1)) {
+              tc::mma_f16(d, da, db, idesc_cat, acc);                          // A_hi [B_hi; B_lo]
+              tc::mma_f16(d, da + (uint64_t)(kATile >> 4), db, idesc_hi, 1);  // + A_lo B_hi
             }
+            tc::mma_commit(&empty[s]);
           }
-          if (BS && !pre_bs) {
-            // this prefix group's B image: rows 16 b + n (hi) / 16 nb + 16 b + n (lo)
-            uint8_t* gb = sStage + (size_t)s * stb + 2 * kHalfBytes;
-            for (int e = ct; e < nb * 64; e += 128) {
-              const int b = e >> 6, cc = (e >> 3) & 7, j = e & 7;
-              const int sp = tapidx[g * nb + b];
-              const float2 q = sp >= 0 ? __ldg(qt + (size_t)(sp * 8 + cc) * 8 + j) : make_float2(0.f, 0.f);
-#pragma unroll
-              for (int tp = 0; tp < 2; ++tp)
-#pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                  int n, k;
-                  float v;
-                  if (MODE < 2) {
-                    n = 2 * j + tp;
-                    k = 2 * cc + t;
-                    v = tp == 0 ? (t == 0 ? q.x : -q.y) : (t == 0 ? q.y : q.x);
-                  } else {
-                    n = 2 * cc + tp;
-                    k = 2 * j + t;
-                    v = tp == 0 ? (t == 0 ? q.x : q.y) : (t == 0 ? -q.y : q.x);
-                  }
-                  const float hi = tc::tf32_rna(v), lo = tc::tf32_rna(v - hi);
-                  const int rh = 16 * b + n, rl = 16 * nb + 16 * b + n;
-                  *reinterpret_cast<float*>(gb + rh * 64 + (((k >> 2) ^ ((rh >> 1) & 3)) << 4) + (k & 3) * 4) = hi;
-                  *reinterpret_cast<float*>(gb + rl * 64 + (((k >> 2) ^ ((rl >> 1) & 3)) << 4) + (k & 3) * 4) = lo;
-                }
-            }
-          }
-          tc::fence_proxy_async();
-          // every lane's shared-memory writes are fenced for the async proxy;
-          // one arrival per warp (128 arrivals on one mbarrier serialised ~300
-          // cycles per stage)
           __syncwarp();
-          if ((threadIdx.x & 31) == 0) tc::mbar_arrive(&ready[s]);
+          if (pf && lane == 0) pc[5] += clock64() - t0i;
           if (++s == S) { s = 0; ph ^= 1; }
         }
+        if (tc::elect_one()) tc::mma_commit(&tfull[tb]);
+        __syncwarp();
+        if (nbuf == 2) {
+          tb ^= 1;
+          if (tb == 0) tph ^= 1;
+        } else {
+          tph ^= 1;
+        }
+      }
+    }
+  } else if (warp < 2 + kConvWarps) {
+    // ---------------- A converters: fp32 tile -> fp16 hi/lo tiles ----------------
+    // group grp converts stages grp, grp + kConvGroups, ...: each warp's
+    // shared-memory fence of one stage overlaps the other group's conversion
+    const int grp = (warp - 2) / (kConvWarps / kConvGroups);
+    const int t = threadIdx.x - 64 - grp * kGroupThreads;
+    const float sa = s_scale[0];
+    int s = 0, k = 0;
+    uint32_t ph = 0;
+    int line = blockIdx.x, c = 0, g = -1, lc[2];
+    decode_line(P, line, lc);
+    while (line < P.nlines && stage_next<MODE>(P, ga, line, c, g, lc)) {
+      if (k % kConvGroups == grp) {
+        const long long t0c = (pf && t == 0 && grp == 0) ? clock64() : 0;
+        tc::mbar_wait(&full[s], ph);
+        long long t1c = 0;
+        if (pf && t == 0 && grp == 0) {
+          t1c = clock64();
+          pc[1] += t1c - t0c;
+        }
+        if (!(P.debug & 4)) stage_convert(sStage + (size_t)s * stb, t, sa, grp);
+        if (!(P.debug & 64)) tc::fence_proxy_async();
+        // every lane's shared-memory writes are fenced for the async proxy; one arrival per warp
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&aready[s]);
+        if (pf && t == 0 && grp == 0) pc[2] += clock64() - t1c;
+      }
+      ++k;
+      if (++s == S) { s = 0; ph ^= 1; }
     }
   } else {
     // ---------------- epilogue ----------------
     // 8 warps: warp w reads TMEM lane quarter q = w & 3 (A-tile rows 32q..)
     // and owns output floats [8h, 8h + 8) of every row (h = column half).
-    const int q = warp & 3, h = (warp - 6) >> 2;
+    const int ew = warp - 2 - kConvWarps;
+    const int q = warp & 3, h = ew >> 2;
     const int m = 32 * q + lane;  // TMEM lane = A-tile row
-    const int et = threadIdx.x - 192;  // epilogue thread index 0..255
+    const int et = threadIdx.x - 32 * (2 + kConvWarps);  // epilogue thread index 0..255
     const int wrow = nb * 16 + 4; // floats per window row (+16 B: conflict-free float4 rows)
+    const float inv = s_scale[1];
     double acc_v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc_v[i] = 0.0;
@@ -511,23 +533,25 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
       if (L >= 2) obase += (int64_t)lc[0] * P.ostride[0];
       if (L >= 3) obase += (int64_t)lc[1] * P.ostride[1];
       const bool active = line_active<MODE>(P, ga, lc);
-      int nvalid = 1;
-      if (BS) {
-        nvalid = 0;
-        for (int gg = 0; gg < ng; ++gg) nvalid += group_valid<MODE>(P, ga, gg, lc) ? 1 : 0;
-      }
+      int nvalid = 0;
+      for (int gg = 0; gg < ng; ++gg) nvalid += group_valid<MODE>(P, ga, gg, lc) ? 1 : 0;
       if (active) {
         // carried rows start at zero (u rows before the line / k-space before the region)
         for (int i = et; i < (nb - 1) * (wrow / 4); i += kEpiWarps * 32)
           reinterpret_cast<float4*>(sWin)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         epi_bar();
         for (int c = 0; c < P.chunks; ++c) {
+          long long t0e = (pf && et == 0) ? clock64() : 0;
           tc::mbar_wait(&tfull[tb], tph);
+          if (pf && et == 0) {
+            const long long t1e = clock64();
+            pc[6] += t1e - t0e;
+            t0e = t1e;
+          }
           tc::fence_after();
-          if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[6] = gtimer();
           const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride) + (uint32_t)(8 * h);
           float* wr = sWin + (size_t)(nb - 1 + m) * wrow + 8 * h;
-          const int nsets = BS ? min(P.nacc, nvalid) : 1;
+          const int nsets = min(P.nacc, nvalid);
           for (int b = 0; b < ((P.debug & 8) ? 0 : nb); ++b) {
             float f[8];
 #pragma unroll
@@ -542,13 +566,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
               for (int i = 0; i < 8; ++i) f[i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
             }
             float4* w4 = reinterpret_cast<float4*>(wr + 16 * b);
-            w4[0] = make_float4(f[0], f[1], f[2], f[3]);
-            w4[1] = make_float4(f[4], f[5], f[6], f[7]);
+            w4[0] = make_float4(f[0] * inv, f[1] * inv, f[2] * inv, f[3] * inv);
+            w4[1] = make_float4(f[4] * inv, f[5] * inv, f[6] * inv, f[7] * inv);
           }
           tc::fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&tempty[tb]);
-          if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[7] = gtimer();
+          if (pf && et == 0) pc[7] += clock64() - t0e;
           if (nbuf == 2) {
             tb ^= 1;
             if (tb == 0) tph ^= 1;
@@ -580,14 +604,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
                 reinterpret_cast<const float4*>(sWin + (size_t)(kTileM + r) * wrow)[k];
           }
           epi_bar();
-          if (tr && m == 0 && h == 0 && line == (int)blockIdx.x && c == 0) trace[8] = gtimer();
           if (MODE < 2) {
             const int i_out = c * kTileM - (nb - 1) + m;
             if (i_out < 0 || i_out >= P.ext_last) continue;
             const int64_t idx = obase + (int64_t)i_out * P.lstride;
             if (MODE == 0) {
               float4* up = reinterpret_cast<float4*>(out + (size_t)idx * 8 + 4 * h);
-              if (!tr) {  // trace mode keeps `out` for the milestones
+              if (!pf) {  // counter mode keeps `out` for its records
                 up[0] = make_float4(v[0], v[1], v[2], v[3]);
                 up[1] = make_float4(v[4], v[5], v[6], v[7]);
               }
@@ -639,15 +662,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
         }
       }
     }
-    if (tr && m == 0 && h == 0) trace[9] = gtimer();
     // fixed-order reduction over the 256 epilogue threads
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       const double t = warp_sum_d(acc_v[i]);
-      if (lane == 0) red[warp - 6][i] = t;
+      if (lane == 0) red[ew][i] = t;
     }
     epi_bar();
-    if (warp == 6 && lane < NV) {
+    if (ew == 0 && lane < NV) {
       double t = 0.0;
 #pragma unroll
       for (int w = 0; w < kEpiWarps; ++w) t += red[w][lane];
@@ -656,24 +678,23 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, const
     if (blockIdx.x == 0)
       for (int i = et + (int)gridDim.x * NV; i < P.nparts_total * NV; i += kEpiWarps * 32) parts[i] = 0.0;
   }
-  if (tr && threadIdx.x == 192) trace[10] = gtimer();
   tc::fence_before();
   __syncthreads();
+  if (pf && threadIdx.x == 0) pc[9] = clock64();
   if (warp == 1) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 512);
   }
-  if (tr && threadIdx.x == 0 && MODE == 0) {
-    trace[11] = gtimer();
-    uint64_t* o = reinterpret_cast<uint64_t*>(out) + (size_t)blockIdx.x * 12;
-    for (int i = 0; i < 12; ++i) o[i] = trace[i];
+  if (pf && threadIdx.x == 0 && MODE == 0) {
+    pc[9] -= pc[8];
+    long long* o = reinterpret_cast<long long*>(out) + (size_t)blockIdx.x * 12;
+    for (int i = 0; i < 12; ++i) o[i] = pc[i];
   }
 }
 
-// Prebuilt B images (resident mode): the bytes the conv prologue would build
-// in shared memory, written once per Q~ to global memory so each conv CTA
-// copies them with one bulk copy (and, when the image is older than the
-// previous kernel, before its grid-dependency wait).  One CTA per image.
+// B images (fp16 hi/lo, scaled) for one Q~, written once to global memory so
+// each conv CTA copies them with one bulk copy; the power-of-two scale sits
+// in a trailer after the ng images.  One CTA per image.
 template <int MODE>
 __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P, const int32_t* __restrict__ pos,
                                                                const float2* __restrict__ qt_all, size_t qt_stride,
@@ -681,24 +702,93 @@ __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P,
                                                                int img_off) {
   hicu_pdl_entry();
   __shared__ int spos[kMaxTaps][3];
+  __shared__ float wmax[kThreads / 32];
   const int L = P.L;
-  const uint32_t gbytes = (uint32_t)P.nb * 2048;
+  const uint32_t gbytes = (uint32_t)P.nb * 1024;
   uint8_t* img = img_all + (size_t)(2 * blockIdx.x + img_off) * img_stride;
   const float2* qt = qt_all + (size_t)blockIdx.x * qt_stride;
   for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
     spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + P.perm[t % L]);
+  const int nq = P.nsp * 64;
+  float m = 0.f;
+  for (int e = threadIdx.x; e < nq; e += kThreads) {
+    const float2 q = __ldg(qt + e);
+    m = fmaxf(m, fmaxf(fabsf(q.x), fabsf(q.y)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m;
   float4* z = reinterpret_cast<float4*>(img);
   for (int i = threadIdx.x; i < P.ng * (int)gbytes / 16; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int nq = P.nsp * 64;
-  __syncthreads();  // zeroing before the image entries
-  for (int e = threadIdx.x; e < nq; e += kThreads) bimage_put<MODE>(img, P, spos, e, __ldg(qt + e), gbytes);
+  __syncthreads();  // zeroing and the max before the image entries
+  float mm = 0.f;
+  for (int w = 0; w < kThreads / 32; ++w) mm = fmaxf(mm, wmax[w]);
+  const float sb = pow2_scale(mm);
+  for (int e = threadIdx.x; e < nq; e += kThreads) bimage_put<MODE>(img, P, spos, e, __ldg(qt + e), gbytes, sb);
+  if (threadIdx.x == 0) *reinterpret_cast<float*>(img + (size_t)P.ng * gbytes) = sb;
+}
+
+// max |component| partials of an fp32 array (the A-operand scale of the next conv)
+__global__ void __launch_bounds__(256) amax_kernel(const float4* __restrict__ x, int64_t n4, float* __restrict__ part) {
+  hicu_pdl_entry();
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  __shared__ float wm[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t = fmaxf(t, wm[w]);
+    part[blockIdx.x] = t;
+  }
 }
 
 thread_local const uint8_t* t_bimg = nullptr;
 thread_local int t_bimg_early = 0;
 
-// The driver entry point is resolved at run time through cudart so the
-// library loads (and its exports can be checked) on hosts without a driver.
+// Per-(device, stream) scratch: amax partials and the B images of calls that
+// arrive without prebuilt ones.  Kernels on one stream run in order, so one
+// buffer per stream is race-free; it only grows.
+uint8_t* stream_scratch(cudaStream_t st, size_t bytes) {
+  struct Entry {
+    int dev;
+    cudaStream_t st;
+    uint8_t* p;
+    size_t n;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> entries;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : entries)
+    if (e.dev == dev && e.st == st) {
+      if (e.n >= bytes) return e.p;
+      cudaStreamSynchronize(st);
+      cudaFree(e.p);
+      e.p = nullptr;
+      if (cudaMalloc(&e.p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        e.n = 0;
+        return nullptr;
+      }
+      e.n = bytes;
+      return e.p;
+    }
+  uint8_t* p = nullptr;
+  if (cudaMalloc(&p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  entries.push_back({dev, st, p, bytes});
+  return p;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -720,7 +810,8 @@ EncodeTiledFn encode_tiled() {
 // 4-D map over a row-major [ext[0], .., ext[L-1], 16 floats] array seen in
 // the kernel's axis order: dims (16, ext[perm[L-1]], ext[perm[L-2]],
 // ext[perm[L-3]]) with the array's own strides (any spatial axis can be the
-// tile axis), 64-row x 16-float boxes, SWIZZLE_64B, zero fill out of bounds.
+// tile axis), 128-row x 16-float boxes (one per stage), no swizzle (only the converter warps
+// read the fp32 tile: linear 16-byte reads), zero fill out of bounds.
 int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled unavailable");
@@ -734,9 +825,9 @@ int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, cons
                         (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
   cuuint64_t strides[3] = {astride[perm[L - 1]], L >= 2 ? astride[perm[L - 2]] : 64 * dims[1],
                            L >= 3 ? astride[perm[L - 3]] : 64 * dims[1] * dims[2]};
-  cuuint32_t box[4] = {16, 64, 1, 1}, es[4] = {1, 1, 1, 1};
+  cuuint32_t box[4] = {16, (cuuint32_t)kTileM, 1, 1}, es[4] = {1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled failed");
   return HICU_OK;
@@ -814,7 +905,7 @@ void choose_perm(const DevGeom& g, int MODE, int (&perm)[3]) {
 
 struct Shape {
   int L, nb, ng, kpre[2];
-  int bstream;       // B images rebuilt per stage
+  int bstream;       // B images copied per stage (they do not fit resident)
   size_t stage;      // bytes per pipeline stage
   size_t fixed;      // resident B images + window + alignment slack
 };
@@ -835,24 +926,26 @@ bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
   sh->kpre[0] = L >= 2 ? (int)g.kext[perm[0]] : 1;
   sh->kpre[1] = L >= 3 ? (int)g.kext[perm[1]] : 1;
   const size_t win = (((size_t)(kTileM + nb - 1) * (nb * 64 + 16)) + 1023) & ~(size_t)1023;
-  // resident B images when they fit next to >= 3 stages, else one group's image per stage
-  const size_t res_fixed = (size_t)ng * nb * 2048 + win + 1024;
-  if (g.nsp <= kMaxTapsRes && res_fixed + 3 * kStageBytes <= (size_t)kSmemBudget) {
+  // resident B images when they fit next to >= 4 stages, else one group's image per stage
+  const size_t res_fixed = (size_t)ng * nb * 1024 + win + 1024;
+  if (res_fixed + 4 * (size_t)kAStage <= (size_t)kSmemBudget) {
     sh->bstream = 0;
-    sh->stage = kStageBytes;
+    sh->stage = kAStage;
     sh->fixed = res_fixed;
   } else {
     sh->bstream = 1;
-    sh->stage = kStageBytes + (size_t)nb * 2048;
+    sh->stage = kAStage + (size_t)nb * 1024;
     sh->fixed = win + 1024;
   }
-  return sh->fixed + 2 * sh->stage <= (size_t)kSmemBudget;
+  return sh->fixed + 3 * sh->stage <= (size_t)kSmemBudget;
 }
 
+// bytes of one B image set (ng fp16 group images + the scale trailer)
+size_t image_bytes(const Shape& sh) { return (size_t)sh.ng * sh.nb * 1024 + 256; }
+
 template <int MODE, bool BS>
-int launch_bs(const DevGeom& g, const Shape& sh, CtParams P, const CUtensorMap& tm, const int32_t* pos,
-              const float2* qt, float2* out, const float2* uin, const uint8_t* mask, const float2* y,
-              const float2* x0, double* parts, int64_t lines, int nparts_total, cudaStream_t st) {
+int launch_bs(const Shape& sh, CtParams P, const CUtensorMap& tm, float2* out, const float2* uin, const uint8_t* mask,
+              const float2* y, const float2* x0, double* parts, int64_t lines, int nparts_total, cudaStream_t st) {
   // dynamic shared memory available to this instantiation on the current
   // device (the opt-in attribute is per device: hicu_allow_max_smem raises it
   // once per (kernel, device) and is called on every launch; the derived
@@ -872,7 +965,7 @@ int launch_bs(const DevGeom& g, const Shape& sh, CtParams P, const CUtensorMap& 
     avail = (size_t)optin - fa.sharedSizeBytes;
     if (dev >= 0 && dev < kMaxDev) avail_a[dev].store(avail, std::memory_order_release);
   }
-  if (avail < sh.fixed + 2 * sh.stage) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory");
+  if (avail < sh.fixed + 3 * sh.stage) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory");
   P.stages = (int)((avail - sh.fixed) / sh.stage);
   if (P.stages > kMaxStages) P.stages = kMaxStages;
   const size_t smem = sh.fixed + (size_t)P.stages * sh.stage;
@@ -880,18 +973,38 @@ int launch_bs(const DevGeom& g, const Shape& sh, CtParams P, const CUtensorMap& 
   if (grid > hicu_sm_count()) grid = hicu_sm_count();
   if (grid > nparts_total) grid = nparts_total;
   if (grid < 1) grid = 1;
-  hicu_launch(conv_tc_kernel<MODE, BS>, (int)grid, kThreads, smem, st, tm, P, pos, qt, out, uin, mask, y, x0, parts);
+  hicu_launch(conv_tc_kernel<MODE, BS>, (int)grid, kThreads, smem, st, tm, P, out, uin, mask, y, x0, parts);
   return hicu_check_launch("conv_tc_kernel");
 }
 
+void fill_shape_params(CtParams& P, const DevGeom& g, const Shape& sh, const int (&perm)[3]) {
+  for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
+  P.L = sh.L;
+  P.nsp = g.nsp;
+  P.ndim = g.ndim;
+  P.nb = sh.nb;
+  P.ng = sh.ng;
+  P.kpre[0] = sh.kpre[0];
+  P.kpre[1] = sh.kpre[1];
+}
+
 template <int MODE>
-int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, const float2* uin, const uint8_t* mask,
+int build_image(const DevGeom& g, const Shape& sh, const int (&perm)[3], const float2* qt_all, int G, uint8_t* img,
+                size_t ib, int img_off, cudaStream_t st) {
+  CtParams P{};
+  fill_shape_params(P, g, sh, perm);
+  hicu_launch(conv_bimage_kernel<MODE>, G, kThreads, 0, st, P, g.pos, qt_all, (size_t)g.nsp * 64, img, ib, img_off);
+  return hicu_check_launch("conv_bimage_kernel");
+}
+
+template <int MODE>
+int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, const float2* uin, const uint8_t* mask,
            const float2* y, const float2* x0, int dc_mode, float lam, double* parts, int nparts_total,
            cudaStream_t st) {
   // the B-image hint is consumed by this launch whatever happens below (an
   // early error return must not leave it set for an unrelated later call)
   const uint8_t* bimg = t_bimg;
-  const int bimg_early = t_bimg_early;
+  int bimg_early = t_bimg_early;
   t_bimg = nullptr;
   int perm[3];
   choose_perm(g, MODE, perm);
@@ -900,22 +1013,12 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
     return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: geometry outside the tensor-core scope");
   const int L = sh.L;
   CtParams P{};
-  for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
-  P.L = L;
-  P.nsp = g.nsp;
-  P.ndim = g.ndim;
-  P.nb = sh.nb;
-  P.ng = sh.ng;
-  P.kpre[0] = sh.kpre[0];
-  P.kpre[1] = sh.kpre[1];
-  if (sh.bstream) {
-    // many prefix groups: one tile buffer, up to 3 accumulator sets (shorter chains)
-    P.tbuf_stride = 0;
-    P.nacc = min(3, 512 / (32 * sh.nb));
-  } else {
-    P.tbuf_stride = 256;  // two accumulator buffers of 32 nb <= 256 columns
-    P.nacc = 1;
-  }
+  fill_shape_params(P, g, sh, perm);
+  // accumulator sets: chains of at most ~18 MMAs per TMEM accumulator (the
+  // tensor core's fp32 accumulation error grows with the chain length)
+  P.nacc = std::min(3, std::max(1, (2 * sh.ng + 17) / 18));
+  if (P.nacc * 32 * sh.nb > 512) P.nacc = 512 / (32 * sh.nb);
+  P.tbuf_stride = 2 * P.nacc * 32 * sh.nb <= 512 ? 256 : 0;  // double-buffered tiles when two fit
   P.dc_mode = dc_mode;
   P.lam = lam;
   P.nparts_total = nparts_total;
@@ -936,10 +1039,10 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   const int64_t* lext = MODE < 2 ? g.rext : g.dims;
   int64_t ostr[3] = {1, 1, 1};
   {
-    int64_t st = 1;
+    int64_t s = 1;
     for (int a = L - 1; a >= 0; --a) {
-      ostr[a] = st;
-      st *= lext[a];
+      ostr[a] = s;
+      s *= lext[a];
     }
   }
   P.ext_last = (int)lext[perm[L - 1]];
@@ -953,16 +1056,35 @@ int launch(const DevGeom& g, const void* tsrc, const float2* qt, float2* out, co
   }
   if (lines > (int64_t)1 << 30) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: too many lines");
   P.nlines = (int)lines;
-  // TMA source: k-space array (conv, extents dims) or u (scatter, extents rext).
+  // A operand (TMA source): k-space array (conv, extents dims) or u (scatter, extents rext)
+  const int64_t* aext = MODE < 2 ? g.dims : g.rext;
   CUtensorMap tm;
-  int s = cached_tmap(&tm, tsrc, L, MODE < 2 ? g.dims : g.rext, perm);
+  int s = cached_tmap(&tm, asrc, L, aext, perm);
   if (s) return s;
+  int64_t arows = 1;
+  for (int a = 0; a < L; ++a) arows *= aext[a];
+  // scratch: amax partials (+ this call's B image when none was prebuilt)
+  const int namax = (int)std::min<int64_t>(2 * hicu_sm_count(), std::max<int64_t>(1, (arows * 4 + 255) / 256));
+  const size_t ib = image_bytes(sh);
+  uint8_t* scr = stream_scratch(st, 4096 + (bimg ? 0 : ib));
+  if (!scr) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: scratch allocation failed");
+  if (!bimg) {
+    s = build_image<MODE>(g, sh, perm, qt, 1, scr + 4096, 0, 0, st);
+    if (s) return s;
+    bimg = scr + 4096;
+  }
+  bimg_early = 1;  // the amax kernel always runs between the image and this launch
+  hicu_launch(amax_kernel, namax, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows * 4,
+              reinterpret_cast<float*>(scr));
+  if ((s = hicu_check_launch("amax_kernel"))) return s;
+  P.amax = reinterpret_cast<const float*>(scr);
+  P.namax = namax;
   P.stage_bytes = (int)sh.stage;
   P.bimg = bimg;
-  P.bimg_early = bimg ? bimg_early : 0;
+  P.bimg_early = bimg_early;
   if (sh.bstream)
-    return launch_bs<MODE, true>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
-  return launch_bs<MODE, false>(g, sh, P, tm, g.pos, qt, out, uin, mask, y, x0, parts, lines, nparts_total, st);
+    return launch_bs<MODE, true>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
+  return launch_bs<MODE, false>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
 }
 
 }  // namespace
@@ -976,40 +1098,25 @@ bool hicu_conv_tc_supported(const DevGeom& g, int p) {
 }
 
 size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p) {
-  Shape sh;
+  Shape sh, sh2;
   int p0[3], p2[3];
   choose_perm(g, 0, p0);
   choose_perm(g, 2, p2);
-  if (!shape_of(g, p, &sh, p0)) return 0;
-  Shape sh2;
-  if (!shape_of(g, p, &sh2, p2)) return 0;
-  return (size_t)std::max(sh.ng * sh.nb, sh2.ng * sh2.nb) * 2048;
+  if (!shape_of(g, p, &sh, p0) || !shape_of(g, p, &sh2, p2)) return 0;
+  return std::max(image_bytes(sh), image_bytes(sh2));
 }
 
 // images for steps j < G: (j, conv/ELS layout) at img + 2j * ib, (j, scatter) at img + (2j+1) * ib
 int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, int G, uint8_t* img, size_t ib,
                                cudaStream_t st) {
-  const size_t qs = (size_t)g.nsp * 64;
   for (int mode = 0; mode <= 2; mode += 2) {
     // each image in the axis order its convolution launch will choose
     int perm[3];
     choose_perm(g, mode, perm);
     Shape sh;
     if (!shape_of(g, p, &sh, perm)) return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: no B image");
-    CtParams P{};
-    for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
-    P.L = sh.L;
-    P.nsp = g.nsp;
-    P.ndim = g.ndim;
-    P.nb = sh.nb;
-    P.ng = sh.ng;
-    P.kpre[0] = sh.kpre[0];
-    P.kpre[1] = sh.kpre[1];
-    if (mode == 0)
-      hicu_launch(conv_bimage_kernel<0>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 0);
-    else
-      hicu_launch(conv_bimage_kernel<2>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, 1);
-    const int s = hicu_check_launch("conv_bimage_kernel");
+    const int s = mode == 0 ? build_image<0>(g, sh, perm, qt_all, G, img, ib, 0, st)
+                            : build_image<2>(g, sh, perm, qt_all, G, img, ib, 1, st);
     if (s) return s;
   }
   return HICU_OK;

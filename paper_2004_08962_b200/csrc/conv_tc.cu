@@ -68,15 +68,11 @@ constexpr int kTileM = 128;
 constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
 constexpr int kMaxTaps = 128;              // spatial taps
-constexpr int kAF32 = kTileM * 64;        // 8 KB: one 128-row fp32 A tile (TMA)
-constexpr int kATile = kTileM * 32;        // 4 KB: one 128-row fp16 A tile (hi or lo)
-constexpr int kAStage = kAF32;             // fp32 tile, converted in place into A hi | A lo
+constexpr int kAStage = kTileM * 64;      // 8 KB: one 128-row A tile, rows [16 fp16 hi | 16 fp16 lo]
 constexpr int kMaxStages = 16;
-constexpr int kConvWarps = 8;              // A converters (fp32 -> fp16 hi/lo), two groups of four
-constexpr int kConvGroups = 2;             // group k converts stages k, k + 2, ... (hides the per-stage fence)
-constexpr int kGroupThreads = kConvWarps * 32 / kConvGroups;
+constexpr int kWinRow = 20;                // floats per window row (16 + 4: conflict-free float4 rows)
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each owning 8 of the 16 output floats
-constexpr int kThreads = (2 + kConvWarps + kEpiWarps) * 32;
+constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kSmemBudget = 220 * 1024;    // conservative dynamic shared memory budget (sm_100a opt-in 227 KB)
 
 struct CtParams {
@@ -280,31 +276,6 @@ __device__ __forceinline__ bool stage_next(const CtParams& P, const int (&ga)[kM
   }
 }
 
-// One stage's fp32 A tile (TMA-landed, 128 rows x 16 floats, unswizzled) ->
-// fp16 hi and lo tiles IN PLACE (8 KB fp32 = 4 KB hi + 4 KB lo): the group's
-// threads read all their chunks, meet at the group barrier, then write.
-// Thread t converts 16-byte chunk t & 3 of rows (t >> 2) + 32 i, i < 4
-// (linear, conflict-free shared-memory reads).
-__device__ __forceinline__ void stage_convert(uint8_t* st, int t, float sa, int grp) {
-  constexpr int kPer = kTileM * 4 / kGroupThreads;  // float4 chunks per thread
-  const float4* a4 = reinterpret_cast<const float4*>(st);
-  const int r0 = t >> 2, k = 4 * (t & 3);
-  float4 r[kPer];
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) r[i] = a4[t + kGroupThreads * i];
-  asm volatile("bar.sync %0, %1;" ::"r"(2 + grp), "n"(kGroupThreads) : "memory");
-#pragma unroll
-  for (int i = 0; i < kPer; ++i) {
-    const float x0 = r[i].x * sa, x1 = r[i].y * sa, x2 = r[i].z * sa, x3 = r[i].w * sa;
-    const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
-    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-    const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y), l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
-    const int off = sw32_off(r0 + kGroupThreads / 4 * i, k);
-    *reinterpret_cast<uint2*>(st + off) = make_uint2(h2u(h01), h2u(h23));
-    *reinterpret_cast<uint2*>(st + kATile + off) = make_uint2(h2u(l01), h2u(l23));
-  }
-}
-
 // MODE 0: conv forward (u, obj); 1: conv ELS (Re<w,u>, |w|^2); 2: scatter + DC.
 // BS: B images streamed per stage (they do not fit next to the pipeline).
 template <int MODE, bool BS>
@@ -320,8 +291,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
   uint8_t* sB = smem;
   uint8_t* sStage = sB + (BS ? 0 : (size_t)ng * gbytes);
   const int stb = P.stage_bytes;
-  float* sWin = reinterpret_cast<float*>(sStage + (size_t)S * stb);  // (128 + nb - 1) x nb x 16
-  __shared__ __align__(8) uint64_t full[kMaxStages], aready[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  float* sWin = reinterpret_cast<float*>(sStage + (size_t)S * stb);  // per-tap window + carries
+  // tempty[buffer * 3 + set]: the epilogue has drained that accumulator set
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[6];
   __shared__ __align__(8) uint64_t bres;
   __shared__ uint32_t tslot;
   __shared__ int ga[kMaxGroups][2];
@@ -344,13 +316,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&aready[s], kConvWarps / kConvGroups);  // one arrival per warp of the converting group
       tc::mbar_init(&empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&tfull[b], 1);
-      tc::mbar_init(&tempty[b], kEpiWarps);  // one arrival per epilogue warp
-    }
+    for (int b = 0; b < 2; ++b) tc::mbar_init(&tfull[b], 1);
+    for (int b = 0; b < 6; ++b) tc::mbar_init(&tempty[b], kEpiWarps);  // one arrival per epilogue warp
     tc::mbar_init(&bres, 1);
     tc::mbar_init_fence();
     if (!BS && P.bimg_early) {  // the images are older than the previous kernel: fetch them now
@@ -365,7 +334,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     tc::mbar_expect_tx(&bres, (uint32_t)ng * gbytes);
     bulk_g2s(sB, P.bimg, (uint32_t)ng * gbytes, &bres);
   }
-  if (warp == 2) {
+  if (warp == 1) {
     float m = 0.f;
     for (int i = lane; i < P.namax; i += 32) m = fmaxf(m, __ldg(P.amax + i));
 #pragma unroll
@@ -417,7 +386,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           tc::mbar_arrive(&full[s]);
         } else {
           uint8_t* dst = sStage + (size_t)s * stb;
-          tc::mbar_expect_tx(&full[s], kAF32 + (BS ? gbytes : 0u));
+          tc::mbar_expect_tx(&full[s], kAStage + (BS ? gbytes : 0u));
           tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
           if (BS) bulk_g2s(dst + kAStage, P.bimg + (size_t)g * gbytes, gbytes, &full[s]);
         }
@@ -432,7 +401,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     if (!BS) tc::mbar_wait(&bres, 0);  // resident B images landed (async proxy, no fence needed)
     const uint32_t idesc_cat = tc::idesc_f16(kTileM, 32 * nb), idesc_hi = tc::idesc_f16(kTileM, 16 * nb);
     // descriptors advance by address >> 4 in their low 14 bits (shared-memory addresses < 256 KB)
-    const uint64_t dstage0 = tc::desc_sw32(tc::smem_u32(sStage)), dimg0 = tc::desc_sw32(tc::smem_u32(sB));
+    const uint64_t dstage0 = tc::desc_sw64(tc::smem_u32(sStage)), dimg0 = tc::desc_sw32(tc::smem_u32(sB));
     const uint32_t stb16 = (uint32_t)stb >> 4, g16 = gbytes >> 4;
     int s = 0, tb = 0;
     uint32_t ph = 0, tph = 0;
@@ -441,16 +410,17 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       decode_line(P, line, lc);
       if (!line_active<MODE>(P, ga, lc)) continue;
       for (int c = 0; c < P.chunks; ++c) {
-        const long long t0m = (pf && lane == 0) ? clock64() : 0;
-        tc::mbar_wait(&tempty[tb], tph ^ 1);
-        if (pf && lane == 0) pc[4] += clock64() - t0m;
-        tc::fence_after();
         const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
         int vi = 0, set = 0;  // valid-group index within the tile; accumulator set = vi % nacc (kept incrementally)
         for (int g = 0; g < ng; ++g) {
           if (!group_valid<MODE>(P, ga, g, lc)) continue;
+          if (vi < P.nacc) {  // first use of this accumulator set in the tile: drained by the epilogue?
+            const long long t0m = (pf && lane == 0) ? clock64() : 0;
+            tc::mbar_wait(&tempty[tb * 3 + set], tph ^ 1);
+            if (pf && lane == 0) pc[4] += clock64() - t0m;
+          }
           const long long t0r = (pf && lane == 0) ? clock64() : 0;
-          tc::mbar_wait(&aready[s], ph);  // converters waited for full[s]: the B image landed too
+          tc::mbar_wait(&full[s], ph);  // A tile (+ streamed B image) landed
           if (pf && lane == 0) pc[3] += clock64() - t0r;
           tc::fence_after();
           const uint64_t da = dstage0 + (uint64_t)(s * stb16);
@@ -462,8 +432,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           const long long t0i = (pf && lane == 0) ? clock64() : 0;
           if (tc::elect_one()) {
             if (!(P.debug & 1)) {
-              tc::mma_f16(d, da, db, idesc_cat, acc);                          // A_hi [B_hi; B_lo]
-              tc::mma_f16(d, da + (uint64_t)(kATile >> 4), db, idesc_hi, 1);  // + A_lo B_hi
+              tc::mma_f16(d, da, db, idesc_cat, acc);         // A_hi [B_hi; B_lo]  (K step 0 of the 64-B rows)
+              tc::mma_f16(d, da + 2, db, idesc_hi, 1);       // + A_lo B_hi        (K step 1: +32 B)
             }
             tc::mma_commit(&empty[s]);
           }
@@ -481,46 +451,19 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
         }
       }
     }
-  } else if (warp < 2 + kConvWarps) {
-    // ---------------- A converters: fp32 tile -> fp16 hi/lo tiles ----------------
-    // group grp converts stages grp, grp + kConvGroups, ...: each warp's
-    // shared-memory fence of one stage overlaps the other group's conversion
-    const int grp = (warp - 2) / (kConvWarps / kConvGroups);
-    const int t = threadIdx.x - 64 - grp * kGroupThreads;
-    const float sa = s_scale[0];
-    int s = 0, k = 0;
-    uint32_t ph = 0;
-    int line = blockIdx.x, c = 0, g = -1, lc[2];
-    decode_line(P, line, lc);
-    while (line < P.nlines && stage_next<MODE>(P, ga, line, c, g, lc)) {
-      if (k % kConvGroups == grp) {
-        const long long t0c = (pf && t == 0 && grp == 0) ? clock64() : 0;
-        tc::mbar_wait(&full[s], ph);
-        long long t1c = 0;
-        if (pf && t == 0 && grp == 0) {
-          t1c = clock64();
-          pc[1] += t1c - t0c;
-        }
-        if (!(P.debug & 4)) stage_convert(sStage + (size_t)s * stb, t, sa, grp);
-        if (!(P.debug & 64)) tc::fence_proxy_async();
-        // every lane's shared-memory writes are fenced for the async proxy; one arrival per warp
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&aready[s]);
-        if (pf && t == 0 && grp == 0) pc[2] += clock64() - t1c;
-      }
-      ++k;
-      if (++s == S) { s = 0; ph ^= 1; }
-    }
   } else {
     // ---------------- epilogue ----------------
     // 8 warps: warp w reads TMEM lane quarter q = w & 3 (A-tile rows 32q..)
     // and owns output floats [8h, 8h + 8) of every row (h = column half).
-    const int ew = warp - 2 - kConvWarps;
+    const int ew = warp - 2;
     const int q = warp & 3, h = ew >> 2;
     const int m = 32 * q + lane;  // TMEM lane = A-tile row
-    const int et = threadIdx.x - 32 * (2 + kConvWarps);  // epilogue thread index 0..255
-    const int wrow = nb * 16 + 4; // floats per window row (+16 B: conflict-free float4 rows)
+    const int et = threadIdx.x - 64;  // epilogue thread index 0..255
     const float inv = s_scale[1];
+    // per-tap window: rows 0..nb-2 = the tap's rows carried from the previous
+    // tile, rows nb-1+m = this tile's D[m, b, :] (kWinRow floats per row)
+    float* tapbuf = sWin;
+    float* carry = sWin + (kTileM + kMaxNb - 1) * kWinRow;  // [b][nb-1][16]
     double acc_v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc_v[i] = 0.0;
@@ -537,8 +480,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       for (int gg = 0; gg < ng; ++gg) nvalid += group_valid<MODE>(P, ga, gg, lc) ? 1 : 0;
       if (active) {
         // carried rows start at zero (u rows before the line / k-space before the region)
-        for (int i = et; i < (nb - 1) * (wrow / 4); i += kEpiWarps * 32)
-          reinterpret_cast<float4*>(sWin)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = et; i < nb * (kMaxNb - 1) * 16; i += kEpiWarps * 32) carry[i] = 0.f;
         epi_bar();
         for (int c = 0; c < P.chunks; ++c) {
           long long t0e = (pf && et == 0) ? clock64() : 0;
@@ -550,28 +492,33 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           }
           tc::fence_after();
           const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride) + (uint32_t)(8 * h);
-          float* wr = sWin + (size_t)(nb - 1 + m) * wrow + 8 * h;
           const int nsets = min(P.nacc, nvalid);
-          for (int b = 0; b < ((P.debug & 8) ? 0 : nb); ++b) {
-            float f[8];
+          // drain set by set into registers; each set is released to the MMA
+          // warp as soon as it is read (the next tile's groups start on set 0)
+          float f[kMaxNb][8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[i] = 0.f;
-            for (int a = 0; a < nsets; ++a) {
-              uint32_t v0[8], v1[8];
+          for (int b = 0; b < kMaxNb; ++b)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[b][i] = 0.f;
+          for (int a = 0; a < P.nacc; ++a) {
+            if (a < nsets && !(P.debug & 8)) {
               const uint32_t ta = t0 + (uint32_t)(a * 32 * nb);
-              tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
-              tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
-              tc::tmem_wait_ld();
 #pragma unroll
-              for (int i = 0; i < 8; ++i) f[i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
+              for (int b = 0; b < kMaxNb; ++b) {
+                if (b < nb) {
+                  uint32_t v0[8], v1[8];
+                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
+                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
+                  tc::tmem_wait_ld();
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) f[b][i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
+                }
+              }
             }
-            float4* w4 = reinterpret_cast<float4*>(wr + 16 * b);
-            w4[0] = make_float4(f[0] * inv, f[1] * inv, f[2] * inv, f[3] * inv);
-            w4[1] = make_float4(f[4] * inv, f[5] * inv, f[6] * inv, f[7] * inv);
+            tc::fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[tb * 3 + a]);
           }
-          tc::fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&tempty[tb]);
           if (pf && et == 0) pc[7] += clock64() - t0e;
           if (nbuf == 2) {
             tb ^= 1;
@@ -579,31 +526,36 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           } else {
             tph ^= 1;
           }
-          epi_bar();
-          // shifted sums: conv row m takes window rows m + b; scatter row m takes rows nb - 1 + m - b
+          // shifted sums, one tap at a time: conv row m takes D[m + b - (nb-1), b]
+          // (window row m + b), scatter row m takes D[m - b, b] (window row nb-1+m-b)
           float v[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) v[i] = 0.f;
-          for (int b = 0; b < nb; ++b) {
-            const int w = MODE < 2 ? m + b : nb - 1 + m - b;
-            const float4* r4 = reinterpret_cast<const float4*>(sWin + (size_t)w * wrow + 16 * b + 8 * h);
 #pragma unroll
-            for (int i = 0; i < 2; ++i) {
-              const float4 t = r4[i];
-              v[4 * i] += t.x;
-              v[4 * i + 1] += t.y;
-              v[4 * i + 2] += t.z;
-              v[4 * i + 3] += t.w;
+          for (int b = 0; b < kMaxNb; ++b) {
+            if (b < nb) {
+              if (et < (nb - 1) * 4) {
+                const int r = et >> 2, k = et & 3;
+                reinterpret_cast<float4*>(tapbuf + r * kWinRow)[k] =
+                    reinterpret_cast<const float4*>(carry + (b * (kMaxNb - 1) + r) * 16)[k];
+              }
+              float4* w4 = reinterpret_cast<float4*>(tapbuf + (nb - 1 + m) * kWinRow + 8 * h);
+              w4[0] = make_float4(f[b][0] * inv, f[b][1] * inv, f[b][2] * inv, f[b][3] * inv);
+              w4[1] = make_float4(f[b][4] * inv, f[b][5] * inv, f[b][6] * inv, f[b][7] * inv);
+              epi_bar();
+              const int w = MODE < 2 ? m + b : nb - 1 + m - b;
+              const float4* r4 = reinterpret_cast<const float4*>(tapbuf + w * kWinRow + 8 * h);
+              const float4 t0v = r4[0], t1v = r4[1];
+              v[0] += t0v.x; v[1] += t0v.y; v[2] += t0v.z; v[3] += t0v.w;
+              v[4] += t1v.x; v[5] += t1v.y; v[6] += t1v.z; v[7] += t1v.w;
+              if (et < (nb - 1) * 4) {  // this tap's last nb - 1 rows carry into the next tile
+                const int r = et >> 2, k = et & 3;
+                reinterpret_cast<float4*>(carry + (b * (kMaxNb - 1) + r) * 16)[k] =
+                    reinterpret_cast<const float4*>(tapbuf + (kTileM + r) * kWinRow)[k];
+              }
+              epi_bar();
             }
           }
-          epi_bar();
-          // carry the last nb - 1 rows into the next tile (float4 copies spread over all threads)
-          for (int i = et; i < (nb - 1) * (wrow / 4); i += kEpiWarps * 32) {
-            const int r = i / (wrow / 4), k = i % (wrow / 4);
-            reinterpret_cast<float4*>(sWin + (size_t)r * wrow)[k] =
-                reinterpret_cast<const float4*>(sWin + (size_t)(kTileM + r) * wrow)[k];
-          }
-          epi_bar();
           if (MODE < 2) {
             const int i_out = c * kTileM - (nb - 1) + m;
             if (i_out < 0 || i_out >= P.ext_last) continue;
@@ -728,6 +680,63 @@ __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P,
   if (threadIdx.x == 0) *reinterpret_cast<float*>(img + (size_t)P.ng * gbytes) = sb;
 }
 
+// A operand split: each row of 16 floats -> 64 bytes [16 fp16 hi | 16 fp16 lo]
+// of x s_A (s_A from the amax partials of the kernel launched just before),
+// written in the conv's axis order (line axis fastest), so that every
+// 128-row TMA box of the conv is one contiguous 8 KB block (a box along a
+// slow axis of the natural layout gathers 128 rows a whole plane apart, and
+// the TMA unit then paces the pipeline).  The conv's MMAs read hi as K step
+// 0 and lo as K step 1 of the same 64-byte operand rows.  One row per thread.
+struct SplitParams {
+  int L;
+  int64_t ext[3];   // natural (C-order) extents of the spatial axes
+  int perm[3];      // kernel axis k = natural axis perm[k]; perm[L-1] is the line axis (fastest in the output)
+  int64_t istr[3];  // input (natural C-order) row stride of natural axis a
+};
+
+__global__ void __launch_bounds__(256) split_kernel(const float4* __restrict__ x, int64_t rows, const SplitParams sp,
+                                                    const float* __restrict__ amax, int namax, uint4* __restrict__ out) {
+  hicu_pdl_entry();
+  __shared__ float s_sa;
+  if (threadIdx.x < 32) {
+    float m = 0.f;
+    for (int i = threadIdx.x; i < namax; i += 32) m = fmaxf(m, __ldg(amax + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) s_sa = pow2_scale(m);
+  }
+  __syncthreads();
+  const float sa = s_sa;
+  // threads walk OUTPUT rows (consecutive threads write consecutive 64-byte
+  // rows: coalesced stores); each reads its whole 64-byte input row
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < rows; o += (int64_t)gridDim.x * blockDim.x) {
+    int64_t t = o, r = 0;
+    for (int k = sp.L - 1; k >= 0; --k) {
+      const int a = sp.perm[k];
+      const int64_t ca = t % sp.ext[a];
+      t /= sp.ext[a];
+      r += ca * sp.istr[a];
+    }
+    uint32_t hw[8], lw[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float4 v = __ldg(x + r * 4 + k);
+      const float x0 = v.x * sa, x1 = v.y * sa, x2 = v.z * sa, x3 = v.w * sa;
+      const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+      hw[2 * k] = h2u(h01);
+      hw[2 * k + 1] = h2u(h23);
+      lw[2 * k] = h2u(__floats2half2_rn(x0 - f01.x, x1 - f01.y));
+      lw[2 * k + 1] = h2u(__floats2half2_rn(x2 - f23.x, x3 - f23.y));
+    }
+    uint4* po = out + o * 4;
+    po[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    po[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+    po[2] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    po[3] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+  }
+}
+
 // max |component| partials of an fp32 array (the A-operand scale of the next conv)
 __global__ void __launch_bounds__(256) amax_kernel(const float4* __restrict__ x, int64_t n4, float* __restrict__ part) {
   hicu_pdl_entry();
@@ -815,19 +824,13 @@ EncodeTiledFn encode_tiled() {
 int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled unavailable");
-  uint64_t astride[3] = {0, 0, 0};  // byte stride of geometry axis a
-  uint64_t st = 64;
-  for (int a = L - 1; a >= 0; --a) {
-    astride[a] = st;
-    st *= (uint64_t)ext[a];
-  }
-  cuuint64_t dims[4] = {16, (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
+  // the split array is stored in kernel axis order: line axis perm[L-1] fastest
+  cuuint64_t dims[4] = {32, (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
                         (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
-  cuuint64_t strides[3] = {astride[perm[L - 1]], L >= 2 ? astride[perm[L - 2]] : 64 * dims[1],
-                           L >= 3 ? astride[perm[L - 3]] : 64 * dims[1] * dims[2]};
-  cuuint32_t box[4] = {16, (cuuint32_t)kTileM, 1, 1}, es[4] = {1, 1, 1, 1};
-  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(base), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+  cuuint64_t strides[3] = {64, 64 * dims[1], 64 * dims[1] * dims[2]};
+  cuuint32_t box[4] = {32, (cuuint32_t)kTileM, 1, 1}, es[4] = {1, 1, 1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled failed");
   return HICU_OK;
@@ -925,7 +928,8 @@ bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
   sh->ng = ng;
   sh->kpre[0] = L >= 2 ? (int)g.kext[perm[0]] : 1;
   sh->kpre[1] = L >= 3 ? (int)g.kext[perm[1]] : 1;
-  const size_t win = (((size_t)(kTileM + nb - 1) * (nb * 64 + 16)) + 1023) & ~(size_t)1023;
+  const size_t win = ((size_t)(kTileM + kMaxNb - 1) * kWinRow * 4 + (size_t)kMaxNb * (kMaxNb - 1) * 64 + 1023) &
+                     ~(size_t)1023;
   // resident B images when they fit next to >= 4 stages, else one group's image per stage
   const size_t res_fixed = (size_t)ng * nb * 1024 + win + 1024;
   if (res_fixed + 4 * (size_t)kAStage <= (size_t)kSmemBudget) {
@@ -1056,27 +1060,45 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
   }
   if (lines > (int64_t)1 << 30) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: too many lines");
   P.nlines = (int)lines;
-  // A operand (TMA source): k-space array (conv, extents dims) or u (scatter, extents rext)
+  // A operand: k-space array (conv, extents dims) or u (scatter, extents rext),
+  // split into fp16 hi|lo rows (the TMA source) in this stream's scratch
   const int64_t* aext = MODE < 2 ? g.dims : g.rext;
-  CUtensorMap tm;
-  int s = cached_tmap(&tm, asrc, L, aext, perm);
-  if (s) return s;
   int64_t arows = 1;
   for (int a = 0; a < L; ++a) arows *= aext[a];
-  // scratch: amax partials (+ this call's B image when none was prebuilt)
   const int namax = (int)std::min<int64_t>(2 * hicu_sm_count(), std::max<int64_t>(1, (arows * 4 + 255) / 256));
   const size_t ib = image_bytes(sh);
-  uint8_t* scr = stream_scratch(st, 4096 + (bimg ? 0 : ib));
+  const size_t split_off = 4096, img_off = split_off + (((size_t)arows * 64 + 1023) & ~(size_t)1023);
+  uint8_t* scr = stream_scratch(st, img_off + (bimg ? 0 : ib));
   if (!scr) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: scratch allocation failed");
+  CUtensorMap tm;
+  int s = cached_tmap(&tm, scr + split_off, L, aext, perm);
+  if (s) return s;
   if (!bimg) {
-    s = build_image<MODE>(g, sh, perm, qt, 1, scr + 4096, 0, 0, st);
+    s = build_image<MODE>(g, sh, perm, qt, 1, scr + img_off, 0, 0, st);
     if (s) return s;
-    bimg = scr + 4096;
+    bimg = scr + img_off;
   }
-  bimg_early = 1;  // the amax kernel always runs between the image and this launch
+  bimg_early = 1;  // the amax and split kernels always run between the image and this launch
   hicu_launch(amax_kernel, namax, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows * 4,
               reinterpret_cast<float*>(scr));
   if ((s = hicu_check_launch("amax_kernel"))) return s;
+  {
+    SplitParams sp{};
+    sp.L = L;
+    for (int a = 0; a < L; ++a) {
+      sp.ext[a] = aext[a];
+      sp.perm[a] = perm[a];
+    }
+    int64_t st2 = 1;  // natural row strides of the input
+    for (int a = L - 1; a >= 0; --a) {
+      sp.istr[a] = st2;
+      st2 *= aext[a];
+    }
+    const int sb = (int)std::min<int64_t>(8 * hicu_sm_count(), std::max<int64_t>(1, (arows + 255) / 256));
+    hicu_launch(split_kernel, sb, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows, sp,
+                reinterpret_cast<const float*>(scr), namax, reinterpret_cast<uint4*>(scr + split_off));
+    if ((s = hicu_check_launch("split_kernel"))) return s;
+  }
   P.amax = reinterpret_cast<const float*>(scr);
   P.namax = namax;
   P.stage_bytes = (int)sh.stage;

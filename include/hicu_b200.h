@@ -73,6 +73,7 @@ typedef struct hicu_geom {
 #define HICU_GEOM_FORCE_SIMT_CONV 4   /* use the SIMT conv/scatter even when tcgen05 applies */
 #define HICU_GEOM_FORCE_DENSE_GRAM 8  /* dense implicit-im2col Gram instead of the lag Gram */
 #define HICU_GEOM_FORCE_LAG_GRAM 16   /* lag Gram wherever it applies (default: by size) */
+#define HICU_GEOM_FORCE_FFMA_LAG 32   /* lag Gram core on the CUDA cores even where its tensor-core form applies */
 
 /* hicu_gram_path() values */
 #define HICU_GRAM_PATH_SIMT 0     /* dense implicit-im2col Gram, fp32 SIMT (gram_simt.cu) */

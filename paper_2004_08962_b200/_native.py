@@ -23,6 +23,7 @@ GEOM_FORCE_SIMT_GRAM = 2
 GEOM_FORCE_SIMT_CONV = 4
 GEOM_FORCE_DENSE_GRAM = 8
 GEOM_FORCE_LAG_GRAM = 16
+GEOM_FORCE_FFMA_LAG = 32
 GRAM_PATHS = {0: "simt", 1: "tcgen05", 2: "lag"}
 PROF_KINDS = ("gram", "nystrom", "householder", "conv_fwd", "scatter", "conv_els", "update")
 

@@ -86,6 +86,7 @@ int hicu_make_devgeom(const hicu_geom* g, DevGeom* out) {
   memset(&d, 0, sizeof(d));
   d.ndim = g->ndim;
   d.n = g->n;
+  d.flags = g->flags;
   d.pos = g->pos;
   d.koff = g->koff;
   int64_t st = 1;

@@ -77,6 +77,7 @@ struct DevGeom {
   int nc;
   int nsp;  // spatial taps (n / nc)
   int64_t kext[HICU_MAX_NDIM];  // kernel bounding box (0 = unknown)
+  uint32_t flags;               // hicu_geom flags (HICU_GEOM_*)
 };
 
 // Non-circular part of the flat address of row i, plus the region coordinates

@@ -28,6 +28,7 @@
 //   lag_reduce_kernel fixed-order fp64 sums of the chunk partials -> T;
 //   lag_assemble_kernel  G from T (Hermitian by construction).
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <vector>
@@ -47,6 +48,14 @@ constexpr int kCoreStages = 4;   // lines in flight (cp.async ring)
 constexpr int kEdgeThreads = 256;
 constexpr int kLinesPerChunkA = 64;
 constexpr int kLinesPerChunkB = 1024;
+// tensor-core core class: per line, fp16 hi/lo polyphase operand tiles
+// [A_hi 8 KB | A_lo 8 KB | B_hi 16 KB | B_lo 16 KB] (K-major SWIZZLE_64B images)
+constexpr int kTcLineBytes = 49152;
+constexpr int kTcStages = 4;        // line pairs in flight (48 KB each)
+constexpr int kTcPPD = 4;           // line pairs per TMEM accumulation chain (12 MMAs each)
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcThreads = (2 + kTcEpiWarps) * 32;
+constexpr int kTcCols = 80;         // TMEM columns each epilogue thread drains
 
 struct LagParams {
   int L;           // spatial axes
@@ -84,8 +93,11 @@ struct LagParams {
 
 struct LagPlan {
   bool ok = false;
+  bool tc = false;  // core class on the tensor cores (lagtc_* kernels)
   LagParams p;
   size_t t_off = 0, a_off = 0, b_off = 0, bytes = 0;
+  size_t prep_off = 0, amax_off = 0;  // tensor path: per-line operand tiles, amax partials
+  int64_t lines_all = 0;
   int64_t nT = 0;   // complex entries of T
   int64_t nA = 0, nB = 0;  // CTAs
   size_t smemA = 0, smemB = 0;
@@ -229,6 +241,10 @@ LagPlan make_plan(const DevGeom& g) {
     }
     return nl;
   };
+  // tensor-core core class (lagtc_core_kernel): 8 coils, a non-circular line
+  // axis of at most 256 positions and at most 9 last-axis lags
+  pl.tc = g.nc == 8 && !p.circ[la] && p.K[la] <= 5 && p.N[la] <= 256 && p.core_cls >= 0 &&
+          !(g.flags & HICU_GEOM_FORCE_FFMA_LAG);
   // core kernel
   if (p.core_cls >= 0) {
     p.P = p.cls_end[la][p.core_cls] - p.cls_beg[la][p.core_cls];
@@ -237,6 +253,10 @@ LagPlan make_plan(const DevGeom& g) {
     int gz = std::max(1, wmax / p.NCB);
     p.NG = (p.DZ + gz - 1) / gz;
     p.GZ = (p.DZ + p.NG - 1) / p.NG;
+    if (pl.tc) {  // one CTA covers all DZ last-axis lags of its outer lag
+      p.NG = 1;
+      p.GZ = p.DZ;
+    }
     p.lpcA = kLinesPerChunkA;
     p.chunksA[0] = 0;
     for (int b = 0; b < p.NB; ++b)
@@ -245,7 +265,7 @@ LagPlan make_plan(const DevGeom& g) {
     pl.nA = (int64_t)p.nol * p.NG * p.CA;
     pl.threadsA = 32 * p.GZ * p.NCB;
     pl.smemA = (size_t)kCoreStages * row_bytes(p.NC) * (2 * p.P + p.GZ);
-    if (pl.smemA > (size_t)200 * 1024) return pl;
+    if (!pl.tc && pl.smemA > (size_t)200 * 1024) return pl;
   }
   // edge kernel
   if (p.NE > 0) {
@@ -267,6 +287,13 @@ LagPlan make_plan(const DevGeom& g) {
   pl.a_off = al(pl.nT * sizeof(double2));
   pl.b_off = pl.a_off + al((size_t)pl.nA * p.GZ * p.NC * p.NC * sizeof(float2));
   pl.bytes = pl.b_off + al((size_t)pl.nB * p.QB * p.CB * p.NC * sizeof(float2));
+  if (pl.tc) {
+    pl.lines_all = 1;
+    for (int a = 0; a < la; ++a) pl.lines_all *= p.N[a];
+    pl.amax_off = al(pl.bytes);
+    pl.prep_off = pl.amax_off + 4096;
+    pl.bytes = pl.prep_off + (size_t)pl.lines_all * kTcLineBytes;
+  }
   pl.ok = true;
   return pl;
 }
@@ -842,6 +869,322 @@ lag_core_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constan
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core core class (8 coils, line axis <= 256 positions, K <= 5 along it).
+//
+// Polyphase form: position j = 8u + v along the line.  For one line pair
+// (base line L, neighbour line R = L + outer lag),
+//   D[(v,c,p), (s,w,c',q)] = sum_u A[u][(v,c,p)] B_s[u][(w,c',q)]
+// with A[u][(v,c,p)] = part p of x_L[8u + v, c] (zero outside the core class)
+// and B_s[u][(w,c',q)] = part q of x_R[8u + w - 4 + 8s, c']: M = 8 phases x
+// 8 coils x re/im = 128 rows, N = 2 shifts x 8 phases x 16 = 256 columns, K =
+// u (32 values: two K = 16 steps).  Entry (v, s, w) is the last-axis lag
+// dz = 8s + w - 4 - v, so every row holds all 9 lags |dz| <= 4 in the 144
+// consecutive columns [16 v, 16 v + 144), and conj(a) b sums re*re + im*im /
+// re*im - im*re of the (p, q) pairs.  Operands: fp16 hi/lo of x s (s a
+// power of two from max |x|); products A_hi B_hi + A_hi B_lo + A_lo B_hi
+// (22-bit operands, fp32 accumulation in TMEM).  One CTA = one outer lag x
+// one chunk of lines of one outer class block (the same grid, partial-sum
+// layout and reduce / assemble kernels as the CUDA-core path).  A line
+// pair is one 48 KB stage (two bulk copies), 6 MMAs of M128 N256 K16; TMEM
+// holds two 256-column accumulators: the MMA warp fills one for kTcPPD pairs
+// while the epilogue drains the other into fp32 registers.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t lag_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float lag_pow2_scale(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  int e;
+  frexpf(amax, &e);
+  e = e < -100 ? -100 : (e > 110 ? 110 : e);
+  return ldexpf(1.f, 15 - e);
+}
+
+__device__ __forceinline__ float lag_amax_reduce(const float* __restrict__ amax, int namax) {
+  const int lane = threadIdx.x & 31;
+  float m = 0.f;
+  for (int i = lane; i < namax; i += 32) m = fmaxf(m, __ldg(amax + i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return m;
+}
+
+__global__ void __launch_bounds__(256) lagtc_amax_kernel(const float4* __restrict__ x, int64_t n4, float* __restrict__ part) {
+  hicu_pdl_entry();
+  float m = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(x + i);
+    m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  __shared__ float wm[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t = fmaxf(t, wm[w]);
+    part[blockIdx.x] = t;
+  }
+}
+
+// byte offset of 16-byte chunk ch (halfs 8ch..8ch+7) of row r in a K-major SW64 tile
+__device__ __forceinline__ int lag_sw64(int r, int ch) { return r * 64 + ((ch ^ ((r >> 1) & 3)) << 4); }
+
+// One CTA per line (plan order): the line's A (core positions only) and B
+// (both shifts) tiles, fp16 hi/lo of x s, in their shared-memory image.
+__global__ void __launch_bounds__(256) lagtc_prep_kernel(const __grid_constant__ LagParams P,
+                                                         const float2* __restrict__ x, const float* __restrict__ amax,
+                                                         int namax, uint8_t* __restrict__ out) {
+  hicu_pdl_entry();
+  __shared__ __align__(16) __half hs[256][16], lsm[256][16];
+  __shared__ float s_sa;
+  const int la = P.L - 1;
+  const int64_t li = blockIdx.x;
+  int64_t base = 0;
+  if (la == 2) base = (li / P.N[1]) * P.cstride[0] + (li % P.N[1]) * P.cstride[1];
+  else if (la == 1) base = li * P.cstride[0];
+  if (threadIdx.x < 32) {
+    const float m = lag_amax_reduce(amax, namax);
+    if (threadIdx.x == 0) s_sa = lag_pow2_scale(m);
+  }
+  __syncthreads();
+  const float sa = s_sa;
+  const int NL = (int)P.N[la];
+  const int64_t lst = P.cstride[la];
+  for (int e = threadIdx.x; e < 256 * 8; e += 256) {
+    const int pos = e >> 3, c = e & 7;
+    const float2 v = pos < NL ? __ldg(x + base + pos * lst + c) : make_float2(0.f, 0.f);
+    const float xr = v.x * sa, xi = v.y * sa;
+    const __half hr = __float2half_rn(xr), hi = __float2half_rn(xi);
+    hs[pos][2 * c] = hr;
+    hs[pos][2 * c + 1] = hi;
+    lsm[pos][2 * c] = __float2half_rn(xr - __half2float(hr));
+    lsm[pos][2 * c + 1] = __float2half_rn(xi - __half2float(hi));
+  }
+  __syncthreads();
+  uint8_t* o = out + li * (int64_t)kTcLineBytes;
+  const int c0 = (int)P.c0, c1 = (int)(P.c0 + P.P);
+  const __half hz = __float2half_rn(0.f);
+  // A: rows (v, c, p) = 16 v + 2 c + p, K = u; zero outside the core class
+  for (int t = threadIdx.x; t < 128 * 4; t += 256) {
+    const int r = t >> 2, ch = t & 3, v = r >> 4, cp = r & 15;
+    __align__(16) __half hv[8], lv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int pos = 8 * (8 * ch + k) + v;
+      const bool in = pos >= c0 && pos < c1;
+      hv[k] = in ? hs[pos][cp] : hz;
+      lv[k] = in ? lsm[pos][cp] : hz;
+    }
+    *reinterpret_cast<uint4*>(o + lag_sw64(r, ch)) = *reinterpret_cast<const uint4*>(hv);
+    *reinterpret_cast<uint4*>(o + 8192 + lag_sw64(r, ch)) = *reinterpret_cast<const uint4*>(lv);
+  }
+  // B: rows (s, w, c', q) = 128 s + 16 w + 2 c' + q at position 8u + w - 4 + 8s
+  for (int t = threadIdx.x; t < 256 * 4; t += 256) {
+    const int r = t >> 2, ch = t & 3, sh = r >> 7, w = (r >> 4) & 7, cq = r & 15;
+    __align__(16) __half hv[8], lv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int pos = 8 * (8 * ch + k) + w - 4 + 8 * sh;
+      const bool in = pos >= 0 && pos < NL;
+      hv[k] = in ? hs[pos][cq] : hz;
+      lv[k] = in ? lsm[pos][cq] : hz;
+    }
+    *reinterpret_cast<uint4*>(o + 16384 + lag_sw64(r, ch)) = *reinterpret_cast<const uint4*>(hv);
+    *reinterpret_cast<uint4*>(o + 32768 + lag_sw64(r, ch)) = *reinterpret_cast<const uint4*>(lv);
+  }
+}
+
+__device__ __forceinline__ void lag_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ int64_t lag_line_index(const LagParams& P, int p0, int p1) {
+  const int la = P.L - 1;
+  return la == 2 ? (int64_t)p0 * P.N[1] + p1 : (la == 1 ? (int64_t)p0 : 0);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict__ lines,
+                  const float* __restrict__ amax, int namax, float2* __restrict__ part) {
+  constexpr int NC = 8;
+  extern __shared__ __align__(1024) uint8_t tcs_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)tcs_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[kTcStages], empty[kTcStages], tfull[2], tempty[2];
+  __shared__ uint32_t tslot;
+  __shared__ float s_inv;
+  const int64_t bid = blockIdx.x;
+  const int nlg = P.nol * P.NG;
+  const int rowblk = (int)(bid / nlg);
+  const int ol = (int)(bid % nlg);  // NG == 1
+  int b = 0;
+  while (P.chunksA[b + 1] <= rowblk) ++b;
+  const int chunk = rowblk - P.chunksA[b];
+  const int la = P.L - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* out = part + (size_t)bid * P.GZ * NC * NC;
+  int beg[2], len[2];
+  block_ranges(P, b, beg, len);
+  const int64_t nlines = (int64_t)len[0] * len[1];
+  const int64_t l0 = (int64_t)chunk * P.lpcA, l1 = min(nlines, l0 + P.lpcA);
+  if (!neighbour_ok(P, beg, len, ol)) {
+    hicu_pdl_entry();
+    for (int i = threadIdx.x; i < P.GZ * NC * NC; i += blockDim.x) out[i] = cf(0.f, 0.f);
+    return;
+  }
+  const int npairs = (int)(l1 - l0);
+  const int ngroups = (npairs + kTcPPD - 1) / kTcPPD;
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < kTcStages; ++k) {
+      tc::mbar_init(&full[k], 1);
+      tc::mbar_init(&empty[k], 1);
+    }
+    for (int k = 0; k < 2; ++k) {
+      tc::mbar_init(&tfull[k], 1);
+      tc::mbar_init(&tempty[k], kTcEpiWarps);
+    }
+    tc::mbar_init_fence();
+  }
+  if (warp == 1) tc::tmem_alloc(&tslot, 512);
+  hicu_pdl_entry();
+  if (warp == 1) {
+    const float m = lag_amax_reduce(amax, namax);
+    if (lane == 0) {
+      const float sa = lag_pow2_scale(m);
+      s_inv = 1.f / (sa * sa);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+
+  if (warp == 0) {
+    // ---------------- producer: base-line A tiles + neighbour-line B tiles ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < npairs; ++k) {
+      const int64_t li = l0 + k;
+      int q0 = (int)li, q1 = 0;
+      if (la == 2) {
+        q0 = (int)(li / len[1]);
+        q1 = (int)(li % len[1]);
+      }
+      const int pa0 = beg[0] + q0, pa1 = beg[1] + q1;
+      const int pn0 = pa0 + P.ol_d[ol][0], pn1 = pa1 + P.ol_d[ol][1];
+      const uint8_t* la_src = lines + lag_line_index(P, pa0, pa1) * kTcLineBytes;
+      const uint8_t* lb_src = lines + lag_line_index(P, pn0, pn1) * kTcLineBytes + 16384;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      if (tc::elect_one()) {
+        uint8_t* st = sm + (size_t)s * kTcLineBytes;
+        tc::mbar_expect_tx(&full[s], kTcLineBytes);
+        lag_bulk(st, la_src, 16384, &full[s]);
+        lag_bulk(st + 16384, lb_src, 32768, &full[s]);
+      }
+      __syncwarp();
+      if (++s == kTcStages) { s = 0; ph ^= 1; }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = tc::idesc_f16(128, 256);
+    const uint64_t d0 = tc::desc_sw64(tc::smem_u32(sm));
+    int s = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < npairs; ++k) {
+      const int grp = k / kTcPPD, tb = grp & 1;
+      const bool first = (k % kTcPPD) == 0;
+      if (first) tc::mbar_wait(&tempty[tb], ((grp >> 1) & 1) ^ 1);
+      tc::mbar_wait(&full[s], ph);
+      tc::fence_after();
+      const uint64_t da = d0 + (uint64_t)((s * kTcLineBytes) >> 4);
+      const uint64_t dal = da + (8192 >> 4), db = da + (16384 >> 4), dbl = da + (32768 >> 4);
+      const uint32_t d = tmem + (uint32_t)(tb * 256);
+      if (tc::elect_one()) {
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+          const uint64_t o = (uint64_t)(ks * 2);  // +32 B: the second K = 16 step of the 64-byte rows
+          tc::mma_f16(d, da + o, db + o, idesc, (first && ks == 0) ? 0u : 1u);  // A_hi B_hi
+          tc::mma_f16(d, da + o, dbl + o, idesc, 1u);                          // A_hi B_lo
+          tc::mma_f16(d, dal + o, db + o, idesc, 1u);                          // A_lo B_hi
+        }
+        tc::mma_commit(&empty[s]);
+        if ((k % kTcPPD) == kTcPPD - 1 || k == npairs - 1) tc::mma_commit(&tfull[tb]);
+      }
+      __syncwarp();
+      if (++s == kTcStages) { s = 0; ph ^= 1; }
+    }
+  } else {
+    // ---------------- epilogue: drain into fp32 registers, reduce at the end ----------------
+    const int ew = warp - 2, q = warp & 3, h = ew >> 2;
+    const int m = 32 * q + lane;  // TMEM lane = A row (v, c, p)
+    const int v = m >> 4;
+    const int cbase = 32 * q + kTcCols * h;  // first of this thread's kTcCols columns
+    float acc[kTcCols];
+#pragma unroll
+    for (int i = 0; i < kTcCols; ++i) acc[i] = 0.f;
+    for (int grp = 0; grp < ngroups; ++grp) {
+      const int tb = grp & 1;
+      tc::mbar_wait(&tfull[tb], (grp >> 1) & 1);
+      tc::fence_after();
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * 256 + cbase);
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t r[5][8];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) tc::tmem_ld8_nowait(ta + (uint32_t)(8 * (5 * half + i)), r[i]);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[8 * (5 * half + i) + j] += __uint_as_float(r[i][j]);
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[tb]);
+    }
+    // all MMAs are complete (the last tfull): the stage buffers become the
+    // reduction table red[row][144] (the row's 9 lags x 16 columns)
+    constexpr int RS = 148;
+    float* red = reinterpret_cast<float*>(sm);
+#pragma unroll
+    for (int i = 0; i < kTcCols; ++i) {
+      const int cr = cbase + i - 16 * v;
+      if (cr >= 0 && cr < 144) red[m * RS + cr] = acc[i];
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kTcEpiWarps * 32) : "memory");
+    const float inv = s_inv;
+    const int et = threadIdx.x - 64;
+    for (int o = et; o < 9 * NC * NC; o += kTcEpiWarps * 32) {
+      const int dzi = o >> 6, c = (o >> 3) & 7, c2 = o & 7;
+      const int col = 16 * dzi + 2 * c2;
+      float re = 0.f, im = 0.f;
+#pragma unroll
+      for (int vv = 0; vv < 8; ++vv) {
+        const float* rr = red + (16 * vv + 2 * c) * RS + col;  // row (vv, c, re)
+        const float* ri = rr + RS;                             // row (vv, c, im)
+        re += rr[0] + ri[1];
+        im += rr[1] - ri[0];
+      }
+      const int pd = dzi - 4 + P.K[la] - 1;  // plan lag index of dz = dzi - 4
+      if (pd >= 0 && pd < P.GZ) out[((size_t)pd * NC + c) * NC + c2] = cf(re * inv, im * inv);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
 typedef CUresult (*LagEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -884,7 +1227,22 @@ int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
   float2* partA = (float2*)((char*)ws + pl.a_off);
   float2* partB = (float2*)((char*)ws + pl.b_off);
   int s;
-  if (pl.nA > 0) {
+  if (pl.nA > 0 && pl.tc) {
+    // tensor-core core class: amax of x, per-line operand tiles, then the MMA kernel
+    float* am = (float*)((char*)ws + pl.amax_off);
+    uint8_t* lines = (uint8_t*)ws + pl.prep_off;
+    int64_t n4 = pl.lines_all * P.N[P.L - 1] * NC / 2;  // float4 count of the k-space array
+    const int namax = (int)std::min<int64_t>(2 * hicu_sm_count(), std::max<int64_t>(1, (n4 + 255) / 256));
+    hicu_launch(lagtc_amax_kernel, namax, 256, 0, st, (const float4*)x, n4, am);
+    if ((s = hicu_check_launch("lagtc_amax_kernel"))) return s;
+    hicu_launch(lagtc_prep_kernel, (unsigned)pl.lines_all, 256, 0, st, P, x, (const float*)am, namax, lines);
+    if ((s = hicu_check_launch("lagtc_prep_kernel"))) return s;
+    const size_t smem = (size_t)kTcStages * kTcLineBytes + 1024;
+    hicu_allow_max_smem((const void*)lagtc_core_kernel);
+    hicu_launch(lagtc_core_kernel, (unsigned)pl.nA, kTcThreads, smem, st, P, (const uint8_t*)lines, (const float*)am,
+                namax, partA);
+    if ((s = hicu_check_launch("lagtc_core_kernel"))) return s;
+  } else if (pl.nA > 0) {
     bool done = false;
     if constexpr (NC == 8) {
       const int la = P.L - 1;

@@ -275,15 +275,18 @@ _PATH_FLAGS = 0
 
 
 @contextlib.contextmanager
-def kernel_paths(simt_conv: bool = False, simt_gram: bool = False, dense_gram: bool = False):
+def kernel_paths(simt_conv: bool = False, simt_gram: bool = False, dense_gram: bool = False,
+                 ffma_lag: bool = False):
     """Select the SIMT conv/scatter and/or Gram kernels even where the
-    tcgen05 kernels apply, or the dense implicit-im2col Gram instead of the
-    lag Gram (cross-checks and A/B timing).  Geometries built inside the
-    context carry the choice; the cache keys on it."""
+    tcgen05 kernels apply, the dense implicit-im2col Gram instead of the
+    lag Gram, or the CUDA-core lag Gram core instead of its tensor-core form
+    (cross-checks and A/B timing).  Geometries built inside the context
+    carry the choice; the cache keys on it."""
     global _PATH_FLAGS
     old = _PATH_FLAGS
     _PATH_FLAGS = ((nat.GEOM_FORCE_SIMT_CONV if simt_conv else 0) | (nat.GEOM_FORCE_SIMT_GRAM if simt_gram else 0)
-                   | (nat.GEOM_FORCE_DENSE_GRAM if (dense_gram or simt_gram) else 0))
+                   | (nat.GEOM_FORCE_DENSE_GRAM if (dense_gram or simt_gram) else 0)
+                   | (nat.GEOM_FORCE_FFMA_LAG if ffma_lag else 0))
     try:
         yield
     finally:

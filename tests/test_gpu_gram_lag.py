@@ -90,3 +90,28 @@ def test_lag_gram_c5_shard_accuracy():
     err = float((G - G64).abs().max() / G64.abs().max())
     print(f"lag Gram, C5 phantom shard {dims}: max rel err {err:.2e}")
     assert err <= 2e-6
+
+
+TC_CASES = [0, 1, 3, 4, 18]  # 8 coils, non-circular line axis <= 256 positions: the tensor-core core class
+
+
+@pytest.mark.parametrize("case", TC_CASES)
+def test_lag_gram_tensor_core_matches_cuda_core(case):
+    """The tcgen05 polyphase core class (lagtc_core_kernel, fp16 hi/lo
+    operands) and the CUDA-core FFMA2 core class give the same Gram (both
+    against the fp64 oracle)."""
+    dims, kext, frac, circ, sup = CASES[case]
+    rng = np.random.default_rng(300 + case)
+    x = c64(rng.standard_normal(dims) + 1j * rng.standard_normal(dims))
+    # a k-space-like dynamic range: one bright centre
+    x[tuple(d // 2 for d in dims[:-1])] *= 300.0
+    k = H.KernelMask.full(kext)
+    reg = H.stage_region(dims, k, frac, circ)
+    G_tc = gram_matrix(x, k, reg, path="lag").cpu().numpy()
+    with H.kernel_paths(ffma_lag=True):
+        G_ff = gram_matrix(x, k, reg, path="lag").cpu().numpy()
+    gm = O.stage_geom(dims, kext, frac, circ, None)
+    Gr = O.gram(x, gm)
+    assert rel(G_ff, Gr) <= 2e-6
+    assert rel(G_tc, Gr) <= 2e-6, rel(G_tc, Gr)
+    assert np.array_equal(G_tc, G_tc.conj().T)

@@ -1079,7 +1079,9 @@ lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict
         q1 = (int)(li % len[1]);
       }
       const int pa0 = beg[0] + q0, pa1 = beg[1] + q1;
-      const int pn0 = pa0 + P.ol_d[ol][0], pn1 = pa1 + P.ol_d[ol][1];
+      int pn0 = pa0 + P.ol_d[ol][0], pn1 = pa1 + P.ol_d[ol][1];
+      if (la >= 1 && P.circ[0]) pn0 = pn0 < 0 ? pn0 + (int)P.N[0] : (pn0 >= P.N[0] ? pn0 - (int)P.N[0] : pn0);
+      if (la >= 2 && P.circ[1]) pn1 = pn1 < 0 ? pn1 + (int)P.N[1] : (pn1 >= P.N[1] ? pn1 - (int)P.N[1] : pn1);
       const uint8_t* la_src = lines + lag_line_index(P, pa0, pa1) * kTcLineBytes;
       const uint8_t* lb_src = lines + lag_line_index(P, pn0, pn1) * kTcLineBytes + 16384;
       tc::mbar_wait(&empty[s], ph ^ 1);

@@ -92,7 +92,8 @@ def test_lag_gram_c5_shard_accuracy():
     assert err <= 2e-6
 
 
-TC_CASES = [0, 1, 3, 4, 18]  # 8 coils, non-circular line axis <= 256 positions: the tensor-core core class
+TC_CASES = [0, 1, 3, 4, 5, 18]  # 8 coils, non-circular line axis <= 256 positions: the tensor-core core class
+# (case 5: circular time as an OUTER axis -- the neighbour lines wrap)
 
 
 @pytest.mark.parametrize("case", TC_CASES)

@@ -132,6 +132,16 @@ __device__ __forceinline__ bool group_valid(const CtParams& P, const int (&ga)[k
   return ok;
 }
 
+// bitmask of the prefix groups that reach line lc (all groups for the conv)
+template <int MODE>
+__device__ __forceinline__ uint64_t line_groups(const CtParams& P, const int (&ga)[kMaxGroups][2], const int (&lc)[2]) {
+  if (MODE < 2) return P.ng >= 64 ? ~0ull : ((1ull << P.ng) - 1ull);
+  uint64_t m = 0;
+  for (int g = 0; g < P.ng; ++g)
+    if (group_valid<MODE>(P, ga, g, lc)) m |= 1ull << g;
+  return m;
+}
+
 template <int MODE>
 __device__ __forceinline__ bool line_active(const CtParams& P, const int (&ga)[kMaxGroups][2], const int (&lc)[2]) {
   if (MODE < 2) return true;
@@ -151,26 +161,43 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 // Scatter epilogue for one k-space position, coils 4h..4h+3 (one half of the
 // 8 coils): data consistency + the four partial sums (|g|^2, |res|^2,
 // <g,res>, |g|^2 on observed).
-__device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[8],
-                                              const uint8_t* __restrict__ mask, const float2* __restrict__ y,
-                                              const float2* __restrict__ x0, float2* __restrict__ gout,
-                                              double (&acc)[4]) {
+// DC inputs of one k-space position (coils 4h..4h+3): loaded before the
+// tile's accumulators are ready, so the global-load latency overlaps the MMAs
+struct DcIn {
+  uint32_t mm;
+  float4 y[2], x[2];
+};
+
+__device__ __forceinline__ DcIn dc_load(const CtParams& P, size_t e0, int h, const uint8_t* __restrict__ mask,
+                                        const float2* __restrict__ y, const float2* __restrict__ x0) {
   const size_t e = e0 + 4 * h;
-  uint8_t mk[4] = {0, 0, 0, 0};
-  if (P.dc_mode != 2) {
-    const uint32_t mm = *reinterpret_cast<const uint32_t*>(mask + e);
+  DcIn d;
+  d.mm = P.dc_mode != 2 ? __ldg(reinterpret_cast<const uint32_t*>(mask + e)) : 0u;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) mk[c] = (uint8_t)(mm >> (8 * c));
+  for (int c2 = 0; c2 < 2; ++c2) {
+    d.y[c2] = d.x[c2] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (P.dc_mode == 1) {
+      d.y[c2] = __ldg(reinterpret_cast<const float4*>(y + e) + c2);
+      d.x[c2] = __ldg(reinterpret_cast<const float4*>(x0 + e) + c2);
+    }
   }
+  return d;
+}
+
+// Scatter epilogue for one k-space position, coils 4h..4h+3 (one half of the
+// 8 coils): data consistency + the four partial sums (|g|^2, |res|^2,
+// <g,res>, |g|^2 on observed).
+__device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[8],
+                                              const DcIn& d, float2* __restrict__ gout, double (&acc)[4]) {
+  const size_t e = e0 + 4 * h;
+  uint8_t mk[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) mk[c] = (uint8_t)(d.mm >> (8 * c));
   float4* gp = reinterpret_cast<float4*>(gout + e);
 #pragma unroll
   for (int c2 = 0; c2 < 2; ++c2) {
     float a[4] = {v[4 * c2], v[4 * c2 + 1], v[4 * c2 + 2], v[4 * c2 + 3]};
-    float4 yy = make_float4(0.f, 0.f, 0.f, 0.f), xx = yy;
-    if (P.dc_mode == 1) {
-      yy = reinterpret_cast<const float4*>(y + e)[c2];
-      xx = reinterpret_cast<const float4*>(x0 + e)[c2];
-    }
+    const float4 yy = d.y[c2], xx = d.x[c2];
     const float yv[4] = {yy.x, yy.y, yy.z, yy.w}, xv[4] = {xx.x, xx.y, xx.z, xx.w};
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
@@ -257,24 +284,6 @@ __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, con
     }
 }
 
-// Stage sequence shared by every role: lines blockIdx.x, +gridDim.x, ...;
-// 128-row chunks; prefix groups that reach the line (all for the conv).
-template <int MODE>
-__device__ __forceinline__ bool stage_next(const CtParams& P, const int (&ga)[kMaxGroups][2], int& line, int& c,
-                                           int& g, int (&lc)[2]) {
-  for (;;) {
-    if (++g >= P.ng) {
-      g = 0;
-      if (++c >= P.chunks) {
-        c = 0;
-        line += gridDim.x;
-        if (line >= P.nlines) return false;
-        decode_line(P, line, lc);
-      }
-    }
-    if (group_valid<MODE>(P, ga, g, lc)) return true;
-  }
-}
 
 // MODE 0: conv forward (u, obj); 1: conv ELS (Re<w,u>, |w|^2); 2: scatter + DC.
 // BS: B images streamed per stage (they do not fit next to the pipeline).
@@ -358,9 +367,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     // warp-uniform loop (loop state in uniform registers); one elected lane issues
     int s = 0;
     uint32_t ph = 0;
-    int line = blockIdx.x, c = 0, g = -1, lc[2];
-    decode_line(P, line, lc);
-    while (line < P.nlines && stage_next<MODE>(P, ga, line, c, g, lc)) {
+    for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
+     int lc[2];
+     decode_line(P, line, lc);
+     const uint64_t gm = line_groups<MODE>(P, ga, lc);
+     for (int c = 0; c < P.chunks; ++c)
+     for (int g = 0; g < ng; ++g) {
+      if (!((gm >> g) & 1ull)) continue;
       const long long t0p = (pf && lane == 0) ? clock64() : 0;
       tc::mbar_wait(&empty[s], ph ^ 1);
       if (pf && lane == 0) pc[0] += clock64() - t0p;
@@ -393,6 +406,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       }
       __syncwarp();
       if (++s == S) { s = 0; ph ^= 1; }
+     }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -408,12 +422,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
       int lc[2];
       decode_line(P, line, lc);
-      if (!line_active<MODE>(P, ga, lc)) continue;
+      const uint64_t gm = line_groups<MODE>(P, ga, lc);
+      if (!gm) continue;
       for (int c = 0; c < P.chunks; ++c) {
         const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
         int vi = 0, set = 0;  // valid-group index within the tile; accumulator set = vi % nacc (kept incrementally)
         for (int g = 0; g < ng; ++g) {
-          if (!group_valid<MODE>(P, ga, g, lc)) continue;
+          if (!((gm >> g) & 1ull)) continue;
           if (vi < P.nacc) {  // first use of this accumulator set in the tile: drained by the epilogue?
             const long long t0m = (pf && lane == 0) ? clock64() : 0;
             tc::mbar_wait(&tempty[tb * 3 + set], tph ^ 1);
@@ -475,14 +490,28 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       int64_t obase = 0;
       if (L >= 2) obase += (int64_t)lc[0] * P.ostride[0];
       if (L >= 3) obase += (int64_t)lc[1] * P.ostride[1];
-      const bool active = line_active<MODE>(P, ga, lc);
-      int nvalid = 0;
-      for (int gg = 0; gg < ng; ++gg) nvalid += group_valid<MODE>(P, ga, gg, lc) ? 1 : 0;
+      const uint64_t gm = line_groups<MODE>(P, ga, lc);
+      const bool active = gm != 0;
+      const int nvalid = __popcll(gm);
       if (active) {
         // carried rows start at zero (u rows before the line / k-space before the region)
         for (int i = et; i < nb * (kMaxNb - 1) * 16; i += kEpiWarps * 32) carry[i] = 0.f;
         epi_bar();
         for (int c = 0; c < P.chunks; ++c) {
+          // this tile's epilogue inputs from global memory, loaded before the accumulators are ready
+          DcIn din{};
+          float4 upre[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+          if (MODE == 2) {
+            const int x = P.roff[L - 1] + c * kTileM + m;
+            if (x < P.ext_last) din = dc_load(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, mask, y, x0);
+          } else if (MODE == 1) {
+            const int i_out = c * kTileM - (nb - 1) + m;
+            if (i_out >= 0 && i_out < P.ext_last) {
+              const float4* up = reinterpret_cast<const float4*>(uin + (size_t)(obase + (int64_t)i_out * P.lstride) * 8 + 4 * h);
+              upre[0] = __ldg(up);
+              upre[1] = __ldg(up + 1);
+            }
+          }
           long long t0e = (pf && et == 0) ? clock64() : 0;
           tc::mbar_wait(&tfull[tb], tph);
           if (pf && et == 0) {
@@ -503,15 +532,24 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           for (int a = 0; a < P.nacc; ++a) {
             if (a < nsets && !(P.debug & 8)) {
               const uint32_t ta = t0 + (uint32_t)(a * 32 * nb);
+              // two taps in flight per wait (A_hi B_hi + A_lo B_hi, and A_hi B_lo columns)
 #pragma unroll
-              for (int b = 0; b < kMaxNb; ++b) {
+              for (int b = 0; b < kMaxNb; b += 2) {
                 if (b < nb) {
-                  uint32_t v0[8], v1[8];
-                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b), v0);            // A_hi B_hi + A_lo B_hi
-                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1);  // A_hi B_lo
+                  uint32_t v0[2][8], v1[2][8];
+                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b), v0[0]);
+                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1[0]);
+                  if (b + 1 < nb) {
+                    tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b + 16), v0[1]);
+                    tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b + 16), v1[1]);
+                  }
                   tc::tmem_wait_ld();
 #pragma unroll
-                  for (int i = 0; i < 8; ++i) f[b][i] += __uint_as_float(v0[i]) + __uint_as_float(v1[i]);
+                  for (int i = 0; i < 8; ++i) f[b][i] += __uint_as_float(v0[0][i]) + __uint_as_float(v1[0][i]);
+                  if (b + 1 < nb) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) f[b + 1][i] += __uint_as_float(v0[1][i]) + __uint_as_float(v1[1][i]);
+                  }
                 }
               }
             }
@@ -519,7 +557,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&tempty[tb * 3 + a]);
           }
-          if (pf && et == 0) pc[7] += clock64() - t0e;
+          if (pf && et == 0) {
+            const long long t1e = clock64();
+            pc[7] += t1e - t0e;
+            t0e = t1e;
+          }
           if (nbuf == 2) {
             tb ^= 1;
             if (tb == 0) tph ^= 1;
@@ -527,6 +569,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             tph ^= 1;
           }
           // shifted sums, one tap at a time: conv row m takes D[m + b - (nb-1), b]
+          // (pc[10]: window time, pc[11]: output time of the counter mode)
           // (window row m + b), scatter row m takes D[m - b, b] (window row nb-1+m-b)
           float v[8];
 #pragma unroll
@@ -556,6 +599,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
               epi_bar();
             }
           }
+          if (pf && et == 0) {
+            const long long t1e = clock64();
+            pc[10] += t1e - t0e;
+            t0e = t1e;
+          }
           if (MODE < 2) {
             const int i_out = c * kTileM - (nb - 1) + m;
             if (i_out < 0 || i_out >= P.ext_last) continue;
@@ -574,11 +622,10 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
               }
               acc_v[0] += s0 + s1;
             } else {
-              const float4* up = reinterpret_cast<const float4*>(uin + (size_t)idx * 8 + 4 * h);
               double d0 = 0.0, d1 = 0.0, n0 = 0.0, n1 = 0.0;
 #pragma unroll
               for (int i = 0; i < 2; ++i) {
-                const float4 uu = up[i];
+                const float4 uu = upre[i];
                 d0 += (double)v[4 * i] * uu.x + (double)v[4 * i + 1] * uu.y;
                 d1 += (double)v[4 * i + 2] * uu.z + (double)v[4 * i + 3] * uu.w;
               }
@@ -594,7 +641,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             const int x = P.roff[L - 1] + c * kTileM + m;
             if (x >= P.ext_last) continue;
             double a4[4] = {0, 0, 0, 0};
-            scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, v, mask, y, x0, out, a4);
+            scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, v, din, out, a4);
 #pragma unroll
             for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
           }
@@ -608,7 +655,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
         for (int x = m; x < P.ext_last; x += kTileM) {
           if (x >= x_lo && x < x_hi) continue;
           double a4[4] = {0, 0, 0, 0};
-          scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, vz, mask, y, x0, out, a4);
+          const size_t e0 = (size_t)(obase + (int64_t)x * P.lstride) * 8;
+          scatter_store(P, e0, h, vz, dc_load(P, e0, h, mask, y, x0), out, a4);
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
         }
@@ -637,7 +685,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     tc::fence_after();
     tc::tmem_dealloc(tmem, 512);
   }
-  if (pf && threadIdx.x == 0 && MODE == 0) {
+  if (pf && threadIdx.x == 0 && MODE != 1) {
     pc[9] -= pc[8];
     long long* o = reinterpret_cast<long long*>(out) + (size_t)blockIdx.x * 12;
     for (int i = 0; i < 12; ++i) o[i] = pc[i];

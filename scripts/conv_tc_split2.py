@@ -84,7 +84,11 @@ if out["debug"] & 32:
     hint(None, 0)
     torch.cuda.synchronize()
     pcs = u.view(torch.int64).flatten()[: 148 * 12].view(148, 12).double().mean(0).tolist()
-    names = ["prod_wait_empty", "conv_wait_full", "conv_work", "mma_wait_ready", "mma_wait_tempty", "mma_issue",
-             "epi_wait_tfull", "epi_drain", "start", "total", "x", "y"]
-    out["conv_fwd_cycles"] = {n: round(v) for n, v in zip(names, pcs) if n not in ("start", "x", "y")}
+    names = ["prod_wait_empty", "conv_wait_full", "conv_work", "mma_wait_full", "mma_wait_tempty", "mma_issue",
+             "epi_wait_tfull", "epi_drain", "start", "total", "epi_window", "y"]
+    out["conv_fwd_cycles"] = {n: round(v) for n, v in zip(names, pcs) if n not in ("start", "y", "conv_wait_full", "conv_work")}
+    calls["scatter_hard"]()
+    torch.cuda.synchronize()
+    pcs = gout.view(torch.int64).flatten()[: 148 * 12].view(148, 12).double().mean(0).tolist()
+    out["scatter_cycles"] = {n: round(v) for n, v in zip(names, pcs) if n not in ("start", "y", "conv_wait_full", "conv_work")}
 print(json.dumps(out), flush=True)

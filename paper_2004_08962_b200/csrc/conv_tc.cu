@@ -68,7 +68,8 @@ constexpr int kTileM = 128;
 constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
 constexpr int kMaxTaps = 128;              // spatial taps
-constexpr int kAStage = kTileM * 64;      // 8 KB: one 128-row A tile, rows [16 fp16 hi | 16 fp16 lo]
+constexpr int kATile = kTileM * 64;       // 8 KB: one 128-row A tile, rows [16 fp16 hi | 16 fp16 lo]
+constexpr int kAStage = 2 * kATile;        // a stage carries two prefix groups (adjacent lines: one TMA box)
 constexpr int kMaxStages = 16;
 constexpr int kWinRow = 20;                // floats per window row (16 + 4: conflict-free float4 rows)
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each owning 8 of the 16 output floats
@@ -85,7 +86,7 @@ struct CtParams {
   int stages;
   int tbuf_stride;        // TMEM columns between the two accumulator buffers (0: one buffer)
   int nacc;               // accumulator sets per tile (prefix groups dealt round-robin; shortens chains)
-  int stage_bytes;        // fp32 A + A hi + A lo (+ one prefix group's B image when streamed)
+  int stage_bytes;        // two A tiles (+ the two prefix groups' B images when streamed)
   int dc_mode;
   float lam;
   int nparts_total;       // entries of `parts` (per value) the ABI promised
@@ -104,6 +105,8 @@ struct CtParams {
   int64_t lstride;        // output stride (rows / positions) along the line axis
   const float* amax;      // max |A component| partials (amax_kernel) -> the A scale
   int namax;
+  int k1;                 // extent of the innermost prefix axis (pairs of groups never straddle it)
+  int abox;               // bytes of one stage's A box (two 8 KB tiles, one when L == 1)
 };
 
 __device__ __forceinline__ void decode_line(const CtParams& P, int line, int (&lc)[2]) {
@@ -363,8 +366,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
   if (pf && threadIdx.x == 0) pc[8] = clock64();
 
   if (warp == 0) {
-    // ---------------- TMA producer: fp32 A tile (+ the group's B image when streamed) ----------------
-    // warp-uniform loop (loop state in uniform registers); one elected lane issues
+    // ---------------- TMA producer: two prefix groups' A tiles per stage (+ their B images when streamed) ----------------
+    // warp-uniform loop (loop state in uniform registers); one elected lane issues.
+    // Groups g and g + 1 of one pair are adjacent lines along tensor dimension
+    // 2 (conv: c2 and c2 + 1; scatter: c2 and c2 - 1), so one TMA box of depth
+    // 2 loads both (scatter: tile 0 = group g + 1).
     int s = 0;
     uint32_t ph = 0;
     for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
@@ -372,8 +378,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
      decode_line(P, line, lc);
      const uint64_t gm = line_groups<MODE>(P, ga, lc);
      for (int c = 0; c < P.chunks; ++c)
-     for (int g = 0; g < ng; ++g) {
-      if (!((gm >> g) & 1ull)) continue;
+     for (int g = 0, t1 = 0; g < ng; ) {
+      const int cnt = t1 + 1 < P.k1 ? 2 : 1;  // pairs never straddle the outer prefix axis
+      const int g0 = g;
+      g += cnt;
+      t1 += cnt;
+      if (t1 >= P.k1) t1 = 0;
+      if (!((gm >> g0) & (cnt == 2 ? 3ull : 1ull))) continue;
       const long long t0p = (pf && lane == 0) ? clock64() : 0;
       tc::mbar_wait(&empty[s], ph ^ 1);
       if (pf && lane == 0) pc[0] += clock64() - t0p;
@@ -381,27 +392,31 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       int c1, c2 = 0, c3 = 0;
       if (MODE < 2) {
         c1 = P.roff[L - 1] + c * kTileM;
-        if (L == 2) c2 = P.roff[0] + lc[0] + ga[g][0];
+        if (L == 2) c2 = P.roff[0] + lc[0] + ga[g0][0];
         if (L == 3) {
-          c2 = P.roff[1] + lc[1] + ga[g][1];
-          c3 = P.roff[0] + lc[0] + ga[g][0];
+          c2 = P.roff[1] + lc[1] + ga[g0][1];
+          c3 = P.roff[0] + lc[0] + ga[g0][0];
         }
       } else {
         c1 = c * kTileM;
-        if (L == 2) c2 = lc[0] - P.roff[0] - ga[g][0];
+        if (L == 2) c2 = lc[0] - P.roff[0] - ga[g0][0];
         if (L == 3) {
-          c2 = lc[1] - P.roff[1] - ga[g][1];
-          c3 = lc[0] - P.roff[0] - ga[g][0];
+          c2 = lc[1] - P.roff[1] - ga[g0][1];
+          c3 = lc[0] - P.roff[0] - ga[g0][0];
         }
+        if (cnt == 2) c2 -= 1;
       }
       if (tc::elect_one()) {
         if (P.debug & 2) {
           tc::mbar_arrive(&full[s]);
         } else {
           uint8_t* dst = sStage + (size_t)s * stb;
-          tc::mbar_expect_tx(&full[s], kAStage + (BS ? gbytes : 0u));
+          tc::mbar_expect_tx(&full[s], (uint32_t)P.abox + (BS ? (uint32_t)cnt * gbytes : 0u));
           tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
-          if (BS) bulk_g2s(dst + kAStage, P.bimg + (size_t)g * gbytes, gbytes, &full[s]);
+          if (BS) {
+            bulk_g2s(dst + kAStage, P.bimg + (size_t)g0 * gbytes, gbytes, &full[s]);
+            if (cnt == 2) bulk_g2s(dst + kAStage + gbytes, P.bimg + (size_t)(g0 + 1) * gbytes, gbytes, &full[s]);
+          }
         }
       }
       __syncwarp();
@@ -427,31 +442,45 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       for (int c = 0; c < P.chunks; ++c) {
         const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
         int vi = 0, set = 0;  // valid-group index within the tile; accumulator set = vi % nacc (kept incrementally)
-        for (int g = 0; g < ng; ++g) {
-          if (!((gm >> g) & 1ull)) continue;
-          if (vi < P.nacc) {  // first use of this accumulator set in the tile: drained by the epilogue?
-            const long long t0m = (pf && lane == 0) ? clock64() : 0;
-            tc::mbar_wait(&tempty[tb * 3 + set], tph ^ 1);
-            if (pf && lane == 0) pc[4] += clock64() - t0m;
-          }
+        for (int g = 0, t1 = 0; g < ng; ) {
+          const int cnt = t1 + 1 < P.k1 ? 2 : 1;
+          const int g0 = g;
+          g += cnt;
+          t1 += cnt;
+          if (t1 >= P.k1) t1 = 0;
+          const uint32_t pv = (uint32_t)((gm >> g0) & (cnt == 2 ? 3ull : 1ull));  // valid groups of the pair
+          if (!pv) continue;
           const long long t0r = (pf && lane == 0) ? clock64() : 0;
-          tc::mbar_wait(&full[s], ph);  // A tile (+ streamed B image) landed
+          tc::mbar_wait(&full[s], ph);  // A tiles (+ streamed B images) landed
           if (pf && lane == 0) pc[3] += clock64() - t0r;
-          tc::fence_after();
-          const uint64_t da = dstage0 + (uint64_t)(s * stb16);
-          const uint64_t db = BS ? da + (uint64_t)(kAStage >> 4) : dimg0 + (uint64_t)(g * g16);
-          const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
-          const uint32_t acc = vi >= P.nacc ? 1u : 0u;
-          ++vi;
-          if (++set == P.nacc) set = 0;
-          const long long t0i = (pf && lane == 0) ? clock64() : 0;
-          if (tc::elect_one()) {
-            if (!(P.debug & 1)) {
-              tc::mma_f16(d, da, db, idesc_cat, acc);         // A_hi [B_hi; B_lo]  (K step 0 of the 64-B rows)
-              tc::mma_f16(d, da + 2, db, idesc_hi, 1);       // + A_lo B_hi        (K step 1: +32 B)
+          const uint64_t dst = dstage0 + (uint64_t)(s * stb16);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            if (!((pv >> j) & 1u)) continue;
+            if (vi < P.nacc) {  // first use of this accumulator set in the tile: drained by the epilogue?
+              const long long t0m = (pf && lane == 0) ? clock64() : 0;
+              tc::mbar_wait(&tempty[tb * 3 + set], tph ^ 1);
+              if (pf && lane == 0) pc[4] += clock64() - t0m;
             }
-            tc::mma_commit(&empty[s]);
+            tc::fence_after();
+            // tile of group g0 + j: conv j, scatter (pair) 1 - j
+            const int tile = (MODE == 2 && cnt == 2) ? 1 - j : j;
+            const uint64_t da = dst + (uint64_t)((tile * kATile) >> 4);
+            const uint64_t db = BS ? dst + (uint64_t)((kAStage + j * (int)gbytes) >> 4) : dimg0 + (uint64_t)((g0 + j) * g16);
+            const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
+            const uint32_t acc = vi >= P.nacc ? 1u : 0u;
+            ++vi;
+            if (++set == P.nacc) set = 0;
+            if (tc::elect_one()) {
+              if (!(P.debug & 1)) {
+                tc::mma_f16(d, da, db, idesc_cat, acc);         // A_hi [B_hi; B_lo]  (K step 0 of the 64-B rows)
+                tc::mma_f16(d, da + 2, db, idesc_hi, 1);       // + A_lo B_hi        (K step 1: +32 B)
+              }
+            }
+            __syncwarp();
           }
+          const long long t0i = (pf && lane == 0) ? clock64() : 0;
+          if (tc::elect_one()) tc::mma_commit(&empty[s]);
           __syncwarp();
           if (pf && lane == 0) pc[5] += clock64() - t0i;
           if (++s == S) { s = 0; ph ^= 1; }
@@ -876,7 +905,8 @@ int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, cons
   cuuint64_t dims[4] = {32, (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
                         (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
   cuuint64_t strides[3] = {64, 64 * dims[1], 64 * dims[1] * dims[2]};
-  cuuint32_t box[4] = {32, (cuuint32_t)kTileM, 1, 1}, es[4] = {1, 1, 1, 1};
+  // depth 2 along dimension 2: a stage's two prefix groups are adjacent lines
+  cuuint32_t box[4] = {32, (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? 2 : 1), 1}, es[4] = {1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -986,7 +1016,7 @@ bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
     sh->fixed = res_fixed;
   } else {
     sh->bstream = 1;
-    sh->stage = kAStage + (size_t)nb * 1024;
+    sh->stage = kAStage + 2 * (size_t)nb * 1024;
     sh->fixed = win + 1024;
   }
   return sh->fixed + 3 * sh->stage <= (size_t)kSmemBudget;
@@ -1150,6 +1180,8 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
   P.amax = reinterpret_cast<const float*>(scr);
   P.namax = namax;
   P.stage_bytes = (int)sh.stage;
+  P.k1 = L == 3 ? sh.kpre[1] : sh.ng;
+  P.abox = L >= 2 ? 2 * kATile : kATile;
   P.bimg = bimg;
   P.bimg_early = bimg_early;
   if (sh.bstream)

@@ -1187,6 +1187,113 @@ lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict
   }
 }
 
+// Edge classes of the tensor-core geometries (8 coils, non-circular line
+// axis, K <= 5 along it, N >= 4K - 4 positions per line): one CTA per (outer
+// lag, chunk of lpcB lines of one outer class block), 288 threads = (edge
+// position e, last-axis lag dz, coil block cbi).  Lines are staged 32 at a
+// time in shared memory -- the edge positions of the base lines and the
+// positions [0, 2K-2) and [N-2K+2, N) of the neighbour lines, each a row of 8
+// coils; consecutive lines of a block row are adjacent in memory, so every
+// staging load is a coalesced run of 64-byte rows (the per-thread
+// gathers of lag_edge_kernel were latency-bound).  Same partial layout as
+// lag_edge_kernel.
+constexpr int kE2Lines = 32;
+constexpr int kE2Threads = 288;
+
+__global__ void __launch_bounds__(kE2Threads)
+lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
+  hicu_pdl_entry();
+  constexpr int NC = 8, CB = 2;
+  const int la = P.L - 1;
+  const int K = P.K[la];
+  const int W = 3 * K - 3;          // neighbour window of one edge group: (K - 1) edges x (2K - 1) lags
+  const int NR = 2 * W;             // staged neighbour positions (left and right edge groups)
+  const int lo_base = P.cls_beg[la][P.edge_cls[0]] - (K - 1);          // first left edge - (K - 1)
+  const int hi_base = P.cls_beg[la][P.edge_cls[K - 1]] - (K - 1);      // first right edge - (K - 1)
+  const int NL = (int)P.N[la];
+  extern __shared__ __align__(16) uint8_t e2sm[];
+  float2 (*sL)[8][NC] = reinterpret_cast<float2 (*)[8][NC]>(e2sm);                          // base-line edge positions
+  float2 (*sR)[24][NC] = reinterpret_cast<float2 (*)[24][NC]>(e2sm + kE2Lines * 8 * NC * 8);  // neighbour positions
+  __shared__ int64_t sbase[kE2Lines], snbr[kE2Lines];
+  const int bidx = blockIdx.x;
+  const int ol = bidx / P.CBt;
+  const int chunk = bidx % P.CBt;  // global chunk id over blocks
+  int b = 0;
+  while (P.chunksB[b + 1] <= chunk) ++b;
+  const int ch = chunk - P.chunksB[b];
+  int beg[2], len[2];
+  block_ranges(P, b, beg, len);
+  const int64_t nlines = (int64_t)len[0] * len[1];
+  const int64_t l0 = (int64_t)ch * P.lpcB, l1 = min(nlines, l0 + P.lpcB);
+  const bool ok = neighbour_ok(P, beg, len, ol);
+  const int t = threadIdx.x;
+  const int q = t;  // (e * DZ + dz) * NCB + cbi
+  const bool qok = q < P.NQ;
+  const int e = q / (P.DZ * P.NCB), dzi = (q / P.NCB) % P.DZ, cbi = q % P.NCB;
+  const int dz = dzi - (K - 1);
+  const int pe = qok ? P.cls_beg[la][P.edge_cls[e]] : 0;
+  const int pr = pe + dz;
+  const bool act = ok && qok && pr >= 0 && pr < NL;
+  const int ridx = e < K - 1 ? pr - lo_base : W + pr - hi_base;
+  float2 accR[CB][NC], accI[CB][NC];
+#pragma unroll
+  for (int a = 0; a < CB; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) accR[a][c] = accI[a][c] = cf(0.f, 0.f);
+  const int64_t ls = P.cstride[la];
+  if (ok) {
+    for (int64_t lb = l0; lb < l1; lb += kE2Lines) {
+      const int nl = (int)min((int64_t)kE2Lines, l1 - lb);
+      __syncthreads();  // the previous sub-chunk's reads are done
+      if (t < nl) line_offsets(P, beg, len, ol, lb + t, sbase[t], snbr[t]);
+      __syncthreads();
+      // stage: 16-byte pieces; consecutive threads -> the pieces of one position
+      // row across consecutive lines (adjacent 64-byte rows in memory)
+      const int per = 4 * nl;
+      for (int i = t; i < (P.NE + NR) * per; i += kE2Threads) {
+        const int r = i / per, rem = i - r * per, j = rem >> 2, pc4 = rem & 3;
+        if (r < P.NE) {
+          const int pos = P.cls_beg[la][P.edge_cls[r]];
+          reinterpret_cast<float4*>(&sL[j][r][0])[pc4] =
+              __ldg(reinterpret_cast<const float4*>(x + sbase[j] + pos * ls) + pc4);
+        } else {
+          const int k = r - P.NE;
+          const int pos = k < W ? lo_base + k : hi_base + k - W;
+          reinterpret_cast<float4*>(&sR[j][k][0])[pc4] =
+              (pos >= 0 && pos < NL) ? __ldg(reinterpret_cast<const float4*>(x + snbr[j] + pos * ls) + pc4)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      __syncthreads();
+      if (act) {
+        for (int j = 0; j < nl; ++j) {
+          float2 a[CB], bv[NC];
+#pragma unroll
+          for (int u = 0; u < CB; ++u) a[u] = sL[j][e][cbi * CB + u];
+#pragma unroll
+          for (int c = 0; c < NC; ++c) bv[c] = sR[j][ridx][c];
+#pragma unroll
+          for (int u = 0; u < CB; ++u)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+              accR[u][c] = __ffma2_rn(make_float2(a[u].x, a[u].x), bv[c], accR[u][c]);
+              accI[u][c] = __ffma2_rn(make_float2(a[u].y, a[u].y), bv[c], accI[u][c]);
+            }
+        }
+      }
+    }
+  }
+  if (!qok) return;
+  // conj(a) b = (accR.x + accI.y, accR.y - accI.x); lag_edge_kernel's partial layout
+  const int qb = q / P.QB, tq = q % P.QB;
+  float2* out = part + ((((size_t)ol * P.NQB + qb) * P.CBt + chunk) * P.QB + tq) * CB * NC;
+#pragma unroll
+  for (int u = 0; u < CB; ++u)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      out[u * NC + c] = act ? cf(accR[u][c].x + accI[u][c].y, accR[u][c].y - accI[u][c].x) : cf(0.f, 0.f);
+}
+
 typedef CUresult (*LagEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1265,7 +1372,12 @@ int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
       if ((s = hicu_check_launch("lag_core_kernel"))) return s;
     }
   }
-  if (pl.nB > 0) {
+  if (pl.nB > 0 && pl.tc && P.NQ <= kE2Threads && P.NE == 2 * (P.K[P.L - 1] - 1)) {
+    hicu_allow_max_smem((const void*)lag_edge2_kernel);
+    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), kE2Threads, (size_t)kE2Lines * 32 * NC * 8, st, P, x,
+                partB);
+    if ((s = hicu_check_launch("lag_edge2_kernel"))) return s;
+  } else if (pl.nB > 0) {
     hicu_allow_max_smem((const void*)lag_edge_kernel<NC, CB>);
     hicu_launch(lag_edge_kernel<NC, CB>, (unsigned)pl.nB, kEdgeThreads, pl.smemB, st, P, x, partB);
     if ((s = hicu_check_launch("lag_edge_kernel"))) return s;

@@ -187,6 +187,10 @@ int hicu_gram_uses_tensor_cores(const hicu_geom* g);
  * n < 400 (measured faster at the 5x5x8 kernels of C1/C2) unless
  * HICU_GEOM_FORCE_LAG_GRAM; -1 on a bad geometry. */
 int hicu_gram_path(const hicu_geom* g);
+/* 1 when the lag Gram runs its core class on the tcgen05 kernels for this
+ * geometry (8 coils, non-circular line axis of <= 256 positions, <= 5 taps
+ * along it; fp16 hi/lo operands, HICU_GEOM_FORCE_FFMA_LAG not set). */
+int hicu_gram_lag_uses_tensor_cores(const hicu_geom* g);
 /* Real flops hicu_gram executes for this geometry on its path (lag: the
  * fp32 lag-correlation products; dense: 4 s n (n+1)); -1 on a bad geometry. */
 double hicu_gram_flops(const hicu_geom* g);

@@ -95,6 +95,7 @@ _SIGS = {
                                 c_void_p]),
     "hicu_gram_workspace": (c_size_t, [_GP]),
     "hicu_gram_uses_tensor_cores": (c_int, [_GP]),
+    "hicu_gram_lag_uses_tensor_cores": (c_int, [_GP]),
     "hicu_gram_path": (c_int, [_GP]),
     "hicu_eigh_top_workspace": (c_size_t, [c_int, c_int]),
     "hicu_eigh_top": (c_int, [c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),

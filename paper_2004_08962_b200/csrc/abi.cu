@@ -197,6 +197,12 @@ extern "C" double hicu_gram_flops(const hicu_geom* hg) {
   return 4.0 * (double)g.s * g.n * (g.n + 1);  // dense Hermitian H^H H
 }
 
+extern "C" int hicu_gram_lag_uses_tensor_cores(const hicu_geom* hg) {
+  DevGeom g;
+  if (hicu_make_devgeom(hg, &g)) return 0;
+  return gram_path(hg, g) == HICU_GRAM_PATH_LAG && hicu_gram_lag_tc(g) ? 1 : 0;
+}
+
 extern "C" int hicu_gram_uses_tensor_cores(const hicu_geom* hg) {
   return hicu_gram_path(hg) == HICU_GRAM_PATH_TCGEN05 ? 1 : 0;
 }

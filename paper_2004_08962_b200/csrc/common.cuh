@@ -223,4 +223,5 @@ void hicu_allow_max_smem(const void* func);
 bool hicu_gram_lag_supported(const DevGeom& g);
 size_t hicu_gram_lag_workspace(const DevGeom& g);
 double hicu_gram_lag_flops(const DevGeom& g);
+bool hicu_gram_lag_tc(const DevGeom& g);
 int hicu_gram_lag(const DevGeom& g, const float2* x, double2* G, void* ws, size_t ws_bytes, cudaStream_t st);

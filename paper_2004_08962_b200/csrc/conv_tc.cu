@@ -814,6 +814,55 @@ __global__ void __launch_bounds__(256) split_kernel(const float4* __restrict__ x
   }
 }
 
+// The same split as a batched tiled transpose, for a line axis that is not
+// the array's fastest: the natural array is [A][Lx][B] rows (Lx = line
+// axis), the output [A][B][Lx].  A 32 x 32 tile of rows is read as 32 runs of
+// 32 contiguous rows (2 KB) and written as 32 runs of 32 contiguous rows, so
+// both directions are coalesced (the row-per-thread split_kernel reads rows a
+// plane apart).  Grid (ceil(B/32), ceil(Lx/32), A), 256 threads.
+constexpr int kTT = 32;
+constexpr int kTTPitch = kTT * 64 + 32;  // bytes per tile b-row (+32: 2-way instead of 8-way store conflicts)
+
+__global__ void __launch_bounds__(256) split_t_kernel(const float4* __restrict__ x, int64_t Lx, int64_t B,
+                                                      const float* __restrict__ amax, int namax,
+                                                      uint4* __restrict__ out) {
+  hicu_pdl_entry();
+  extern __shared__ __align__(16) uint8_t tt[];
+  __shared__ float s_sa;
+  if (threadIdx.x < 32) {
+    float m = 0.f;
+    for (int i = threadIdx.x; i < namax; i += 32) m = fmaxf(m, __ldg(amax + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) s_sa = pow2_scale(m);
+  }
+  __syncthreads();
+  const float sa = s_sa;
+  const int64_t b0 = (int64_t)blockIdx.x * kTT, l0 = (int64_t)blockIdx.y * kTT, a = blockIdx.z;
+  // read: piece i -> (lx_l = i >> 7, b_l = (i >> 2) & 31, pc = i & 3): runs of 32 rows along B
+  for (int i = threadIdx.x; i < kTT * kTT * 4; i += 256) {
+    const int lx_l = i >> 7, b_l = (i >> 2) & 31, pc = i & 3;
+    const int64_t lx = l0 + lx_l, b = b0 + b_l;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (lx < Lx && b < B) v = __ldg(x + ((a * Lx + lx) * B + b) * 4 + pc);
+    const float x0 = v.x * sa, x1 = v.y * sa, x2 = v.z * sa, x3 = v.w * sa;
+    const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+    uint8_t* row = tt + b_l * kTTPitch + lx_l * 64;
+    *reinterpret_cast<uint2*>(row + pc * 8) = make_uint2(h2u(h01), h2u(h23));
+    *reinterpret_cast<uint2*>(row + 32 + pc * 8) =
+        make_uint2(h2u(__floats2half2_rn(x0 - f01.x, x1 - f01.y)), h2u(__floats2half2_rn(x2 - f23.x, x3 - f23.y)));
+  }
+  __syncthreads();
+  // write: piece i -> (b_l = i >> 7, lx_l = (i >> 2) & 31, chunk = i & 3): runs of 32 rows along Lx
+  for (int i = threadIdx.x; i < kTT * kTT * 4; i += 256) {
+    const int b_l = i >> 7, lx_l = (i >> 2) & 31, ch = i & 3;
+    const int64_t lx = l0 + lx_l, b = b0 + b_l;
+    if (lx < Lx && b < B)
+      out[((a * B + b) * Lx + lx) * 4 + ch] = *reinterpret_cast<const uint4*>(tt + b_l * kTTPitch + lx_l * 64 + ch * 16);
+  }
+}
+
 // max |component| partials of an fp32 array (the A-operand scale of the next conv)
 __global__ void __launch_bounds__(256) amax_kernel(const float4* __restrict__ x, int64_t n4, float* __restrict__ part) {
   hicu_pdl_entry();
@@ -1172,10 +1221,23 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
       sp.istr[a] = st2;
       st2 *= aext[a];
     }
-    const int sb = (int)std::min<int64_t>(8 * hicu_sm_count(), std::max<int64_t>(1, (arows + 255) / 256));
-    hicu_launch(split_kernel, sb, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows, sp,
-                reinterpret_cast<const float*>(scr), namax, reinterpret_cast<uint4*>(scr + split_off));
-    if ((s = hicu_check_launch("split_kernel"))) return s;
+    const int la = perm[L - 1];  // the line axis (natural index)
+    int64_t A = 1, B = 1;
+    for (int a = 0; a < la; ++a) A *= aext[a];
+    for (int a = la + 1; a < L; ++a) B *= aext[a];
+    const int64_t Lx = aext[la];
+    if (B >= kTT && A <= 65535 && (Lx + kTT - 1) / kTT <= 65535) {
+      hicu_allow_max_smem((const void*)split_t_kernel);
+      const dim3 grid((unsigned)((B + kTT - 1) / kTT), (unsigned)((Lx + kTT - 1) / kTT), (unsigned)A);
+      hicu_launch(split_t_kernel, grid, 256, (size_t)kTT * kTTPitch, st, reinterpret_cast<const float4*>(asrc), Lx, B,
+                  reinterpret_cast<const float*>(scr), namax, reinterpret_cast<uint4*>(scr + split_off));
+      if ((s = hicu_check_launch("split_t_kernel"))) return s;
+    } else {
+      const int sb = (int)std::min<int64_t>(8 * hicu_sm_count(), std::max<int64_t>(1, (arows + 255) / 256));
+      hicu_launch(split_kernel, sb, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows, sp,
+                  reinterpret_cast<const float*>(scr), namax, reinterpret_cast<uint4*>(scr + split_off));
+      if ((s = hicu_check_launch("split_kernel"))) return s;
+    }
   }
   P.amax = reinterpret_cast<const float*>(scr);
   P.namax = namax;

@@ -1425,6 +1425,11 @@ double hicu_gram_lag_flops(const DevGeom& g) {
   return lines_pos * P.NC * P.NC * 8.0;
 }
 
+bool hicu_gram_lag_tc(const DevGeom& g) {
+  LagPlan pl = make_plan(g);
+  return pl.ok && pl.tc;
+}
+
 size_t hicu_gram_lag_workspace(const DevGeom& g) {
   LagPlan pl = make_plan(g);
   return pl.ok ? pl.bytes : 0;

@@ -69,7 +69,11 @@ constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
 constexpr int kMaxTaps = 128;              // spatial taps
 constexpr int kATile = kTileM * 64;       // 8 KB: one 128-row A tile, rows [16 fp16 hi | 16 fp16 lo]
-constexpr int kAStage = 2 * kATile;        // a stage carries two prefix groups (adjacent lines: one TMA box)
+#ifndef HICU_CONV_GPS
+#define HICU_CONV_GPS 5
+#endif
+constexpr int kGPS = HICU_CONV_GPS;        // prefix groups per pipeline stage (adjacent lines: one TMA box)
+constexpr int kAStage = kGPS * kATile;
 constexpr int kMaxStages = 16;
 constexpr int kWinRow = 20;                // floats per window row (16 + 4: conflict-free float4 rows)
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each owning 8 of the 16 output floats
@@ -379,12 +383,12 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
      const uint64_t gm = line_groups<MODE>(P, ga, lc);
      for (int c = 0; c < P.chunks; ++c)
      for (int g = 0, t1 = 0; g < ng; ) {
-      const int cnt = t1 + 1 < P.k1 ? 2 : 1;  // pairs never straddle the outer prefix axis
+      const int cnt = min(kGPS, P.k1 - t1);  // a stage's groups never straddle the outer prefix axis
       const int g0 = g;
       g += cnt;
       t1 += cnt;
       if (t1 >= P.k1) t1 = 0;
-      if (!((gm >> g0) & (cnt == 2 ? 3ull : 1ull))) continue;
+      if (!((gm >> g0) & ((1ull << cnt) - 1ull))) continue;
       const long long t0p = (pf && lane == 0) ? clock64() : 0;
       tc::mbar_wait(&empty[s], ph ^ 1);
       if (pf && lane == 0) pc[0] += clock64() - t0p;
@@ -404,7 +408,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           c2 = lc[1] - P.roff[1] - ga[g0][1];
           c3 = lc[0] - P.roff[0] - ga[g0][0];
         }
-        if (cnt == 2) c2 -= 1;
+        c2 -= cnt - 1;  // the box starts at the last group's line
       }
       if (tc::elect_one()) {
         if (P.debug & 2) {
@@ -414,8 +418,8 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           tc::mbar_expect_tx(&full[s], (uint32_t)P.abox + (BS ? (uint32_t)cnt * gbytes : 0u));
           tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
           if (BS) {
-            bulk_g2s(dst + kAStage, P.bimg + (size_t)g0 * gbytes, gbytes, &full[s]);
-            if (cnt == 2) bulk_g2s(dst + kAStage + gbytes, P.bimg + (size_t)(g0 + 1) * gbytes, gbytes, &full[s]);
+            for (int j = 0; j < cnt; ++j)
+              bulk_g2s(dst + kAStage + j * gbytes, P.bimg + (size_t)(g0 + j) * gbytes, gbytes, &full[s]);
           }
         }
       }
@@ -431,6 +435,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     const uint32_t idesc_cat = tc::idesc_f16(kTileM, 32 * nb), idesc_hi = tc::idesc_f16(kTileM, 16 * nb);
     // descriptors advance by address >> 4 in their low 14 bits (shared-memory addresses < 256 KB)
     const uint64_t dstage0 = tc::desc_sw64(tc::smem_u32(sStage)), dimg0 = tc::desc_sw32(tc::smem_u32(sB));
+    const uint64_t dstageb0 = tc::desc_sw32(tc::smem_u32(sStage));  // streamed B images: SW32 like the resident ones
     const uint32_t stb16 = (uint32_t)stb >> 4, g16 = gbytes >> 4;
     int s = 0, tb = 0;
     uint32_t ph = 0, tph = 0;
@@ -443,19 +448,19 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
         const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
         int vi = 0, set = 0;  // valid-group index within the tile; accumulator set = vi % nacc (kept incrementally)
         for (int g = 0, t1 = 0; g < ng; ) {
-          const int cnt = t1 + 1 < P.k1 ? 2 : 1;
+          const int cnt = min(kGPS, P.k1 - t1);
           const int g0 = g;
           g += cnt;
           t1 += cnt;
           if (t1 >= P.k1) t1 = 0;
-          const uint32_t pv = (uint32_t)((gm >> g0) & (cnt == 2 ? 3ull : 1ull));  // valid groups of the pair
+          const uint32_t pv = (uint32_t)((gm >> g0) & ((1ull << cnt) - 1ull));  // valid groups of the stage
           if (!pv) continue;
           const long long t0r = (pf && lane == 0) ? clock64() : 0;
           tc::mbar_wait(&full[s], ph);  // A tiles (+ streamed B images) landed
           if (pf && lane == 0) pc[3] += clock64() - t0r;
           const uint64_t dst = dstage0 + (uint64_t)(s * stb16);
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
+          for (int j = 0; j < kGPS; ++j) {
             if (!((pv >> j) & 1u)) continue;
             if (vi < P.nacc) {  // first use of this accumulator set in the tile: drained by the epilogue?
               const long long t0m = (pf && lane == 0) ? clock64() : 0;
@@ -463,10 +468,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
               if (pf && lane == 0) pc[4] += clock64() - t0m;
             }
             tc::fence_after();
-            // tile of group g0 + j: conv j, scatter (pair) 1 - j
-            const int tile = (MODE == 2 && cnt == 2) ? 1 - j : j;
+            // tile of group g0 + j: conv j, scatter cnt - 1 - j (its lines run backwards)
+            const int tile = MODE == 2 ? cnt - 1 - j : j;
             const uint64_t da = dst + (uint64_t)((tile * kATile) >> 4);
-            const uint64_t db = BS ? dst + (uint64_t)((kAStage + j * (int)gbytes) >> 4) : dimg0 + (uint64_t)((g0 + j) * g16);
+            const uint64_t db = BS ? dstageb0 + (uint64_t)(s * stb16) + (uint64_t)((kAStage + j * (int)gbytes) >> 4)
+                                   : dimg0 + (uint64_t)((g0 + j) * g16);
             const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
             const uint32_t acc = vi >= P.nacc ? 1u : 0u;
             ++vi;
@@ -954,8 +960,8 @@ int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, cons
   cuuint64_t dims[4] = {32, (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
                         (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
   cuuint64_t strides[3] = {64, 64 * dims[1], 64 * dims[1] * dims[2]};
-  // depth 2 along dimension 2: a stage's two prefix groups are adjacent lines
-  cuuint32_t box[4] = {32, (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? 2 : 1), 1}, es[4] = {1, 1, 1, 1};
+  // depth kGPS along dimension 2: a stage's prefix groups are adjacent lines
+  cuuint32_t box[4] = {32, (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? kGPS : 1), 1}, es[4] = {1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1057,15 +1063,15 @@ bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
   sh->kpre[1] = L >= 3 ? (int)g.kext[perm[1]] : 1;
   const size_t win = ((size_t)(kTileM + kMaxNb - 1) * kWinRow * 4 + (size_t)kMaxNb * (kMaxNb - 1) * 64 + 1023) &
                      ~(size_t)1023;
-  // resident B images when they fit next to >= 4 stages, else one group's image per stage
+  // resident B images when they fit next to >= 3 stages, else the stage groups' images per stage
   const size_t res_fixed = (size_t)ng * nb * 1024 + win + 1024;
-  if (res_fixed + 4 * (size_t)kAStage <= (size_t)kSmemBudget) {
+  if (res_fixed + 3 * (size_t)kAStage <= (size_t)kSmemBudget) {
     sh->bstream = 0;
     sh->stage = kAStage;
     sh->fixed = res_fixed;
   } else {
     sh->bstream = 1;
-    sh->stage = kAStage + 2 * (size_t)nb * 1024;
+    sh->stage = kAStage + kGPS * (size_t)nb * 1024;
     sh->fixed = win + 1024;
   }
   return sh->fixed + 3 * sh->stage <= (size_t)kSmemBudget;
@@ -1243,7 +1249,7 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
   P.namax = namax;
   P.stage_bytes = (int)sh.stage;
   P.k1 = L == 3 ? sh.kpre[1] : sh.ng;
-  P.abox = L >= 2 ? 2 * kATile : kATile;
+  P.abox = L >= 2 ? kGPS * kATile : kATile;
   P.bimg = bimg;
   P.bimg_early = bimg_early;
   if (sh.bstream)

@@ -12,6 +12,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace {
@@ -155,6 +157,139 @@ hetrd_kernel(int l, const double2* __restrict__ Ain, double2* __restrict__ Aws,
     __syncthreads();
   }
   if (tid == 0) d[l - 1] = A[(size_t)(l - 1) * lda + (l - 1)].x;
+}
+
+// Householder tridiagonalisation on a thread-block cluster (l in (96, 256]:
+// the C3 / C4 / C5 nullspace, l = 150 / 225 / 180).  One cluster of kHcCS
+// CTAs holds the matrix in distributed shared memory: row i lives in CTA
+// i % kHcCS (cyclic, so the shrinking trailing block stays balanced), at
+// most 32 rows x (l + 1) per CTA.  Per step k: the owner of row k forms the
+// reflector from conj(row k) (the matrix is Hermitian and both triangles are
+// updated) and writes v and tau into every CTA's shared memory; after a
+// cluster barrier each CTA forms y = A22 v for its rows, w = tau y, and
+// writes its w entries and its w^H v partial into every CTA; after a second
+// barrier each CTA updates its rows with the rank-2 term.  v, w, tau and the
+// partials are double-buffered by step parity, so a CTA still updating step k
+// never sees step k + 1's broadcasts.  Two cluster barriers per step instead
+// of the single-CTA kernel's L2 round trips over A22 (hetrd_kernel<false>
+// streams the whole trailing block from L2 twice per step).  Same outputs as
+// hetrd_kernel: d, e, tau, Vt.
+constexpr int kHcCS = 8;
+constexpr int kHcThreads = 512;
+constexpr int kHcMaxL = 256;
+
+__global__ void __cluster_dims__(kHcCS, 1, 1) __launch_bounds__(kHcThreads, 1)
+hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict__ d, double* __restrict__ e,
+                     double2* __restrict__ tau, double2* __restrict__ Vt) {
+  hicu_pdl_entry();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  extern __shared__ double2 hcA[];  // [nr][lda]
+  __shared__ double2 sv[2][kHcMaxL], sw[2][kHcMaxL];
+  __shared__ double2 pdot[2][kHcCS];
+  __shared__ double2 s_tau[2], s_scal;
+  __shared__ double2 redz[kHcThreads / 32];
+  const int lda = l + 1;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kHcThreads / 32;
+  const int nr = (l - cr + kHcCS - 1) / kHcCS;  // rows of this CTA: i = cr + kHcCS * r
+  for (int q = tid; q < nr * l; q += kHcThreads) {
+    const int r = q / l, j = q - r * l;
+    hcA[(size_t)r * lda + j] = Ain[(size_t)(cr + kHcCS * r) * l + j];
+  }
+  for (int q = cr * kHcThreads + tid; q < l * l; q += kHcCS * kHcThreads) Vt[q] = cd(0.0, 0.0);
+  cluster.sync();
+  for (int k = 0; k + 1 < l; ++k) {
+    const int buf = k & 1, k1 = k + 1, m = l - k1;
+    // ---- (a) the owner of row k forms the reflector and broadcasts v, tau ----
+    if (cr == k % kHcCS) {
+      const double2* row = hcA + (size_t)(k / kHcCS) * lda;
+      if (warp == 0) {
+        double t = 0.0;
+        for (int j = k + 2 + lane; j < l; j += 32) t += abs2d(row[j]);
+        t = warp_sum_d(t);
+        if (lane == 0) {
+          const double2 alpha = conjd(row[k1]);
+          double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
+          double beta;
+          if (t == 0.0 && alpha.y == 0.0) {
+            beta = alpha.x;  // H = I
+          } else {
+            beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + t), alpha.x);
+            const double ib = 1.0 / beta;
+            tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
+            const double2 den = cd(alpha.x - beta, alpha.y);
+            const double idd = 1.0 / abs2d(den);
+            scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
+          }
+          e[k] = beta;
+          d[k] = row[k].x;
+          tau[k] = tv;
+          s_scal = scal;
+          for (int c = 0; c < kHcCS; ++c) *cluster.map_shared_rank(&s_tau[buf], c) = tv;
+        }
+      }
+      __syncthreads();
+      const double2 sc = s_scal;
+      for (int q = tid; q < kHcCS * m; q += kHcThreads) {
+        const int c = q / m, j = k1 + (q - c * m);
+        const double2 v = j == k1 ? cd(1.0, 0.0) : cmul(conjd(row[j]), sc);
+        *cluster.map_shared_rank(&sv[buf][j], c) = v;
+        if (c == 0) Vt[(size_t)k * l + j] = v;
+      }
+    }
+    cluster.sync();  // v, tau everywhere
+    const double2 tk = s_tau[buf];
+    if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform over the cluster
+    // ---- (b) y = A22 v for this CTA's rows, w = tau y, broadcast w and w^H v ----
+    double2 pz = cd(0.0, 0.0);
+    for (int r = warp; r < nr; r += nw) {
+      const int i = cr + kHcCS * r;
+      if (i < k1) continue;
+      const double2* Ai = hcA + (size_t)r * lda;
+      double2 a0 = cd(0.0, 0.0), a1 = a0;
+      int j = k1 + lane;
+      for (; j + 32 < l; j += 64) {
+        zfma(a0, Ai[j], sv[buf][j]);
+        zfma(a1, Ai[j + 32], sv[buf][j + 32]);
+      }
+      if (j < l) zfma(a0, Ai[j], sv[buf][j]);
+      const double2 y = warp_sum_z(a0 + a1);
+      const double2 wv = cmul(tk, y);
+      if (lane < kHcCS) *cluster.map_shared_rank(&sw[buf][i], lane) = wv;
+      if (lane == 0) zfmac(pz, wv, sv[buf][i]);
+    }
+    if (lane == 0) redz[warp] = pz;
+    __syncthreads();
+    if (warp == 0) {
+      double2 t = lane < nw ? redz[lane] : cd(0.0, 0.0);
+      t = warp_sum_z(t);
+      if (lane < kHcCS) *cluster.map_shared_rank(&pdot[buf][cr], lane) = t;
+    }
+    cluster.sync();  // w and the partials everywhere
+    // ---- (c) rank-2 update of this CTA's rows: A22 -= v w'^H + w' v^H, w' = w + alpha2 v ----
+    double2 dot = cd(0.0, 0.0);
+#pragma unroll
+    for (int c = 0; c < kHcCS; ++c) dot = dot + pdot[buf][c];
+    const double2 td = cmul(tk, dot);
+    const double2 a2 = cd(-0.5 * td.x, -0.5 * td.y);
+    for (int r = warp; r < nr; r += nw) {
+      const int i = cr + kHcCS * r;
+      if (i < k1) continue;
+      const double2 vi = sv[buf][i];
+      const double2 wi = sw[buf][i] + cmul(a2, vi);
+      double2* Ai = hcA + (size_t)r * lda;
+      for (int j = k1 + lane; j < l; j += 32) {
+        const double2 vj = sv[buf][j];
+        const double2 wj = sw[buf][j] + cmul(a2, vj);
+        Ai[j] = Ai[j] - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
+      }
+    }
+    __syncthreads();  // the next owner reads its updated row
+  }
+  if (cr == (l - 1) % kHcCS && tid == 0) d[l - 1] = hcA[(size_t)((l - 1) / kHcCS) * lda + (l - 1)].x;
+  cluster.sync();  // no CTA exits while others may still write into its shared memory
 }
 
 // Latency-oriented variant for l <= kHetrd2Max (A resident in shared memory):
@@ -1171,6 +1306,11 @@ int hicu_heev_top(int l, int r, const double2* A, double* lam, double2* F, void*
       hicu_allow_max_smem((const void*)hetrd_kernel<true>);
       hicu_launch(hetrd_kernel<true>, 1, 1024, abytes, st, l, A, Aws, d, e, tau, Vt);
     }
+  } else if (l <= kHcMaxL) {
+    // distributed over a cluster (the matrix does not fit one SM's shared memory)
+    const size_t hsm = (size_t)((l + kHcCS - 1) / kHcCS) * (l + 1) * sizeof(double2);
+    hicu_allow_max_smem((const void*)hetrd_cluster_kernel);
+    hicu_launch(hetrd_cluster_kernel, kHcCS, kHcThreads, hsm, st, l, A, d, e, tau, Vt);
   } else {
     hicu_launch(hetrd_kernel<false>, 1, 1024, 0, st, l, A, Aws, d, e, tau, Vt);
   }

@@ -12,6 +12,8 @@
 //
 // All kernels are fp64; single-CTA kernels keep their matrix in shared
 // memory when it fits and fall back to a global workspace otherwise.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 #include <math.h>
@@ -211,6 +213,105 @@ chol_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, c
     Cg[e] = (j >= i) ? A[e] : cd(0.0, 0.0);
   }
   if (threadIdx.x == 0) *nu_out = s_nu;
+}
+
+// Cholesky on an 8-CTA cluster for ell > 96 when C does not fit one SM's
+// shared memory (C3 / C4 / C5: ell = 150 / 225 / 180).  Row i of the upper
+// triangle lives in CTA i % 8 (cyclic); per step the owner of row k takes
+// the pivot's square root, scales its row and writes it into every CTA's
+// shared memory (double-buffered by step parity); one cluster barrier; each
+// CTA folds row k into its rows.  Same arithmetic per element as chol_kernel
+// (A[i][j] -= conj(R[k][i]) R[k][j]); the shift escalation on a non-positive
+// pivot is decided identically by every CTA (the failing pivot's owner
+// broadcasts the flag with the row).
+constexpr int kCcCS = 8;
+constexpr int kCcThreads = 512;
+constexpr int kCcMaxL = 256;
+
+__global__ void __cluster_dims__(kCcCS, 1, 1) __launch_bounds__(kCcThreads, 1)
+chol_cluster_kernel(int ell, double2* __restrict__ Cg, const double2* __restrict__ Og, const double2* __restrict__ G,
+                    int n, double* __restrict__ nu_out, int* __restrict__ status) {
+  hicu_pdl_entry();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  extern __shared__ double2 ccA[];  // [nr][ell]
+  __shared__ double2 srow[2][kCcMaxL];
+  __shared__ int sfail[2];
+  __shared__ double s_scale;
+  __shared__ double wred[kCcThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kCcThreads / 32;
+  const int nr = (ell - cr + kCcCS - 1) / kCcCS;
+  {  // shift scale: trace(G) / n, summed warp-parallel in a fixed order (every CTA the same value)
+    double t = 0.0;
+    for (int i = tid; i < n; i += kCcThreads) t += G[(size_t)i * n + i].x;
+    t = warp_sum_d_(t);
+    if (lane == 0) wred[warp] = t;
+    __syncthreads();
+    if (tid == 0) {
+      double tr = 0.0;
+      for (int w = 0; w < nw; ++w) tr += wred[w];
+      s_scale = tr > 0.0 ? tr / n : 1.0;
+    }
+    __syncthreads();
+  }
+  double nu = 0.0;
+  bool failed = false;
+  for (int attempt = 0; attempt < 12; ++attempt) {
+    for (int q = tid; q < nr * ell; q += kCcThreads) {
+      const int r = q / ell, j = q - r * ell;
+      const size_t gi = (size_t)(cr + kCcCS * r) * ell + j;
+      ccA[q] = Cg[gi] + nu * Og[gi];
+    }
+    if (tid < 2) sfail[tid] = 0;
+    cluster.sync();
+    failed = false;
+    for (int k = 0; k < ell; ++k) {
+      const int buf = k & 1;
+      if (cr == k % kCcCS) {
+        double2* row = ccA + (size_t)(k / kCcCS) * ell;
+        const double dg = row[k].x;
+        const bool bad = !(dg > 0.0) || !isfinite(dg);
+        if (bad) {
+          if (tid < kCcCS) *cluster.map_shared_rank(&sfail[buf], tid) = 1;
+        } else {
+          const double rs = sqrt(dg), inv = 1.0 / rs;
+          for (int q = tid; q < kCcCS * (ell - k); q += kCcThreads) {
+            const int c = q / (ell - k), j = k + (q - c * (ell - k));
+            const double2 v = j == k ? cd(rs, 0.0) : inv * row[j];
+            *cluster.map_shared_rank(&srow[buf][j], c) = v;
+          }
+          __syncthreads();  // every thread has read the unscaled row
+          for (int j = k + tid; j < ell; j += kCcThreads) row[j] = srow[buf][j];
+        }
+      }
+      cluster.sync();
+      if (sfail[buf]) {
+        failed = true;
+        break;
+      }
+      // fold row k into this CTA's rows i > k (upper triangle j >= i)
+      for (int r = warp; r < nr; r += nw) {
+        const int i = cr + kCcCS * r;
+        if (i <= k) continue;
+        const double2 a = srow[buf][i];
+        double2* Ai = ccA + (size_t)r * ell;
+        for (int j = i + lane; j < ell; j += 32) Ai[j] = Ai[j] - cmulc(a, srow[buf][j]);
+      }
+      __syncthreads();  // the next owner reads its updated row
+    }
+    if (!failed) break;
+    nu = nu == 0.0 ? 1e-14 * s_scale : nu * 100.0;
+    cluster.sync();  // every CTA has seen the failure before the flags are cleared
+    if (attempt == 11 && cr == 0 && tid == 0) *status = HICU_ERR_DEGENERATE_INPUT;
+  }
+  for (int q = tid; q < nr * ell; q += kCcThreads) {
+    const int r = q / ell, j = q - r * ell, i = cr + kCcCS * r;
+    Cg[(size_t)i * ell + j] = j >= i ? ccA[q] : cd(0.0, 0.0);
+  }
+  if (cr == 0 && tid == 0) *nu_out = nu;
+  cluster.sync();
 }
 
 // Register-resident variant (ell <= 96): row i of the upper triangle lives
@@ -1340,6 +1441,11 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     } else if (sm) {
       hicu_allow_max_smem((const void*)chol_kernel<true>);
       hicu_launch(chol_kernel<true>, 1, 512, bytes, st, ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
+    } else if (ell <= kCcMaxL) {
+      const size_t csm = (size_t)((ell + kCcCS - 1) / kCcCS) * ell * sizeof(double2);
+      hicu_allow_max_smem((const void*)chol_cluster_kernel);
+      hicu_launch(chol_cluster_kernel, kCcCS, kCcThreads, csm, st, ell, w.C, (const double2*)w.O, Gp, n, w.nu,
+                  status_dev);
     } else {
       hicu_launch(chol_kernel<false>, 1, 512, 0, st, ell, w.C, w.O, Gp, n, w.scratch, w.nu, status_dev);
     }

@@ -25,8 +25,10 @@
 //                     one warp per (last-axis lag, coil block), lanes over
 //                     positions, an Nc x CB register block of accumulators;
 //   lag_edge_kernel   the short last-axis classes (edge positions);
-//   lag_reduce_kernel fixed-order fp64 sums of the chunk partials -> T;
-//   lag_assemble_kernel  G from T (Hermitian by construction).
+//   lag_reduceU_kernel fixed-order fp64 sums of the chunk partials, folded
+//                     over the line-axis classes containing each tap;
+//   lag_axis_kernel   the same containment sum over each outer axis;
+//   lag_gather_kernel G from the per-(lag, tap) table (Hermitian by construction).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -99,6 +101,8 @@ struct LagPlan {
   size_t prep_off = 0, amax_off = 0;  // tensor path: per-line operand tiles, amax partials
   int64_t lines_all = 0;
   int64_t nT = 0;   // complex entries of T
+  int64_t nU = 0, nV = 0, nW = 0;  // containment-sum tables (U: line axis, V: + axis 1, W: all axes)
+  size_t u_off = 0, v_off = 0, w_off = 0;
   int64_t nA = 0, nB = 0;  // CTAs
   size_t smemA = 0, smemB = 0;
   int threadsA = 0;
@@ -281,12 +285,23 @@ LagPlan make_plan(const DevGeom& g) {
     pl.nB = (int64_t)p.nol * p.NQB * p.CBt;
     pl.smemB = (size_t)p.QB * p.CB * p.NC * sizeof(float2);
   }
-  pl.nT = (int64_t)p.nol * p.DZ * p.NB * p.NCL * p.NC * p.NC;
+  pl.nT = 0;  // T is never stored: lag_reduceU folds the line-axis classes directly
   auto al = [](size_t v) { return (v + 255) & ~(size_t)255; };
   pl.t_off = 0;
-  pl.a_off = al(pl.nT * sizeof(double2));
+  pl.a_off = 0;
   pl.b_off = pl.a_off + al((size_t)pl.nA * p.GZ * p.NC * p.NC * sizeof(float2));
   pl.bytes = pl.b_off + al((size_t)pl.nB * p.QB * p.CB * p.NC * sizeof(float2));
+  {
+    const int NC2 = p.NC * p.NC, KL = p.K[la];
+    const int K0 = la >= 1 ? p.K[0] : 1, K1 = la >= 2 ? p.K[1] : 1;
+    pl.nU = (int64_t)p.nol * p.DZ * p.NB * KL * NC2;
+    pl.nV = la >= 2 ? (int64_t)p.nol * p.DZ * p.ncls[0] * K1 * KL * NC2 : 0;
+    pl.nW = (int64_t)p.nol * p.DZ * K0 * K1 * KL * NC2;
+    pl.u_off = al(pl.bytes);
+    pl.v_off = pl.u_off + al(pl.nU * sizeof(double2));
+    pl.w_off = pl.v_off + al(pl.nV * sizeof(double2));
+    pl.bytes = pl.w_off + al(pl.nW * sizeof(double2));
+  }
   if (pl.tc) {
     pl.lines_all = 1;
     for (int a = 0; a < la; ++a) pl.lines_all *= p.N[a];
@@ -594,56 +609,95 @@ lag_edge_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ 
   }
 }
 
-// T[((ol * DZ + dz) * NB + b) * NCL + cls][c][c'] = fixed-order fp64 sum of the chunk partials
-__global__ void lag_reduce_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ partA,
-                                  const float2* __restrict__ partB, double2* __restrict__ T, int64_t total) {
+// Containment sums (replace lag_reduce + lag_assemble's per-entry loop over
+// every cell that contains the tap: up to (K)^3 = 125 T reads per G entry at
+// C4/C5).  G[(t,c),(t+d,c')] = sum over cells containing t of T[d][cell] is
+// separable over the axes, so it is formed axis by axis:
+//   U[ol][dz][b][tl]        = sum_{line class kl contains tl} T[ol][dz][b][kl]   (lag_reduceU: T never stored)
+//   V[ol][dz][k0][t1][tl]   = sum_{k1 contains t1} U[ol][dz][k0*n1+k1][tl]       (two outer axes)
+//   W[ol][dz][t0][t1][tl]   = sum_{k0 contains t0} V (or U with one outer axis)
+// and the G entries are a gather from W.  Fixed summation order: deterministic.
+__global__ void lag_reduceU_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ partA,
+                                   const float2* __restrict__ partB, double2* __restrict__ U, int64_t total) {
   hicu_pdl_entry();
-  const int NC = P.NC, NC2 = NC * NC;
+  const int NC = P.NC, NC2 = NC * NC, la = P.L - 1, KL = P.K[la];
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int cc = (int)(idx % NC2);
     int64_t r = idx / NC2;
-    const int cls = (int)(r % P.NCL);
-    r /= P.NCL;
     const int b = (int)(r % P.NB);
     r /= P.NB;
     const int dz = (int)(r % P.DZ);
     const int ol = (int)(r / P.DZ);
     const int c = cc / NC, c2 = cc % NC;
-    double sx = 0.0, sy = 0.0;
-    if (cls == P.core_cls) {
-      const int gzi = dz / P.GZ, dzi = dz % P.GZ;
-      const int64_t nlg = (int64_t)P.nol * P.NG;
-      const int64_t bid0 = (int64_t)P.chunksA[b] * nlg + (int64_t)ol * P.NG + gzi;
-      const int nch = P.chunksA[b + 1] - P.chunksA[b];
-      for (int ch = 0; ch < nch; ++ch) {
-        const float2 v = partA[((bid0 + ch * nlg) * P.GZ + dzi) * NC2 + cc];
-        sx += v.x;
-        sy += v.y;
+    double2 u[kMaxK];
+#pragma unroll
+    for (int t = 0; t < kMaxK; ++t) u[t] = cd(0.0, 0.0);
+    for (int cls = 0; cls < P.NCL; ++cls) {
+      double sx = 0.0, sy = 0.0;
+      if (cls == P.core_cls) {
+        const int gzi = dz / P.GZ, dzi = dz % P.GZ;
+        const int64_t nlg = (int64_t)P.nol * P.NG;
+        const int64_t bid0 = (int64_t)P.chunksA[b] * nlg + (int64_t)ol * P.NG + gzi;
+        const int nch = P.chunksA[b + 1] - P.chunksA[b];
+        for (int ch = 0; ch < nch; ++ch) {
+          const float2 v = partA[((bid0 + ch * nlg) * P.GZ + dzi) * NC2 + cc];
+          sx += v.x;
+          sy += v.y;
+        }
+      } else {
+        int e = 0;
+        while (e < P.NE && P.edge_cls[e] != cls) ++e;
+        const int cbi = c / P.CB, t = c % P.CB;
+        const int q = (e * P.DZ + dz) * P.NCB + cbi;
+        const int qb = q / P.QB, tq = q % P.QB;
+        const int64_t bid0 = ((int64_t)ol * P.NQB + qb) * P.CBt + P.chunksB[b];
+        const int nch = P.chunksB[b + 1] - P.chunksB[b];
+        for (int ch = 0; ch < nch; ++ch) {
+          const float2 v = partB[(((bid0 + ch) * P.QB + tq) * P.CB + t) * NC + c2];
+          sx += v.x;
+          sy += v.y;
+        }
       }
-    } else {
-      int e = 0;
-      while (e < P.NE && P.edge_cls[e] != cls) ++e;
-      const int cbi = c / P.CB, t = c % P.CB;
-      const int q = (e * P.DZ + dz) * P.NCB + cbi;
-      const int qb = q / P.QB, tq = q % P.QB;
-      const int64_t bid0 = ((int64_t)ol * P.NQB + qb) * P.CBt + P.chunksB[b];
-      const int nch = P.chunksB[b + 1] - P.chunksB[b];
-      for (int ch = 0; ch < nch; ++ch) {
-        const float2 v = partB[(((bid0 + ch) * P.QB + tq) * P.CB + t) * NC + c2];
-        sx += v.x;
-        sy += v.y;
-      }
+#pragma unroll
+      for (int tl = 0; tl < kMaxK; ++tl)
+        if (tl < KL && tl >= P.cls_lo[la][cls] && tl <= P.cls_hi[la][cls]) u[tl] = u[tl] + cd(sx, sy);
     }
-    T[idx] = cd(sx, sy);
+    double2* o = U + (((int64_t)(ol * P.DZ + dz) * P.NB + b) * KL) * NC2 + cc;
+    for (int tl = 0; tl < KL; ++tl) o[(int64_t)tl * NC2] = u[tl];
   }
 }
 
-// G[i][j] = sum over the cells containing tap t_i of T[d = t_j - t_i][cell][c_i][c_j]
-// (lexicographically negative d, or d = 0 with c_i > c_j: conj of the mirrored entry)
-__global__ void lag_assemble_kernel(const __grid_constant__ LagParams P, const double2* __restrict__ T,
-                                    const int32_t* __restrict__ pos, int ndim, int n, double2* __restrict__ G) {
+// one outer axis reduction: out[pre][t][post] = sum_{k contains t} in[pre][k][post]
+// (pre = (ol, dz) [x k0 for the inner outer axis], post = taps of later axes x NC^2)
+__global__ void lag_axis_kernel(const __grid_constant__ LagParams P, int axis, int64_t npre, int nk, int64_t npost,
+                                const double2* __restrict__ in, double2* __restrict__ out) {
+  hicu_pdl_entry();
+  const int K = P.K[axis];
+  const int64_t total = npre * K * npost;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t post = idx % npost;
+    int64_t r = idx / npost;
+    const int t = (int)(r % K);
+    const int64_t pre = r / K;
+    double sx = 0.0, sy = 0.0;
+    const double2* src = in + pre * nk * npost + post;
+    for (int k = 0; k < nk; ++k) {
+      if (t < P.cls_lo[axis][k] || t > P.cls_hi[axis][k]) continue;
+      const double2 v = src[(int64_t)k * npost];
+      sx += v.x;
+      sy += v.y;
+    }
+    out[idx] = cd(sx, sy);
+  }
+}
+
+// G[i][j] = W[ol][dz][t0][t1][tl][c][c'] of the lexicographically non-negative
+// lag (mirrored entries: the conjugate); real diagonal.
+__global__ void lag_gather_kernel(const __grid_constant__ LagParams P, const double2* __restrict__ W,
+                                  const int32_t* __restrict__ pos, int ndim, int n, double2* __restrict__ G) {
   hicu_pdl_entry();
   const int L = P.L, la = L - 1, NC = P.NC;
+  const int K0 = la >= 1 ? P.K[0] : 1, K1 = la >= 2 ? P.K[1] : 1, KL = P.K[la];
   const int64_t total = (int64_t)n * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(idx / n), j = (int)(idx % n);
@@ -665,24 +719,10 @@ __global__ void lag_assemble_kernel(const __grid_constant__ LagParams P, const d
     const int i0 = la >= 1 ? d[0] + P.K[0] - 1 : 0, i1 = la >= 2 ? d[1] + P.K[1] - 1 : 0;
     const int ol = P.ol_index[i0][i1];
     const int dz = d[la] + P.K[la] - 1;
-    double sx = 0.0, sy = 0.0;
-    const int n0 = la >= 1 ? P.ncls[0] : 1, n1 = la >= 2 ? P.ncls[1] : 1;
-    for (int k0 = 0; k0 < n0; ++k0) {
-      if (la >= 1 && (t[0] < P.cls_lo[0][k0] || t[0] > P.cls_hi[0][k0])) continue;
-      for (int k1 = 0; k1 < n1; ++k1) {
-        if (la >= 2 && (t[1] < P.cls_lo[1][k1] || t[1] > P.cls_hi[1][k1])) continue;
-        const int b = k0 * n1 + k1;
-        const double2* Tb = T + ((((int64_t)ol * P.DZ + dz) * P.NB + b) * P.NCL) * NC * NC + (size_t)c * NC + c2;
-        for (int kl = 0; kl < P.NCL; ++kl) {
-          if (t[la] < P.cls_lo[la][kl] || t[la] > P.cls_hi[la][kl]) continue;
-          const double2 v = Tb[(size_t)kl * NC * NC];
-          sx += v.x;
-          sy += v.y;
-        }
-      }
-    }
-    if (i == j) sy = 0.0;
-    G[idx] = cd(sx, mirror ? -sy : sy);
+    const int t0 = la >= 1 ? t[0] : 0, t1 = la >= 2 ? t[1] : 0;
+    const double2 v =
+        W[((((int64_t)(ol * P.DZ + dz) * K0 + t0) * K1 + t1) * KL + t[la]) * NC * NC + (int64_t)c * NC + c2];
+    G[idx] = cd(v.x, i == j ? 0.0 : (mirror ? -v.y : v.y));
   }
 }
 
@@ -891,10 +931,6 @@ lag_core_tma_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constan
 // while the epilogue drains the other into fp32 registers.
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ uint32_t lag_h2(float a, float b) {
-  const __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 __device__ __forceinline__ float lag_pow2_scale(float amax) {
   if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
@@ -1455,16 +1491,35 @@ int hicu_gram_lag(const DevGeom& g, const float2* x, double2* G, void* ws, size_
     default: return hicu_set_error(HICU_ERR_PARAMETER, "gram_lag: coil count");
   }
   if (s) return s;
-  double2* T = (double2*)((char*)ws + pl.t_off);
   const float2* partA = (const float2*)((char*)ws + pl.a_off);
   const float2* partB = (const float2*)((char*)ws + pl.b_off);
+  const LagParams& P = pl.p;
+  const int la = P.L - 1, NC2 = P.NC * P.NC, KL = P.K[la];
+  double2* U = (double2*)((char*)ws + pl.u_off);
+  double2* V = (double2*)((char*)ws + pl.v_off);
+  double2* W = (double2*)((char*)ws + pl.w_off);
+  auto blocks_for = [](int64_t n) { return (int)std::min<int64_t>((n + 255) / 256, (int64_t)hicu_sm_count() * 16); };
   {
-    const int blocks = (int)std::min<int64_t>((pl.nT + 255) / 256, (int64_t)hicu_sm_count() * 16);
-    hicu_launch(lag_reduce_kernel, blocks, 256, 0, st, pl.p, partA, partB, T, pl.nT);
-    if ((s = hicu_check_launch("lag_reduce_kernel"))) return s;
+    const int64_t nU = pl.nU / NC2 * NC2;
+    hicu_launch(lag_reduceU_kernel, blocks_for(nU), 256, 0, st, P, partA, partB, U, (int64_t)P.nol * P.DZ * P.NB * NC2);
+    if ((s = hicu_check_launch("lag_reduceU_kernel"))) return s;
+  }
+  const int64_t od = (int64_t)P.nol * P.DZ;
+  if (la == 2) {  // axis 1: U[od][k0][k1][tl] -> V[od][k0][t1][tl]
+    hicu_launch(lag_axis_kernel, blocks_for(pl.nV), 256, 0, st, P, 1, od * P.ncls[0], P.ncls[1], (int64_t)KL * NC2,
+                (const double2*)U, V);
+    if ((s = hicu_check_launch("lag_axis_kernel"))) return s;
+    hicu_launch(lag_axis_kernel, blocks_for(pl.nW), 256, 0, st, P, 0, od, P.ncls[0], (int64_t)P.K[1] * KL * NC2,
+                (const double2*)V, W);
+    if ((s = hicu_check_launch("lag_axis_kernel"))) return s;
+  } else if (la == 1) {  // axis 0: U[od][k0][tl] -> W[od][t0][tl]
+    hicu_launch(lag_axis_kernel, blocks_for(pl.nW), 256, 0, st, P, 0, od, P.ncls[0], (int64_t)KL * NC2,
+                (const double2*)U, W);
+    if ((s = hicu_check_launch("lag_axis_kernel"))) return s;
+  } else {
+    W = U;  // one spatial axis: NB = 1
   }
   const int64_t total = (int64_t)g.n * g.n;
-  const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)hicu_sm_count() * 16);
-  hicu_launch(lag_assemble_kernel, blocks, 256, 0, st, pl.p, (const double2*)T, g.pos, g.ndim, g.n, G);
-  return hicu_check_launch("lag_assemble_kernel");
+  hicu_launch(lag_gather_kernel, blocks_for(total), 256, 0, st, P, (const double2*)W, g.pos, g.ndim, g.n, G);
+  return hicu_check_launch("lag_gather_kernel");
 }

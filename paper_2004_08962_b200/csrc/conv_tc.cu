@@ -65,6 +65,7 @@
 namespace {
 
 constexpr int kTileM = 128;
+constexpr int kAmaxSlot = 512;             // entries of a producer's max partials (consumers read all of them)
 constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
 constexpr int kMaxTaps = 128;              // spatial taps
@@ -109,6 +110,7 @@ struct CtParams {
   int64_t lstride;        // output stride (rows / positions) along the line axis
   const float* amax;      // max |A component| partials (amax_kernel) -> the A scale
   int namax;
+  float* amax_out;        // optional: per-CTA max |output component| (conv: u, scatter: g), zero-filled to kAmaxSlot
   int k1;                 // extent of the innermost prefix axis (pairs of groups never straddle it)
   int abox;               // bytes of one stage's A box (two 8 KB tiles, one when L == 1)
 };
@@ -194,8 +196,9 @@ __device__ __forceinline__ DcIn dc_load(const CtParams& P, size_t e0, int h, con
 // Scatter epilogue for one k-space position, coils 4h..4h+3 (one half of the
 // 8 coils): data consistency + the four partial sums (|g|^2, |res|^2,
 // <g,res>, |g|^2 on observed).
-__device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[8],
-                                              const DcIn& d, float2* __restrict__ gout, double (&acc)[4]) {
+__device__ __forceinline__ float scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[8],
+                                               const DcIn& d, float2* __restrict__ gout, double (&acc)[4]) {
+  float mx = 0.f;
   const size_t e = e0 + 4 * h;
   uint8_t mk[4];
 #pragma unroll
@@ -225,9 +228,11 @@ __device__ __forceinline__ void scatter_store(const CtParams& P, size_t e0, int 
       acc[0] += (double)ar * ar + (double)ai * ai;
       a[2 * hh] = ar;
       a[2 * hh + 1] = ai;
+      mx = fmaxf(mx, fmaxf(fabsf(ar), fabsf(ai)));
     }
     gp[c2] = make_float4(a[0], a[1], a[2], a[3]);
   }
+  return mx;
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -517,6 +522,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     double acc_v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc_v[i] = 0.0;
+    float omax = 0.f;  // max |output component| of this thread (producer max partials)
     int tb = 0;
     uint32_t tph = 0;
     for (int line = blockIdx.x; line < P.nlines; line += gridDim.x) {
@@ -654,6 +660,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
               for (int i = 0; i < 8; i += 2) {
                 s0 += (double)v[i] * v[i];
                 s1 += (double)v[i + 1] * v[i + 1];
+                omax = fmaxf(omax, fmaxf(fabsf(v[i]), fabsf(v[i + 1])));
               }
               acc_v[0] += s0 + s1;
             } else {
@@ -676,7 +683,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             const int x = P.roff[L - 1] + c * kTileM + m;
             if (x >= P.ext_last) continue;
             double a4[4] = {0, 0, 0, 0};
-            scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, v, din, out, a4);
+            omax = fmaxf(omax, scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, v, din, out, a4));
 #pragma unroll
             for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
           }
@@ -691,7 +698,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           if (x >= x_lo && x < x_hi) continue;
           double a4[4] = {0, 0, 0, 0};
           const size_t e0 = (size_t)(obase + (int64_t)x * P.lstride) * 8;
-          scatter_store(P, e0, h, vz, dc_load(P, e0, h, mask, y, x0), out, a4);
+          omax = fmaxf(omax, scatter_store(P, e0, h, vz, dc_load(P, e0, h, mask, y, x0), out, a4));
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
         }
@@ -712,6 +719,21 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     }
     if (blockIdx.x == 0)
       for (int i = et + (int)gridDim.x * NV; i < P.nparts_total * NV; i += kEpiWarps * 32) parts[i] = 0.0;
+    if (P.amax_out) {  // this CTA's max |output|; CTA 0 zero-fills the slot past the grid
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) omax = fmaxf(omax, __shfl_xor_sync(0xffffffffu, omax, o));
+      __shared__ float wmx[kEpiWarps];
+      if (lane == 0) wmx[ew] = omax;
+      epi_bar();
+      if (et == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < kEpiWarps; ++w) t = fmaxf(t, wmx[w]);
+        P.amax_out[blockIdx.x] = t;
+      }
+      if (blockIdx.x == 0)
+        for (int i = (int)gridDim.x + et; i < kAmaxSlot; i += kEpiWarps * 32) P.amax_out[i] = 0.f;
+    }
   }
   tc::fence_before();
   __syncthreads();
@@ -891,6 +913,8 @@ __global__ void __launch_bounds__(256) amax_kernel(const float4* __restrict__ x,
 
 thread_local const uint8_t* t_bimg = nullptr;
 thread_local int t_bimg_early = 0;
+thread_local const float* t_amax_in = nullptr;  // the A operand's max partials, written by its producer
+thread_local float* t_amax_out = nullptr;       // where this launch's epilogue writes its output's max partials
 
 // Per-(device, stream) scratch: amax partials and the B images of calls that
 // arrive without prebuilt ones.  Kernels on one stream run in order, so one
@@ -1003,6 +1027,30 @@ int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, co
   next = (next + 1) % 16;
   if (used < 16) ++used;
   return HICU_OK;
+}
+
+// Per-(device, stream) producer max slots (3 x kAmaxSlot floats), never
+// reallocated: a slot written by one call is read by a later call.
+float* stream_amax_slots(cudaStream_t st) {
+  struct Entry {
+    int dev;
+    cudaStream_t st;
+    float* p;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> entries;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : entries)
+    if (e.dev == dev && e.st == st) return e.p;
+  float* p = nullptr;
+  if (cudaMalloc(&p, 3 * kAmaxSlot * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  entries.push_back({dev, st, p});
+  return p;
 }
 
 // Tile ("line") axis: the spatial axis that minimises the 128-row tiles the
@@ -1143,6 +1191,10 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
   const uint8_t* bimg = t_bimg;
   int bimg_early = t_bimg_early;
   t_bimg = nullptr;
+  const float* amax_in = t_amax_in;
+  float* amax_out = t_amax_out;
+  t_amax_in = nullptr;
+  t_amax_out = nullptr;
   int perm[3];
   choose_perm(g, MODE, perm);
   Shape sh;
@@ -1212,9 +1264,16 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
     bimg = scr + img_off;
   }
   bimg_early = 1;  // the amax and split kernels always run between the image and this launch
-  hicu_launch(amax_kernel, namax, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows * 4,
-              reinterpret_cast<float*>(scr));
-  if ((s = hicu_check_launch("amax_kernel"))) return s;
+  const float* amax = reinterpret_cast<const float*>(scr);
+  int namax_used = namax;
+  if (amax_in) {  // the producer of the A operand wrote its max partials: no amax pass
+    amax = amax_in;
+    namax_used = kAmaxSlot;
+  } else {
+    hicu_launch(amax_kernel, namax, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows * 4,
+                reinterpret_cast<float*>(scr));
+    if ((s = hicu_check_launch("amax_kernel"))) return s;
+  }
   {
     SplitParams sp{};
     sp.L = L;
@@ -1236,17 +1295,18 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
       hicu_allow_max_smem((const void*)split_t_kernel);
       const dim3 grid((unsigned)((B + kTT - 1) / kTT), (unsigned)((Lx + kTT - 1) / kTT), (unsigned)A);
       hicu_launch(split_t_kernel, grid, 256, (size_t)kTT * kTTPitch, st, reinterpret_cast<const float4*>(asrc), Lx, B,
-                  reinterpret_cast<const float*>(scr), namax, reinterpret_cast<uint4*>(scr + split_off));
+                  amax, namax_used, reinterpret_cast<uint4*>(scr + split_off));
       if ((s = hicu_check_launch("split_t_kernel"))) return s;
     } else {
       const int sb = (int)std::min<int64_t>(8 * hicu_sm_count(), std::max<int64_t>(1, (arows + 255) / 256));
       hicu_launch(split_kernel, sb, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows, sp,
-                  reinterpret_cast<const float*>(scr), namax, reinterpret_cast<uint4*>(scr + split_off));
+                  amax, namax_used, reinterpret_cast<uint4*>(scr + split_off));
       if ((s = hicu_check_launch("split_kernel"))) return s;
     }
   }
-  P.amax = reinterpret_cast<const float*>(scr);
-  P.namax = namax;
+  P.amax = amax;
+  P.namax = namax_used;
+  P.amax_out = amax_out;
   P.stage_bytes = (int)sh.stage;
   P.k1 = L == 3 ? sh.kpre[1] : sh.ng;
   P.abox = L >= 2 ? kGPS * kATile : kATile;
@@ -1291,6 +1351,16 @@ int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, in
   }
   return HICU_OK;
 }
+
+// the next conv_tc launch on this host thread takes its A-operand scale from
+// the max partials `in` (kAmaxSlot floats written by the operand's producer)
+// instead of an amax pass, and writes its output's max partials to `out`
+void hicu_conv_tc_amax_hint(const float* in, float* out) {
+  t_amax_in = in;
+  t_amax_out = out;
+}
+
+float* hicu_conv_tc_amax_slots(cudaStream_t st) { return stream_amax_slots(st); }
 
 // the next conv_tc launch on this host thread copies its B image from `img`
 // (early: the image was written at least two kernels before that launch)

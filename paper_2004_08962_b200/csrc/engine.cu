@@ -9,6 +9,11 @@
 size_t hicu_conv_images_prepare(const hicu_geom* hg, const void* qt_all, int p, int G, void* ws, size_t ws_bytes,
                                 void* stream);
 void hicu_conv_image_hint(const void* img, int early);
+void hicu_conv_amax_hint(const float* in, float* out);
+float* hicu_conv_amax_slots(void* stream);
+int hicu_step_update_amax(int64_t N, void* y, const void* gdir, const double* obj_parts, int n_obj,
+                          const double* dc_parts, int n_dc, const double* els_parts, int n_els, int dc_mode,
+                          double lam, double* rec, float* amax_out, void* stream);
 int hicu_householder_gated(int n, int r, const void* V, double tol, void* refl, void* tau, int* flags, int* status_dev,
                            const int* gate, void* stream);
 int hicu_apply_reflectors_gated(int n, int r, const void* refl, const void* tau, const int* flags, int cols,
@@ -78,6 +83,16 @@ struct ImageHint {
   ~ImageHint() { hicu_conv_image_hint(nullptr, 0); }
 };
 
+// Operand-scale hint for the next tensor-core convolution on this thread:
+// the A operand's max partials (written by its producer) and where the
+// launch writes its own output's max partials; cleared when the scope ends.
+struct AmaxHint {
+  explicit AmaxHint(bool on, const float* in, float* out) {
+    if (on) hicu_conv_amax_hint(in, out);
+  }
+  ~AmaxHint() { hicu_conv_amax_hint(nullptr, nullptr); }
+};
+
 struct ProfScope {
   HicuProf* p;
   cudaStream_t st;
@@ -125,6 +140,14 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
   if (ncp < 0 || nsp < 0) return HICU_ERR_SHAPE;
   const size_t nomega = (size_t)n * ell, npbig = (size_t)n * G * p;
   int s;
+  // producer max partials (tensor-core convolutions): y from the update, u
+  // from the forward convolution, g from the scatter -- no amax pass per call
+  const bool tcv = hicu_conv_uses_tensor_cores(gm, p) == 1;
+  float* slots = tcv ? hicu_conv_amax_slots(stream) : nullptr;
+  float* sY = slots;
+  float* sU = slots ? slots + 512 : nullptr;
+  float* sG = slots ? slots + 1024 : nullptr;
+  bool y_valid = false;  // sY holds max |y| of the current y
   for (int it = 0; it < a->iters; ++it) {
     // ---- nullspace: Gram + Nystrom (== rSVD subspace), or injected V ----
     if (a->inject_v) {
@@ -168,11 +191,13 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
       {
         ProfScope ps(a->prof, HICU_PROF_CONV_FWD, st);
         ImageHint hint(ib ? imgs + (size_t)(2 * j) * ib : nullptr, j > 0 ? 1 : 0);
+        AmaxHint ah(slots != nullptr, y_valid ? sY : nullptr, sU);
         if ((s = hicu_conv_fwd(gm, a->y, qt, p, a->u, a->obj_parts, stream))) return s;
       }
       {
         ProfScope ps(a->prof, HICU_PROF_SCATTER, st);
         ImageHint hint(ib ? imgs + (size_t)(2 * j + 1) * ib : nullptr, 1);
+        AmaxHint ah(slots != nullptr, sU, sG);
         if ((s = hicu_scatter_dc(gm, qt, p, a->u, a->mask, a->y, a->x0, a->dc_mode, a->lam, a->g, a->dc_parts,
                                  stream)))
           return s;
@@ -180,13 +205,15 @@ extern "C" int hicu_run_stage(const hicu_stage_args* a, void* stream) {
       {
         ProfScope ps(a->prof, HICU_PROF_CONV_ELS, st);
         ImageHint hint(ib ? imgs + (size_t)(2 * j) * ib : nullptr, 1);
+        AmaxHint ah(slots != nullptr, sG, nullptr);
         if ((s = hicu_conv_els(gm, a->g, qt, p, a->u, a->els_parts, stream))) return s;
       }
       {
         ProfScope ps(a->prof, HICU_PROF_UPDATE, st);
-        if ((s = hicu_step_update(a->N, a->y, a->g, a->obj_parts, ncp, a->dc_parts, nsp, a->els_parts, ncp,
-                                  a->dc_mode, a->lam, rec, stream)))
+        if ((s = hicu_step_update_amax(a->N, a->y, a->g, a->obj_parts, ncp, a->dc_parts, nsp, a->els_parts, ncp,
+                                       a->dc_mode, a->lam, rec, sY, stream)))
           return s;
+        y_valid = sY != nullptr;
       }
       if (a->ref && a->ser_parts) {
         double* sp = a->ser_parts + ((size_t)it * G + j) * a->ser_stride;

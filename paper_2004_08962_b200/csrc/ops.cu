@@ -17,6 +17,8 @@ size_t hicu_conv_tc_bimage_bytes(const DevGeom& g, int p);
 int hicu_conv_tc_build_bimages(const DevGeom& g, const float2* qt_all, int p, int G, uint8_t* img, size_t ib,
                                cudaStream_t st);
 void hicu_conv_tc_bimage_hint(const void* img, int early);
+void hicu_conv_tc_amax_hint(const float* in, float* out);
+float* hicu_conv_tc_amax_slots(cudaStream_t st);
 int hicu_conv_tc(const DevGeom& g, const float2* y, const float2* qt, float2* u, double* parts, int mode,
                  int nparts_total, cudaStream_t st);
 int hicu_scatter_tc(const DevGeom& g, const float2* qt, const float2* u, const uint8_t* mask, const float2* y,
@@ -224,12 +226,30 @@ __device__ __forceinline__ double warp_sum_batched(const double* __restrict__ pa
   return t;
 }
 
+// this CTA's max |y component| into amax_out[blockIdx.x] (the next
+// convolution's operand scale); CTA 0 zero-fills the slot past the grid
+__device__ __forceinline__ void update_amax_store(float mx, float* __restrict__ amax_out) {
+  if (!amax_out) return;
+  __shared__ float wm[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t = fmaxf(t, wm[w]);
+    amax_out[blockIdx.x] = t;
+  }
+  if (blockIdx.x == 0)
+    for (int i = (int)gridDim.x + threadIdx.x; i < 512; i += blockDim.x) amax_out[i] = 0.f;
+}
+
 __global__ void __launch_bounds__(256)
 update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir,
               const double* __restrict__ obj_parts, int n_obj,
               const double* __restrict__ dc_parts, int n_dc,
               const double* __restrict__ els_parts, int n_els, int dc_mode, double lam,
-              double* __restrict__ rec, bool vec) {
+              double* __restrict__ rec, bool vec, float* __restrict__ amax_out) {
   hicu_pdl_entry();
   __shared__ double s_eta;
   __shared__ int s_skip;
@@ -277,8 +297,9 @@ update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir
     }
   }
   __syncthreads();
-  if (s_skip) return;
-  const float eta = (float)s_eta;
+  if (s_skip && !amax_out) return;
+  const float eta = s_skip ? 0.f : (float)s_eta;  // (a skipped step still reports max |y|)
+  float mx = 0.f;
   if (!vec) {  // operands not 16-byte aligned
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < N; m += (int64_t)gridDim.x * blockDim.x) {
       const float2 gv = gdir[m];
@@ -286,7 +307,9 @@ update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir
       yv.x = fmaf(-eta, gv.x, yv.x);
       yv.y = fmaf(-eta, gv.y, yv.y);
       y[m] = yv;
+      mx = fmaxf(mx, fmaxf(fabsf(yv.x), fabsf(yv.y)));
     }
+    update_amax_store(mx, amax_out);
     return;
   }
   // two complex elements per thread per pass (16-byte accesses)
@@ -314,6 +337,7 @@ update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir
         yv[u].z = fmaf(-eta, gv[u].z, yv[u].z);
         yv[u].w = fmaf(-eta, gv[u].w, yv[u].w);
         y4[m] = yv[u];
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(yv[u].x), fabsf(yv[u].y)), fmaxf(fabsf(yv[u].z), fabsf(yv[u].w))));
       }
     }
   }
@@ -323,7 +347,9 @@ update_kernel(int64_t N, float2* __restrict__ y, const float2* __restrict__ gdir
     yv.x = fmaf(-eta, gv.x, yv.x);
     yv.y = fmaf(-eta, gv.y, yv.y);
     y[N - 1] = yv;
+    mx = fmaxf(mx, fmaxf(fabsf(yv.x), fabsf(yv.y)));
   }
+  update_amax_store(mx, amax_out);
 }
 
 __global__ void ser_kernel(int64_t N, const float2* __restrict__ ref, const float2* __restrict__ y,
@@ -738,9 +764,22 @@ extern "C" int hicu_scatter_dc(const hicu_geom* hg, const void* qt, int p, const
                             (float2*)gout, dc_parts, s);
 }
 
+int hicu_step_update_amax(int64_t N, void* y, const void* gdir, const double* obj_parts, int n_obj,
+                          const double* dc_parts, int n_dc, const double* els_parts, int n_els, int dc_mode,
+                          double lam, double* rec, float* amax_out, void* stream);
+
 extern "C" int hicu_step_update(int64_t N, void* y, const void* gdir, const double* obj_parts, int n_obj,
                                 const double* dc_parts, int n_dc, const double* els_parts, int n_els,
                                 int dc_mode, double lam, double* rec, void* stream) {
+  return hicu_step_update_amax(N, y, gdir, obj_parts, n_obj, dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec,
+                               nullptr, stream);
+}
+
+// hicu_step_update that also writes the per-CTA max |y| partials (<= 512)
+// the next convolution takes its operand scale from (engine.cu)
+int hicu_step_update_amax(int64_t N, void* y, const void* gdir, const double* obj_parts, int n_obj,
+                          const double* dc_parts, int n_dc, const double* els_parts, int n_els, int dc_mode,
+                          double lam, double* rec, float* amax_out, void* stream) {
   if (!y || !gdir || !obj_parts || !dc_parts || !els_parts || !rec || N < 1)
     return hicu_set_error(HICU_ERR_PARAMETER, "update: bad arguments");
   int64_t b = (N / 2 + 255) / 256;
@@ -749,7 +788,8 @@ extern "C" int hicu_step_update(int64_t N, void* y, const void* gdir, const doub
   if (b < 1) b = 1;
   const bool vec = (((uintptr_t)y | (uintptr_t)gdir) & 15) == 0;
   hicu_launch(update_kernel, (int)b, 256, 0, (cudaStream_t)stream, N, (float2*)y, (const float2*)gdir, obj_parts, n_obj,
-                                                           dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec, vec);
+                                                           dc_parts, n_dc, els_parts, n_els, dc_mode, lam, rec, vec,
+                                                           amax_out);
   return hicu_check_launch("update_kernel");
 }
 
@@ -1001,3 +1041,5 @@ size_t hicu_conv_images_prepare(const hicu_geom* hg, const void* qt_all, int p, 
 }
 
 void hicu_conv_image_hint(const void* img, int early) { hicu_conv_tc_bimage_hint(img, early); }
+void hicu_conv_amax_hint(const float* in, float* out) { hicu_conv_tc_amax_hint(in, out); }
+float* hicu_conv_amax_slots(void* stream) { return hicu_conv_tc_amax_slots((cudaStream_t)stream); }

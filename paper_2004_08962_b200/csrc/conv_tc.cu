@@ -69,17 +69,49 @@ constexpr int kAmaxSlot = 512;             // entries of a producer's max partia
 constexpr int kMaxNb = 8;                  // last-axis kernel extent
 constexpr int kMaxGroups = 64;             // kernel prefixes (product of the other spatial extents)
 constexpr int kMaxTaps = 128;              // spatial taps
-constexpr int kATile = kTileM * 64;       // 8 KB: one 128-row A tile, rows [16 fp16 hi | 16 fp16 lo]
-#ifndef HICU_CONV_GPS
-#define HICU_CONV_GPS 5
-#endif
-constexpr int kGPS = HICU_CONV_GPS;        // prefix groups per pipeline stage (adjacent lines: one TMA box)
-constexpr int kAStage = kGPS * kATile;
 constexpr int kMaxStages = 16;
-constexpr int kWinRow = 20;                // floats per window row (16 + 4: conflict-free float4 rows)
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter, each owning 8 of the 16 output floats
 constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kSmemBudget = 220 * 1024;    // conservative dynamic shared memory budget (sm_100a opt-in 227 KB)
+
+// Operand geometry per complex row width CW (coils == JL columns: 8 for
+// C1/C2/C4/C5, 10 for C3).  A row carries KA = 2 CW real components; its
+// split form is [KP fp16 hi | KP fp16 lo] with KP = KA rounded up to K = 16
+// steps (zero padded); a tap contributes NO = 2 CW output columns.
+template <int CW>
+struct Cw {
+  static constexpr int KA = 2 * CW;
+  static constexpr int NO = 2 * CW;
+  static constexpr int KP = (KA + 15) / 16 * 16;  // halfs per hi (lo) part
+  static constexpr int KS = KP / 16;               // K = 16 steps per part
+  static constexpr int RB = 4 * KP;                // split row bytes: 64 (SW64) or 128 (SW128)
+  static constexpr int ATILE = kTileM * RB;        // one 128-row A tile
+  static constexpr int GPS = CW == 8 ? 5 : 1;      // prefix groups per pipeline stage (one TMA box; CW 10: 6 MMAs per group already)
+  static constexpr int ASTAGE = GPS * ATILE;
+  static constexpr int BROW = 2 * KP;              // B image row bytes: 32 (SW32) or 64 (SW64)
+  static constexpr int NH = NO / 2;                // output floats per epilogue thread (two per row)
+  static constexpr int CH = CW / 2;                // coils per epilogue thread (scatter)
+  static constexpr int WROW = NO + 4;              // window row floats (+16 B: conflict-free rows)
+  static constexpr bool CAT = CW == 8;             // A_hi [B_hi; B_lo] in one MMA (N = 2 ntot = 32 nb <= 256)
+  static constexpr int WIN_FLOATS = (kTileM + kMaxNb - 1) * WROW + kMaxNb * (kMaxNb - 1) * NO;
+};
+
+// byte offset of (row r, 16-byte chunk ch) in a K-major swizzled tile with
+// rows of RBY bytes (SW32 / SW64 / SW128: the swizzle is on absolute address
+// bits; every operand buffer is 1024-byte aligned)
+template <int RBY>
+__host__ __device__ __forceinline__ int swz(int r, int ch) {
+  if (RBY == 32) return r * 32 + ((ch ^ ((r >> 2) & 1)) << 4);
+  if (RBY == 64) return r * 64 + ((ch ^ ((r >> 1) & 3)) << 4);
+  return r * 128 + ((ch ^ (r & 7)) << 4);
+}
+
+template <int RBY>
+__device__ __forceinline__ uint64_t desc_swz(uint32_t saddr) {
+  if (RBY == 32) return tc::desc_sw32(saddr);
+  if (RBY == 64) return tc::desc_sw64(saddr);
+  return tc::desc_sw128(saddr);
+}
 
 struct CtParams {
   int L;                  // spatial axes (1..3)
@@ -112,7 +144,9 @@ struct CtParams {
   int namax;
   float* amax_out;        // optional: per-CTA max |output component| (conv: u, scatter: g), zero-filled to kAmaxSlot
   int k1;                 // extent of the innermost prefix axis (pairs of groups never straddle it)
-  int abox;               // bytes of one stage's A box (two 8 KB tiles, one when L == 1)
+  int abox;               // bytes of one stage's A box (GPS tiles, one when L == 1)
+  int ntot;               // MMA N of one precision block: round16(NO nb)
+  int cat;                // 1: A_hi [B_hi; B_lo] in one MMA (2 ntot <= 256), else separate hi / lo MMAs
 };
 
 __device__ __forceinline__ void decode_line(const CtParams& P, int line, int (&lc)[2]) {
@@ -167,70 +201,76 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory"); }
 
-// Scatter epilogue for one k-space position, coils 4h..4h+3 (one half of the
-// 8 coils): data consistency + the four partial sums (|g|^2, |res|^2,
-// <g,res>, |g|^2 on observed).
-// DC inputs of one k-space position (coils 4h..4h+3): loaded before the
-// tile's accumulators are ready, so the global-load latency overlaps the MMAs
+// DC inputs of one k-space position (the CH coils of one epilogue thread):
+// loaded before the tile's accumulators are ready, so the global-load
+// latency overlaps the MMAs
+template <int CH>
 struct DcIn {
-  uint32_t mm;
-  float4 y[2], x[2];
+  uint8_t mk[CH];
+  float2 y[CH], x[CH];
 };
 
-__device__ __forceinline__ DcIn dc_load(const CtParams& P, size_t e0, int h, const uint8_t* __restrict__ mask,
-                                        const float2* __restrict__ y, const float2* __restrict__ x0) {
-  const size_t e = e0 + 4 * h;
-  DcIn d;
-  d.mm = P.dc_mode != 2 ? __ldg(reinterpret_cast<const uint32_t*>(mask + e)) : 0u;
+template <int CH>
+__device__ __forceinline__ DcIn<CH> dc_load(const CtParams& P, size_t e0, int h, const uint8_t* __restrict__ mask,
+                                            const float2* __restrict__ y, const float2* __restrict__ x0) {
+  const size_t e = e0 + (size_t)CH * h;
+  DcIn<CH> d;
+  if (CH == 4) {
+    const uint32_t mm = P.dc_mode != 2 ? __ldg(reinterpret_cast<const uint32_t*>(mask + e)) : 0u;
 #pragma unroll
-  for (int c2 = 0; c2 < 2; ++c2) {
-    d.y[c2] = d.x[c2] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c = 0; c < CH; ++c) d.mk[c] = (uint8_t)(mm >> (8 * c));
+  } else {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) d.mk[c] = P.dc_mode != 2 ? __ldg(mask + e + c) : (uint8_t)0;
+  }
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    d.y[c] = d.x[c] = make_float2(0.f, 0.f);
     if (P.dc_mode == 1) {
-      d.y[c2] = __ldg(reinterpret_cast<const float4*>(y + e) + c2);
-      d.x[c2] = __ldg(reinterpret_cast<const float4*>(x0 + e) + c2);
+      d.y[c] = __ldg(y + e + c);
+      d.x[c] = __ldg(x0 + e + c);
     }
   }
   return d;
 }
 
-// Scatter epilogue for one k-space position, coils 4h..4h+3 (one half of the
-// 8 coils): data consistency + the four partial sums (|g|^2, |res|^2,
-// <g,res>, |g|^2 on observed).
-__device__ __forceinline__ float scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[8],
-                                               const DcIn& d, float2* __restrict__ gout, double (&acc)[4]) {
+// Scatter epilogue for one k-space position, the CH coils of this thread:
+// data consistency + the four partial sums (|g|^2, |res|^2, <g,res>, |g|^2
+// on observed); returns max |g component| written.
+template <int CH>
+__device__ __forceinline__ float scatter_store(const CtParams& P, size_t e0, int h, const float (&v)[2 * CH],
+                                               const DcIn<CH>& d, float2* __restrict__ gout, double (&acc)[4]) {
   float mx = 0.f;
-  const size_t e = e0 + 4 * h;
-  uint8_t mk[4];
+  const size_t e = e0 + (size_t)CH * h;
+  float a[2 * CH];
 #pragma unroll
-  for (int c = 0; c < 4; ++c) mk[c] = (uint8_t)(d.mm >> (8 * c));
-  float4* gp = reinterpret_cast<float4*>(gout + e);
-#pragma unroll
-  for (int c2 = 0; c2 < 2; ++c2) {
-    float a[4] = {v[4 * c2], v[4 * c2 + 1], v[4 * c2 + 2], v[4 * c2 + 3]};
-    const float4 yy = d.y[c2], xx = d.x[c2];
-    const float yv[4] = {yy.x, yy.y, yy.z, yy.w}, xv[4] = {xx.x, xx.y, xx.z, xx.w};
-#pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const bool on = P.dc_mode != 2 && mk[2 * c2 + hh] == 1;
-      float ar = a[2 * hh], ai = a[2 * hh + 1];
-      if (P.dc_mode == 0) {
-        if (on) ar = ai = 0.f;
-      } else if (P.dc_mode == 1) {
-        const float rr = on ? yv[2 * hh] - xv[2 * hh] : 0.f, ri = on ? yv[2 * hh + 1] - xv[2 * hh + 1] : 0.f;
-        acc[1] += (double)rr * rr + (double)ri * ri;
-        ar = ar + P.lam * rr;
-        ai = ai + P.lam * ri;
-        if (on) {
-          acc[2] += (double)ar * rr + (double)ai * ri;
-          acc[3] += (double)ar * ar + (double)ai * ai;
-        }
+  for (int c = 0; c < CH; ++c) {
+    const bool on = P.dc_mode != 2 && d.mk[c] == 1;
+    float ar = v[2 * c], ai = v[2 * c + 1];
+    if (P.dc_mode == 0) {
+      if (on) ar = ai = 0.f;
+    } else if (P.dc_mode == 1) {
+      const float rr = on ? d.y[c].x - d.x[c].x : 0.f, ri = on ? d.y[c].y - d.x[c].y : 0.f;
+      acc[1] += (double)rr * rr + (double)ri * ri;
+      ar = ar + P.lam * rr;
+      ai = ai + P.lam * ri;
+      if (on) {
+        acc[2] += (double)ar * rr + (double)ai * ri;
+        acc[3] += (double)ar * ar + (double)ai * ai;
       }
-      acc[0] += (double)ar * ar + (double)ai * ai;
-      a[2 * hh] = ar;
-      a[2 * hh + 1] = ai;
-      mx = fmaxf(mx, fmaxf(fabsf(ar), fabsf(ai)));
     }
-    gp[c2] = make_float4(a[0], a[1], a[2], a[3]);
+    acc[0] += (double)ar * ar + (double)ai * ai;
+    a[2 * c] = ar;
+    a[2 * c + 1] = ai;
+    mx = fmaxf(mx, fmaxf(fabsf(ar), fabsf(ai)));
+  }
+  if (CH == 4) {
+    float4* gp = reinterpret_cast<float4*>(gout + e);
+    gp[0] = make_float4(a[0], a[1], a[2], a[3]);
+    gp[1] = make_float4(a[4], a[5], a[6], a[7]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) gout[e + c] = make_float2(a[2 * c], a[2 * c + 1]);
   }
   return mx;
 }
@@ -258,18 +298,15 @@ __host__ __device__ __forceinline__ float pow2_scale(float amax) {
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
-// SW32 K-major fp16 operand layout: row r (16 halfs = 32 B), half k at
-// r * 32 + ((k >> 3) ^ ((r >> 2) & 1)) * 16 + (k & 7) * 2 (the swizzle is on
-// absolute address bits; every operand buffer is 1024-byte aligned).
-__device__ __forceinline__ int sw32_off(int r, int k) { return r * 32 + (((k >> 3) ^ ((r >> 2) & 1)) << 4) + (k & 7) * 2; }
-
-// B images of all prefix groups, fp16: prefix g at base + g * gbytes; row
-// 16 b + n (hi) / 16 nb + 16 b + n (lo), scaled by sb.
-template <int MODE>
+// B images of all prefix groups, fp16: prefix g at base + g * gbytes; rows
+// b NO + n (hi block) and ntot + b NO + n (lo block), K = the operand's real
+// components (zero padded to KP), scaled by sb.
+template <int MODE, int CW>
 __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, const int (&spos)[kMaxTaps][3], int e,
                                            float2 q, uint32_t gbytes, float sb) {
-  const int L = P.L, nb = P.nb;
-  const int sp = e >> 6, c = (e >> 3) & 7, j = e & 7;
+  using T = Cw<CW>;
+  const int L = P.L;
+  const int sp = e / (CW * CW), c = (e / CW) % CW, j = e % CW;
   const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
   const int b = spos[sp][L - 1];
   uint8_t* gb = base + (size_t)g * gbytes;
@@ -291,24 +328,41 @@ __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, con
       const float x = v * sb;
       const __half hi = __float2half_rn(x);
       const __half lo = __float2half_rn(x - __half2float(hi));
-      *reinterpret_cast<__half*>(gb + sw32_off(16 * b + n, k)) = hi;
-      *reinterpret_cast<__half*>(gb + sw32_off(16 * nb + 16 * b + n, k)) = lo;
+      const int rh = b * T::NO + n, rl = P.ntot + rh;
+      *reinterpret_cast<__half*>(gb + swz<T::BROW>(rh, k >> 3) + (k & 7) * 2) = hi;
+      *reinterpret_cast<__half*>(gb + swz<T::BROW>(rl, k >> 3) + (k & 7) * 2) = lo;
     }
 }
 
+// NH consecutive TMEM columns of this thread's lane (8 or 10), without the wait
+template <int NH>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, uint32_t (&r)[NH]) {
+  uint32_t a[8];
+  tc::tmem_ld8_nowait(taddr, a);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r[i] = a[i];
+  if (NH > 8) {
+    uint32_t b2[2];
+    tc::tmem_ld2_nowait(taddr + 8, b2);
+    r[8 % NH] = b2[0];
+    r[9 % NH] = b2[1];
+  }
+}
 
 // MODE 0: conv forward (u, obj); 1: conv ELS (Re<w,u>, |w|^2); 2: scatter + DC.
 // BS: B images streamed per stage (they do not fit next to the pipeline).
-template <int MODE, bool BS>
+template <int MODE, bool BS, int CW>
 __global__ void __launch_bounds__(kThreads, 1)
 conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float2* __restrict__ out,
                const float2* __restrict__ uin, const uint8_t* __restrict__ mask, const float2* __restrict__ y,
                const float2* __restrict__ x0, double* __restrict__ parts) {
   constexpr int NV = MODE == 0 ? 1 : (MODE == 1 ? 2 : 4);
+  using T = Cw<CW>;
+  constexpr int NH = T::NH, CH = T::CH, NO = T::NO, WROW = T::WROW;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int nb = P.nb, ng = P.ng, L = P.L, S = P.stages;
-  const uint32_t gbytes = (uint32_t)nb * 1024;  // B image of one prefix: 32 nb fp16 rows x 32 B
+  const uint32_t gbytes = 2u * (uint32_t)P.ntot * T::BROW;  // B image of one prefix: hi and lo blocks
   uint8_t* sB = smem;
   uint8_t* sStage = sB + (BS ? 0 : (size_t)ng * gbytes);
   const int stb = P.stage_bytes;
@@ -388,7 +442,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
      const uint64_t gm = line_groups<MODE>(P, ga, lc);
      for (int c = 0; c < P.chunks; ++c)
      for (int g = 0, t1 = 0; g < ng; ) {
-      const int cnt = min(kGPS, P.k1 - t1);  // a stage's groups never straddle the outer prefix axis
+      const int cnt = min(T::GPS, P.k1 - t1);  // a stage's groups never straddle the outer prefix axis
       const int g0 = g;
       g += cnt;
       t1 += cnt;
@@ -424,7 +478,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
           if (BS) {
             for (int j = 0; j < cnt; ++j)
-              bulk_g2s(dst + kAStage + j * gbytes, P.bimg + (size_t)(g0 + j) * gbytes, gbytes, &full[s]);
+              bulk_g2s(dst + T::ASTAGE + j * gbytes, P.bimg + (size_t)(g0 + j) * gbytes, gbytes, &full[s]);
           }
         }
       }
@@ -437,10 +491,11 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     // warp-uniform loop; one elected lane (always lane 0: the warp is
     // converged) issues the MMAs and the commits that track them
     if (!BS) tc::mbar_wait(&bres, 0);  // resident B images landed (async proxy, no fence needed)
-    const uint32_t idesc_cat = tc::idesc_f16(kTileM, 32 * nb), idesc_hi = tc::idesc_f16(kTileM, 16 * nb);
+    const uint32_t idesc_cat = tc::idesc_f16(kTileM, 2 * P.ntot), idesc_hi = tc::idesc_f16(kTileM, P.ntot);
     // descriptors advance by address >> 4 in their low 14 bits (shared-memory addresses < 256 KB)
-    const uint64_t dstage0 = tc::desc_sw64(tc::smem_u32(sStage)), dimg0 = tc::desc_sw32(tc::smem_u32(sB));
-    const uint64_t dstageb0 = tc::desc_sw32(tc::smem_u32(sStage));  // streamed B images: SW32 like the resident ones
+    const uint64_t dstage0 = desc_swz<T::RB>(tc::smem_u32(sStage)), dimg0 = desc_swz<T::BROW>(tc::smem_u32(sB));
+    const uint64_t dstageb0 = desc_swz<T::BROW>(tc::smem_u32(sStage));  // streamed B images
+    const uint32_t blo16 = ((uint32_t)P.ntot * T::BROW) >> 4;  // the B image's lo block
     const uint32_t stb16 = (uint32_t)stb >> 4, g16 = gbytes >> 4;
     int s = 0, tb = 0;
     uint32_t ph = 0, tph = 0;
@@ -453,7 +508,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
         const uint32_t d0 = tmem + (uint32_t)(tb * P.tbuf_stride);
         int vi = 0, set = 0;  // valid-group index within the tile; accumulator set = vi % nacc (kept incrementally)
         for (int g = 0, t1 = 0; g < ng; ) {
-          const int cnt = min(kGPS, P.k1 - t1);
+          const int cnt = min(T::GPS, P.k1 - t1);
           const int g0 = g;
           g += cnt;
           t1 += cnt;
@@ -465,7 +520,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
           if (pf && lane == 0) pc[3] += clock64() - t0r;
           const uint64_t dst = dstage0 + (uint64_t)(s * stb16);
 #pragma unroll
-          for (int j = 0; j < kGPS; ++j) {
+          for (int j = 0; j < T::GPS; ++j) {
             if (!((pv >> j) & 1u)) continue;
             if (vi < P.nacc) {  // first use of this accumulator set in the tile: drained by the epilogue?
               const long long t0m = (pf && lane == 0) ? clock64() : 0;
@@ -475,17 +530,29 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             tc::fence_after();
             // tile of group g0 + j: conv j, scatter cnt - 1 - j (its lines run backwards)
             const int tile = MODE == 2 ? cnt - 1 - j : j;
-            const uint64_t da = dst + (uint64_t)((tile * kATile) >> 4);
-            const uint64_t db = BS ? dstageb0 + (uint64_t)(s * stb16) + (uint64_t)((kAStage + j * (int)gbytes) >> 4)
+            const uint64_t da = dst + (uint64_t)((tile * T::ATILE) >> 4);
+            const uint64_t db = BS ? dstageb0 + (uint64_t)(s * stb16) + (uint64_t)((T::ASTAGE + j * (int)gbytes) >> 4)
                                    : dimg0 + (uint64_t)((g0 + j) * g16);
-            const uint32_t d = d0 + (uint32_t)(set * 32 * nb);
+            const uint32_t d = d0 + (uint32_t)(set * (T::CAT ? 2 : 1) * P.ntot);
             const uint32_t acc = vi >= P.nacc ? 1u : 0u;
             ++vi;
             if (++set == P.nacc) set = 0;
             if (tc::elect_one()) {
               if (!(P.debug & 1)) {
-                tc::mma_f16(d, da, db, idesc_cat, acc);         // A_hi [B_hi; B_lo]  (K step 0 of the 64-B rows)
-                tc::mma_f16(d, da + 2, db, idesc_hi, 1);       // + A_lo B_hi        (K step 1: +32 B)
+                // A row [hi KP | lo KP]: hi K step ks at +32 ks bytes, lo at +2 KP + 32 ks; B K step at +32 ks
+#pragma unroll
+                for (int ks = 0; ks < T::KS; ++ks) {
+                  const uint64_t ah = da + (uint64_t)(2 * ks), al = da + (uint64_t)((2 * T::KP + 32 * ks) >> 4);
+                  const uint64_t bk = db + (uint64_t)(2 * ks);
+                  if constexpr (T::CAT) {
+                    tc::mma_f16(d, ah, bk, idesc_cat, ks == 0 ? acc : 1u);  // A_hi [B_hi; B_lo]
+                    tc::mma_f16(d, al, bk, idesc_hi, 1);                    // + A_lo B_hi
+                  } else {
+                    tc::mma_f16(d, ah, bk, idesc_hi, ks == 0 ? acc : 1u);   // A_hi B_hi
+                    tc::mma_f16(d, ah, bk + blo16, idesc_hi, 1);            // + A_hi B_lo
+                    tc::mma_f16(d, al, bk, idesc_hi, 1);                    // + A_lo B_hi
+                  }
+                }
               }
             }
             __syncwarp();
@@ -516,9 +583,9 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
     const int et = threadIdx.x - 64;  // epilogue thread index 0..255
     const float inv = s_scale[1];
     // per-tap window: rows 0..nb-2 = the tap's rows carried from the previous
-    // tile, rows nb-1+m = this tile's D[m, b, :] (kWinRow floats per row)
+    // tile, rows nb-1+m = this tile's D[m, b, :] (WROW floats per row)
     float* tapbuf = sWin;
-    float* carry = sWin + (kTileM + kMaxNb - 1) * kWinRow;  // [b][nb-1][16]
+    float* carry = sWin + (kTileM + kMaxNb - 1) * WROW;  // [b][nb-1][NO]
     double acc_v[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc_v[i] = 0.0;
@@ -536,21 +603,31 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
       const int nvalid = __popcll(gm);
       if (active) {
         // carried rows start at zero (u rows before the line / k-space before the region)
-        for (int i = et; i < nb * (kMaxNb - 1) * 16; i += kEpiWarps * 32) carry[i] = 0.f;
+        for (int i = et; i < nb * (kMaxNb - 1) * NO; i += kEpiWarps * 32) carry[i] = 0.f;
         epi_bar();
         for (int c = 0; c < P.chunks; ++c) {
           // this tile's epilogue inputs from global memory, loaded before the accumulators are ready
-          DcIn din{};
-          float4 upre[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+          DcIn<CH> din{};
+          float2 upre[CH];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) upre[i] = make_float2(0.f, 0.f);
           if (MODE == 2) {
             const int x = P.roff[L - 1] + c * kTileM + m;
-            if (x < P.ext_last) din = dc_load(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, mask, y, x0);
+            if (x < P.ext_last) din = dc_load<CH>(P, (size_t)(obase + (int64_t)x * P.lstride) * CW, h, mask, y, x0);
           } else if (MODE == 1) {
             const int i_out = c * kTileM - (nb - 1) + m;
             if (i_out >= 0 && i_out < P.ext_last) {
-              const float4* up = reinterpret_cast<const float4*>(uin + (size_t)(obase + (int64_t)i_out * P.lstride) * 8 + 4 * h);
-              upre[0] = __ldg(up);
-              upre[1] = __ldg(up + 1);
+              const float2* up = uin + (size_t)(obase + (int64_t)i_out * P.lstride) * CW + CH * h;
+              if (CH == 4) {
+                const float4 a0 = __ldg(reinterpret_cast<const float4*>(up)), a1 = __ldg(reinterpret_cast<const float4*>(up) + 1);
+                upre[0] = make_float2(a0.x, a0.y);
+                upre[1] = make_float2(a0.z, a0.w);
+                upre[2 % CH] = make_float2(a1.x, a1.y);
+                upre[3 % CH] = make_float2(a1.z, a1.w);
+              } else {
+#pragma unroll
+                for (int i = 0; i < CH; ++i) upre[i] = __ldg(up + i);
+              }
             }
           }
           long long t0e = (pf && et == 0) ? clock64() : 0;
@@ -561,37 +638,54 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             t0e = t1e;
           }
           tc::fence_after();
-          const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride) + (uint32_t)(8 * h);
+          const uint32_t t0 = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(tb * P.tbuf_stride) + (uint32_t)(NH * h);
           const int nsets = min(P.nacc, nvalid);
+          const int scols = (T::CAT ? 2 : 1) * P.ntot;  // TMEM columns of one accumulator set
           // drain set by set into registers; each set is released to the MMA
           // warp as soon as it is read (the next tile's groups start on set 0)
-          float f[kMaxNb][8];
+          float f[kMaxNb][NH];
 #pragma unroll
           for (int b = 0; b < kMaxNb; ++b)
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[b][i] = 0.f;
+            for (int i = 0; i < NH; ++i) f[b][i] = 0.f;
           for (int a = 0; a < P.nacc; ++a) {
             if (a < nsets && !(P.debug & 8)) {
-              const uint32_t ta = t0 + (uint32_t)(a * 32 * nb);
-              // two taps in flight per wait (A_hi B_hi + A_lo B_hi, and A_hi B_lo columns)
+              const uint32_t ta = t0 + (uint32_t)(a * scols);
+              if constexpr (NH == 8 && T::CAT) {
+                // two taps in flight per wait (A_hi B_hi + A_lo B_hi, and A_hi B_lo columns)
 #pragma unroll
-              for (int b = 0; b < kMaxNb; b += 2) {
-                if (b < nb) {
-                  uint32_t v0[2][8], v1[2][8];
-                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b), v0[0]);
-                  tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b), v1[0]);
-                  if (b + 1 < nb) {
-                    tc::tmem_ld8_nowait(ta + (uint32_t)(16 * b + 16), v0[1]);
-                    tc::tmem_ld8_nowait(ta + (uint32_t)(16 * nb + 16 * b + 16), v1[1]);
-                  }
-                  tc::tmem_wait_ld();
+                for (int b = 0; b < kMaxNb; b += 2) {
+                  if (b < nb) {
+                    uint32_t v0[2][8], v1[2][8];
+                    tc::tmem_ld8_nowait(ta + (uint32_t)(NO * b), v0[0]);
+                    tc::tmem_ld8_nowait(ta + (uint32_t)(P.ntot + NO * b), v1[0]);
+                    if (b + 1 < nb) {
+                      tc::tmem_ld8_nowait(ta + (uint32_t)(NO * b + NO), v0[1]);
+                      tc::tmem_ld8_nowait(ta + (uint32_t)(P.ntot + NO * b + NO), v1[1]);
+                    }
+                    tc::tmem_wait_ld();
 #pragma unroll
-                  for (int i = 0; i < 8; ++i) f[b][i] += __uint_as_float(v0[0][i]) + __uint_as_float(v1[0][i]);
-                  if (b + 1 < nb) {
+                    for (int i = 0; i < NH; ++i) f[b][i] += __uint_as_float(v0[0][i]) + __uint_as_float(v1[0][i]);
+                    if (b + 1 < nb) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) f[b + 1][i] += __uint_as_float(v0[1][i]) + __uint_as_float(v1[1][i]);
+                      for (int i = 0; i < NH; ++i) f[b + 1][i] += __uint_as_float(v0[1][i]) + __uint_as_float(v1[1][i]);
+                    }
                   }
                 }
+              } else {
+#pragma unroll
+              for (int b = 0; b < kMaxNb; ++b) {
+                if (b < nb) {
+                  // hi block (A_hi B_hi + A_lo B_hi [+ A_hi B_lo when separate]) and, when
+                  // concatenated, the A_hi B_lo block ntot columns further
+                  uint32_t v0[NH], v1[NH];
+                  tmem_ld_row<NH>(ta + (uint32_t)(b * NO), v0);
+                  if constexpr (T::CAT) tmem_ld_row<NH>(ta + (uint32_t)(P.ntot + b * NO), v1);
+                  tc::tmem_wait_ld();
+#pragma unroll
+                  for (int i = 0; i < NH; ++i) f[b][i] += __uint_as_float(v0[i]) + (T::CAT ? __uint_as_float(v1[i]) : 0.f);
+                }
+              }
               }
             }
             tc::fence_before();
@@ -610,32 +704,53 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             tph ^= 1;
           }
           // shifted sums, one tap at a time: conv row m takes D[m + b - (nb-1), b]
-          // (pc[10]: window time, pc[11]: output time of the counter mode)
           // (window row m + b), scatter row m takes D[m - b, b] (window row nb-1+m-b)
-          float v[8];
+          float v[NH];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = 0.f;
+          for (int i = 0; i < NH; ++i) v[i] = 0.f;
+          constexpr int NQ4 = NO / 4;  // float4 pieces per window row
 #pragma unroll
           for (int b = 0; b < kMaxNb; ++b) {
             if (b < nb) {
-              if (et < (nb - 1) * 4) {
-                const int r = et >> 2, k = et & 3;
-                reinterpret_cast<float4*>(tapbuf + r * kWinRow)[k] =
-                    reinterpret_cast<const float4*>(carry + (b * (kMaxNb - 1) + r) * 16)[k];
+              if (et < (nb - 1) * NQ4) {
+                const int r = et / NQ4, kk = et - r * NQ4;
+                reinterpret_cast<float4*>(tapbuf + r * WROW)[kk] =
+                    reinterpret_cast<const float4*>(carry + (b * (kMaxNb - 1) + r) * NO)[kk];
               }
-              float4* w4 = reinterpret_cast<float4*>(tapbuf + (nb - 1 + m) * kWinRow + 8 * h);
-              w4[0] = make_float4(f[b][0] * inv, f[b][1] * inv, f[b][2] * inv, f[b][3] * inv);
-              w4[1] = make_float4(f[b][4] * inv, f[b][5] * inv, f[b][6] * inv, f[b][7] * inv);
-              epi_bar();
               const int w = MODE < 2 ? m + b : nb - 1 + m - b;
-              const float4* r4 = reinterpret_cast<const float4*>(tapbuf + w * kWinRow + 8 * h);
-              const float4 t0v = r4[0], t1v = r4[1];
-              v[0] += t0v.x; v[1] += t0v.y; v[2] += t0v.z; v[3] += t0v.w;
-              v[4] += t1v.x; v[5] += t1v.y; v[6] += t1v.z; v[7] += t1v.w;
-              if (et < (nb - 1) * 4) {  // this tap's last nb - 1 rows carry into the next tile
-                const int r = et >> 2, k = et & 3;
-                reinterpret_cast<float4*>(carry + (b * (kMaxNb - 1) + r) * 16)[k] =
-                    reinterpret_cast<const float4*>(tapbuf + (kTileM + r) * kWinRow)[k];
+              if (NH % 4 == 0) {  // 16-byte window traffic
+                float4* w4 = reinterpret_cast<float4*>(tapbuf + (nb - 1 + m) * WROW + NH * h);
+#pragma unroll
+                for (int i = 0; i < NH / 4; ++i)
+                  w4[i] = make_float4(f[b][4 * i] * inv, f[b][4 * i + 1] * inv, f[b][4 * i + 2] * inv,
+                                      f[b][4 * i + 3] * inv);
+                epi_bar();
+                const float4* r4 = reinterpret_cast<const float4*>(tapbuf + w * WROW + NH * h);
+#pragma unroll
+                for (int i = 0; i < NH / 4; ++i) {
+                  const float4 t4 = r4[i];
+                  v[4 * i] += t4.x;
+                  v[4 * i + 1] += t4.y;
+                  v[4 * i + 2] += t4.z;
+                  v[4 * i + 3] += t4.w;
+                }
+              } else {
+                float2* w2 = reinterpret_cast<float2*>(tapbuf + (nb - 1 + m) * WROW + NH * h);
+#pragma unroll
+                for (int i = 0; i < NH / 2; ++i) w2[i] = make_float2(f[b][2 * i] * inv, f[b][2 * i + 1] * inv);
+                epi_bar();
+                const float2* r2 = reinterpret_cast<const float2*>(tapbuf + w * WROW + NH * h);
+#pragma unroll
+                for (int i = 0; i < NH / 2; ++i) {
+                  const float2 t2 = r2[i];
+                  v[2 * i] += t2.x;
+                  v[2 * i + 1] += t2.y;
+                }
+              }
+              if (et < (nb - 1) * NQ4) {  // this tap's last nb - 1 rows carry into the next tile
+                const int r = et / NQ4, kk = et - r * NQ4;
+                reinterpret_cast<float4*>(carry + (b * (kMaxNb - 1) + r) * NO)[kk] =
+                    reinterpret_cast<const float4*>(tapbuf + (kTileM + r) * WROW)[kk];
               }
               epi_bar();
             }
@@ -650,14 +765,19 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             if (i_out < 0 || i_out >= P.ext_last) continue;
             const int64_t idx = obase + (int64_t)i_out * P.lstride;
             if (MODE == 0) {
-              float4* up = reinterpret_cast<float4*>(out + (size_t)idx * 8 + 4 * h);
+              float2* up = out + (size_t)idx * CW + CH * h;
               if (!pf) {  // counter mode keeps `out` for its records
-                up[0] = make_float4(v[0], v[1], v[2], v[3]);
-                up[1] = make_float4(v[4], v[5], v[6], v[7]);
+                if (CH == 4) {
+                  reinterpret_cast<float4*>(up)[0] = make_float4(v[0], v[1], v[2], v[3]);
+                  reinterpret_cast<float4*>(up)[1] = make_float4(v[4], v[5], v[6], v[7 % NH]);
+                } else {
+#pragma unroll
+                  for (int i = 0; i < CH; ++i) up[i] = make_float2(v[2 * i], v[2 * i + 1]);
+                }
               }
               double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-              for (int i = 0; i < 8; i += 2) {
+              for (int i = 0; i < NH; i += 2) {
                 s0 += (double)v[i] * v[i];
                 s1 += (double)v[i + 1] * v[i + 1];
                 omax = fmaxf(omax, fmaxf(fabsf(v[i]), fabsf(v[i + 1])));
@@ -666,13 +786,13 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             } else {
               double d0 = 0.0, d1 = 0.0, n0 = 0.0, n1 = 0.0;
 #pragma unroll
-              for (int i = 0; i < 2; ++i) {
-                const float4 uu = upre[i];
-                d0 += (double)v[4 * i] * uu.x + (double)v[4 * i + 1] * uu.y;
-                d1 += (double)v[4 * i + 2] * uu.z + (double)v[4 * i + 3] * uu.w;
+              for (int i = 0; i < CH; ++i) {
+                const float2 uu = upre[i];
+                if (i & 1) d1 += (double)v[2 * i] * uu.x + (double)v[2 * i + 1] * uu.y;
+                else d0 += (double)v[2 * i] * uu.x + (double)v[2 * i + 1] * uu.y;
               }
 #pragma unroll
-              for (int i = 0; i < 8; i += 2) {
+              for (int i = 0; i < NH; i += 2) {
                 n0 += (double)v[i] * v[i];
                 n1 += (double)v[i + 1] * v[i + 1];
               }
@@ -683,7 +803,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
             const int x = P.roff[L - 1] + c * kTileM + m;
             if (x >= P.ext_last) continue;
             double a4[4] = {0, 0, 0, 0};
-            omax = fmaxf(omax, scatter_store(P, (size_t)(obase + (int64_t)x * P.lstride) * 8, h, v, din, out, a4));
+            omax = fmaxf(omax, scatter_store<CH>(P, (size_t)(obase + (int64_t)x * P.lstride) * CW, h, v, din, out, a4));
 #pragma unroll
             for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
           }
@@ -693,12 +813,14 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
         // positions no tile covers: DC term only
         const int x_lo = active ? P.roff[L - 1] : 0;
         const int x_hi = active ? P.roff[L - 1] + P.chunks * kTileM : 0;
-        const float vz[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float vz[NH];
+#pragma unroll
+        for (int i = 0; i < NH; ++i) vz[i] = 0.f;
         for (int x = m; x < P.ext_last; x += kTileM) {
           if (x >= x_lo && x < x_hi) continue;
           double a4[4] = {0, 0, 0, 0};
-          const size_t e0 = (size_t)(obase + (int64_t)x * P.lstride) * 8;
-          omax = fmaxf(omax, scatter_store(P, e0, h, vz, dc_load(P, e0, h, mask, y, x0), out, a4));
+          const size_t e0 = (size_t)(obase + (int64_t)x * P.lstride) * CW;
+          omax = fmaxf(omax, scatter_store<CH>(P, e0, h, vz, dc_load<CH>(P, e0, h, mask, y, x0), out, a4));
 #pragma unroll
           for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
         }
@@ -752,7 +874,7 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
 // B images (fp16 hi/lo, scaled) for one Q~, written once to global memory so
 // each conv CTA copies them with one bulk copy; the power-of-two scale sits
 // in a trailer after the ng images.  One CTA per image.
-template <int MODE>
+template <int MODE, int CW>
 __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P, const int32_t* __restrict__ pos,
                                                                const float2* __restrict__ qt_all, size_t qt_stride,
                                                                uint8_t* __restrict__ img_all, size_t img_stride,
@@ -761,12 +883,12 @@ __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P,
   __shared__ int spos[kMaxTaps][3];
   __shared__ float wmax[kThreads / 32];
   const int L = P.L;
-  const uint32_t gbytes = (uint32_t)P.nb * 1024;
+  const uint32_t gbytes = 2u * (uint32_t)P.ntot * Cw<CW>::BROW;
   uint8_t* img = img_all + (size_t)(2 * blockIdx.x + img_off) * img_stride;
   const float2* qt = qt_all + (size_t)blockIdx.x * qt_stride;
   for (int t = threadIdx.x; t < P.nsp * L; t += kThreads)
-    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * 8 * P.ndim + P.perm[t % L]);
-  const int nq = P.nsp * 64;
+    spos[t / L][t % L] = __ldg(pos + (size_t)(t / L) * CW * P.ndim + P.perm[t % L]);
+  const int nq = P.nsp * CW * CW;
   float m = 0.f;
   for (int e = threadIdx.x; e < nq; e += kThreads) {
     const float2 q = __ldg(qt + e);
@@ -781,7 +903,7 @@ __global__ void __launch_bounds__(kThreads) conv_bimage_kernel(const CtParams P,
   float mm = 0.f;
   for (int w = 0; w < kThreads / 32; ++w) mm = fmaxf(mm, wmax[w]);
   const float sb = pow2_scale(mm);
-  for (int e = threadIdx.x; e < nq; e += kThreads) bimage_put<MODE>(img, P, spos, e, __ldg(qt + e), gbytes, sb);
+  for (int e = threadIdx.x; e < nq; e += kThreads) bimage_put<MODE, CW>(img, P, spos, e, __ldg(qt + e), gbytes, sb);
   if (threadIdx.x == 0) *reinterpret_cast<float*>(img + (size_t)P.ng * gbytes) = sb;
 }
 
@@ -799,21 +921,38 @@ struct SplitParams {
   int64_t istr[3];  // input (natural C-order) row stride of natural axis a
 };
 
+// 4 floats x s -> 4 fp16 hi + 4 fp16 lo halves (8 bytes each)
+__device__ __forceinline__ void split4(float4 v, float sa, uint2& hi, uint2& lo) {
+  const float x0 = v.x * sa, x1 = v.y * sa, x2 = v.z * sa, x3 = v.w * sa;
+  const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+  const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+  hi = make_uint2(h2u(h01), h2u(h23));
+  lo = make_uint2(h2u(__floats2half2_rn(x0 - f01.x, x1 - f01.y)), h2u(__floats2half2_rn(x2 - f23.x, x3 - f23.y)));
+}
+
+__device__ __forceinline__ float split_scale(const float* __restrict__ amax, int namax) {
+  float m = 0.f;
+  for (int i = threadIdx.x; i < namax; i += 32) m = fmaxf(m, __ldg(amax + i));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  return pow2_scale(m);
+}
+
+template <int CW>
 __global__ void __launch_bounds__(256) split_kernel(const float4* __restrict__ x, int64_t rows, const SplitParams sp,
                                                     const float* __restrict__ amax, int namax, uint4* __restrict__ out) {
+  using T = Cw<CW>;
+  constexpr int QR = T::KA / 4, QP = T::KP / 4;  // float4 pieces per input row; 8-byte pieces per half
   hicu_pdl_entry();
   __shared__ float s_sa;
   if (threadIdx.x < 32) {
-    float m = 0.f;
-    for (int i = threadIdx.x; i < namax; i += 32) m = fmaxf(m, __ldg(amax + i));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) s_sa = pow2_scale(m);
+    const float m = split_scale(amax, namax);
+    if (threadIdx.x == 0) s_sa = m;
   }
   __syncthreads();
   const float sa = s_sa;
-  // threads walk OUTPUT rows (consecutive threads write consecutive 64-byte
-  // rows: coalesced stores); each reads its whole 64-byte input row
+  // threads walk OUTPUT rows (consecutive threads write consecutive rows:
+  // coalesced stores); each reads its whole input row
   for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < rows; o += (int64_t)gridDim.x * blockDim.x) {
     int64_t t = o, r = 0;
     for (int k = sp.L - 1; k >= 0; --k) {
@@ -822,72 +961,71 @@ __global__ void __launch_bounds__(256) split_kernel(const float4* __restrict__ x
       t /= sp.ext[a];
       r += ca * sp.istr[a];
     }
-    uint32_t hw[8], lw[8];
+    uint2 hw[QP], lw[QP];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 v = __ldg(x + r * 4 + k);
-      const float x0 = v.x * sa, x1 = v.y * sa, x2 = v.z * sa, x3 = v.w * sa;
-      const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
-      const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-      hw[2 * k] = h2u(h01);
-      hw[2 * k + 1] = h2u(h23);
-      lw[2 * k] = h2u(__floats2half2_rn(x0 - f01.x, x1 - f01.y));
-      lw[2 * k + 1] = h2u(__floats2half2_rn(x2 - f23.x, x3 - f23.y));
+    for (int k = 0; k < QP; ++k) {
+      if (k < QR) split4(__ldg(x + r * QR + k), sa, hw[k], lw[k]);
+      else hw[k] = lw[k] = make_uint2(0u, 0u);
     }
-    uint4* po = out + o * 4;
-    po[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
-    po[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
-    po[2] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
-    po[3] = make_uint4(lw[4], lw[5], lw[6], lw[7]);
+    uint4* po = out + o * (T::RB / 16);
+#pragma unroll
+    for (int k = 0; k < QP / 2; ++k) {
+      po[k] = make_uint4(hw[2 * k].x, hw[2 * k].y, hw[2 * k + 1].x, hw[2 * k + 1].y);
+      po[QP / 2 + k] = make_uint4(lw[2 * k].x, lw[2 * k].y, lw[2 * k + 1].x, lw[2 * k + 1].y);
+    }
   }
 }
 
 // The same split as a batched tiled transpose, for a line axis that is not
 // the array's fastest: the natural array is [A][Lx][B] rows (Lx = line
-// axis), the output [A][B][Lx].  A 32 x 32 tile of rows is read as 32 runs of
-// 32 contiguous rows (2 KB) and written as 32 runs of 32 contiguous rows, so
-// both directions are coalesced (the row-per-thread split_kernel reads rows a
-// plane apart).  Grid (ceil(B/32), ceil(Lx/32), A), 256 threads.
+// axis), the output [A][B][Lx].  A kTT x TB tile of rows is read as runs of
+// TB contiguous rows and written as runs of kTT contiguous rows, so both
+// directions are coalesced (the row-per-thread split_kernel reads rows a
+// plane apart).  Grid (ceil(B/TB), ceil(Lx/kTT), A), 256 threads.
 constexpr int kTT = 32;
-constexpr int kTTPitch = kTT * 64 + 32;  // bytes per tile b-row (+32: 2-way instead of 8-way store conflicts)
+template <int CW>
+struct TT {
+  static constexpr int TB = Cw<CW>::RB == 64 ? 32 : 16;      // B rows per tile (<= 64 KB of shared memory)
+  static constexpr int PITCH = kTT * Cw<CW>::RB + 32;         // bytes per tile b-row (+32: fewer store conflicts)
+  static constexpr int SMEM = TB * PITCH;
+};
 
+template <int CW>
 __global__ void __launch_bounds__(256) split_t_kernel(const float4* __restrict__ x, int64_t Lx, int64_t B,
                                                       const float* __restrict__ amax, int namax,
                                                       uint4* __restrict__ out) {
+  using T = Cw<CW>;
+  constexpr int QR = T::KA / 4, QP = T::KP / 4, TB = TT<CW>::TB, PITCH = TT<CW>::PITCH;
   hicu_pdl_entry();
   extern __shared__ __align__(16) uint8_t tt[];
   __shared__ float s_sa;
   if (threadIdx.x < 32) {
-    float m = 0.f;
-    for (int i = threadIdx.x; i < namax; i += 32) m = fmaxf(m, __ldg(amax + i));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (threadIdx.x == 0) s_sa = pow2_scale(m);
+    const float m = split_scale(amax, namax);
+    if (threadIdx.x == 0) s_sa = m;
   }
   __syncthreads();
   const float sa = s_sa;
-  const int64_t b0 = (int64_t)blockIdx.x * kTT, l0 = (int64_t)blockIdx.y * kTT, a = blockIdx.z;
-  // read: piece i -> (lx_l = i >> 7, b_l = (i >> 2) & 31, pc = i & 3): runs of 32 rows along B
-  for (int i = threadIdx.x; i < kTT * kTT * 4; i += 256) {
-    const int lx_l = i >> 7, b_l = (i >> 2) & 31, pc = i & 3;
+  const int64_t b0 = (int64_t)blockIdx.x * TB, l0 = (int64_t)blockIdx.y * kTT, a = blockIdx.z;
+  // read: piece i -> (lx_l, b_l, pc): runs of TB rows along B (pads written as zeros)
+  for (int i = threadIdx.x; i < kTT * TB * QP; i += 256) {
+    const int pc = i % QP, b_l = (i / QP) % TB, lx_l = i / (QP * TB);
     const int64_t lx = l0 + lx_l, b = b0 + b_l;
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lx < Lx && b < B) v = __ldg(x + ((a * Lx + lx) * B + b) * 4 + pc);
-    const float x0 = v.x * sa, x1 = v.y * sa, x2 = v.z * sa, x3 = v.w * sa;
-    const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
-    const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-    uint8_t* row = tt + b_l * kTTPitch + lx_l * 64;
-    *reinterpret_cast<uint2*>(row + pc * 8) = make_uint2(h2u(h01), h2u(h23));
-    *reinterpret_cast<uint2*>(row + 32 + pc * 8) =
-        make_uint2(h2u(__floats2half2_rn(x0 - f01.x, x1 - f01.y)), h2u(__floats2half2_rn(x2 - f23.x, x3 - f23.y)));
+    if (pc < QR && lx < Lx && b < B) v = __ldg(x + ((a * Lx + lx) * B + b) * QR + pc);
+    uint2 hi, lo;
+    split4(v, sa, hi, lo);
+    uint8_t* row = tt + b_l * PITCH + lx_l * T::RB;
+    *reinterpret_cast<uint2*>(row + pc * 8) = hi;
+    *reinterpret_cast<uint2*>(row + 2 * T::KP + pc * 8) = lo;
   }
   __syncthreads();
-  // write: piece i -> (b_l = i >> 7, lx_l = (i >> 2) & 31, chunk = i & 3): runs of 32 rows along Lx
-  for (int i = threadIdx.x; i < kTT * kTT * 4; i += 256) {
-    const int b_l = i >> 7, lx_l = (i >> 2) & 31, ch = i & 3;
+  // write: piece i -> (b_l, lx_l, chunk): runs of kTT rows along Lx
+  constexpr int NCH = T::RB / 16;
+  for (int i = threadIdx.x; i < kTT * TB * NCH; i += 256) {
+    const int ch = i % NCH, lx_l = (i / NCH) % kTT, b_l = i / (NCH * kTT);
     const int64_t lx = l0 + lx_l, b = b0 + b_l;
     if (lx < Lx && b < B)
-      out[((a * B + b) * Lx + lx) * 4 + ch] = *reinterpret_cast<const uint4*>(tt + b_l * kTTPitch + lx_l * 64 + ch * 16);
+      out[((a * B + b) * Lx + lx) * NCH + ch] = *reinterpret_cast<const uint4*>(tt + b_l * PITCH + lx_l * T::RB + ch * 16);
   }
 }
 
@@ -977,28 +1115,30 @@ EncodeTiledFn encode_tiled() {
 // ext[perm[L-3]]) with the array's own strides (any spatial axis can be the
 // tile axis), 128-row x 16-float boxes (one per stage), no swizzle (only the converter warps
 // read the fp32 tile: linear 16-byte reads), zero fill out of bounds.
-int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm) {
+int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm, int cw) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled unavailable");
-  // the split array is stored in kernel axis order: line axis perm[L-1] fastest
-  cuuint64_t dims[4] = {32, (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
+  // the split array is stored in kernel axis order: line axis perm[L-1] fastest; rows of
+  // [KP hi | KP lo] fp16 (64 B: SWIZZLE_64B, 128 B: SWIZZLE_128B)
+  const int kp = cw == 8 ? 16 : 32, rb = 4 * kp, gps = cw == 8 ? Cw<8>::GPS : Cw<10>::GPS;
+  cuuint64_t dims[4] = {(cuuint64_t)(2 * kp), (cuuint64_t)ext[perm[L - 1]], (cuuint64_t)(L >= 2 ? ext[perm[L - 2]] : 1),
                         (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
-  cuuint64_t strides[3] = {64, 64 * dims[1], 64 * dims[1] * dims[2]};
-  // depth kGPS along dimension 2: a stage's prefix groups are adjacent lines
-  cuuint32_t box[4] = {32, (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? kGPS : 1), 1}, es[4] = {1, 1, 1, 1};
+  cuuint64_t strides[3] = {(cuuint64_t)rb, rb * dims[1], rb * dims[1] * dims[2]};
+  // depth GPS along dimension 2: a stage's prefix groups are adjacent lines
+  cuuint32_t box[4] = {(cuuint32_t)(2 * kp), (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? gps : 1), 1}, es[4] = {1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled failed");
   return HICU_OK;
 }
 
 // Tensor maps depend only on (pointer, extents, axis order): a small
 // per-thread cache keeps cuTensorMapEncodeTiled off the per-launch path.
-int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm) {
+int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm, int cw) {
   struct Entry {
     const void* base;
-    int L;
+    int L, cw;
     int64_t ext[3];
     int perm[3];
     CUtensorMap map;
@@ -1007,18 +1147,19 @@ int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, co
   static thread_local int used = 0, next = 0;
   for (int i = 0; i < used; ++i) {
     const Entry& e = cache[i];
-    bool same = e.base == base && e.L == L;
+    bool same = e.base == base && e.L == L && e.cw == cw;
     for (int d = 0; d < L && same; ++d) same = e.ext[d] == ext[d] && e.perm[d] == perm[d];
     if (same) {
       *tm = e.map;
       return HICU_OK;
     }
   }
-  const int st = make_tmap(tm, base, L, ext, perm);
+  const int st = make_tmap(tm, base, L, ext, perm, cw);
   if (st) return st;
   Entry& e = cache[next];
   e.base = base;
   e.L = L;
+  e.cw = cw;
   for (int d = 0; d < 3; ++d) {
     e.ext[d] = d < L ? ext[d] : 0;
     e.perm[d] = d < L ? perm[d] : 0;
@@ -1089,46 +1230,63 @@ void choose_perm(const DevGeom& g, int MODE, int (&perm)[3]) {
 
 struct Shape {
   int L, nb, ng, kpre[2];
+  int cw;            // complex row width (8 or 10)
+  int ntot, cat;     // MMA N of one precision block; A_hi [B_hi; B_lo] in one MMA
+  size_t gbytes;     // B image bytes of one prefix (hi + lo blocks)
   int bstream;       // B images copied per stage (they do not fit resident)
   size_t stage;      // bytes per pipeline stage
   size_t fixed;      // resident B images + window + alignment slack
 };
 
-bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
+template <int CW>
+bool shape_cw(const DevGeom& g, Shape* sh, const int* perm) {
+  using T = Cw<CW>;
   const int L = g.ndim - 1;
-  if (g.nc != 8 || p != 8 || g.ncirc != 0 || L < 1 || L > 3 || g.nsp < 1 || g.nsp > kMaxTaps) return false;
-  if (g.kext[L] != 8) return false;
   int ng = 1;
   for (int d = 0; d < L; ++d)
     if (g.kext[d] < 1) return false;
   for (int d = 0; d < L - 1; ++d) ng *= (int)g.kext[perm[d]];
   const int nb = (int)g.kext[perm[L - 1]];
   if (nb > kMaxNb || ng > kMaxGroups) return false;
+  const int ntot = (T::NO * nb + 15) / 16 * 16;
+  if (ntot > 256) return false;
   sh->L = L;
   sh->nb = nb;
   sh->ng = ng;
   sh->kpre[0] = L >= 2 ? (int)g.kext[perm[0]] : 1;
   sh->kpre[1] = L >= 3 ? (int)g.kext[perm[1]] : 1;
-  const size_t win = ((size_t)(kTileM + kMaxNb - 1) * kWinRow * 4 + (size_t)kMaxNb * (kMaxNb - 1) * 64 + 1023) &
-                     ~(size_t)1023;
+  sh->cw = CW;
+  sh->ntot = ntot;
+  sh->cat = T::CAT ? 1 : 0;
+  if (T::CAT && 2 * ntot > 256) return false;
+  sh->gbytes = (size_t)2 * ntot * T::BROW;
+  const size_t win = ((size_t)T::WIN_FLOATS * 4 + 1023) & ~(size_t)1023;
   // resident B images when they fit next to >= 3 stages, else the stage groups' images per stage
-  const size_t res_fixed = (size_t)ng * nb * 1024 + win + 1024;
-  if (res_fixed + 3 * (size_t)kAStage <= (size_t)kSmemBudget) {
+  const size_t res_fixed = (size_t)ng * sh->gbytes + win + 1024;
+  if (res_fixed + 3 * (size_t)T::ASTAGE <= (size_t)kSmemBudget) {
     sh->bstream = 0;
-    sh->stage = kAStage;
+    sh->stage = T::ASTAGE;
     sh->fixed = res_fixed;
   } else {
     sh->bstream = 1;
-    sh->stage = kAStage + kGPS * (size_t)nb * 1024;
+    sh->stage = T::ASTAGE + T::GPS * sh->gbytes;
     sh->fixed = win + 1024;
   }
   return sh->fixed + 3 * sh->stage <= (size_t)kSmemBudget;
 }
 
-// bytes of one B image set (ng fp16 group images + the scale trailer)
-size_t image_bytes(const Shape& sh) { return (size_t)sh.ng * sh.nb * 1024 + 256; }
+bool shape_of(const DevGeom& g, int p, Shape* sh, const int* perm) {
+  const int L = g.ndim - 1;
+  if (g.ncirc != 0 || L < 1 || L > 3 || g.nsp < 1 || g.nsp > kMaxTaps) return false;
+  if (g.nc == 8 && p == 8 && g.kext[L] == 8) return shape_cw<8>(g, sh, perm);
+  if (g.nc == 10 && p == 10 && g.kext[L] == 10) return shape_cw<10>(g, sh, perm);
+  return false;
+}
 
-template <int MODE, bool BS>
+// bytes of one B image set (ng fp16 group images + the scale trailer)
+size_t image_bytes(const Shape& sh) { return (size_t)sh.ng * sh.gbytes + 256; }
+
+template <int MODE, bool BS, int CW>
 int launch_bs(const Shape& sh, CtParams P, const CUtensorMap& tm, float2* out, const float2* uin, const uint8_t* mask,
               const float2* y, const float2* x0, double* parts, int64_t lines, int nparts_total, cudaStream_t st) {
   // dynamic shared memory available to this instantiation on the current
@@ -1140,11 +1298,11 @@ int launch_bs(const Shape& sh, CtParams P, const CUtensorMap& tm, float2* out, c
   static std::atomic<size_t> avail_a[kMaxDev];
   int dev = 0;
   cudaGetDevice(&dev);
-  hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS>);
+  hicu_allow_max_smem((const void*)conv_tc_kernel<MODE, BS, CW>);
   size_t avail = (dev >= 0 && dev < kMaxDev) ? avail_a[dev].load(std::memory_order_acquire) : 0;
   if (!avail) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, (const void*)conv_tc_kernel<MODE, BS>);
+    cudaFuncGetAttributes(&fa, (const void*)conv_tc_kernel<MODE, BS, CW>);
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     avail = (size_t)optin - fa.sharedSizeBytes;
@@ -1158,11 +1316,13 @@ int launch_bs(const Shape& sh, CtParams P, const CUtensorMap& tm, float2* out, c
   if (grid > hicu_sm_count()) grid = hicu_sm_count();
   if (grid > nparts_total) grid = nparts_total;
   if (grid < 1) grid = 1;
-  hicu_launch(conv_tc_kernel<MODE, BS>, (int)grid, kThreads, smem, st, tm, P, out, uin, mask, y, x0, parts);
+  hicu_launch(conv_tc_kernel<MODE, BS, CW>, (int)grid, kThreads, smem, st, tm, P, out, uin, mask, y, x0, parts);
   return hicu_check_launch("conv_tc_kernel");
 }
 
 void fill_shape_params(CtParams& P, const DevGeom& g, const Shape& sh, const int (&perm)[3]) {
+  P.ntot = sh.ntot;
+  P.cat = sh.cat;
   for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
   P.L = sh.L;
   P.nsp = g.nsp;
@@ -1178,36 +1338,30 @@ int build_image(const DevGeom& g, const Shape& sh, const int (&perm)[3], const f
                 size_t ib, int img_off, cudaStream_t st) {
   CtParams P{};
   fill_shape_params(P, g, sh, perm);
-  hicu_launch(conv_bimage_kernel<MODE>, G, kThreads, 0, st, P, g.pos, qt_all, (size_t)g.nsp * 64, img, ib, img_off);
+  const size_t qs = (size_t)g.nsp * sh.cw * sh.cw;
+  if (sh.cw == 8)
+    hicu_launch(conv_bimage_kernel<MODE, 8>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, img_off);
+  else
+    hicu_launch(conv_bimage_kernel<MODE, 10>, G, kThreads, 0, st, P, g.pos, qt_all, qs, img, ib, img_off);
   return hicu_check_launch("conv_bimage_kernel");
 }
 
-template <int MODE>
-int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, const float2* uin, const uint8_t* mask,
-           const float2* y, const float2* x0, int dc_mode, float lam, double* parts, int nparts_total,
-           cudaStream_t st) {
-  // the B-image hint is consumed by this launch whatever happens below (an
-  // early error return must not leave it set for an unrelated later call)
-  const uint8_t* bimg = t_bimg;
-  int bimg_early = t_bimg_early;
-  t_bimg = nullptr;
-  const float* amax_in = t_amax_in;
-  float* amax_out = t_amax_out;
-  t_amax_in = nullptr;
-  t_amax_out = nullptr;
-  int perm[3];
-  choose_perm(g, MODE, perm);
-  Shape sh;
-  if (!shape_of(g, 8, &sh, perm))
-    return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: geometry outside the tensor-core scope");
+template <int MODE, int CW>
+int launch_cw(const DevGeom& g, const Shape& sh, const int (&perm)[3], const uint8_t* bimg, int bimg_early,
+              const float* amax_in, float* amax_out, const float2* asrc, const float2* qt, float2* out,
+              const float2* uin, const uint8_t* mask, const float2* y, const float2* x0, int dc_mode, float lam,
+              double* parts, int nparts_total, cudaStream_t st) {
+  using T = Cw<CW>;
   const int L = sh.L;
   CtParams P{};
   fill_shape_params(P, g, sh, perm);
   // accumulator sets: chains of at most ~18 MMAs per TMEM accumulator (the
   // tensor core's fp32 accumulation error grows with the chain length)
-  P.nacc = std::min(3, std::max(1, (2 * sh.ng + 17) / 18));
-  if (P.nacc * 32 * sh.nb > 512) P.nacc = 512 / (32 * sh.nb);
-  P.tbuf_stride = 2 * P.nacc * 32 * sh.nb <= 512 ? 256 : 0;  // double-buffered tiles when two fit
+  const int mpp = T::KS * (sh.cat ? 2 : 3);  // MMAs per prefix
+  const int scols = (sh.cat ? 2 : 1) * sh.ntot;  // TMEM columns of one accumulator set
+  P.nacc = std::min(3, std::max(1, (mpp * sh.ng + 17) / 18));
+  if (P.nacc * scols > 512) P.nacc = 512 / scols;
+  P.tbuf_stride = 2 * P.nacc * scols <= 512 ? 256 : 0;  // double-buffered tiles when two fit
   P.dc_mode = dc_mode;
   P.lam = lam;
   P.nparts_total = nparts_total;
@@ -1250,13 +1404,14 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
   const int64_t* aext = MODE < 2 ? g.dims : g.rext;
   int64_t arows = 1;
   for (int a = 0; a < L; ++a) arows *= aext[a];
-  const int namax = (int)std::min<int64_t>(2 * hicu_sm_count(), std::max<int64_t>(1, (arows * 4 + 255) / 256));
+  const int64_t a4n = arows * (T::KA / 4);  // float4 count of the A operand
+  const int namax = (int)std::min<int64_t>(2 * hicu_sm_count(), std::max<int64_t>(1, (a4n + 255) / 256));
   const size_t ib = image_bytes(sh);
-  const size_t split_off = 4096, img_off = split_off + (((size_t)arows * 64 + 1023) & ~(size_t)1023);
+  const size_t split_off = 4096, img_off = split_off + (((size_t)arows * T::RB + 1023) & ~(size_t)1023);
   uint8_t* scr = stream_scratch(st, img_off + (bimg ? 0 : ib));
   if (!scr) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: scratch allocation failed");
   CUtensorMap tm;
-  int s = cached_tmap(&tm, scr + split_off, L, aext, perm);
+  int s = cached_tmap(&tm, scr + split_off, L, aext, perm, CW);
   if (s) return s;
   if (!bimg) {
     s = build_image<MODE>(g, sh, perm, qt, 1, scr + img_off, 0, 0, st);
@@ -1270,7 +1425,7 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
     amax = amax_in;
     namax_used = kAmaxSlot;
   } else {
-    hicu_launch(amax_kernel, namax, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows * 4,
+    hicu_launch(amax_kernel, namax, 256, 0, st, reinterpret_cast<const float4*>(asrc), a4n,
                 reinterpret_cast<float*>(scr));
     if ((s = hicu_check_launch("amax_kernel"))) return s;
   }
@@ -1291,15 +1446,16 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
     for (int a = 0; a < la; ++a) A *= aext[a];
     for (int a = la + 1; a < L; ++a) B *= aext[a];
     const int64_t Lx = aext[la];
-    if (B >= kTT && A <= 65535 && (Lx + kTT - 1) / kTT <= 65535) {
-      hicu_allow_max_smem((const void*)split_t_kernel);
-      const dim3 grid((unsigned)((B + kTT - 1) / kTT), (unsigned)((Lx + kTT - 1) / kTT), (unsigned)A);
-      hicu_launch(split_t_kernel, grid, 256, (size_t)kTT * kTTPitch, st, reinterpret_cast<const float4*>(asrc), Lx, B,
-                  amax, namax_used, reinterpret_cast<uint4*>(scr + split_off));
+    constexpr int TB = TT<CW>::TB;
+    if (B >= TB && A <= 65535 && (Lx + kTT - 1) / kTT <= 65535) {
+      hicu_allow_max_smem((const void*)split_t_kernel<CW>);
+      const dim3 grid((unsigned)((B + TB - 1) / TB), (unsigned)((Lx + kTT - 1) / kTT), (unsigned)A);
+      hicu_launch(split_t_kernel<CW>, grid, 256, (size_t)TT<CW>::SMEM, st, reinterpret_cast<const float4*>(asrc), Lx,
+                  B, amax, namax_used, reinterpret_cast<uint4*>(scr + split_off));
       if ((s = hicu_check_launch("split_t_kernel"))) return s;
     } else {
       const int sb = (int)std::min<int64_t>(8 * hicu_sm_count(), std::max<int64_t>(1, (arows + 255) / 256));
-      hicu_launch(split_kernel, sb, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows, sp,
+      hicu_launch(split_kernel<CW>, sb, 256, 0, st, reinterpret_cast<const float4*>(asrc), arows, sp,
                   amax, namax_used, reinterpret_cast<uint4*>(scr + split_off));
       if ((s = hicu_check_launch("split_kernel"))) return s;
     }
@@ -1309,12 +1465,37 @@ int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, 
   P.amax_out = amax_out;
   P.stage_bytes = (int)sh.stage;
   P.k1 = L == 3 ? sh.kpre[1] : sh.ng;
-  P.abox = L >= 2 ? kGPS * kATile : kATile;
+  P.abox = L >= 2 ? T::ASTAGE : T::ATILE;
   P.bimg = bimg;
   P.bimg_early = bimg_early;
   if (sh.bstream)
-    return launch_bs<MODE, true>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
-  return launch_bs<MODE, false>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
+    return launch_bs<MODE, true, CW>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
+  return launch_bs<MODE, false, CW>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
+}
+
+template <int MODE>
+int launch(const DevGeom& g, const float2* asrc, const float2* qt, float2* out, const float2* uin, const uint8_t* mask,
+           const float2* y, const float2* x0, int dc_mode, float lam, double* parts, int nparts_total,
+           cudaStream_t st) {
+  // the hints are consumed by this launch whatever happens below (an early
+  // error return must not leave them set for an unrelated later call)
+  const uint8_t* bimg = t_bimg;
+  const int bimg_early = t_bimg_early;
+  t_bimg = nullptr;
+  const float* amax_in = t_amax_in;
+  float* amax_out = t_amax_out;
+  t_amax_in = nullptr;
+  t_amax_out = nullptr;
+  int perm[3];
+  choose_perm(g, MODE, perm);
+  Shape sh;
+  if (!shape_of(g, g.nc, &sh, perm))
+    return hicu_set_error(HICU_ERR_SHAPE, "conv_tc: geometry outside the tensor-core scope");
+  if (sh.cw == 8)
+    return launch_cw<MODE, 8>(g, sh, perm, bimg, bimg_early, amax_in, amax_out, asrc, qt, out, uin, mask, y, x0,
+                              dc_mode, lam, parts, nparts_total, st);
+  return launch_cw<MODE, 10>(g, sh, perm, bimg, bimg_early, amax_in, amax_out, asrc, qt, out, uin, mask, y, x0,
+                             dc_mode, lam, parts, nparts_total, st);
 }
 
 }  // namespace

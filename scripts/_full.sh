@@ -4,7 +4,9 @@ timeout 900 python bench.py --no-cpu > gpurun_out/bench_c5.json 2> gpurun_out/be
 python -c "
 import json;d=json.loads(open('gpurun_out/bench_c5.json').read().strip().splitlines()[-1])
 print(d['value'], d['ms_per_step'], d['e2e']['value'], d['kernel_ms_per_step'], d['roofline']['frac'])"
-timeout 900 python bench.py --config C4 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "bench C4 rc $?"
+for c in C3; do
+timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c rc $?"
 python -c "
-import json;d=json.loads(open('gpurun_out/bench_c4.json').read().strip().splitlines()[-1])
+import json;d=json.loads(open('gpurun_out/bench_$c.json').read().strip().splitlines()[-1])
 print(d['value'], d['ms_per_step'], d['e2e']['value'], d['kernel_ms_per_step'])"
+done

@@ -17,12 +17,12 @@ pytestmark = pytest.mark.gpu
 NC = 8
 
 
-def spatial_kernel(sp_ext, sp_support=None):
-    ext = tuple(sp_ext) + (NC,)
+def spatial_kernel(sp_ext, sp_support=None, nc=NC):
+    ext = tuple(sp_ext) + (nc,)
     if sp_support is None:
         sup = np.ones(ext, bool)
     else:
-        sup = np.repeat(np.asarray(sp_support, bool)[..., None], NC, axis=-1)
+        sup = np.repeat(np.asarray(sp_support, bool)[..., None], nc, axis=-1)
     return H.KernelMask(ext, sup)
 
 
@@ -149,3 +149,70 @@ def test_tc_deterministic():
     a = H.objective_and_gradient(x, q, kernel, region, dc)
     b = H.objective_and_gradient(x, q, kernel, region, dc)
     assert np.array_equal(a[0], b[0]) and a[1] == b[1]
+
+
+# 10 coils with p = 10 (C3's kernels: 7x7x10, rank 100): the CW = 10 kernel
+# instantiations -- 20-component rows split into [32 hi | 32 lo] fp16 halves
+# (SW128 operand rows, two K steps), separate hi / lo MMAs (N = 144 > 128).
+NC10 = 10
+CASES10 = {
+    "c3_2d": ((50, 300), spatial_kernel((7, 7), nc=NC10), None),
+    "2d_sub": ((64, 96), spatial_kernel((5, 5), nc=NC10), ((10, 20), (30, 40))),
+    "2d_ell": ((40, 150), spatial_kernel((7, 7), ellipse(7), nc=NC10), None),
+    "3d": ((12, 10, 60), spatial_kernel((3, 3, 3), nc=NC10), None),
+    "2d_nb8": ((20, 200), spatial_kernel((3, 8), nc=NC10), None),
+}
+
+
+def make10(name, seed=0):
+    dims_sp, kernel, reg = CASES10[name]
+    dims = tuple(dims_sp) + (NC10,)
+    if reg is None:
+        region = H.full_region(dims, kernel)
+    else:
+        region = H.Region(tuple(reg[0]) + (0,), tuple(reg[1]) + (1,), frozenset())
+    og = O.Geom(dims, kernel.positions, region.offsets, region.extents, frozenset())
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal(dims) + 1j * rng.standard_normal(dims)).astype(np.complex64).astype(np.complex128)
+    q = (rng.standard_normal((kernel.n, NC10)) + 1j * rng.standard_normal((kernel.n, NC10))) / np.sqrt(kernel.n)
+    q = q.astype(np.complex64).astype(np.complex128)
+    mask = (rng.random(dims[:-1]) < 0.3).astype(np.uint8)
+    mask = np.repeat(mask[..., None], NC10, axis=-1)
+    x0 = x * mask
+    return dims, kernel, region, og, x, q, mask, x0
+
+
+@pytest.mark.parametrize("name", list(CASES10))
+def test_tc10_path_and_conv_scatter(name):
+    dims, kernel, region, og, x, q, mask, x0 = make10(name)
+    assert H.conv_uses_tensor_cores(kernel, region, dims, NC10)
+    assert not H.conv_uses_tensor_cores(kernel, region, dims, 8)
+    tol = tol_for(kernel)
+    u_tc = H.hankel_apply(x, q, kernel, region)
+    u_ref = O.hankel_apply(x, q, og)
+    assert rel(u_tc, u_ref) <= tol
+    g_tc = H.kspace_adjoint_scatter(q, u_ref, kernel, region, dims)
+    g_ref = O.kspace_adjoint_scatter(q, u_ref, og)
+    assert rel(g_tc, g_ref) <= tol
+
+
+@pytest.mark.parametrize("name", list(CASES10))
+@pytest.mark.parametrize("mode", ["hard", "soft"])
+def test_tc10_objective_gradient_els(name, mode):
+    dims, kernel, region, og, x, q, mask, x0 = make10(name, seed=1)
+    tol = tol_for(kernel)
+    dc = H.DataConsistency(mode, mask, x0=x0 if mode == "soft" else None, lam=0.6 if mode == "soft" else 0.0)
+    g_tc, obj_tc, u_tc = H.objective_and_gradient(x, q, kernel, region, dc, return_products=True)
+    eta_tc = H.exact_line_search(x, g_tc, q, kernel, region, dc, u=u_tc)
+    with H.kernel_paths(simt_conv=True):
+        g_s, obj_s, u_s = H.objective_and_gradient(x, q, kernel, region, dc, return_products=True)
+    g_o, obj_o, u_o = O.objective_and_gradient(x, q, og, mask, mode, x0 if mode == "soft" else None,
+                                               0.6 if mode == "soft" else 0.0)
+    eta_o = O.exact_line_search(x, g_o, q, og, mask, u_o, mode, x0 if mode == "soft" else None,
+                                0.6 if mode == "soft" else 0.0)[0]
+    e_tc, e_simt = rel(g_tc, g_o), rel(g_s, g_o)
+    assert e_tc <= max(tol, 1.5 * e_simt), (e_tc, e_simt)
+    assert abs(obj_tc - obj_o) <= 2 * tol * abs(obj_o)
+    assert abs(eta_tc - eta_o) <= 1e-5 * abs(eta_o)
+    if mode == "hard":
+        assert not np.any(g_tc[mask == 1])

@@ -417,7 +417,7 @@ class DeviceWorkload:
             self.engines.append(eng)
             self.resets.append((xd, md))
             self.dims = dims
-        self.streams = [torch.cuda.Stream() for _ in range(min(4, len(self.engines)))] if name == "C3" else None
+        self.streams = [torch.cuda.Stream() for _ in range(min(C3_LANES, len(self.engines)))] if name == "C3" else None
 
     def step(self):
         torch = self.torch
@@ -502,7 +502,7 @@ class DeviceWorkload:
             xl = [self.host[i][2] if i in self.host else None for i in range(n_all)]
             ml = [self.host[i][1] if i in self.host else None for i in range(n_all)]
             out = reconstruct_slices(xl, ml, self.kernel, self.sched, rank=self.rank, world=self.world,
-                                     concurrency=4, tail_energy_threshold=0, coil_compress=cc)
+                                     concurrency=C3_LANES, tail_energy_threshold=0, coil_compress=cc)
             dt = time.perf_counter() - t
             h2d = sum(r.device["h2d_bytes"] for _, r in out.values())
             d2h = sum(r.device["d2h_bytes"] for _, r in out.values())
@@ -511,6 +511,12 @@ class DeviceWorkload:
         _, rep = H.hicu_reconstruct(x0, mask, self.kernel, self.sched, tail_energy_threshold=0, coil_compress=cc)
         dt = time.perf_counter() - t
         return dt, spec.iterations, rep.device["h2d_bytes"], rep.device["d2h_bytes"]
+
+
+# C3: independent slices in flight on one GPU (CUDA streams); the nullspace
+# kernels are single-CTA / 8-CTA-cluster latency chains, so more slices in
+# flight fill more SMs
+C3_LANES = int(os.environ.get("HICU_C3_LANES", "16"))
 
 
 def _work_per_step(dw):

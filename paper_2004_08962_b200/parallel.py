@@ -61,7 +61,7 @@ def partition_slices(n_slices: int, world: int, rank: int) -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
-def reconstruct_slices(x0_slices, masks, kernel, schedule, rank: int = 0, world: int = 1, concurrency: int = 4,
+def reconstruct_slices(x0_slices, masks, kernel, schedule, rank: int = 0, world: int = 1, concurrency: int = 8,
                        **kw):
     """C3-style slice parallelism: reconstruct this rank's block of
     independent slices, ``concurrency`` at a time on separate CUDA streams

@@ -786,7 +786,7 @@ def hicu_reconstruct(x0, mask, kernel: KernelMask, schedule: SolverSchedule, ref
     return xhat, report
 
 
-def hicu_reconstruct_batch(x0s, masks, kernel: KernelMask, schedule: SolverSchedule, *, concurrency: int = 4,
+def hicu_reconstruct_batch(x0s, masks, kernel: KernelMask, schedule: SolverSchedule, *, concurrency: int = 8,
                            **kw):
     """Independent reconstructions (the slices of a multi-slice exam, C3)
     run concurrently on ``concurrency`` CUDA streams of the current device;

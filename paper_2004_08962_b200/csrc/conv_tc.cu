@@ -985,7 +985,7 @@ __global__ void __launch_bounds__(256) split_kernel(const float4* __restrict__ x
 constexpr int kTT = 32;
 template <int CW>
 struct TT {
-  static constexpr int TB = Cw<CW>::RB == 64 ? 32 : 16;      // B rows per tile (<= 64 KB of shared memory)
+  static constexpr int TB = Cw<CW>::RB == 64 ? 8 : 4;        // B rows per tile (16 KB of shared memory)
   static constexpr int PITCH = kTT * Cw<CW>::RB + 32;         // bytes per tile b-row (+32: fewer store conflicts)
   static constexpr int SMEM = TB * PITCH;
 };

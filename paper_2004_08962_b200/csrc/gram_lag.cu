@@ -1236,7 +1236,7 @@ lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict
 constexpr int kE2Lines = 32;
 constexpr int kE2Threads = 288;
 
-__global__ void __launch_bounds__(kE2Threads)
+__global__ void __launch_bounds__(kE2Threads, 2)
 lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
   hicu_pdl_entry();
   constexpr int NC = 8, CB = 2;

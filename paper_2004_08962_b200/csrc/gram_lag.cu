@@ -639,11 +639,26 @@ __global__ void lag_reduceU_kernel(const __grid_constant__ LagParams P, const fl
         const int64_t nlg = (int64_t)P.nol * P.NG;
         const int64_t bid0 = (int64_t)P.chunksA[b] * nlg + (int64_t)ol * P.NG + gzi;
         const int nch = P.chunksA[b + 1] - P.chunksA[b];
-        for (int ch = 0; ch < nch; ++ch) {
-          const float2 v = partA[((bid0 + ch * nlg) * P.GZ + dzi) * NC2 + cc];
-          sx += v.x;
-          sy += v.y;
+        // four independent chains (four loads in flight), combined in a fixed order
+        double ax[4] = {0.0, 0.0, 0.0, 0.0}, ay[4] = {0.0, 0.0, 0.0, 0.0};
+        const float2* pa = partA + (bid0 * P.GZ + dzi) * NC2 + cc;
+        const int64_t cst = nlg * P.GZ * NC2;
+        int ch = 0;
+        for (; ch + 3 < nch; ch += 4) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float2 v = pa[(int64_t)(ch + u) * cst];
+            ax[u] += v.x;
+            ay[u] += v.y;
+          }
         }
+        for (; ch < nch; ++ch) {
+          const float2 v = pa[(int64_t)ch * cst];
+          ax[0] += v.x;
+          ay[0] += v.y;
+        }
+        sx = (ax[0] + ax[1]) + (ax[2] + ax[3]);
+        sy = (ay[0] + ay[1]) + (ay[2] + ay[3]);
       } else {
         int e = 0;
         while (e < P.NE && P.edge_cls[e] != cls) ++e;

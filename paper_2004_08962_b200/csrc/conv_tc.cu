@@ -147,6 +147,11 @@ struct CtParams {
   int abox;               // bytes of one stage's A box (GPS tiles, one when L == 1)
   int ntot;               // MMA N of one precision block: round16(NO nb)
   int cat;                // 1: A_hi [B_hi; B_lo] in one MMA (2 ntot <= 256), else separate hi / lo MMAs
+  // three-line tiles (conv_tri_kernel): a tile computes output lines i, i+1, i+2 along the inner prefix axis
+  int tri;                // 1: B images in the three-line layout (per outer prefix: hi block, lo block)
+  int ko;                 // outer prefix extent (1 when L == 2)
+  int ntri;               // three-line groups along the inner line axis
+  int sd;                 // input lines per stage (k1 + 2: one TMA box)
 };
 
 __device__ __forceinline__ void decode_line(const CtParams& P, int line, int (&lc)[2]) {
@@ -310,6 +315,16 @@ __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, con
   const int g = L == 1 ? 0 : (L == 2 ? spos[sp][0] : spos[sp][0] * P.kpre[1] + spos[sp][1]);
   const int b = spos[sp][L - 1];
   uint8_t* gb = base + (size_t)g * gbytes;
+  if (P.tri) {
+    // three-line layout: per outer prefix go a hi block then a lo block of k1
+    // images each (inner prefix ga1 at image k1 - 1 - ga1 for the conv, ga1
+    // for the scatter), so an MMA's B rows for output slots t_lo..t_hi are
+    // consecutive images; an image's lo rows sit k1 images after its hi rows
+    const int go = L == 3 ? spos[sp][0] : 0, ga1 = L == 3 ? spos[sp][1] : spos[sp][0];
+    const int k1 = L == 3 ? P.kpre[1] : P.kpre[0];
+    const int idx = MODE < 2 ? k1 - 1 - ga1 : ga1;
+    gb = base + (size_t)go * gbytes * k1 + (size_t)idx * P.ntot * T::BROW;
+  }
 #pragma unroll
   for (int tp = 0; tp < 2; ++tp)
 #pragma unroll
@@ -328,7 +343,8 @@ __device__ __forceinline__ void bimage_put(uint8_t* base, const CtParams& P, con
       const float x = v * sb;
       const __half hi = __float2half_rn(x);
       const __half lo = __float2half_rn(x - __half2float(hi));
-      const int rh = b * T::NO + n, rl = P.ntot + rh;
+      const int rh = b * T::NO + n;
+      const int rl = P.tri ? (L == 3 ? P.kpre[1] : P.kpre[0]) * P.ntot + rh : P.ntot + rh;  // tri: lo block k1 images on
       *reinterpret_cast<__half*>(gb + swz<T::BROW>(rh, k >> 3) + (k & 7) * 2) = hi;
       *reinterpret_cast<__half*>(gb + swz<T::BROW>(rl, k >> 3) + (k & 7) * 2) = lo;
     }
@@ -871,6 +887,380 @@ conv_tc_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float
   }
 }
 
+// ---------------------------------------------------------------------------
+// Three-line tiles (8 coils, p = 8, last-axis extent nb <= 5, 2-3 spatial axes).
+//
+// A kind::f16 MMA costs ~175 cycles whatever its N <= 256
+// (scripts/tc_rate2.cu), so the one-line tile above, whose MMAs have N = 160
+// (A_hi [B_hi; B_lo]) and N = 80 (A_lo B_hi), runs the tensor pipe at ~half
+// its rate.  Here a tile computes THREE adjacent output lines i, i+1, i+2
+// along the inner prefix axis.  An input line j (of the k1 + 2 that feed the
+// three) serves output slot t through inner prefix j - t (conv) or
+// t + k1 - 1 - j (scatter); with the prefix images of one outer prefix stored
+// as consecutive images (descending / ascending), the B rows of all valid
+// slots are one contiguous block, so each input line costs three MMAs of
+// N = 80 (#valid slots) <= 240: A_hi B_hi, A_hi B_lo, A_lo B_hi, all into the
+// slots' own columns.  Per three output lines: ko (k1 + 2) 3 MMAs instead of
+// 3 ko k1 2 (C5: 105 instead of 150), and each input line is staged once per
+// three outputs instead of once per output.
+//
+// Pipeline: a stage = one outer prefix go: a depth-(k1 + 2) TMA box of input
+// lines + that prefix's hi / lo image blocks (bulk copy).  Each stage's MMAs
+// accumulate into one of two TMEM sets (240 columns, alternating), reset by
+// an MMA against a zero B block, and are drained by the epilogue as soon as
+// they complete (chains of <= 3 k1 + 1 MMAs, as short as the one-line
+// kernel's).  The epilogue sums the stages in fp32 registers per slot, then
+// runs the one-line kernel's per-tap shift window, carries and fused
+// objective / ELS / data-consistency epilogues for each slot.
+constexpr int kTriNb = 5;
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+conv_tri_kernel(const __grid_constant__ CUtensorMap tmap, const CtParams P, float2* __restrict__ out,
+                const float2* __restrict__ uin, const uint8_t* __restrict__ mask, const float2* __restrict__ y,
+                const float2* __restrict__ x0, double* __restrict__ parts) {
+  constexpr int CW = 8;
+  constexpr int NV = MODE == 0 ? 1 : (MODE == 1 ? 2 : 4);
+  using T = Cw<CW>;
+  constexpr int NH = T::NH, CH = T::CH, NO = T::NO, WROW = T::WROW;
+  constexpr int CARRY = kMaxNb * (kMaxNb - 1) * NO;  // carry floats of one slot
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int nb = P.nb, L = P.L, S = P.stages, sd = P.sd, ko = P.ko;
+  const int k1 = L == 3 ? P.kpre[1] : P.kpre[0];
+  const int nob = P.ntot;  // columns of one output slot (NO nb)
+  const uint32_t hblk = (uint32_t)k1 * nob * T::BROW;  // one outer prefix's hi (or lo) image block
+  const uint32_t abox = (uint32_t)sd * T::ATILE;
+  const int stb = P.stage_bytes;
+  uint8_t* sZero = smem;  // 3 nob zero B rows: the per-stage accumulator reset
+  uint8_t* sStage = smem + 8192;
+  float* sWin = reinterpret_cast<float*>(sStage + (size_t)S * stb);
+  float* tapbuf = sWin;
+  float* carry = sWin + (kTileM + kMaxNb - 1) * WROW;  // [slot][b][nb-1][NO]
+  __shared__ __align__(8) uint64_t full[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tslot;
+  __shared__ double red[kEpiWarps][NV];
+  __shared__ float s_scale[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int inner_ext = P.ldim[L - 2];
+  // debug bit 32: per-role cycle counters, written to `out` (conv forward only; same slots as conv_tc_kernel)
+  __shared__ long long pc[12];
+  const bool pf = (P.debug & 32) != 0;
+  if (threadIdx.x < 12) pc[threadIdx.x] = 0;
+  const int nunits = (L == 3 ? P.ldim[0] : 1) * P.ntri;
+
+  for (int i = threadIdx.x; i < 8192 / 16; i += kThreads) reinterpret_cast<float4*>(sZero)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  tc::fence_proxy_async();  // the zero block is an MMA operand (async proxy)
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&tfull[b], 1);
+      tc::mbar_init(&tempty[b], kEpiWarps);
+    }
+    tc::mbar_init_fence();
+  }
+  if (warp == 1) tc::tmem_alloc(&tslot, 512);
+  hicu_pdl_entry();
+  if (warp == 1) {
+    float m = 0.f;
+    for (int i = lane; i < P.namax; i += 32) m = fmaxf(m, __ldg(P.amax + i));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      const float sa = pow2_scale(m);
+      const float sb = *reinterpret_cast<const float*>(P.bimg + (size_t)P.ng * 2u * nob * T::BROW);
+      s_scale[0] = sa;
+      s_scale[1] = 1.f / (sa * sb);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tslot;
+  if (pf && threadIdx.x == 0) pc[8] = clock64();
+
+  if (warp == 0) {
+    // ---------------- TMA producer: per stage the k1 + 2 input lines of one outer prefix + its image blocks ----------------
+    int s = 0;
+    uint32_t ph = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int lo0 = L == 3 ? u / P.ntri : 0, lin0 = 3 * (u % P.ntri);
+      for (int c = 0; c < P.chunks; ++c)
+        for (int go = 0; go < ko; ++go) {
+          const long long t0p = (pf && lane == 0) ? clock64() : 0;
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          if (pf && lane == 0) pc[0] += clock64() - t0p;
+          const int c1 = MODE < 2 ? P.roff[L - 1] + c * kTileM : c * kTileM;
+          const int c2 = MODE < 2 ? P.roff[L - 2] + lin0 : lin0 - P.roff[L - 2] - (k1 - 1);
+          const int c3 = L == 3 ? (MODE < 2 ? P.roff[0] + lo0 + go : lo0 - P.roff[0] - go) : 0;
+          if (tc::elect_one()) {
+            uint8_t* dst = sStage + (size_t)s * stb;
+            tc::mbar_expect_tx(&full[s], abox + 2u * hblk);
+            tc::tma_load_4d(dst, &tmap, 0, c1, c2, c3, &full[s]);
+            bulk_g2s(dst + abox, P.bimg + (size_t)go * 2u * hblk, 2u * hblk, &full[s]);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint64_t dstage0 = desc_swz<T::RB>(tc::smem_u32(sStage));
+    const uint64_t dimg0 = desc_swz<T::BROW>(tc::smem_u32(sStage + abox));
+    const uint64_t dzero = desc_swz<T::BROW>(tc::smem_u32(sZero));
+    const uint32_t idesc3 = tc::idesc_f16(kTileM, 3 * nob);
+    const uint32_t stb16 = (uint32_t)stb >> 4, img16 = ((uint32_t)nob * T::BROW) >> 4, lo16 = hblk >> 4;
+    int s = 0;
+    uint32_t ph = 0, tcnt = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x)
+      for (int c = 0; c < P.chunks; ++c) {
+        // one TMEM set per tile, alternating: the next tile's MMAs run while the epilogue drains this one
+        const uint32_t set = tcnt & 1u, tp = (tcnt >> 1) & 1u;
+        const uint32_t d = tmem + set * 256u;
+        for (int go = 0; go < ko; ++go) {
+          const long long t0r = (pf && lane == 0) ? clock64() : 0;
+          tc::mbar_wait(&full[s], ph);
+          const long long t1r = (pf && lane == 0) ? clock64() : 0;
+          if (pf && lane == 0) pc[3] += t1r - t0r;
+          if (go == 0) tc::mbar_wait(&tempty[set], tp ^ 1u);  // the epilogue drained this set's previous tile
+          if (pf && lane == 0) pc[4] += clock64() - t1r;
+          tc::fence_after();
+          if (tc::elect_one()) {
+            const uint64_t da = dstage0 + (uint64_t)(s * stb16);
+            const uint64_t db = dimg0 + (uint64_t)(s * stb16);
+            if (go == 0) tc::mma_f16(d, da, dzero, idesc3, 0u);  // reset the set's 3 nob columns
+            for (int j = 0; j < sd; ++j) {
+              const int t_lo = max(0, j - k1 + 1), t_hi = min(2, j);
+              if (t_lo > t_hi) continue;
+              const uint32_t idesc = tc::idesc_f16(kTileM, (t_hi - t_lo + 1) * nob);
+              const uint64_t ah = da + (uint64_t)((j * T::ATILE) >> 4), al = ah + 2u;  // lo half: +32 B of the row
+              const uint64_t bh = db + (uint64_t)((t_lo + k1 - 1 - j) * img16), bl = bh + lo16;
+              const uint32_t dd = d + (uint32_t)(t_lo * nob);
+              tc::mma_f16(dd, ah, bh, idesc, 1u);  // A_hi B_hi
+              tc::mma_f16(dd, ah, bl, idesc, 1u);  // A_hi B_lo
+              tc::mma_f16(dd, al, bh, idesc, 1u);  // A_lo B_hi
+            }
+            tc::mma_commit(&empty[s]);
+            if (go == ko - 1) tc::mma_commit(&tfull[set]);
+          }
+          __syncwarp();
+          if (++s == S) { s = 0; ph ^= 1; }
+        }
+        ++tcnt;
+      }
+  } else {
+    // ---------------- epilogue ----------------
+    const int ew = warp - 2;
+    const int q = warp & 3, h = ew >> 2;
+    const int m = 32 * q + lane;
+    const int et = threadIdx.x - 64;
+    const float inv = s_scale[1];
+    constexpr int NQ4 = NO / 4;
+    double acc_v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc_v[i] = 0.0;
+    float omax = 0.f;
+    uint32_t tcnt = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      const int lo0 = L == 3 ? u / P.ntri : 0, lin0 = 3 * (u % P.ntri);
+      for (int i = et; i < 3 * CARRY; i += kEpiWarps * 32) carry[i] = 0.f;
+      epi_bar();
+      for (int c = 0; c < P.chunks; ++c) {
+        const uint32_t set = tcnt & 1u, tp = (tcnt >> 1) & 1u;
+        {
+          const long long t0e = (pf && et == 0) ? clock64() : 0;
+          tc::mbar_wait(&tfull[set], tp);
+          if (pf && et == 0) pc[6] += clock64() - t0e;
+        }
+        tc::fence_after();
+        const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + set * 256u + (uint32_t)(NH * h);
+        const long long t0w = (pf && et == 0) ? clock64() : 0;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          const int inner = lin0 + t;
+          if (inner >= inner_ext) continue;  // uniform: the partial group at the end of the inner axis
+          const int64_t obase = L == 3 ? (int64_t)lo0 * P.ostride[0] + (int64_t)inner * P.ostride[1]
+                                       : (int64_t)inner * P.ostride[0];
+          float* cy = carry + t * CARRY;
+          // this slot's accumulators (nb taps x NH floats of this thread's row)
+          float f[kTriNb][NH];
+          {
+            uint32_t v0[kTriNb][NH];
+#pragma unroll
+            for (int b = 0; b < kTriNb; ++b)
+              if (b < nb) tc::tmem_ld8_nowait(ta + (uint32_t)(t * nob + b * NO), v0[b]);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int b = 0; b < kTriNb; ++b)
+#pragma unroll
+              for (int i = 0; i < NH; ++i) f[b][i] = __uint_as_float(v0[b][i]);
+          }
+          // this slot's epilogue inputs from global memory
+          DcIn<CH> din{};
+          float2 upre[CH];
+#pragma unroll
+          for (int i = 0; i < CH; ++i) upre[i] = make_float2(0.f, 0.f);
+          if (MODE == 2) {
+            const int x = P.roff[L - 1] + c * kTileM + m;
+            if (x < P.ext_last) din = dc_load<CH>(P, (size_t)(obase + (int64_t)x * P.lstride) * CW, h, mask, y, x0);
+          } else if (MODE == 1) {
+            const int i_out = c * kTileM - (nb - 1) + m;
+            if (i_out >= 0 && i_out < P.ext_last) {
+              const float4* up = reinterpret_cast<const float4*>(uin + (size_t)(obase + (int64_t)i_out * P.lstride) * CW + CH * h);
+              const float4 a0 = __ldg(up), a1 = __ldg(up + 1);
+              upre[0] = make_float2(a0.x, a0.y);
+              upre[1] = make_float2(a0.z, a0.w);
+              upre[2] = make_float2(a1.x, a1.y);
+              upre[3] = make_float2(a1.z, a1.w);
+            }
+          }
+          // shifted sums, one tap at a time (as in conv_tc_kernel)
+          float v[NH];
+#pragma unroll
+          for (int i = 0; i < NH; ++i) v[i] = 0.f;
+#pragma unroll
+          for (int b = 0; b < kTriNb; ++b) {
+            if (b < nb) {
+              if (et < (nb - 1) * NQ4) {
+                const int r = et / NQ4, kk = et - r * NQ4;
+                reinterpret_cast<float4*>(tapbuf + r * WROW)[kk] =
+                    reinterpret_cast<const float4*>(cy + (b * (kMaxNb - 1) + r) * NO)[kk];
+              }
+              const int w = MODE < 2 ? m + b : nb - 1 + m - b;
+              float4* w4 = reinterpret_cast<float4*>(tapbuf + (nb - 1 + m) * WROW + NH * h);
+              w4[0] = make_float4(f[b][0] * inv, f[b][1] * inv, f[b][2] * inv, f[b][3] * inv);
+              w4[1] = make_float4(f[b][4] * inv, f[b][5] * inv, f[b][6] * inv, f[b][7] * inv);
+              epi_bar();
+              const float4* r4 = reinterpret_cast<const float4*>(tapbuf + w * WROW + NH * h);
+              const float4 t0 = r4[0], t1 = r4[1];
+              v[0] += t0.x; v[1] += t0.y; v[2] += t0.z; v[3] += t0.w;
+              v[4] += t1.x; v[5] += t1.y; v[6] += t1.z; v[7] += t1.w;
+              if (et < (nb - 1) * NQ4) {
+                const int r = et / NQ4, kk = et - r * NQ4;
+                reinterpret_cast<float4*>(cy + (b * (kMaxNb - 1) + r) * NO)[kk] =
+                    reinterpret_cast<const float4*>(tapbuf + (kTileM + r) * WROW)[kk];
+              }
+              epi_bar();
+            }
+          }
+          if (MODE < 2) {
+            const int i_out = c * kTileM - (nb - 1) + m;
+            if (i_out < 0 || i_out >= P.ext_last) continue;
+            const int64_t idx = obase + (int64_t)i_out * P.lstride;
+            if (MODE == 0) {
+              float4* up = reinterpret_cast<float4*>(out + (size_t)idx * CW + CH * h);
+              if (!pf) {  // counter mode keeps `out` for its records
+                up[0] = make_float4(v[0], v[1], v[2], v[3]);
+                up[1] = make_float4(v[4], v[5], v[6], v[7]);
+              }
+              double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+              for (int i = 0; i < NH; i += 2) {
+                s0 += (double)v[i] * v[i];
+                s1 += (double)v[i + 1] * v[i + 1];
+                omax = fmaxf(omax, fmaxf(fabsf(v[i]), fabsf(v[i + 1])));
+              }
+              acc_v[0] += s0 + s1;
+            } else {
+              double d0 = 0.0, d1 = 0.0, n0 = 0.0, n1 = 0.0;
+#pragma unroll
+              for (int i = 0; i < CH; ++i) {
+                const float2 uu = upre[i];
+                if (i & 1) d1 += (double)v[2 * i] * uu.x + (double)v[2 * i + 1] * uu.y;
+                else d0 += (double)v[2 * i] * uu.x + (double)v[2 * i + 1] * uu.y;
+              }
+#pragma unroll
+              for (int i = 0; i < NH; i += 2) {
+                n0 += (double)v[i] * v[i];
+                n1 += (double)v[i + 1] * v[i + 1];
+              }
+              acc_v[0] += d0 + d1;
+              acc_v[NV - 1] += n0 + n1;
+            }
+          } else {
+            const int x = P.roff[L - 1] + c * kTileM + m;
+            if (x >= P.ext_last) continue;
+            double a4[4] = {0, 0, 0, 0};
+            omax = fmaxf(omax, scatter_store<CH>(P, (size_t)(obase + (int64_t)x * P.lstride) * CW, h, v, din, out, a4));
+#pragma unroll
+            for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
+          }
+        }
+        if (pf && et == 0) pc[10] += clock64() - t0w;
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[set]);  // all three slots read
+        ++tcnt;
+      }
+      if (MODE == 2) {
+        // positions no tile covers (before the region's reach / past the last tile): DC term only
+        const int x_lo = P.roff[L - 1], x_hi = P.roff[L - 1] + P.chunks * kTileM;
+        float vz[NH];
+#pragma unroll
+        for (int i = 0; i < NH; ++i) vz[i] = 0.f;
+        for (int t = 0; t < 3; ++t) {
+          const int inner = lin0 + t;
+          if (inner >= inner_ext) break;
+          const int64_t obase = L == 3 ? (int64_t)lo0 * P.ostride[0] + (int64_t)inner * P.ostride[1]
+                                       : (int64_t)inner * P.ostride[0];
+          for (int x = m; x < P.ext_last; x += kTileM) {
+            if (x >= x_lo && x < x_hi) continue;
+            double a4[4] = {0, 0, 0, 0};
+            const size_t e0 = (size_t)(obase + (int64_t)x * P.lstride) * CW;
+            omax = fmaxf(omax, scatter_store<CH>(P, e0, h, vz, dc_load<CH>(P, e0, h, mask, y, x0), out, a4));
+#pragma unroll
+            for (int i = 0; i < NV; ++i) acc_v[i] += a4[i > 3 ? 3 : i];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const double t = warp_sum_d(acc_v[i]);
+      if (lane == 0) red[ew][i] = t;
+    }
+    epi_bar();
+    if (ew == 0 && lane < NV) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < kEpiWarps; ++w) t += red[w][lane];
+      parts[(size_t)blockIdx.x * NV + lane] = t;
+    }
+    if (blockIdx.x == 0)
+      for (int i = et + (int)gridDim.x * NV; i < P.nparts_total * NV; i += kEpiWarps * 32) parts[i] = 0.0;
+    if (P.amax_out) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) omax = fmaxf(omax, __shfl_xor_sync(0xffffffffu, omax, o));
+      __shared__ float wmx[kEpiWarps];
+      if (lane == 0) wmx[ew] = omax;
+      epi_bar();
+      if (et == 0) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < kEpiWarps; ++w) t = fmaxf(t, wmx[w]);
+        P.amax_out[blockIdx.x] = t;
+      }
+      if (blockIdx.x == 0)
+        for (int i = (int)gridDim.x + et; i < kAmaxSlot; i += kEpiWarps * 32) P.amax_out[i] = 0.f;
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (pf && threadIdx.x == 0) pc[9] = clock64();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+  if (pf && threadIdx.x == 0 && MODE == 0) {
+    pc[9] -= pc[8];
+    long long* o = reinterpret_cast<long long*>(out) + (size_t)blockIdx.x * 12;
+    for (int i = 0; i < 12; ++i) o[i] = pc[i];
+  }
+}
+
 // B images (fp16 hi/lo, scaled) for one Q~, written once to global memory so
 // each conv CTA copies them with one bulk copy; the power-of-two scale sits
 // in a trailer after the ng images.  One CTA per image.
@@ -1115,7 +1505,7 @@ EncodeTiledFn encode_tiled() {
 // ext[perm[L-3]]) with the array's own strides (any spatial axis can be the
 // tile axis), 128-row x 16-float boxes (one per stage), no swizzle (only the converter warps
 // read the fp32 tile: linear 16-byte reads), zero fill out of bounds.
-int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm, int cw) {
+int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm, int cw, int depth) {
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: cuTensorMapEncodeTiled unavailable");
   // the split array is stored in kernel axis order: line axis perm[L-1] fastest; rows of
@@ -1125,7 +1515,8 @@ int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, cons
                         (cuuint64_t)(L >= 3 ? ext[perm[L - 3]] : 1)};
   cuuint64_t strides[3] = {(cuuint64_t)rb, rb * dims[1], rb * dims[1] * dims[2]};
   // depth GPS along dimension 2: a stage's prefix groups are adjacent lines
-  cuuint32_t box[4] = {(cuuint32_t)(2 * kp), (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? gps : 1), 1}, es[4] = {1, 1, 1, 1};
+  cuuint32_t box[4] = {(cuuint32_t)(2 * kp), (cuuint32_t)kTileM, (cuuint32_t)(L >= 2 ? (depth > 0 ? depth : gps) : 1), 1},
+             es[4] = {1, 1, 1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, rb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1135,10 +1526,10 @@ int make_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, cons
 
 // Tensor maps depend only on (pointer, extents, axis order): a small
 // per-thread cache keeps cuTensorMapEncodeTiled off the per-launch path.
-int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm, int cw) {
+int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, const int* perm, int cw, int depth) {
   struct Entry {
     const void* base;
-    int L, cw;
+    int L, cw, depth;
     int64_t ext[3];
     int perm[3];
     CUtensorMap map;
@@ -1147,19 +1538,20 @@ int cached_tmap(CUtensorMap* tm, const void* base, int L, const int64_t* ext, co
   static thread_local int used = 0, next = 0;
   for (int i = 0; i < used; ++i) {
     const Entry& e = cache[i];
-    bool same = e.base == base && e.L == L && e.cw == cw;
+    bool same = e.base == base && e.L == L && e.cw == cw && e.depth == depth;
     for (int d = 0; d < L && same; ++d) same = e.ext[d] == ext[d] && e.perm[d] == perm[d];
     if (same) {
       *tm = e.map;
       return HICU_OK;
     }
   }
-  const int st = make_tmap(tm, base, L, ext, perm, cw);
+  const int st = make_tmap(tm, base, L, ext, perm, cw, depth);
   if (st) return st;
   Entry& e = cache[next];
   e.base = base;
   e.L = L;
   e.cw = cw;
+  e.depth = depth;
   for (int d = 0; d < 3; ++d) {
     e.ext[d] = d < L ? ext[d] : 0;
     e.perm[d] = d < L ? perm[d] : 0;
@@ -1228,6 +1620,16 @@ void choose_perm(const DevGeom& g, int MODE, int (&perm)[3]) {
   for (int d = L; d < 3; ++d) perm[d] = d;
 }
 
+// HICU_CONV_TC_TRI=0 keeps the one-line tiles (A/B measurement of the three-line kernel)
+bool tri_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HICU_CONV_TC_TRI");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 struct Shape {
   int L, nb, ng, kpre[2];
   int cw;            // complex row width (8 or 10)
@@ -1236,6 +1638,9 @@ struct Shape {
   int bstream;       // B images copied per stage (they do not fit resident)
   size_t stage;      // bytes per pipeline stage
   size_t fixed;      // resident B images + window + alignment slack
+  int tri;           // three-line tiles (conv_tri_kernel) and their B-image layout
+  int sd;            // tri: input lines per stage (k1 + 2)
+  size_t tstage, tfixed;  // tri: bytes per stage, fixed bytes (zero block + window + 3 carries + slack)
 };
 
 template <int CW>
@@ -1271,6 +1676,18 @@ bool shape_cw(const DevGeom& g, Shape* sh, const int* perm) {
     sh->bstream = 1;
     sh->stage = T::ASTAGE + T::GPS * sh->gbytes;
     sh->fixed = win + 1024;
+  }
+  // three-line tiles: 8 coils, 3 slots x 16 nb <= 256 MMA columns, a
+  // depth-(k1 + 2) box of input lines per stage, >= 2 stages
+  sh->tri = 0;
+  if (CW == 8 && L >= 2 && nb <= kTriNb && !(tri_disabled())) {
+    const int k1 = L == 3 ? sh->kpre[1] : sh->kpre[0];
+    sh->sd = k1 + 2;
+    const size_t twin = ((size_t)((kTileM + kMaxNb - 1) * T::WROW + 3 * kMaxNb * (kMaxNb - 1) * T::NO) * 4 + 1023) &
+                        ~(size_t)1023;
+    sh->tfixed = 8192 + twin + 1024;
+    sh->tstage = ((size_t)sh->sd * T::ATILE + 2 * (size_t)k1 * ntot * T::BROW + 1023) & ~(size_t)1023;
+    if (sh->sd <= 8 && sh->tfixed + 2 * sh->tstage <= (size_t)kSmemBudget) sh->tri = 1;
   }
   return sh->fixed + 3 * sh->stage <= (size_t)kSmemBudget;
 }
@@ -1320,7 +1737,40 @@ int launch_bs(const Shape& sh, CtParams P, const CUtensorMap& tm, float2* out, c
   return hicu_check_launch("conv_tc_kernel");
 }
 
+template <int MODE>
+int launch_tri(const Shape& sh, CtParams P, const CUtensorMap& tm, float2* out, const float2* uin, const uint8_t* mask,
+               const float2* y, const float2* x0, double* parts, int nparts_total, cudaStream_t st) {
+  constexpr int kMaxDev = 64;
+  static std::atomic<size_t> avail_a[kMaxDev];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  hicu_allow_max_smem((const void*)conv_tri_kernel<MODE>);
+  size_t avail = (dev >= 0 && dev < kMaxDev) ? avail_a[dev].load(std::memory_order_acquire) : 0;
+  if (!avail) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, (const void*)conv_tri_kernel<MODE>);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    avail = (size_t)optin - fa.sharedSizeBytes;
+    if (dev >= 0 && dev < kMaxDev) avail_a[dev].store(avail, std::memory_order_release);
+  }
+  if (avail < sh.tfixed + 2 * sh.tstage) return hicu_set_error(HICU_ERR_SIZE, "conv_tc: shared memory (three-line tiles)");
+  P.stage_bytes = (int)sh.tstage;
+  P.stages = (int)std::min<size_t>(kMaxStages, (avail - sh.tfixed) / sh.tstage);
+  const size_t smem = sh.tfixed + (size_t)P.stages * sh.tstage;
+  P.ntri = (P.ldim[P.L - 2] + 2) / 3;
+  const int64_t units = (int64_t)(P.L == 3 ? P.ldim[0] : 1) * P.ntri;
+  int64_t grid = std::min<int64_t>(units, hicu_sm_count());
+  if (grid > nparts_total) grid = nparts_total;
+  if (grid < 1) grid = 1;
+  hicu_launch(conv_tri_kernel<MODE>, (int)grid, kThreads, smem, st, tm, P, out, uin, mask, y, x0, parts);
+  return hicu_check_launch("conv_tri_kernel");
+}
+
 void fill_shape_params(CtParams& P, const DevGeom& g, const Shape& sh, const int (&perm)[3]) {
+  P.tri = sh.tri;
+  P.ko = sh.L == 3 ? sh.kpre[0] : 1;
+  P.sd = sh.sd;
   P.ntot = sh.ntot;
   P.cat = sh.cat;
   for (int d = 0; d < 3; ++d) P.perm[d] = perm[d];
@@ -1411,7 +1861,7 @@ int launch_cw(const DevGeom& g, const Shape& sh, const int (&perm)[3], const uin
   uint8_t* scr = stream_scratch(st, img_off + (bimg ? 0 : ib));
   if (!scr) return hicu_set_error(HICU_ERR_CUDA, "conv_tc: scratch allocation failed");
   CUtensorMap tm;
-  int s = cached_tmap(&tm, scr + split_off, L, aext, perm, CW);
+  int s = cached_tmap(&tm, scr + split_off, L, aext, perm, CW, sh.tri ? sh.sd : 0);
   if (s) return s;
   if (!bimg) {
     s = build_image<MODE>(g, sh, perm, qt, 1, scr + img_off, 0, 0, st);
@@ -1468,6 +1918,7 @@ int launch_cw(const DevGeom& g, const Shape& sh, const int (&perm)[3], const uin
   P.abox = L >= 2 ? T::ASTAGE : T::ATILE;
   P.bimg = bimg;
   P.bimg_early = bimg_early;
+  if (sh.tri) return launch_tri<MODE>(sh, P, tm, out, uin, mask, y, x0, parts, nparts_total, st);
   if (sh.bstream)
     return launch_bs<MODE, true, CW>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);
   return launch_bs<MODE, false, CW>(sh, P, tm, out, uin, mask, y, x0, parts, lines, nparts_total, st);

@@ -15,8 +15,8 @@ echo "launch list rc $?"
 python scripts/summarize_launches.py gpurun_out/launches_$T.csv gpurun_out/launches_$T.md > /dev/null 2>&1
 prof() { timeout 900 ncu --set full --clock-control none --import-source on -k "regex:$1" -s $2 -c $3 -o gpurun_out/prof_$4_$T -f $CMD > gpurun_out/ncu_$4_$T.log 2>&1; echo "ncu $4 rc $?"; }
 prof "lagtc_core|lag_edge2" 2 2 gram
-prof conv_tc_kernel 15 3 conv
-prof "split_kernel|amax_kernel" 30 2 split
+prof "conv_tri_kernel|conv_tc_kernel" 15 3 conv
+prof "split_t_kernel|split_kernel|amax_kernel" 30 2 split
 prof update_kernel 5 1 update
 python scripts/ncu_summary.py gpurun_out/prof_gram_$T.ncu-rep gpurun_out/prof_conv_$T.ncu-rep gpurun_out/prof_split_$T.ncu-rep gpurun_out/prof_update_$T.ncu-rep \
     -o gpurun_out/ncu_full_summary_$T.md --json gpurun_out/ncu_full_$T.json > /dev/null 2>&1

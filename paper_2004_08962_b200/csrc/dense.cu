@@ -605,6 +605,103 @@ void trsm_rl_launch(int n, int ell, const double2* Y, const double2* Om, const d
   hicu_launch(trsm_rl_kernel<PER>, (n + warps - 1) / warps, warps * 32, smem, st, n, ell, Y, Om, nu, R, W);
 }
 
+// Streaming variant for ell > 112 (R no longer fits one SM's shared memory:
+// C3 / C4 / C5, ell = 150 / 225 / 180): the same right-looking steps, with the
+// rows of R staged kTrsJB at a time through a double-buffered cp.async ring
+// shared by the CTA's warps (one row of Y per warp, every warp walks the
+// blocks in lockstep).  trsm_rows_kernel read R column-wise from L2 with a
+// warp reduction per column: 250 / 430 us at ell = 180 / 225.
+constexpr int kTrsJB = 16;
+constexpr int kTrsWarps = 8;
+
+template <int PER>
+__global__ void __launch_bounds__(kTrsWarps * 32)
+trsm_rls_kernel(int n, int ell, const double2* __restrict__ Y, const double2* __restrict__ Om,
+                const double* __restrict__ nu_p, const double2* __restrict__ R, double2* __restrict__ W) {
+  hicu_pdl_entry();
+  extern __shared__ double2 smr[];
+  double2* sR = smr;                                                          // 2 x kTrsJB x ell
+  double* rinv = reinterpret_cast<double*>(sR + (size_t)2 * kTrsJB * ell);   // 1 / R_jj
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nblk = (ell + kTrsJB - 1) / kTrsJB;
+  auto stage = [&](int b) {
+    const int j0 = b * kTrsJB, rows = min(kTrsJB, ell - j0);
+    double2* dst = sR + (size_t)(b & 1) * kTrsJB * ell;
+    const double2* src = R + (size_t)j0 * ell;
+    for (int e = tid; e < rows * ell; e += kTrsWarps * 32)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(dst + e)),
+                   "l"(src + e)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(0);
+  for (int j = tid; j < ell; j += kTrsWarps * 32) rinv[j] = 1.0 / R[(size_t)j * ell + j].x;
+  const double nu = *nu_p;
+  const int row = blockIdx.x * kTrsWarps + warp;
+  const bool live = row < n;
+  int kc[PER];
+  double2 acc[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int j = lane + 32 * u;
+    kc[u] = min(j, ell - 1);
+    acc[u] = (live && j < ell) ? Y[(size_t)row * ell + j] + nu * Om[(size_t)row * ell + j] : cd(0.0, 0.0);
+  }
+  for (int b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) {
+      stage(b + 1);  // its buffer was last read in block b - 1 (barrier at the end of that block)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double2* blk = sR + (size_t)(b & 1) * kTrsJB * ell;
+    const int j0 = b * kTrsJB, rows = min(kTrsJB, ell - j0);
+    for (int jj = 0; jj < rows; ++jj) {
+      const int j = j0 + jj;
+      const double2* Rj = blk + (size_t)jj * ell;
+      double2 rj[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) rj[u] = Rj[kc[u]];
+      const double ri = rinv[j];
+      const int uj = j >> 5;
+      double2 wj = acc[0];
+#pragma unroll
+      for (int u = 1; u < PER; ++u) wj = (u == uj) ? acc[u] : wj;
+      wj = ri * wj;
+      wj.x = __shfl_sync(0xffffffffu, wj.x, j & 31);
+      wj.y = __shfl_sync(0xffffffffu, wj.y, j & 31);
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int k = lane + 32 * u;
+        const double2 t = acc[u] - cmul(wj, rj[u]);
+        acc[u] = (k == j) ? wj : ((k > j) ? t : acc[u]);
+      }
+    }
+    __syncthreads();  // block b's buffer is free for block b + 2
+  }
+  if (live) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int j = lane + 32 * u;
+      if (j < ell) W[(size_t)row * ell + j] = acc[u];
+    }
+  }
+}
+
+template <int PER>
+void trsm_rls_launch(int n, int ell, const double2* Y, const double2* Om, const double* nu, const double2* R,
+                     double2* W, cudaStream_t st) {
+  if (PER * 32 < ell) {
+    if constexpr (PER < kTrsmMaxPer) trsm_rls_launch<PER + 1>(n, ell, Y, Om, nu, R, W, st);
+    return;
+  }
+  const size_t smem = (size_t)2 * kTrsJB * ell * sizeof(double2) + (size_t)ell * sizeof(double);
+  hicu_allow_max_smem((const void*)trsm_rls_kernel<PER>);
+  hicu_launch(trsm_rls_kernel<PER>, (n + kTrsWarps - 1) / kTrsWarps, kTrsWarps * 32, smem, st, n, ell, Y, Om, nu, R,
+              W);
+}
+
 // ---------------------------------------------------------------------------
 // Cyclic parallel two-sided Jacobi for a Hermitian PSD matrix (round-robin
 // ordering).  Logs every rotation (p, q, c, s*e^{i phi}) so the same unitary
@@ -1456,6 +1553,9 @@ extern "C" int hicu_nystrom(int n, int ell, int r, const void* G, const void* om
     if (rbytes + (size_t)ell * sizeof(double) <= kSmemCap) {
       trsm_rl_launch<1>(n, ell, w.Y, Om, w.nu, w.C, w.W, rbytes + (size_t)ell * sizeof(double), st);
       if ((s = hicu_check_launch("trsm_rl_kernel"))) return s;
+    } else if (ell <= 32 * kTrsmMaxPer) {
+      trsm_rls_launch<4>(n, ell, w.Y, Om, w.nu, w.C, w.W, st);
+      if ((s = hicu_check_launch("trsm_rls_kernel"))) return s;
     } else {
     const int warps = 8;
     const size_t rowb = (size_t)warps * ell * sizeof(double2);

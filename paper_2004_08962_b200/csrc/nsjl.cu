@@ -22,6 +22,8 @@
 // stage driver's gated Householder kernels (dense.cu) recompute Q~ the
 // reference way.  Verified against the reference's householder_nullspace to
 // ~1e-15 (tests/test_gpu_ops.py::test_nullspace_jl_*).
+#include <cooperative_groups.h>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -533,6 +535,79 @@ nsjl_lu_global_kernel(int r, const double2* __restrict__ V, double2* __restrict_
   }
 }
 
+// The same LU on one 8-CTA thread-block cluster (the default for these
+// ranks): row i of A_1 lives in the shared memory of CTA i % 8 (cyclic, so the
+// shrinking trailing block stays balanced).  Step k: the owner of row k
+// writes U[k][k..r) into every CTA's shared memory with DSMEM stores
+// (double-buffered by step parity), one cluster barrier, then every CTA
+// forms l = A[i][k] / U[k][k] for its rows i > k (stored to global at once:
+// column k is never read again) and folds row k into them, a warp per row.
+// Same arithmetic per element as nsjl_lu_global_kernel (l = a * (1 / pivot),
+// a -= l * u), same outputs (LUg: U on and above the diagonal, L below;
+// idg = 1 / pivot; pd = |pivot|^2; *gate).  The single CTA streaming the
+// trailing block through L2 took 0.48 / 0.85 ms at r = 120 / 150.
+constexpr int kLcCS = 8;
+constexpr int kLcThreads = 512;
+constexpr int kLcMaxR = 256;
+
+__global__ void __cluster_dims__(kLcCS, 1, 1) __launch_bounds__(kLcThreads, 1)
+nsjl_lu_cluster_kernel(int r, const double2* __restrict__ V, double2* __restrict__ LUg, double2* __restrict__ idg,
+                       double* __restrict__ pd, int* __restrict__ gate) {
+  hicu_pdl_entry();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  extern __shared__ double2 lcA[];  // [nr][r]: rows cr, cr + 8, ...
+  __shared__ double2 srow[2][kLcMaxR];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kLcThreads / 32;
+  const int nr = (r - cr + kLcCS - 1) / kLcCS;
+  for (int q = tid; q < nr * r; q += kLcThreads) {
+    const int rl = q / r, j = q - rl * r, i = cr + kLcCS * rl;
+    double2 v = V[(size_t)i * r + j];
+    if (i == j) v.x -= 1.0;
+    lcA[q] = v;
+  }
+  bool bad = false;
+  cluster.sync();
+  for (int k = 0; k < r; ++k) {
+    const int buf = k & 1;
+    if (cr == k % kLcCS) {
+      const double2* row = lcA + (size_t)(k / kLcCS) * r;
+      const int m = r - k;
+      for (int q = tid; q < kLcCS * m; q += kLcThreads) {
+        const int c = q / m, j = k + (q - c * m);
+        *cluster.map_shared_rank(&srow[buf][j], c) = row[j];
+      }
+    }
+    cluster.sync();
+    const double2 piv = srow[buf][k];
+    const double p2 = abs2d(piv);
+    const double2 inv = nsjl_inv(piv);
+    bad |= !(p2 >= kPivotFloor * kPivotFloor);  // NaN -> fallback
+    if (cr == k % kLcCS && tid == 0) {
+      idg[k] = inv;
+      pd[k] = p2;
+    }
+    // fold row k into this CTA's rows i > k
+    const int first = k >= cr ? (k - cr) / kLcCS + 1 : 0;
+    for (int rl = first + warp; rl < nr; rl += nw) {
+      double2* Ai = lcA + (size_t)rl * r;
+      const double2 l = cmul(Ai[k], inv);
+      if (lane == 0) LUg[(size_t)(cr + kLcCS * rl) * r + k] = l;
+      for (int j = k + 1 + lane; j < r; j += 32) Ai[j] = Ai[j] - cmul(l, srow[buf][j]);
+    }
+    __syncthreads();  // the next owner reads its updated row
+  }
+  // U: rows are final from their own step on
+  for (int q = tid; q < nr * r; q += kLcThreads) {
+    const int rl = q / r, j = q - rl * r, i = cr + kLcCS * rl;
+    if (j >= i) LUg[(size_t)i * r + j] = lcA[q];
+  }
+  if (cr == 0 && tid == 0) *gate = bad ? 1 : 0;
+  cluster.sync();
+}
+
 template <int CT, int NT>
 __global__ void __launch_bounds__(NT)
 nsjl_big_kernel(int n, int r, const double2* __restrict__ V, int cols, const double2* __restrict__ Pin,
@@ -616,8 +691,22 @@ extern "C" int hicu_nullspace_jl_ws(int n, int r, const void* V, int cols, const
     double2* idg = Lg + (size_t)r * r;
     double* pd = (double*)(idg + r);
     cudaStream_t st = (cudaStream_t)stream;
-    hicu_launch(nsjl_lu_global_kernel, 1, kLuThreads, 0, st, r, (const double2*)V, LUg, Lg, idg, pd, gate_dev);
-    int s = hicu_check_launch("nsjl_lu_global_kernel");
+    // one 8-CTA cluster holds A_1 in distributed shared memory; the single-CTA
+    // global-memory LU stays for ranks beyond it (and HICU_NSJL_LU_GLOBAL=1, tests)
+    static const bool force_global = [] {
+      const char* e = getenv("HICU_NSJL_LU_GLOBAL");
+      return e && e[0] == '1';
+    }();
+    const size_t lsm = (size_t)((r + kLcCS - 1) / kLcCS) * r * sizeof(double2);
+    int s;
+    if (!force_global && r <= kLcMaxR && lsm <= (size_t)200 * 1024) {
+      hicu_allow_max_smem((const void*)nsjl_lu_cluster_kernel);
+      hicu_launch(nsjl_lu_cluster_kernel, kLcCS, kLcThreads, lsm, st, r, (const double2*)V, LUg, idg, pd, gate_dev);
+      s = hicu_check_launch("nsjl_lu_cluster_kernel");
+    } else {
+      hicu_launch(nsjl_lu_global_kernel, 1, kLuThreads, 0, st, r, (const double2*)V, LUg, Lg, idg, pd, gate_dev);
+      s = hicu_check_launch("nsjl_lu_global_kernel");
+    }
     if (s) return s;
     const int ct = nsjl_big_ct(r), nt = nsjl_big_nt(ct);
     const size_t fixed = nsjl_big_fixed(n, r, ct, nt);

@@ -1,0 +1,8 @@
+cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc $?"; tail -5 gpurun_out/pytest_gpu.log
+for c in C4 C3 C5; do
+timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err; echo "bench $c rc $?"
+python -c "
+import json;d=json.loads(open('gpurun_out/bench_$c.json').read().strip().splitlines()[-1])
+print(round(d['value'],2), round(d['ms_per_step'],2), round(d['e2e']['value'],2), {k:round(v,2) for k,v in d['kernel_ms_per_step'].items()})"
+done

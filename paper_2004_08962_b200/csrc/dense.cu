@@ -130,6 +130,76 @@ zgemm_panel_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restr
   if (row < m && col < n) C[(size_t)row * ldc + col] = (c0 + c1) + (c2 + c3);
 }
 
+// Long-K variant (K > kZgK: the Nystrom products over n = 490 / 1000 rows):
+// 32 x 32 output tiles, 2 x 2 outputs per thread, K chunks of 32 staged
+// K-major through a double-buffered cp.async ring (coalesced along the
+// contiguous global index for either op), conjugation applied as a sign when
+// the panels are read.  zgemm_kernel above pays two block barriers and an L2
+// round trip per 16-wide chunk with one output per thread (120 - 145 us per
+// call at C5 / C4).
+constexpr int kZtT = 32, kZtK = 32, kZtLd = kZtT + 1;
+
+__global__ void __launch_bounds__(256)
+zgemm_tile_kernel(bool ca, bool cb, int m, int n, int k, const double2* __restrict__ A, int lda,
+                  const double2* __restrict__ B, int ldb, double2* __restrict__ C, int ldc) {
+  hicu_pdl_entry();
+  extern __shared__ double2 zt[];
+  double2* As = zt;                        // [2][kZtK][kZtLd]: op(A)(row0 + i, l0 + l) at [l][i]
+  double2* Bs = zt + 2 * kZtK * kZtLd;     // [2][kZtK][kZtLd]: op(B)(l0 + l, col0 + j) at [l][j]
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int row0 = blockIdx.y * kZtT, col0 = blockIdx.x * kZtT;
+  auto stage = [&](int c, int buf) {
+    const int l0 = c * kZtK;
+    for (int e = tid; e < kZtT * kZtK; e += 256) {
+      const int i = ca ? e % kZtT : e / kZtK, l = ca ? e / kZtT : e % kZtK;
+      double2* dst = As + ((size_t)buf * kZtK + l) * kZtLd + i;
+      const int row = row0 + i, ll = l0 + l;
+      if (row < m && ll < k) zp_cp16(dst, ca ? A + (size_t)ll * lda + row : A + (size_t)row * lda + ll);
+      else *dst = cd(0.0, 0.0);
+    }
+    for (int e = tid; e < kZtT * kZtK; e += 256) {
+      const int j = cb ? e / kZtK : e % kZtT, l = cb ? e % kZtK : e / kZtT;
+      double2* dst = Bs + ((size_t)buf * kZtK + l) * kZtLd + j;
+      const int col = col0 + j, ll = l0 + l;
+      if (col < n && ll < k) zp_cp16(dst, cb ? B + (size_t)col * ldb + ll : B + (size_t)ll * ldb + col);
+      else *dst = cd(0.0, 0.0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const double sa = ca ? -1.0 : 1.0, sb = cb ? -1.0 : 1.0;
+  double2 c00 = cd(0.0, 0.0), c01 = c00, c10 = c00, c11 = c00;
+  const int nch = (k + kZtK - 1) / kZtK;
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nch) {
+      stage(c + 1, buf ^ 1);  // last read in chunk c - 1 (barrier at the end of that chunk)
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double2* a = As + (size_t)buf * kZtK * kZtLd;
+    const double2* b = Bs + (size_t)buf * kZtK * kZtLd;
+#pragma unroll 8
+    for (int l = 0; l < kZtK; ++l) {
+      double2 a0 = a[l * kZtLd + ty], a1 = a[l * kZtLd + ty + 16];
+      double2 b0 = b[l * kZtLd + tx], b1 = b[l * kZtLd + tx + 16];
+      a0.y *= sa, a1.y *= sa, b0.y *= sb, b1.y *= sb;
+      zfma(c00, a0, b0);
+      zfma(c01, a0, b1);
+      zfma(c10, a1, b0);
+      zfma(c11, a1, b1);
+    }
+    __syncthreads();
+  }
+  const int r0 = row0 + ty, r1 = r0 + 16, q0 = col0 + tx, q1 = q0 + 16;
+  if (r0 < m && q0 < n) C[(size_t)r0 * ldc + q0] = c00;
+  if (r0 < m && q1 < n) C[(size_t)r0 * ldc + q1] = c01;
+  if (r1 < m && q0 < n) C[(size_t)r1 * ldc + q0] = c10;
+  if (r1 < m && q1 < n) C[(size_t)r1 * ldc + q1] = c11;
+}
+
 int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int lda, const double2* B, int ldb,
                  double2* C, int ldc, cudaStream_t st) {
   if (k <= kZgK) {
@@ -138,6 +208,13 @@ int zgemm_launch(char opa, char opb, int m, int n, int k, const double2* A, int 
     dim3 grid((n + 15) / 16, (m + 15) / 16);
     hicu_launch(zgemm_panel_kernel, grid, 256, smem, st, opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
     return hicu_check_launch("zgemm_panel_kernel");
+  }
+  if (m * (size_t)n >= 4096) {
+    const size_t smem = (size_t)4 * kZtK * kZtLd * sizeof(double2);
+    hicu_allow_max_smem((const void*)zgemm_tile_kernel);
+    dim3 grid((n + kZtT - 1) / kZtT, (m + kZtT - 1) / kZtT);
+    hicu_launch(zgemm_tile_kernel, grid, 256, smem, st, opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);
+    return hicu_check_launch("zgemm_tile_kernel");
   }
   dim3 grid((n + 15) / 16, (m + 15) / 16);
   hicu_launch(zgemm_kernel, grid, 256, 0, st, opa == 'C', opb == 'C', m, n, k, A, lda, B, ldb, C, ldc);

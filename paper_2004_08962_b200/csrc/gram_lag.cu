@@ -1250,6 +1250,7 @@ lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict
 // lag_edge_kernel.
 constexpr int kE2Lines = 32;
 constexpr int kE2Threads = 288;
+constexpr int kE2LS = 8 * 8 + 2, kE2RS = 24 * (8 + 2) + 2;  // float2 per staged line (base edges, neighbour window)
 
 __global__ void __launch_bounds__(kE2Threads, 2)
 lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
@@ -1263,8 +1264,12 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
   const int hi_base = P.cls_beg[la][P.edge_cls[K - 1]] - (K - 1);      // first right edge - (K - 1)
   const int NL = (int)P.N[la];
   extern __shared__ __align__(16) uint8_t e2sm[];
-  float2 (*sL)[8][NC] = reinterpret_cast<float2 (*)[8][NC]>(e2sm);                          // base-line edge positions
-  float2 (*sR)[24][NC] = reinterpret_cast<float2 (*)[24][NC]>(e2sm + kE2Lines * 8 * NC * 8);  // neighbour positions
+  // base-line edge positions: [line][8][NC]; neighbour positions: [line][24][NC + 2] -- rows padded
+  // to 5 16-byte chunks (80 B) so the 8 rows a warp reads at once (its 8 lags) fall on distinct banks
+  // (64-byte rows: 4-way conflicts); both line strides are an odd number of chunks (staging stores)
+  constexpr int LS = kE2LS, RS = kE2RS, RW = NC + 2;
+  float2* sL = reinterpret_cast<float2*>(e2sm);
+  float2* sR = sL + kE2Lines * LS;
   __shared__ int64_t sbase[kE2Lines], snbr[kE2Lines];
   const int bidx = blockIdx.x;
   const int ol = bidx / P.CBt;
@@ -1305,12 +1310,12 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
         const int r = i / per, rem = i - r * per, j = rem >> 2, pc4 = rem & 3;
         if (r < P.NE) {
           const int pos = P.cls_beg[la][P.edge_cls[r]];
-          reinterpret_cast<float4*>(&sL[j][r][0])[pc4] =
+          reinterpret_cast<float4*>(sL + j * LS + r * NC)[pc4] =
               __ldg(reinterpret_cast<const float4*>(x + sbase[j] + pos * ls) + pc4);
         } else {
           const int k = r - P.NE;
           const int pos = k < W ? lo_base + k : hi_base + k - W;
-          reinterpret_cast<float4*>(&sR[j][k][0])[pc4] =
+          reinterpret_cast<float4*>(sR + j * RS + k * RW)[pc4] =
               (pos >= 0 && pos < NL) ? __ldg(reinterpret_cast<const float4*>(x + snbr[j] + pos * ls) + pc4)
                                      : make_float4(0.f, 0.f, 0.f, 0.f);
         }
@@ -1320,9 +1325,9 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
         for (int j = 0; j < nl; ++j) {
           float2 a[CB], bv[NC];
 #pragma unroll
-          for (int u = 0; u < CB; ++u) a[u] = sL[j][e][cbi * CB + u];
+          for (int u = 0; u < CB; ++u) a[u] = sL[j * LS + e * NC + cbi * CB + u];
 #pragma unroll
-          for (int c = 0; c < NC; ++c) bv[c] = sR[j][ridx][c];
+          for (int c = 0; c < NC; ++c) bv[c] = sR[j * RS + ridx * RW + c];
 #pragma unroll
           for (int u = 0; u < CB; ++u)
 #pragma unroll
@@ -1425,7 +1430,7 @@ int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
   }
   if (pl.nB > 0 && pl.tc && P.NQ <= kE2Threads && P.NE == 2 * (P.K[P.L - 1] - 1)) {
     hicu_allow_max_smem((const void*)lag_edge2_kernel);
-    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), kE2Threads, (size_t)kE2Lines * 32 * NC * 8, st, P, x,
+    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), kE2Threads, (size_t)kE2Lines * (kE2LS + kE2RS) * 8, st, P, x,
                 partB);
     if ((s = hicu_check_launch("lag_edge2_kernel"))) return s;
   } else if (pl.nB > 0) {

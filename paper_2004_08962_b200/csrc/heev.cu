@@ -200,12 +200,10 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
   }
   for (int q = cr * kHcThreads + tid; q < l * l; q += kHcCS * kHcThreads) Vt[q] = cd(0.0, 0.0);
   cluster.sync();
-  bool prebuilt = false;  // step k's reflector was built inside step k - 1's update (uniform over the cluster)
   for (int k = 0; k + 1 < l; ++k) {
     const int buf = k & 1, k1 = k + 1, m = l - k1;
     // ---- (a) the owner of row k forms the reflector and broadcasts v, tau ----
-    if (!prebuilt) __syncthreads();  // the owner reads its updated row
-    if (!prebuilt && cr == k % kHcCS) {
+    if (cr == k % kHcCS) {
       const double2* row = hcA + (size_t)(k / kHcCS) * lda;
       if (warp == 0) {
         double t = 0.0;
@@ -243,10 +241,7 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
     }
     cluster.sync();  // v, tau everywhere
     const double2 tk = s_tau[buf];
-    if (tk.x == 0.0 && tk.y == 0.0) {  // uniform over the cluster
-      prebuilt = false;
-      continue;
-    }
+    if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform over the cluster
     // ---- (b) y = A22 v for this CTA's rows, w = tau y, broadcast w and w^H v ----
     double2 pz = cd(0.0, 0.0);
     for (int r = warp; r < nr; r += nw) {
@@ -279,8 +274,9 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
     for (int c = 0; c < kHcCS; ++c) dot = dot + pdot[buf][c];
     const double2 td = cmul(tk, dot);
     const double2 a2 = cd(-0.5 * td.x, -0.5 * td.y);
-    auto update_row = [&](int r) {
+    for (int r = warp; r < nr; r += nw) {
       const int i = cr + kHcCS * r;
+      if (i < k1) continue;
       const double2 vi = sv[buf][i];
       const double2 wi = sw[buf][i] + cmul(a2, vi);
       double2* Ai = hcA + (size_t)r * lda;
@@ -289,55 +285,9 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
         const double2 wj = sw[buf][j] + cmul(a2, vj);
         Ai[j] = Ai[j] - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
       }
-    };
-    // One-step lookahead: warp 0 of the owner of row k + 1 updates that row
-    // first and builds step k + 1's reflector (e, d, tau, v broadcast into
-    // the other parity's buffers) while the other warps / CTAs are still
-    // updating, so the next step starts at its first cluster barrier.
-    const bool look = k1 + 1 < l;
-    const int rnext = (look && cr == k1 % kHcCS) ? k1 / kHcCS : -1;
-    if (rnext >= 0 && warp == 0) {
-      update_row(rnext);
-      __syncwarp();
-      const double2* row = hcA + (size_t)rnext * lda;
-      const int nb = buf ^ 1, k2 = k1 + 1;
-      double t = 0.0;
-      for (int j = k2 + 1 + lane; j < l; j += 32) t += abs2d(row[j]);
-      t = warp_sum_d(t);
-      const double2 alpha = conjd(row[k2]);
-      double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
-      double beta;
-      if (t == 0.0 && alpha.y == 0.0) {
-        beta = alpha.x;  // H = I
-      } else {
-        beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + t), alpha.x);
-        const double ib = 1.0 / beta;
-        tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
-        const double2 den = cd(alpha.x - beta, alpha.y);
-        const double idd = 1.0 / abs2d(den);
-        scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
-      }
-      if (lane == 0) {
-        e[k1] = beta;
-        d[k1] = row[k1].x;
-        tau[k1] = tv;
-      }
-      if (lane < kHcCS) *cluster.map_shared_rank(&s_tau[nb], lane) = tv;
-      const int m2 = l - k2;
-      for (int q = lane; q < kHcCS * m2; q += 32) {
-        const int c = q / m2, j = k2 + (q - c * m2);
-        const double2 v = j == k2 ? cd(1.0, 0.0) : cmul(conjd(row[j]), scal);
-        *cluster.map_shared_rank(&sv[nb][j], c) = v;
-        if (c == 0) Vt[(size_t)k1 * l + j] = v;
-      }
     }
-    for (int r = warp; r < nr; r += nw) {
-      if (cr + kHcCS * r < k1 || r == rnext) continue;
-      update_row(r);
-    }
-    prebuilt = look;  // the next step's first cluster barrier orders the update and the broadcasts
+    __syncthreads();  // the next owner reads its updated row
   }
-  __syncthreads();
   if (cr == (l - 1) % kHcCS && tid == 0) d[l - 1] = hcA[(size_t)((l - 1) / kHcCS) * lda + (l - 1)].x;
   cluster.sync();  // no CTA exits while others may still write into its shared memory
 }

@@ -671,10 +671,12 @@ static bool nsjl_small_ok(int n, int r) {
 
 extern "C" int hicu_nullspace_jl_supported(int n, int r) { return (nsjl_small_ok(n, r) || nsjl_big_ok(n, r)) ? 1 : 0; }
 
-extern "C" size_t hicu_nullspace_jl_workspace(int n, int r) {
-  if (nsjl_small_ok(n, r) || !nsjl_big_ok(n, r)) return 0;
-  return nsjl_big_ws(r);
-}
+// The cluster LU + per-column CTAs serve every rank above the warp-column LU
+// (r > 64) that fits them: the single-CTA kernel's barrier-per-step LU,
+// redundant in each of its CTAs, took 0.78 ms at C3's r = 100.
+static bool nsjl_use_big(int n, int r) { return nsjl_big_ok(n, r) && (r > 64 || !nsjl_small_ok(n, r)); }
+
+extern "C" size_t hicu_nullspace_jl_workspace(int n, int r) { return nsjl_use_big(n, r) ? nsjl_big_ws(r) : 0; }
 
 extern "C" int hicu_nullspace_jl_ws(int n, int r, const void* V, int cols, const void* Bin, void* B, void* out32,
                                     int p, int* gate_dev, void* ws, size_t ws_bytes, void* stream) {
@@ -682,7 +684,7 @@ extern "C" int hicu_nullspace_jl_ws(int n, int r, const void* V, int cols, const
     return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad arguments");
   if (out32 && (p < 1 || cols % p != 0)) return hicu_set_error(HICU_ERR_PARAMETER, "nullspace_jl: bad p");
   if (!hicu_nullspace_jl_supported(n, r)) return hicu_set_error(HICU_ERR_SIZE, "nullspace_jl: rank not supported");
-  if (!nsjl_small_ok(n, r)) {
+  if (nsjl_use_big(n, r) && (!nsjl_small_ok(n, r) || (ws && ws_bytes >= nsjl_big_ws(r)))) {
     const size_t need = nsjl_big_ws(r);
     if (!ws || ws_bytes < need) return hicu_set_error(HICU_ERR_WORKSPACE, "nullspace_jl: workspace too small");
     uint8_t* w = (uint8_t*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);

@@ -1248,7 +1248,7 @@ lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict
 // staging load is a coalesced run of 64-byte rows (the per-thread
 // gathers of lag_edge_kernel were latency-bound).  Same partial layout as
 // lag_edge_kernel.
-constexpr int kE2Lines = 32;
+constexpr int kE2Lines = 16;
 constexpr int kE2Threads = 288;
 constexpr int kE2LS = 8 * 8 + 2, kE2RS = 24 * (8 + 2) + 2;  // float2 per staged line (base edges, neighbour window)
 
@@ -1264,13 +1264,13 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
   const int hi_base = P.cls_beg[la][P.edge_cls[K - 1]] - (K - 1);      // first right edge - (K - 1)
   const int NL = (int)P.N[la];
   extern __shared__ __align__(16) uint8_t e2sm[];
-  // base-line edge positions: [line][8][NC]; neighbour positions: [line][24][NC + 2] -- rows padded
-  // to 5 16-byte chunks (80 B) so the 8 rows a warp reads at once (its 8 lags) fall on distinct banks
-  // (64-byte rows: 4-way conflicts); both line strides are an odd number of chunks (staging stores)
-  constexpr int LS = kE2LS, RS = kE2RS, RW = NC + 2;
-  float2* sL = reinterpret_cast<float2*>(e2sm);
-  float2* sR = sL + kE2Lines * LS;
-  __shared__ int64_t sbase[kE2Lines], snbr[kE2Lines];
+  // Two staging buffers of kE2Lines lines each.  Per line: the base line's edge positions [8][NC] and the
+  // neighbour window [24][NC + 2] -- rows padded to 5 16-byte chunks (80 B) so the 8 rows a warp reads at
+  // once (its 8 lags) fall on distinct banks; both line strides are an odd number of chunks (staging
+  // stores).  The next sub-chunk's lines are in flight (cp.async) while this one is multiplied.
+  constexpr int LS = kE2LS, RS = kE2RS, RW = NC + 2, BUF = kE2Lines * (kE2LS + kE2RS);
+  float2* sbuf = reinterpret_cast<float2*>(e2sm);
+  __shared__ int64_t sbase[2][kE2Lines], snbr[2][kE2Lines];
   const int bidx = blockIdx.x;
   const int ol = bidx / P.CBt;
   const int chunk = bidx % P.CBt;  // global chunk id over blocks
@@ -1297,31 +1297,53 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
 #pragma unroll
     for (int c = 0; c < NC; ++c) accR[a][c] = accI[a][c] = cf(0.f, 0.f);
   const int64_t ls = P.cstride[la];
-  if (ok) {
-    for (int64_t lb = l0; lb < l1; lb += kE2Lines) {
+  if (ok && l0 < l1) {
+    auto offsets = [&](int64_t lb, int bf) {
+      if (lb + t < l1 && t < kE2Lines) line_offsets(P, beg, len, ol, lb + t, sbase[bf][t], snbr[bf][t]);
+    };
+    // 16-byte pieces; consecutive threads -> the pieces of one position row across consecutive lines
+    // (adjacent 64-byte rows in memory)
+    auto issue = [&](int64_t lb, int bf) {
       const int nl = (int)min((int64_t)kE2Lines, l1 - lb);
-      __syncthreads();  // the previous sub-chunk's reads are done
-      if (t < nl) line_offsets(P, beg, len, ol, lb + t, sbase[t], snbr[t]);
-      __syncthreads();
-      // stage: 16-byte pieces; consecutive threads -> the pieces of one position
-      // row across consecutive lines (adjacent 64-byte rows in memory)
+      float2* sL = sbuf + (size_t)bf * BUF;
+      float2* sR = sL + kE2Lines * LS;
       const int per = 4 * nl;
       for (int i = t; i < (P.NE + NR) * per; i += kE2Threads) {
         const int r = i / per, rem = i - r * per, j = rem >> 2, pc4 = rem & 3;
         if (r < P.NE) {
           const int pos = P.cls_beg[la][P.edge_cls[r]];
-          reinterpret_cast<float4*>(sL + j * LS + r * NC)[pc4] =
-              __ldg(reinterpret_cast<const float4*>(x + sbase[j] + pos * ls) + pc4);
+          cp_async16(reinterpret_cast<float4*>(sL + j * LS + r * NC) + pc4,
+                     reinterpret_cast<const float4*>(x + sbase[bf][j] + pos * ls) + pc4);
         } else {
           const int k = r - P.NE;
           const int pos = k < W ? lo_base + k : hi_base + k - W;
-          reinterpret_cast<float4*>(sR + j * RS + k * RW)[pc4] =
-              (pos >= 0 && pos < NL) ? __ldg(reinterpret_cast<const float4*>(x + snbr[j] + pos * ls) + pc4)
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+          float4* dst = reinterpret_cast<float4*>(sR + j * RS + k * RW) + pc4;
+          if (pos >= 0 && pos < NL) cp_async16(dst, reinterpret_cast<const float4*>(x + snbr[bf][j] + pos * ls) + pc4);
+          else *dst = make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-      __syncthreads();
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    offsets(l0, 0);
+    __syncthreads();
+    issue(l0, 0);
+    int it = 0;
+    for (int64_t lb = l0; lb < l1; lb += kE2Lines, ++it) {
+      const int bf = it & 1;
+      const int64_t nx = lb + kE2Lines;
+      const int nl = (int)min((int64_t)kE2Lines, l1 - lb);
+      if (nx < l1) offsets(nx, bf ^ 1);
+      __syncthreads();  // the next offsets are visible; the other buffer's reads (previous sub-chunk) are done
+      if (nx < l1) {
+        issue(nx, bf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();  // this sub-chunk has landed for every thread
       if (act) {
+        const float2* sL = sbuf + (size_t)bf * BUF;
+        const float2* sR = sL + kE2Lines * LS;
         for (int j = 0; j < nl; ++j) {
           float2 a[CB], bv[NC];
 #pragma unroll
@@ -1430,7 +1452,7 @@ int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
   }
   if (pl.nB > 0 && pl.tc && P.NQ <= kE2Threads && P.NE == 2 * (P.K[P.L - 1] - 1)) {
     hicu_allow_max_smem((const void*)lag_edge2_kernel);
-    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), kE2Threads, (size_t)kE2Lines * (kE2LS + kE2RS) * 8, st, P, x,
+    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), kE2Threads, (size_t)2 * kE2Lines * (kE2LS + kE2RS) * 8, st, P, x,
                 partB);
     if ((s = hicu_check_launch("lag_edge2_kernel"))) return s;
   } else if (pl.nB > 0) {

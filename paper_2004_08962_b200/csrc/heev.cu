@@ -200,48 +200,67 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
   }
   for (int q = cr * kHcThreads + tid; q < l * l; q += kHcCS * kHcThreads) Vt[q] = cd(0.0, 0.0);
   cluster.sync();
-  for (int k = 0; k + 1 < l; ++k) {
-    const int buf = k & 1, k1 = k + 1, m = l - k1;
-    // ---- (a) the owner of row k forms the reflector and broadcasts v, tau ----
-    if (cr == k % kHcCS) {
-      const double2* row = hcA + (size_t)(k / kHcCS) * lda;
-      if (warp == 0) {
-        double t = 0.0;
-        for (int j = k + 2 + lane; j < l; j += 32) t += abs2d(row[j]);
-        t = warp_sum_d(t);
-        if (lane == 0) {
-          const double2 alpha = conjd(row[k1]);
-          double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
-          double beta;
-          if (t == 0.0 && alpha.y == 0.0) {
-            beta = alpha.x;  // H = I
-          } else {
-            beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + t), alpha.x);
-            const double ib = 1.0 / beta;
-            tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
-            const double2 den = cd(alpha.x - beta, alpha.y);
-            const double idd = 1.0 / abs2d(den);
-            scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
-          }
-          e[k] = beta;
-          d[k] = row[k].x;
-          tau[k] = tv;
-          s_scal = scal;
-          for (int c = 0; c < kHcCS; ++c) *cluster.map_shared_rank(&s_tau[buf], c) = tv;
+  // (a) the owner of row kk forms reflector kk from conj(row kk) and broadcasts v, tau into the
+  // buffers of parity kk & 1; called by every thread of the owner CTA (row kk is final and visible)
+  auto build_reflector = [&](int kk) {
+    const int nb = kk & 1, kk1 = kk + 1, mm = l - kk1;
+    const double2* row = hcA + (size_t)(kk / kHcCS) * lda;
+    if (warp == 0) {
+      double t = 0.0;
+      for (int j = kk + 2 + lane; j < l; j += 32) t += abs2d(row[j]);
+      t = warp_sum_d(t);
+      if (lane == 0) {
+        const double2 alpha = conjd(row[kk1]);
+        double2 tv = cd(0.0, 0.0), scal = cd(0.0, 0.0);
+        double beta;
+        if (t == 0.0 && alpha.y == 0.0) {
+          beta = alpha.x;  // H = I
+        } else {
+          beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + t), alpha.x);
+          const double ib = 1.0 / beta;
+          tv = cd((beta - alpha.x) * ib, -alpha.y * ib);
+          const double2 den = cd(alpha.x - beta, alpha.y);
+          const double idd = 1.0 / abs2d(den);
+          scal = cd(den.x * idd, -den.y * idd);  // 1 / (alpha - beta)
         }
-      }
-      __syncthreads();
-      const double2 sc = s_scal;
-      for (int q = tid; q < kHcCS * m; q += kHcThreads) {
-        const int c = q / m, j = k1 + (q - c * m);
-        const double2 v = j == k1 ? cd(1.0, 0.0) : cmul(conjd(row[j]), sc);
-        *cluster.map_shared_rank(&sv[buf][j], c) = v;
-        if (c == 0) Vt[(size_t)k * l + j] = v;
+        e[kk] = beta;
+        d[kk] = row[kk].x;
+        tau[kk] = tv;
+        s_scal = scal;
+        for (int c = 0; c < kHcCS; ++c) *cluster.map_shared_rank(&s_tau[nb], c) = tv;
       }
     }
-    cluster.sync();  // v, tau everywhere
+    __syncthreads();
+    const double2 sc = s_scal;
+    for (int q = tid; q < kHcCS * mm; q += kHcThreads) {
+      const int c = q / mm, j = kk1 + (q - c * mm);
+      const double2 v = j == kk1 ? cd(1.0, 0.0) : cmul(conjd(row[j]), sc);
+      *cluster.map_shared_rank(&sv[nb][j], c) = v;
+      if (c == 0) Vt[(size_t)kk * l + j] = v;
+    }
+  };
+  // Split cluster barrier: every CTA arrives as soon as it has nothing more to publish for the
+  // next step (the next owner: after broadcasting the next reflector) and waits only when it
+  // needs that reflector, so the rank-2 update of the other rows runs under the barrier.
+  auto arrive = [] { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); };
+  auto wait = [] { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); };
+  if (l > 1) {
+    if (cr == 0) build_reflector(0);
+    arrive();
+  }
+  for (int k = 0; k + 1 < l; ++k) {
+    const int buf = k & 1, k1 = k + 1;
+    const bool more = k1 + 1 < l;  // reflector k + 1 exists
+    wait();                        // v, tau of step k everywhere
     const double2 tk = s_tau[buf];
-    if (tk.x == 0.0 && tk.y == 0.0) continue;  // uniform over the cluster
+    if (tk.x == 0.0 && tk.y == 0.0) {  // H = I (uniform over the cluster): nothing to update
+      if (more) {
+        __syncthreads();  // row k + 1 was last updated by another warp (the wait above orders arrivals only)
+        if (cr == k1 % kHcCS) build_reflector(k1);
+        arrive();
+      }
+      continue;
+    }
     // ---- (b) y = A22 v for this CTA's rows, w = tau y, broadcast w and w^H v ----
     double2 pz = cd(0.0, 0.0);
     for (int r = warp; r < nr; r += nw) {
@@ -274,9 +293,26 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
     for (int c = 0; c < kHcCS; ++c) dot = dot + pdot[buf][c];
     const double2 td = cmul(tk, dot);
     const double2 a2 = cd(-0.5 * td.x, -0.5 * td.y);
+    // the next pivot row first (one element per thread), then its reflector, then the barrier arrival
+    const int rnext = (more && cr == k1 % kHcCS) ? k1 / kHcCS : -1;
+    if (more) {
+      if (rnext >= 0) {
+        const double2 vi = sv[buf][k1];
+        const double2 wi = sw[buf][k1] + cmul(a2, vi);
+        double2* Ai = hcA + (size_t)rnext * lda;
+        for (int j = k1 + tid; j < l; j += kHcThreads) {
+          const double2 vj = sv[buf][j];
+          const double2 wj = sw[buf][j] + cmul(a2, vj);
+          Ai[j] = Ai[j] - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
+        }
+        __syncthreads();
+        build_reflector(k1);
+      }
+      arrive();
+    }
     for (int r = warp; r < nr; r += nw) {
       const int i = cr + kHcCS * r;
-      if (i < k1) continue;
+      if (i < k1 || r == rnext) continue;
       const double2 vi = sv[buf][i];
       const double2 wi = sw[buf][i] + cmul(a2, vi);
       double2* Ai = hcA + (size_t)r * lda;
@@ -286,8 +322,8 @@ hetrd_cluster_kernel(int l, const double2* __restrict__ Ain, double* __restrict_
         Ai[j] = Ai[j] - cmul(vi, conjd(wj)) - cmul(wi, conjd(vj));
       }
     }
-    __syncthreads();  // the next owner reads its updated row
   }
+  __syncthreads();
   if (cr == (l - 1) % kHcCS && tid == 0) d[l - 1] = hcA[(size_t)((l - 1) / kHcCS) * lda + (l - 1)].x;
   cluster.sync();  // no CTA exits while others may still write into its shared memory
 }

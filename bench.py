@@ -573,8 +573,8 @@ def roofline(kinds, work, peaks, sm_mhz=None, profiled=True):
     # CUDA-core fp32 peak (FFMA2: 148 SMs x 128 lanes x 2 flop at the max SM clock)
     fp32_peak = 148 * 128 * 2 * (peaks.get("sm_max_mhz", 1965.0) * 1e6) / 1e12
     ncu = {rec["kernel"]: rec for rec in _load_json("profiles/r02_ncu_full.json", [])}
-    ncu_name = {"gram": "lagtc_core_kernel", "conv_fwd": "conv_tc_kernel<0", "scatter": "conv_tc_kernel<2",
-                "conv_els": "conv_tc_kernel<1", "update": "update_kernel"}
+    ncu_name = {"gram": "lagtc_core_kernel", "conv_fwd": "conv_tri_kernel<0", "scatter": "conv_tri_kernel<2",
+                "conv_els": "conv_tri_kernel<1", "update": "update_kernel"}
 
     def traffic(kind):
         if not profiled:  # the committed ncu captures are of the C5 workload
@@ -619,20 +619,33 @@ def roofline(kinds, work, peaks, sm_mhz=None, profiled=True):
         if ms_by.get(k, 0) > 0:
             roof_all[k] = {"bound": "fp64 latency (small dense algebra, reported separately, SURVEY 8d)",
                            "ms_per_step": ms_by[k]}
+    # The dominant kernel: the three convolution classes are launches of ONE kernel template
+    # (conv_tri_kernel / conv_tc_kernel<MODE>), the Gram class is several kernels; the template with
+    # the largest summed time in the step wins, and of the convolution template its slowest
+    # instantiation is the roofline object.  roofline_all keeps every class.
     tens = [k for k in roof_all if roof_all[k]["bound"] == "tensor"]
-    dom = max(tens, key=lambda k: ms_by[k]) if tens else None
+    convs = [k for k in ("conv_fwd", "scatter", "conv_els") if k in tens]
+    conv_ms = sum(ms_by[k] for k in convs)
+    if convs and conv_ms >= ms_by.get("gram", 0.0):
+        dom = max(convs, key=lambda k: ms_by[k])
+    else:
+        dom = max(tens, key=lambda k: ms_by[k]) if tens else None
     roof = dict(roof_all[dom]) if dom else None
     if roof:
         top = max((k for k in roof_all if k in ms_by), key=lambda k: ms_by[k])
         roof.update({"kernel": dom,
+                     "dominant_rule": ("kernel template with the largest summed time in the step "
+                                       f"(convolution template {conv_ms:.2f} ms, Gram class "
+                                       f"{ms_by.get('gram', 0.0):.2f} ms); its slowest instantiation"),
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense 16-bit tensor rate) / 3: "
                                     "three fp16 MMA products per FP32-grade product",
                      "achieved_def": "algorithmic flops of the class in one step / its summed CUDA-event time "
                                      "(native profiler, one extra step on the launching stream)",
                      "traffic_def": "ncu dram read+write bytes per launch (profiles/r02_ncu_full.json)",
                      "achieved_note": "includes the operand split passes (amax + fp16 hi/lo split) inside each call",
-                     "note": ("the dominant tensor-core class; the largest class overall is "
-                              f"{top} ({roof_all[top]['bound']})") if top != dom else "the largest class"})
+                     "note": (f"the largest class overall is {top} ({roof_all[top]['bound']}"
+                              + (f", frac {roof_all[top]['frac']:.3f}" if "frac" in roof_all[top] else "")
+                              + "), see roofline_all") if top != dom else "also the largest class"})
     return roof, roof_all
 
 

@@ -58,3 +58,34 @@ def test_eigh_top_matches_numpy():
     Vh = V.cpu().numpy()
     P1, P2 = Vh @ Vh.conj().T, vec[:, ::-1][:, :r] @ vec[:, ::-1][:, :r].conj().T
     assert np.linalg.norm(P1 - P2, 2) <= 1e-8
+
+
+def test_eigh_top_block_diagonal_identity_reflector():
+    """Two decoupled Hermitian blocks: at the block boundary the column below
+    the diagonal is exactly zero, so the tridiagonalisation takes its
+    H = I branch (tau = 0) in the middle of the reduction -- on the cluster
+    kernel that branch re-arms the split barrier without an update phase."""
+    import torch
+
+    from paper_2004_08962_b200 import _native as nat
+
+    rng = np.random.default_rng(9)
+    n1, n2, r = 60, 90, 30
+    n = n1 + n2
+    a1 = rng.standard_normal((n1, n1)) + 1j * rng.standard_normal((n1, n1))
+    a2 = rng.standard_normal((n2, n2)) + 1j * rng.standard_normal((n2, n2))
+    A = np.zeros((n, n), np.complex128)
+    A[:n1, :n1] = a1 @ a1.conj().T
+    A[n1:, n1:] = a2 @ a2.conj().T
+    L = nat.lib()
+    Ad = torch.as_tensor(A).cuda()
+    ev = torch.empty(r, dtype=torch.float64, device="cuda")
+    V = torch.empty((n, r), dtype=torch.complex128, device="cuda")
+    ws = torch.empty(int(L.hicu_eigh_top_workspace(n, r)), dtype=torch.uint8, device="cuda")
+    nat.check(L.hicu_eigh_top(n, r, Ad.data_ptr(), ev.data_ptr(), V.data_ptr(), ws.data_ptr(), ws.numel(),
+                              nat.stream_handle()))
+    lam, vec = np.linalg.eigh(A)
+    assert np.allclose(ev.cpu().numpy(), lam[::-1][:r], rtol=1e-10)
+    Vh = V.cpu().numpy()
+    P1, P2 = Vh @ Vh.conj().T, vec[:, ::-1][:, :r] @ vec[:, ::-1][:, :r].conj().T
+    assert np.linalg.norm(P1 - P2, 2) <= 1e-8

@@ -1283,13 +1283,34 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
   const int64_t l0 = (int64_t)ch * P.lpcB, l1 = min(nlines, l0 + P.lpcB);
   const bool ok = neighbour_ok(P, beg, len, ol);
   const int t = threadIdx.x;
-  const int q = t;  // (e * DZ + dz) * NCB + cbi
-  const bool qok = q < P.NQ;
-  const int e = q / (P.DZ * P.NCB), dzi = (q / P.NCB) % P.DZ, cbi = q % P.NCB;
+  // Output slot q = (e * DZ + dz) * NCB + cbi.  An (edge position, lag) pair whose neighbour
+  // position falls outside the line contributes nothing (28 % of the pairs for 5 taps), so the
+  // threads are dealt the ACTIVE pairs in slot order: the products fill the first warps densely
+  // and the remaining warps only stage (they also write the zero partials of the inactive slots).
+  auto pair_pr = [&](int pair) { return P.cls_beg[la][P.edge_cls[pair / P.DZ]] + pair % P.DZ - (K - 1); };
+  const int npairs = P.NE * P.DZ;
+  __shared__ int s_pairs[kE2Threads], s_nact;  // the active pairs in slot order (built by warp 0)
+  if (t < 32) {
+    int base = 0;
+    for (int r0 = 0; r0 < npairs; r0 += 32) {
+      const int pair = r0 + t;
+      const int prp = pair < npairs ? pair_pr(pair) : -1;
+      const bool a = prp >= 0 && prp < NL;
+      const unsigned m = __ballot_sync(0xffffffffu, a);
+      if (a) s_pairs[base + __popc(m & ((1u << t) - 1u))] = pair;
+      base += __popc(m);
+    }
+    if (t == 0) s_nact = base;
+  }
+  __syncthreads();
+  const int q = (t / P.NCB < s_nact) ? s_pairs[t / P.NCB] * P.NCB + t % P.NCB : -1;
+  const bool qok = q >= 0;
+  const int qq = qok ? q : 0;
+  const int e = qq / (P.DZ * P.NCB), dzi = (qq / P.NCB) % P.DZ, cbi = qq % P.NCB;
   const int dz = dzi - (K - 1);
-  const int pe = qok ? P.cls_beg[la][P.edge_cls[e]] : 0;
+  const int pe = P.cls_beg[la][P.edge_cls[e]];
   const int pr = pe + dz;
-  const bool act = ok && qok && pr >= 0 && pr < NL;
+  const bool act = ok && qok;
   const int ridx = e < K - 1 ? pr - lo_base : W + pr - hi_base;
   float2 accR[CB][NC], accI[CB][NC];
 #pragma unroll
@@ -1361,15 +1382,25 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
       }
     }
   }
-  if (!qok) return;
   // conj(a) b = (accR.x + accI.y, accR.y - accI.x); lag_edge_kernel's partial layout
-  const int qb = q / P.QB, tq = q % P.QB;
-  float2* out = part + ((((size_t)ol * P.NQB + qb) * P.CBt + chunk) * P.QB + tq) * CB * NC;
+  auto slot = [&](int qs) {
+    const int qb = qs / P.QB, tq = qs % P.QB;
+    return part + ((((size_t)ol * P.NQB + qb) * P.CBt + chunk) * P.QB + tq) * CB * NC;
+  };
+  if (act) {
+    float2* out = slot(q);
 #pragma unroll
-  for (int u = 0; u < CB; ++u)
+    for (int u = 0; u < CB; ++u)
 #pragma unroll
-    for (int c = 0; c < NC; ++c)
-      out[u * NC + c] = act ? cf(accR[u][c].x + accI[u][c].y, accR[u][c].y - accI[u][c].x) : cf(0.f, 0.f);
+      for (int c = 0; c < NC; ++c) out[u * NC + c] = cf(accR[u][c].x + accI[u][c].y, accR[u][c].y - accI[u][c].x);
+  }
+  // zero partials: every slot when the neighbour block does not exist, else the inactive pairs' slots
+  for (int qs = t; qs < P.NQ; qs += kE2Threads) {
+    const int prs = pair_pr(qs / P.NCB);
+    if (ok && prs >= 0 && prs < NL) continue;
+    float2* out = slot(qs);
+    for (int i = 0; i < CB * NC; ++i) out[i] = cf(0.f, 0.f);
+  }
 }
 
 typedef CUresult (*LagEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -1248,11 +1248,12 @@ lagtc_core_kernel(const __grid_constant__ LagParams P, const uint8_t* __restrict
 // staging load is a coalesced run of 64-byte rows (the per-thread
 // gathers of lag_edge_kernel were latency-bound).  Same partial layout as
 // lag_edge_kernel.
-constexpr int kE2Lines = 16;
-constexpr int kE2Threads = 288;
+constexpr int kE2Lines = 14;   // 2 x 14 staged lines = 69 KB: three CTAs per SM
+constexpr int kE2Threads = 288; // most threads of a CTA; launched with the active pairs x NCB rounded up to warps
+                                // (224 at 5 taps when the edges touch the array bounds: three CTAs of 96 registers per SM)
 constexpr int kE2LS = 8 * 8 + 2, kE2RS = 24 * (8 + 2) + 2;  // float2 per staged line (base edges, neighbour window)
 
-__global__ void __launch_bounds__(kE2Threads, 2)
+__global__ void __maxnreg__(96)
 lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__ x, float2* __restrict__ part) {
   hicu_pdl_entry();
   constexpr int NC = 8, CB = 2;
@@ -1282,7 +1283,7 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
   const int64_t nlines = (int64_t)len[0] * len[1];
   const int64_t l0 = (int64_t)ch * P.lpcB, l1 = min(nlines, l0 + P.lpcB);
   const bool ok = neighbour_ok(P, beg, len, ol);
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, nthr = blockDim.x;
   // Output slot q = (e * DZ + dz) * NCB + cbi.  An (edge position, lag) pair whose neighbour
   // position falls outside the line contributes nothing (28 % of the pairs for 5 taps), so the
   // threads are dealt the ACTIVE pairs in slot order: the products fill the first warps densely
@@ -1329,7 +1330,7 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
       float2* sL = sbuf + (size_t)bf * BUF;
       float2* sR = sL + kE2Lines * LS;
       const int per = 4 * nl;
-      for (int i = t; i < (P.NE + NR) * per; i += kE2Threads) {
+      for (int i = t; i < (P.NE + NR) * per; i += nthr) {
         const int r = i / per, rem = i - r * per, j = rem >> 2, pc4 = rem & 3;
         if (r < P.NE) {
           const int pos = P.cls_beg[la][P.edge_cls[r]];
@@ -1395,7 +1396,7 @@ lag_edge2_kernel(const __grid_constant__ LagParams P, const float2* __restrict__
       for (int c = 0; c < NC; ++c) out[u * NC + c] = cf(accR[u][c].x + accI[u][c].y, accR[u][c].y - accI[u][c].x);
   }
   // zero partials: every slot when the neighbour block does not exist, else the inactive pairs' slots
-  for (int qs = t; qs < P.NQ; qs += kE2Threads) {
+  for (int qs = t; qs < P.NQ; qs += nthr) {
     const int prs = pair_pr(qs / P.NCB);
     if (ok && prs >= 0 && prs < NL) continue;
     float2* out = slot(qs);
@@ -1481,9 +1482,19 @@ int launch_nc(const LagPlan& pl, const float2* x, void* ws, cudaStream_t st) {
       if ((s = hicu_check_launch("lag_core_kernel"))) return s;
     }
   }
-  if (pl.nB > 0 && pl.tc && P.NQ <= kE2Threads && P.NE == 2 * (P.K[P.L - 1] - 1)) {
+  int e2_active = 0;  // (edge position, lag) pairs whose neighbour position lies inside the line
+  {
+    const int la = P.L - 1;
+    for (int e = 0; e < P.NE; ++e)
+      for (int dzi = 0; dzi < P.DZ; ++dzi) {
+        const int pr = P.cls_beg[la][P.edge_cls[e]] + dzi - (P.K[la] - 1);
+        if (pr >= 0 && pr < (int)P.N[la]) ++e2_active;
+      }
+  }
+  const int e2_threads = max(64, (e2_active * P.NCB + 31) / 32 * 32);
+  if (pl.nB > 0 && pl.tc && e2_threads <= kE2Threads && P.NQ <= kE2Threads && P.NE == 2 * (P.K[P.L - 1] - 1)) {
     hicu_allow_max_smem((const void*)lag_edge2_kernel);
-    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), kE2Threads, (size_t)2 * kE2Lines * (kE2LS + kE2RS) * 8, st, P, x,
+    hicu_launch(lag_edge2_kernel, (unsigned)(P.nol * P.CBt), e2_threads, (size_t)2 * kE2Lines * (kE2LS + kE2RS) * 8, st, P, x,
                 partB);
     if ((s = hicu_check_launch("lag_edge2_kernel"))) return s;
   } else if (pl.nB > 0) {
